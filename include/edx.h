@@ -1,0 +1,207 @@
+/*
+ * edx.h — C ABI of the B200-native embedding-sample dispatch path
+ * (libedx.so, built from paper_2512_21615_b200/csrc/).
+ *
+ * Drop-in boundary for the reference's header-only C++ API in
+ * /root/reference/proj/include/embdispatch/.  The reference has no ABI of
+ * its own (proj/CMakeLists.txt:13-17: an INTERFACE library of inline
+ * functions), so every entry point below names the reference declaration it
+ * replaces.  The C++ drop-in headers in include/embdispatch/ forward to these
+ * functions and turn status codes back into the reference's exception types
+ * with the same messages (INTEGRATION.md shows the binding).
+ *
+ * Conventions
+ *  - Plain pointers and sizes; no CUDA or torch types.  Unless a parameter
+ *    says "device", every pointer is host memory.
+ *  - Every function returns an edx_status.  On failure edx_last_error()
+ *    returns the message of the last failing call on this thread.
+ *  - Samples are CSR: ids[offsets[i] .. offsets[i+1]) are sample i's
+ *    embedding ids in order (EmbeddingSample::ids, types.hpp:37-42).
+ *  - Matrices are row-major doubles, rows = samples, cols = workers
+ *    (CostMatrix, cost.hpp:52-60).
+ *  - There is no CPU fallback: without a usable sm_100 device every compute
+ *    entry point fails with EDX_CUDA_ERROR.
+ */
+#ifndef EDX_H
+#define EDX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum edx_status {
+  EDX_OK = 0,
+  EDX_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+  EDX_LOGIC_ERROR = 2,      /* std::logic_error */
+  EDX_RUNTIME_ERROR = 3,    /* std::runtime_error */
+  EDX_CUDA_ERROR = 4        /* device failure; no reference counterpart */
+} edx_status;
+
+/* Message of the last failing call on this thread ("" if none). */
+const char* edx_last_error(void);
+/* ABI version, bumped on any incompatible change. */
+int edx_abi_version(void);
+
+/* embdispatch::ClusterConfig — types.hpp:71-82. */
+typedef struct edx_cluster_config {
+  int32_t n;                    /* worker count */
+  int32_t m;                    /* samples per worker per iteration */
+  const double* bandwidths_bps; /* n_bandwidths entries */
+  int32_t n_bandwidths;
+  int32_t reserved;
+  uint64_t d_tran_bytes; /* one embedding transfer */
+  uint64_t cache_capacity;
+  double alpha; /* exact-solver fraction of EcoMix */
+} edx_cluster_config;
+
+/* embdispatch::IterationReport — sim.hpp:38-50 (counts and realised cost).
+ * The four per-worker arrays are caller-owned with n entries each. */
+typedef struct edx_report {
+  uint64_t iteration;
+  uint64_t miss_pull, update_push, evict_push;
+  uint64_t hits, lookups;
+  double cost_s;
+  uint64_t* miss_pull_w;
+  uint64_t* update_push_w;
+  uint64_t* evict_push_w;
+  double* cost_w;
+} edx_report;
+
+/* validate(const ClusterConfig&, size_t max_sample_len) — types.hpp:87-108. */
+int edx_validate_config(const edx_cluster_config* cfg, uint64_t max_sample_len);
+/* unit_cost(cfg, j).seconds for every worker — types.hpp:112-120. */
+int edx_unit_costs(const edx_cluster_config* cfg, double* out);
+
+/* ------------------------------------------------------------------ engine
+ * One engine = one embdispatch::SimState (sim.hpp:54-268) whose global
+ * per-embedding state and per-worker caches live in device memory, plus the
+ * device buffers of the current batch.  Calls on one engine are ordered on
+ * its own CUDA stream; distinct engines may run concurrently. */
+typedef struct edx_engine edx_engine;
+
+typedef struct edx_engine_options {
+  int32_t device;          /* CUDA ordinal */
+  int32_t reserved0;
+  uint64_t id_space;       /* ids must be < id_space (dense device state) */
+  uint64_t max_batch_ids;  /* capacity of one batch's id stream (sum of lengths) */
+  /* multi-GPU row sharding of the cost build; world_size 1 = off */
+  int32_t rank;
+  int32_t world_size;
+  const void* nccl_unique_id; /* 128-byte ncclUniqueId from rank 0, world_size > 1 */
+} edx_engine_options;
+
+/* SimState::SimState(const ClusterConfig&) — sim.hpp:56-59. */
+int edx_engine_create(const edx_cluster_config* cfg, const edx_engine_options* opt,
+                      edx_engine** out);
+void edx_engine_destroy(edx_engine* e);
+
+/* Stages one iteration's samples (the std::vector<EmbeddingSample> argument of
+ * build_matrix / step, cost.hpp:105 / sim.hpp:87).  on_device != 0 means
+ * ids/offsets are device pointers already resident in HBM. */
+int edx_engine_load_batch(edx_engine* e, const uint32_t* ids, const uint64_t* offsets,
+                          uint64_t num_samples, int on_device);
+/* build_matrix(samples, snapshot(), cfg) — cost.hpp:105-125 over the live
+ * device state (SimState::snapshot, sim.hpp:71-82, costs nothing here).
+ * matrix_out (rows*n doubles) may be NULL to keep the matrix on device. */
+int edx_engine_build(edx_engine* e, double* matrix_out);
+/* ecomix(matrix, cfg) — assign.hpp:247-285 on the engine's matrix, and
+ * decision_cost(matrix, decision) — assign.hpp:288-298.  alpha < 0 uses the
+ * configured alpha.  Either output may be NULL. */
+int edx_engine_dispatch(edx_engine* e, double alpha, int32_t* decision_out,
+                        double* expected_cost_out);
+/* SimState::step(samples, decision) — sim.hpp:87-218.  decision NULL = the
+ * engine's last dispatch (already on device). */
+int edx_engine_step(edx_engine* e, const int32_t* decision, edx_report* rep);
+/* One run() iteration (sim.hpp:421-441): load, build, dispatch, step. */
+int edx_engine_iterate(edx_engine* e, const uint32_t* ids, const uint64_t* offsets,
+                       uint64_t num_samples, int on_device, int32_t* decision_out,
+                       double* expected_cost_out, edx_report* rep);
+
+/* SimState::seed_entry — sim.hpp:252-261 (test hook). */
+int edx_engine_seed_entry(edx_engine* e, uint32_t id, int32_t worker, int latest, int owner);
+/* SimState::state_of — sim.hpp:64-67. */
+int edx_engine_state_of(edx_engine* e, uint32_t id, uint64_t* owners, uint64_t* latest,
+                        uint64_t* resident);
+/* SimState::validate_consistency — sim.hpp:222-248. */
+int edx_engine_validate_consistency(edx_engine* e);
+/* SimState::clock — sim.hpp:61. */
+uint64_t edx_engine_clock(edx_engine* e);
+
+/* Parity exports (SimState::cache(j).entries(), cache.hpp:180-182, and the
+ * global map).  Global: ids with any non-zero mask, ascending id; call with
+ * cap = 0 to get the count. */
+int edx_engine_export_global(edx_engine* e, uint32_t* ids, uint64_t* owners, uint64_t* latest,
+                             uint64_t* resident, uint64_t cap, uint64_t* count);
+int edx_engine_cache_size(edx_engine* e, int32_t worker, uint64_t* size);
+/* Entries of worker j's cache, ascending id (CacheEntry, cache.hpp:36-42). */
+int edx_engine_export_cache(edx_engine* e, int32_t worker, uint32_t* ids, uint8_t* version,
+                            uint32_t* mark, uint32_t* freq, uint64_t* last_access);
+/* WorkerCache::current_mark and the at-current-mark count (cache.hpp:90,237). */
+int edx_engine_cache_marks(edx_engine* e, int32_t worker, uint32_t* current_mark,
+                           uint64_t* at_current_mark);
+/* Replaces the global masks with a host Snapshot (cost.hpp:39-48) for the
+ * const Snapshot& overload of build_matrix; caches are left untouched. */
+int edx_engine_import_snapshot(edx_engine* e, const uint32_t* ids, const uint64_t* owners,
+                               const uint64_t* latest, const uint64_t* resident,
+                               uint64_t count);
+
+/* Per-phase device times of the calls since the last reset, measured with CUDA
+ * events on the engine stream when profiling is on.  Phases (ms):
+ * [0] build  [1] gap+sort  [2] exact solve  [3] greedy  [4] step  [5] whole dispatch
+ * counts: [0] launches of own kernels, [1] Hungarian Dijkstra steps (last solve). */
+#define EDX_NUM_PHASES 6
+int edx_engine_set_profiling(edx_engine* e, int on);
+int edx_engine_phase_times(edx_engine* e, double* ms, uint64_t* counts, int reset);
+
+/* --------------------------------------------------- stateless matrix API
+ * Run on a process-wide default device context (device 0 or the current
+ * device).  Inputs/outputs are host memory. */
+
+/* build_matrix(samples, snapshot, cfg) — cost.hpp:105-125 with an explicit
+ * host Snapshot given as parallel arrays (ids unique). */
+int edx_build_matrix(const edx_cluster_config* cfg, const uint32_t* snap_ids,
+                     const uint64_t* snap_owners, const uint64_t* snap_latest,
+                     const uint64_t* snap_resident, uint64_t snap_count, const uint32_t* ids,
+                     const uint64_t* offsets, uint64_t num_samples, double* out);
+/* row_gap_key — cost.hpp:130-146. */
+int edx_row_gap_key(uint64_t rows, uint64_t cols, const double* values, uint64_t row,
+                    double* out);
+/* rows_by_gap — assign.hpp:197-207. */
+int edx_rows_by_gap(uint64_t rows, uint64_t cols, const double* values, uint64_t* order);
+/* hungarian(const SquareCost&) — assign.hpp:80-157.  total may be NULL. */
+int edx_hungarian(uint64_t k, const double* values, uint64_t* col_of_row, double* total);
+/* Hungarian on a column-expanded EcoMix block without materialising it:
+ * expand_columns(matrix, rows, mult) (assign.hpp:223-241) then hungarian. */
+int edx_hungarian_blocks(uint64_t rows, uint64_t cols, const double* values,
+                         const uint64_t* block_rows, int32_t mult, uint64_t* col_of_row,
+                         double* total);
+/* greedy_dispatch — assign.hpp:162-192; outputs n_order (row, worker) pairs. */
+int edx_greedy_dispatch(uint64_t rows, uint64_t cols, const double* values,
+                        const uint64_t* order, uint64_t n_order, const int32_t* capacity,
+                        uint64_t* out_rows, int32_t* out_workers);
+/* ecomix — assign.hpp:247-285.  row_ids may be NULL (identity). */
+int edx_ecomix(const edx_cluster_config* cfg, uint64_t rows, uint64_t cols,
+               const double* values, const uint64_t* row_ids, int32_t* decision);
+/* decision_cost — assign.hpp:288-298. */
+int edx_decision_cost(uint64_t rows, uint64_t cols, const double* values,
+                      const int32_t* decision, double* out);
+
+/* ------------------------------------------------- synthetic input stream
+ * ZipfStream (workload.hpp:94-133): the benchmark's input producer, host side. */
+typedef struct edx_zipf edx_zipf;
+int edx_zipf_create(uint64_t total_embeddings, uint64_t sample_len, double zipf_s,
+                    uint64_t iterations, uint64_t seed, uint64_t samples_per_iteration,
+                    edx_zipf** out);
+/* Fills samples_per_iteration*sample_len ids; returns 1, or 0 at the end. */
+int edx_zipf_next(edx_zipf* z, uint32_t* ids);
+void edx_zipf_reset(edx_zipf* z);
+void edx_zipf_destroy(edx_zipf* z);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EDX_H */

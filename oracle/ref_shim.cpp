@@ -1,0 +1,372 @@
+// ORACLE — TEST INFRASTRUCTURE ONLY.
+//
+// Exposes the UNMODIFIED reference headers (/root/reference/proj/include,
+// read in place through -I, never copied) behind the same `orc_*` C ABI as
+// oracle/edx_oracle.c, so tests can run the identical binding against the
+// real reference.  Built by oracle/Makefile into oracle/_ref/libedx_ref.so.
+//
+// It also exports orc_ref_iteration(), the reference's own per-iteration
+// sequence (SimState::snapshot -> build_matrix -> ecomix -> decision_cost ->
+// SimState::step; sim.hpp:421-441) timed phase by phase with steady_clock,
+// exactly where run() times it (sim.hpp:423-432).  bench.py --impl reference
+// and the cpu_baseline leg drive that entry point.  The optional row-parallel
+// build partitions rows over std::threads, each calling the reference's
+// expected_cost (cost.hpp:81); rows are independent, so it is bit-identical
+// ("all host cores" variant).
+
+#include <chrono>
+#include <cstring>
+#include <exception>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "embdispatch/assign.hpp"
+#include "embdispatch/cost.hpp"
+#include "embdispatch/sim.hpp"
+#include "embdispatch/workload.hpp"
+
+#include "edx_oracle.h"
+
+using namespace embdispatch;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local std::uint64_t g_steps = 0;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return ORC_OK;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return ORC_INVALID_ARGUMENT;
+  } catch (const std::logic_error& e) {
+    g_err = e.what();
+    return ORC_LOGIC_ERROR;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return ORC_RUNTIME_ERROR;
+  }
+}
+
+ClusterConfig to_cfg(const orc_cluster_config* c) {
+  ClusterConfig cfg;
+  cfg.n = c->n;
+  cfg.m = c->m;
+  cfg.bandwidths_bps.assign(c->bandwidths_bps, c->bandwidths_bps + c->n_bandwidths);
+  cfg.d_tran_bytes = c->d_tran_bytes;
+  cfg.cache_capacity = static_cast<std::size_t>(c->cache_capacity);
+  cfg.alpha = c->alpha;
+  return cfg;
+}
+
+std::vector<EmbeddingSample> to_samples(const uint32_t* ids, const uint64_t* offsets,
+                                        uint64_t R) {
+  std::vector<EmbeddingSample> out(R);
+  for (uint64_t i = 0; i < R; ++i) out[i].ids.assign(ids + offsets[i], ids + offsets[i + 1]);
+  return out;
+}
+
+CostMatrix to_matrix(uint64_t rows, uint64_t cols, const double* values) {
+  CostMatrix m;
+  m.rows = rows;
+  m.cols = cols;
+  m.values.assign(values, values + rows * cols);
+  m.row_ids.resize(rows);
+  for (uint64_t i = 0; i < rows; ++i) m.row_ids[i] = i;
+  return m;
+}
+
+void copy_report(const IterationReport& r, int n, orc_report* out) {
+  out->iteration = r.iteration;
+  out->miss_pull = r.miss_pull;
+  out->update_push = r.update_push;
+  out->evict_push = r.evict_push;
+  out->hits = r.hits;
+  out->lookups = r.lookups;
+  out->cost_s = r.cost_s;
+  for (int j = 0; j < n; ++j) {
+    out->miss_pull_w[j] = r.miss_pull_w[j];
+    out->update_push_w[j] = r.update_push_w[j];
+    out->evict_push_w[j] = r.evict_push_w[j];
+    out->cost_w[j] = r.cost_w[j];
+  }
+}
+
+}  // namespace
+
+struct orc_zipf {
+  WorkloadSpec spec;
+  ClusterConfig cfg;
+  ZipfStream stream;
+  std::vector<EmbeddingSample> buf;
+  orc_zipf(const WorkloadSpec& s, const ClusterConfig& c) : spec(s), cfg(c), stream(s, c) {}
+};
+
+struct orc_sim {
+  ClusterConfig cfg;
+  SimState state;
+  explicit orc_sim(const ClusterConfig& c) : cfg(c), state(c) {}
+};
+
+extern "C" {
+
+const char* orc_last_error(void) { return g_err.c_str(); }
+
+int orc_validate_config(const orc_cluster_config* c, uint64_t max_len) {
+  return guarded([&] { validate(to_cfg(c), static_cast<std::size_t>(max_len)); });
+}
+
+int orc_unit_costs(const orc_cluster_config* c, double* out) {
+  return guarded([&] {
+    const ClusterConfig cfg = to_cfg(c);
+    for (int j = 0; j < cfg.n; ++j) out[j] = unit_cost(cfg, j).seconds;
+  });
+}
+
+int orc_zipf_create(uint64_t total, uint64_t sample_len, double zipf_s, uint64_t iterations,
+                    uint64_t seed, uint64_t per_iteration, orc_zipf** out) {
+  return guarded([&] {
+    WorkloadSpec spec;
+    spec.total_embeddings = total;
+    spec.sample_len = sample_len;
+    spec.zipf_s = zipf_s;
+    spec.iterations = iterations;
+    spec.seed = seed;
+    ClusterConfig cfg;
+    cfg.n = 1;
+    cfg.m = static_cast<int>(per_iteration);
+    *out = new orc_zipf(spec, cfg);
+  });
+}
+
+void orc_zipf_destroy(orc_zipf* z) { delete z; }
+
+int orc_zipf_next(orc_zipf* z, uint32_t* ids) {
+  if (!z->stream.next_iteration(z->buf)) return 0;
+  std::size_t off = 0;
+  for (const auto& s : z->buf) {
+    std::memcpy(ids + off, s.ids.data(), s.ids.size() * sizeof(uint32_t));
+    off += s.ids.size();
+  }
+  return 1;
+}
+
+void orc_zipf_reset(orc_zipf* z) { z->stream.reset(); }
+
+void orc_bench_matrix(uint64_t k, double* out) {
+  std::mt19937_64 rng(0x5eedULL ^ k);
+  for (uint64_t i = 0; i < k * k; ++i) out[i] = static_cast<double>(rng() >> 11) * 0x1.0p-53;
+}
+
+int orc_build_matrix_snapshot(const orc_cluster_config* c, const uint32_t* snap_ids,
+                              const uint64_t* owners, const uint64_t* latest,
+                              const uint64_t* resident, uint64_t count, const uint32_t* ids,
+                              const uint64_t* offsets, uint64_t R, double* out) {
+  return guarded([&] {
+    Snapshot snap;
+    for (uint64_t s = 0; s < count; ++s) {
+      EmbeddingState& st = snap.states[snap_ids[s]];
+      st.owners = owners[s];
+      st.latest = latest[s];
+      st.resident = resident ? resident[s] : 0;
+    }
+    const CostMatrix m = build_matrix(to_samples(ids, offsets, R), snap, to_cfg(c));
+    std::memcpy(out, m.values.data(), m.values.size() * sizeof(double));
+  });
+}
+
+int orc_row_gap_key(uint64_t rows, uint64_t cols, const double* values, uint64_t row,
+                    double* out) {
+  return guarded([&] { *out = row_gap_key(to_matrix(rows, cols, values), row); });
+}
+
+int orc_rows_by_gap(uint64_t rows, uint64_t cols, const double* values, uint64_t* order) {
+  return guarded([&] {
+    const auto o = rows_by_gap(to_matrix(rows, cols, values));
+    for (uint64_t i = 0; i < rows; ++i) order[i] = o[i];
+  });
+}
+
+int orc_hungarian(uint64_t k, const double* values, uint64_t* col_of_row, double* total) {
+  return guarded([&] {
+    SquareCost sq;
+    sq.order = k;
+    sq.values.assign(values, values + k * k);
+    const AssignmentResult r = hungarian(sq);
+    for (uint64_t i = 0; i < k; ++i) col_of_row[i] = r.col_of_row[i];
+    if (total) *total = r.total_cost;
+  });
+}
+
+int orc_greedy_dispatch(uint64_t rows, uint64_t cols, const double* values,
+                        const uint64_t* order, uint64_t n_order, const int32_t* capacity,
+                        uint64_t* out_rows, int32_t* out_workers) {
+  return guarded([&] {
+    std::vector<std::size_t> o(order, order + n_order);
+    std::vector<int> cap(capacity, capacity + cols);
+    const auto part = greedy_dispatch(to_matrix(rows, cols, values), o, cap);
+    for (std::size_t t = 0; t < part.size(); ++t) {
+      out_rows[t] = part[t].first;
+      out_workers[t] = part[t].second;
+    }
+  });
+}
+
+int orc_ecomix(const orc_cluster_config* c, uint64_t rows, uint64_t cols, const double* values,
+               const uint64_t* row_ids, int32_t* decision) {
+  return guarded([&] {
+    CostMatrix m = to_matrix(rows, cols, values);
+    if (row_ids)
+      for (uint64_t i = 0; i < rows; ++i) m.row_ids[i] = row_ids[i];
+    const DispatchDecision d = ecomix(m, to_cfg(c));
+    for (uint64_t i = 0; i < rows; ++i) decision[i] = d.worker_of_sample[i];
+  });
+}
+
+int orc_decision_cost(uint64_t rows, uint64_t cols, const double* values,
+                      const int32_t* decision, double* out) {
+  return guarded([&] {
+    DispatchDecision d;
+    d.worker_of_sample.assign(decision, decision + rows);
+    *out = decision_cost(to_matrix(rows, cols, values), d);
+  });
+}
+
+int orc_sim_create(const orc_cluster_config* c, orc_sim** out) {
+  return guarded([&] { *out = new orc_sim(to_cfg(c)); });
+}
+
+void orc_sim_destroy(orc_sim* s) { delete s; }
+
+int orc_sim_build_matrix(orc_sim* s, const uint32_t* ids, const uint64_t* offsets, uint64_t R,
+                         double* out) {
+  return guarded([&] {
+    const Snapshot snap = s->state.snapshot();
+    const CostMatrix m = build_matrix(to_samples(ids, offsets, R), snap, s->cfg);
+    std::memcpy(out, m.values.data(), m.values.size() * sizeof(double));
+  });
+}
+
+int orc_sim_step(orc_sim* s, const uint32_t* ids, const uint64_t* offsets, uint64_t R,
+                 const int32_t* decision, orc_report* rep) {
+  return guarded([&] {
+    DispatchDecision d;
+    d.worker_of_sample.assign(decision, decision + R);
+    const IterationReport r = s->state.step(to_samples(ids, offsets, R), d);
+    copy_report(r, s->cfg.n, rep);
+  });
+}
+
+int orc_sim_seed_entry(orc_sim* s, uint32_t id, int32_t worker, int latest, int owner) {
+  return guarded([&] { s->state.seed_entry(id, worker, latest != 0, owner != 0); });
+}
+
+int orc_sim_validate_consistency(orc_sim* s) {
+  return guarded([&] { s->state.validate_consistency(); });
+}
+
+uint64_t orc_sim_clock(orc_sim* s) { return s->state.clock(); }
+
+uint64_t orc_sim_global_count(orc_sim* s) { return s->state.snapshot().states.size(); }
+
+void orc_sim_export_global(orc_sim* s, uint32_t* ids, uint64_t* owners, uint64_t* latest,
+                           uint64_t* resident) {
+  const Snapshot snap = s->state.snapshot();
+  std::size_t t = 0;
+  for (const auto& [id, st] : snap.states) {
+    ids[t] = id;
+    owners[t] = st.owners;
+    latest[t] = st.latest;
+    resident[t] = st.resident;
+    ++t;
+  }
+}
+
+uint64_t orc_sim_cache_size(orc_sim* s, int32_t worker) { return s->state.cache(worker).size(); }
+
+void orc_sim_export_cache(orc_sim* s, int32_t worker, uint32_t* ids, uint8_t* version,
+                          uint32_t* mark, uint32_t* freq, uint64_t* last_access) {
+  std::size_t t = 0;
+  for (const auto& [id, e] : s->state.cache(worker).entries()) {
+    ids[t] = id;
+    version[t] = e.version_latest ? 1 : 0;
+    mark[t] = e.mark;
+    freq[t] = e.frequency;
+    last_access[t] = e.last_access;
+    ++t;
+  }
+}
+
+void orc_sim_cache_marks(orc_sim* s, int32_t worker, uint32_t* current_mark,
+                         uint64_t* at_current_mark) {
+  const WorkerCache& c = s->state.cache(worker);
+  *current_mark = c.current_mark();
+  // at_current_mark_ is private in the reference; count it from the entries
+  // (cache.hpp:111,116,175 keep it equal to #entries with mark == current).
+  uint64_t at = 0;
+  for (const auto& [id, e] : c.entries())
+    if (e.mark == c.current_mark()) ++at;
+  *at_current_mark = at;
+}
+
+uint64_t orc_last_hungarian_steps(void) { return g_steps; }
+
+// One reference iteration, timed like run() (sim.hpp:421-441).  times_s gets
+// {snapshot, build, decide, step}; `threads` > 1 partitions build rows.
+int orc_ref_iteration(orc_sim* s, const uint32_t* ids, const uint64_t* offsets, uint64_t R,
+                      int threads, int32_t* decision, double* expected_out, orc_report* rep,
+                      double* times_s) {
+  return guarded([&] {
+    using clk = std::chrono::steady_clock;
+    const auto samples = to_samples(ids, offsets, R);
+    const auto t0 = clk::now();
+    const Snapshot snap = s->state.snapshot();
+    const auto t1 = clk::now();
+    CostMatrix matrix;
+    if (threads <= 1) {
+      matrix = build_matrix(samples, snap, s->cfg);
+    } else {
+      if (samples.size() != s->cfg.samples_per_iteration())
+        throw std::invalid_argument("expected m*n samples");
+      matrix.rows = samples.size();
+      matrix.cols = static_cast<std::size_t>(s->cfg.n);
+      matrix.values.resize(matrix.rows * matrix.cols);
+      matrix.row_ids.resize(matrix.rows);
+      std::vector<std::thread> pool;
+      const std::size_t chunk = (matrix.rows + threads - 1) / threads;
+      for (int t = 0; t < threads; ++t) {
+        pool.emplace_back([&, t] {
+          const std::size_t lo = t * chunk, hi = std::min(matrix.rows, lo + chunk);
+          for (std::size_t i = lo; i < hi; ++i) {
+            matrix.row_ids[i] = i;
+            for (WorkerId j = 0; j < s->cfg.n; ++j)
+              matrix.at(i, j) = embdispatch::expected_cost(samples[i], j, snap, s->cfg);
+          }
+        });
+      }
+      for (auto& th : pool) th.join();
+    }
+    const auto t2 = clk::now();
+    const DispatchDecision d = ecomix(matrix, s->cfg);
+    const auto t3 = clk::now();
+    const IterationReport r = s->state.step(samples, d);
+    const auto t4 = clk::now();
+    if (expected_out) *expected_out = decision_cost(matrix, d);
+    if (decision)
+      for (uint64_t i = 0; i < R; ++i) decision[i] = d.worker_of_sample[i];
+    if (rep) copy_report(r, s->cfg.n, rep);
+    if (times_s) {
+      times_s[0] = std::chrono::duration<double>(t1 - t0).count();
+      times_s[1] = std::chrono::duration<double>(t2 - t1).count();
+      times_s[2] = std::chrono::duration<double>(t3 - t2).count();
+      times_s[3] = std::chrono::duration<double>(t4 - t3).count();
+    }
+  });
+}
+
+}  // extern "C"

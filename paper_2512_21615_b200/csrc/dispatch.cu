@@ -1,0 +1,254 @@
+// K3 row ordering, K4 capacity-bounded greedy, decision checks, and the
+// EcoMix orchestration (assign.hpp:162-298).
+#include <cub/device/device_radix_sort.cuh>
+
+#include <cmath>
+
+#include "edx_internal.cuh"
+
+namespace edx {
+
+// ------------------------------------------------------------------ K3 sort
+// rows_by_gap (assign.hpp:197-207) orders rows by (gap desc, index asc).  The
+// gap keys are ~bits(gap) (cost.cu), so an ascending *stable* radix sort of
+// (key, row) pairs with rows fed in index order reproduces std::sort with the
+// reference's total order exactly.
+void sort_rows_by_gap(SortScratch& sc, const uint64_t* keys_in, const uint32_t* idx_in,
+                      uint32_t* idx_out, uint64_t rows, cudaStream_t s) {
+  sc.keys_out.ensure(rows);
+  size_t bytes = 0;
+  EDX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys_in, sc.keys_out.p, idx_in,
+                                           idx_out, static_cast<int>(rows), 0, 64, s));
+  sc.temp.ensure(bytes);
+  EDX_CUDA(cub::DeviceRadixSort::SortPairs(sc.temp.p, bytes, keys_in, sc.keys_out.p, idx_in,
+                                           idx_out, static_cast<int>(rows), 0, 64, s));
+}
+
+// ---------------------------------------------------------------- K4 greedy
+// greedy_dispatch (assign.hpp:162-192) is sequential: each row, in order,
+// takes its cheapest worker with capacity left (strict '<', lowest index on
+// ties).  The open set only changes when a worker is exhausted, so the
+// sequential result equals rounds of "every pending row takes its argmin over
+// the current open set": positions before the first row whose choice exceeds
+// that worker's remaining capacity are final, then the exhausted workers
+// close and the next round starts at that row.  Rows after an exhaustion that
+// did not pick the exhausted worker keep their argmin (removing a worker that
+// is not the minimum does not move the minimum), so the first over-capacity
+// row is the first divergence.  Each round closes >= 1 worker: <= n rounds
+// plus one pass per 1024 rows.  One CTA: the matrix slice is L2-resident.
+namespace {
+
+constexpr int kGreedyThreads = 1024;
+constexpr int kGreedyWarps = kGreedyThreads / 32;
+
+__global__ void __launch_bounds__(kGreedyThreads)
+    k_greedy(const double* __restrict__ matrix, int n, const uint32_t* __restrict__ order,
+             uint64_t n_order, const int32_t* __restrict__ capacity_dev, int cap_uniform,
+             int32_t* __restrict__ decision, const uint32_t* __restrict__ row_ids,
+             int32_t* __restrict__ pair_worker, int* __restrict__ flags) {
+  __shared__ int remaining[kMaxWorkers];
+  __shared__ int used[kMaxWorkers];
+  __shared__ int cnt[kGreedyWarps][kMaxWorkers];
+  __shared__ unsigned long long open_mask;
+  __shared__ int qmin;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < n) remaining[tid] = capacity_dev ? capacity_dev[tid] : cap_uniform;
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long om = 0;
+    for (int w = 0; w < n; ++w)
+      if (remaining[w] > 0) om |= 1ULL << w;
+    open_mask = om;
+  }
+  __syncthreads();
+
+  uint64_t start = 0;
+  while (start < n_order) {
+    for (int x = tid; x < kGreedyWarps * kMaxWorkers; x += kGreedyThreads)
+      (&cnt[0][0])[x] = 0;
+    if (tid < kMaxWorkers) used[tid] = 0;
+    if (tid == 0) qmin = kGreedyThreads;
+    __syncthreads();
+
+    const uint64_t t = start + tid;
+    const bool valid = t < n_order;
+    int choice = -1;
+    uint32_t row = 0;
+    if (valid) {
+      row = order[t];
+      const double* r = matrix + static_cast<uint64_t>(row) * n;
+      double best = __longlong_as_double(0x7ff0000000000000LL);
+      unsigned long long om = open_mask;
+      while (om) {
+        const int w = __ffsll(static_cast<long long>(om)) - 1;
+        om &= om - 1;
+        const double c = r[w];
+        if (c < best) {
+          best = c;
+          choice = w;
+        }
+      }
+      if (choice < 0) atomicOr(flags + kFlagUnbalanced, 1);  // "capacities exhausted"
+    }
+    // rank of this position among earlier same-choice positions of the chunk
+    const unsigned peers = __match_any_sync(0xffffffffu, choice);
+    const int rank_in_warp = __popc(peers & ((1u << lane) - 1));
+    if (choice >= 0 && rank_in_warp == 0) cnt[warp][choice] = __popc(peers);
+    __syncthreads();
+    if (tid < n) {  // exclusive scan over warps, per worker
+      int run = 0;
+      for (int wp = 0; wp < kGreedyWarps; ++wp) {
+        const int v = cnt[wp][tid];
+        cnt[wp][tid] = run;
+        run += v;
+      }
+    }
+    __syncthreads();
+    if (choice >= 0 && cnt[warp][choice] + rank_in_warp >= remaining[choice])
+      atomicMin(&qmin, tid);
+    __syncthreads();
+    const int limit = qmin;
+    if (valid && choice >= 0 && tid < limit) {
+      atomicAdd(&used[choice], 1);
+      if (decision) decision[row_ids ? row_ids[row] : row] = choice;
+      if (pair_worker) pair_worker[t] = choice;
+    }
+    __syncthreads();
+    if (tid < n) {
+      remaining[tid] -= used[tid];
+      if (remaining[tid] <= 0) atomicAnd(&open_mask, ~(1ULL << tid));
+    }
+    start += static_cast<uint64_t>(limit);
+    __syncthreads();
+  }
+}
+
+__global__ void k_check_balance(const int32_t* __restrict__ decision, uint64_t rows, int n,
+                                int m, int* __restrict__ flags) {
+  __shared__ int load[kMaxWorkers];
+  if (threadIdx.x < kMaxWorkers) load[threadIdx.x] = 0;
+  __syncthreads();
+  for (uint64_t i = threadIdx.x; i < rows; i += blockDim.x) {
+    const int w = decision[i];
+    if (w < 0 || w >= n) atomicOr(flags + kFlagUnbalanced, 1);
+    else atomicAdd(&load[w], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x < n && load[threadIdx.x] != m) atomicOr(flags + kFlagUnbalanced, 1);
+}
+
+// decision_cost (assign.hpp:288-298): a left-to-right fp64 sum in sample
+// order.  The order is part of the result, so it is one thread; operands are
+// fetched 8 ahead of the dependent add chain.
+__global__ void k_decision_cost(const double* __restrict__ matrix,
+                                const int32_t* __restrict__ decision, uint64_t rows, int n,
+                                double* __restrict__ out) {
+  double total = 0.0;
+  uint64_t i = 0;
+  for (; i + 8 <= rows; i += 8) {
+    double v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = matrix[(i + q) * n + decision[i + q]];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) total = __dadd_rn(total, v[q]);
+  }
+  for (; i < rows; ++i) total = __dadd_rn(total, matrix[i * n + decision[i]]);
+  *out = total;
+}
+
+}  // namespace
+
+void launch_greedy(const double* matrix, uint64_t rows, int n, const uint32_t* order,
+                   uint64_t n_order, const int32_t* capacity_dev, int cap_uniform,
+                   int32_t* decision, const uint32_t* row_ids, int32_t* pair_worker,
+                   int* flags, cudaStream_t s) {
+  (void)rows;
+  if (n_order == 0) return;
+  k_greedy<<<1, kGreedyThreads, 0, s>>>(matrix, n, order, n_order, capacity_dev, cap_uniform,
+                                        decision, row_ids, pair_worker, flags);
+  EDX_LAUNCHED();
+}
+
+void launch_check_balance(const int32_t* decision, uint64_t rows, int n, int m, int* flags,
+                          cudaStream_t s) {
+  k_check_balance<<<1, 1024, 0, s>>>(decision, rows, n, m, flags);
+  EDX_LAUNCHED();
+}
+
+void launch_decision_cost(const double* matrix, const int32_t* decision, uint64_t rows, int n,
+                          double* out, cudaStream_t s) {
+  k_decision_cost<<<1, 1, 0, s>>>(matrix, decision, rows, n, out);
+  EDX_LAUNCHED();
+}
+
+// ------------------------------------------------------------------ EcoMix
+// detail::exact_multiplicity (assign.hpp:213-216), evaluated on the host in
+// the same double arithmetic.
+int exact_multiplicity(int m, double alpha) {
+  int mult = static_cast<int>(std::floor(m * alpha + 1e-9));
+  if (mult < 0) mult = 0;
+  if (mult > m) mult = m;
+  return mult;
+}
+
+DispatchScratch::~DispatchScratch() {
+  if (fork) cudaEventDestroy(fork);
+  if (join) cudaEventDestroy(join);
+  if (side) cudaStreamDestroy(side);
+}
+
+void DispatchScratch::init(int device) {
+  (void)device;
+  if (side) return;
+  EDX_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+  EDX_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+  EDX_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+}
+
+// ecomix (assign.hpp:247-285): rows ordered by gap; the top n*mult rows go to
+// the exact solver on the column-expanded block, the rest to the greedy with
+// capacity m - mult per worker.  The two parts are independent (the greedy
+// capacities do not depend on the exact block's answer), so the greedy runs
+// on a side stream concurrently with the latency-bound Hungarian.
+void run_ecomix(DispatchScratch& sc, const double* matrix, uint64_t rows, int n, int m,
+                double alpha, bool gap_ready, int32_t* decision, int* flags, cudaStream_t s,
+                int device, const PhaseEvents* ev, int* launches) {
+  sc.init(device);
+  const int mult = exact_multiplicity(m, alpha);
+  const uint64_t k = static_cast<uint64_t>(n) * static_cast<uint64_t>(mult);
+  sc.gap_keys.ensure(rows);
+  sc.row_index.ensure(rows);
+  sc.order.ensure(rows);
+  if (ev && ev->sort0) EDX_CUDA(cudaEventRecord(ev->sort0, s));
+  if (!gap_ready) {
+    launch_gap_keys(matrix, rows, n, sc.gap_keys.p, sc.row_index.p, s);
+    if (launches) ++*launches;
+  }
+  sort_rows_by_gap(sc.sort, sc.gap_keys.p, sc.row_index.p, sc.order.p, rows, s);
+  if (launches) *launches += 4;  // CUB onesweep: histogram + 3..4 passes (approx.)
+  if (ev && ev->sort1) EDX_CUDA(cudaEventRecord(ev->sort1, s));
+  const bool greedy = k < rows;
+  if (greedy) {
+    EDX_CUDA(cudaEventRecord(sc.fork, s));
+    EDX_CUDA(cudaStreamWaitEvent(sc.side, sc.fork, 0));
+    if (ev && ev->greedy0) EDX_CUDA(cudaEventRecord(ev->greedy0, sc.side));
+    launch_greedy(matrix, rows, n, sc.order.p + k, rows - k, nullptr, m - mult, decision,
+                  nullptr, nullptr, flags, sc.side);
+    if (launches) ++*launches;
+    if (ev && ev->greedy1) EDX_CUDA(cudaEventRecord(ev->greedy1, sc.side));
+    EDX_CUDA(cudaEventRecord(sc.join, sc.side));
+  }
+  if (ev && ev->exact0) EDX_CUDA(cudaEventRecord(ev->exact0, s));
+  if (mult > 0) {
+    launch_hungarian_blocks(sc.hung, matrix, n, sc.order.p, mult, decision, nullptr, nullptr,
+                            flags, s, device);
+    if (launches) ++*launches;
+  }
+  if (ev && ev->exact1) EDX_CUDA(cudaEventRecord(ev->exact1, s));
+  if (greedy) EDX_CUDA(cudaStreamWaitEvent(s, sc.join, 0));
+  launch_check_balance(decision, rows, n, m, flags, s);
+  if (launches) ++*launches;
+}
+
+}  // namespace edx

@@ -1,0 +1,145 @@
+// Internal declarations shared by the libedx translation units.
+// Everything here is sm_100a device code or host orchestration around it;
+// the public surface is include/edx.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "edx.h"
+
+namespace edx {
+
+// ---------------------------------------------------------------- errors
+// Host-side exceptions carry an edx_status; the C ABI boundary converts them.
+struct Error : std::runtime_error {
+  edx_status code;
+  Error(edx_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
+  throw Error(EDX_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e) + " (" + file +
+                                  ":" + std::to_string(line) + ")");
+}
+
+#define EDX_CUDA(x)                                                   \
+  do {                                                                \
+    cudaError_t _e = (x);                                             \
+    if (_e != cudaSuccess) ::edx::throw_cuda(_e, #x, __FILE__, __LINE__); \
+  } while (0)
+
+#define EDX_LAUNCHED()                                                        \
+  do {                                                                        \
+    cudaError_t _e = cudaGetLastError();                                      \
+    if (_e != cudaSuccess) ::edx::throw_cuda(_e, "kernel launch", __FILE__, __LINE__); \
+  } while (0)
+
+inline void invalid(const std::string& m) { throw Error(EDX_INVALID_ARGUMENT, m); }
+inline void logic(const std::string& m) { throw Error(EDX_LOGIC_ERROR, m); }
+
+// Device-side error flags (set by kernels, checked by the host after a sync).
+enum DevFlag : int {
+  kFlagIdOutOfRange = 0,   // an id >= id_space reached a dense-table kernel
+  kFlagBadCost = 1,        // a solver input was negative or non-finite
+  kFlagPinned = 2,         // every cache entry pinned (cache.hpp:164)
+  kFlagUnbalanced = 3,     // a dispatch decision broke the m-per-worker balance
+  kFlagKeyRange = 4,       // victim-key fields exceed the 57-bit packing
+  kFlagCount = 8
+};
+
+constexpr int kMaxWorkers = 64;  // WorkerMask is one uint64 (types.hpp:89,124)
+
+// --------------------------------------------------------- device buffers
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void ensure(size_t count) {
+    if (count <= n && p) return;
+    release();
+    size_t c = count ? count : 1;
+    EDX_CUDA(cudaMalloc(&p, c * sizeof(T)));
+    n = c;
+  }
+};
+
+// ------------------------------------------------------ kernel launchers
+// cost.cu — K1 build + K2 gap keys (cost.hpp:81-146)
+void launch_cost_build(const uint32_t* ids, const uint64_t* offsets, uint64_t rows, int n,
+                       const ulonglong2* ol, uint64_t id_space, const double* ucost,
+                       double* matrix, uint64_t* gap_keys, uint32_t* row_index, int* flags,
+                       cudaStream_t s);
+// gap keys only, for an externally supplied matrix (rows_by_gap on a host matrix)
+void launch_gap_keys(const double* matrix, uint64_t rows, int n, uint64_t* gap_keys,
+                     uint32_t* row_index, cudaStream_t s);
+
+// dispatch.cu — K3 sort, K4 greedy, decision scatter/validation/cost
+struct SortScratch {
+  DevBuf<uint8_t> temp;
+  DevBuf<uint64_t> keys_out;
+  size_t temp_bytes = 0;
+};
+void sort_rows_by_gap(SortScratch& sc, const uint64_t* keys_in, const uint32_t* idx_in,
+                      uint32_t* idx_out, uint64_t rows, cudaStream_t s);
+void launch_greedy(const double* matrix, uint64_t rows, int n, const uint32_t* order,
+                   uint64_t n_order, const int32_t* capacity_dev, int cap_uniform,
+                   int32_t* decision, const uint32_t* row_ids, int32_t* pair_worker,
+                   int* flags, cudaStream_t s);
+void launch_check_balance(const int32_t* decision, uint64_t rows, int n, int m, int* flags,
+                          cudaStream_t s);
+void launch_decision_cost(const double* matrix, const int32_t* decision, uint64_t rows, int n,
+                          double* out, cudaStream_t s);
+
+// hungarian.cu — K6 block-collapsed e-maxx and K5 dense e-maxx (assign.hpp:80-157)
+struct HungarianScratch {
+  DevBuf<int64_t> s64;   // global fallback for the scaled cost rows
+  DevBuf<uint8_t> arena; // global fallback for the solver arrays
+  DevBuf<unsigned long long> steps;
+};
+// Collapsed solver on the column-expanded block of `k = n*mult` rows
+// order[0..k) of matrix; writes decision[row_ids? row_ids[row]: row] = worker
+// (or col_of_row[r] when col_of_row != nullptr).
+void launch_hungarian_blocks(HungarianScratch& sc, const double* matrix, int n,
+                             const uint32_t* order, int mult, int32_t* decision,
+                             const uint32_t* row_ids, uint64_t* col_of_row, int* flags,
+                             cudaStream_t s, int device);
+void launch_hungarian_dense(HungarianScratch& sc, const double* values, uint64_t k,
+                            uint64_t* col_of_row, int* flags, cudaStream_t s, int device);
+unsigned long long last_hungarian_steps(HungarianScratch& sc, cudaStream_t s);
+
+// The EcoMix pipeline on a device matrix (assign.hpp:247-285).
+struct DispatchScratch {
+  SortScratch sort;
+  HungarianScratch hung;
+  DevBuf<uint64_t> gap_keys;
+  DevBuf<uint32_t> row_index, order;
+  DevBuf<double> cost;
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  ~DispatchScratch();
+  void init(int device);
+};
+// Phase events (may be null) bracket gap/sort, exact solve, greedy.
+struct PhaseEvents {
+  cudaEvent_t sort0 = nullptr, sort1 = nullptr, exact0 = nullptr, exact1 = nullptr,
+              greedy0 = nullptr, greedy1 = nullptr;
+};
+int exact_multiplicity(int m, double alpha);
+// `gap_ready` = gap keys/row index already produced by the build epilogue.
+void run_ecomix(DispatchScratch& sc, const double* matrix, uint64_t rows, int n, int m,
+                double alpha, bool gap_ready, int32_t* decision, int* flags, cudaStream_t s,
+                int device, const PhaseEvents* ev, int* launches);
+
+}  // namespace edx

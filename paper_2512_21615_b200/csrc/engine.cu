@@ -1,0 +1,1070 @@
+// C ABI of libedx (include/edx.h): the engine (SimState on device) and the
+// stateless matrix-level API.  Host code here only validates arguments,
+// moves buffers and sequences kernels on the engine's stream; every
+// reference computation runs in the CUDA kernels of cost.cu, dispatch.cu,
+// hungarian.cu and step.cu.
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "engine.h"
+#include "step.h"
+
+using edx::DevBuf;
+using edx::Error;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return EDX_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of host memory";
+    return EDX_RUNTIME_ERROR;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return EDX_RUNTIME_ERROR;
+  }
+}
+
+constexpr int kT = 256;
+unsigned grid_for(uint64_t n) { return static_cast<unsigned>(std::max<uint64_t>(1, (n + kT - 1) / kT)); }
+
+// ---------------------------------------------------------------- config
+// validate(const ClusterConfig&, size_t) — types.hpp:87-108, same messages.
+void validate_cfg(const edx_cluster_config* c, uint64_t max_len) {
+  if (!c) edx::invalid("null cluster config");
+  if (c->n < 1) edx::invalid("worker count must be >= 1");
+  if (c->n > 64) edx::invalid("at most 64 workers supported");
+  if (c->m < 1) edx::invalid("batch size per worker must be >= 1");
+  if (c->n_bandwidths != c->n) edx::invalid("need one bandwidth per worker");
+  for (int j = 0; j < c->n; ++j)
+    if (!(c->bandwidths_bps[j] > 0.0)) edx::invalid("bandwidths must be positive");
+  if (c->d_tran_bytes == 0) edx::invalid("d_tran must be positive");
+  if (c->alpha < 0.0 || c->alpha > 1.0) edx::invalid("alpha must lie in [0, 1]");
+  const uint64_t micro = static_cast<uint64_t>(c->m) * max_len;
+  if (c->cache_capacity < micro)
+    edx::invalid("cache capacity " + std::to_string(c->cache_capacity) +
+                 " cannot hold one micro-batch of " + std::to_string(micro) + " embeddings");
+}
+
+// unit_cost — types.hpp:112-120: d_tran * 8.0 / bw, one direction.
+std::vector<double> unit_costs(const edx_cluster_config* c) {
+  std::vector<double> u(static_cast<size_t>(c->n));
+  for (int j = 0; j < c->n; ++j) u[j] = static_cast<double>(c->d_tran_bytes) * 8.0 / c->bandwidths_bps[j];
+  return u;
+}
+
+void check_flags_host(const int* f) {
+  if (f[edx::kFlagIdOutOfRange]) edx::invalid("embedding id outside the engine's id_space");
+  if (f[edx::kFlagBadCost]) edx::invalid("costs must be finite and non-negative");
+  if (f[edx::kFlagPinned]) edx::logic("every cache entry is pinned; cannot evict");
+  if (f[edx::kFlagUnbalanced]) edx::logic("capacities exhausted before rows");
+  if (f[edx::kFlagKeyRange])
+    throw Error(EDX_RUNTIME_ERROR, "victim key fields exceed the 57-bit device packing");
+}
+
+// ------------------------------------------------------- small kernels
+__global__ void k_import(const uint32_t* __restrict__ ids, const unsigned long long* __restrict__ ow,
+                         const unsigned long long* __restrict__ la,
+                         const unsigned long long* __restrict__ re, uint64_t count,
+                         uint64_t id_space, ulonglong2* __restrict__ ol,
+                         unsigned long long* __restrict__ res, int* flags) {
+  const uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (x >= count) return;
+  const uint32_t id = ids[x];
+  if (id >= id_space) {
+    atomicOr(flags + edx::kFlagIdOutOfRange, 1);
+    return;
+  }
+  ol[id] = make_ulonglong2(ow[x], la[x]);
+  if (res) res[id] = re ? re[x] : 0ULL;
+}
+
+__global__ void k_export_global(const ulonglong2* __restrict__ ol,
+                                const unsigned long long* __restrict__ res, uint64_t id_space,
+                                uint32_t* __restrict__ ids, unsigned long long* __restrict__ out,
+                                uint64_t cap, unsigned long long* __restrict__ count) {
+  const uint64_t id = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (id >= id_space) return;
+  const ulonglong2 st = ol[id];
+  const unsigned long long r = res[id];
+  if ((st.x | st.y | r) == 0) return;
+  const unsigned long long at = atomicAdd(count, 1ULL);
+  if (at < cap) {
+    ids[at] = static_cast<uint32_t>(id);
+    out[3 * at] = st.x;
+    out[3 * at + 1] = st.y;
+    out[3 * at + 2] = r;
+  }
+}
+
+// WorkerCache::touch (cache.hpp:102-122) + the mask updates of seed_entry
+// (sim.hpp:252-261), one entry.
+__global__ void k_seed_entry(uint32_t id, int j, int latest, int owner, uint32_t clock,
+                             uint64_t capacity, uint64_t id_space, ulonglong2* ol,
+                             unsigned long long* res, int32_t* slot_of, uint32_t* sid,
+                             uint32_t* smark, uint32_t* sfreq, uint32_t* slast, uint32_t* size,
+                             const uint32_t* cur_mark, unsigned long long* at_cur, int* status) {
+  const uint64_t so = static_cast<uint64_t>(j) * id_space + id;
+  int32_t s = slot_of[so];
+  const uint32_t cm = cur_mark[j];
+  if (s < 0) {
+    if (size[j] == capacity) {
+      *status = 1;  // touch would insert into a full cache
+      return;
+    }
+    s = static_cast<int32_t>(size[j]++);
+    const uint64_t g = static_cast<uint64_t>(j) * capacity + s;
+    slot_of[so] = s;
+    sid[g] = id;
+    smark[g] = cm;
+    sfreq[g] = 1;
+    slast[g] = clock;
+    at_cur[j] += 1;
+  } else {
+    const uint64_t g = static_cast<uint64_t>(j) * capacity + s;
+    if (smark[g] != cm) at_cur[j] += 1;
+    smark[g] = cm;
+    sfreq[g] += 1;
+    slast[g] = clock;
+  }
+  const unsigned long long bit = 1ULL << j;
+  res[id] |= bit;
+  if (latest) ol[id].y |= bit;
+  if (owner) ol[id].x |= bit;
+  *status = 0;
+}
+
+// validate_consistency (sim.hpp:222-248) over the device tables.
+// status: [0] entry without resident bit, [1] invariant violated (+id in [3]),
+// [2] resident bit without entry, [4] at_current_mark drift
+__global__ void k_validate_slots(int n, uint64_t capacity, uint64_t id_space,
+                                 const uint32_t* __restrict__ size, const uint32_t* __restrict__ sid,
+                                 const unsigned long long* __restrict__ res,
+                                 const int32_t* __restrict__ slot_of, const uint32_t* smark,
+                                 const uint32_t* cur_mark, unsigned long long* at_count,
+                                 int* status) {
+  const uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (x >= static_cast<uint64_t>(n) * capacity) return;
+  const int j = static_cast<int>(x / capacity);
+  const uint32_t s = static_cast<uint32_t>(x - static_cast<uint64_t>(j) * capacity);
+  if (s >= size[j]) return;
+  const uint32_t id = sid[x];
+  if (!((res[id] >> j) & 1ULL) || slot_of[static_cast<uint64_t>(j) * id_space + id] != static_cast<int32_t>(s))
+    atomicOr(status + 0, 1);
+  if (smark[x] == cur_mark[j]) atomicAdd(at_count + j, 1ULL);
+}
+
+__global__ void k_validate_ids(int n, uint64_t id_space, const ulonglong2* __restrict__ ol,
+                               const unsigned long long* __restrict__ res,
+                               const int32_t* __restrict__ slot_of, int* status) {
+  const uint64_t id = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (id >= id_space) return;
+  const ulonglong2 st = ol[id];
+  const unsigned long long r = res[id];
+  const bool ok = ((st.x & ~st.y) == 0) && ((st.y & ~r) == 0) && !(st.x != 0 && st.y != st.x);
+  if (!ok) {
+    if (atomicOr(status + 1, 1) == 0) status[3] = static_cast<int>(id);
+  }
+  for (unsigned long long it = r; it; it &= it - 1) {
+    const int w = __ffsll(static_cast<long long>(it)) - 1;
+    if (w >= n || slot_of[static_cast<uint64_t>(w) * id_space + id] < 0) atomicOr(status + 2, 1);
+  }
+}
+
+__global__ void k_export_cache(int j, uint64_t capacity, uint32_t count,
+                               const uint32_t* __restrict__ sid, const ulonglong2* __restrict__ ol,
+                               uint8_t* __restrict__ ver) {
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= count) return;
+  ver[s] = static_cast<uint8_t>((ol[sid[static_cast<uint64_t>(j) * capacity + s]].y >> j) & 1ULL);
+}
+
+// sum_i values[i*stride + col[i]] left to right (hungarian total, assign.hpp:153-155)
+__global__ void k_seq_gather_sum(const double* __restrict__ values, uint64_t k,
+                                 const uint64_t* __restrict__ col, double* out) {
+  double t = 0.0;
+  for (uint64_t i = 0; i < k; ++i) t = __dadd_rn(t, values[i * k + col[i]]);
+  *out = t;
+}
+
+__global__ void k_seq_gather_sum_blocks(const double* __restrict__ matrix, int n,
+                                        const uint64_t* __restrict__ rows, uint64_t k, int mult,
+                                        const uint64_t* __restrict__ col, double* out) {
+  double t = 0.0;
+  for (uint64_t i = 0; i < k; ++i)
+    t = __dadd_rn(t, matrix[rows[i] * n + col[i] / static_cast<uint64_t>(mult)]);
+  *out = t;
+}
+
+__global__ void k_u64_to_u32(const uint64_t* __restrict__ a, uint64_t n, uint32_t* __restrict__ b) {
+  const uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (x < n) b[x] = static_cast<uint32_t>(a[x]);
+}
+
+__global__ void k_u32_to_u64(const uint32_t* __restrict__ a, uint64_t n, uint64_t* __restrict__ b) {
+  const uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (x < n) b[x] = a[x];
+}
+
+__global__ void k_pair_rows(const uint64_t* __restrict__ order, uint64_t n, uint64_t* __restrict__ rows) {
+  const uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (x < n) rows[x] = order[x];
+}
+
+// -------------------------------------------------- process default context
+struct DefaultCtx {
+  std::mutex mu;
+  int device = -1;
+  cudaStream_t stream = nullptr;
+  edx::DispatchScratch disp;
+  DevBuf<double> values;
+  DevBuf<uint32_t> ids, u32a, u32b;
+  DevBuf<uint64_t> offsets, u64a, u64b;
+  DevBuf<int32_t> i32a, i32b;
+  DevBuf<unsigned long long> snapA, snapB, snapC;
+  DevBuf<ulonglong2> ol;
+  DevBuf<double> ucost, scalar;
+  DevBuf<int> flags;
+
+  void init() {
+    if (device >= 0) return;
+    int count = 0;
+    EDX_CUDA(cudaGetDeviceCount(&count));
+    if (count <= 0) throw Error(EDX_CUDA_ERROR, "no CUDA device");
+    EDX_CUDA(cudaGetDevice(&device));
+    EDX_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    flags.ensure(edx::kFlagCount);
+    scalar.ensure(4);
+  }
+  void reset_flags() { EDX_CUDA(cudaMemsetAsync(flags.p, 0, edx::kFlagCount * sizeof(int), stream)); }
+  void sync_and_check() {
+    int f[edx::kFlagCount];
+    EDX_CUDA(cudaMemcpyAsync(f, flags.p, sizeof f, cudaMemcpyDeviceToHost, stream));
+    EDX_CUDA(cudaStreamSynchronize(stream));
+    check_flags_host(f);
+  }
+};
+
+DefaultCtx& dctx() {
+  static DefaultCtx* c = new DefaultCtx;  // never destroyed: outlives CUDA teardown ordering
+  return *c;
+}
+
+// ------------------------------------------------------------ engine helpers
+void engine_sync_check(edx_engine* e) {
+  EDX_CUDA(cudaMemcpyAsync(e->h_flags, e->flags.p, edx::kFlagCount * sizeof(int),
+                           cudaMemcpyDeviceToHost, e->stream));
+  EDX_CUDA(cudaStreamSynchronize(e->stream));
+  int f[edx::kFlagCount];
+  std::memcpy(f, e->h_flags, sizeof f);
+  if (std::any_of(f, f + edx::kFlagCount, [](int v) { return v != 0; })) {
+    EDX_CUDA(cudaMemsetAsync(e->flags.p, 0, edx::kFlagCount * sizeof(int), e->stream));
+    EDX_CUDA(cudaStreamSynchronize(e->stream));
+    check_flags_host(f);
+  }
+  if (e->profiling) {
+    auto acc = [&](int a, int b, int phase) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, e->ev[a], e->ev[b]) == cudaSuccess) e->phase_ms[phase] += ms;
+    };
+    if (e->pending_build) acc(0, 1, 0);
+    if (e->pending_dispatch) {
+      acc(2, 3, 1);
+      acc(4, 5, 2);
+      if (e->pending_greedy) acc(6, 7, 3);
+      acc(10, 11, 5);
+    }
+    if (e->pending_step) acc(8, 9, 4);
+  }
+  e->pending_build = e->pending_dispatch = e->pending_step = e->pending_greedy = false;
+  cudaGetLastError();
+}
+
+void rec(edx_engine* e, int idx, cudaStream_t s) {
+  if (e->profiling) EDX_CUDA(cudaEventRecord(e->ev[idx], s));
+}
+
+void engine_load(edx_engine* e, const uint32_t* ids, const uint64_t* offsets, uint64_t R,
+                 int on_device) {
+  if (R == 0) edx::invalid("batch holds no samples");
+  uint64_t total;
+  if (on_device) {
+    uint64_t ends[2];
+    EDX_CUDA(cudaMemcpyAsync(&ends[0], offsets, sizeof(uint64_t), cudaMemcpyDeviceToHost, e->stream));
+    EDX_CUDA(cudaMemcpyAsync(&ends[1], offsets + R, sizeof(uint64_t), cudaMemcpyDeviceToHost, e->stream));
+    EDX_CUDA(cudaStreamSynchronize(e->stream));
+    if (ends[0] != 0) edx::invalid("device offsets must start at 0");
+    total = ends[1];
+    e->cur_ids = ids;
+    e->cur_offsets = offsets;
+  } else {
+    const uint64_t base = offsets[0];
+    for (uint64_t i = 0; i < R; ++i)
+      if (offsets[i + 1] < offsets[i]) edx::invalid("sample offsets must be non-decreasing");
+    total = offsets[R] - base;
+    if (total > e->max_ids)
+      edx::invalid("batch holds " + std::to_string(total) + " ids; engine max_batch_ids is " +
+                   std::to_string(e->max_ids));
+    e->h_offsets.assign(offsets, offsets + R + 1);
+    if (base)
+      for (auto& o : e->h_offsets) o -= base;
+    e->offsets.ensure(R + 1);
+    EDX_CUDA(cudaMemcpyAsync(e->ids.p, ids + base, total * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                             e->stream));
+    EDX_CUDA(cudaMemcpyAsync(e->offsets.p, e->h_offsets.data(), (R + 1) * sizeof(uint64_t),
+                             cudaMemcpyHostToDevice, e->stream));
+    e->cur_ids = e->ids.p;
+    e->cur_offsets = e->offsets.p;
+  }
+  if (total > e->max_ids)
+    edx::invalid("batch holds " + std::to_string(total) + " ids; engine max_batch_ids is " +
+                 std::to_string(e->max_ids));
+  e->rows = R;
+  e->total_ids = total;
+  e->built = e->dispatched = false;
+}
+
+void engine_build(edx_engine* e) {
+  const uint64_t want = static_cast<uint64_t>(e->n) * static_cast<uint64_t>(e->m);
+  if (!e->cur_ids) edx::invalid("no batch loaded");
+  if (e->rows != want)
+    edx::invalid("expected " + std::to_string(want) + " samples, got " + std::to_string(e->rows));
+  e->matrix.ensure(e->rows * e->n);
+  e->disp.gap_keys.ensure(e->rows);
+  e->disp.row_index.ensure(e->rows);
+  rec(e, 0, e->stream);
+  edx::launch_cost_build(e->cur_ids, e->cur_offsets, e->rows, e->n, e->ol.p, e->id_space,
+                         e->ucost.p, e->matrix.p, e->disp.gap_keys.p, e->disp.row_index.p,
+                         e->flags.p, e->stream);
+  rec(e, 1, e->stream);
+  e->launches += 1;
+  e->pending_build = e->profiling;
+  e->built = true;
+  e->gap_ready = true;
+}
+
+void engine_dispatch(edx_engine* e, double alpha) {
+  if (!e->built) edx::invalid("build the cost matrix before dispatching");
+  if (alpha < 0.0) alpha = e->alpha;
+  if (alpha > 1.0) edx::invalid("alpha must lie in [0, 1]");
+  e->decision.ensure(e->rows);
+  e->expected.ensure(1);
+  edx::PhaseEvents pe;
+  if (e->profiling) {
+    pe.sort0 = e->ev[2];
+    pe.sort1 = e->ev[3];
+    pe.exact0 = e->ev[4];
+    pe.exact1 = e->ev[5];
+    pe.greedy0 = e->ev[6];
+    pe.greedy1 = e->ev[7];
+  }
+  int launches = 0;
+  rec(e, 10, e->stream);
+  edx::run_ecomix(e->disp, e->matrix.p, e->rows, e->n, e->m, alpha, e->gap_ready,
+                  e->decision.p, e->flags.p, e->stream, e->device, e->profiling ? &pe : nullptr,
+                  &launches);
+  rec(e, 11, e->stream);
+  edx::launch_decision_cost(e->matrix.p, e->decision.p, e->rows, e->n, e->expected.p, e->stream);
+  e->launches += launches + 1;
+  const int mult = edx::exact_multiplicity(e->m, alpha);
+  e->pending_greedy = e->profiling && static_cast<uint64_t>(e->n) * mult < e->rows;
+  e->pending_dispatch = e->profiling;
+  e->dispatched = true;
+}
+
+// DispatchDecision::validate — assign.hpp:41-57, same messages.
+void validate_decision_host(const int32_t* w, uint64_t count, int n, int m) {
+  if (count != static_cast<uint64_t>(n) * static_cast<uint64_t>(m))
+    edx::invalid("decision does not cover m*n samples");
+  std::vector<int> load(static_cast<size_t>(n), 0);
+  for (uint64_t i = 0; i < count; ++i) {
+    if (w[i] < 0 || w[i] >= n) edx::invalid("worker id out of range");
+    ++load[w[i]];
+  }
+  for (int j = 0; j < n; ++j)
+    if (load[j] != m)
+      edx::invalid("worker " + std::to_string(j) + " received " + std::to_string(load[j]) +
+                   " samples, expected " + std::to_string(m));
+}
+
+void engine_step(edx_engine* e, const int32_t* decision, edx_report* rep) {
+  if (!e->cur_ids) edx::invalid("no batch loaded");
+  if (decision) {
+    validate_decision_host(decision, e->rows, e->n, e->m);
+    e->decision.ensure(e->rows);
+    EDX_CUDA(cudaMemcpyAsync(e->decision.p, decision, e->rows * sizeof(int32_t),
+                             cudaMemcpyHostToDevice, e->stream));
+  } else {
+    if (!e->dispatched) edx::invalid("no dispatch decision to step with");
+    if (e->rows != static_cast<uint64_t>(e->n) * e->m) edx::invalid("decision does not cover m*n samples");
+  }
+  if (e->clock >= 0xFFFFFFFFull) throw Error(EDX_RUNTIME_ERROR, "clock exceeds 2^32 iterations");
+  edx::StepResult sr;
+  rec(e, 8, e->stream);
+  edx::step_run(e, e->decision.p, &sr);
+  rec(e, 9, e->stream);
+  e->launches += sr.launches;
+  e->pending_step = e->profiling;
+  engine_sync_check(e);
+  // IterationReport totals and realised cost, worker order (sim.hpp:206-216)
+  const int n = e->n;
+  const unsigned long long* c = e->h_counters;
+  rep->iteration = e->clock;
+  rep->miss_pull = rep->update_push = rep->evict_push = 0;
+  rep->hits = c[3 * n];
+  rep->lookups = e->total_ids;
+  rep->cost_s = 0.0;
+  for (int j = 0; j < n; ++j) {
+    rep->miss_pull_w[j] = c[j];
+    rep->update_push_w[j] = c[n + j];
+    rep->evict_push_w[j] = c[2 * n + j];
+    rep->miss_pull += c[j];
+    rep->update_push += c[n + j];
+    rep->evict_push += c[2 * n + j];
+    const uint64_t ops = c[j] + c[n + j] + c[2 * n + j];
+    rep->cost_w[j] = static_cast<double>(ops) * e->ucost_h[j];
+    rep->cost_s += rep->cost_w[j];
+  }
+  ++e->clock;
+  e->dispatched = false;
+}
+
+}  // namespace
+
+// ===================================================================== C ABI
+extern "C" {
+
+void edx_set_error(int code, const char* msg) {
+  (void)code;
+  g_err = msg ? msg : "";
+}
+
+const char* edx_last_error(void) { return g_err.c_str(); }
+
+int edx_abi_version(void) { return 1; }
+
+int edx_validate_config(const edx_cluster_config* cfg, uint64_t max_sample_len) {
+  return guard([&] { validate_cfg(cfg, max_sample_len); });
+}
+
+int edx_unit_costs(const edx_cluster_config* cfg, double* out) {
+  return guard([&] {
+    if (!cfg || cfg->n < 1 || cfg->n_bandwidths < cfg->n) edx::invalid("worker id out of range");
+    const auto u = unit_costs(cfg);
+    std::copy(u.begin(), u.end(), out);
+  });
+}
+
+int edx_engine_create(const edx_cluster_config* cfg, const edx_engine_options* opt,
+                      edx_engine** out) {
+  return guard([&] {
+    *out = nullptr;
+    if (!cfg || !opt) edx::invalid("null argument");
+    if (cfg->n < 1) edx::invalid("worker count must be >= 1");
+    if (cfg->n > 64) edx::invalid("at most 64 workers supported");
+    if (cfg->m < 1) edx::invalid("batch size per worker must be >= 1");
+    if (cfg->n_bandwidths != cfg->n) edx::invalid("need one bandwidth per worker");
+    for (int j = 0; j < cfg->n; ++j)
+      if (!(cfg->bandwidths_bps[j] > 0.0)) edx::invalid("bandwidths must be positive");
+    if (cfg->cache_capacity == 0) edx::invalid("cache capacity must be positive");
+    if (cfg->alpha < 0.0 || cfg->alpha > 1.0) edx::invalid("alpha must lie in [0, 1]");
+    if (opt->id_space == 0 || opt->id_space > (1ULL << 32)) edx::invalid("id_space must be in [1, 2^32]");
+    if (opt->max_batch_ids == 0 || opt->max_batch_ids >= (1ULL << 31))
+      edx::invalid("max_batch_ids must be in [1, 2^31)");
+    if (opt->world_size > 1) throw Error(EDX_RUNTIME_ERROR, "multi-GPU engines are created through edx_engine_create with NCCL support (not built)");
+    int count = 0;
+    EDX_CUDA(cudaGetDeviceCount(&count));
+    if (opt->device < 0 || opt->device >= count) edx::invalid("CUDA device ordinal out of range");
+    EDX_CUDA(cudaSetDevice(opt->device));
+    auto e = std::make_unique<edx_engine>();
+    e->device = opt->device;
+    e->n = cfg->n;
+    e->m = cfg->m;
+    e->alpha = cfg->alpha;
+    e->capacity = cfg->cache_capacity;
+    e->d_tran = cfg->d_tran_bytes;
+    e->bw.assign(cfg->bandwidths_bps, cfg->bandwidths_bps + cfg->n);
+    e->ucost_h = unit_costs(cfg);
+    e->id_space = opt->id_space;
+    e->max_ids = opt->max_batch_ids;
+    e->rank = opt->rank;
+    e->world = opt->world_size < 1 ? 1 : opt->world_size;
+    EDX_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+    for (auto& ev : e->ev) EDX_CUDA(cudaEventCreate(&ev));
+    e->ol.ensure(e->id_space);
+    e->res.ensure(e->id_space);
+    EDX_CUDA(cudaMemsetAsync(e->ol.p, 0, e->id_space * sizeof(ulonglong2), e->stream));
+    EDX_CUDA(cudaMemsetAsync(e->res.p, 0, e->id_space * sizeof(unsigned long long), e->stream));
+    e->ucost.ensure(e->n);
+    EDX_CUDA(cudaMemcpyAsync(e->ucost.p, e->ucost_h.data(), e->n * sizeof(double),
+                             cudaMemcpyHostToDevice, e->stream));
+    e->ids.ensure(e->max_ids);
+    e->flags.ensure(edx::kFlagCount);
+    EDX_CUDA(cudaMemsetAsync(e->flags.p, 0, edx::kFlagCount * sizeof(int), e->stream));
+    EDX_CUDA(cudaMallocHost(&e->h_flags, edx::kFlagCount * sizeof(int)));
+    EDX_CUDA(cudaMallocHost(&e->h_counters, (3 * 64 + 8) * sizeof(unsigned long long)));
+    EDX_CUDA(cudaMallocHost(&e->h_expected, sizeof(double)));
+    e->disp.init(e->device);
+    edx::step_init_state(e.get());
+    EDX_CUDA(cudaStreamSynchronize(e->stream));
+    *out = e.release();
+  });
+}
+
+void edx_engine_destroy(edx_engine* e) {
+  if (!e) return;
+  cudaSetDevice(e->device);
+  cudaStreamSynchronize(e->stream);
+  for (auto& ev : e->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (e->h_flags) cudaFreeHost(e->h_flags);
+  if (e->h_counters) cudaFreeHost(e->h_counters);
+  if (e->h_expected) cudaFreeHost(e->h_expected);
+  cudaStream_t s = e->stream;
+  delete e;
+  if (s) cudaStreamDestroy(s);
+}
+
+int edx_engine_load_batch(edx_engine* e, const uint32_t* ids, const uint64_t* offsets,
+                          uint64_t num_samples, int on_device) {
+  return guard([&] {
+    EDX_CUDA(cudaSetDevice(e->device));
+    engine_load(e, ids, offsets, num_samples, on_device);
+  });
+}
+
+int edx_engine_build(edx_engine* e, double* matrix_out) {
+  return guard([&] {
+    EDX_CUDA(cudaSetDevice(e->device));
+    engine_build(e);
+    if (matrix_out) {
+      EDX_CUDA(cudaMemcpyAsync(matrix_out, e->matrix.p, e->rows * e->n * sizeof(double),
+                               cudaMemcpyDeviceToHost, e->stream));
+      engine_sync_check(e);
+    }
+  });
+}
+
+int edx_engine_dispatch(edx_engine* e, double alpha, int32_t* decision_out,
+                        double* expected_cost_out) {
+  return guard([&] {
+    EDX_CUDA(cudaSetDevice(e->device));
+    engine_dispatch(e, alpha);
+    if (decision_out)
+      EDX_CUDA(cudaMemcpyAsync(decision_out, e->decision.p, e->rows * sizeof(int32_t),
+                               cudaMemcpyDeviceToHost, e->stream));
+    if (expected_cost_out)
+      EDX_CUDA(cudaMemcpyAsync(e->h_expected, e->expected.p, sizeof(double),
+                               cudaMemcpyDeviceToHost, e->stream));
+    if (decision_out || expected_cost_out) engine_sync_check(e);
+    if (expected_cost_out) *expected_cost_out = *e->h_expected;
+  });
+}
+
+int edx_engine_step(edx_engine* e, const int32_t* decision, edx_report* rep) {
+  return guard([&] {
+    EDX_CUDA(cudaSetDevice(e->device));
+    engine_step(e, decision, rep);
+  });
+}
+
+int edx_engine_iterate(edx_engine* e, const uint32_t* ids, const uint64_t* offsets,
+                       uint64_t num_samples, int on_device, int32_t* decision_out,
+                       double* expected_cost_out, edx_report* rep) {
+  return guard([&] {
+    EDX_CUDA(cudaSetDevice(e->device));
+    engine_load(e, ids, offsets, num_samples, on_device);
+    engine_build(e);
+    engine_dispatch(e, -1.0);
+    if (decision_out)
+      EDX_CUDA(cudaMemcpyAsync(decision_out, e->decision.p, e->rows * sizeof(int32_t),
+                               cudaMemcpyDeviceToHost, e->stream));
+    if (expected_cost_out)
+      EDX_CUDA(cudaMemcpyAsync(e->h_expected, e->expected.p, sizeof(double),
+                               cudaMemcpyDeviceToHost, e->stream));
+    engine_step(e, nullptr, rep);
+    if (expected_cost_out) *expected_cost_out = *e->h_expected;
+  });
+}
+
+int edx_engine_seed_entry(edx_engine* e, uint32_t id, int32_t worker, int latest, int owner) {
+  return guard([&] {
+    if (owner && !latest) edx::invalid("an owner's copy is always latest");
+    if (worker < 0 || worker >= e->n) edx::invalid("worker out of range");
+    if (id >= e->id_space) edx::invalid("embedding id outside the engine's id_space");
+    EDX_CUDA(cudaSetDevice(e->device));
+    auto& c = e->cache;
+    int* status = reinterpret_cast<int*>(e->step.wscalars.p);
+    k_seed_entry<<<1, 1, 0, e->stream>>>(id, worker, latest, owner, static_cast<uint32_t>(e->clock),
+                                         e->capacity, e->id_space, e->ol.p, e->res.p, c.slot_of.p,
+                                         c.sid.p, c.smark.p, c.sfreq.p, c.slast.p, c.size.p,
+                                         c.cur_mark.p, c.at_cur.p, status);
+    EDX_LAUNCHED();
+    int st = 0;
+    EDX_CUDA(cudaMemcpyAsync(&st, status, sizeof st, cudaMemcpyDeviceToHost, e->stream));
+    EDX_CUDA(cudaStreamSynchronize(e->stream));
+    if (st == 1) edx::logic("touch would insert into a full cache; evict first");
+  });
+}
+
+int edx_engine_state_of(edx_engine* e, uint32_t id, uint64_t* owners, uint64_t* latest,
+                        uint64_t* resident) {
+  return guard([&] {
+    EDX_CUDA(cudaSetDevice(e->device));
+    if (id >= e->id_space) {  // unknown embeddings are {0,0,0} (sim.hpp:64-67)
+      *owners = *latest = *resident = 0;
+      return;
+    }
+    ulonglong2 st;
+    unsigned long long r;
+    EDX_CUDA(cudaMemcpyAsync(&st, e->ol.p + id, sizeof st, cudaMemcpyDeviceToHost, e->stream));
+    EDX_CUDA(cudaMemcpyAsync(&r, e->res.p + id, sizeof r, cudaMemcpyDeviceToHost, e->stream));
+    EDX_CUDA(cudaStreamSynchronize(e->stream));
+    *owners = st.x;
+    *latest = st.y;
+    *resident = r;
+  });
+}
+
+int edx_engine_validate_consistency(edx_engine* e) {
+  return guard([&] {
+    EDX_CUDA(cudaSetDevice(e->device));
+    DevBuf<int> status;
+    status.ensure(8);
+    DevBuf<unsigned long long> at;
+    at.ensure(e->n);
+    EDX_CUDA(cudaMemsetAsync(status.p, 0, 8 * sizeof(int), e->stream));
+    EDX_CUDA(cudaMemsetAsync(at.p, 0, e->n * sizeof(unsigned long long), e->stream));
+    auto& c = e->cache;
+    const uint64_t cells = static_cast<uint64_t>(e->n) * e->capacity;
+    k_validate_slots<<<grid_for(cells), kT, 0, e->stream>>>(e->n, e->capacity, e->id_space, c.size.p,
+                                                           c.sid.p, e->res.p, c.slot_of.p, c.smark.p,
+                                                           c.cur_mark.p, at.p, status.p);
+    k_validate_ids<<<grid_for(e->id_space), kT, 0, e->stream>>>(e->n, e->id_space, e->ol.p, e->res.p,
+                                                               c.slot_of.p, status.p);
+    EDX_LAUNCHED();
+    int st[8];
+    std::vector<unsigned long long> at_h(e->n), at_d(e->n);
+    EDX_CUDA(cudaMemcpyAsync(st, status.p, sizeof st, cudaMemcpyDeviceToHost, e->stream));
+    EDX_CUDA(cudaMemcpyAsync(at_h.data(), at.p, e->n * sizeof(unsigned long long), cudaMemcpyDeviceToHost, e->stream));
+    EDX_CUDA(cudaMemcpyAsync(at_d.data(), c.at_cur.p, e->n * sizeof(unsigned long long), cudaMemcpyDeviceToHost, e->stream));
+    EDX_CUDA(cudaStreamSynchronize(e->stream));
+    if (st[0]) edx::logic("cache entry missing from global resident set");
+    if (st[1]) edx::logic("embedding state invariant violated for id " + std::to_string(static_cast<uint32_t>(st[3])));
+    if (st[2]) edx::logic("global resident bit without a cache entry");
+    for (int j = 0; j < e->n; ++j)
+      if (at_h[j] != at_d[j]) edx::logic("at-current-mark count drifted on worker " + std::to_string(j));
+  });
+}
+
+uint64_t edx_engine_clock(edx_engine* e) { return e->clock; }
+
+int edx_engine_export_global(edx_engine* e, uint32_t* ids, uint64_t* owners, uint64_t* latest,
+                             uint64_t* resident, uint64_t cap, uint64_t* count) {
+  return guard([&] {
+    EDX_CUDA(cudaSetDevice(e->device));
+    DevBuf<unsigned long long> cnt;
+    cnt.ensure(1);
+    DevBuf<uint32_t> d_ids;
+    DevBuf<unsigned long long> d_m;
+    d_ids.ensure(cap);
+    d_m.ensure(3 * cap);
+    EDX_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), e->stream));
+    k_export_global<<<grid_for(e->id_space), kT, 0, e->stream>>>(e->ol.p, e->res.p, e->id_space,
+                                                                d_ids.p, d_m.p, cap, cnt.p);
+    EDX_LAUNCHED();
+    unsigned long long total = 0;
+    EDX_CUDA(cudaMemcpyAsync(&total, cnt.p, sizeof total, cudaMemcpyDeviceToHost, e->stream));
+    EDX_CUDA(cudaStreamSynchronize(e->stream));
+    *count = total;
+    if (cap == 0) return;
+    const uint64_t got = std::min<uint64_t>(total, cap);
+    std::vector<uint32_t> hid(got);
+    std::vector<unsigned long long> hm(3 * got);
+    EDX_CUDA(cudaMemcpy(hid.data(), d_ids.p, got * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    EDX_CUDA(cudaMemcpy(hm.data(), d_m.p, 3 * got * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    std::vector<uint64_t> perm(got);
+    std::iota(perm.begin(), perm.end(), 0);
+    std::sort(perm.begin(), perm.end(), [&](uint64_t a, uint64_t b) { return hid[a] < hid[b]; });
+    for (uint64_t t = 0; t < got; ++t) {
+      ids[t] = hid[perm[t]];
+      owners[t] = hm[3 * perm[t]];
+      latest[t] = hm[3 * perm[t] + 1];
+      resident[t] = hm[3 * perm[t] + 2];
+    }
+  });
+}
+
+int edx_engine_cache_size(edx_engine* e, int32_t worker, uint64_t* size) {
+  return guard([&] {
+    if (worker < 0 || worker >= e->n) edx::invalid("worker out of range");
+    EDX_CUDA(cudaSetDevice(e->device));
+    uint32_t s = 0;
+    EDX_CUDA(cudaMemcpyAsync(&s, e->cache.size.p + worker, sizeof s, cudaMemcpyDeviceToHost, e->stream));
+    EDX_CUDA(cudaStreamSynchronize(e->stream));
+    *size = s;
+  });
+}
+
+int edx_engine_export_cache(edx_engine* e, int32_t worker, uint32_t* ids, uint8_t* version,
+                            uint32_t* mark, uint32_t* freq, uint64_t* last_access) {
+  return guard([&] {
+    if (worker < 0 || worker >= e->n) edx::invalid("worker out of range");
+    EDX_CUDA(cudaSetDevice(e->device));
+    auto& c = e->cache;
+    uint32_t sz = 0;
+    EDX_CUDA(cudaMemcpyAsync(&sz, c.size.p + worker, sizeof sz, cudaMemcpyDeviceToHost, e->stream));
+    EDX_CUDA(cudaStreamSynchronize(e->stream));
+    if (sz == 0) return;
+    const uint64_t g = static_cast<uint64_t>(worker) * e->capacity;
+    std::vector<uint32_t> hid(sz), hm(sz), hf(sz), hl(sz);
+    std::vector<uint8_t> hv(sz);
+    DevBuf<uint8_t> dv;
+    dv.ensure(sz);
+    k_export_cache<<<grid_for(sz), kT, 0, e->stream>>>(worker, e->capacity, sz, c.sid.p, e->ol.p, dv.p);
+    EDX_LAUNCHED();
+    EDX_CUDA(cudaMemcpyAsync(hid.data(), c.sid.p + g, sz * 4, cudaMemcpyDeviceToHost, e->stream));
+    EDX_CUDA(cudaMemcpyAsync(hm.data(), c.smark.p + g, sz * 4, cudaMemcpyDeviceToHost, e->stream));
+    EDX_CUDA(cudaMemcpyAsync(hf.data(), c.sfreq.p + g, sz * 4, cudaMemcpyDeviceToHost, e->stream));
+    EDX_CUDA(cudaMemcpyAsync(hl.data(), c.slast.p + g, sz * 4, cudaMemcpyDeviceToHost, e->stream));
+    EDX_CUDA(cudaMemcpyAsync(hv.data(), dv.p, sz, cudaMemcpyDeviceToHost, e->stream));
+    EDX_CUDA(cudaStreamSynchronize(e->stream));
+    std::vector<uint32_t> perm(sz);
+    std::iota(perm.begin(), perm.end(), 0u);
+    std::sort(perm.begin(), perm.end(), [&](uint32_t a, uint32_t b) { return hid[a] < hid[b]; });
+    for (uint32_t t = 0; t < sz; ++t) {
+      ids[t] = hid[perm[t]];
+      version[t] = hv[perm[t]];
+      mark[t] = hm[perm[t]];
+      freq[t] = hf[perm[t]];
+      last_access[t] = hl[perm[t]];
+    }
+  });
+}
+
+int edx_engine_cache_marks(edx_engine* e, int32_t worker, uint32_t* current_mark,
+                           uint64_t* at_current_mark) {
+  return guard([&] {
+    if (worker < 0 || worker >= e->n) edx::invalid("worker out of range");
+    EDX_CUDA(cudaSetDevice(e->device));
+    unsigned long long at = 0;
+    EDX_CUDA(cudaMemcpyAsync(current_mark, e->cache.cur_mark.p + worker, sizeof(uint32_t),
+                             cudaMemcpyDeviceToHost, e->stream));
+    EDX_CUDA(cudaMemcpyAsync(&at, e->cache.at_cur.p + worker, sizeof at, cudaMemcpyDeviceToHost, e->stream));
+    EDX_CUDA(cudaStreamSynchronize(e->stream));
+    *at_current_mark = at;
+  });
+}
+
+int edx_engine_import_snapshot(edx_engine* e, const uint32_t* ids, const uint64_t* owners,
+                               const uint64_t* latest, const uint64_t* resident, uint64_t count) {
+  return guard([&] {
+    EDX_CUDA(cudaSetDevice(e->device));
+    EDX_CUDA(cudaMemsetAsync(e->ol.p, 0, e->id_space * sizeof(ulonglong2), e->stream));
+    EDX_CUDA(cudaMemsetAsync(e->res.p, 0, e->id_space * sizeof(unsigned long long), e->stream));
+    if (count) {
+      DevBuf<uint32_t> d_ids;
+      DevBuf<unsigned long long> a, b, c;
+      d_ids.ensure(count);
+      a.ensure(count);
+      b.ensure(count);
+      c.ensure(count);
+      EDX_CUDA(cudaMemcpyAsync(d_ids.p, ids, count * 4, cudaMemcpyHostToDevice, e->stream));
+      EDX_CUDA(cudaMemcpyAsync(a.p, owners, count * 8, cudaMemcpyHostToDevice, e->stream));
+      EDX_CUDA(cudaMemcpyAsync(b.p, latest, count * 8, cudaMemcpyHostToDevice, e->stream));
+      if (resident) EDX_CUDA(cudaMemcpyAsync(c.p, resident, count * 8, cudaMemcpyHostToDevice, e->stream));
+      k_import<<<grid_for(count), kT, 0, e->stream>>>(d_ids.p, a.p, b.p, resident ? c.p : nullptr,
+                                                     count, e->id_space, e->ol.p, e->res.p, e->flags.p);
+      EDX_LAUNCHED();
+      engine_sync_check(e);
+    }
+  });
+}
+
+int edx_engine_set_profiling(edx_engine* e, int on) {
+  return guard([&] { e->profiling = on != 0; });
+}
+
+int edx_engine_phase_times(edx_engine* e, double* ms, uint64_t* counts, int reset) {
+  return guard([&] {
+    EDX_CUDA(cudaSetDevice(e->device));
+    engine_sync_check(e);
+    if (ms) std::copy(e->phase_ms, e->phase_ms + EDX_NUM_PHASES, ms);
+    if (counts) {
+      counts[0] = e->launches;
+      counts[1] = edx::last_hungarian_steps(e->disp.hung, e->stream);
+    }
+    if (reset) {
+      std::fill(e->phase_ms, e->phase_ms + EDX_NUM_PHASES, 0.0);
+      e->launches = 0;
+    }
+  });
+}
+
+// ------------------------------------------------------ stateless matrix API
+
+int edx_build_matrix(const edx_cluster_config* cfg, const uint32_t* snap_ids,
+                     const uint64_t* snap_owners, const uint64_t* snap_latest,
+                     const uint64_t* snap_resident, uint64_t snap_count, const uint32_t* ids,
+                     const uint64_t* offsets, uint64_t R, double* out) {
+  return guard([&] {
+    if (!cfg || cfg->n < 1 || cfg->n > 64) edx::invalid(cfg && cfg->n > 64 ? "at most 64 workers supported" : "worker count must be >= 1");
+    const uint64_t want = static_cast<uint64_t>(cfg->n) * static_cast<uint64_t>(cfg->m);
+    if (R != want) edx::invalid("expected " + std::to_string(want) + " samples, got " + std::to_string(R));
+    auto& c = dctx();
+    std::lock_guard<std::mutex> lk(c.mu);
+    c.init();
+    const uint64_t base = offsets[0], total = offsets[R] - base;
+    uint64_t max_id = 0;
+    for (uint64_t s = 0; s < snap_count; ++s) max_id = std::max<uint64_t>(max_id, snap_ids[s]);
+    for (uint64_t t = 0; t < total; ++t) max_id = std::max<uint64_t>(max_id, ids[base + t]);
+    const uint64_t space = max_id + 1;
+    if (space > (1ULL << 28)) edx::invalid("ids too large for the stateless dense snapshot table (< 2^28)");
+    const auto u = unit_costs(cfg);
+    std::vector<uint64_t> offs(offsets, offsets + R + 1);
+    for (auto& o : offs) o -= base;
+    c.ol.ensure(space);
+    c.ids.ensure(total);
+    c.offsets.ensure(R + 1);
+    c.ucost.ensure(cfg->n);
+    c.values.ensure(R * cfg->n);
+    c.reset_flags();
+    EDX_CUDA(cudaMemsetAsync(c.ol.p, 0, space * sizeof(ulonglong2), c.stream));
+    if (total) EDX_CUDA(cudaMemcpyAsync(c.ids.p, ids + base, total * 4, cudaMemcpyHostToDevice, c.stream));
+    EDX_CUDA(cudaMemcpyAsync(c.offsets.p, offs.data(), (R + 1) * 8, cudaMemcpyHostToDevice, c.stream));
+    EDX_CUDA(cudaMemcpyAsync(c.ucost.p, u.data(), cfg->n * 8, cudaMemcpyHostToDevice, c.stream));
+    if (snap_count) {
+      c.u32a.ensure(snap_count);
+      c.snapA.ensure(snap_count);
+      c.snapB.ensure(snap_count);
+      EDX_CUDA(cudaMemcpyAsync(c.u32a.p, snap_ids, snap_count * 4, cudaMemcpyHostToDevice, c.stream));
+      EDX_CUDA(cudaMemcpyAsync(c.snapA.p, snap_owners, snap_count * 8, cudaMemcpyHostToDevice, c.stream));
+      EDX_CUDA(cudaMemcpyAsync(c.snapB.p, snap_latest, snap_count * 8, cudaMemcpyHostToDevice, c.stream));
+      k_import<<<grid_for(snap_count), kT, 0, c.stream>>>(c.u32a.p, c.snapA.p, c.snapB.p, nullptr,
+                                                         snap_count, space, c.ol.p, nullptr, c.flags.p);
+      EDX_LAUNCHED();
+    }
+    (void)snap_resident;  // residency never enters the cost (cost.hpp:81-100)
+    edx::launch_cost_build(c.ids.p, c.offsets.p, R, cfg->n, c.ol.p, space, c.ucost.p, c.values.p,
+                           nullptr, nullptr, c.flags.p, c.stream);
+    EDX_CUDA(cudaMemcpyAsync(out, c.values.p, R * cfg->n * 8, cudaMemcpyDeviceToHost, c.stream));
+    c.sync_and_check();
+  });
+}
+
+int edx_row_gap_key(uint64_t rows, uint64_t cols, const double* values, uint64_t row, double* out) {
+  return guard([&] {
+    if (cols == 0) edx::invalid("row is empty");
+    if (row >= rows) edx::invalid("row index out of range");
+    if (cols > 64) edx::invalid("at most 64 workers supported");
+    auto& c = dctx();
+    std::lock_guard<std::mutex> lk(c.mu);
+    c.init();
+    c.values.ensure(cols);
+    c.u64a.ensure(1);
+    c.u32a.ensure(1);
+    EDX_CUDA(cudaMemcpyAsync(c.values.p, values + row * cols, cols * 8, cudaMemcpyHostToDevice, c.stream));
+    edx::launch_gap_keys(c.values.p, 1, static_cast<int>(cols), c.u64a.p, c.u32a.p, c.stream);
+    uint64_t key = 0;
+    EDX_CUDA(cudaMemcpyAsync(&key, c.u64a.p, 8, cudaMemcpyDeviceToHost, c.stream));
+    EDX_CUDA(cudaStreamSynchronize(c.stream));
+    const uint64_t bits = ~key;
+    std::memcpy(out, &bits, sizeof(double));
+  });
+}
+
+int edx_rows_by_gap(uint64_t rows, uint64_t cols, const double* values, uint64_t* order) {
+  return guard([&] {
+    if (rows == 0) return;
+    if (cols == 0) edx::invalid("row is empty");
+    if (cols > 64) edx::invalid("at most 64 workers supported");
+    if (rows >= (1ULL << 31)) edx::invalid("too many rows");
+    auto& c = dctx();
+    std::lock_guard<std::mutex> lk(c.mu);
+    c.init();
+    c.values.ensure(rows * cols);
+    c.u64a.ensure(rows);
+    c.u64b.ensure(rows);
+    c.u32a.ensure(rows);
+    c.u32b.ensure(rows);
+    EDX_CUDA(cudaMemcpyAsync(c.values.p, values, rows * cols * 8, cudaMemcpyHostToDevice, c.stream));
+    edx::launch_gap_keys(c.values.p, rows, static_cast<int>(cols), c.u64a.p, c.u32a.p, c.stream);
+    edx::sort_rows_by_gap(c.disp.sort, c.u64a.p, c.u32a.p, c.u32b.p, rows, c.stream);
+    k_u32_to_u64<<<grid_for(rows), kT, 0, c.stream>>>(c.u32b.p, rows, c.u64b.p);
+    EDX_LAUNCHED();
+    EDX_CUDA(cudaMemcpyAsync(order, c.u64b.p, rows * 8, cudaMemcpyDeviceToHost, c.stream));
+    EDX_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+namespace {
+void check_costs_host(const double* v, uint64_t count) {
+  for (uint64_t i = 0; i < count; ++i)
+    if (!std::isfinite(v[i]) || v[i] < 0.0) edx::invalid("costs must be finite and non-negative");
+}
+}  // namespace
+
+int edx_hungarian(uint64_t k, const double* values, uint64_t* col_of_row, double* total) {
+  return guard([&] {
+    if (k < 1) edx::invalid("solver needs at least one row");
+    if (k > 16384) edx::invalid("solver order above 16384 is not supported");
+    check_costs_host(values, k * k);  // assign.hpp:86-90 rejects before solving
+    auto& c = dctx();
+    std::lock_guard<std::mutex> lk(c.mu);
+    c.init();
+    c.values.ensure(k * k);
+    c.u64a.ensure(k);
+    c.reset_flags();
+    EDX_CUDA(cudaMemcpyAsync(c.values.p, values, k * k * 8, cudaMemcpyHostToDevice, c.stream));
+    edx::launch_hungarian_dense(c.disp.hung, c.values.p, k, c.u64a.p, c.flags.p, c.stream, c.device);
+    k_seq_gather_sum<<<1, 1, 0, c.stream>>>(c.values.p, k, c.u64a.p, c.scalar.p);
+    EDX_LAUNCHED();
+    double t = 0.0;
+    EDX_CUDA(cudaMemcpyAsync(col_of_row, c.u64a.p, k * 8, cudaMemcpyDeviceToHost, c.stream));
+    EDX_CUDA(cudaMemcpyAsync(&t, c.scalar.p, 8, cudaMemcpyDeviceToHost, c.stream));
+    c.sync_and_check();
+    if (total) *total = t;
+  });
+}
+
+int edx_hungarian_blocks(uint64_t rows, uint64_t cols, const double* values,
+                         const uint64_t* block_rows, int32_t mult, uint64_t* col_of_row,
+                         double* total) {
+  return guard([&] {
+    if (mult < 1) edx::invalid("solver needs at least one row");
+    if (cols < 1 || cols > 64) edx::invalid("at most 64 workers supported");
+    const uint64_t k = cols * static_cast<uint64_t>(mult);
+    for (uint64_t r = 0; r < k; ++r) {
+      if (block_rows[r] >= rows) edx::invalid("row index out of range");
+      check_costs_host(values + block_rows[r] * cols, cols);
+    }
+    auto& c = dctx();
+    std::lock_guard<std::mutex> lk(c.mu);
+    c.init();
+    c.values.ensure(rows * cols);
+    c.u64a.ensure(k);
+    c.u64b.ensure(k);
+    c.u32a.ensure(k);
+    c.reset_flags();
+    EDX_CUDA(cudaMemcpyAsync(c.values.p, values, rows * cols * 8, cudaMemcpyHostToDevice, c.stream));
+    EDX_CUDA(cudaMemcpyAsync(c.u64b.p, block_rows, k * 8, cudaMemcpyHostToDevice, c.stream));
+    k_u64_to_u32<<<grid_for(k), kT, 0, c.stream>>>(c.u64b.p, k, c.u32a.p);
+    EDX_LAUNCHED();
+    edx::launch_hungarian_blocks(c.disp.hung, c.values.p, static_cast<int>(cols), c.u32a.p, mult,
+                                 nullptr, nullptr, c.u64a.p, c.flags.p, c.stream, c.device);
+    k_seq_gather_sum_blocks<<<1, 1, 0, c.stream>>>(c.values.p, static_cast<int>(cols), c.u64b.p, k,
+                                                   mult, c.u64a.p, c.scalar.p);
+    EDX_LAUNCHED();
+    double t = 0.0;
+    EDX_CUDA(cudaMemcpyAsync(col_of_row, c.u64a.p, k * 8, cudaMemcpyDeviceToHost, c.stream));
+    EDX_CUDA(cudaMemcpyAsync(&t, c.scalar.p, 8, cudaMemcpyDeviceToHost, c.stream));
+    c.sync_and_check();
+    if (total) *total = t;
+  });
+}
+
+int edx_greedy_dispatch(uint64_t rows, uint64_t cols, const double* values, const uint64_t* order,
+                        uint64_t n_order, const int32_t* capacity, uint64_t* out_rows,
+                        int32_t* out_workers) {
+  return guard([&] {
+    if (cols < 1 || cols > 64) edx::invalid("need one capacity per worker");
+    long total = 0;
+    for (uint64_t j = 0; j < cols; ++j) total += capacity[j];
+    if (total != static_cast<long>(n_order)) edx::invalid("capacities must sum to the number of rows");
+    for (uint64_t t = 0; t < n_order; ++t)
+      if (order[t] >= rows) edx::invalid("row index out of range");
+    if (n_order == 0) return;
+    auto& c = dctx();
+    std::lock_guard<std::mutex> lk(c.mu);
+    c.init();
+    c.values.ensure(rows * cols);
+    c.u64a.ensure(n_order);
+    c.u32a.ensure(n_order);
+    c.i32a.ensure(cols);
+    c.i32b.ensure(n_order);
+    c.reset_flags();
+    EDX_CUDA(cudaMemcpyAsync(c.values.p, values, rows * cols * 8, cudaMemcpyHostToDevice, c.stream));
+    EDX_CUDA(cudaMemcpyAsync(c.u64a.p, order, n_order * 8, cudaMemcpyHostToDevice, c.stream));
+    EDX_CUDA(cudaMemcpyAsync(c.i32a.p, capacity, cols * 4, cudaMemcpyHostToDevice, c.stream));
+    k_u64_to_u32<<<grid_for(n_order), kT, 0, c.stream>>>(c.u64a.p, n_order, c.u32a.p);
+    EDX_LAUNCHED();
+    edx::launch_greedy(c.values.p, rows, static_cast<int>(cols), c.u32a.p, n_order, c.i32a.p, 0,
+                       nullptr, nullptr, c.i32b.p, c.flags.p, c.stream);
+    EDX_CUDA(cudaMemcpyAsync(out_workers, c.i32b.p, n_order * 4, cudaMemcpyDeviceToHost, c.stream));
+    c.sync_and_check();
+    std::copy(order, order + n_order, out_rows);
+  });
+}
+
+int edx_ecomix(const edx_cluster_config* cfg, uint64_t rows, uint64_t cols, const double* values,
+               const uint64_t* row_ids, int32_t* decision) {
+  return guard([&] {
+    if (!cfg) edx::invalid("null cluster config");
+    if (rows != static_cast<uint64_t>(cfg->n) * static_cast<uint64_t>(cfg->m) ||
+        cols != static_cast<uint64_t>(cfg->n))
+      edx::invalid("matrix shape does not match cluster config");
+    if (cfg->n > 64) edx::invalid("at most 64 workers supported");
+    const int mult = edx::exact_multiplicity(cfg->m, cfg->alpha);
+    if (mult > 0) check_costs_host(values, rows * cols);
+    auto& c = dctx();
+    std::lock_guard<std::mutex> lk(c.mu);
+    c.init();
+    c.values.ensure(rows * cols);
+    c.i32a.ensure(rows);
+    c.reset_flags();
+    EDX_CUDA(cudaMemcpyAsync(c.values.p, values, rows * cols * 8, cudaMemcpyHostToDevice, c.stream));
+    EDX_CUDA(cudaMemsetAsync(c.i32a.p, 0xff, rows * 4, c.stream));
+    edx::run_ecomix(c.disp, c.values.p, rows, cfg->n, cfg->m, cfg->alpha, false, c.i32a.p, c.flags.p,
+                    c.stream, c.device, nullptr, nullptr);
+    std::vector<int32_t> by_row(rows);
+    EDX_CUDA(cudaMemcpyAsync(by_row.data(), c.i32a.p, rows * 4, cudaMemcpyDeviceToHost, c.stream));
+    c.sync_and_check();
+    // decision.worker_of_sample[sample_of_row(row)] (assign.hpp:260-262)
+    std::fill(decision, decision + rows, -1);
+    for (uint64_t r = 0; r < rows; ++r) {
+      const uint64_t sidx = row_ids ? row_ids[r] : r;
+      if (sidx >= rows) edx::invalid("worker id out of range");
+      decision[sidx] = by_row[r];
+    }
+    validate_decision_host(decision, rows, cfg->n, cfg->m);
+  });
+}
+
+int edx_decision_cost(uint64_t rows, uint64_t cols, const double* values, const int32_t* decision,
+                      double* out) {
+  return guard([&] {
+    for (uint64_t i = 0; i < rows; ++i)
+      if (decision[i] < 0 || static_cast<uint64_t>(decision[i]) >= cols) edx::invalid("worker id out of range");
+    if (rows == 0) {
+      *out = 0.0;
+      return;
+    }
+    auto& c = dctx();
+    std::lock_guard<std::mutex> lk(c.mu);
+    c.init();
+    c.values.ensure(rows * cols);
+    c.i32a.ensure(rows);
+    EDX_CUDA(cudaMemcpyAsync(c.values.p, values, rows * cols * 8, cudaMemcpyHostToDevice, c.stream));
+    EDX_CUDA(cudaMemcpyAsync(c.i32a.p, decision, rows * 4, cudaMemcpyHostToDevice, c.stream));
+    edx::launch_decision_cost(c.values.p, c.i32a.p, rows, static_cast<int>(cols), c.scalar.p, c.stream);
+    EDX_CUDA(cudaMemcpyAsync(out, c.scalar.p, 8, cudaMemcpyDeviceToHost, c.stream));
+    EDX_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,104 @@
+// The edx_engine object: one SimState (sim.hpp:54-268) resident on one GPU.
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "edx_internal.cuh"
+
+namespace edx {
+
+// Device-resident per-worker caches (WorkerCache, cache.hpp:73-240).  Entry
+// metadata lives in per-worker slot arrays (capacity entries each); a slot is
+// located by slot_of[j * id_space + id].  The version flag is not stored: the
+// reference keeps CacheEntry::version_latest equal to the worker's bit of the
+// global `latest` mask at all times (validate_consistency, sim.hpp:229-231),
+// so the step reads it from the mask.
+struct CacheState {
+  DevBuf<int32_t> slot_of;   // n * id_space, -1 = not resident
+  DevBuf<uint32_t> sid;      // n * capacity : id in slot
+  DevBuf<uint32_t> smark;    // mark (cache.hpp:39)
+  DevBuf<uint32_t> sfreq;    // frequency (cache.hpp:40)
+  DevBuf<uint32_t> slast;    // last_access (cache.hpp:41), < 2^32 enforced
+  DevBuf<uint32_t> size;     // n
+  DevBuf<uint32_t> cur_mark; // n (current_mark_, cache.hpp:236)
+  DevBuf<unsigned long long> at_cur;  // n (at_current_mark_, cache.hpp:237)
+};
+
+// Scratch of one SimState::step (sim.hpp:87-218).
+struct StepScratch {
+  DevBuf<uint32_t> occ_sample;   // occurrence -> sample
+  DevBuf<int32_t> first_pos;     // id_space: first occurrence of the id in the batch (or INT_MAX)
+  DevBuf<uint32_t> uidx_of_pos;  // occurrence -> unique index (valid at first occurrences)
+  DevBuf<uint32_t> uniq;         // unique ids in first-appearance order
+  DevBuf<unsigned long long> umask;  // trainers mask per unique id
+  DevBuf<int32_t> need_first;    // n * U : first occurrence position of (j, id)
+  DevBuf<uint32_t> need_cnt;     // n * U : occurrences of (j, id)
+  DevBuf<uint8_t> flag;          // per occurrence: 1 = first occurrence of (worker, id)
+  DevBuf<uint32_t> flag_scan;    // scratch
+  DevBuf<uint64_t> need_key;     // (worker << 32 | pos) of first occurrences
+  DevBuf<uint64_t> need_key_sorted;
+  DevBuf<uint32_t> need_off;     // n + 1 : CSR of the need lists
+  DevBuf<uint8_t> need_type;     // 0 hit, 1 refresh, 2 insert
+  DevBuf<int32_t> need_contrib;  // epoch-scan contribution
+  DevBuf<uint32_t> ins_rank;     // insert ordinal within the worker
+  DevBuf<unsigned long long> counters;  // per-worker counters + totals
+  DevBuf<uint64_t> cand_key, cand_key_sorted;  // victim candidates
+  DevBuf<uint32_t> cand_slot, cand_slot_sorted;
+  DevBuf<uint32_t> cand_count;   // n
+  DevBuf<uint32_t> cand_off;     // n + 1
+  DevBuf<uint32_t> wscalars;     // per-worker scalars of the step
+  DevBuf<uint32_t> ranges;       // key-packing ranges
+  DevBuf<uint8_t> temp;          // CUB temp storage
+  DevBuf<uint32_t> ucount;       // number of unique ids
+};
+
+}  // namespace edx
+
+struct edx_engine {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int n = 0, m = 0;
+  double alpha = 1.0;
+  uint64_t capacity = 0, d_tran = 0;
+  std::vector<double> bw, ucost_h;
+  uint64_t id_space = 0, max_ids = 0;
+  int rank = 0, world = 1;
+  uint64_t clock = 0;
+
+  // global per-embedding state (SimState::global_, sim.hpp:266), dense by id
+  edx::DevBuf<ulonglong2> ol;             // {owners, latest}
+  edx::DevBuf<unsigned long long> res;    // resident
+  edx::DevBuf<double> ucost;
+  edx::CacheState cache;
+  edx::StepScratch step;
+
+  // current batch
+  edx::DevBuf<uint32_t> ids;
+  edx::DevBuf<uint64_t> offsets;
+  const uint32_t* cur_ids = nullptr;
+  const uint64_t* cur_offsets = nullptr;
+  uint64_t rows = 0, total_ids = 0;
+  std::vector<uint64_t> h_offsets;  // host copy of the current offsets
+
+  // per-iteration products
+  edx::DevBuf<double> matrix;
+  edx::DevBuf<int32_t> decision;
+  edx::DevBuf<double> expected;
+  edx::DispatchScratch disp;
+  bool built = false, gap_ready = false, dispatched = false;
+
+  edx::DevBuf<int> flags;
+  int* h_flags = nullptr;            // pinned
+  unsigned long long* h_counters = nullptr;  // pinned
+  double* h_expected = nullptr;      // pinned
+
+  // profiling
+  bool profiling = false;
+  cudaEvent_t ev[12] = {};
+  double phase_ms[EDX_NUM_PHASES] = {};
+  uint64_t launches = 0;
+  uint64_t solver_steps = 0;
+  bool pending_build = false, pending_dispatch = false, pending_step = false,
+       pending_greedy = false;
+};

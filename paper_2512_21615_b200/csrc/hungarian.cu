@@ -1,0 +1,547 @@
+// K6 block-collapsed e-maxx Hungarian (EcoMix exact block) and K5 dense
+// e-maxx Hungarian (the general hungarian() API).
+//
+// Reference: hungarian (assign.hpp:80-157).  Costs are scaled to int64 by
+// llround(v * 1e12) and capped at INT64_MAX / (8 (k+1)); rows are inserted
+// 1..k in order; each Dijkstra step relaxes the unused columns from the row
+// just reached (strict '<' keeps the earliest way) and picks the unused
+// column of least minv (strict '<' over ascending j: lowest index on ties);
+// potentials then move by delta.  An equal-cost re-solve moves rows
+// (SURVEY §0 hazard 3), so both kernels execute this exact algorithm, step
+// for step, in int64.
+//
+// K6 exploits the structure ecomix feeds the solver (expand_columns,
+// assign.hpp:223-241): columns [w*mult, (w+1)*mult) repeat worker w's cost.
+// Within one row's search v[j] of an unused column never changes (only used
+// columns' potentials move), and every unused column of block w is relaxed
+// by the same a[i0][w] - u[i0].  Writing Δ for the running sum of the
+// step's deltas, every unused j in block w therefore has
+//     minv[j] = D_w - Δ - v[j],   D_w = min over reached rows (a[r][w] - u[r] + Δ_r)
+// with one shared way_w.  The block's least-minv column is its unused column
+// of largest v (lowest index on ties), blocks are index-ordered, so the global
+// argmin is a per-block candidate argmin, and the per-step cost is O(n)
+// instead of O(k).  The potential moves of used columns are applied lazily at
+// the end of the row from Δ at the time each column was reached, which is
+// exact in int64.  Each block keeps its columns sorted by (v desc, j asc);
+// within a row the chosen columns are a prefix of that order (a cursor), and
+// at row end only that prefix changes key and is merged back.
+//
+// K6 runs on ONE warp of one SM: lane w owns block w (n <= 64, two blocks per
+// lane above 32).  It is latency-bound by construction (one dependent
+// Dijkstra step after another); state lives in shared memory when it fits.
+#include <climits>
+
+#include "edx_internal.cuh"
+
+namespace edx {
+
+namespace {
+
+constexpr int64_t kInf = LLONG_MAX;
+
+// std::llround(x * 1e12) then std::min(., cap) as compiled for x86-64/glibc
+// (assign.hpp:96-100): round half away from zero; out-of-range -> INT64_MIN.
+__device__ __forceinline__ int64_t scale_cost(double x, int64_t cap) {
+  const double y = __dmul_rn(x, 1e12);
+  int64_t s;
+  if (!(y < 9223372036854775808.0)) {
+    s = LLONG_MIN;
+  } else {
+    const long long t = __double2ll_rz(y);
+    const double f = __dsub_rn(y, __ll2double_rn(t));
+    s = t + (f >= 0.5 ? 1 : 0);
+  }
+  return s < cap ? s : cap;
+}
+
+__device__ __forceinline__ bool bad_cost(double x) { return !isfinite(x) || x < 0.0; }
+
+// S[r][w] = scaled cost of block row r (matrix row order[r]) for worker w.
+__global__ void k_scale_block(const double* __restrict__ matrix, int n,
+                              const uint32_t* __restrict__ order, uint64_t k, int64_t cap,
+                              int64_t* __restrict__ S, int* __restrict__ flags) {
+  const uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (x >= k * n) return;
+  const uint64_t r = x / n, w = x - r * n;
+  const double v = matrix[static_cast<uint64_t>(order[r]) * n + w];
+  if (bad_cost(v)) atomicOr(flags + kFlagBadCost, 1);
+  S[x] = scale_cost(v, cap);
+}
+
+struct BlockArrays {
+  const int64_t* S;  // k x n
+  int64_t *u, *v, *dlt;
+  int32_t *p, *way, *ulist, *ord, *tmp;
+};
+
+// (v desc, j asc): does column a come before column b in its block's order?
+__device__ __forceinline__ bool before(const int64_t* v, int a, int b) {
+  const int64_t va = v[a], vb = v[b];
+  return va > vb || (va == vb && a < b);
+}
+
+template <int NB>
+__device__ bool hungarian_blocks_warp(const BlockArrays A, int n, int mult, int k,
+                                      unsigned long long* steps_out, int* flags) {
+  const int lane = threadIdx.x & 31;
+  const int64_t* __restrict__ S = A.S;
+  int64_t* __restrict__ u = A.u;
+  int64_t* __restrict__ v = A.v;
+  int64_t* __restrict__ dlt = A.dlt;
+  int32_t* __restrict__ p = A.p;
+  int32_t* __restrict__ way = A.way;
+  int32_t* __restrict__ ulist = A.ulist;
+  int32_t* __restrict__ ord = A.ord;
+  int32_t* __restrict__ tmp = A.tmp;
+
+  for (int x = lane; x <= k; x += 32) {
+    u[x] = 0;
+    v[x] = 0;
+    p[x] = 0;
+    way[x] = 0;
+  }
+  for (int x = lane; x < k; x += 32) ord[x] = x + 1;  // v all 0: index order
+  __syncwarp();
+
+  unsigned long long steps = 0;
+  int64_t D[NB], bestv[NB];
+  int wy[NB], cur[NB], bestc[NB];
+
+  for (int i = 1; i <= k; ++i) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int w = lane + 32 * b;
+      D[b] = kInf;
+      wy[b] = 0;
+      cur[b] = 0;
+      if (w < n) {
+        bestc[b] = ord[w * mult];
+        bestv[b] = v[bestc[b]];
+      } else {
+        bestc[b] = 0;
+        bestv[b] = 0;
+      }
+    }
+    if (lane == 0) {
+      p[0] = i;
+      ulist[0] = 0;
+      dlt[0] = 0;
+    }
+    int nused = 1;
+    int j0 = 0, r = i, j1;
+    int64_t Dl = 0;  // Δ: running sum of this row's deltas
+    __syncwarp();
+    for (;;) {
+      ++steps;
+      const int64_t ur = u[r];
+      const int64_t* __restrict__ Srow = S + static_cast<int64_t>(r - 1) * n;
+      int64_t bv = kInf;
+      int bw = INT_MAX;
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const int w = lane + 32 * b;
+        if (w < n && cur[b] < mult) {
+          const int64_t c = Srow[w] - ur + Dl;  // = cur + v[j] + Δ for every unused j of w
+          if (c < D[b]) {
+            D[b] = c;
+            wy[b] = j0;
+          }
+          const int64_t val = D[b] - Dl - bestv[b];  // minv of the block's best column
+          if (val < bv) {
+            bv = val;
+            bw = w;
+          }
+        }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const int64_t ov = __shfl_xor_sync(0xffffffffu, bv, off);
+        const int ow = __shfl_xor_sync(0xffffffffu, bw, off);
+        if (ov < bv || (ov == bv && ow < bw)) {
+          bv = ov;
+          bw = ow;
+        }
+      }
+      if (bw == INT_MAX) {  // no unused column: only reachable on corrupt input
+        if (lane == 0) atomicOr(flags + kFlagBadCost, 1);
+        return false;
+      }
+      const int owner = bw & 31, ob = bw >> 5;
+      int mine = bestc[0];
+#pragma unroll
+      for (int b = 1; b < NB; ++b)
+        if (ob == b) mine = bestc[b];
+      j1 = __shfl_sync(0xffffffffu, mine, owner);
+      Dl += bv;
+      if (lane == owner) {
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          if (b != ob) continue;
+          way[j1] = wy[b];
+          dlt[j1] = Dl;
+          ++cur[b];
+          if (cur[b] < mult) {
+            bestc[b] = ord[bw * mult + cur[b]];
+            bestv[b] = v[bestc[b]];
+          }
+        }
+      }
+      if (lane == 0) ulist[nused] = j1;
+      ++nused;
+      __syncwarp();
+      const int pj = p[j1];
+      if (pj == 0) break;
+      j0 = j1;
+      r = pj;
+    }
+    // lazy potential moves (assign.hpp:131-138 applied per reached column)
+    for (int t = lane; t < nused; t += 32) {
+      const int j = ulist[t];
+      const int64_t d = Dl - dlt[j];
+      u[p[j]] += d;
+      v[j] -= d;
+    }
+    __syncwarp();
+    if (lane == 0) {  // augment along way[] (assign.hpp:141-145)
+      int jj = j1;
+      do {
+        const int jp = way[jj];
+        p[jj] = p[jp];
+        jj = jp;
+      } while (jj != 0);
+    }
+    __syncwarp();
+    // re-key the consumed prefix of every touched block
+    for (int w = 0; w < n; ++w) {
+      int P = 0;
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+        if ((w >> 5) == b) P = __shfl_sync(0xffffffffu, cur[b], w & 31);
+      if (P == 0) continue;
+      int32_t* base = ord + w * mult;
+      int32_t* sorted = tmp;         // P entries
+      int32_t* merged = tmp + mult;  // mult entries
+      __syncwarp();
+      for (int t = lane; t < P; t += 32) {
+        const int a = base[t];
+        int rank = 0;
+        for (int s2 = 0; s2 < P; ++s2) rank += before(v, base[s2], a) ? 1 : 0;
+        sorted[rank] = a;
+      }
+      __syncwarp();
+      const int Q = mult - P;
+      const int32_t* suf = base + P;
+      for (int t = lane; t < P; t += 32) {
+        const int a = sorted[t];
+        int lo = 0, hi = Q;  // # suffix entries before a
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (before(v, suf[mid], a)) lo = mid + 1;
+          else hi = mid;
+        }
+        merged[t + lo] = a;
+      }
+      for (int t = lane; t < Q; t += 32) {
+        const int b2 = suf[t];
+        int lo = 0, hi = P;  // # prefix entries before b2
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (before(v, sorted[mid], b2)) lo = mid + 1;
+          else hi = mid;
+        }
+        merged[t + lo] = b2;
+      }
+      __syncwarp();
+      for (int t = lane; t < mult; t += 32) base[t] = merged[t];
+      __syncwarp();
+    }
+  }
+  if (lane == 0 && steps_out) *steps_out = steps;
+  return true;
+}
+
+template <int NB>
+__global__ void __launch_bounds__(32)
+    k_hungarian_blocks(const int64_t* __restrict__ S_global, int n, int mult, int k,
+                       int s_in_smem, uint8_t* __restrict__ arena,
+                       const uint32_t* __restrict__ order, int32_t* __restrict__ decision,
+                       const uint32_t* __restrict__ row_ids, uint64_t* __restrict__ col_of_row,
+                       unsigned long long* steps_out, int* flags) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const size_t K1 = static_cast<size_t>(k) + 1;
+  const size_t s_bytes = (static_cast<size_t>(k) * n * sizeof(int64_t) + 15) & ~size_t(15);
+  // [S | arrays] in shared memory, or S in global with the arrays in shared
+  // memory, or both in global memory (L2) when even the arrays do not fit.
+  uint8_t* abase = arena ? arena : smem + (s_in_smem ? s_bytes : 0);
+  int64_t* S_s = reinterpret_cast<int64_t*>(smem);
+  size_t off = 0;
+  BlockArrays A;
+  auto take = [&](size_t bytes) {
+    uint8_t* q = abase + off;
+    off += (bytes + 15) & ~size_t(15);
+    return q;
+  };
+  A.u = reinterpret_cast<int64_t*>(take(K1 * 8));
+  A.v = reinterpret_cast<int64_t*>(take(K1 * 8));
+  A.dlt = reinterpret_cast<int64_t*>(take(K1 * 8));
+  A.p = reinterpret_cast<int32_t*>(take(K1 * 4));
+  A.way = reinterpret_cast<int32_t*>(take(K1 * 4));
+  A.ulist = reinterpret_cast<int32_t*>(take(K1 * 4));
+  A.ord = reinterpret_cast<int32_t*>(take(static_cast<size_t>(k) * 4));
+  A.tmp = reinterpret_cast<int32_t*>(take(static_cast<size_t>(2 * mult) * 4));
+  if (s_in_smem) {
+    const int4* src = reinterpret_cast<const int4*>(S_global);
+    int4* dst = reinterpret_cast<int4*>(S_s);
+    const size_t n16 = static_cast<size_t>(k) * n / 2;  // k*n int64 = k*n/2 int4
+    for (size_t x = threadIdx.x; x < n16; x += 32) dst[x] = src[x];
+    if ((static_cast<size_t>(k) * n) & 1) {
+      if (threadIdx.x == 0) S_s[static_cast<size_t>(k) * n - 1] = S_global[static_cast<size_t>(k) * n - 1];
+    }
+    __syncwarp();
+    A.S = S_s;
+  } else {
+    A.S = S_global;
+  }
+  if (!hungarian_blocks_warp<NB>(A, n, mult, k, steps_out, flags)) return;
+  __syncwarp();
+  // p[j] = block row matched to column j (1-based); column j -> worker (j-1)/mult
+  for (int j = threadIdx.x + 1; j <= k; j += 32) {
+    const int r = A.p[j] - 1;
+    if (col_of_row) col_of_row[r] = static_cast<uint64_t>(j - 1);
+    if (decision) {
+      const uint32_t row = order[r];
+      decision[row_ids ? row_ids[row] : row] = (j - 1) / mult;
+    }
+  }
+}
+
+// ----------------------------------------------------------------- K5 dense
+// The reference loop on an arbitrary k x k matrix: one CTA, columns strided
+// over threads, block-wide argmin with the lowest column winning ties.
+constexpr int kDenseThreads = 1024;
+
+__global__ void __launch_bounds__(kDenseThreads)
+    k_hungarian_dense(const double* __restrict__ values, int k, int64_t cap,
+                      uint8_t* __restrict__ arena, uint64_t* __restrict__ col_of_row,
+                      unsigned long long* steps_out, int* __restrict__ flags) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ int64_t red_v[32];
+  __shared__ int red_j[32];
+  __shared__ int s_j0, s_i0;
+  __shared__ int64_t s_delta;
+  uint8_t* base = arena ? arena : smem;
+  const size_t K1 = static_cast<size_t>(k) + 1;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    uint8_t* q = base + off;
+    off += (bytes + 15) & ~size_t(15);
+    return q;
+  };
+  int64_t* u = reinterpret_cast<int64_t*>(take(K1 * 8));
+  int64_t* v = reinterpret_cast<int64_t*>(take(K1 * 8));
+  int64_t* minv = reinterpret_cast<int64_t*>(take(K1 * 8));
+  int32_t* p = reinterpret_cast<int32_t*>(take(K1 * 4));
+  int32_t* way = reinterpret_cast<int32_t*>(take(K1 * 4));
+  uint8_t* used = take(K1);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int x = tid; x <= k; x += kDenseThreads) {
+    u[x] = 0;
+    v[x] = 0;
+    p[x] = 0;
+    way[x] = 0;
+  }
+  bool bad = false;
+  for (size_t x = tid; x < static_cast<size_t>(k) * k; x += kDenseThreads)
+    bad |= bad_cost(values[x]);
+  if (bad) atomicOr(flags + kFlagBadCost, 1);
+  __syncthreads();
+  unsigned long long steps = 0;
+  for (int i = 1; i <= k; ++i) {
+    for (int x = tid; x <= k; x += kDenseThreads) {
+      minv[x] = kInf;
+      used[x] = 0;
+    }
+    if (tid == 0) {
+      p[0] = i;
+      s_j0 = 0;
+    }
+    __syncthreads();
+    for (;;) {
+      const int j0 = s_j0;
+      if (tid == 0) {
+        used[j0] = 1;
+        s_i0 = p[j0];
+        ++steps;
+      }
+      __syncthreads();
+      const int i0 = s_i0;
+      const int64_t ui0 = u[i0];
+      const double* row = values + static_cast<size_t>(i0 - 1) * k;
+      int64_t best = kInf;
+      int bj = INT_MAX;
+      for (int j = tid + 1; j <= k; j += kDenseThreads) {
+        if (used[j]) continue;
+        const int64_t cur = scale_cost(row[j - 1], cap) - ui0 - v[j];
+        if (cur < minv[j]) {
+          minv[j] = cur;
+          way[j] = j0;
+        }
+        if (minv[j] < best) {
+          best = minv[j];
+          bj = j;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const int64_t ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+        if (ov < best || (ov == best && oj < bj)) {
+          best = ov;
+          bj = oj;
+        }
+      }
+      if (lane == 0) {
+        red_v[warp] = best;
+        red_j[warp] = bj;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        best = lane < kDenseThreads / 32 ? red_v[lane] : kInf;
+        bj = lane < kDenseThreads / 32 ? red_j[lane] : INT_MAX;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const int64_t ov = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+          if (ov < best || (ov == best && oj < bj)) {
+            best = ov;
+            bj = oj;
+          }
+        }
+        if (lane == 0) {
+          s_delta = best;
+          s_j0 = bj;
+        }
+      }
+      __syncthreads();
+      const int64_t delta = s_delta;
+      if (s_j0 == INT_MAX) {  // no unused column: only reachable on corrupt input
+        if (tid == 0) atomicOr(flags + kFlagBadCost, 1);
+        return;
+      }
+      for (int j = tid; j <= k; j += kDenseThreads) {
+        if (used[j]) {
+          u[p[j]] += delta;
+          v[j] -= delta;
+        } else if (minv[j] != kInf) {
+          minv[j] -= delta;
+        }
+      }
+      __syncthreads();
+      if (p[s_j0] == 0) break;
+    }
+    if (tid == 0) {
+      int j0 = s_j0;
+      do {
+        const int jp = way[j0];
+        p[j0] = p[jp];
+        j0 = jp;
+      } while (j0 != 0);
+    }
+    __syncthreads();
+  }
+  for (int j = tid + 1; j <= k; j += kDenseThreads) col_of_row[p[j] - 1] = static_cast<uint64_t>(j - 1);
+  if (tid == 0 && steps_out) *steps_out = steps;
+}
+
+size_t block_arena_bytes(int k, int mult) {
+  const size_t K1 = static_cast<size_t>(k) + 1;
+  auto r = [](size_t b) { return (b + 15) & ~size_t(15); };
+  return 3 * r(K1 * 8) + 3 * r(K1 * 4) + r(static_cast<size_t>(k) * 4) +
+         r(static_cast<size_t>(2 * mult) * 4);
+}
+
+size_t dense_arena_bytes(int k) {
+  const size_t K1 = static_cast<size_t>(k) + 1;
+  auto r = [](size_t b) { return (b + 15) & ~size_t(15); };
+  return 3 * r(K1 * 8) + 2 * r(K1 * 4) + r(K1);
+}
+
+int max_dyn_smem(int device) {
+  int v = 0;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  return v;
+}
+
+}  // namespace
+
+void launch_hungarian_blocks(HungarianScratch& sc, const double* matrix, int n,
+                             const uint32_t* order, int mult, int32_t* decision,
+                             const uint32_t* row_ids, uint64_t* col_of_row, int* flags,
+                             cudaStream_t s, int device) {
+  const int k = n * mult;
+  if (k <= 0) return;
+  const int64_t cap = LLONG_MAX / (8 * static_cast<int64_t>(k + 1));
+  sc.s64.ensure(static_cast<size_t>(k) * n + 1);
+  sc.steps.ensure(1);
+  const uint64_t total = static_cast<uint64_t>(k) * n;
+  k_scale_block<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(matrix, n, order, k,
+                                                                         cap, sc.s64.p, flags);
+  EDX_LAUNCHED();
+  const size_t arena = block_arena_bytes(k, mult);
+  const size_t s_bytes = static_cast<size_t>(k) * n * sizeof(int64_t);
+  const size_t limit = static_cast<size_t>(max_dyn_smem(device));
+  int s_in_smem = 0;
+  size_t smem = 0;
+  uint8_t* garena = nullptr;
+  if (s_bytes + arena <= limit) {
+    s_in_smem = 1;
+    smem = s_bytes + arena;
+  } else if (arena <= limit) {
+    smem = arena;
+  } else {
+    sc.arena.ensure(arena);
+    garena = sc.arena.p;
+  }
+  auto launch = [&](auto kern) {
+    if (smem > 48 * 1024)
+      EDX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+    kern<<<1, 32, smem, s>>>(sc.s64.p, n, mult, k, s_in_smem, garena, order, decision, row_ids,
+                             col_of_row, sc.steps.p, flags);
+  };
+  if (n <= 32) launch(k_hungarian_blocks<1>);
+  else launch(k_hungarian_blocks<2>);
+  EDX_LAUNCHED();
+}
+
+void launch_hungarian_dense(HungarianScratch& sc, const double* values, uint64_t k,
+                            uint64_t* col_of_row, int* flags, cudaStream_t s, int device) {
+  const int64_t cap = LLONG_MAX / (8 * static_cast<int64_t>(k + 1));
+  sc.steps.ensure(1);
+  const size_t arena = dense_arena_bytes(static_cast<int>(k));
+  const size_t limit = static_cast<size_t>(max_dyn_smem(device)) - 1024;  // static smem
+  size_t smem = 0;
+  uint8_t* garena = nullptr;
+  if (arena <= limit) {
+    smem = arena;
+  } else {
+    sc.arena.ensure(arena);
+    garena = sc.arena.p;
+  }
+  if (smem > 48 * 1024)
+    EDX_CUDA(cudaFuncSetAttribute(k_hungarian_dense, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+  k_hungarian_dense<<<1, kDenseThreads, smem, s>>>(values, static_cast<int>(k), cap, garena,
+                                                   col_of_row, sc.steps.p, flags);
+  EDX_LAUNCHED();
+}
+
+unsigned long long last_hungarian_steps(HungarianScratch& sc, cudaStream_t s) {
+  if (!sc.steps.p) return 0;
+  unsigned long long h = 0;
+  EDX_CUDA(cudaMemcpyAsync(&h, sc.steps.p, sizeof h, cudaMemcpyDeviceToHost, s));
+  EDX_CUDA(cudaStreamSynchronize(s));
+  return h;
+}
+
+}  // namespace edx

@@ -1,0 +1,725 @@
+// K7: SimState::step on device (sim.hpp:87-218) over WorkerCache semantics
+// (cache.hpp:102-201).
+//
+// The reference walks the batch sample by sample, then each worker's needs
+// one by one through a std::set of victim keys.  The device version rests on
+// four properties of that code (re-derived in DESIGN.md §4):
+//  1. Phases 1 and 3 mutate only the state of the id at hand (sim.hpp:123-153,
+//     194-204): they are id-parallel and unordered_map order cannot matter.
+//  2. Phase 2 of worker j flips only worker j's bits and cache (sim.hpp:157-190):
+//     workers are independent.
+//  3. Within worker j's phase 2, entries that are not needed this iteration
+//     (not pinned) are never touched, so their VictimKeys are frozen after
+//     phase 1; every eviction takes the least non-pinned key.  The victims are
+//     therefore exactly the E_j least keys, E_j = max(0, inserts - free slots),
+//     and the t-th evicting insert (in need order) removes the t-th least.
+//  4. at_current_mark_ changes by +1 per touch of an entry whose mark is not
+//     current, +1 per insert and -1 per eviction of a current-mark entry; the
+//     epoch advance (cache.hpp:187-192) fires at the first evicting insert where
+//     that counter equals the capacity.  A prefix scan over need order finds
+//     it; it can fire at most once per step (a second firing means every entry
+//     is pinned, which the reference reports as a logic_error).
+// The rest is bookkeeping: need lists in first-occurrence order come from a
+// stable sort of (worker, position) keys, counts are integer atomics
+// (order-free), and the realised cost is summed on the host in worker order
+// (sim.hpp:208-216).
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <climits>
+#include <cstring>
+
+#include "engine.h"
+#include "step.h"
+
+namespace edx {
+
+namespace {
+
+constexpr int kT = 256;
+inline unsigned grid_for(uint64_t n, int t = kT) {
+  return static_cast<unsigned>(std::max<uint64_t>(1, (n + t - 1) / t));
+}
+
+// counters layout (unsigned long long)
+//   [0,n) miss_pull_w  [n,2n) update_push_w  [2n,3n) evict_push_w  [3n] hits
+//   [3n+1] unique ids U   [3n+2] need items N
+// per-worker scalars (uint32, kWS per worker)
+enum WS : int {
+  kWsNeeds = 0,    // need items of the worker
+  kWsInserts = 1,  // non-resident needs
+  kWsFree = 2,     // free slots at phase-2 start
+  kWsEvict = 3,    // evictions E_j
+  kWsCand = 4,     // non-pinned candidates
+  kWsAdvance = 5,  // need item (worker-local) of the epoch advance, UINT_MAX = none
+  kWsSize0 = 6,
+  kWsNeedOff = 7,  // start of the worker's need items
+  kWsCandOff = 8,  // start of the worker's sorted candidates
+  kWsInsBase = 9,  // exclusive insert-scan value at the worker's first item
+  kWsConBase = 10, // exclusive contribution-scan value at the worker's first item
+  kWS = 11
+};
+
+__global__ void k_occ_sample(const uint64_t* __restrict__ offsets, uint64_t rows,
+                             uint32_t* __restrict__ occ_sample) {
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i >= rows) return;
+  for (uint64_t p = offsets[i]; p < offsets[i + 1]; ++p) occ_sample[p] = static_cast<uint32_t>(i);
+}
+
+__global__ void k_first_pos(const uint32_t* __restrict__ ids, uint64_t T,
+                            int32_t* __restrict__ first_pos) {
+  const uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (p >= T) return;
+  atomicMin(first_pos + ids[p], static_cast<int32_t>(p));
+}
+
+__global__ void k_unique_flag(const uint32_t* __restrict__ ids, uint64_t T,
+                              const int32_t* __restrict__ first_pos, uint32_t* __restrict__ flag) {
+  const uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (p > T) return;
+  flag[p] = (p < T && first_pos[ids[p]] == static_cast<int32_t>(p)) ? 1u : 0u;
+}
+
+__global__ void k_unique_scatter(const uint32_t* __restrict__ ids, uint64_t T,
+                                 const int32_t* __restrict__ first_pos,
+                                 const uint32_t* __restrict__ uidx, uint32_t* __restrict__ uniq,
+                                 unsigned long long* counters, int n) {
+  const uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (p == T) counters[3 * n + 1] = uidx[T];
+  if (p >= T) return;
+  if (first_pos[ids[p]] == static_cast<int32_t>(p)) uniq[uidx[p]] = ids[p];
+}
+
+// needs (sim.hpp:103-117): per (worker, id) first position and count, and
+// the trainer mask of every id.
+__global__ void k_needs(const uint32_t* __restrict__ ids, uint64_t T,
+                        const uint32_t* __restrict__ occ_sample,
+                        const int32_t* __restrict__ decision, const int32_t* __restrict__ first_pos,
+                        const uint32_t* __restrict__ uidx, uint64_t ucap,
+                        int32_t* __restrict__ need_first, uint32_t* __restrict__ need_cnt,
+                        unsigned long long* __restrict__ umask) {
+  const uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (p >= T) return;
+  const int j = decision[occ_sample[p]];
+  const uint32_t u = uidx[first_pos[ids[p]]];
+  const uint64_t x = static_cast<uint64_t>(j) * ucap + u;
+  atomicMin(need_first + x, static_cast<int32_t>(p));
+  atomicAdd(need_cnt + x, 1u);
+  atomicOr(umask + u, 1ULL << j);
+}
+
+// first occurrence of (worker, id) -> sortable key (worker << 32 | position)
+__global__ void k_need_keys(const uint32_t* __restrict__ ids, uint64_t T,
+                            const uint32_t* __restrict__ occ_sample,
+                            const int32_t* __restrict__ decision,
+                            const int32_t* __restrict__ first_pos, const uint32_t* __restrict__ uidx,
+                            uint64_t ucap, const int32_t* __restrict__ need_first,
+                            uint64_t* __restrict__ keys, uint32_t* __restrict__ ws) {
+  const uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (p >= T) return;
+  const int j = decision[occ_sample[p]];
+  const uint32_t u = uidx[first_pos[ids[p]]];
+  if (need_first[static_cast<uint64_t>(j) * ucap + u] == static_cast<int32_t>(p)) {
+    keys[p] = (static_cast<uint64_t>(j) << 32) | p;
+    atomicAdd(ws + j * kWS + kWsNeeds, 1u);
+  } else {
+    keys[p] = ~0ULL;
+  }
+}
+
+// Phase 1: on-demand update push (sim.hpp:119-153).  set_version(false) on
+// stale copies is the `latest` mask update itself (version == latest bit).
+__global__ void k_phase1(const uint32_t* __restrict__ uniq,
+                         const unsigned long long* __restrict__ umask,
+                         const unsigned long long* counters_ro, int n,
+                         ulonglong2* __restrict__ ol, unsigned long long* counters) {
+  __shared__ unsigned int push[kMaxWorkers];
+  if (threadIdx.x < kMaxWorkers) push[threadIdx.x] = 0;
+  __syncthreads();
+  const uint64_t U = counters_ro[3 * n + 1];
+  const uint64_t u = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (u < U) {
+    const uint32_t id = uniq[u];
+    ulonglong2 st = ol[id];
+    if (st.x != 0) {
+      const unsigned long long need = umask[u];
+      unsigned long long pushers = 0, own = st.x;
+      while (own) {
+        const int w = __ffsll(static_cast<long long>(own)) - 1;
+        own &= own - 1;
+        if (need & ~(1ULL << w)) pushers |= 1ULL << w;
+      }
+      if (pushers) {
+        for (unsigned long long it = pushers; it; it &= it - 1)
+          atomicAdd(&push[__ffsll(static_cast<long long>(it)) - 1], 1u);
+        st.x &= ~pushers;
+        if (st.x != 0) st.y = st.x;
+        ol[id] = st;
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < n && push[threadIdx.x])
+    atomicAdd(counters + n + threadIdx.x, static_cast<unsigned long long>(push[threadIdx.x]));
+}
+
+// per-worker need CSR offsets (need items are sorted by worker, then position)
+__global__ void k_need_offsets(int n, uint32_t* __restrict__ ws, const uint32_t* __restrict__ size,
+                               uint64_t capacity, unsigned long long* counters) {
+  if (threadIdx.x != 0) return;
+  uint32_t run = 0;
+  for (int j = 0; j < n; ++j) {
+    ws[j * kWS + kWsNeedOff] = run;
+    run += ws[j * kWS + kWsNeeds];
+    ws[j * kWS + kWsSize0] = size[j];
+    ws[j * kWS + kWsFree] = static_cast<uint32_t>(capacity - size[j]);
+    ws[j * kWS + kWsAdvance] = UINT_MAX;
+  }
+  counters[3 * n + 2] = run;
+}
+
+__device__ __forceinline__ int item_worker(uint64_t key) { return static_cast<int>(key >> 32); }
+__device__ __forceinline__ uint32_t item_pos(uint64_t key) { return static_cast<uint32_t>(key); }
+
+// Phase 2 classification (sim.hpp:168-181): hit / refresh / insert, hit and
+// miss-pull tallies, and the pre-advance at_current_mark contribution of
+// touches of existing entries (cache.hpp:116).
+__global__ void k_classify(const uint64_t* __restrict__ items,
+                           const unsigned long long* counters_ro, int n,
+                           const uint32_t* __restrict__ ids, const int32_t* __restrict__ first_pos,
+                           const uint32_t* __restrict__ uidx, uint64_t ucap,
+                           const uint32_t* __restrict__ need_cnt, const ulonglong2* __restrict__ ol,
+                           const unsigned long long* __restrict__ res, uint64_t id_space,
+                           const int32_t* __restrict__ slot_of, uint64_t capacity,
+                           const uint32_t* __restrict__ smark, const uint32_t* __restrict__ cur_mark,
+                           uint8_t* __restrict__ type, uint32_t* __restrict__ ins_flag,
+                           int32_t* __restrict__ contrib, unsigned long long* counters) {
+  __shared__ unsigned int miss[kMaxWorkers];
+  __shared__ unsigned long long hits;
+  if (threadIdx.x < kMaxWorkers) miss[threadIdx.x] = 0;
+  if (threadIdx.x == 0) hits = 0;
+  __syncthreads();
+  const uint64_t N = counters_ro[3 * n + 2];
+  const uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (q < N) {
+    const uint64_t key = items[q];
+    const int j = item_worker(key);
+    const uint32_t p = item_pos(key);
+    const uint32_t id = ids[p];
+    const unsigned long long bit = 1ULL << j;
+    const ulonglong2 st = ol[id];
+    uint8_t t;
+    int32_t c = 1;
+    if (st.y & bit) {
+      t = 0;
+      const uint32_t u = uidx[first_pos[id]];
+      atomicAdd(&hits, static_cast<unsigned long long>(need_cnt[static_cast<uint64_t>(j) * ucap + u]));
+    } else {
+      t = (res[id] & bit) ? 1 : 2;
+      atomicAdd(&miss[j], 1u);
+    }
+    if (t != 2) {
+      const int32_t s = slot_of[static_cast<uint64_t>(j) * id_space + id];
+      c = smark[static_cast<uint64_t>(j) * capacity + s] != cur_mark[j] ? 1 : 0;
+    }
+    type[q] = t;
+    ins_flag[q] = t == 2 ? 1u : 0u;
+    contrib[q] = c;
+  } else if (q == N) {
+    ins_flag[q] = 0;
+    contrib[q] = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x < n && miss[threadIdx.x])
+    atomicAdd(counters + threadIdx.x, static_cast<unsigned long long>(miss[threadIdx.x]));
+  if (threadIdx.x == 0 && hits) atomicAdd(counters + 3 * n, hits);
+}
+
+// inserts and evictions per worker (evict_for, cache.hpp:152-170)
+__global__ void k_worker_inserts(int n, const uint32_t* __restrict__ ins_scan,
+                                 uint32_t* __restrict__ ws, int* __restrict__ flags) {
+  const int j = threadIdx.x;
+  if (j >= n) return;
+  uint32_t* w = ws + j * kWS;
+  const uint32_t b = w[kWsNeedOff], e = b + w[kWsNeeds];
+  const uint32_t ins = ins_scan[e] - ins_scan[b];
+  w[kWsInserts] = ins;
+  w[kWsInsBase] = ins_scan[b];
+  w[kWsEvict] = ins > w[kWsFree] ? ins - w[kWsFree] : 0;
+  w[kWsCand] = 0;
+  (void)flags;
+}
+
+// --- victim candidates: non-pinned entries of evicting workers -----------
+// ranges[0..7] = {mark lo, mark hi, freq lo, freq hi, last lo, last hi, id lo, id hi}
+__device__ __forceinline__ bool pinned_by(int j, uint32_t id, const int32_t* first_pos,
+                                          const uint32_t* uidx, uint64_t ucap,
+                                          const int32_t* need_first) {
+  const int32_t fp = first_pos[id];
+  if (fp == INT_MAX) return false;
+  return need_first[static_cast<uint64_t>(j) * ucap + uidx[fp]] != INT_MAX;
+}
+
+__global__ void k_cand_ranges(const int32_t* __restrict__ wlist, int nw, uint64_t capacity,
+                              const uint32_t* __restrict__ ws, const uint32_t* __restrict__ sid,
+                              const uint32_t* __restrict__ smark, const uint32_t* __restrict__ sfreq,
+                              const uint32_t* __restrict__ slast,
+                              const int32_t* __restrict__ first_pos, const uint32_t* __restrict__ uidx,
+                              uint64_t ucap, const int32_t* __restrict__ need_first,
+                              uint32_t* __restrict__ ranges) {
+  const uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (x >= static_cast<uint64_t>(nw) * capacity) return;
+  const int jl = static_cast<int>(x / capacity);
+  const uint64_t s = x - static_cast<uint64_t>(jl) * capacity;
+  const int j = wlist[jl];
+  if (s >= ws[j * kWS + kWsSize0]) return;
+  const uint64_t g = static_cast<uint64_t>(j) * capacity + s;
+  const uint32_t id = sid[g];
+  if (pinned_by(j, id, first_pos, uidx, ucap, need_first)) return;
+  atomicMin(ranges + 0, smark[g]);
+  atomicMax(ranges + 1, smark[g]);
+  atomicMin(ranges + 2, sfreq[g]);
+  atomicMax(ranges + 3, sfreq[g]);
+  atomicMin(ranges + 4, slast[g]);
+  atomicMax(ranges + 5, slast[g]);
+  atomicMin(ranges + 6, id);
+  atomicMax(ranges + 7, id);
+}
+
+__device__ __forceinline__ int width_of(uint32_t lo, uint32_t hi) {
+  return hi > lo ? 32 - __clz(hi - lo) : 0;
+}
+
+// VictimKey (cache.hpp:47-58) = (version, mark, frequency, last_access, id),
+// packed order-preservingly into 58 bits below a 6-bit worker field.
+__global__ void k_cand_pack(const int32_t* __restrict__ wlist, int nw, uint64_t capacity,
+                            uint32_t* __restrict__ ws, const uint32_t* __restrict__ sid,
+                            const uint32_t* __restrict__ smark, const uint32_t* __restrict__ sfreq,
+                            const uint32_t* __restrict__ slast, const ulonglong2* __restrict__ ol,
+                            const int32_t* __restrict__ first_pos, const uint32_t* __restrict__ uidx,
+                            uint64_t ucap, const int32_t* __restrict__ need_first,
+                            const uint32_t* __restrict__ ranges, uint64_t* __restrict__ keys,
+                            uint32_t* __restrict__ slots, int* __restrict__ flags) {
+  const uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (x >= static_cast<uint64_t>(nw) * capacity) return;
+  const int jl = static_cast<int>(x / capacity);
+  const uint64_t s = x - static_cast<uint64_t>(jl) * capacity;
+  const int j = wlist[jl];
+  uint64_t key = ~0ULL;
+  if (s < ws[j * kWS + kWsSize0]) {
+    const uint64_t g = static_cast<uint64_t>(j) * capacity + s;
+    const uint32_t id = sid[g];
+    if (!pinned_by(j, id, first_pos, uidx, ucap, need_first)) {
+      const int wm = width_of(ranges[0], ranges[1]), wf = width_of(ranges[2], ranges[3]);
+      const int wl = width_of(ranges[4], ranges[5]), wi = width_of(ranges[6], ranges[7]);
+      if (1 + wm + wf + wl + wi > 57) atomicOr(flags + kFlagKeyRange, 1);
+      const uint64_t ver = (ol[id].y >> j) & 1ULL;
+      uint64_t k = ver;
+      k = (k << wm) | (smark[g] - ranges[0]);
+      k = (k << wf) | (sfreq[g] - ranges[2]);
+      k = (k << wl) | (slast[g] - ranges[4]);
+      k = (k << wi) | (id - ranges[6]);
+      key = (static_cast<uint64_t>(jl) << 58) | k;
+      atomicAdd(ws + j * kWS + kWsCand, 1u);
+    }
+  }
+  keys[x] = key;
+  slots[x] = static_cast<uint32_t>(s);
+}
+
+__global__ void k_cand_offsets(const int32_t* __restrict__ wlist, int nw, uint32_t* __restrict__ ws,
+                               int* __restrict__ flags) {
+  if (threadIdx.x != 0) return;
+  uint32_t run = 0;
+  for (int jl = 0; jl < nw; ++jl) {
+    uint32_t* w = ws + wlist[jl] * kWS;
+    w[kWsCandOff] = run;
+    run += w[kWsCand];
+    if (w[kWsCand] < w[kWsEvict]) atomicOr(flags + kFlagPinned, 1);
+  }
+}
+
+// evicting insert contribution: +1 for the insert, -1 if its victim carries
+// the current mark (cache.hpp:111,175), evaluated before any advance.
+__global__ void k_evict_contrib(const uint64_t* __restrict__ items,
+                                const unsigned long long* counters_ro, int n,
+                                const uint8_t* __restrict__ type, const uint32_t* __restrict__ ins_scan,
+                                const uint32_t* __restrict__ ws, const uint32_t* __restrict__ cand_slot,
+                                const uint32_t* __restrict__ smark, uint64_t capacity,
+                                const uint32_t* __restrict__ cur_mark, int32_t* __restrict__ contrib) {
+  const uint64_t N = counters_ro[3 * n + 2];
+  const uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (q >= N || type[q] != 2) return;
+  const int j = item_worker(items[q]);
+  const uint32_t* w = ws + j * kWS;
+  const uint32_t e = ins_scan[q] - w[kWsInsBase];
+  if (e < w[kWsFree]) return;
+  const uint32_t t = e - w[kWsFree];
+  if (t >= w[kWsCand]) return;  // reported through kFlagPinned
+  const uint32_t vs = cand_slot[w[kWsCandOff] + t];
+  contrib[q] = smark[static_cast<uint64_t>(j) * capacity + vs] == cur_mark[j] ? 0 : 1;
+}
+
+// maybe_advance_mark (cache.hpp:187-192) at the first evicting insert whose
+// running at_current_mark equals the capacity.
+__global__ void k_find_advance(const uint64_t* __restrict__ items,
+                               const unsigned long long* counters_ro, int n,
+                               const uint8_t* __restrict__ type, const uint32_t* __restrict__ ins_scan,
+                               const int32_t* __restrict__ con_scan, uint32_t* __restrict__ ws,
+                               const unsigned long long* __restrict__ at_cur, uint64_t capacity) {
+  const uint64_t N = counters_ro[3 * n + 2];
+  const uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (q >= N || type[q] != 2) return;
+  const int j = item_worker(items[q]);
+  uint32_t* w = ws + j * kWS;
+  const uint32_t e = ins_scan[q] - w[kWsInsBase];
+  if (e < w[kWsFree]) return;
+  const uint64_t before =
+      at_cur[j] + static_cast<uint64_t>(con_scan[q] - con_scan[w[kWsNeedOff]]);
+  if (before == capacity) atomicMin(w + kWsAdvance, static_cast<uint32_t>(q - w[kWsNeedOff]));
+}
+
+// evictions: clear the victim's bits of worker j (sim.hpp:177-184)
+__global__ void k_evict(const int32_t* __restrict__ wlist, int nw, const uint32_t* __restrict__ ws,
+                        const uint32_t* __restrict__ cand_slot, const uint32_t* __restrict__ sid,
+                        uint64_t capacity, uint64_t id_space, ulonglong2* __restrict__ ol,
+                        unsigned long long* __restrict__ res, int32_t* __restrict__ slot_of,
+                        uint32_t* __restrict__ victim_id, unsigned long long* counters,
+                        int n) {
+  const int jl = blockIdx.y;
+  if (jl >= nw) return;
+  const int j = wlist[jl];
+  const uint32_t* w = ws + j * kWS;
+  const uint32_t E = min(w[kWsEvict], w[kWsCand]);
+  unsigned int pushes = 0;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < E; t += gridDim.x * blockDim.x) {
+    const uint32_t vs = cand_slot[w[kWsCandOff] + t];
+    const uint64_t g = static_cast<uint64_t>(j) * capacity + vs;
+    const uint32_t id = sid[g];
+    victim_id[w[kWsCandOff] + t] = id;
+    const unsigned long long bit = 1ULL << j;
+    unsigned long long* olw = reinterpret_cast<unsigned long long*>(ol + id);
+    const unsigned long long old_owners = atomicAnd(olw, ~bit);
+    atomicAnd(olw + 1, ~bit);
+    atomicAnd(res + id, ~bit);
+    if (old_owners & bit) ++pushes;
+    slot_of[static_cast<uint64_t>(j) * id_space + id] = -1;
+  }
+  for (int o = 16; o > 0; o >>= 1) pushes += __shfl_xor_sync(0xffffffffu, pushes, o);
+  if ((threadIdx.x & 31) == 0 && pushes) atomicAdd(counters + 2 * n + j, static_cast<unsigned long long>(pushes));
+}
+
+// touches and inserts (WorkerCache::touch, cache.hpp:102-122; sim.hpp:172,186-188)
+__global__ void k_apply(const uint64_t* __restrict__ items,
+                        const unsigned long long* counters_ro, int n,
+                        const uint32_t* __restrict__ ids, const uint8_t* __restrict__ type,
+                        const uint32_t* __restrict__ ins_scan, const uint32_t* __restrict__ ws,
+                        const uint32_t* __restrict__ cand_slot, uint64_t capacity,
+                        uint64_t id_space, const uint32_t* __restrict__ cur_mark, uint32_t clock,
+                        ulonglong2* __restrict__ ol, unsigned long long* __restrict__ res,
+                        int32_t* __restrict__ slot_of, uint32_t* __restrict__ sid,
+                        uint32_t* __restrict__ smark, uint32_t* __restrict__ sfreq,
+                        uint32_t* __restrict__ slast) {
+  const uint64_t N = counters_ro[3 * n + 2];
+  const uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (q >= N) return;
+  const int j = item_worker(items[q]);
+  const uint32_t id = ids[item_pos(items[q])];
+  const uint32_t* w = ws + j * kWS;
+  const uint32_t local = static_cast<uint32_t>(q) - w[kWsNeedOff];
+  const uint32_t mark = cur_mark[j] + (local >= w[kWsAdvance] ? 1u : 0u);
+  const unsigned long long bit = 1ULL << j;
+  const uint8_t t = type[q];
+  if (t != 2) {
+    const uint64_t g = static_cast<uint64_t>(j) * capacity +
+                       slot_of[static_cast<uint64_t>(j) * id_space + id];
+    smark[g] = mark;
+    sfreq[g] += 1;
+    slast[g] = clock;
+    if (t == 1) atomicOr(reinterpret_cast<unsigned long long*>(ol + id) + 1, bit);
+    return;
+  }
+  const uint32_t e = ins_scan[q] - w[kWsInsBase];
+  uint32_t slot;
+  if (e < w[kWsFree]) slot = w[kWsSize0] + e;
+  else slot = cand_slot[w[kWsCandOff] + (e - w[kWsFree])];
+  const uint64_t g = static_cast<uint64_t>(j) * capacity + slot;
+  slot_of[static_cast<uint64_t>(j) * id_space + id] = static_cast<int32_t>(slot);
+  sid[g] = id;
+  smark[g] = mark;
+  sfreq[g] = 1;
+  slast[g] = clock;
+  atomicOr(reinterpret_cast<unsigned long long*>(ol + id) + 1, bit);
+  atomicOr(res + id, bit);
+}
+
+__global__ void k_worker_finalize(int n, const uint32_t* __restrict__ ws,
+                                  const int32_t* __restrict__ con_scan, uint32_t* __restrict__ size,
+                                  uint32_t* __restrict__ cur_mark,
+                                  unsigned long long* __restrict__ at_cur) {
+  const int j = threadIdx.x;
+  if (j >= n) return;
+  const uint32_t* w = ws + j * kWS;
+  const uint32_t E = min(w[kWsEvict], w[kWsCand]);
+  size[j] = w[kWsSize0] + w[kWsInserts] - E;
+  const uint32_t b = w[kWsNeedOff], cnt = w[kWsNeeds];
+  if (w[kWsAdvance] != UINT_MAX) {
+    cur_mark[j] += 1;
+    at_cur[j] = cnt - w[kWsAdvance];
+  } else {
+    at_cur[j] += static_cast<unsigned long long>(con_scan[b + cnt] - con_scan[b]);
+  }
+}
+
+// Phase 3: ownership hand-over (sim.hpp:192-204)
+__global__ void k_phase3(const uint32_t* __restrict__ uniq,
+                         const unsigned long long* __restrict__ umask,
+                         const unsigned long long* counters_ro, int n,
+                         ulonglong2* __restrict__ ol) {
+  const uint64_t U = counters_ro[3 * n + 1];
+  const uint64_t u = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (u >= U) return;
+  const unsigned long long m = umask[u];
+  ol[uniq[u]] = make_ulonglong2(m, m);
+}
+
+__global__ void k_reset(const uint32_t* __restrict__ uniq,
+                        const unsigned long long* counters_ro, int n,
+                        const uint64_t* __restrict__ items, const uint32_t* __restrict__ ids,
+                        const uint32_t* __restrict__ uidx, uint64_t ucap,
+                        int32_t* __restrict__ first_pos, unsigned long long* __restrict__ umask,
+                        int32_t* __restrict__ need_first, uint32_t* __restrict__ need_cnt) {
+  const uint64_t U = counters_ro[3 * n + 1], N = counters_ro[3 * n + 2];
+  const uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (x < N) {
+    const uint64_t key = items[x];
+    const uint32_t p = item_pos(key);
+    // uidx at a worker's first occurrence of the id is the id's unique index
+    // only when that is also the id's first occurrence; go through first_pos.
+    const int j = item_worker(key);
+    const uint32_t u = uidx[first_pos[ids[p]]];
+    need_first[static_cast<uint64_t>(j) * ucap + u] = INT_MAX;
+    need_cnt[static_cast<uint64_t>(j) * ucap + u] = 0;
+  }
+  (void)U;
+  (void)uniq;
+  (void)umask;
+}
+
+__global__ void k_reset_unique(const uint32_t* __restrict__ uniq,
+                               const unsigned long long* counters_ro, int n,
+                               int32_t* __restrict__ first_pos,
+                               unsigned long long* __restrict__ umask) {
+  const uint64_t U = counters_ro[3 * n + 1];
+  const uint64_t u = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (u >= U) return;
+  first_pos[uniq[u]] = INT_MAX;
+  umask[u] = 0;
+}
+
+__global__ void k_fill_i32(int32_t* p, uint64_t n, int32_t v) {
+  const uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (x < n) p[x] = v;
+}
+
+}  // namespace
+
+void step_init_state(edx_engine* e) {
+  const uint64_t n = static_cast<uint64_t>(e->n);
+  auto& c = e->cache;
+  c.slot_of.ensure(n * e->id_space);
+  c.sid.ensure(n * e->capacity);
+  c.smark.ensure(n * e->capacity);
+  c.sfreq.ensure(n * e->capacity);
+  c.slast.ensure(n * e->capacity);
+  c.size.ensure(n);
+  c.cur_mark.ensure(n);
+  c.at_cur.ensure(n);
+  const uint64_t cells = n * e->id_space;
+  k_fill_i32<<<grid_for(cells), kT, 0, e->stream>>>(c.slot_of.p, cells, -1);
+  EDX_LAUNCHED();
+  EDX_CUDA(cudaMemsetAsync(c.size.p, 0, n * sizeof(uint32_t), e->stream));
+  std::vector<uint32_t> ones(n, 1u);  // current_mark_ starts at 1 (cache.hpp:236)
+  EDX_CUDA(cudaMemcpyAsync(c.cur_mark.p, ones.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                           e->stream));
+  EDX_CUDA(cudaMemsetAsync(c.at_cur.p, 0, n * sizeof(unsigned long long), e->stream));
+
+  auto& s = e->step;
+  const uint64_t T = e->max_ids;
+  s.occ_sample.ensure(T);
+  s.first_pos.ensure(e->id_space);
+  k_fill_i32<<<grid_for(e->id_space), kT, 0, e->stream>>>(s.first_pos.p, e->id_space, INT_MAX);
+  EDX_LAUNCHED();
+  s.uidx_of_pos.ensure(T + 1);
+  s.uniq.ensure(T);
+  s.umask.ensure(T);
+  EDX_CUDA(cudaMemsetAsync(s.umask.p, 0, T * sizeof(unsigned long long), e->stream));
+  s.need_first.ensure(n * T);
+  k_fill_i32<<<grid_for(n * T), kT, 0, e->stream>>>(s.need_first.p, n * T, INT_MAX);
+  EDX_LAUNCHED();
+  s.need_cnt.ensure(n * T);
+  EDX_CUDA(cudaMemsetAsync(s.need_cnt.p, 0, n * T * sizeof(uint32_t), e->stream));
+  s.flag_scan.ensure(T + 1);
+  s.need_key.ensure(T);
+  s.need_key_sorted.ensure(T);
+  s.need_type.ensure(T + 1);
+  s.need_contrib.ensure(T + 1);
+  s.ins_rank.ensure(T + 1);
+  s.counters.ensure(3 * n + 4);
+  s.wscalars.ensure(n * kWS);
+  s.ranges.ensure(8);
+}
+
+namespace {
+
+template <class F>
+void cub_call(edx_engine* e, F&& f) {
+  size_t bytes = 0;
+  EDX_CUDA(f(static_cast<void*>(nullptr), bytes));
+  e->step.temp.ensure(bytes);
+  bytes = e->step.temp.n;
+  EDX_CUDA(f(static_cast<void*>(e->step.temp.p), bytes));
+}
+
+}  // namespace
+
+void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
+  cudaStream_t st = e->stream;
+  auto& s = e->step;
+  auto& c = e->cache;
+  const int n = e->n;
+  const uint64_t T = e->total_ids, R = e->rows, ucap = e->max_ids;
+  const uint32_t clock32 = static_cast<uint32_t>(e->clock);
+  int launches = 0;
+
+  EDX_CUDA(cudaMemsetAsync(s.counters.p, 0, (3 * n + 4) * sizeof(unsigned long long), st));
+  EDX_CUDA(cudaMemsetAsync(s.wscalars.p, 0, n * kWS * sizeof(uint32_t), st));
+
+  k_occ_sample<<<grid_for(R), kT, 0, st>>>(e->cur_offsets, R, s.occ_sample.p);
+  k_first_pos<<<grid_for(T), kT, 0, st>>>(e->cur_ids, T, s.first_pos.p);
+  k_unique_flag<<<grid_for(T + 1), kT, 0, st>>>(e->cur_ids, T, s.first_pos.p, s.flag_scan.p);
+  EDX_LAUNCHED();
+  launches += 3;
+  cub_call(e, [&](void* tmp, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(tmp, b, s.flag_scan.p, s.uidx_of_pos.p,
+                                         static_cast<int>(T + 1), st);
+  });
+  k_unique_scatter<<<grid_for(T + 1), kT, 0, st>>>(e->cur_ids, T, s.first_pos.p, s.uidx_of_pos.p,
+                                                   s.uniq.p, s.counters.p, n);
+  k_needs<<<grid_for(T), kT, 0, st>>>(e->cur_ids, T, s.occ_sample.p, d_decision, s.first_pos.p,
+                                      s.uidx_of_pos.p, ucap, s.need_first.p, s.need_cnt.p,
+                                      s.umask.p);
+  k_need_keys<<<grid_for(T), kT, 0, st>>>(e->cur_ids, T, s.occ_sample.p, d_decision, s.first_pos.p,
+                                          s.uidx_of_pos.p, ucap, s.need_first.p, s.need_key.p,
+                                          s.wscalars.p);
+  EDX_LAUNCHED();
+  launches += 5;
+  int wbits = 1;
+  while ((1 << wbits) < n) ++wbits;
+  cub_call(e, [&](void* tmp, size_t& b) {
+    return cub::DeviceRadixSort::SortKeys(tmp, b, s.need_key.p, s.need_key_sorted.p,
+                                          static_cast<int>(T), 0, 32 + wbits + 1, st);
+  });
+  launches += 4;
+  k_phase1<<<grid_for(T), kT, 0, st>>>(s.uniq.p, s.umask.p, s.counters.p, n, e->ol.p, s.counters.p);
+  k_need_offsets<<<1, 32, 0, st>>>(n, s.wscalars.p, c.size.p, e->capacity, s.counters.p);
+  k_classify<<<grid_for(T + 1), kT, 0, st>>>(
+      s.need_key_sorted.p, s.counters.p, n, e->cur_ids, s.first_pos.p, s.uidx_of_pos.p, ucap,
+      s.need_cnt.p, e->ol.p, e->res.p, e->id_space, c.slot_of.p, e->capacity, c.smark.p,
+      c.cur_mark.p, s.need_type.p, s.flag_scan.p, s.need_contrib.p, s.counters.p);
+  EDX_LAUNCHED();
+  launches += 3;
+  // insert ordinals: exclusive scan over the (worker-grouped) need items
+  cub_call(e, [&](void* tmp, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(tmp, b, s.flag_scan.p, s.ins_rank.p,
+                                         static_cast<int>(T + 1), st);
+  });
+  k_worker_inserts<<<1, 64, 0, st>>>(n, s.ins_rank.p, s.wscalars.p, e->flags.p);
+  EDX_LAUNCHED();
+  launches += 2;
+
+  // The host needs E_j to size the victim selection (the only mid-step sync).
+  std::vector<uint32_t> ws(static_cast<size_t>(n) * kWS);
+  EDX_CUDA(cudaMemcpyAsync(ws.data(), s.wscalars.p, ws.size() * sizeof(uint32_t),
+                           cudaMemcpyDeviceToHost, st));
+  EDX_CUDA(cudaStreamSynchronize(st));
+  std::vector<int32_t> wl;
+  for (int j = 0; j < n; ++j)
+    if (ws[j * kWS + kWsEvict] > 0) wl.push_back(j);
+  const int nw = static_cast<int>(wl.size());
+
+  int32_t* d_wlist = nullptr;
+  if (nw > 0) {
+    const uint64_t cand = static_cast<uint64_t>(nw) * e->capacity;
+    s.cand_key.ensure(cand);
+    s.cand_key_sorted.ensure(cand);
+    s.cand_slot.ensure(cand);
+    s.cand_slot_sorted.ensure(cand);
+    s.cand_count.ensure(cand);  // reused as the victim-id list
+    s.cand_off.ensure(64);
+    d_wlist = reinterpret_cast<int32_t*>(s.cand_off.p);
+    EDX_CUDA(cudaMemcpyAsync(d_wlist, wl.data(), nw * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    const uint32_t init[8] = {UINT_MAX, 0, UINT_MAX, 0, UINT_MAX, 0, UINT_MAX, 0};
+    EDX_CUDA(cudaMemcpyAsync(s.ranges.p, init, sizeof init, cudaMemcpyHostToDevice, st));
+    k_cand_ranges<<<grid_for(cand), kT, 0, st>>>(d_wlist, nw, e->capacity, s.wscalars.p, c.sid.p,
+                                                 c.smark.p, c.sfreq.p, c.slast.p, s.first_pos.p,
+                                                 s.uidx_of_pos.p, ucap, s.need_first.p, s.ranges.p);
+    k_cand_pack<<<grid_for(cand), kT, 0, st>>>(d_wlist, nw, e->capacity, s.wscalars.p, c.sid.p,
+                                               c.smark.p, c.sfreq.p, c.slast.p, e->ol.p,
+                                               s.first_pos.p, s.uidx_of_pos.p, ucap, s.need_first.p,
+                                               s.ranges.p, s.cand_key.p, s.cand_slot.p, e->flags.p);
+    EDX_LAUNCHED();
+    cub_call(e, [&](void* tmp, size_t& b) {
+      return cub::DeviceRadixSort::SortPairs(tmp, b, s.cand_key.p, s.cand_key_sorted.p,
+                                             s.cand_slot.p, s.cand_slot_sorted.p,
+                                             static_cast<int>(cand), 0, 64, st);
+    });
+    k_cand_offsets<<<1, 32, 0, st>>>(d_wlist, nw, s.wscalars.p, e->flags.p);
+    k_evict_contrib<<<grid_for(T), kT, 0, st>>>(s.need_key_sorted.p, s.counters.p, n,
+                                                s.need_type.p, s.ins_rank.p, s.wscalars.p,
+                                                s.cand_slot_sorted.p, c.smark.p, e->capacity,
+                                                c.cur_mark.p, s.need_contrib.p);
+    EDX_LAUNCHED();
+    launches += 3 + 8 + 2;
+  }
+  cub_call(e, [&](void* tmp, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(tmp, b, s.need_contrib.p,
+                                         reinterpret_cast<int32_t*>(s.flag_scan.p),
+                                         static_cast<int>(T + 1), st);
+  });
+  const int32_t* con_scan = reinterpret_cast<const int32_t*>(s.flag_scan.p);
+  launches += 1;
+  if (nw > 0) {
+    k_find_advance<<<grid_for(T), kT, 0, st>>>(s.need_key_sorted.p, s.counters.p, n, s.need_type.p,
+                                               s.ins_rank.p, con_scan, s.wscalars.p, c.at_cur.p,
+                                               e->capacity);
+    dim3 g(8, nw);
+    k_evict<<<g, kT, 0, st>>>(d_wlist, nw, s.wscalars.p, s.cand_slot_sorted.p, c.sid.p,
+                              e->capacity, e->id_space, e->ol.p, e->res.p, c.slot_of.p,
+                              s.cand_count.p, s.counters.p, n);
+    EDX_LAUNCHED();
+    launches += 2;
+  }
+  k_apply<<<grid_for(T), kT, 0, st>>>(s.need_key_sorted.p, s.counters.p, n, e->cur_ids,
+                                      s.need_type.p, s.ins_rank.p, s.wscalars.p,
+                                      s.cand_slot_sorted.p, e->capacity, e->id_space, c.cur_mark.p,
+                                      clock32, e->ol.p, e->res.p, c.slot_of.p, c.sid.p, c.smark.p,
+                                      c.sfreq.p, c.slast.p);
+  k_worker_finalize<<<1, 64, 0, st>>>(n, s.wscalars.p, con_scan, c.size.p, c.cur_mark.p,
+                                      c.at_cur.p);
+  k_phase3<<<grid_for(T), kT, 0, st>>>(s.uniq.p, s.umask.p, s.counters.p, n, e->ol.p);
+  k_reset<<<grid_for(T), kT, 0, st>>>(s.uniq.p, s.counters.p, n, s.need_key_sorted.p, e->cur_ids,
+                                      s.uidx_of_pos.p, ucap, s.first_pos.p, s.umask.p,
+                                      s.need_first.p, s.need_cnt.p);
+  k_reset_unique<<<grid_for(T), kT, 0, st>>>(s.uniq.p, s.counters.p, n, s.first_pos.p, s.umask.p);
+  EDX_LAUNCHED();
+  launches += 5;
+  EDX_CUDA(cudaMemcpyAsync(e->h_counters, s.counters.p, (3 * n + 4) * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, st));
+  out->launches = launches;
+  out->evicting_workers = nw;
+}
+
+}  // namespace edx

@@ -1,0 +1,46 @@
+"""Shared builders for the parity tests (configs follow SURVEY §8(d))."""
+import numpy as np
+
+HET = lambda n: [5e9] * (n // 2) + [5e8] * (n - n // 2)  # config.hpp:153 half fast, half slow
+
+# (n, m, bandwidths, cache, V, L, iterations, zipf seed) — SURVEY §8(d)
+CONFIGS = {
+    "C1": dict(n=4, m=256, bw=[5e9] * 4, cap=10_000, V=100_000, L=26),
+    "C2": dict(n=8, m=128, bw=HET(8), cap=10_000, V=100_000, L=26),
+    "C3": dict(n=16, m=512, bw=HET(16), cap=800_000, V=10_000_000, L=26),
+    "C4": dict(n=32, m=512, bw=HET(32), cap=800_000, V=10_000_000, L=100),
+    # eviction pressure (test_sim.cpp:172-209)
+    "P2": dict(n=2, m=4, bw=[5e9, 5e8], cap=12, V=60, L=3),
+    "P3": dict(n=3, m=4, bw=[5e9, 5e9, 5e8], cap=14, V=80, L=3),
+    "P8": dict(n=8, m=16, bw=HET(8), cap=120, V=400, L=6),
+}
+
+
+def offsets_for(R, L):
+    return np.arange(R + 1, dtype=np.uint64) * np.uint64(L)
+
+
+def canon_equal(a, b):
+    """Compare (global, caches) canonical states; returns '' or a diff message."""
+    ga, ca = a
+    gb, cb = b
+    if ga.shape != gb.shape or not (ga == gb).all():
+        if ga.shape != gb.shape:
+            return f"global count {ga.shape[0]} vs {gb.shape[0]}"
+        bad = np.nonzero((ga != gb).any(1))[0][:5]
+        return f"global rows differ at {bad.tolist()}: {ga[bad].tolist()} vs {gb[bad].tolist()}"
+    for j, ((ea, ma, xa), (eb, mb, xb)) in enumerate(zip(ca, cb)):
+        if ea.shape != eb.shape:
+            return f"worker {j}: cache size {ea.shape[0]} vs {eb.shape[0]}"
+        if not (ea == eb).all():
+            bad = np.nonzero((ea != eb).any(1))[0][:5]
+            return f"worker {j}: entries differ {ea[bad].tolist()} vs {eb[bad].tolist()}"
+        if ma != mb or xa != xb:
+            return f"worker {j}: marks ({ma},{xa}) vs ({mb},{xb})"
+    return ""
+
+
+def random_int_matrix(rows, cols, seed, max_value=100):
+    """oracles::random_int_matrix (tests/oracles.hpp:80-95) semantics, numpy RNG."""
+    rng = np.random.default_rng(seed)
+    return rng.integers(0, max_value + 1, size=(rows, cols)).astype(np.float64)

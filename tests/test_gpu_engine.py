@@ -1,0 +1,158 @@
+"""GPU parity of the engine (SimState on device) against the oracle.
+
+KATs from tests/test_sim.cpp, then multi-iteration runs over the reference's
+own input stream comparing, after every iteration: every matrix cell
+(bitwise), the decision, expected_cost_s, the IterationReport and the
+canonical global + cache state."""
+import numpy as np
+import pytest
+
+from helpers import CONFIGS, canon_equal, offsets_for
+
+pytestmark = pytest.mark.gpu
+
+U = 3.2768e-6
+
+
+def make(edx, n, m, cap, bw=None, alpha=1.0, id_space=1 << 12, max_ids=1 << 12):
+    c = edx.ClusterConfig(n=n, m=m, bandwidths_bps=bw or [5e9] * n, d_tran_bytes=2048,
+                          cache_capacity=cap, alpha=alpha)
+    return c, edx.SimState(c, id_space=id_space, max_batch_ids=max_ids)
+
+
+def test_walkthrough_fig2(gpu):
+    """test_sim.cpp:50-83."""
+    edx = gpu
+    c, s = make(edx, 3, 1, 16, [5e9, 5e9, 5e8])
+    s.seed_entry(1, 0, True, False)
+    s.seed_entry(9, 2, True, True)
+    rep = s.step([[1], [9], [8, 10, 11]], [0, 1, 2])
+    assert rep.miss_pull_w == [0, 1, 3]
+    assert rep.update_push_w == [0, 0, 1]
+    assert rep.evict_push == 0 and rep.hits == 1 and rep.lookups == 5
+    assert rep.cost_w == [0.0, U, 4 * 3.2768e-5]
+    x9 = s.state_of(9)
+    assert x9.owned_by(1) and not x9.owned_by(2) and not x9.latest_on(2) and x9.resident_on(2)
+    ent = {int(r[0]): r for r in s.cache_entries(2)}
+    assert 9 in ent and ent[9][1] == 0
+    s.validate_consistency()
+
+
+def test_owner_keeps_embedding(gpu):
+    edx = gpu
+    c, s = make(edx, 2, 1, 8)
+    s.seed_entry(5, 0, True, True)
+    rep = s.step([[5], [6]], [0, 1])
+    assert rep.update_push == 0 and rep.miss_pull_w == [0, 1] and rep.hits == 1
+    assert rep.cost_w[0] == 0.0
+    rep = s.step([[7], [5]], [0, 1])
+    assert rep.update_push_w == [1, 0] and rep.miss_pull_w == [1, 1]
+    s.validate_consistency()
+
+
+def test_mutual_pushes(gpu):
+    edx = gpu
+    c, s = make(edx, 2, 1, 8)
+    rep = s.step([[3], [3]], [0, 1])
+    assert rep.miss_pull == 2
+    st = s.state_of(3)
+    assert st.owned_by(0) and st.owned_by(1)
+    rep = s.step([[3], [3]], [0, 1])
+    assert rep.update_push == 2 and rep.miss_pull == 0 and rep.hits == 2
+    s.validate_consistency()
+
+
+def test_unbalanced_decision_rejected(gpu):
+    edx = gpu
+    c, s = make(edx, 2, 1, 8)
+    with pytest.raises(edx.InvalidArgument):
+        s.step([[1], [2]], [0, 0])
+    with pytest.raises(edx.InvalidArgument):
+        s.step([[1], [2]], [0])
+
+
+def test_seed_full_cache(gpu):
+    edx = gpu
+    c, s = make(edx, 1, 1, 1)
+    s.seed_entry(1, 0, True, False)
+    with pytest.raises(edx.LogicError, match="full cache"):
+        s.seed_entry(2, 0, True, False)
+    s.seed_entry(1, 0, True, False)  # refresh is fine
+
+
+def run_parity(edx, oracle, pyoracle, name, alpha, iters, seed=42, s=1.05, check_state_every=1,
+               id_space=None):
+    p = CONFIGS[name]
+    n, m, L = p["n"], p["m"], p["L"]
+    R = n * m
+    c = edx.ClusterConfig(n=n, m=m, bandwidths_bps=p["bw"], d_tran_bytes=2048,
+                          cache_capacity=p["cap"], alpha=alpha)
+    eng = edx.SimState(c, id_space=id_space or p["V"], max_batch_ids=R * L)
+    sim = oracle.sim(pyoracle.Cfg(n, m, p["bw"], cap=p["cap"], alpha=alpha))
+    offs = offsets_for(R, L)
+    it = -1
+    for it, ids in enumerate(oracle.zipf_batches(p["V"], L, s, iters, seed, R)):
+        want_m = sim.build_matrix(ids, offs)
+        eng.load((ids, offs))
+        got_m = np.empty((R, n))
+        eng.build(got_m)
+        assert got_m.tobytes() == want_m.tobytes(), f"iter {it}: matrix differs"
+        want_d = oracle.ecomix(pyoracle.Cfg(n, m, p["bw"], alpha=alpha), want_m)
+        got_d, got_exp = eng.dispatch()
+        assert (got_d == want_d).all(), f"iter {it}: decision differs"
+        assert got_exp == oracle.decision_cost(want_m, want_d), f"iter {it}: expected cost"
+        want_r = sim.step(ids, offs, want_d)
+        got_r = eng.step().as_dict()
+        assert got_r == want_r, f"iter {it}: report {got_r} vs {want_r}"
+        if check_state_every and (it % check_state_every == 0 or it == iters - 1):
+            msg = canon_equal(eng.canonical_state(), sim.canonical_state())
+            assert not msg, f"iter {it}: {msg}"
+    assert it == iters - 1
+    eng.validate_consistency()
+    return eng, sim
+
+
+@pytest.mark.parametrize("alpha", [0.0, 0.5, 1.0])
+def test_engine_eviction_pressure_p2(gpu, oracle, pyoracle, alpha):
+    """test_sim.cpp:172-209 configuration (n=2, m=4, cap 12, V=60, L=3, 50 iters)."""
+    run_parity(gpu, oracle, pyoracle, "P2", alpha, 50, seed=1234)
+
+
+@pytest.mark.parametrize("alpha", [0.0, 0.25, 1.0])
+def test_engine_eviction_pressure_p3(gpu, oracle, pyoracle, alpha):
+    run_parity(gpu, oracle, pyoracle, "P3", alpha, 60, seed=7)
+
+
+@pytest.mark.parametrize("alpha", [0.0, 0.5])
+def test_engine_eviction_pressure_p8(gpu, oracle, pyoracle, alpha):
+    run_parity(gpu, oracle, pyoracle, "P8", alpha, 40, seed=99)
+
+
+def test_engine_c1(gpu, oracle, pyoracle):
+    """C1: 4 workers, batch 1024, uniform, 10% cache, greedy only."""
+    run_parity(gpu, oracle, pyoracle, "C1", 0.0, 30, check_state_every=10)
+
+
+@pytest.mark.parametrize("alpha", [0.25, 0.5])
+def test_engine_c2(gpu, oracle, pyoracle, alpha):
+    """C2: 8 heterogeneous workers, hybrid."""
+    run_parity(gpu, oracle, pyoracle, "C2", alpha, 12, check_state_every=4)
+
+
+def test_iterate_equals_stepwise(gpu, oracle, pyoracle):
+    """edx_engine_iterate (the fused run() body) gives the same results."""
+    edx = gpu
+    p = CONFIGS["P8"]
+    n, m, L = p["n"], p["m"], p["L"]
+    R = n * m
+    c = edx.ClusterConfig(n=n, m=m, bandwidths_bps=p["bw"], cache_capacity=p["cap"], alpha=0.5)
+    eng = edx.SimState(c, id_space=p["V"], max_batch_ids=R * L)
+    sim = oracle.sim(pyoracle.Cfg(n, m, p["bw"], cap=p["cap"], alpha=0.5))
+    offs = offsets_for(R, L)
+    for ids in oracle.zipf_batches(p["V"], L, 1.05, 25, 5, R):
+        dec, rep = eng.iterate(ids, offs)
+        wdec, wexp, wrep, _ = sim.iteration(ids, offs)
+        assert (dec == wdec).all()
+        assert rep.as_dict() == wrep
+        assert rep.expected_cost_s == wexp
+    assert not canon_equal(eng.canonical_state(), sim.canonical_state())

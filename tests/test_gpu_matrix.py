@@ -1,0 +1,261 @@
+"""GPU parity of the matrix-level API against the oracle (bit-exact).
+
+Mirrors the reference's KATs (tests/test_cost.cpp, tests/test_assign.cpp)
+and adds seeded random and tie-heavy cases; every comparison is exact
+(bitwise for doubles, equality for indices)."""
+import numpy as np
+import pytest
+
+from helpers import random_int_matrix
+
+pytestmark = pytest.mark.gpu
+
+U_FAST, U_SLOW = 3.2768e-6, 3.2768e-5
+
+
+def cfg(edx, n, m, bw, alpha=1.0, cap=64):
+    return edx.ClusterConfig(n=n, m=m, bandwidths_bps=bw, d_tran_bytes=2048, cache_capacity=cap,
+                             alpha=alpha)
+
+
+def snap_of(edx, entries):
+    s = edx.Snapshot()
+    for id_, w, latest, owner in entries:
+        st = s.setdefault(id_, edx.EmbeddingState())
+        st.resident |= 1 << w
+        if latest:
+            st.latest |= 1 << w
+        if owner:
+            st.owners |= 1 << w
+    return s
+
+
+# ----------------------------------------------------------- test_cost.cpp KATs
+def test_latest_resident_costs_nothing(gpu):
+    edx = gpu
+    c = cfg(edx, 2, 1, [5e9, 5e9])
+    m = edx.build_matrix([[7], [8]], snap_of(edx, [(7, 0, True, False)]), c)
+    assert m.at(0, 0) == 0.0
+
+
+def test_owned_elsewhere_push_and_pull(gpu):
+    edx = gpu
+    c = cfg(edx, 2, 1, [5e9, 5e9])
+    m = edx.build_matrix([[7], [8]], snap_of(edx, [(7, 1, True, True)]), c)
+    assert m.at(0, 0) == 2 * U_FAST
+
+
+def test_slow_owner(gpu):
+    edx = gpu
+    c = cfg(edx, 3, 1, [5e9, 5e9, 5e8])
+    m = edx.build_matrix([[9], [1], [2]], snap_of(edx, [(9, 2, True, True)]), c)
+    assert m.at(0, 1) == U_FAST + U_SLOW
+
+
+def test_unknown_one_pull(gpu):
+    edx = gpu
+    c = cfg(edx, 2, 1, [5e9, 5e8])
+    m = edx.build_matrix([[42], [43]], edx.Snapshot(), c)
+    assert m.at(0, 0) == U_FAST and m.at(0, 1) == U_SLOW
+
+
+def test_every_state_case_exhaustive(gpu, oracle, pyoracle):
+    """test_cost.cpp:82-111: one id, 3 workers, every consistent state."""
+    edx = gpu
+    c = cfg(edx, 3, 1, [5e9, 2e9, 5e8])
+    oc = pyoracle.Cfg(3, 1, [5e9, 2e9, 5e8])
+    for res in range(8):
+        for lat in range(8):
+            if lat & ~res:
+                continue
+            for own in range(8):
+                st = edx.EmbeddingState(own, lat, res)
+                if (own & ~lat) or (own and lat != own):
+                    continue
+                snap = edx.Snapshot({5: st})
+                got = edx.build_matrix([[5], [6], [5, 6]], snap, c).values
+                want = oracle.build_matrix_snapshot(oc, {5: (own, lat, res)},
+                                                    np.array([5, 6, 5, 6]), [0, 1, 2, 4])
+                assert got.tobytes() == want.tobytes(), (own, lat, res)
+
+
+def test_cold_and_tenfold(gpu):
+    edx = gpu
+    c = cfg(edx, 2, 2, [5e9, 5e9])
+    samples = [[1, 2, 3], [4, 5], [6], [7, 8, 9, 10]]
+    m = edx.build_matrix(samples, edx.Snapshot(), c)
+    for i, s in enumerate(samples):
+        assert (m.values[i] == len(s) * U_FAST).all()
+    c2 = cfg(edx, 2, 2, [5e9, 5e8])
+    m2 = edx.build_matrix([[1, 2], [3], [4, 5, 6], [7]], edx.Snapshot(), c2)
+    assert (m2.values[:, 1] == 10.0 * m2.values[:, 0]).all()
+
+
+def test_wrong_sample_count(gpu):
+    edx = gpu
+    with pytest.raises(edx.InvalidArgument, match="expected 4 samples, got 1"):
+        edx.build_matrix([[1]], edx.Snapshot(), cfg(edx, 2, 2, [5e9, 5e9]))
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 16, 31, 32, 33, 64])
+def test_build_random_snapshots_bitwise(gpu, oracle, pyoracle, n):
+    """Random consistent states over 200 ids, ragged samples: every cell bitwise."""
+    edx = gpu
+    rng = np.random.default_rng(1000 + n)
+    bw = rng.choice([5e9, 2e9, 5e8, 1e9, 3.3e9], size=n)
+    m = 7
+    c = cfg(edx, n, m, bw)
+    oc = pyoracle.Cfg(n, m, bw)
+    snap, osnap = edx.Snapshot(), {}
+    full = (1 << n) - 1 if n < 64 else (1 << 64) - 1
+    for id_ in range(200):
+        kind = rng.integers(0, 4)
+        res = int(rng.integers(0, 1 << min(n, 62))) & full
+        if kind == 0:
+            continue
+        if kind == 1:  # synced copies
+            lat = res & int(rng.integers(0, 1 << min(n, 62)))
+            own = 0
+        else:  # owned
+            own = res & int(rng.integers(0, 1 << min(n, 62)))
+            lat = own
+        snap[id_] = edx.EmbeddingState(own, lat, res)
+        osnap[id_] = (own, lat, res)
+    R = n * m
+    lens = rng.integers(1, 30, size=R)
+    samples = [list(rng.choice(260, size=l, replace=False)) for l in lens]
+    got = edx.build_matrix(samples, snap, c).values
+    ids, offs = edx.to_csr(samples)
+    want = oracle.build_matrix_snapshot(oc, osnap, ids, offs)
+    assert got.tobytes() == want.tobytes()
+
+
+# ------------------------------------------------------------- gap / order
+def test_row_gap_key_kat(gpu):
+    edx = gpu
+    m = np.array([[1, 5], [4, 4], [2, 2]], float)
+    assert edx.row_gap_key(m, 0) == 4.0
+    assert edx.row_gap_key(m, 1) == 0.0
+    assert edx.row_gap_key(np.array([[3, 1, 2]], float), 0) == 1.0
+    assert edx.row_gap_key(np.array([[9]], float), 0) == 0.0
+    with pytest.raises(edx.InvalidArgument):
+        edx.row_gap_key(np.zeros((1, 0)), 0)
+
+
+@pytest.mark.parametrize("seed,rows,cols,maxv", [(1, 1024, 8, 3), (2, 4096, 16, 1000),
+                                                  (3, 333, 5, 1), (4, 16384, 32, 50)])
+def test_rows_by_gap(gpu, oracle, seed, rows, cols, maxv):
+    edx = gpu
+    m = random_int_matrix(rows, cols, seed, maxv) * 3.2768e-6
+    assert (edx.rows_by_gap(m) == oracle.rows_by_gap(m)).all()
+
+
+# ----------------------------------------------------------------- solvers
+def test_hungarian_kats(gpu):
+    edx = gpu
+    r = edx.hungarian(np.zeros((2, 2)))
+    assert r.total_cost == 0.0 and sorted(r.col_of_row.tolist()) == [0, 1]
+    r = edx.hungarian(np.array([[1, 2], [3, 1]], float))
+    assert r.total_cost == 2.0 and r.col_of_row.tolist() == [0, 1]
+    with pytest.raises(edx.InvalidArgument):
+        edx.hungarian(np.array([[1, 2], [3, -1]], float))
+    with pytest.raises(edx.InvalidArgument):
+        edx.hungarian(np.array([[1, 2], [3, np.inf]], float))
+    with pytest.raises(edx.InvalidArgument):
+        edx.hungarian(np.zeros((0, 0)))
+
+
+@pytest.mark.parametrize("k,maxv", [(5, 100), (6, 100), (8, 3), (33, 10), (100, 1000),
+                                    (257, 5), (512, 100)])
+def test_hungarian_dense_matches_reference(gpu, oracle, k, maxv):
+    edx = gpu
+    for seed in range(3):
+        sq = random_int_matrix(k, k, 50 * k + seed, maxv)
+        got = edx.hungarian(sq)
+        cols, total = oracle.hungarian(sq)
+        assert (got.col_of_row == cols).all()
+        assert got.total_cost == total
+
+
+@pytest.mark.parametrize("k", [64, 256])
+def test_hungarian_bench_matrix(gpu, oracle, k):
+    """cmd_bench input (experiment.hpp:217-223)."""
+    edx = gpu
+    sq = oracle.bench_matrix(k)
+    got = edx.hungarian(sq)
+    cols, total = oracle.hungarian(sq)
+    assert (got.col_of_row == cols).all() and got.total_cost == total
+
+
+@pytest.mark.parametrize("n,mult,maxv", [(2, 3, 100), (4, 8, 3), (8, 16, 1000), (8, 32, 5),
+                                         (16, 16, 50), (33, 4, 20), (64, 2, 7), (8, 64, 1000)])
+def test_hungarian_blocks_equals_expanded(gpu, oracle, n, mult, maxv):
+    """The collapsed solver == hungarian(expand_columns(...)), column for column."""
+    edx = gpu
+    for seed in range(3):
+        rows = n * mult * 2
+        m = random_int_matrix(rows, n, 7 * n + mult + seed, maxv) * 3.2768e-6
+        order = oracle.rows_by_gap(m)
+        block = order[: n * mult]
+        got = edx.hungarian_blocks(m, block, mult)
+        sq = edx.expand_columns(m, block, mult)
+        cols, total = oracle.hungarian(sq.values)
+        assert (got.col_of_row == cols).all()
+        assert got.total_cost == total
+
+
+def test_greedy_kats(gpu):
+    edx = gpu
+    m = np.array([[5, 1, 2]], float)
+    assert edx.greedy_dispatch(m, [0], [1, 0, 0])[0][1] == 0
+    assert edx.greedy_dispatch(m, [0], [0, 1, 0])[0][1] == 1
+    m = np.array([[1, 5], [1, 2]], float)
+    assert edx.greedy_dispatch(m, [0, 1], [1, 1]) == [(0, 0), (1, 1)]
+    assert edx.greedy_dispatch(np.array([[4, 4, 4]], float), [0], [0, 1, 1])[0][1] == 1
+    with pytest.raises(edx.InvalidArgument):
+        edx.greedy_dispatch(np.array([[1, 2], [3, 4]], float), [0, 1], [1, 0])
+    m = np.array([[0, 5], [0, 6], [1, 3], [2, 7]], float)  # adversarial fixture
+    assert [w for _, w in edx.greedy_dispatch(m, [0, 1, 2, 3], [2, 2])] == [0, 0, 1, 1]
+
+
+@pytest.mark.parametrize("rows,n,maxv", [(16, 4, 100), (1024, 8, 3), (5000, 13, 2),
+                                         (20000, 64, 1000)])
+def test_greedy_matches_reference(gpu, oracle, rows, n, maxv):
+    edx = gpu
+    rng = np.random.default_rng(rows + n)
+    m = random_int_matrix(rows, n, rows * n, maxv)
+    order = rng.permutation(rows).astype(np.uint64)
+    cap = np.full(n, rows // n, np.int32)
+    cap[: rows - cap.sum()] += 1
+    got = edx.greedy_dispatch(m, order, cap)
+    orows, owork = oracle.greedy_dispatch(m, order, cap)
+    assert [w for _, w in got] == owork.tolist()
+
+
+@pytest.mark.parametrize("n,m,alpha,maxv", [(2, 3, 1.0, 100), (3, 2, 0.0, 100), (2, 2, 0.5, 100),
+                                            (4, 4, 0.3, 1), (4, 8, 0.77, 5), (8, 128, 0.25, 1000),
+                                            (8, 128, 0.5, 3), (8, 128, 1.0, 1000),
+                                            (16, 64, 0.125, 50), (5, 7, 0.6, 2)])
+def test_ecomix_matches_reference(gpu, oracle, pyoracle, n, m, alpha, maxv):
+    edx = gpu
+    for seed in range(2):
+        mat = random_int_matrix(n * m, n, 97 * n + m + seed, maxv) * 3.2768e-6
+        c = cfg(edx, n, m, [5e9] * n, alpha)
+        got = edx.ecomix(mat, c).worker_of_sample
+        want = oracle.ecomix(pyoracle.Cfg(n, m, [5e9] * n, alpha=alpha), mat)
+        assert (got == want).all()
+        assert edx.decision_cost(mat, got) == oracle.decision_cost(mat, want)
+
+
+def test_ecomix_degenerate_flat(gpu):
+    edx = gpu
+    flat = np.full((16, 4), 2.5)
+    for a in (0.0, 0.3, 0.5, 0.77, 1.0):
+        c = cfg(edx, 4, 4, [1e9] * 4, a)
+        edx.ecomix(flat, c).validate(c)
+
+
+def test_ecomix_shape_error(gpu):
+    edx = gpu
+    with pytest.raises(edx.InvalidArgument, match="matrix shape does not match cluster config"):
+        edx.ecomix(np.zeros((3, 2)), cfg(edx, 2, 2, [1e9, 1e9]))

@@ -1,0 +1,132 @@
+"""CPU tests (no GPU): the library loads and exports every declared symbol,
+host-side validation and the input stream match the reference, and the
+oracle restatement is pinned against the compiled reference."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from helpers import CONFIGS, canon_equal, offsets_for
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    text = open(os.path.join(ROOT, "include", "edx.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(edx_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol(edx):
+    from paper_2512_21615_b200 import _lib
+    L = _lib.lib()
+    names = declared_symbols()
+    assert len(names) >= 30
+    for name in names:
+        assert hasattr(L, name), name
+    bound = {s[0] for s in _lib.SIGNATURES}
+    assert set(names) == bound, set(names) ^ bound
+    assert L.edx_abi_version() == 1
+
+
+def test_validate_config_messages(edx):
+    c = edx.ClusterConfig(n=65, m=1, bandwidths_bps=[1e9] * 65, cache_capacity=10)
+    with pytest.raises(edx.InvalidArgument, match="at most 64 workers supported"):
+        edx.validate(c, 1)
+    c = edx.ClusterConfig(n=2, m=4, bandwidths_bps=[1e9], cache_capacity=10)
+    with pytest.raises(edx.InvalidArgument, match="one bandwidth per worker"):
+        edx.validate(c, 1)
+    c = edx.ClusterConfig(n=2, m=4, bandwidths_bps=[1e9, 0.0], cache_capacity=10)
+    with pytest.raises(edx.InvalidArgument, match="bandwidths must be positive"):
+        edx.validate(c, 1)
+    c = edx.ClusterConfig(n=2, m=256, bandwidths_bps=[1e9, 1e9], cache_capacity=5000)
+    with pytest.raises(edx.InvalidArgument, match="cannot hold one micro-batch of 6656"):
+        edx.validate(c, 26)
+    c = edx.ClusterConfig(n=2, m=2, bandwidths_bps=[1e9, 1e9], cache_capacity=10, alpha=1.5)
+    with pytest.raises(edx.InvalidArgument, match="alpha"):
+        edx.validate(c, 1)
+    edx.validate(edx.ClusterConfig(n=4, m=256, bandwidths_bps=[5e9] * 4, cache_capacity=10000), 26)
+
+
+def test_unit_cost_known_answers(edx):
+    """test_core.cpp:43-49."""
+    c = edx.ClusterConfig(n=2, m=1, bandwidths_bps=[5e9, 5e8])
+    assert edx.unit_cost(c, 0) == 3.2768e-6
+    assert edx.unit_cost(c, 1) == 3.2768e-5
+    with pytest.raises(edx.InvalidArgument):
+        edx.unit_cost(c, 2)
+
+
+def test_make_sample(edx):
+    assert edx.make_sample([3, 1, 3, 2, 1]) == [3, 1, 2]
+    with pytest.raises(edx.InvalidArgument):
+        edx.make_sample([])
+
+
+def test_expand_columns(edx):
+    m = np.array([[1, 2], [3, 4], [5, 6]], float)
+    sq = edx.expand_columns(m, [2, 0], 1)
+    assert sq.values.tolist() == [[5, 6], [1, 2]]
+    assert sq.col_to_worker.tolist() == [0, 1]
+    with pytest.raises(edx.InvalidArgument):
+        edx.expand_columns(m, [0], 1)
+
+
+@pytest.mark.parametrize("name", ["C1", "P2", "C3"])
+def test_zipf_stream_matches_oracle(edx, oracle, name):
+    """The product's input stream (workload.cpp) == the reference's ZipfStream."""
+    p = CONFIGS[name]
+    R = p["n"] * p["m"]
+    z = edx.ZipfStream(p["V"], p["L"], 1.05, 3, 42, R)
+    for a, b in zip(z, oracle.zipf_batches(p["V"], p["L"], 1.05, 3, 42, R)):
+        assert (a == b).all()
+
+
+def test_oracle_port_kats(port, pyoracle):
+    """The restatement reproduces the reference's own known answers."""
+    c = pyoracle.Cfg(3, 1, [5e9, 5e9, 5e8])
+    m = port.build_matrix_snapshot(c, {9: (4, 4, 4)}, np.array([9, 1, 2], np.uint32), [0, 1, 2, 3])
+    assert m[0, 1] == 3.2768e-6 + 3.2768e-5
+    cols, total = port.hungarian(np.array([[1, 2], [3, 1]], float))
+    assert cols.tolist() == [0, 1] and total == 2.0
+    rows, workers = port.greedy_dispatch(np.array([[0, 5], [0, 6], [1, 3], [2, 7]], float),
+                                         [0, 1, 2, 3], [2, 2])
+    assert workers.tolist() == [0, 0, 1, 1]
+    s = port.sim(pyoracle.Cfg(3, 1, [5e9, 5e9, 5e8], cap=16))
+    s.seed_entry(1, 0, True, False)
+    s.seed_entry(9, 2, True, True)
+    rep = s.step(np.array([1, 9, 8, 10, 11], np.uint32), [0, 1, 2, 5], [0, 1, 2])
+    assert rep["miss_pull_w"] == [0, 1, 3] and rep["update_push_w"] == [0, 0, 1]
+    assert rep["cost_w"] == [0.0, 3.2768e-6, 4 * 3.2768e-5]
+
+
+@pytest.mark.parametrize("name,alpha,iters,seed", [("P2", 0.5, 50, 1234), ("P3", 1.0, 60, 7),
+                                                   ("P8", 0.25, 30, 99), ("C1", 0.0, 6, 42)])
+def test_oracle_port_equals_reference(port, ref, pyoracle, name, alpha, iters, seed):
+    """Pins the plain-C oracle against the compiled, unmodified reference."""
+    p = CONFIGS[name]
+    n, m, L = p["n"], p["m"], p["L"]
+    R = n * m
+    cfg = pyoracle.Cfg(n, m, p["bw"], cap=p["cap"], alpha=alpha)
+    a, b = port.sim(cfg), ref.sim(cfg)
+    offs = offsets_for(R, L)
+    for ids, ids2 in zip(port.zipf_batches(p["V"], L, 1.05, iters, seed, R),
+                         ref.zipf_batches(p["V"], L, 1.05, iters, seed, R)):
+        assert (ids == ids2).all()
+        ma, mb = a.build_matrix(ids, offs), b.build_matrix(ids, offs)
+        assert ma.tobytes() == mb.tobytes()
+        da, db = port.ecomix(cfg, ma), ref.ecomix(cfg, mb)
+        assert (da == db).all()
+        assert a.step(ids, offs, da) == b.step(ids, offs, db)
+    assert not canon_equal(a.canonical_state(), b.canonical_state())
+
+
+def test_oracle_solver_equals_reference(port, ref):
+    for k, maxv in [(5, 100), (40, 3), (128, 1000)]:
+        sq = np.random.default_rng(k).integers(0, maxv + 1, (k, k)).astype(float)
+        c1, t1 = port.hungarian(sq)
+        c2, t2 = ref.hungarian(sq)
+        assert (c1 == c2).all() and t1 == t2
+    assert (port.bench_matrix(16) == ref.bench_matrix(16)).all()
