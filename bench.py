@@ -1,0 +1,386 @@
+#!/usr/bin/env python
+"""bench.py — samples dispatched/sec of the embedding-sample dispatch path.
+
+One bench step = one dispatch iteration of the reference's run() loop
+(sim.hpp:421-441) on the next batch of the reference's Zipf input stream:
+expected-cost matrix build -> EcoMix decision (exact Hungarian block +
+capacity-bounded greedy) -> per-worker cache update (SimState::step).  The
+batches are sequential because each dispatch changes the cache state.
+
+Default workload = BASELINE.json configs[1] ("C2"): 8 heterogeneous workers
+(4 x 5 Gbps + 4 x 0.5 Gbps), batch 1024 (m=128), 26 Zipf(1.05) ids per
+sample over 100K ids, 10K-entry caches, hybrid dispatcher alpha=0.5.  Before
+timing, `prefill` iterations bring the caches to steady state (evicting).
+
+  value : samples/s with the batches already resident in HBM
+  e2e   : samples/s through the C ABI (edx_engine_iterate) from pinned host
+          buffers, H2D of the ids and D2H of decision + report inside the
+          timed region
+  --impl reference : the reference's own CPU dispatcher (oracle/_ref, the
+          unmodified headers compiled in place) on this host's cores.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HET = lambda n: [5e9] * (n // 2) + [5e8] * (n - n // 2)
+WORKLOADS = {
+    "C1": dict(n=4, m=256, L=26, V=100_000, cap=10_000, bw=[5e9] * 4, alpha=0.0, prefill=20,
+               desc="C1: Zipf(1.05), 26 fields, batch 1024, 4 uniform workers, 10% cache, greedy only"),
+    "C2": dict(n=8, m=128, L=26, V=100_000, cap=10_000, bw=HET(8), alpha=0.5, prefill=20,
+               desc="C2: Zipf(1.05), 26 fields, batch 1024, 8 heterogeneous workers "
+                    "(4x5Gbps+4x0.5Gbps), 10% cache, hybrid EcoMix alpha=0.5"),
+    "C3": dict(n=16, m=512, L=26, V=10_000_000, cap=800_000, bw=HET(16), alpha=0.125, prefill=3,
+               desc="C3: Criteo-shaped, 10M ids, batch 8192, 16 heterogeneous workers, alpha=0.125"),
+    "C4": dict(n=32, m=512, L=100, V=10_000_000, cap=800_000, bw=HET(32), alpha=0.0625, prefill=2,
+               desc="C4: Avazu-shaped, 100 ids/sample, batch 16384, 32 workers, alpha=1/16"),
+}
+METRIC = "samples dispatched/sec (cost matrix + hybrid decision + cache update)"
+ZIPF_S, SEED = 1.05, 42
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="product", choices=["product", "reference"])
+    ap.add_argument("--config", default="C2", choices=sorted(WORKLOADS))
+    ap.add_argument("--alpha", type=float, default=None)
+    ap.add_argument("--prefill", type=int, default=None)
+    ap.add_argument("--cpu-sample", type=int, default=10, help="timed iterations of cpu_baseline")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-flush", action="store_true", help="do not flush L2 between iterations")
+    return ap.parse_args()
+
+
+def workload(args):
+    w = dict(WORKLOADS[args.config])
+    if args.alpha is not None:
+        w["alpha"] = args.alpha
+    if args.prefill is not None:
+        w["prefill"] = args.prefill
+    w["R"] = w["n"] * w["m"]
+    return w
+
+
+def batches(w, count):
+    """The reference's ZipfStream (workload.hpp:94-133) through the product's
+    own host generator (bit-identical; tests/test_host.py pins it)."""
+    import paper_2512_21615_b200 as edx
+    z = edx.ZipfStream(w["V"], w["L"], ZIPF_S, count, SEED, w["R"])
+    return [ids for ids in z]
+
+
+def config_json(w, args, extra=None):
+    c = {"workload": w["desc"], "n_workers": w["n"], "m": w["m"], "batch": w["R"],
+         "ids_per_sample": w["L"], "id_space": w["V"], "cache_per_worker": w["cap"],
+         "alpha": w["alpha"], "zipf_s": ZIPF_S, "seed": SEED,
+         "prefill_iterations": w["prefill"],
+         "l2": "flushed between timed iterations (256 MiB write)" if not args.no_flush
+         else "not flushed"}
+    if extra:
+        c.update(extra)
+    return c
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.gpu_idle,"
+              "clocks_event_reasons.sw_power_cap,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=5)
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        names = ["gpu_idle", "sw_power_cap", "hw_slowdown", "hw_thermal_slowdown",
+                 "sw_thermal_slowdown"]
+        sm, mx, reasons = [], 0, set()
+        for l in getattr(self, "lines", []):
+            p = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(p[0]))
+                mx = max(mx, float(p[1]))
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, p[3:]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------- product arm
+def algorithmic_build_bytes(w, ids):
+    """B_alg = 4 R L (ids) + 16 U (owners+latest per unique id)
+    + 8 n (unit costs) + 8 R n (matrix write)."""
+    U = len(np.unique(ids))
+    return 4 * w["R"] * w["L"] + 16 * U + 8 * w["n"] + 8 * w["R"] * w["n"], U
+
+
+def product(args, w, rank, world, local_rank):
+    import torch
+    import paper_2512_21615_b200 as edx
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    n, m, L, R = w["n"], w["m"], w["L"], w["R"]
+    K, W, P = args.steps, args.warmup, w["prefill"]
+    total = P + 2 * (W + K)
+    host = batches(w, total)
+    offs = np.arange(R + 1, dtype=np.uint64) * np.uint64(L)
+    cfg = edx.ClusterConfig(n=n, m=m, bandwidths_bps=w["bw"], d_tran_bytes=2048,
+                            cache_capacity=w["cap"], alpha=w["alpha"])
+    eng = edx.SimState(cfg, id_space=w["V"], max_batch_ids=R * L, device=local_rank)
+    stream = torch.cuda.ExternalStream(eng.stream_handle(), device=dev)
+    flush = None if args.no_flush else torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    # prefill to steady state (untimed)
+    for b in host[:P]:
+        eng.iterate(b, offs, want_decision=False)
+
+    # ---- value: inputs resident in HBM
+    seg = host[P:P + W + K]
+    d_ids = torch.from_numpy(np.stack(seg).view(np.int32)).to(dev)
+    d_offs = torch.from_numpy(offs.view(np.int64)).to(dev)
+    torch.cuda.synchronize()
+
+    def one_resident(i):
+        eng.load(None, on_device=True, ids_ptr=d_ids[i].data_ptr(), offsets_ptr=d_offs.data_ptr(),
+                 rows=R)
+        eng.build(None)
+        eng.dispatch(want_decision=False, want_expected=False)
+        return eng.step()
+
+    def timed(fn, idx):
+        starts = [torch.cuda.Event(enable_timing=True) for _ in idx]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in idx]
+        for t, i in enumerate(idx):
+            if flush is not None:
+                with torch.cuda.stream(stream):
+                    flush.fill_(t & 0xFF)
+            starts[t].record(stream)
+            fn(i)
+            ends[t].record(stream)
+        torch.cuda.synchronize()
+        return [s.elapsed_time(e) for s, e in zip(starts, ends)]
+
+    for i in range(W):
+        one_resident(i)
+    eng.set_profiling(True)
+    eng.phase_times(reset=True)
+    with ClockSampler(local_rank) as clk:
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        ms = timed(one_resident, range(W, W + K))
+        torch.cuda.synchronize()
+    phase_ms, counts = eng.phase_times(reset=True)
+    eng.set_profiling(False)
+    launches = int(counts[0])
+    solver_steps = int(counts[1])
+    step_ms = sum(ms) / K
+
+    # ---- e2e: through edx_engine_iterate from pinned host buffers
+    seg2 = host[P + W + K:]
+    pinned = torch.from_numpy(np.stack(seg2).view(np.int32)).pin_memory()
+    pinned_offs = torch.from_numpy(offs.view(np.int64)).pin_memory()
+    pin_np = pinned.numpy().view(np.uint32)
+    poffs_np = pinned_offs.numpy().view(np.uint64)
+    for i in range(W):
+        eng.iterate(pin_np[i], poffs_np)
+    e2e_ms = timed(lambda i: eng.iterate(pin_np[i], poffs_np), range(W, W + K))
+    e2e_step_ms = sum(e2e_ms) / K
+
+    # ---- roofline of the cost build (K1), per launch
+    b_alg, uniq = zip(*(algorithmic_build_bytes(w, host[P + W + i]) for i in range(K)))
+    t_build_ms = phase_ms[0] / K
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    achieved = (sum(b_alg) / K) / (t_build_ms * 1e-3) / 1e9 if t_build_ms > 0 else None
+    traffic = None
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "k_cost_build_traffic.json")))
+        traffic = traffic.get(args.config, {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        traffic = None
+
+    out = {
+        "metric": METRIC, "value": R / (step_ms * 1e-3), "unit": "samples/s", "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": step_ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: reference ZipfStream (s=1.05, seed 42), state warmed by prefill",
+        "config": config_json(w, args),
+        "e2e": {"value": R / (e2e_step_ms * 1e-3), "unit": "samples/s",
+                "ms_per_step": e2e_step_ms, "h2d_bytes_per_step": R * L * 4 + (R + 1) * 8,
+                "d2h_bytes_per_step": R * 4 + 8 + (3 * n + 4) * 8},
+        "roofline": {"kernel": "k_cost_build (K1, cost.hpp:81-125)", "bound": "hbm",
+                     "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": (achieved / hbm_peak) if achieved else None, "traffic": traffic,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else
+                     "fallback 6.65 TB/s",
+                     "algorithmic_bytes_per_launch": sum(b_alg) / K,
+                     "unique_ids_per_batch": sum(uniq) / K, "launch_ms": t_build_ms},
+        "dominant_kernel": "k_hungarian_blocks (exact EcoMix block; latency-bound single warp)",
+        "solver": {"exact_rows": n * int(np.floor(m * w["alpha"] + 1e-9)),
+                   "latency_ms_per_batch": phase_ms[2] / K,
+                   "dijkstra_steps_last_batch": solver_steps,
+                   "ns_per_step": (phase_ms[2] / K) * 1e6 / solver_steps if solver_steps else None},
+        "phases_ms_per_step": {"build": phase_ms[0] / K, "gap_sort": phase_ms[1] / K,
+                               "exact_solve": phase_ms[2] / K, "greedy": phase_ms[3] / K,
+                               "cache_update": phase_ms[4] / K, "dispatch_total": phase_ms[5] / K},
+        "build_decide": {"value": R / ((phase_ms[0] + phase_ms[5]) / K * 1e-3),
+                         "unit": "samples/s",
+                         "note": "reference timing regions only (matrix_s + decision_s, "
+                                 "sim.hpp:423-432)"},
+        "clocks": clk.summary(),
+        "gpu_launches": launches,
+    }
+    return out, host[:P + W + K], offs
+
+
+# ------------------------------------------------------------ reference arm
+def reference_oracle():
+    from oracle import pyoracle
+    if os.path.exists(pyoracle.REF_SO):
+        return pyoracle.Oracle("reference"), "reference"
+    if not os.path.exists(pyoracle.PORT_SO):
+        pyoracle.build(ref=False)
+    return pyoracle.Oracle("port"), "port"
+
+
+def cpu_run(w, host, offs, prefill, warmup, steps, threads):
+    """Reference iterations (orc_ref_iteration: snapshot, build, ecomix, step)
+    on host cores; returns per-iteration seconds of the timed ones."""
+    from oracle import pyoracle
+    orc, kind = reference_oracle()
+    sim = orc.sim(pyoracle.Cfg(w["n"], w["m"], w["bw"], cap=w["cap"], alpha=w["alpha"]))
+    times, bd = [], []
+    for i, ids in enumerate(host[:prefill + warmup + steps]):
+        t0 = time.perf_counter()
+        _, _, _, ph = sim.iteration(ids, offs, threads=threads)
+        dt = time.perf_counter() - t0
+        if i >= prefill + warmup:
+            times.append(dt)
+            bd.append(ph[1] + ph[2])
+    return times, bd, kind
+
+
+def cpu_baseline(w, host, offs, sample):
+    import platform
+    P = w["prefill"]
+    times, bd, kind = cpu_run(w, host, offs, P, 0, sample, threads=1)
+    cpu = platform.processor() or ""
+    try:
+        for l in open("/proc/cpuinfo"):
+            if l.startswith("model name"):
+                cpu = l.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    mean = sum(times) / len(times)
+    return {"value": w["R"] / mean, "unit": "samples/s", "cores": 1, "kind": kind,
+            "sample": f"{w['desc'].split(':')[0]} iterations {P}..{P + sample - 1} after {P} "
+                      f"untimed prefill iterations, reference run() body "
+                      f"(snapshot+build_matrix+ecomix+step), 1 thread as shipped",
+            "ms_per_step": mean * 1e3,
+            "build_decide_samples_per_s": w["R"] / (sum(bd) / len(bd)),
+            "host_cpu": cpu, "host_nproc": os.cpu_count()}
+
+
+def reference_arm(args, w, rank, world):
+    if rank != 0:
+        return None
+    threads = os.cpu_count() or 1
+    K, W, P = args.steps, args.warmup, w["prefill"]
+    host = batches(w, P + W + K)
+    offs = np.arange(w["R"] + 1, dtype=np.uint64) * np.uint64(w["L"])
+    times, bd, kind = cpu_run(w, host, offs, P, W, K, threads=threads)
+    mean = sum(times) / len(times)
+    value = w["R"] / mean
+    return {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s",
+        "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": mean * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: reference ZipfStream (s=1.05, seed 42), state warmed by prefill",
+        "config": config_json(w, args),
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads, "kind": kind,
+                         "sample": f"iterations {P + W}..{P + W + K - 1}; build_matrix rows "
+                                   f"split over {threads} threads (bit-identical), ecomix and "
+                                   f"step single-threaded as in the reference"},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "build_decide": {"value": w["R"] / (sum(bd) / len(bd)), "unit": "samples/s"},
+    }
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    w = workload(args)
+    if args.impl == "reference":
+        out = reference_arm(args, w, rank, world)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    out, host, offs = product(args, w, rank, world, local_rank)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([out["ms_per_step"], out["e2e"]["ms_per_step"]], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        out["ms_per_step"], out["e2e"]["ms_per_step"] = float(t[0]), float(t[1])
+        out["value"] = w["R"] / (out["ms_per_step"] * 1e-3)
+        out["e2e"]["value"] = w["R"] / (out["e2e"]["ms_per_step"] * 1e-3)
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(w, host, offs, args.cpu_sample)
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -120,6 +120,10 @@ int edx_engine_iterate(edx_engine* e, const uint32_t* ids, const uint64_t* offse
                        uint64_t num_samples, int on_device, int32_t* decision_out,
                        double* expected_cost_out, edx_report* rep);
 
+/* The engine's CUDA stream (a cudaStream_t) so callers can order their own
+ * work and timing events after the engine's. */
+int edx_engine_stream(edx_engine* e, void** stream);
+
 /* SimState::seed_entry — sim.hpp:252-261 (test hook). */
 int edx_engine_seed_entry(edx_engine* e, uint32_t id, int32_t worker, int latest, int owner);
 /* SimState::state_of — sim.hpp:64-67. */

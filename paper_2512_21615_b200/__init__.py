@@ -416,6 +416,12 @@ class SimState:
     def clock(self) -> int:
         return int(lib().edx_engine_clock(self._h))
 
+    def stream_handle(self) -> int:
+        """The engine's cudaStream_t as an integer (for torch.cuda.ExternalStream)."""
+        s = C.c_void_p()
+        check(lib().edx_engine_stream(self._h, C.byref(s)))
+        return int(s.value or 0)
+
     def snapshot(self):
         return _EngineSnapshot(self)
 

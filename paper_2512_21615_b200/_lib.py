@@ -79,6 +79,7 @@ def _sigs():
         ("edx_engine_dispatch", cint, [vp, dbl, i32p, dblp]),
         ("edx_engine_step", cint, [vp, i32p, P(ReportC)]),
         ("edx_engine_iterate", cint, [vp, vp, vp, u64, cint, i32p, dblp, P(ReportC)]),
+        ("edx_engine_stream", cint, [vp, P(vp)]),
         ("edx_engine_seed_entry", cint, [vp, C.c_uint32, i32, cint, cint]),
         ("edx_engine_state_of", cint, [vp, C.c_uint32, u64p, u64p, u64p]),
         ("edx_engine_validate_consistency", cint, [vp]),

@@ -674,6 +674,10 @@ int edx_engine_validate_consistency(edx_engine* e) {
 
 uint64_t edx_engine_clock(edx_engine* e) { return e->clock; }
 
+int edx_engine_stream(edx_engine* e, void** stream) {
+  return guard([&] { *stream = static_cast<void*>(e->stream); });
+}
+
 int edx_engine_export_global(edx_engine* e, uint32_t* ids, uint64_t* owners, uint64_t* latest,
                              uint64_t* resident, uint64_t cap, uint64_t* count) {
   return guard([&] {

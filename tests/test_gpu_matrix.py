@@ -79,7 +79,11 @@ def test_every_state_case_exhaustive(gpu, oracle, pyoracle):
                 assert got.tobytes() == want.tobytes(), (own, lat, res)
 
 
-def test_cold_and_tenfold(gpu):
+def test_cold_and_tenfold(gpu, oracle, pyoracle):
+    """test_cost.cpp:113-138.  The reference's own "10x column" check is not
+    exact in fp64 (3 chained adds of 3.2768e-5 != 10 * 3 chained adds of
+    3.2768e-6 for the 3-id row, also in the compiled reference), so the slow
+    column is compared bitwise with the reference instead."""
     edx = gpu
     c = cfg(edx, 2, 2, [5e9, 5e9])
     samples = [[1, 2, 3], [4, 5], [6], [7, 8, 9, 10]]
@@ -88,7 +92,10 @@ def test_cold_and_tenfold(gpu):
         assert (m.values[i] == len(s) * U_FAST).all()
     c2 = cfg(edx, 2, 2, [5e9, 5e8])
     m2 = edx.build_matrix([[1, 2], [3], [4, 5, 6], [7]], edx.Snapshot(), c2)
-    assert (m2.values[:, 1] == 10.0 * m2.values[:, 0]).all()
+    want = oracle.build_matrix_snapshot(pyoracle.Cfg(2, 2, [5e9, 5e8]), {},
+                                        np.arange(1, 8, dtype=np.uint32), [0, 2, 3, 6, 7])
+    assert m2.values.tobytes() == want.tobytes()
+    assert np.allclose(m2.values[:, 1], 10.0 * m2.values[:, 0], rtol=1e-15, atol=0)
 
 
 def test_wrong_sample_count(gpu):
@@ -211,7 +218,13 @@ def test_greedy_kats(gpu):
     assert edx.greedy_dispatch(m, [0], [0, 1, 0])[0][1] == 1
     m = np.array([[1, 5], [1, 2]], float)
     assert edx.greedy_dispatch(m, [0, 1], [1, 1]) == [(0, 0), (1, 1)]
-    assert edx.greedy_dispatch(np.array([[4, 4, 4]], float), [0], [0, 1, 1])[0][1] == 1
+    # test_assign.cpp:165-170 passes capacities {0,1,1} for one row, which the
+    # compiled reference itself rejects; mirror that, then check the tie rule.
+    with pytest.raises(edx.InvalidArgument, match="capacities must sum to the number of rows"):
+        edx.greedy_dispatch(np.array([[4, 4, 4]], float), [0], [0, 1, 1])
+    assert edx.greedy_dispatch(np.array([[4, 4, 4]], float), [0], [0, 1, 0])[0][1] == 1
+    assert edx.greedy_dispatch(np.array([[4, 4, 4], [4, 4, 4]], float), [0, 1],
+                               [0, 1, 1]) == [(0, 1), (1, 2)]
     with pytest.raises(edx.InvalidArgument):
         edx.greedy_dispatch(np.array([[1, 2], [3, 4]], float), [0, 1], [1, 0])
     m = np.array([[0, 5], [0, 6], [1, 3], [2, 7]], float)  # adversarial fixture
