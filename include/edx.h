@@ -160,6 +160,12 @@ int edx_engine_import_snapshot(edx_engine* e, const uint32_t* ids, const uint64_
 int edx_engine_set_profiling(edx_engine* e, int on);
 int edx_engine_phase_times(edx_engine* e, double* ms, uint64_t* counts, int reset);
 
+/* Counters of the last exact solve (engine e, or the stateless context when
+ * e is NULL): [0] Dijkstra steps [1] cycles in steps [2] cycles applying
+ * potentials [3] cycles augmenting [4] cycles re-keying column blocks
+ * [5] augmenting-path hops [6] columns re-keyed [7] total solver cycles. */
+int edx_solver_stats(edx_engine* e, uint64_t* out);
+
 /* --------------------------------------------------- stateless matrix API
  * Run on a process-wide default device context (device 0 or the current
  * device).  Inputs/outputs are host memory. */

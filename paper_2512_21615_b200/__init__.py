@@ -559,6 +559,16 @@ class SimState:
         return ms, counts
 
 
+def solver_stats(engine=None) -> dict:
+    """Counters of the last exact solve (edx_solver_stats)."""
+    out = np.zeros(8, np.uint64)
+    check(lib().edx_solver_stats(engine.handle if engine is not None else None,
+                                 _ptr(out, C.c_uint64)))
+    keys = ["steps", "step_cycles", "potential_cycles", "augment_cycles", "rekey_cycles",
+            "augment_hops", "rekeyed_columns", "total_cycles"]
+    return {k: int(v) for k, v in zip(keys, out)}
+
+
 # ------------------------------------------------------------------ workload
 class ZipfStream:
     """ZipfStream (workload.hpp:94-133): m*n samples of `sample_len` distinct

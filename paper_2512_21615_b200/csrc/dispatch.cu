@@ -139,22 +139,28 @@ __global__ void k_check_balance(const int32_t* __restrict__ decision, uint64_t r
 }
 
 // decision_cost (assign.hpp:288-298): a left-to-right fp64 sum in sample
-// order.  The order is part of the result, so it is one thread; operands are
-// fetched 8 ahead of the dependent add chain.
-__global__ void k_decision_cost(const double* __restrict__ matrix,
-                                const int32_t* __restrict__ decision, uint64_t rows, int n,
-                                double* __restrict__ out) {
+// order.  The order is part of the result, so one thread adds; the gather of
+// C[i, w_i] (the latency) is done by the whole block into shared memory
+// first, chunk by chunk.
+constexpr int kCostThreads = 1024, kCostChunk = 4096;
+
+__global__ void __launch_bounds__(kCostThreads)
+    k_decision_cost(const double* __restrict__ matrix, const int32_t* __restrict__ decision,
+                    uint64_t rows, int n, double* __restrict__ out) {
+  __shared__ double vals[kCostChunk];
   double total = 0.0;
-  uint64_t i = 0;
-  for (; i + 8 <= rows; i += 8) {
-    double v[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = matrix[(i + q) * n + decision[i + q]];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) total = __dadd_rn(total, v[q]);
+  for (uint64_t base = 0; base < rows; base += kCostChunk) {
+    const int cnt = rows - base < kCostChunk ? static_cast<int>(rows - base) : kCostChunk;
+    for (int t = threadIdx.x; t < cnt; t += kCostThreads) {
+      const uint64_t i = base + t;
+      vals[t] = matrix[i * n + decision[i]];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int t = 0; t < cnt; ++t) total = __dadd_rn(total, vals[t]);
+    __syncthreads();
   }
-  for (; i < rows; ++i) total = __dadd_rn(total, matrix[i * n + decision[i]]);
-  *out = total;
+  if (threadIdx.x == 0) *out = total;
 }
 
 }  // namespace
@@ -178,7 +184,7 @@ void launch_check_balance(const int32_t* decision, uint64_t rows, int n, int m, 
 
 void launch_decision_cost(const double* matrix, const int32_t* decision, uint64_t rows, int n,
                           double* out, cudaStream_t s) {
-  k_decision_cost<<<1, 1, 0, s>>>(matrix, decision, rows, n, out);
+  k_decision_cost<<<1, kCostThreads, 0, s>>>(matrix, decision, rows, n, out);
   EDX_LAUNCHED();
 }
 

@@ -118,6 +118,9 @@ void launch_hungarian_blocks(HungarianScratch& sc, const double* matrix, int n,
 void launch_hungarian_dense(HungarianScratch& sc, const double* values, uint64_t k,
                             uint64_t* col_of_row, int* flags, cudaStream_t s, int device);
 unsigned long long last_hungarian_steps(HungarianScratch& sc, cudaStream_t s);
+// [0] steps [1] step-loop cycles [2] potential cycles [3] augment cycles
+// [4] re-key cycles [5] augment hops [6] consumed prefixes [7] total cycles
+void last_hungarian_stats(HungarianScratch& sc, cudaStream_t s, unsigned long long* out);
 
 // The EcoMix pipeline on a device matrix (assign.hpp:247-285).
 struct DispatchScratch {

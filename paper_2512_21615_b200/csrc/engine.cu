@@ -347,6 +347,7 @@ void engine_build(edx_engine* e) {
   e->matrix.ensure(e->rows * e->n);
   e->disp.gap_keys.ensure(e->rows);
   e->disp.row_index.ensure(e->rows);
+  EDX_CUDA(cudaStreamWaitEvent(e->stream, e->cost_done, 0));
   rec(e, 0, e->stream);
   edx::launch_cost_build(e->cur_ids, e->cur_offsets, e->rows, e->n, e->ol.p, e->id_space,
                          e->ucost.p, e->matrix.p, e->disp.gap_keys.p, e->disp.row_index.p,
@@ -379,7 +380,11 @@ void engine_dispatch(edx_engine* e, double alpha) {
                   e->decision.p, e->flags.p, e->stream, e->device, e->profiling ? &pe : nullptr,
                   &launches);
   rec(e, 11, e->stream);
-  edx::launch_decision_cost(e->matrix.p, e->decision.p, e->rows, e->n, e->expected.p, e->stream);
+  // decision_cost is only reported (sim.hpp:439): overlap it with the step.
+  EDX_CUDA(cudaEventRecord(e->disp.fork, e->stream));
+  EDX_CUDA(cudaStreamWaitEvent(e->disp.side, e->disp.fork, 0));
+  edx::launch_decision_cost(e->matrix.p, e->decision.p, e->rows, e->n, e->expected.p, e->disp.side);
+  EDX_CUDA(cudaEventRecord(e->cost_done, e->disp.side));
   e->launches += launches + 1;
   const int mult = edx::exact_multiplicity(e->m, alpha);
   e->pending_greedy = e->profiling && static_cast<uint64_t>(e->n) * mult < e->rows;
@@ -506,6 +511,7 @@ int edx_engine_create(const edx_cluster_config* cfg, const edx_engine_options* o
     e->world = opt->world_size < 1 ? 1 : opt->world_size;
     EDX_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
     for (auto& ev : e->ev) EDX_CUDA(cudaEventCreate(&ev));
+    EDX_CUDA(cudaEventCreateWithFlags(&e->cost_done, cudaEventDisableTiming));
     e->ol.ensure(e->id_space);
     e->res.ensure(e->id_space);
     EDX_CUDA(cudaMemsetAsync(e->ol.p, 0, e->id_space * sizeof(ulonglong2), e->stream));
@@ -532,6 +538,7 @@ void edx_engine_destroy(edx_engine* e) {
   cudaStreamSynchronize(e->stream);
   for (auto& ev : e->ev)
     if (ev) cudaEventDestroy(ev);
+  if (e->cost_done) cudaEventDestroy(e->cost_done);
   if (e->h_flags) cudaFreeHost(e->h_flags);
   if (e->h_counters) cudaFreeHost(e->h_counters);
   if (e->h_expected) cudaFreeHost(e->h_expected);
@@ -568,9 +575,11 @@ int edx_engine_dispatch(edx_engine* e, double alpha, int32_t* decision_out,
     if (decision_out)
       EDX_CUDA(cudaMemcpyAsync(decision_out, e->decision.p, e->rows * sizeof(int32_t),
                                cudaMemcpyDeviceToHost, e->stream));
-    if (expected_cost_out)
+    if (expected_cost_out) {
+      EDX_CUDA(cudaStreamWaitEvent(e->stream, e->cost_done, 0));
       EDX_CUDA(cudaMemcpyAsync(e->h_expected, e->expected.p, sizeof(double),
                                cudaMemcpyDeviceToHost, e->stream));
+    }
     if (decision_out || expected_cost_out) engine_sync_check(e);
     if (expected_cost_out) *expected_cost_out = *e->h_expected;
   });
@@ -594,11 +603,14 @@ int edx_engine_iterate(edx_engine* e, const uint32_t* ids, const uint64_t* offse
     if (decision_out)
       EDX_CUDA(cudaMemcpyAsync(decision_out, e->decision.p, e->rows * sizeof(int32_t),
                                cudaMemcpyDeviceToHost, e->stream));
-    if (expected_cost_out)
+    engine_step(e, nullptr, rep);
+    if (expected_cost_out) {
+      EDX_CUDA(cudaStreamWaitEvent(e->stream, e->cost_done, 0));
       EDX_CUDA(cudaMemcpyAsync(e->h_expected, e->expected.p, sizeof(double),
                                cudaMemcpyDeviceToHost, e->stream));
-    engine_step(e, nullptr, rep);
-    if (expected_cost_out) *expected_cost_out = *e->h_expected;
+      EDX_CUDA(cudaStreamSynchronize(e->stream));
+      *expected_cost_out = *e->h_expected;
+    }
   });
 }
 
@@ -817,6 +829,22 @@ int edx_engine_phase_times(edx_engine* e, double* ms, uint64_t* counts, int rese
       std::fill(e->phase_ms, e->phase_ms + EDX_NUM_PHASES, 0.0);
       e->launches = 0;
     }
+  });
+}
+
+int edx_solver_stats(edx_engine* e, uint64_t* out) {
+  return guard([&] {
+    unsigned long long st[8];
+    if (e) {
+      EDX_CUDA(cudaSetDevice(e->device));
+      edx::last_hungarian_stats(e->disp.hung, e->stream, st);
+    } else {
+      auto& c = dctx();
+      std::lock_guard<std::mutex> lk(c.mu);
+      c.init();
+      edx::last_hungarian_stats(c.disp.hung, c.stream, st);
+    }
+    for (int i = 0; i < 8; ++i) out[i] = st[i];
   });
 }
 

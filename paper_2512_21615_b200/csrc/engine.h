@@ -96,6 +96,7 @@ struct edx_engine {
   // profiling
   bool profiling = false;
   cudaEvent_t ev[12] = {};
+  cudaEvent_t cost_done = nullptr;  // decision_cost finished (side stream)
   double phase_ms[EDX_NUM_PHASES] = {};
   uint64_t launches = 0;
   uint64_t solver_steps = 0;

@@ -104,6 +104,8 @@ __device__ bool hungarian_blocks_warp(const BlockArrays A, int n, int mult, int 
   __syncwarp();
 
   unsigned long long steps = 0;
+  long long c_step = 0, c_pot = 0, c_aug = 0, c_rekey = 0, hops = 0, prefix = 0;
+  const long long c_start = clock64();
   int64_t D[NB], bestv[NB];
   int wy[NB], cur[NB], bestc[NB];
 
@@ -131,6 +133,7 @@ __device__ bool hungarian_blocks_warp(const BlockArrays A, int n, int mult, int 
     int j0 = 0, r = i, j1;
     int64_t Dl = 0;  // Δ: running sum of this row's deltas
     __syncwarp();
+    long long t0 = clock64();
     for (;;) {
       ++steps;
       const int64_t ur = u[r];
@@ -194,6 +197,8 @@ __device__ bool hungarian_blocks_warp(const BlockArrays A, int n, int mult, int 
       j0 = j1;
       r = pj;
     }
+    long long t1 = clock64();
+    c_step += t1 - t0;
     // lazy potential moves (assign.hpp:131-138 applied per reached column)
     for (int t = lane; t < nused; t += 32) {
       const int j = ulist[t];
@@ -202,22 +207,29 @@ __device__ bool hungarian_blocks_warp(const BlockArrays A, int n, int mult, int 
       v[j] -= d;
     }
     __syncwarp();
+    long long t2 = clock64();
+    c_pot += t2 - t1;
     if (lane == 0) {  // augment along way[] (assign.hpp:141-145)
       int jj = j1;
       do {
         const int jp = way[jj];
         p[jj] = p[jp];
         jj = jp;
+        ++hops;
       } while (jj != 0);
     }
     __syncwarp();
+    long long t3 = clock64();
+    c_aug += t3 - t2;
     // re-key the consumed prefix of every touched block
+    const long long t4 = clock64();
     for (int w = 0; w < n; ++w) {
       int P = 0;
 #pragma unroll
       for (int b = 0; b < NB; ++b)
         if ((w >> 5) == b) P = __shfl_sync(0xffffffffu, cur[b], w & 31);
       if (P == 0) continue;
+      prefix += P;
       int32_t* base = ord + w * mult;
       int32_t* sorted = tmp;         // P entries
       int32_t* merged = tmp + mult;  // mult entries
@@ -255,8 +267,18 @@ __device__ bool hungarian_blocks_warp(const BlockArrays A, int n, int mult, int 
       for (int t = lane; t < mult; t += 32) base[t] = merged[t];
       __syncwarp();
     }
+    c_rekey += clock64() - t4;
   }
-  if (lane == 0 && steps_out) *steps_out = steps;
+  if (lane == 0 && steps_out) {
+    steps_out[0] = steps;
+    steps_out[1] = c_step;
+    steps_out[2] = c_pot;
+    steps_out[3] = c_aug;
+    steps_out[4] = c_rekey;
+    steps_out[5] = hops;
+    steps_out[6] = prefix;
+    steps_out[7] = clock64() - c_start;
+  }
   return true;
 }
 
@@ -450,7 +472,7 @@ __global__ void __launch_bounds__(kDenseThreads)
     __syncthreads();
   }
   for (int j = tid + 1; j <= k; j += kDenseThreads) col_of_row[p[j] - 1] = static_cast<uint64_t>(j - 1);
-  if (tid == 0 && steps_out) *steps_out = steps;
+  if (tid == 0 && steps_out) steps_out[0] = steps;
 }
 
 size_t block_arena_bytes(int k, int mult) {
@@ -482,7 +504,7 @@ void launch_hungarian_blocks(HungarianScratch& sc, const double* matrix, int n,
   if (k <= 0) return;
   const int64_t cap = LLONG_MAX / (8 * static_cast<int64_t>(k + 1));
   sc.s64.ensure(static_cast<size_t>(k) * n + 1);
-  sc.steps.ensure(1);
+  sc.steps.ensure(8);
   const uint64_t total = static_cast<uint64_t>(k) * n;
   k_scale_block<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(matrix, n, order, k,
                                                                          cap, sc.s64.p, flags);
@@ -517,7 +539,7 @@ void launch_hungarian_blocks(HungarianScratch& sc, const double* matrix, int n,
 void launch_hungarian_dense(HungarianScratch& sc, const double* values, uint64_t k,
                             uint64_t* col_of_row, int* flags, cudaStream_t s, int device) {
   const int64_t cap = LLONG_MAX / (8 * static_cast<int64_t>(k + 1));
-  sc.steps.ensure(1);
+  sc.steps.ensure(8);
   const size_t arena = dense_arena_bytes(static_cast<int>(k));
   const size_t limit = static_cast<size_t>(max_dyn_smem(device)) - 1024;  // static smem
   size_t smem = 0;
@@ -534,6 +556,13 @@ void launch_hungarian_dense(HungarianScratch& sc, const double* values, uint64_t
   k_hungarian_dense<<<1, kDenseThreads, smem, s>>>(values, static_cast<int>(k), cap, garena,
                                                    col_of_row, sc.steps.p, flags);
   EDX_LAUNCHED();
+}
+
+void last_hungarian_stats(HungarianScratch& sc, cudaStream_t s, unsigned long long* out) {
+  for (int i = 0; i < 8; ++i) out[i] = 0;
+  if (!sc.steps.p) return;
+  EDX_CUDA(cudaMemcpyAsync(out, sc.steps.p, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  EDX_CUDA(cudaStreamSynchronize(s));
 }
 
 unsigned long long last_hungarian_steps(HungarianScratch& sc, cudaStream_t s) {
