@@ -29,7 +29,9 @@
 // K6 runs on ONE warp of one SM: lane w owns block w (n <= 64, two blocks per
 // lane above 32).  It is latency-bound by construction (one dependent
 // Dijkstra step after another); state lives in shared memory when it fits.
+#include <algorithm>
 #include <climits>
+#include <cmath>
 
 #include "edx_internal.cuh"
 
@@ -59,13 +61,23 @@ __device__ __forceinline__ bool bad_cost(double x) { return !isfinite(x) || x < 
 // S[r][w] = scaled cost of block row r (matrix row order[r]) for worker w.
 __global__ void k_scale_block(const double* __restrict__ matrix, int n,
                               const uint32_t* __restrict__ order, uint64_t k, int64_t cap,
-                              int64_t* __restrict__ S, int* __restrict__ flags) {
+                              int64_t* __restrict__ S, int* __restrict__ flags,
+                              unsigned long long* __restrict__ max_scaled) {
   const uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  if (x >= k * n) return;
-  const uint64_t r = x / n, w = x - r * n;
-  const double v = matrix[static_cast<uint64_t>(order[r]) * n + w];
-  if (bad_cost(v)) atomicOr(flags + kFlagBadCost, 1);
-  S[x] = scale_cost(v, cap);
+  unsigned long long sv = 0;
+  if (x < k * n) {
+    const uint64_t r = x / n, w = x - r * n;
+    const double v = matrix[static_cast<uint64_t>(order[r]) * n + w];
+    if (bad_cost(v)) atomicOr(flags + kFlagBadCost, 1);
+    const int64_t sc = scale_cost(v, cap);
+    S[x] = sc;
+    sv = sc < 0 ? ~0ULL : static_cast<unsigned long long>(sc);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long ov = __shfl_xor_sync(0xffffffffu, sv, o);
+    sv = ov > sv ? ov : sv;
+  }
+  if ((threadIdx.x & 31) == 0 && sv) atomicMax(max_scaled, sv);
 }
 
 struct BlockArrays {
@@ -284,7 +296,7 @@ __device__ bool hungarian_blocks_warp(const BlockArrays A, int n, int mult, int 
 
 template <int NB>
 __global__ void __launch_bounds__(32)
-    k_hungarian_blocks(const int64_t* __restrict__ S_global, int n, int mult, int k,
+    k_hungarian_blocks_wide(const int64_t* __restrict__ S_global, int n, int mult, int k,
                        int s_in_smem, uint8_t* __restrict__ arena,
                        const uint32_t* __restrict__ order, int32_t* __restrict__ decision,
                        const uint32_t* __restrict__ row_ids, uint64_t* __restrict__ col_of_row,
@@ -334,6 +346,344 @@ __global__ void __launch_bounds__(32)
       const uint32_t row = order[r];
       decision[row_ids ? row_ids[row] : row] = (j - 1) / mult;
     }
+  }
+}
+
+// ------------------------------------------------------ K6 fast (packed keys)
+// Same algorithm as k_hungarian_blocks_wide, organised for the latency of one
+// Dijkstra step on a B200 SM (measured: LDS 29 cycles, SHFL 26, REDUX 22):
+//  * every array is addressed through __shared__ (LDS/STS, no generic loads);
+//  * a block's minv key is packed as (minv << 6 | w) and the warp argmin is
+//    two redux.sync.min.u32 (high word, then low word among the minima); the
+//    block index in the low bits makes the lowest block win ties, i.e. the
+//    lowest column (blocks are index-ordered);
+//  * E_w = D_w - Δ is kept pre-shifted, so a step's relax is
+//    E_w = min(E_w - delta, A_w(r)) with A_w(r) = (S[r][w] - u[r]) << 6
+//    staged in shared memory for every block's current candidate row;
+//    the only load on the step's critical path is the winner's A;
+//  * `way` is recorded as the index (in the row's list of reached columns)
+//    of the column whose row last improved the block, so no shuffle is
+//    needed to broadcast it;
+//  * at the end of a row, potentials and the (v desc, j asc) re-keying of
+//    every touched block run on all warps (one block per warp) while one
+//    thread augments.
+// Packing needs 0 <= minv < 2^57; the launcher checks the cost range and
+// falls back to the wide kernel otherwise.
+constexpr int kFastMaxWarps = 16;
+
+template <int NB, int MODE>  // MODE 0: S + arrays shared; 1: S global; 2: S + arrays global
+__global__ void __launch_bounds__(kFastMaxWarps * 32, 1)
+    k_hungarian_blocks_fast(const int64_t* __restrict__ S_global, int n, int mult, int k,
+                            uint8_t* __restrict__ arena, const uint32_t* __restrict__ order,
+                            int32_t* __restrict__ decision, const uint32_t* __restrict__ row_ids,
+                            uint64_t* __restrict__ col_of_row, unsigned long long* stats,
+                            int* flags, const unsigned long long* __restrict__ max_scaled) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  constexpr int W = 32 * NB;
+  // Packed keys need minv < 2^57; reduced costs stay below (k+1) * max cost
+  // (the reference's own overflow budget, assign.hpp:93-94).
+  const unsigned long long mx = *max_scaled;
+  const bool packable = mx < (1ULL << 57) / (8ULL * static_cast<unsigned long long>(k + 1));  // row stride of the A staging
+  const size_t K1 = static_cast<size_t>(k) + 1;
+  size_t so = 0, go = 0;
+  auto stake = [&](size_t bytes) {
+    uint8_t* q = smem + so;
+    so += (bytes + 15) & ~size_t(15);
+    return q;
+  };
+  auto gtake = [&](size_t bytes) {
+    uint8_t* q = arena + go;
+    go += (bytes + 15) & ~size_t(15);
+    return q;
+  };
+  const int64_t* S;
+  int64_t *u, *v, *dlt;
+  int32_t *p, *way, *ulist, *ord;
+  if constexpr (MODE == 0) {
+    int64_t* Ss = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(k) * n * 8));
+    const size_t total = static_cast<size_t>(k) * n;
+    for (size_t x = tid; x < total; x += blockDim.x) Ss[x] = S_global[x];
+    S = Ss;
+  } else {
+    S = S_global;
+  }
+  if constexpr (MODE <= 1) {
+    u = reinterpret_cast<int64_t*>(stake(K1 * 8));
+    v = reinterpret_cast<int64_t*>(stake(K1 * 8));
+    dlt = reinterpret_cast<int64_t*>(stake(K1 * 8));
+    p = reinterpret_cast<int32_t*>(stake(K1 * 4));
+    way = reinterpret_cast<int32_t*>(stake(K1 * 4));
+    ulist = reinterpret_cast<int32_t*>(stake(K1 * 4));
+    ord = reinterpret_cast<int32_t*>(stake(static_cast<size_t>(k) * 4));
+  } else {
+    u = reinterpret_cast<int64_t*>(gtake(K1 * 8));
+    v = reinterpret_cast<int64_t*>(gtake(K1 * 8));
+    dlt = reinterpret_cast<int64_t*>(gtake(K1 * 8));
+    p = reinterpret_cast<int32_t*>(gtake(K1 * 4));
+    way = reinterpret_cast<int32_t*>(gtake(K1 * 4));
+    ulist = reinterpret_cast<int32_t*>(gtake(K1 * 4));
+    ord = reinterpret_cast<int32_t*>(gtake(static_cast<size_t>(k) * 4));
+  }
+  int64_t* A6 = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(n) * W * 8));
+  int32_t* cand_r = reinterpret_cast<int32_t*>(stake(64 * 4));
+  int32_t* cur_s = reinterpret_cast<int32_t*>(stake(64 * 4));
+  int64_t* scal = reinterpret_cast<int64_t*>(stake(4 * 8));  // Dl, nused, abort
+  int64_t* rk_v = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(nw) * mult * 8));
+  int32_t* rk_i = reinterpret_cast<int32_t*>(stake(static_cast<size_t>(nw) * 2 * mult * 4));
+
+  for (size_t x = tid; x < K1; x += blockDim.x) {
+    u[x] = 0;
+    v[x] = 0;
+    p[x] = 0;
+    way[x] = 0;
+  }
+  for (int x = tid; x < k; x += blockDim.x) ord[x] = x + 1;  // all v = 0: index order
+  if (tid == 0) scal[2] = 0;
+  __syncthreads();
+
+  if (!packable) {  // wide-range path: the 64-bit (value, index) shuffle argmin
+    if (warp == 0) {
+      BlockArrays A{S, u, v, dlt, p, way, ulist, ord, rk_i};
+      if (!hungarian_blocks_warp<NB>(A, n, mult, k, stats, flags)) return;
+      __syncwarp();
+      for (int j = lane + 1; j <= k; j += 32) {
+        const int r = p[j] - 1;
+        if (col_of_row) col_of_row[r] = static_cast<uint64_t>(j - 1);
+        if (decision) {
+          const uint32_t row = order[r];
+          decision[row_ids ? row_ids[row] : row] = (j - 1) / mult;
+        }
+      }
+    }
+    return;
+  }
+
+  unsigned long long steps = 0;
+  long long c_step = 0, c_end = 0, rekeyed = 0;
+  const long long c_start = clock64();
+  for (int i = 1; i <= k; ++i) {
+    const long long t0 = clock64();
+    if (warp == 0) {
+      int64_t E6[NB], B[NB];
+      int wyi[NB], cur[NB], bestc[NB];
+      const int64_t ui = u[i];
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const int w = lane + 32 * b;
+        cur[b] = 0;
+        wyi[b] = 0;
+        E6[b] = 0;
+        B[b] = 0;
+        bestc[b] = 0;
+        if (w < n) {
+          const int c = ord[w * mult];
+          bestc[b] = c;
+          B[b] = static_cast<int64_t>(w) - (v[c] << 6);
+          cand_r[w] = p[c];
+          // relax from row i (reached through the virtual column 0, Δ = 0)
+          E6[b] = (S[static_cast<size_t>(i - 1) * n + w] - ui) << 6;
+        }
+      }
+      if (lane == 0) {
+        p[0] = i;
+        ulist[0] = 0;
+        dlt[0] = 0;
+      }
+      __syncwarp();
+      for (int x = 0; x < n; ++x) {  // stage every block's candidate row
+        const int r = cand_r[x];
+        if (r > 0) {
+          const int64_t ur = u[r];
+#pragma unroll
+          for (int b = 0; b < NB; ++b) {
+            const int w = lane + 32 * b;
+            if (w < n) A6[x * W + w] = (S[static_cast<size_t>(r - 1) * n + w] - ur) << 6;
+          }
+        }
+      }
+      int nused = 1, pw = -1;
+      int64_t Dl = 0;
+      bool abort = false;
+      for (;;) {
+        ++steps;
+        if (pw >= 0) {  // the previous winner block moved to a new candidate: restage it
+          const int r = cand_r[pw];
+          if (r > 0) {
+            const int64_t ur = u[r];
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+              const int w = lane + 32 * b;
+              if (w < n) A6[pw * W + w] = (S[static_cast<size_t>(r - 1) * n + w] - ur) << 6;
+            }
+          }
+        }
+        uint64_t key = ~0ULL;
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          const int w = lane + 32 * b;
+          if (w < n && cur[b] < mult) {
+            const uint64_t kb = static_cast<uint64_t>(E6[b] + B[b]);
+            key = kb < key ? kb : key;
+          }
+        }
+        const unsigned hi = static_cast<unsigned>(key >> 32), lo = static_cast<unsigned>(key);
+        const unsigned mh = __reduce_min_sync(0xffffffffu, hi);
+        const unsigned ml = __reduce_min_sync(0xffffffffu, hi == mh ? lo : 0xffffffffu);
+        const uint64_t kmin = (static_cast<uint64_t>(mh) << 32) | ml;
+        if (kmin == ~0ULL) {  // no unused column: only reachable on corrupt input
+          abort = true;
+          break;
+        }
+        const int ws = static_cast<int>(ml & 63u);
+        const int64_t delta6 = static_cast<int64_t>(kmin & ~63ULL);
+        Dl += delta6 >> 6;
+        const int r = cand_r[ws];
+        int64_t a[NB];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) a[b] = A6[ws * W + lane + 32 * b];
+        __syncwarp();  // cand_r[ws] read by all lanes before its owner moves on
+        const int owner = ws & 31, ob = ws >> 5;
+        if (lane == owner) {
+#pragma unroll
+          for (int b = 0; b < NB; ++b) {
+            if (b != ob) continue;
+            const int j1 = bestc[b];
+            way[j1] = ulist[wyi[b]];
+            dlt[j1] = Dl;
+            ulist[nused] = j1;
+            if (++cur[b] < mult) {
+              const int c = ord[ws * mult + cur[b]];
+              bestc[b] = c;
+              B[b] = static_cast<int64_t>(ws) - (v[c] << 6);
+              cand_r[ws] = p[c];
+            }
+          }
+        }
+        const int s_cur = nused++;
+        if (r == 0) break;  // a free column: the augmenting path ends here
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {  // relax from row r (assign.hpp:119-125)
+          const int64_t t = E6[b] - delta6;
+          if (a[b] < t) {
+            E6[b] = a[b];
+            wyi[b] = s_cur;
+          } else {
+            E6[b] = t;
+          }
+        }
+        __syncwarp();
+        pw = ws;
+      }
+      if (lane == 0) {
+        scal[0] = Dl;
+        scal[1] = nused;
+        if (abort) scal[2] = 1;
+      }
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const int w = lane + 32 * b;
+        if (w < n) cur_s[w] = cur[b];
+      }
+    }
+    __syncthreads();
+    const long long t1 = clock64();
+    c_step += t1 - t0;
+    if (scal[2]) {
+      if (tid == 0) atomicOr(flags + kFlagBadCost, 1);
+      return;
+    }
+    const int64_t Dl = scal[0];
+    const int nu = static_cast<int>(scal[1]);
+    for (int t = tid; t < nu; t += blockDim.x) {  // potentials (assign.hpp:131-138), lazily
+      const int j = ulist[t];
+      const int64_t d = Dl - dlt[j];
+      u[p[j]] += d;
+      v[j] -= d;
+    }
+    __syncthreads();
+    if (tid == 0) {  // augment (assign.hpp:141-145)
+      int jj = ulist[nu - 1];
+      do {
+        const int jp = way[jj];
+        p[jj] = p[jp];
+        jj = jp;
+      } while (jj != 0);
+    }
+    // re-key each touched block's consumed prefix (v changed), one block per warp
+    for (int w = warp; w < n; w += nw) {
+      const int P = cur_s[w];
+      if (P == 0) continue;
+      if (lane == 0) rekeyed += P;
+      int32_t* base = ord + w * mult;
+      int64_t* pv = rk_v + static_cast<size_t>(warp) * mult;
+      int32_t* sorted = rk_i + static_cast<size_t>(warp) * 2 * mult;
+      int32_t* merged = sorted + mult;
+      for (int t = lane; t < P; t += 32) pv[t] = v[base[t]];
+      __syncwarp();
+      for (int t = lane; t < P; t += 32) {
+        const int a = base[t];
+        const int64_t va = pv[t];
+        int rank = 0;
+        for (int s2 = 0; s2 < P; ++s2) {
+          const int64_t vb = pv[s2];
+          rank += (vb > va || (vb == va && base[s2] < a)) ? 1 : 0;
+        }
+        sorted[rank] = a;
+      }
+      __syncwarp();
+      const int Q = mult - P;
+      const int32_t* suf = base + P;
+      for (int t = lane; t < P; t += 32) {
+        const int a = sorted[t];
+        const int64_t va = v[a];
+        int lo2 = 0, hi2 = Q;  // suffix entries ordered before a
+        while (lo2 < hi2) {
+          const int mid = (lo2 + hi2) >> 1;
+          const int b2 = suf[mid];
+          const int64_t vb = v[b2];
+          if (vb > va || (vb == va && b2 < a)) lo2 = mid + 1;
+          else hi2 = mid;
+        }
+        merged[t + lo2] = a;
+      }
+      for (int t = lane; t < Q; t += 32) {
+        const int b2 = suf[t];
+        const int64_t vb = v[b2];
+        int lo2 = 0, hi2 = P;  // prefix entries ordered before b2
+        while (lo2 < hi2) {
+          const int mid = (lo2 + hi2) >> 1;
+          const int a = sorted[mid];
+          const int64_t va = v[a];
+          if (va > vb || (va == vb && a < b2)) lo2 = mid + 1;
+          else hi2 = mid;
+        }
+        merged[t + lo2] = b2;
+      }
+      __syncwarp();
+      for (int t = lane; t < mult; t += 32) base[t] = merged[t];
+      __syncwarp();
+    }
+    __syncthreads();
+    c_end += clock64() - t1;
+  }
+  for (int j = tid + 1; j <= k; j += blockDim.x) {
+    const int r = p[j] - 1;
+    if (col_of_row) col_of_row[r] = static_cast<uint64_t>(j - 1);
+    if (decision) {
+      const uint32_t row = order[r];
+      decision[row_ids ? row_ids[row] : row] = (j - 1) / mult;
+    }
+  }
+  if (tid == 0 && stats) {
+    stats[0] = steps;
+    stats[1] = c_step;
+    stats[2] = c_end;
+    stats[3] = 0;
+    stats[4] = 0;
+    stats[5] = 0;
+    stats[6] = rekeyed;
+    stats[7] = clock64() - c_start;
   }
 }
 
@@ -496,6 +846,18 @@ int max_dyn_smem(int device) {
 
 }  // namespace
 
+size_t fast_smem_bytes(int k, int n, int mult, int nw, int mode) {
+  const size_t K1 = static_cast<size_t>(k) + 1;
+  auto r = [](size_t b) { return (b + 15) & ~size_t(15); };
+  size_t b = 0;
+  if (mode == 0) b += r(static_cast<size_t>(k) * n * 8);
+  if (mode <= 1) b += 3 * r(K1 * 8) + 3 * r(K1 * 4) + r(static_cast<size_t>(k) * 4);
+  const int W = n <= 32 ? 32 : 64;
+  b += r(static_cast<size_t>(n) * W * 8) + 2 * r(64 * 4) + r(32) +
+       r(static_cast<size_t>(nw) * mult * 8) + r(static_cast<size_t>(nw) * 2 * mult * 4);
+  return b;
+}
+
 void launch_hungarian_blocks(HungarianScratch& sc, const double* matrix, int n,
                              const uint32_t* order, int mult, int32_t* decision,
                              const uint32_t* row_ids, uint64_t* col_of_row, int* flags,
@@ -504,35 +866,49 @@ void launch_hungarian_blocks(HungarianScratch& sc, const double* matrix, int n,
   if (k <= 0) return;
   const int64_t cap = LLONG_MAX / (8 * static_cast<int64_t>(k + 1));
   sc.s64.ensure(static_cast<size_t>(k) * n + 1);
-  sc.steps.ensure(8);
+  sc.steps.ensure(9);
+  unsigned long long* max_scaled = sc.steps.p + 8;
+  EDX_CUDA(cudaMemsetAsync(max_scaled, 0, sizeof(unsigned long long), s));
   const uint64_t total = static_cast<uint64_t>(k) * n;
-  k_scale_block<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(matrix, n, order, k,
-                                                                         cap, sc.s64.p, flags);
+  k_scale_block<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(
+      matrix, n, order, k, cap, sc.s64.p, flags, max_scaled);
   EDX_LAUNCHED();
-  const size_t arena = block_arena_bytes(k, mult);
-  const size_t s_bytes = static_cast<size_t>(k) * n * sizeof(int64_t);
   const size_t limit = static_cast<size_t>(max_dyn_smem(device));
-  int s_in_smem = 0;
-  size_t smem = 0;
-  uint8_t* garena = nullptr;
-  if (s_bytes + arena <= limit) {
-    s_in_smem = 1;
-    smem = s_bytes + arena;
-  } else if (arena <= limit) {
-    smem = arena;
-  } else {
-    sc.arena.ensure(arena);
-    garena = sc.arena.p;
+  const int nw = std::min(n, kFastMaxWarps);
+  int mode = -1;
+  for (int md = 0; md <= 2 && mode < 0; ++md)
+    if (fast_smem_bytes(k, n, mult, nw, md) <= limit) mode = md;
+  if (mode >= 0) {
+    const size_t smem = fast_smem_bytes(k, n, mult, nw, mode);
+    uint8_t* garena = nullptr;
+    if (mode == 2) {
+      sc.arena.ensure(block_arena_bytes(k, mult));
+      garena = sc.arena.p;
+    }
+    auto launch = [&](auto kern) {
+      if (smem > 48 * 1024)
+        EDX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+      kern<<<1, 32 * nw, smem, s>>>(sc.s64.p, n, mult, k, garena, order, decision, row_ids,
+                                    col_of_row, sc.steps.p, flags, max_scaled);
+    };
+    if (n <= 32) {
+      if (mode == 0) launch(k_hungarian_blocks_fast<1, 0>);
+      else if (mode == 1) launch(k_hungarian_blocks_fast<1, 1>);
+      else launch(k_hungarian_blocks_fast<1, 2>);
+    } else {
+      if (mode == 0) launch(k_hungarian_blocks_fast<2, 0>);
+      else if (mode == 1) launch(k_hungarian_blocks_fast<2, 1>);
+      else launch(k_hungarian_blocks_fast<2, 2>);
+    }
+    EDX_LAUNCHED();
+    return;
   }
-  auto launch = [&](auto kern) {
-    if (smem > 48 * 1024)
-      EDX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem)));
-    kern<<<1, 32, smem, s>>>(sc.s64.p, n, mult, k, s_in_smem, garena, order, decision, row_ids,
-                             col_of_row, sc.steps.p, flags);
-  };
-  if (n <= 32) launch(k_hungarian_blocks<1>);
-  else launch(k_hungarian_blocks<2>);
+  // only for very large blocks: the single-warp kernel with global arrays
+  const size_t arena = block_arena_bytes(k, mult);
+  sc.arena.ensure(arena);
+  k_hungarian_blocks_wide<2><<<1, 32, 0, s>>>(sc.s64.p, n, mult, k, 0, sc.arena.p, order, decision,
+                                              row_ids, col_of_row, sc.steps.p, flags);
   EDX_LAUNCHED();
 }
 

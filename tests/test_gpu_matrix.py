@@ -194,14 +194,19 @@ def test_hungarian_bench_matrix(gpu, oracle, k):
     assert (got.col_of_row == cols).all() and got.total_cost == total
 
 
-@pytest.mark.parametrize("n,mult,maxv", [(2, 3, 100), (4, 8, 3), (8, 16, 1000), (8, 32, 5),
-                                         (16, 16, 50), (33, 4, 20), (64, 2, 7), (8, 64, 1000)])
-def test_hungarian_blocks_equals_expanded(gpu, oracle, n, mult, maxv):
+@pytest.mark.parametrize("n,mult,maxv,scale", [(2, 3, 100, 3.2768e-6), (4, 8, 3, 3.2768e-6),
+                                               (8, 16, 1000, 3.2768e-6), (8, 32, 5, 3.2768e-6),
+                                               (16, 16, 50, 3.2768e-6), (33, 4, 20, 3.2768e-6),
+                                               (64, 2, 7, 3.2768e-6), (8, 64, 1000, 3.2768e-6),
+                                               (40, 8, 9, 3.2768e-6), (32, 32, 100, 3.2768e-6),
+                                               # magnitudes beyond the packed-key range: wide path
+                                               (8, 16, 1000, 4.0), (40, 4, 50, 100.0)])
+def test_hungarian_blocks_equals_expanded(gpu, oracle, n, mult, maxv, scale):
     """The collapsed solver == hungarian(expand_columns(...)), column for column."""
     edx = gpu
     for seed in range(3):
         rows = n * mult * 2
-        m = random_int_matrix(rows, n, 7 * n + mult + seed, maxv) * 3.2768e-6
+        m = random_int_matrix(rows, n, 7 * n + mult + seed, maxv) * scale
         order = oracle.rows_by_gap(m)
         block = order[: n * mult]
         got = edx.hungarian_blocks(m, block, mult)
