@@ -687,6 +687,322 @@ __global__ void __launch_bounds__(kFastMaxWarps * 32, 1)
   }
 }
 
+// --------------------------------------------- K6 tabled (per-row operand table)
+// Fastest variant, used when the operand table fits in shared memory.  At the
+// start of each row (phase) all warps rebuild, for every block x and every
+// position d of its (v desc, j asc) column order,
+//     A[x][d][w] = (S[r][w] - u[r]) << 6,  r = p[ord[x][d]]   (relax operand)
+//     Btab[x][d] = x - (v[ord[x][d]] << 6)                    (key offset)
+//     rtab[x][d] = r                                          (0 = free column)
+// so that during the row a Dijkstra step only needs: key = E + B -> two
+// redux.sync.min.u32 -> one LDS of A[winner][cursor][lane] -> relax.  The
+// winner's bookkeeping uses values prefetched one consumption ahead, and the
+// per-block cursors are packed 8 bits each in one uniform register (n <= 8)
+// or kept in shared memory.  `way` is recorded as a step index (see the
+// fast kernel).  Row end is the same as the fast kernel.
+template <int NB, int SMODE, bool PACK>  // SMODE 0: S shared, 1: S global
+__global__ void __launch_bounds__(kFastMaxWarps * 32, 1)
+    k_hungarian_blocks_tab(const int64_t* __restrict__ S_global, int n, int mult, int k,
+                           const uint32_t* __restrict__ order, int32_t* __restrict__ decision,
+                           const uint32_t* __restrict__ row_ids, uint64_t* __restrict__ col_of_row,
+                           unsigned long long* stats, int* flags,
+                           const unsigned long long* __restrict__ max_scaled) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const size_t K1 = static_cast<size_t>(k) + 1;
+  size_t so = 0;
+  auto stake = [&](size_t bytes) {
+    uint8_t* q = smem + so;
+    so += (bytes + 15) & ~size_t(15);
+    return q;
+  };
+  const int64_t* S;
+  if constexpr (SMODE == 0) {
+    int64_t* Ss = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(k) * n * 8));
+    for (size_t x = tid; x < static_cast<size_t>(k) * n; x += blockDim.x) Ss[x] = S_global[x];
+    S = Ss;
+  } else {
+    S = S_global;
+  }
+  int64_t* A = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(k) * n * 8));
+  int64_t* Btab = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(k) * 8));
+  int64_t* u = reinterpret_cast<int64_t*>(stake(K1 * 8));
+  int64_t* v = reinterpret_cast<int64_t*>(stake(K1 * 8));
+  int64_t* dlt = reinterpret_cast<int64_t*>(stake(K1 * 8));
+  int32_t* p = reinterpret_cast<int32_t*>(stake(K1 * 4));
+  int32_t* wayi = reinterpret_cast<int32_t*>(stake(K1 * 4));
+  int32_t* ulist = reinterpret_cast<int32_t*>(stake(K1 * 4));
+  int32_t* ord = reinterpret_cast<int32_t*>(stake(K1 * 4));
+  int32_t* rtab = reinterpret_cast<int32_t*>(stake(K1 * 4));
+  int32_t* curs = reinterpret_cast<int32_t*>(stake(64 * 4));
+  int64_t* scal = reinterpret_cast<int64_t*>(stake(4 * 8));
+  int64_t* rk_v = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(nw) * mult * 8));
+  int32_t* rk_i = reinterpret_cast<int32_t*>(stake(static_cast<size_t>(nw) * 2 * mult * 4));
+
+  const unsigned long long mx = *max_scaled;
+  const bool packable = mx < (1ULL << 57) / (8ULL * static_cast<unsigned long long>(k + 1));
+  for (size_t x = tid; x < K1; x += blockDim.x) {
+    u[x] = 0;
+    v[x] = 0;
+    p[x] = 0;
+    wayi[x] = 0;
+  }
+  for (int x = tid; x < k; x += blockDim.x) ord[x] = x + 1;
+  if (tid == 0) scal[2] = 0;
+  __syncthreads();
+  if (!packable) {  // wide-range path (see k_hungarian_blocks_wide)
+    if (warp == 0) {
+      BlockArrays Aw{S, u, v, dlt, p, wayi, ulist, ord, rk_i};
+      if (!hungarian_blocks_warp<NB>(Aw, n, mult, k, stats, flags)) return;
+      __syncwarp();
+      for (int j = lane + 1; j <= k; j += 32) {
+        const int r = p[j] - 1;
+        if (col_of_row) col_of_row[r] = static_cast<uint64_t>(j - 1);
+        if (decision) {
+          const uint32_t row = order[r];
+          decision[row_ids ? row_ids[row] : row] = (j - 1) / mult;
+        }
+      }
+    }
+    return;
+  }
+
+  unsigned long long steps = 0;
+  long long c_step = 0, c_end = 0, c_tab = 0, rekeyed = 0;
+  const long long c_start = clock64();
+  for (int i = 1; i <= k; ++i) {
+    const long long t0 = clock64();
+    // ---- operand tables for this row (all warps)
+    for (int idx = tid; idx < k; idx += blockDim.x) {
+      const int c = ord[idx];
+      const int r = p[c];
+      const int x = idx / mult;
+      rtab[idx] = r;
+      Btab[idx] = static_cast<int64_t>(x) - (v[c] << 6);
+      if (r > 0) {
+        const int64_t ur = u[r];
+        const int64_t* Sr = S + static_cast<size_t>(r - 1) * n;
+        int64_t* Ar = A + static_cast<size_t>(idx) * n;
+        for (int w = 0; w < n; ++w) Ar[w] = (Sr[w] - ur) << 6;
+      }
+    }
+    __syncthreads();
+    const long long t1 = clock64();
+    c_tab += t1 - t0;
+    if (warp == 0) {
+      int64_t E6[NB], B[NB], Bn[NB];
+      int wyi[NB], curl[NB], col[NB], coln[NB];
+      const int64_t ui = u[i];
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const int w = lane + 32 * b;
+        curl[b] = mult;  // lanes without a block never offer a key
+        E6[b] = 0;
+        B[b] = Bn[b] = 0;
+        col[b] = coln[b] = 0;
+        wyi[b] = 0;
+        if (w < n) {
+          curl[b] = 0;
+          const int base = w * mult;
+          col[b] = ord[base];
+          B[b] = Btab[base];
+          if (mult > 1) {
+            coln[b] = ord[base + 1];
+            Bn[b] = Btab[base + 1];
+          }
+          E6[b] = (S[static_cast<size_t>(i - 1) * n + w] - ui) << 6;  // relax from row i
+        }
+      }
+      if constexpr (!PACK) {
+        if (lane < n) curs[lane] = 0;
+        if (NB > 1 && lane + 32 < n) curs[lane + 32] = 0;
+      }
+      if (lane == 0) {
+        p[0] = i;
+        ulist[0] = 0;
+        dlt[0] = 0;
+      }
+      __syncwarp();
+      uint64_t cp = 0;  // packed cursors (PACK)
+      int nused = 1;
+      int64_t Dl = 0;
+      bool abort = false;
+      for (;;) {
+        ++steps;
+        uint64_t key = ~0ULL;
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          if (curl[b] < mult) {
+            const uint64_t kb = static_cast<uint64_t>(E6[b] + B[b]);
+            key = kb < key ? kb : key;
+          }
+        }
+        const unsigned hi = static_cast<unsigned>(key >> 32), lo = static_cast<unsigned>(key);
+        const unsigned mh = __reduce_min_sync(0xffffffffu, hi);
+        const unsigned ml = __reduce_min_sync(0xffffffffu, hi == mh ? lo : 0xffffffffu);
+        const uint64_t kmin = (static_cast<uint64_t>(mh) << 32) | ml;
+        if (kmin == ~0ULL) {
+          abort = true;
+          break;
+        }
+        const int ws = static_cast<int>(ml & 63u);
+        const int64_t delta6 = static_cast<int64_t>(kmin & ~63ULL);
+        Dl += delta6 >> 6;
+        int d;
+        if constexpr (PACK) d = static_cast<int>((cp >> (ws * 8)) & 255u);
+        else d = curs[ws];
+        const int idx = ws * mult + d;
+        int64_t a[NB];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) a[b] = A[static_cast<size_t>(idx) * n + lane + 32 * b];
+        const int r = rtab[idx];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          if (lane + 32 * b == ws) {  // the winner's bookkeeping, from prefetched values
+            const int j1 = col[b];
+            wayi[j1] = wyi[b];
+            dlt[j1] = Dl;
+            ulist[nused] = j1;
+            curl[b] = d + 1;
+            col[b] = coln[b];
+            B[b] = Bn[b];
+            if (d + 2 < mult) {
+              coln[b] = ord[idx + 2];
+              Bn[b] = Btab[idx + 2];
+            }
+          }
+        }
+        if constexpr (PACK) {
+          cp += 1ULL << (ws * 8);
+        } else {
+          __syncwarp();
+          if (lane == 0) curs[ws] = d + 1;
+          __syncwarp();
+        }
+        const int s_cur = nused++;
+        if (r == 0) break;  // free column: augmenting path found
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+          const int64_t t = E6[b] - delta6;
+          if (a[b] < t) {
+            E6[b] = a[b];
+            wyi[b] = s_cur;
+          } else {
+            E6[b] = t;
+          }
+        }
+      }
+      if (lane == 0) {
+        scal[0] = Dl;
+        scal[1] = nused;
+        if (abort) scal[2] = 1;
+      }
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const int w = lane + 32 * b;
+        if (w < n) curs[w] = curl[b];
+      }
+    }
+    __syncthreads();
+    const long long t2 = clock64();
+    c_step += t2 - t1;
+    if (scal[2]) {
+      if (tid == 0) atomicOr(flags + kFlagBadCost, 1);
+      return;
+    }
+    const int64_t Dl = scal[0];
+    const int nu = static_cast<int>(scal[1]);
+    for (int t = tid; t < nu; t += blockDim.x) {  // potentials (assign.hpp:131-138)
+      const int j = ulist[t];
+      const int64_t dd = Dl - dlt[j];
+      u[p[j]] += dd;
+      v[j] -= dd;
+    }
+    __syncthreads();
+    if (tid == 0) {  // augment (assign.hpp:141-145); way[j] = ulist[wayi[j]]
+      int jj = ulist[nu - 1];
+      do {
+        const int jp = ulist[wayi[jj]];
+        p[jj] = p[jp];
+        jj = jp;
+      } while (jj != 0);
+    }
+    for (int w = warp; w < n; w += nw) {  // re-key touched blocks
+      const int P = curs[w];
+      if (P == 0) continue;
+      if (lane == 0) rekeyed += P;
+      int32_t* base = ord + w * mult;
+      int64_t* pv = rk_v + static_cast<size_t>(warp) * mult;
+      int32_t* sorted = rk_i + static_cast<size_t>(warp) * 2 * mult;
+      int32_t* merged = sorted + mult;
+      for (int t = lane; t < P; t += 32) pv[t] = v[base[t]];
+      __syncwarp();
+      for (int t = lane; t < P; t += 32) {
+        const int a = base[t];
+        const int64_t va = pv[t];
+        int rank = 0;
+        for (int s2 = 0; s2 < P; ++s2) {
+          const int64_t vb = pv[s2];
+          rank += (vb > va || (vb == va && base[s2] < a)) ? 1 : 0;
+        }
+        sorted[rank] = a;
+      }
+      __syncwarp();
+      const int Q = mult - P;
+      const int32_t* suf = base + P;
+      for (int t = lane; t < P; t += 32) {
+        const int a = sorted[t];
+        const int64_t va = v[a];
+        int lo2 = 0, hi2 = Q;
+        while (lo2 < hi2) {
+          const int mid = (lo2 + hi2) >> 1;
+          const int b2 = suf[mid];
+          const int64_t vb = v[b2];
+          if (vb > va || (vb == va && b2 < a)) lo2 = mid + 1;
+          else hi2 = mid;
+        }
+        merged[t + lo2] = a;
+      }
+      for (int t = lane; t < Q; t += 32) {
+        const int b2 = suf[t];
+        const int64_t vb = v[b2];
+        int lo2 = 0, hi2 = P;
+        while (lo2 < hi2) {
+          const int mid = (lo2 + hi2) >> 1;
+          const int a = sorted[mid];
+          const int64_t va = v[a];
+          if (va > vb || (va == vb && a < b2)) lo2 = mid + 1;
+          else hi2 = mid;
+        }
+        merged[t + lo2] = b2;
+      }
+      __syncwarp();
+      for (int t = lane; t < mult; t += 32) base[t] = merged[t];
+      __syncwarp();
+    }
+    __syncthreads();
+    c_end += clock64() - t2;
+  }
+  for (int j = tid + 1; j <= k; j += blockDim.x) {
+    const int r = p[j] - 1;
+    if (col_of_row) col_of_row[r] = static_cast<uint64_t>(j - 1);
+    if (decision) {
+      const uint32_t row = order[r];
+      decision[row_ids ? row_ids[row] : row] = (j - 1) / mult;
+    }
+  }
+  if (tid == 0 && stats) {
+    stats[0] = steps;
+    stats[1] = c_step;
+    stats[2] = c_end;
+    stats[3] = c_tab;
+    stats[4] = 0;
+    stats[5] = 0;
+    stats[6] = rekeyed;
+    stats[7] = clock64() - c_start;
+  }
+}
+
 // ----------------------------------------------------------------- K5 dense
 // The reference loop on an arbitrary k x k matrix: one CTA, columns strided
 // over threads, block-wide argmin with the lowest column winning ties.
@@ -846,6 +1162,17 @@ int max_dyn_smem(int device) {
 
 }  // namespace
 
+size_t tab_smem_bytes(int k, int n, int mult, int nw, int smode) {
+  const size_t K1 = static_cast<size_t>(k) + 1;
+  auto r = [](size_t b) { return (b + 15) & ~size_t(15); };
+  size_t b = 0;
+  if (smode == 0) b += r(static_cast<size_t>(k) * n * 8);
+  b += r(static_cast<size_t>(k) * n * 8) + r(static_cast<size_t>(k) * 8) + 3 * r(K1 * 8) +
+       5 * r(K1 * 4) + r(64 * 4) + r(32) + r(static_cast<size_t>(nw) * mult * 8) +
+       r(static_cast<size_t>(nw) * 2 * mult * 4);
+  return b;
+}
+
 size_t fast_smem_bytes(int k, int n, int mult, int nw, int mode) {
   const size_t K1 = static_cast<size_t>(k) + 1;
   auto r = [](size_t b) { return (b + 15) & ~size_t(15); };
@@ -875,6 +1202,30 @@ void launch_hungarian_blocks(HungarianScratch& sc, const double* matrix, int n,
   EDX_LAUNCHED();
   const size_t limit = static_cast<size_t>(max_dyn_smem(device));
   const int nw = std::min(n, kFastMaxWarps);
+  // tabled kernel when its per-row operand table fits in shared memory
+  for (int sm = 0; sm <= 1; ++sm) {
+    const size_t smem = tab_smem_bytes(k, n, mult, nw, sm);
+    if (smem > limit) continue;
+    auto launch = [&](auto kern) {
+      if (smem > 48 * 1024)
+        EDX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+      kern<<<1, 32 * nw, smem, s>>>(sc.s64.p, n, mult, k, order, decision, row_ids, col_of_row,
+                                    sc.steps.p, flags, max_scaled);
+    };
+    if (n <= 8 && mult <= 255) {  // 8-bit packed cursors
+      if (sm == 0) launch(k_hungarian_blocks_tab<1, 0, true>);
+      else launch(k_hungarian_blocks_tab<1, 1, true>);
+    } else if (n <= 32) {
+      if (sm == 0) launch(k_hungarian_blocks_tab<1, 0, false>);
+      else launch(k_hungarian_blocks_tab<1, 1, false>);
+    } else {
+      if (sm == 0) launch(k_hungarian_blocks_tab<2, 0, false>);
+      else launch(k_hungarian_blocks_tab<2, 1, false>);
+    }
+    EDX_LAUNCHED();
+    return;
+  }
   int mode = -1;
   for (int md = 0; md <= 2 && mode < 0; ++md)
     if (fast_smem_bytes(k, n, mult, nw, md) <= limit) mode = md;
