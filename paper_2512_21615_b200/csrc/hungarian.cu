@@ -687,6 +687,87 @@ __global__ void __launch_bounds__(kFastMaxWarps * 32, 1)
   }
 }
 
+// Warp-wide bitonic sort of 32*E (hi, lo) keys held in registers, element
+// index i = e*32 + lane, ascending by (hi, lo).  Used to re-sort a block's
+// columns by (v desc, j asc) = ascending (-v, j) at the end of a row.
+template <int E>
+__device__ __forceinline__ void warp_bitonic_sort(int64_t (&hi)[E], int32_t (&lo)[E], int lane) {
+  constexpr int M = 32 * E;
+#pragma unroll
+  for (int size = 2; size <= M; size <<= 1) {
+#pragma unroll
+    for (int d = size >> 1; d > 0; d >>= 1) {
+      if (d >= 32) {
+        const int de = d >> 5;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int pe = e ^ de;
+          if (pe > e) {
+            const bool asc = ((e * 32 + lane) & size) == 0;
+            const bool gt = hi[e] > hi[pe] || (hi[e] == hi[pe] && lo[e] > lo[pe]);
+            if (gt == asc) {
+              const int64_t th = hi[e];
+              const int32_t tl = lo[e];
+              hi[e] = hi[pe];
+              lo[e] = lo[pe];
+              hi[pe] = th;
+              lo[pe] = tl;
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int64_t oh = __shfl_xor_sync(0xffffffffu, hi[e], d);
+          const int32_t ol = __shfl_xor_sync(0xffffffffu, lo[e], d);
+          const bool asc = ((e * 32 + lane) & size) == 0;
+          const bool lower = (lane & d) == 0;
+          const bool other_less = oh < hi[e] || (oh == hi[e] && ol < lo[e]);
+          if ((lower == asc) ? other_less : !other_less) {
+            hi[e] = oh;
+            lo[e] = ol;
+          }
+        }
+      }
+    }
+  }
+}
+
+// Re-sorts ord[base .. base+mult) by (v desc, j asc) with one warp.
+template <int E>
+__device__ __forceinline__ void warp_resort_block(int32_t* ord, const int64_t* v, int base,
+                                                  int mult, int lane) {
+  int64_t hi[E];
+  int32_t lo[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = e * 32 + lane;
+    if (i < mult) {
+      const int c = ord[base + i];
+      lo[e] = c;
+      hi[e] = -v[c];
+    } else {
+      lo[e] = INT_MAX;
+      hi[e] = LLONG_MAX;
+    }
+  }
+  warp_bitonic_sort<E>(hi, lo, lane);
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = e * 32 + lane;
+    if (i < mult) ord[base + i] = lo[e];
+  }
+}
+
+__device__ __forceinline__ void warp_resort_dispatch(int32_t* ord, const int64_t* v, int base,
+                                                     int mult, int lane) {
+  if (mult <= 32) warp_resort_block<1>(ord, v, base, mult, lane);
+  else if (mult <= 64) warp_resort_block<2>(ord, v, base, mult, lane);
+  else if (mult <= 128) warp_resort_block<4>(ord, v, base, mult, lane);
+  else if (mult <= 256) warp_resort_block<8>(ord, v, base, mult, lane);
+  else warp_resort_block<16>(ord, v, base, mult, lane);
+}
+
 // --------------------------------------------- K6 tabled (per-row operand table)
 // Fastest variant, used when the operand table fits in shared memory.  At the
 // start of each row (phase) all warps rebuild, for every block x and every
@@ -700,8 +781,10 @@ __global__ void __launch_bounds__(kFastMaxWarps * 32, 1)
 // per-block cursors are packed 8 bits each in one uniform register (n <= 8)
 // or kept in shared memory.  `way` is recorded as a step index (see the
 // fast kernel).  Row end is the same as the fast kernel.
+constexpr int kTabMaxWarps = 8;
+
 template <int NB, int SMODE, bool PACK>  // SMODE 0: S shared, 1: S global
-__global__ void __launch_bounds__(kFastMaxWarps * 32, 1)
+__global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
     k_hungarian_blocks_tab(const int64_t* __restrict__ S_global, int n, int mult, int k,
                            const uint32_t* __restrict__ order, int32_t* __restrict__ decision,
                            const uint32_t* __restrict__ row_ids, uint64_t* __restrict__ col_of_row,
@@ -768,7 +851,7 @@ __global__ void __launch_bounds__(kFastMaxWarps * 32, 1)
   }
 
   unsigned long long steps = 0;
-  long long c_step = 0, c_end = 0, c_tab = 0, rekeyed = 0;
+  long long c_step = 0, c_end = 0, c_tab = 0, rekeyed = 0, c_pot = 0, p2 = 0, pmax = 0;
   const long long c_start = clock64();
   for (int i = 1; i <= k; ++i) {
     const long long t0 = clock64();
@@ -919,6 +1002,7 @@ __global__ void __launch_bounds__(kFastMaxWarps * 32, 1)
       v[j] -= dd;
     }
     __syncthreads();
+    c_pot += clock64() - t2;
     if (tid == 0) {  // augment (assign.hpp:141-145); way[j] = ulist[wayi[j]]
       int jj = ulist[nu - 1];
       do {
@@ -931,6 +1015,15 @@ __global__ void __launch_bounds__(kFastMaxWarps * 32, 1)
       const int P = curs[w];
       if (P == 0) continue;
       if (lane == 0) rekeyed += P;
+      if (lane == 0 && warp == 0) {
+        p2 += static_cast<long long>(P) * P;
+        pmax = P > pmax ? P : pmax;
+      }
+      if (mult <= 512) {
+        warp_resort_dispatch(ord, v, w * mult, mult, lane);
+        __syncwarp();
+        continue;
+      }
       int32_t* base = ord + w * mult;
       int64_t* pv = rk_v + static_cast<size_t>(warp) * mult;
       int32_t* sorted = rk_i + static_cast<size_t>(warp) * 2 * mult;
@@ -996,8 +1089,8 @@ __global__ void __launch_bounds__(kFastMaxWarps * 32, 1)
     stats[1] = c_step;
     stats[2] = c_end;
     stats[3] = c_tab;
-    stats[4] = 0;
-    stats[5] = 0;
+    stats[4] = c_pot;
+    stats[5] = p2 * 1000000 + pmax;
     stats[6] = rekeyed;
     stats[7] = clock64() - c_start;
   }
@@ -1203,15 +1296,16 @@ void launch_hungarian_blocks(HungarianScratch& sc, const double* matrix, int n,
   const size_t limit = static_cast<size_t>(max_dyn_smem(device));
   const int nw = std::min(n, kFastMaxWarps);
   // tabled kernel when its per-row operand table fits in shared memory
+  const int nwt = std::min(n, kTabMaxWarps);
   for (int sm = 0; sm <= 1; ++sm) {
-    const size_t smem = tab_smem_bytes(k, n, mult, nw, sm);
+    const size_t smem = tab_smem_bytes(k, n, mult, nwt, sm);
     if (smem > limit) continue;
     auto launch = [&](auto kern) {
       if (smem > 48 * 1024)
         EDX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(smem)));
-      kern<<<1, 32 * nw, smem, s>>>(sc.s64.p, n, mult, k, order, decision, row_ids, col_of_row,
-                                    sc.steps.p, flags, max_scaled);
+      kern<<<1, 32 * nwt, smem, s>>>(sc.s64.p, n, mult, k, order, decision, row_ids, col_of_row,
+                                     sc.steps.p, flags, max_scaled);
     };
     if (n <= 8 && mult <= 255) {  // 8-bit packed cursors
       if (sm == 0) launch(k_hungarian_blocks_tab<1, 0, true>);
