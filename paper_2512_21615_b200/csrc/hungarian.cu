@@ -906,7 +906,7 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
         dlt[0] = 0;
       }
       __syncwarp();
-      uint64_t cp = 0;  // packed cursors (PACK)
+      uint32_t cpl = 0, cph = 0;  // packed 8-bit cursors of blocks 0-3 / 4-7 (PACK)
       int nused = 1;
       int64_t Dl = 0;
       bool abort = false;
@@ -915,48 +915,50 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
         uint64_t key = ~0ULL;
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
-          if (curl[b] < mult) {
-            const uint64_t kb = static_cast<uint64_t>(E6[b] + B[b]);
-            key = kb < key ? kb : key;
-          }
+          const uint64_t kb = static_cast<uint64_t>(E6[b] + B[b]);
+          key = (curl[b] < mult && kb < key) ? kb : key;
         }
         const unsigned hi = static_cast<unsigned>(key >> 32), lo = static_cast<unsigned>(key);
         const unsigned mh = __reduce_min_sync(0xffffffffu, hi);
         const unsigned ml = __reduce_min_sync(0xffffffffu, hi == mh ? lo : 0xffffffffu);
-        const uint64_t kmin = (static_cast<uint64_t>(mh) << 32) | ml;
-        if (kmin == ~0ULL) {
-          abort = true;
-          break;
-        }
-        const int ws = static_cast<int>(ml & 63u);
-        const int64_t delta6 = static_cast<int64_t>(kmin & ~63ULL);
-        Dl += delta6 >> 6;
+        const int ws = min(static_cast<int>(ml & 63u), n - 1);  // clamp: corrupt input only
         int d;
-        if constexpr (PACK) d = static_cast<int>((cp >> (ws * 8)) & 255u);
+        if constexpr (PACK) d = static_cast<int>(__byte_perm(ws < 4 ? cpl : cph, 0, 0x4440 | (ws & 3)));
         else d = curs[ws];
         const int idx = ws * mult + d;
         int64_t a[NB];
 #pragma unroll
         for (int b = 0; b < NB; ++b) a[b] = A[static_cast<size_t>(idx) * n + lane + 32 * b];
         const int r = rtab[idx];
+        if (mh == 0xffffffffu && ml == 0xffffffffu) {  // nothing left: corrupt input only
+          abort = true;
+          break;
+        }
+        const int64_t delta6 = static_cast<int64_t>(((static_cast<uint64_t>(mh) << 32) | ml) & ~63ULL);
+        Dl += delta6 >> 6;
+        // the winner's bookkeeping (predicated; values prefetched one consumption ahead)
+        const int nxt = idx + 2 < (ws + 1) * mult ? idx + 2 : idx;
+        const int pc = ord[nxt];
+        const int64_t pb = Btab[nxt];
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
-          if (lane + 32 * b == ws) {  // the winner's bookkeeping, from prefetched values
+          const bool mine = lane + 32 * b == ws;
+          if (mine) {
             const int j1 = col[b];
             wayi[j1] = wyi[b];
             dlt[j1] = Dl;
             ulist[nused] = j1;
-            curl[b] = d + 1;
-            col[b] = coln[b];
-            B[b] = Bn[b];
-            if (d + 2 < mult) {
-              coln[b] = ord[idx + 2];
-              Bn[b] = Btab[idx + 2];
-            }
           }
+          curl[b] = mine ? d + 1 : curl[b];
+          col[b] = mine ? coln[b] : col[b];
+          B[b] = mine ? Bn[b] : B[b];
+          coln[b] = mine ? pc : coln[b];
+          Bn[b] = mine ? pb : Bn[b];
         }
         if constexpr (PACK) {
-          cp += 1ULL << (ws * 8);
+          const uint32_t inc = 1u << ((ws & 3) * 8);
+          cpl += ws < 4 ? inc : 0u;
+          cph += ws < 4 ? 0u : inc;
         } else {
           __syncwarp();
           if (lane == 0) curs[ws] = d + 1;
@@ -967,12 +969,9 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
 #pragma unroll
         for (int b = 0; b < NB; ++b) {
           const int64_t t = E6[b] - delta6;
-          if (a[b] < t) {
-            E6[b] = a[b];
-            wyi[b] = s_cur;
-          } else {
-            E6[b] = t;
-          }
+          const bool imp = a[b] < t;
+          E6[b] = imp ? a[b] : t;
+          wyi[b] = imp ? s_cur : wyi[b];
         }
       }
       if (lane == 0) {
