@@ -807,14 +807,15 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
   } else {
     S = S_global;
   }
-  int64_t* A = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(k) * n * 8));
+  const int AST = PACK ? 8 : n;  // row stride of the operand table
+  int64_t* A = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(k) * AST * 8));
   int64_t* Btab = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(k) * 8));
   int64_t* u = reinterpret_cast<int64_t*>(stake(K1 * 8));
   int64_t* v = reinterpret_cast<int64_t*>(stake(K1 * 8));
-  int64_t* dlt = reinterpret_cast<int64_t*>(stake(K1 * 8));
+  int64_t* dlt = reinterpret_cast<int64_t*>(stake((K1 + 32) * 8));
   int32_t* p = reinterpret_cast<int32_t*>(stake(K1 * 4));
-  int32_t* wayi = reinterpret_cast<int32_t*>(stake(K1 * 4));
-  int32_t* ulist = reinterpret_cast<int32_t*>(stake(K1 * 4));
+  int32_t* wayi = reinterpret_cast<int32_t*>(stake((K1 + 32) * 4));
+  int32_t* ulist = reinterpret_cast<int32_t*>(stake((K1 + 32) * 4));
   int32_t* ord = reinterpret_cast<int32_t*>(stake(K1 * 4));
   int32_t* rtab = reinterpret_cast<int32_t*>(stake(K1 * 4));
   int32_t* curs = reinterpret_cast<int32_t*>(stake(64 * 4));
@@ -865,7 +866,7 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
       if (r > 0) {
         const int64_t ur = u[r];
         const int64_t* Sr = S + static_cast<size_t>(r - 1) * n;
-        int64_t* Ar = A + static_cast<size_t>(idx) * n;
+        int64_t* Ar = A + static_cast<size_t>(idx) * AST;
         for (int w = 0; w < n; ++w) Ar[w] = (Sr[w] - ur) << 6;
       }
     }
@@ -906,10 +907,60 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
         dlt[0] = 0;
       }
       __syncwarp();
-      uint32_t cpl = 0, cph = 0;  // packed 8-bit cursors of blocks 0-3 / 4-7 (PACK)
       int nused = 1;
       int64_t Dl = 0;
       bool abort = false;
+      if constexpr (PACK) {
+        // n <= 8: lane w owns block w; cursors are 8-bit fields of (cpl, cph);
+        // an exhausted block (or a lane without one) carries B = 2^62, above
+        // every real key (< 2^57), so no per-step validity select is needed.
+        constexpr int64_t kBig = 1LL << 62;
+        int64_t E6v = E6[0], Bv = (lane < n && mult > 0) ? B[0] : kBig, Bnv = Bn[0];
+        int colv = col[0], colnv = coln[0], wyv = wyi[0];
+        uint32_t cpl = 0, cph = 0;
+        const int64_t* Alane = A + lane;
+        const int dummy = k + 1 + lane;
+        for (;;) {
+          ++steps;
+          const uint64_t key = static_cast<uint64_t>(E6v + Bv);
+          const unsigned hi = static_cast<unsigned>(key >> 32), lo = static_cast<unsigned>(key);
+          const unsigned mh = __reduce_min_sync(0xffffffffu, hi);
+          const unsigned ml = __reduce_min_sync(0xffffffffu, hi == mh ? lo : 0xffffffffu);
+          const int ws = static_cast<int>(ml & 7u);
+          const int d = static_cast<int>(__byte_perm(cpl, cph, static_cast<unsigned>(ws)) & 255u);
+          const int idx = ws * mult + d;
+          const int64_t av = Alane[static_cast<size_t>(idx) * 8];
+          const int r = rtab[idx];
+          const int64_t delta6 = static_cast<int64_t>(((static_cast<uint64_t>(mh) << 32) | ml) & ~63ULL);
+          Dl += delta6 >> 6;
+          const int nxt = d + 2 < mult ? idx + 2 : idx;
+          const int pc = ord[nxt];
+          const int64_t pb = Btab[nxt];
+          const bool mine = lane == ws;
+          const int js = mine ? colv : dummy;  // non-owners write to their dummy slot
+          wayi[js] = wyv;
+          dlt[js] = Dl;
+          ulist[mine ? nused : dummy] = colv;
+          colv = mine ? colnv : colv;
+          Bv = mine ? (d + 1 < mult ? Bnv : kBig) : Bv;
+          colnv = mine ? pc : colnv;
+          Bnv = mine ? pb : Bnv;
+          const uint32_t inc = 1u << ((ws & 3) * 8);
+          cpl += ws < 4 ? inc : 0u;
+          cph += ws < 4 ? 0u : inc;
+          const int s_cur = nused++;
+          if (r == 0) break;  // free column: augmenting path found
+          const int64_t tt = E6v - delta6;
+          const bool imp = av < tt;
+          E6v = imp ? av : tt;
+          wyv = imp ? s_cur : wyv;
+          if (ml == 0xffffffffu && mh == 0xffffffffu) {  // nothing left: corrupt input only
+            abort = true;
+            break;
+          }
+        }
+        curl[0] = lane < n ? static_cast<int>(__byte_perm(cpl, cph, static_cast<unsigned>(lane & 7)) & 255u) : 0;
+      } else {
       for (;;) {
         ++steps;
         uint64_t key = ~0ULL;
@@ -922,13 +973,11 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
         const unsigned mh = __reduce_min_sync(0xffffffffu, hi);
         const unsigned ml = __reduce_min_sync(0xffffffffu, hi == mh ? lo : 0xffffffffu);
         const int ws = min(static_cast<int>(ml & 63u), n - 1);  // clamp: corrupt input only
-        int d;
-        if constexpr (PACK) d = static_cast<int>(__byte_perm(ws < 4 ? cpl : cph, 0, 0x4440 | (ws & 3)));
-        else d = curs[ws];
+        const int d = curs[ws];
         const int idx = ws * mult + d;
         int64_t a[NB];
 #pragma unroll
-        for (int b = 0; b < NB; ++b) a[b] = A[static_cast<size_t>(idx) * n + lane + 32 * b];
+        for (int b = 0; b < NB; ++b) a[b] = A[static_cast<size_t>(idx) * AST + lane + 32 * b];
         const int r = rtab[idx];
         if (mh == 0xffffffffu && ml == 0xffffffffu) {  // nothing left: corrupt input only
           abort = true;
@@ -936,7 +985,6 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
         }
         const int64_t delta6 = static_cast<int64_t>(((static_cast<uint64_t>(mh) << 32) | ml) & ~63ULL);
         Dl += delta6 >> 6;
-        // the winner's bookkeeping (predicated; values prefetched one consumption ahead)
         const int nxt = idx + 2 < (ws + 1) * mult ? idx + 2 : idx;
         const int pc = ord[nxt];
         const int64_t pb = Btab[nxt];
@@ -955,15 +1003,9 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
           coln[b] = mine ? pc : coln[b];
           Bn[b] = mine ? pb : Bn[b];
         }
-        if constexpr (PACK) {
-          const uint32_t inc = 1u << ((ws & 3) * 8);
-          cpl += ws < 4 ? inc : 0u;
-          cph += ws < 4 ? 0u : inc;
-        } else {
-          __syncwarp();
-          if (lane == 0) curs[ws] = d + 1;
-          __syncwarp();
-        }
+        __syncwarp();
+        if (lane == 0) curs[ws] = d + 1;
+        __syncwarp();
         const int s_cur = nused++;
         if (r == 0) break;  // free column: augmenting path found
 #pragma unroll
@@ -973,6 +1015,7 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
           E6[b] = imp ? a[b] : t;
           wyi[b] = imp ? s_cur : wyi[b];
         }
+      }
       }
       if (lane == 0) {
         scal[0] = Dl;
@@ -1259,9 +1302,10 @@ size_t tab_smem_bytes(int k, int n, int mult, int nw, int smode) {
   auto r = [](size_t b) { return (b + 15) & ~size_t(15); };
   size_t b = 0;
   if (smode == 0) b += r(static_cast<size_t>(k) * n * 8);
-  b += r(static_cast<size_t>(k) * n * 8) + r(static_cast<size_t>(k) * 8) + 3 * r(K1 * 8) +
-       5 * r(K1 * 4) + r(64 * 4) + r(32) + r(static_cast<size_t>(nw) * mult * 8) +
-       r(static_cast<size_t>(nw) * 2 * mult * 4);
+  const int ast = (n <= 8 && mult <= 255) ? 8 : n;
+  b += r(static_cast<size_t>(k) * ast * 8) + r(static_cast<size_t>(k) * 8) + 2 * r(K1 * 8) +
+       r((K1 + 32) * 8) + 3 * r(K1 * 4) + 2 * r((K1 + 32) * 4) + r(64 * 4) + r(32) +
+       r(static_cast<size_t>(nw) * mult * 8) + r(static_cast<size_t>(nw) * 2 * mult * 4);
   return b;
 }
 
