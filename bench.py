@@ -161,7 +161,16 @@ def product(args, w, rank, world, local_rank):
     offs = np.arange(R + 1, dtype=np.uint64) * np.uint64(L)
     cfg = edx.ClusterConfig(n=n, m=m, bandwidths_bps=w["bw"], d_tran_bytes=2048,
                             cache_capacity=w["cap"], alpha=w["alpha"])
-    eng = edx.SimState(cfg, id_space=w["V"], max_batch_ids=R * L, device=local_rank)
+    nccl_id = None
+    if world > 1:  # rank 0's ncclUniqueId, shared over the torch process group
+        import torch.distributed as dist
+        buf = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            buf.copy_(torch.frombuffer(bytearray(edx.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(buf, 0)
+        nccl_id = bytes(buf.cpu().numpy().tobytes())
+    eng = edx.SimState(cfg, id_space=w["V"], max_batch_ids=R * L, device=local_rank, rank=rank,
+                       world_size=world, nccl_id=nccl_id)
     stream = torch.cuda.ExternalStream(eng.stream_handle(), device=dev)
     flush = None if args.no_flush else torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
@@ -244,7 +253,9 @@ def product(args, w, rank, world, local_rank):
         "steps": K, "warmup": W, "ms_per_step": step_ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: reference ZipfStream (s=1.05, seed 42), state warmed by prefill",
-        "config": config_json(w, args),
+        "config": config_json(w, args, {"parallelism": f"row-sharded cost build x{world}, "
+                                        "NCCL gather to rank 0, rank-0 solve, decision broadcast, "
+                                        "replicated cache update" if world > 1 else "1 GPU"}),
         "e2e": {"value": R / (e2e_step_ms * 1e-3), "unit": "samples/s",
                 "ms_per_step": e2e_step_ms, "h2d_bytes_per_step": R * L * 4 + (R + 1) * 8,
                 "d2h_bytes_per_step": R * 4 + 8 + (3 * n + 4) * 8},

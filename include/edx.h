@@ -93,7 +93,14 @@ typedef struct edx_engine_options {
   const void* nccl_unique_id; /* 128-byte ncclUniqueId from rank 0, world_size > 1 */
 } edx_engine_options;
 
-/* SimState::SimState(const ClusterConfig&) — sim.hpp:56-59. */
+/* 128-byte ncclUniqueId for a multi-GPU engine group (call on rank 0 and
+ * share the bytes with the other ranks, e.g. through torch.distributed). */
+int edx_nccl_unique_id(void* out, uint64_t len);
+
+/* SimState::SimState(const ClusterConfig&) — sim.hpp:56-59.  With world_size
+ * > 1 every rank holds a replica of the state; edx_engine_build computes this
+ * rank's row shard and gathers the matrix to rank 0 over NCCL, rank 0 solves
+ * and broadcasts the decision, and every rank applies the step. */
 int edx_engine_create(const edx_cluster_config* cfg, const edx_engine_options* opt,
                       edx_engine** out);
 void edx_engine_destroy(edx_engine* e);

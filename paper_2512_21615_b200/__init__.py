@@ -390,10 +390,14 @@ class SimState:
     id_space: ids must lie in [0, id_space) (dense device tables).
     max_batch_ids: capacity of one batch's id stream (sum of sample lengths)."""
 
-    def __init__(self, cfg: ClusterConfig, id_space: int, max_batch_ids: int, device: int = 0):
+    def __init__(self, cfg: ClusterConfig, id_space: int, max_batch_ids: int, device: int = 0,
+                 rank: int = 0, world_size: int = 1, nccl_id: Optional[bytes] = None):
         self.cfg = cfg
         self._h = C.c_void_p()
-        opt = EngineOptionsC(int(device), 0, int(id_space), int(max_batch_ids), 0, 1, None)
+        self._nid = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        opt = EngineOptionsC(int(device), 0, int(id_space), int(max_batch_ids), int(rank),
+                             int(world_size),
+                             C.cast(self._nid, C.c_void_p) if self._nid is not None else None)
         c = cfg._c()
         check(lib().edx_engine_create(C.byref(c), C.byref(opt), C.byref(self._h)))
         self._batch = None
@@ -557,6 +561,18 @@ class SimState:
         check(lib().edx_engine_phase_times(self._h, _ptr(ms, C.c_double), _ptr(counts, C.c_uint64),
                                            int(bool(reset))))
         return ms, counts
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId for a multi-GPU SimState group (rank 0)."""
+    buf = C.create_string_buffer(128)
+    check(lib().edx_nccl_unique_id(buf, 128))
+    return buf.raw
+
+
+def shard_rows(rows: int, world: int):
+    """Row shard [lo, hi) of every rank (nccl_comm.h shard_rows)."""
+    return [(rows * r // world, rows * (r + 1) // world) for r in range(world)]
 
 
 def solver_stats(engine=None) -> dict:

@@ -72,6 +72,7 @@ def _sigs():
         ("edx_abi_version", cint, []),
         ("edx_validate_config", cint, [cfgp, u64]),
         ("edx_unit_costs", cint, [cfgp, dblp]),
+        ("edx_nccl_unique_id", cint, [vp, u64]),
         ("edx_engine_create", cint, [cfgp, P(EngineOptionsC), P(vp)]),
         ("edx_engine_destroy", None, [vp]),
         ("edx_engine_load_batch", cint, [vp, vp, vp, u64, cint]),

@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "engine.h"
+#include "nccl_comm.h"
 #include "step.h"
 
 using edx::DevBuf;
@@ -349,21 +350,35 @@ void engine_build(edx_engine* e) {
   e->disp.row_index.ensure(e->rows);
   EDX_CUDA(cudaStreamWaitEvent(e->stream, e->cost_done, 0));
   rec(e, 0, e->stream);
-  edx::launch_cost_build(e->cur_ids, e->cur_offsets, e->rows, e->n, e->ol.p, e->id_space,
-                         e->ucost.p, e->matrix.p, e->disp.gap_keys.p, e->disp.row_index.p,
-                         e->flags.p, e->stream);
+  if (e->world == 1) {
+    edx::launch_cost_build(e->cur_ids, e->cur_offsets, e->rows, e->n, e->ol.p, e->id_space,
+                           e->ucost.p, e->matrix.p, e->disp.gap_keys.p, e->disp.row_index.p,
+                           e->flags.p, e->stream);
+    e->gap_ready = true;
+  } else {
+    // row shards (samples are independent, cost.hpp:102-104), gathered to rank 0
+    std::vector<uint64_t> lo(e->world), hi(e->world);
+    edx::shard_rows(e->rows, e->world, lo.data(), hi.data());
+    const uint64_t a = lo[e->rank], b = hi[e->rank];
+    if (b > a)
+      edx::launch_cost_build(e->cur_ids, e->cur_offsets + a, b - a, e->n, e->ol.p, e->id_space,
+                             e->ucost.p, e->matrix.p + a * e->n, nullptr, nullptr, e->flags.p,
+                             e->stream);
+    edx::nccl_gather_rows(e->comm, e->matrix.p, lo.data(), hi.data(), e->world, e->rank, 0, e->n,
+                          e->stream);
+    e->gap_ready = false;
+  }
   rec(e, 1, e->stream);
   e->launches += 1;
   e->pending_build = e->profiling;
   e->built = true;
-  e->gap_ready = true;
 }
 
 void engine_dispatch(edx_engine* e, double alpha) {
   if (!e->built) edx::invalid("build the cost matrix before dispatching");
   if (alpha < 0.0) alpha = e->alpha;
   if (alpha > 1.0) edx::invalid("alpha must lie in [0, 1]");
-  e->decision.ensure(e->rows);
+  e->decision.ensure(e->rows + 2);
   e->expected.ensure(1);
   edx::PhaseEvents pe;
   if (e->profiling) {
@@ -376,15 +391,32 @@ void engine_dispatch(edx_engine* e, double alpha) {
   }
   int launches = 0;
   rec(e, 10, e->stream);
-  edx::run_ecomix(e->disp, e->matrix.p, e->rows, e->n, e->m, alpha, e->gap_ready,
-                  e->decision.p, e->flags.p, e->stream, e->device, e->profiling ? &pe : nullptr,
-                  &launches);
+  if (e->rank == 0)
+    edx::run_ecomix(e->disp, e->matrix.p, e->rows, e->n, e->m, alpha, e->gap_ready,
+                    e->decision.p, e->flags.p, e->stream, e->device, e->profiling ? &pe : nullptr,
+                    &launches);
   rec(e, 11, e->stream);
-  // decision_cost is only reported (sim.hpp:439): overlap it with the step.
-  EDX_CUDA(cudaEventRecord(e->disp.fork, e->stream));
-  EDX_CUDA(cudaStreamWaitEvent(e->disp.side, e->disp.fork, 0));
-  edx::launch_decision_cost(e->matrix.p, e->decision.p, e->rows, e->n, e->expected.p, e->disp.side);
-  EDX_CUDA(cudaEventRecord(e->cost_done, e->disp.side));
+  if (e->world == 1) {
+    // decision_cost is only reported (sim.hpp:439): overlap it with the step.
+    EDX_CUDA(cudaEventRecord(e->disp.fork, e->stream));
+    EDX_CUDA(cudaStreamWaitEvent(e->disp.side, e->disp.fork, 0));
+    edx::launch_decision_cost(e->matrix.p, e->decision.p, e->rows, e->n, e->expected.p,
+                              e->disp.side);
+    EDX_CUDA(cudaEventRecord(e->cost_done, e->disp.side));
+  } else {
+    // rank 0 appends decision_cost's bits to the decision; one broadcast to all
+    if (e->rank == 0) {
+      edx::launch_decision_cost(e->matrix.p, e->decision.p, e->rows, e->n, e->expected.p,
+                                e->stream);
+      EDX_CUDA(cudaMemcpyAsync(e->decision.p + e->rows, e->expected.p, sizeof(double),
+                               cudaMemcpyDeviceToDevice, e->stream));
+    }
+    edx::nccl_broadcast_i32(e->comm, e->decision.p, e->rows + 2, 0, e->stream);
+    if (e->rank != 0)
+      EDX_CUDA(cudaMemcpyAsync(e->expected.p, e->decision.p + e->rows, sizeof(double),
+                               cudaMemcpyDeviceToDevice, e->stream));
+    EDX_CUDA(cudaEventRecord(e->cost_done, e->stream));
+  }
   e->launches += launches + 1;
   const int mult = edx::exact_multiplicity(e->m, alpha);
   e->pending_greedy = e->profiling && static_cast<uint64_t>(e->n) * mult < e->rows;
@@ -491,7 +523,10 @@ int edx_engine_create(const edx_cluster_config* cfg, const edx_engine_options* o
     if (opt->id_space == 0 || opt->id_space > (1ULL << 32)) edx::invalid("id_space must be in [1, 2^32]");
     if (opt->max_batch_ids == 0 || opt->max_batch_ids >= (1ULL << 31))
       edx::invalid("max_batch_ids must be in [1, 2^31)");
-    if (opt->world_size > 1) throw Error(EDX_RUNTIME_ERROR, "multi-GPU engines are created through edx_engine_create with NCCL support (not built)");
+    if (opt->world_size > 1) {
+      if (!opt->nccl_unique_id) edx::invalid("world_size > 1 needs the rank-0 nccl_unique_id");
+      if (opt->rank < 0 || opt->rank >= opt->world_size) edx::invalid("rank out of range");
+    }
     int count = 0;
     EDX_CUDA(cudaGetDeviceCount(&count));
     if (opt->device < 0 || opt->device >= count) edx::invalid("CUDA device ordinal out of range");
@@ -528,6 +563,7 @@ int edx_engine_create(const edx_cluster_config* cfg, const edx_engine_options* o
     e->disp.init(e->device);
     edx::step_init_state(e.get());
     EDX_CUDA(cudaStreamSynchronize(e->stream));
+    if (e->world > 1) e->comm = edx::nccl_comm_create(opt->nccl_unique_id, e->world, e->rank);
     *out = e.release();
   });
 }
@@ -543,6 +579,7 @@ void edx_engine_destroy(edx_engine* e) {
   if (e->h_counters) cudaFreeHost(e->h_counters);
   if (e->h_expected) cudaFreeHost(e->h_expected);
   cudaStream_t s = e->stream;
+  if (e->comm) edx::nccl_comm_destroy(e->comm);
   delete e;
   if (s) cudaStreamDestroy(s);
 }
@@ -685,6 +722,13 @@ int edx_engine_validate_consistency(edx_engine* e) {
 }
 
 uint64_t edx_engine_clock(edx_engine* e) { return e->clock; }
+
+int edx_nccl_unique_id(void* out, uint64_t len) {
+  return guard([&] {
+    if (len < 128) edx::invalid("nccl unique id buffer must hold 128 bytes");
+    edx::nccl_unique_id(out);
+  });
+}
 
 int edx_engine_stream(edx_engine* e, void** stream) {
   return guard([&] { *stream = static_cast<void*>(e->stream); });

@@ -64,6 +64,7 @@ struct edx_engine {
   std::vector<double> bw, ucost_h;
   uint64_t id_space = 0, max_ids = 0;
   int rank = 0, world = 1;
+  void* comm = nullptr;  // ncclComm_t when world > 1; rank 0 is the solver rank
   uint64_t clock = 0;
 
   // global per-embedding state (SimState::global_, sim.hpp:266), dense by id
