@@ -183,6 +183,12 @@ int edx_build_matrix(const edx_cluster_config* cfg, const uint32_t* snap_ids,
                      const uint64_t* snap_owners, const uint64_t* snap_latest,
                      const uint64_t* snap_resident, uint64_t snap_count, const uint32_t* ids,
                      const uint64_t* offsets, uint64_t num_samples, double* out);
+/* expected_cost(sample, j, snapshot, cfg) for every j and every given sample
+ * (cost.hpp:81-100) — build_matrix without the m*n sample-count check. */
+int edx_expected_costs(const edx_cluster_config* cfg, const uint32_t* snap_ids,
+                       const uint64_t* snap_owners, const uint64_t* snap_latest,
+                       uint64_t snap_count, const uint32_t* ids, const uint64_t* offsets,
+                       uint64_t num_samples, double* out);
 /* row_gap_key — cost.hpp:130-146. */
 int edx_row_gap_key(uint64_t rows, uint64_t cols, const double* values, uint64_t row,
                     double* out);

@@ -94,6 +94,7 @@ def _sigs():
         ("edx_engine_phase_times", cint, [vp, dblp, u64p, cint]),
         ("edx_solver_stats", cint, [vp, u64p]),
         ("edx_build_matrix", cint, [cfgp, u32p, u64p, u64p, u64p, u64, u32p, u64p, u64, dblp]),
+        ("edx_expected_costs", cint, [cfgp, u32p, u64p, u64p, u64, u32p, u64p, u64, dblp]),
         ("edx_row_gap_key", cint, [u64, u64, dblp, u64, dblp]),
         ("edx_rows_by_gap", cint, [u64, u64, dblp, u64p]),
         ("edx_hungarian", cint, [u64, dblp, u64p, dblp]),

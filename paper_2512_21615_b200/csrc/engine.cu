@@ -894,6 +894,13 @@ int edx_solver_stats(edx_engine* e, uint64_t* out) {
 
 // ------------------------------------------------------ stateless matrix API
 
+namespace {
+void stateless_build(const edx_cluster_config* cfg, const uint32_t* snap_ids,
+                     const uint64_t* snap_owners, const uint64_t* snap_latest,
+                     uint64_t snap_count, const uint32_t* ids, const uint64_t* offsets,
+                     uint64_t R, double* out);
+}  // namespace
+
 int edx_build_matrix(const edx_cluster_config* cfg, const uint32_t* snap_ids,
                      const uint64_t* snap_owners, const uint64_t* snap_latest,
                      const uint64_t* snap_resident, uint64_t snap_count, const uint32_t* ids,
@@ -902,6 +909,30 @@ int edx_build_matrix(const edx_cluster_config* cfg, const uint32_t* snap_ids,
     if (!cfg || cfg->n < 1 || cfg->n > 64) edx::invalid(cfg && cfg->n > 64 ? "at most 64 workers supported" : "worker count must be >= 1");
     const uint64_t want = static_cast<uint64_t>(cfg->n) * static_cast<uint64_t>(cfg->m);
     if (R != want) edx::invalid("expected " + std::to_string(want) + " samples, got " + std::to_string(R));
+    (void)snap_resident;  // residency never enters the cost (cost.hpp:81-100)
+    stateless_build(cfg, snap_ids, snap_owners, snap_latest, snap_count, ids, offsets, R, out);
+  });
+}
+
+int edx_expected_costs(const edx_cluster_config* cfg, const uint32_t* snap_ids,
+                       const uint64_t* snap_owners, const uint64_t* snap_latest,
+                       uint64_t snap_count, const uint32_t* ids, const uint64_t* offsets,
+                       uint64_t num_samples, double* out) {
+  return guard([&] {
+    if (!cfg || cfg->n < 1 || cfg->n > 64) edx::invalid(cfg && cfg->n > 64 ? "at most 64 workers supported" : "worker count must be >= 1");
+    if (cfg->n_bandwidths < cfg->n) edx::invalid("need one bandwidth per worker");
+    if (num_samples == 0) return;
+    stateless_build(cfg, snap_ids, snap_owners, snap_latest, snap_count, ids, offsets,
+                    num_samples, out);
+  });
+}
+
+namespace {
+void stateless_build(const edx_cluster_config* cfg, const uint32_t* snap_ids,
+                     const uint64_t* snap_owners, const uint64_t* snap_latest,
+                     uint64_t snap_count, const uint32_t* ids, const uint64_t* offsets,
+                     uint64_t R, double* out) {
+  {
     auto& c = dctx();
     std::lock_guard<std::mutex> lk(c.mu);
     c.init();
@@ -935,13 +966,13 @@ int edx_build_matrix(const edx_cluster_config* cfg, const uint32_t* snap_ids,
                                                          snap_count, space, c.ol.p, nullptr, c.flags.p);
       EDX_LAUNCHED();
     }
-    (void)snap_resident;  // residency never enters the cost (cost.hpp:81-100)
     edx::launch_cost_build(c.ids.p, c.offsets.p, R, cfg->n, c.ol.p, space, c.ucost.p, c.values.p,
                            nullptr, nullptr, c.flags.p, c.stream);
     EDX_CUDA(cudaMemcpyAsync(out, c.values.p, R * cfg->n * 8, cudaMemcpyDeviceToHost, c.stream));
     c.sync_and_check();
-  });
+  }
 }
+}  // namespace
 
 int edx_row_gap_key(uint64_t rows, uint64_t cols, const double* values, uint64_t row, double* out) {
   return guard([&] {

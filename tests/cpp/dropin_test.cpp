@@ -1,0 +1,146 @@
+// Drop-in test: code written against the reference's embdispatch API (the
+// sequence of tests/test_sim.cpp:189-206 and acceptance.cpp:210-242) compiled
+// against include/embdispatch/ + libedx.so, checked against the oracle
+// (oracle/edx_oracle.c, the plain-C restatement of the reference) on the
+// same inputs.  Exit code 0 = every iteration bit-identical.
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "embdispatch/sim.hpp"
+extern "C" {
+#include "edx_oracle.h"
+}
+
+using namespace embdispatch;
+
+static int failures = 0;
+#define EXPECT(c, ...)                      \
+  do {                                      \
+    if (!(c)) {                             \
+      std::printf("FAIL %s:%d ", __FILE__, __LINE__); \
+      std::printf(__VA_ARGS__);             \
+      std::printf("\n");                    \
+      ++failures;                           \
+    }                                       \
+  } while (0)
+
+static void fig2_walkthrough() {
+  ClusterConfig cfg;
+  cfg.n = 3;
+  cfg.m = 1;
+  cfg.cache_capacity = 16;
+  cfg.bandwidths_bps = {5e9, 5e9, 5e8};
+  SimState state(cfg, EngineOptions{0, 64, 64});
+  state.seed_entry(1, 0, true, false);
+  state.seed_entry(9, 2, true, true);
+  const std::vector<EmbeddingSample> samples = {make_sample({1}), make_sample({9}),
+                                                make_sample({8, 10, 11})};
+  DispatchDecision d;
+  d.worker_of_sample = {0, 1, 2};
+  const IterationReport rep = state.step(samples, d);
+  EXPECT((rep.miss_pull_w == std::vector<std::uint64_t>{0, 1, 3}), "miss_pull_w");
+  EXPECT((rep.update_push_w == std::vector<std::uint64_t>{0, 0, 1}), "update_push_w");
+  EXPECT(rep.hits == 1 && rep.lookups == 5, "hits/lookups");
+  EXPECT(rep.cost_w[1] == 3.2768e-6 && rep.cost_w[2] == 4 * 3.2768e-5, "cost_w");
+  EXPECT(state.state_of(9).owned_by(1) && !state.state_of(9).latest_on(2), "x9 state");
+  EXPECT(state.cache(2).find(9) && !state.cache(2).find(9)->version_latest, "x9 cache flag");
+  state.validate_consistency();
+  bool threw = false;
+  try {
+    DispatchDecision bad;
+    bad.worker_of_sample = {0, 0, 1};
+    state.step(samples, bad);
+  } catch (const std::invalid_argument&) {
+    threw = true;
+  }
+  EXPECT(threw, "unbalanced decision must throw std::invalid_argument");
+}
+
+static void engine_vs_oracle(double alpha) {
+  ClusterConfig cfg;
+  cfg.n = 8;
+  cfg.m = 16;
+  cfg.cache_capacity = 120;
+  cfg.alpha = alpha;
+  cfg.bandwidths_bps = {5e9, 5e9, 5e9, 5e9, 5e8, 5e8, 5e8, 5e8};
+  WorkloadSpec spec;
+  spec.total_embeddings = 400;
+  spec.sample_len = 6;
+  spec.iterations = 30;
+  spec.seed = 99;
+  ZipfStream stream(spec, cfg);
+  SimState engine(cfg, EngineOptions{0, 400, 8 * 16 * 6});
+  orc_cluster_config oc{cfg.n, cfg.m, cfg.bandwidths_bps.data(), cfg.n, 0, cfg.d_tran_bytes,
+                        cfg.cache_capacity, alpha};
+  orc_sim* oracle = nullptr;
+  orc_sim_create(&oc, &oracle);
+  std::vector<EmbeddingSample> samples;
+  int iter = 0;
+  while (stream.next_iteration(samples)) {
+    // the reference's own per-iteration sequence (test_sim.cpp:189-206)
+    const Snapshot snap = engine.snapshot();
+    const CostMatrix matrix = build_matrix(samples, snap, cfg);
+    const DispatchDecision decision = ecomix(matrix, cfg);
+    const IterationReport rep = engine.step(samples, decision);
+    const double expected = decision_cost(matrix, decision);
+
+    std::vector<uint32_t> ids;
+    std::vector<uint64_t> offs{0};
+    for (auto& s : samples) {
+      ids.insert(ids.end(), s.ids.begin(), s.ids.end());
+      offs.push_back(ids.size());
+    }
+    std::vector<double> om(matrix.values.size());
+    orc_sim_build_matrix(oracle, ids.data(), offs.data(), samples.size(), om.data());
+    EXPECT(std::memcmp(om.data(), matrix.values.data(), om.size() * 8) == 0, "matrix iter %d", iter);
+    std::vector<int32_t> od(samples.size());
+    orc_ecomix(&oc, samples.size(), cfg.n, om.data(), nullptr, od.data());
+    bool same = true;
+    for (std::size_t i = 0; i < od.size(); ++i) same &= od[i] == decision.worker_of_sample[i];
+    EXPECT(same, "decision iter %d", iter);
+    double oexp = 0;
+    orc_decision_cost(samples.size(), cfg.n, om.data(), od.data(), &oexp);
+    EXPECT(oexp == expected, "expected cost iter %d", iter);
+    std::vector<uint64_t> mp(8), up(8), ep(8);
+    std::vector<double> cw(8);
+    orc_report orep{0, 0, 0, 0, 0, 0, 0.0, mp.data(), up.data(), ep.data(), cw.data()};
+    orc_sim_step(oracle, ids.data(), offs.data(), samples.size(), od.data(), &orep);
+    EXPECT(rep.miss_pull_w == mp && rep.update_push_w == up && rep.evict_push_w == ep,
+           "counts iter %d", iter);
+    EXPECT(rep.cost_s == orep.cost_s && rep.hits == orep.hits, "cost/hits iter %d", iter);
+    ++iter;
+  }
+  engine.validate_consistency();
+  orc_sim_destroy(oracle);
+  EXPECT(iter == 30, "iterations");
+}
+
+static void run_loop() {
+  ClusterConfig cfg;
+  cfg.n = 2;
+  cfg.m = 4;
+  cfg.cache_capacity = 12;
+  cfg.bandwidths_bps = {5e9, 5e8};
+  WorkloadSpec spec;
+  spec.total_embeddings = 60;
+  spec.sample_len = 3;
+  spec.iterations = 50;
+  spec.seed = 1234;
+  ZipfStream stream(spec, cfg);
+  RunOptions opt;
+  opt.validate_state = true;
+  const RunResult r = run(stream, Mechanism::parse("ecomix:0.5"), cfg, opt, EngineOptions{0, 64, 64});
+  EXPECT(r.reports.size() == 50 && r.summary.measured_iterations == 40, "run() bookkeeping");
+}
+
+int main() {
+  fig2_walkthrough();
+  engine_vs_oracle(0.0);
+  engine_vs_oracle(0.5);
+  engine_vs_oracle(1.0);
+  run_loop();
+  std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
+  return failures ? 1 : 0;
+}
