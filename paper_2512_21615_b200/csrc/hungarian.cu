@@ -782,6 +782,7 @@ __device__ __forceinline__ void warp_resort_dispatch(int32_t* ord, const int64_t
 // or kept in shared memory.  `way` is recorded as a step index (see the
 // fast kernel).  Row end is the same as the fast kernel.
 constexpr int kTabMaxWarps = 8;
+constexpr int kRunMax = 32;  // speculative run length of the batched Dijkstra steps
 
 template <int NB, int SMODE, bool PACK>  // SMODE 0: S shared, 1: S global
 __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
@@ -819,6 +820,7 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
   int32_t* ord = reinterpret_cast<int32_t*>(stake(K1 * 4));
   int32_t* rtab = reinterpret_cast<int32_t*>(stake(K1 * 4));
   int32_t* curs = reinterpret_cast<int32_t*>(stake(64 * 4));
+  int64_t* Pbuf = reinterpret_cast<int64_t*>(stake((kRunMax + 1) * 8));
   int64_t* scal = reinterpret_cast<int64_t*>(stake(4 * 8));
   int64_t* rk_v = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(nw) * mult * 8));
   int32_t* rk_i = reinterpret_cast<int32_t*>(stake(static_cast<size_t>(nw) * 2 * mult * 4));
@@ -914,51 +916,107 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
         // n <= 8: lane w owns block w; cursors are 8-bit fields of (cpl, cph);
         // an exhausted block (or a lane without one) carries B = 2^62, above
         // every real key (< 2^57), so no per-step validity select is needed.
+        //
+        // Run-batched steps.  After the argmin picks block w, the next steps
+        // are evaluated speculatively assuming w keeps winning (in practice
+        // ~97% of consecutive steps share the winner block).  While w wins,
+        // its key sequence is closed form: with V6_t = v(c_t) << 6,
+        //     delta6_t = min(V6_{t-1}, A_w(r_{t-1})) - V6_t      (t >= 2),
+        // and every block's relaxed value obeys E^{t+1} = min(E^t - delta6_t,
+        // A(r_t)), i.e. with P_t = sum of delta6 up to t and F = E + P_{t-1},
+        //     F^{t+1} = min(F^t, A(r_t) + P_t)      (a prefix min).
+        // Step t is the sequential step iff no other block has a smaller key:
+        // F_x^t + (B_x - w) > P_t for every x != w (keys carry the block index
+        // in their low bits, so they are never equal across blocks).  The
+        // first failing t over all lanes (one REDUX) bounds the valid prefix,
+        // which is then committed exactly as the one-step loop would.
         constexpr int64_t kBig = 1LL << 62;
-        int64_t E6v = E6[0], Bv = (lane < n && mult > 0) ? B[0] : kBig, Bnv = Bn[0];
-        int colv = col[0], colnv = coln[0], wyv = wyi[0];
+        int64_t E6v = E6[0], Bv = (lane < n && mult > 0) ? B[0] : kBig;
+        int colv = col[0], wyv = wyi[0];
         uint32_t cpl = 0, cph = 0;
         const int64_t* Alane = A + lane;
         const int dummy = k + 1 + lane;
         for (;;) {
-          ++steps;
           const uint64_t key = static_cast<uint64_t>(E6v + Bv);
           const unsigned hi = static_cast<unsigned>(key >> 32), lo = static_cast<unsigned>(key);
           const unsigned mh = __reduce_min_sync(0xffffffffu, hi);
           const unsigned ml = __reduce_min_sync(0xffffffffu, hi == mh ? lo : 0xffffffffu);
-          const int ws = static_cast<int>(ml & 7u);
-          const int d = static_cast<int>(__byte_perm(cpl, cph, static_cast<unsigned>(ws)) & 255u);
-          const int idx = ws * mult + d;
-          const int64_t av = Alane[static_cast<size_t>(idx) * 8];
-          const int r = rtab[idx];
-          const int64_t delta6 = static_cast<int64_t>(((static_cast<uint64_t>(mh) << 32) | ml) & ~63ULL);
-          Dl += delta6 >> 6;
-          const int nxt = d + 2 < mult ? idx + 2 : idx;
-          const int pc = ord[nxt];
-          const int64_t pb = Btab[nxt];
-          const bool mine = lane == ws;
-          const int js = mine ? colv : dummy;  // non-owners write to their dummy slot
-          wayi[js] = wyv;
-          dlt[js] = Dl;
-          ulist[mine ? nused : dummy] = colv;
-          colv = mine ? colnv : colv;
-          Bv = mine ? (d + 1 < mult ? Bnv : kBig) : Bv;
-          colnv = mine ? pc : colnv;
-          Bnv = mine ? pb : Bnv;
-          const uint32_t inc = 1u << ((ws & 3) * 8);
-          cpl += ws < 4 ? inc : 0u;
-          cph += ws < 4 ? 0u : inc;
-          const int s_cur = nused++;
-          if (r == 0) break;  // free column: augmenting path found
-          const int64_t tt = E6v - delta6;
-          const bool imp = av < tt;
-          E6v = imp ? av : tt;
-          wyv = imp ? s_cur : wyv;
           if (ml == 0xffffffffu && mh == 0xffffffffu) {  // nothing left: corrupt input only
             abort = true;
             break;
           }
+          const int ws = static_cast<int>(ml & 7u);
+          const int d = static_cast<int>(__byte_perm(cpl, cph, static_cast<unsigned>(ws)) & 255u);
+          const int base = ws * mult + d;  // position of the winner's candidate c_1
+          const int Tm = min(kRunMax, mult - d);
+          const int64_t delta1 = static_cast<int64_t>(((static_cast<uint64_t>(mh) << 32) | ml) & ~63ULL);
+          const bool mine = lane == ws;
+          const int64_t Bx_w = Bv - ws;  // B_x - w (this lane)
+          // ---- pass 1: deltas, prefix sums, validity, free column
+          int64_t P = 0, F = E6v, V6prev = 0, Awprev = 0;
+          int tfail = mine ? kRunMax + 1 : kRunMax + 1, tfree = kRunMax + 1, t = 1;
+          for (; t <= Tm; ++t) {
+            const int pos = base + t - 1;
+            const int64_t V6 = static_cast<int64_t>(ws) - Btab[pos];
+            const int r = rtab[pos];
+            const int64_t Aw = A[static_cast<size_t>(pos) * 8 + ws];
+            const int64_t Ax = Alane[static_cast<size_t>(pos) * 8];
+            const int64_t d6 = t == 1 ? delta1 : (V6prev < Awprev ? V6prev : Awprev) - V6;
+            P += d6;
+            if (t >= 2 && tfail > kRunMax && !mine && !(F + Bx_w > P)) tfail = t;
+            if (lane == 0) Pbuf[t] = P;
+            if (r == 0) {  // free column: the augmenting path (and the run) ends at t
+              tfree = t;
+              break;
+            }
+            const int64_t cand = Ax + P;
+            F = cand < F ? cand : F;
+            V6prev = V6;
+            Awprev = Aw;
+          }
+          const int V = static_cast<int>(__reduce_min_sync(0xffffffffu, static_cast<unsigned>(tfail)));
+          int sN = V - 1 < Tm ? V - 1 : Tm;
+          const bool phase_end = tfree <= sN;
+          if (phase_end) sN = tfree;
+          __syncwarp();
+          // ---- pass 2: commit steps 1..sN (relaxes of steps 1..sN, except a final free column)
+          F = E6v;
+          const int nused0 = nused;
+          const int64_t Dl0 = Dl;
+          for (int t2 = 1; t2 <= sN; ++t2) {
+            const int pos = base + t2 - 1;
+            const int64_t Pt = Pbuf[t2];
+            const int c = ord[pos];
+            const int js = mine ? c : dummy;  // the winner's bookkeeping; others hit a dummy slot
+            wayi[js] = wyv;
+            dlt[js] = Dl0 + (Pt >> 6);
+            ulist[mine ? nused0 + t2 - 1 : dummy] = c;
+            if (t2 == sN && phase_end) break;
+            const int64_t cand = Alane[static_cast<size_t>(pos) * 8] + Pt;
+            const bool imp = cand < F;
+            F = imp ? cand : F;
+            wyv = imp ? nused0 + t2 - 1 : wyv;
+          }
+          const int64_t Ps = Pbuf[sN];
+          Dl = Dl0 + (Ps >> 6);
+          nused = nused0 + sN;
+          steps += sN;
+          E6v = F - Ps;
+          {  // advance block ws by sN columns
+            const uint32_t inc = static_cast<uint32_t>(sN) << ((ws & 3) * 8);
+            cpl += ws < 4 ? inc : 0u;
+            cph += ws < 4 ? 0u : inc;
+            const int np = base + sN;
+            const bool left = d + sN < mult;
+            const int cn = left ? ord[np] : 0;
+            const int64_t bn = left ? Btab[np] : kBig;
+            colv = mine ? cn : colv;
+            Bv = mine ? bn : Bv;
+          }
+          __syncwarp();
+          if (phase_end) break;
         }
+        (void)colv;
         curl[0] = lane < n ? static_cast<int>(__byte_perm(cpl, cph, static_cast<unsigned>(lane & 7)) & 255u) : 0;
       } else {
       for (;;) {
