@@ -47,6 +47,7 @@ enum DevFlag : int {
   kFlagPinned = 2,         // every cache entry pinned (cache.hpp:164)
   kFlagUnbalanced = 3,     // a dispatch decision broke the m-per-worker balance
   kFlagKeyRange = 4,       // victim-key fields exceed the 57-bit packing
+  kFlagInternal = 5,       // internal launch-configuration error (bug)
   kFlagCount = 8
 };
 

@@ -74,6 +74,7 @@ void check_flags_host(const int* f) {
   if (f[edx::kFlagBadCost]) edx::invalid("costs must be finite and non-negative");
   if (f[edx::kFlagPinned]) edx::logic("every cache entry is pinned; cannot evict");
   if (f[edx::kFlagUnbalanced]) edx::logic("capacities exhausted before rows");
+  if (f[edx::kFlagInternal]) throw Error(EDX_RUNTIME_ERROR, "internal error: solver shared-memory layout");
   if (f[edx::kFlagKeyRange])
     throw Error(EDX_RUNTIME_ERROR, "victim key fields exceed the 57-bit device packing");
 }

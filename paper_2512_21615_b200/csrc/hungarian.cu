@@ -58,6 +58,12 @@ __device__ __forceinline__ int64_t scale_cost(double x, int64_t cap) {
 
 __device__ __forceinline__ bool bad_cost(double x) { return !isfinite(x) || x < 0.0; }
 
+__device__ __forceinline__ size_t dynamic_smem_bytes() {
+  unsigned v;
+  asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(v));
+  return v;
+}
+
 // S[r][w] = scaled cost of block row r (matrix row order[r]) for worker w.
 __global__ void k_scale_block(const double* __restrict__ matrix, int n,
                               const uint32_t* __restrict__ order, uint64_t k, int64_t cap,
@@ -431,6 +437,10 @@ __global__ void __launch_bounds__(kFastMaxWarps * 32, 1)
   int64_t* scal = reinterpret_cast<int64_t*>(stake(4 * 8));  // Dl, nused, abort
   int64_t* rk_v = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(nw) * mult * 8));
   int32_t* rk_i = reinterpret_cast<int32_t*>(stake(static_cast<size_t>(nw) * 2 * mult * 4));
+  if (so > dynamic_smem_bytes()) {  // host/device layout mismatch: fail loudly, touch nothing
+    if (tid == 0) atomicOr(flags + kFlagInternal, 1);
+    return;
+  }
 
   for (size_t x = tid; x < K1; x += blockDim.x) {
     u[x] = 0;
@@ -824,6 +834,10 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
   int64_t* scal = reinterpret_cast<int64_t*>(stake(4 * 8));
   int64_t* rk_v = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(nw) * mult * 8));
   int32_t* rk_i = reinterpret_cast<int32_t*>(stake(static_cast<size_t>(nw) * 2 * mult * 4));
+  if (so > dynamic_smem_bytes()) {  // host/device layout mismatch: fail loudly, touch nothing
+    if (tid == 0) atomicOr(flags + kFlagInternal, 1);
+    return;
+  }
 
   const unsigned long long mx = *max_scaled;
   const bool packable = mx < (1ULL << 57) / (8ULL * static_cast<unsigned long long>(k + 1));
@@ -854,7 +868,7 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
   }
 
   unsigned long long steps = 0;
-  long long c_step = 0, c_end = 0, c_tab = 0, rekeyed = 0, c_pot = 0, p2 = 0, pmax = 0;
+  long long c_step = 0, c_end = 0, c_tab = 0, rekeyed = 0, c_pot = 0, p2 = 0, pmax = 0, runs = 0;
   const long long c_start = clock64();
   for (int i = 1; i <= k; ++i) {
     const long long t0 = clock64();
@@ -998,6 +1012,7 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
             wyv = imp ? nused0 + t2 - 1 : wyv;
           }
           const int64_t Ps = Pbuf[sN];
+          ++runs;
           Dl = Dl0 + (Ps >> 6);
           nused = nused0 + sN;
           steps += sN;
@@ -1190,7 +1205,7 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
     stats[2] = c_end;
     stats[3] = c_tab;
     stats[4] = c_pot;
-    stats[5] = p2 * 1000000 + pmax;
+    stats[5] = runs;
     stats[6] = rekeyed;
     stats[7] = clock64() - c_start;
   }
@@ -1362,8 +1377,9 @@ size_t tab_smem_bytes(int k, int n, int mult, int nw, int smode) {
   if (smode == 0) b += r(static_cast<size_t>(k) * n * 8);
   const int ast = (n <= 8 && mult <= 255) ? 8 : n;
   b += r(static_cast<size_t>(k) * ast * 8) + r(static_cast<size_t>(k) * 8) + 2 * r(K1 * 8) +
-       r((K1 + 32) * 8) + 3 * r(K1 * 4) + 2 * r((K1 + 32) * 4) + r(64 * 4) + r(32) +
-       r(static_cast<size_t>(nw) * mult * 8) + r(static_cast<size_t>(nw) * 2 * mult * 4);
+       r((K1 + 32) * 8) + 3 * r(K1 * 4) + 2 * r((K1 + 32) * 4) + r(64 * 4) +
+       r(static_cast<size_t>(kRunMax + 1) * 8) + r(32) + r(static_cast<size_t>(nw) * mult * 8) +
+       r(static_cast<size_t>(nw) * 2 * mult * 4);
   return b;
 }
 
