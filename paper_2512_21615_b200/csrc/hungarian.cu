@@ -792,7 +792,8 @@ __device__ __forceinline__ void warp_resort_dispatch(int32_t* ord, const int64_t
 // or kept in shared memory.  `way` is recorded as a step index (see the
 // fast kernel).  Row end is the same as the fast kernel.
 constexpr int kTabMaxWarps = 8;
-constexpr int kRunMax = 32;  // speculative run length of the batched Dijkstra steps
+constexpr int kRunMax = 255;  // speculative run length cap of the batched Dijkstra steps
+constexpr int kChunk = 8;     // steps evaluated per speculation chunk
 
 template <int NB, int SMODE, bool PACK>  // SMODE 0: S shared, 1: S global
 __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
@@ -830,7 +831,6 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
   int32_t* ord = reinterpret_cast<int32_t*>(stake(K1 * 4));
   int32_t* rtab = reinterpret_cast<int32_t*>(stake(K1 * 4));
   int32_t* curs = reinterpret_cast<int32_t*>(stake(64 * 4));
-  int64_t* Pbuf = reinterpret_cast<int64_t*>(stake((kRunMax + 1) * 8));
   int64_t* scal = reinterpret_cast<int64_t*>(stake(4 * 8));
   int64_t* rk_v = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(nw) * mult * 8));
   int32_t* rk_i = reinterpret_cast<int32_t*>(stake(static_cast<size_t>(nw) * 2 * mult * 4));
@@ -966,52 +966,72 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
           const int64_t delta1 = static_cast<int64_t>(((static_cast<uint64_t>(mh) << 32) | ml) & ~63ULL);
           const bool mine = lane == ws;
           const int64_t Bx_w = Bv - ws;  // B_x - w (this lane)
-          // ---- pass 1: deltas, prefix sums, validity, free column
+          // The run is evaluated in chunks of kChunk steps: operands are loaded
+          // up front, the prefix recurrences run in registers, one REDUX finds
+          // the first step some other block would win, and the valid prefix is
+          // committed from register snapshots.
           int64_t P = 0, F = E6v, V6prev = 0, Awprev = 0;
-          int tfail = mine ? kRunMax + 1 : kRunMax + 1, tfree = kRunMax + 1, t = 1;
-          for (; t <= Tm; ++t) {
-            const int pos = base + t - 1;
-            const int64_t V6 = static_cast<int64_t>(ws) - Btab[pos];
-            const int r = rtab[pos];
-            const int64_t Aw = A[static_cast<size_t>(pos) * 8 + ws];
-            const int64_t Ax = Alane[static_cast<size_t>(pos) * 8];
-            const int64_t d6 = t == 1 ? delta1 : (V6prev < Awprev ? V6prev : Awprev) - V6;
-            P += d6;
-            if (t >= 2 && tfail > kRunMax && !mine && !(F + Bx_w > P)) tfail = t;
-            if (lane == 0) Pbuf[t] = P;
-            if (r == 0) {  // free column: the augmenting path (and the run) ends at t
-              tfree = t;
-              break;
-            }
-            const int64_t cand = Ax + P;
-            F = cand < F ? cand : F;
-            V6prev = V6;
-            Awprev = Aw;
-          }
-          const int V = static_cast<int>(__reduce_min_sync(0xffffffffu, static_cast<unsigned>(tfail)));
-          int sN = V - 1 < Tm ? V - 1 : Tm;
-          const bool phase_end = tfree <= sN;
-          if (phase_end) sN = tfree;
-          __syncwarp();
-          // ---- pass 2: commit steps 1..sN (relaxes of steps 1..sN, except a final free column)
-          F = E6v;
+          int sN = 0;
+          bool phase_end = false;
           const int nused0 = nused;
           const int64_t Dl0 = Dl;
-          for (int t2 = 1; t2 <= sN; ++t2) {
-            const int pos = base + t2 - 1;
-            const int64_t Pt = Pbuf[t2];
-            const int c = ord[pos];
-            const int js = mine ? c : dummy;  // the winner's bookkeeping; others hit a dummy slot
-            wayi[js] = wyv;
-            dlt[js] = Dl0 + (Pt >> 6);
-            ulist[mine ? nused0 + t2 - 1 : dummy] = c;
-            if (t2 == sN && phase_end) break;
-            const int64_t cand = Alane[static_cast<size_t>(pos) * 8] + Pt;
-            const bool imp = cand < F;
-            F = imp ? cand : F;
-            wyv = imp ? nused0 + t2 - 1 : wyv;
+          while (sN < Tm) {
+            const int cnt = min(kChunk, Tm - sN);
+            const int64_t P_in = P, F_in = F;
+            int64_t V6q[kChunk], Awq[kChunk], Axq[kChunk];
+            int rq[kChunk], cq[kChunk];
+#pragma unroll
+            for (int q = 0; q < kChunk; ++q) {
+              const int pos = base + sN + (q < cnt ? q : 0);
+              V6q[q] = static_cast<int64_t>(ws) - Btab[pos];
+              rq[q] = rtab[pos];
+              cq[q] = ord[pos];
+              Awq[q] = A[static_cast<size_t>(pos) * 8 + ws];
+              Axq[q] = Alane[static_cast<size_t>(pos) * 8];
+            }
+            int64_t Pq[kChunk], Fq[kChunk];
+            unsigned impm = 0;
+            int failq = kChunk, freeq = kChunk;
+#pragma unroll
+            for (int q = 0; q < kChunk; ++q) {
+              const bool live = q < cnt && q <= freeq;
+              const bool first = sN == 0 && q == 0;
+              const int64_t d6 = first ? delta1 : (V6prev < Awprev ? V6prev : Awprev) - V6q[q];
+              if (live) P += d6;
+              Pq[q] = P;
+              if (live && !first && failq == kChunk && !mine && !(F + Bx_w > P)) failq = q;
+              if (live && rq[q] == 0 && freeq == kChunk) freeq = q;
+              const int64_t cand = Axq[q] + P;
+              const bool imp = live && q != freeq && cand < F;
+              impm |= imp ? (1u << q) : 0u;
+              F = imp ? cand : F;
+              Fq[q] = F;
+              V6prev = V6q[q];
+              Awprev = Awq[q];
+            }
+            const int fail = static_cast<int>(__reduce_min_sync(0xffffffffu, static_cast<unsigned>(failq)));
+            int vq = fail < cnt ? fail : cnt;
+            if (freeq < vq) {
+              vq = freeq + 1;
+              phase_end = true;
+            }
+            // commit steps q < vq of this chunk
+#pragma unroll
+            for (int q = 0; q < kChunk; ++q) {
+              if (q < vq) {
+                const int js = mine ? cq[q] : dummy;  // the winner's bookkeeping; others hit a dummy slot
+                wayi[js] = wyv;
+                dlt[js] = Dl0 + (Pq[q] >> 6);
+                ulist[mine ? nused0 + sN + q : dummy] = cq[q];
+                if ((impm >> q) & 1u) wyv = nused0 + sN + q;
+              }
+            }
+            P = vq > 0 ? Pq[vq - 1] : P_in;
+            F = vq > 0 ? Fq[vq - 1] : F_in;
+            sN += vq;
+            if (vq < cnt || phase_end) break;
           }
-          const int64_t Ps = Pbuf[sN];
+          const int64_t Ps = P;
           ++runs;
           Dl = Dl0 + (Ps >> 6);
           nused = nused0 + sN;
@@ -1378,7 +1398,7 @@ size_t tab_smem_bytes(int k, int n, int mult, int nw, int smode) {
   const int ast = (n <= 8 && mult <= 255) ? 8 : n;
   b += r(static_cast<size_t>(k) * ast * 8) + r(static_cast<size_t>(k) * 8) + 2 * r(K1 * 8) +
        r((K1 + 32) * 8) + 3 * r(K1 * 4) + 2 * r((K1 + 32) * 4) + r(64 * 4) +
-       r(static_cast<size_t>(kRunMax + 1) * 8) + r(32) + r(static_cast<size_t>(nw) * mult * 8) +
+       r(32) + r(static_cast<size_t>(nw) * mult * 8) +
        r(static_cast<size_t>(nw) * 2 * mult * 4);
   return b;
 }
