@@ -977,7 +977,6 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
           const int64_t Dl0 = Dl;
           while (sN < Tm) {
             const int cnt = min(kChunk, Tm - sN);
-            const int64_t P_in = P, F_in = F;
             int64_t V6q[kChunk], Awq[kChunk], Axq[kChunk];
             int rq[kChunk], cq[kChunk];
 #pragma unroll
@@ -989,45 +988,77 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
               Awq[q] = A[static_cast<size_t>(pos) * 8 + ws];
               Axq[q] = Alane[static_cast<size_t>(pos) * 8];
             }
-            int64_t Pq[kChunk], Fq[kChunk];
-            unsigned impm = 0;
-            int failq = kChunk, freeq = kChunk;
+            // deltas (independent), then depth-3 prefix sum / prefix min
+            int64_t Pq[kChunk], Cq[kChunk], Fb[kChunk], Fa[kChunk];
 #pragma unroll
             for (int q = 0; q < kChunk; ++q) {
-              const bool live = q < cnt && q <= freeq;
-              const bool first = sN == 0 && q == 0;
-              const int64_t d6 = first ? delta1 : (V6prev < Awprev ? V6prev : Awprev) - V6q[q];
-              if (live) P += d6;
-              Pq[q] = P;
-              if (live && !first && failq == kChunk && !mine && !(F + Bx_w > P)) failq = q;
-              if (live && rq[q] == 0 && freeq == kChunk) freeq = q;
-              const int64_t cand = Axq[q] + P;
-              const bool imp = live && q != freeq && cand < F;
-              impm |= imp ? (1u << q) : 0u;
-              F = imp ? cand : F;
-              Fq[q] = F;
-              V6prev = V6q[q];
-              Awprev = Awq[q];
+              const int64_t vp = q == 0 ? V6prev : V6q[q - 1];
+              const int64_t ap = q == 0 ? Awprev : Awq[q - 1];
+              const int64_t d6 = (sN == 0 && q == 0) ? delta1 : (vp < ap ? vp : ap) - V6q[q];
+              Pq[q] = q < cnt ? d6 : 0;
             }
+#pragma unroll
+            for (int off = 1; off < kChunk; off <<= 1) {
+#pragma unroll
+              for (int q = kChunk - 1; q >= off; --q) Pq[q] += Pq[q - off];
+            }
+#pragma unroll
+            for (int q = 0; q < kChunk; ++q) {
+              Pq[q] += P;
+              Cq[q] = Axq[q] + Pq[q];  // relax candidate of step q
+              Fa[q] = Cq[q];
+            }
+#pragma unroll
+            for (int off = 1; off < kChunk; off <<= 1) {
+#pragma unroll
+              for (int q = kChunk - 1; q >= off; --q) Fa[q] = Fa[q - off] < Fa[q] ? Fa[q - off] : Fa[q];
+            }
+            unsigned failm = 0, impm = 0, freem = 0;
+#pragma unroll
+            for (int q = 0; q < kChunk; ++q) {
+              const int64_t incl = Fa[q] < F ? Fa[q] : F;               // F after the relax of step q
+              Fb[q] = q == 0 ? F : (Fa[q - 1] < F ? Fa[q - 1] : F);     // F before step q
+              Fa[q] = incl;
+              const bool live = q < cnt;
+              const bool first = sN == 0 && q == 0;
+              failm |= (live && !first && !mine && !(Fb[q] + Bx_w > Pq[q])) ? (1u << q) : 0u;
+              freem |= (live && rq[q] == 0) ? (1u << q) : 0u;
+              impm |= (live && Cq[q] < Fb[q]) ? (1u << q) : 0u;
+            }
+            const int failq = failm ? __ffs(failm) - 1 : kChunk;
+            const int freeq = freem ? __ffs(freem) - 1 : kChunk;
+            impm &= freeq < kChunk ? ((1u << freeq) - 1u) : 0xffu;  // no relax at/after a free column
+            V6prev = V6q[kChunk - 1];
+            Awprev = Awq[kChunk - 1];
             const int fail = static_cast<int>(__reduce_min_sync(0xffffffffu, static_cast<unsigned>(failq)));
             int vq = fail < cnt ? fail : cnt;
             if (freeq < vq) {
               vq = freeq + 1;
               phase_end = true;
             }
-            // commit steps q < vq of this chunk
+            // commit steps q < vq of this chunk (way = last improving step before q)
+            const int wbase = nused0 + sN;
 #pragma unroll
             for (int q = 0; q < kChunk; ++q) {
               if (q < vq) {
+                const unsigned prev = impm & ((1u << q) - 1u);
+                const int wy = prev ? wbase + 31 - __clz(prev) : wyv;
                 const int js = mine ? cq[q] : dummy;  // the winner's bookkeeping; others hit a dummy slot
-                wayi[js] = wyv;
+                wayi[js] = wy;
                 dlt[js] = Dl0 + (Pq[q] >> 6);
-                ulist[mine ? nused0 + sN + q : dummy] = cq[q];
-                if ((impm >> q) & 1u) wyv = nused0 + sN + q;
+                ulist[mine ? wbase + q : dummy] = cq[q];
               }
             }
-            P = vq > 0 ? Pq[vq - 1] : P_in;
-            F = vq > 0 ? Fq[vq - 1] : F_in;
+            const unsigned cm = impm & (vq >= 32 ? 0xffffffffu : ((1u << vq) - 1u));
+            wyv = cm ? wbase + 31 - __clz(cm) : wyv;
+            int64_t Pn = P, Fn = F;
+#pragma unroll
+            for (int q = 0; q < kChunk; ++q) {
+              Pn = q == vq - 1 ? Pq[q] : Pn;
+              Fn = q == vq - 1 ? Fa[q] : Fn;
+            }
+            P = Pn;
+            F = Fn;
             sN += vq;
             if (vq < cnt || phase_end) break;
           }
