@@ -1051,14 +1051,14 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
             }
             const unsigned cm = impm & (vq >= 32 ? 0xffffffffu : ((1u << vq) - 1u));
             wyv = cm ? wbase + 31 - __clz(cm) : wyv;
-            int64_t Pn = P, Fn = F;
+            // P, F after the committed prefix: a forward select chain (no indexing,
+            // which the compiler would otherwise lower to local memory)
 #pragma unroll
             for (int q = 0; q < kChunk; ++q) {
-              Pn = q == vq - 1 ? Pq[q] : Pn;
-              Fn = q == vq - 1 ? Fa[q] : Fn;
+              const bool take = q < vq;
+              P = take ? Pq[q] : P;
+              F = take ? Fa[q] : F;
             }
-            P = Pn;
-            F = Fn;
             sN += vq;
             if (vq < cnt || phase_end) break;
           }
