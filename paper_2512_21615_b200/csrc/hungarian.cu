@@ -962,103 +962,107 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
           const int ws = static_cast<int>(ml & 7u);
           const int d = static_cast<int>(__byte_perm(cpl, cph, static_cast<unsigned>(ws)) & 255u);
           const int base = ws * mult + d;  // position of the winner's candidate c_1
-          const int Tm = min(kRunMax, mult - d);
+          const int Tm = mult - d;
           const int64_t delta1 = static_cast<int64_t>(((static_cast<uint64_t>(mh) << 32) | ml) & ~63ULL);
-          const bool mine = lane == ws;
-          const int64_t Bx_w = Bv - ws;  // B_x - w (this lane)
-          // The run is evaluated in chunks of kChunk steps: operands are loaded
-          // up front, the prefix recurrences run in registers, one REDUX finds
-          // the first step some other block would win, and the valid prefix is
-          // committed from register snapshots.
-          int64_t P = 0, F = E6v, V6prev = 0, Awprev = 0;
+          // Block state broadcast to every lane: F (= E + P), key offset B, way.
+          int64_t Fx[8], Bx[8];
+          int wyx[8];
+#pragma unroll
+          for (int x = 0; x < 8; ++x) {
+            Fx[x] = __shfl_sync(0xffffffffu, E6v, x);
+            Bx[x] = __shfl_sync(0xffffffffu, Bv, x);
+            wyx[x] = __shfl_sync(0xffffffffu, wyv, x);
+          }
+          // Lanes = steps: lane q evaluates step sN+q+1 of the run for all blocks.
+          int64_t P = 0, V6prev = 0, Awprev = 0;
           int sN = 0;
           bool phase_end = false;
           const int nused0 = nused;
           const int64_t Dl0 = Dl;
           while (sN < Tm) {
-            const int cnt = min(kChunk, Tm - sN);
-            int64_t V6q[kChunk], Awq[kChunk], Axq[kChunk];
-            int rq[kChunk], cq[kChunk];
+            const int cnt = min(32, Tm - sN);
+            const bool live = lane < cnt;
+            const int pos = base + sN + (live ? lane : 0);
+            const int64_t V6 = static_cast<int64_t>(ws) - Btab[pos];
+            const int r = rtab[pos];
+            const int c = ord[pos];
+            const int64_t Aw = A[static_cast<size_t>(pos) * 8 + ws];
+            int64_t Ax[8];
+            {
+              const longlong2* row = reinterpret_cast<const longlong2*>(A + static_cast<size_t>(pos) * 8);
 #pragma unroll
-            for (int q = 0; q < kChunk; ++q) {
-              const int pos = base + sN + (q < cnt ? q : 0);
-              V6q[q] = static_cast<int64_t>(ws) - Btab[pos];
-              rq[q] = rtab[pos];
-              cq[q] = ord[pos];
-              Awq[q] = A[static_cast<size_t>(pos) * 8 + ws];
-              Axq[q] = Alane[static_cast<size_t>(pos) * 8];
+              for (int h = 0; h < 4; ++h) {
+                const longlong2 v2 = row[h];
+                Ax[2 * h] = v2.x;
+                Ax[2 * h + 1] = v2.y;
+              }
             }
-            // deltas (independent), then depth-3 prefix sum / prefix min
-            int64_t Pq[kChunk], Cq[kChunk], Fb[kChunk], Fa[kChunk];
-#pragma unroll
-            for (int q = 0; q < kChunk; ++q) {
-              const int64_t vp = q == 0 ? V6prev : V6q[q - 1];
-              const int64_t ap = q == 0 ? Awprev : Awq[q - 1];
-              const int64_t d6 = (sN == 0 && q == 0) ? delta1 : (vp < ap ? vp : ap) - V6q[q];
-              Pq[q] = q < cnt ? d6 : 0;
+            int64_t V6p = __shfl_up_sync(0xffffffffu, V6, 1), Awp = __shfl_up_sync(0xffffffffu, Aw, 1);
+            if (lane == 0) {
+              V6p = V6prev;
+              Awp = Awprev;
             }
+            const bool first = sN == 0 && lane == 0;
+            int64_t Pt = first ? delta1 : (V6p < Awp ? V6p : Awp) - V6;
+            if (!live) Pt = 0;
 #pragma unroll
-            for (int off = 1; off < kChunk; off <<= 1) {
-#pragma unroll
-              for (int q = kChunk - 1; q >= off; --q) Pq[q] += Pq[q - off];
+            for (int off = 1; off < 32; off <<= 1) {  // inclusive prefix sum of the deltas
+              const int64_t y = __shfl_up_sync(0xffffffffu, Pt, off);
+              if (lane >= off) Pt += y;
             }
+            Pt += P;
+            bool fail = false;
+            unsigned impw = 0;
+            unsigned impm[8];
+            int64_t Fa[8];
 #pragma unroll
-            for (int q = 0; q < kChunk; ++q) {
-              Pq[q] += P;
-              Cq[q] = Axq[q] + Pq[q];  // relax candidate of step q
-              Fa[q] = Cq[q];
+            for (int x = 0; x < 8; ++x) {
+              const int64_t cand = Ax[x] + Pt;  // relax candidate of this step for block x
+              int64_t incl = cand;
+#pragma unroll
+              for (int off = 1; off < 32; off <<= 1) {  // inclusive prefix min over steps
+                const int64_t y = __shfl_up_sync(0xffffffffu, incl, off);
+                if (lane >= off) incl = y < incl ? y : incl;
+              }
+              int64_t excl = __shfl_up_sync(0xffffffffu, incl, 1);
+              const int64_t Fb = lane == 0 ? Fx[x] : (excl < Fx[x] ? excl : Fx[x]);  // F before the step
+              Fa[x] = cand < Fb ? cand : Fb;                                            // F after its relax
+              if (x < n && x != ws && !(Fb + Bx[x] - ws > Pt)) fail = true;           // x would win here
+              impm[x] = __ballot_sync(0xffffffffu, live && cand < Fb);
+              impw = x == ws ? impm[x] : impw;
             }
-#pragma unroll
-            for (int off = 1; off < kChunk; off <<= 1) {
-#pragma unroll
-              for (int q = kChunk - 1; q >= off; --q) Fa[q] = Fa[q - off] < Fa[q] ? Fa[q - off] : Fa[q];
-            }
-            unsigned failm = 0, impm = 0, freem = 0;
-#pragma unroll
-            for (int q = 0; q < kChunk; ++q) {
-              const int64_t incl = Fa[q] < F ? Fa[q] : F;               // F after the relax of step q
-              Fb[q] = q == 0 ? F : (Fa[q - 1] < F ? Fa[q - 1] : F);     // F before step q
-              Fa[q] = incl;
-              const bool live = q < cnt;
-              const bool first = sN == 0 && q == 0;
-              failm |= (live && !first && !mine && !(Fb[q] + Bx_w > Pq[q])) ? (1u << q) : 0u;
-              freem |= (live && rq[q] == 0) ? (1u << q) : 0u;
-              impm |= (live && Cq[q] < Fb[q]) ? (1u << q) : 0u;
-            }
-            const int failq = failm ? __ffs(failm) - 1 : kChunk;
-            const int freeq = freem ? __ffs(freem) - 1 : kChunk;
-            impm &= freeq < kChunk ? ((1u << freeq) - 1u) : 0xffu;  // no relax at/after a free column
-            V6prev = V6q[kChunk - 1];
-            Awprev = Awq[kChunk - 1];
-            const int fail = static_cast<int>(__reduce_min_sync(0xffffffffu, static_cast<unsigned>(failq)));
-            int vq = fail < cnt ? fail : cnt;
+            const unsigned failm = __ballot_sync(0xffffffffu, live && !first && fail);
+            const unsigned freem = __ballot_sync(0xffffffffu, live && r == 0);
+            const int failq = failm ? __ffs(failm) - 1 : 32;
+            const int freeq = freem ? __ffs(freem) - 1 : 32;
+            int vq = failq < cnt ? failq : cnt;
             if (freeq < vq) {
               vq = freeq + 1;
               phase_end = true;
             }
-            // commit steps q < vq of this chunk (way = last improving step before q)
-            const int wbase = nused0 + sN;
+            const unsigned relax_m = freeq < 32 ? ((1u << freeq) - 1u) : 0xffffffffu;  // no relax at a free column
+            int wyw = wyx[0];
 #pragma unroll
-            for (int q = 0; q < kChunk; ++q) {
-              if (q < vq) {
-                const unsigned prev = impm & ((1u << q) - 1u);
-                const int wy = prev ? wbase + 31 - __clz(prev) : wyv;
-                const int js = mine ? cq[q] : dummy;  // the winner's bookkeeping; others hit a dummy slot
-                wayi[js] = wy;
-                dlt[js] = Dl0 + (Pq[q] >> 6);
-                ulist[mine ? wbase + q : dummy] = cq[q];
+            for (int x = 1; x < 8; ++x) wyw = x == ws ? wyx[x] : wyw;
+            const int wbase = nused0 + sN;
+            if (lane < vq) {  // each lane commits its own step
+              const unsigned prev = impw & relax_m & ((1u << lane) - 1u);
+              wayi[c] = prev ? wbase + 31 - __clz(prev) : wyw;
+              dlt[c] = Dl0 + (Pt >> 6);
+              ulist[wbase + lane] = c;
+            }
+            if (vq > 0) {
+              P = __shfl_sync(0xffffffffu, Pt, vq - 1);
+              const unsigned cm = relax_m & (vq >= 32 ? 0xffffffffu : ((1u << vq) - 1u));
+#pragma unroll
+              for (int x = 0; x < 8; ++x) {
+                Fx[x] = __shfl_sync(0xffffffffu, Fa[x], vq - 1);
+                const unsigned mx2 = impm[x] & cm;
+                wyx[x] = mx2 ? wbase + 31 - __clz(mx2) : wyx[x];
               }
             }
-            const unsigned cm = impm & (vq >= 32 ? 0xffffffffu : ((1u << vq) - 1u));
-            wyv = cm ? wbase + 31 - __clz(cm) : wyv;
-            // P, F after the committed prefix: a forward select chain (no indexing,
-            // which the compiler would otherwise lower to local memory)
-#pragma unroll
-            for (int q = 0; q < kChunk; ++q) {
-              const bool take = q < vq;
-              P = take ? Pq[q] : P;
-              F = take ? Fa[q] : F;
-            }
+            V6prev = __shfl_sync(0xffffffffu, V6, 31);
+            Awprev = __shfl_sync(0xffffffffu, Aw, 31);
             sN += vq;
             if (vq < cnt || phase_end) break;
           }
@@ -1067,7 +1071,20 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
           Dl = Dl0 + (Ps >> 6);
           nused = nused0 + sN;
           steps += sN;
-          E6v = F - Ps;
+          {
+            int64_t fme = Fx[0];
+            int wme = wyx[0];
+#pragma unroll
+            for (int x = 1; x < 8; ++x) {
+              fme = x == lane ? Fx[x] : fme;
+              wme = x == lane ? wyx[x] : wme;
+            }
+            if (lane < n) {
+              E6v = fme - Ps;
+              wyv = wme;
+            }
+          }
+          const bool mine = lane == ws;
           {  // advance block ws by sN columns
             const uint32_t inc = static_cast<uint32_t>(sN) << ((ws & 3) * 8);
             cpl += ws < 4 ? inc : 0u;
