@@ -872,18 +872,37 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
   const long long c_start = clock64();
   for (int i = 1; i <= k; ++i) {
     const long long t0 = clock64();
-    // ---- operand tables for this row (all warps)
-    for (int idx = tid; idx < k; idx += blockDim.x) {
-      const int c = ord[idx];
-      const int r = p[c];
-      const int x = idx / mult;
-      rtab[idx] = r;
-      Btab[idx] = static_cast<int64_t>(x) - (v[c] << 6);
-      if (r > 0) {
-        const int64_t ur = u[r];
-        const int64_t* Sr = S + static_cast<size_t>(r - 1) * n;
-        int64_t* Ar = A + static_cast<size_t>(idx) * AST;
-        for (int w = 0; w < n; ++w) Ar[w] = (Sr[w] - ur) << 6;
+    // ---- operand tables for this row (all warps).  One thread per (position,
+    // worker) pair, 4 independent pairs in flight per thread: the chain
+    // ord -> p -> (u, S) is 3 dependent loads, so memory-level parallelism
+    // decides the cost.
+    {
+      const int pairs = k * n;
+      for (int e0 = tid; e0 < pairs; e0 += 4 * blockDim.x) {
+        int cc[4], rr[4], ii[4], ww[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int e = e0 + q * blockDim.x;
+          const int ee = e < pairs ? e : 0;
+          ii[q] = ee / n;
+          ww[q] = ee - ii[q] * n;
+          cc[q] = ord[ii[q]];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) rr[q] = p[cc[q]];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int e = e0 + q * blockDim.x;
+          if (e >= pairs) continue;
+          const int r = rr[q];
+          if (ww[q] == 0) {
+            rtab[ii[q]] = r;
+            Btab[ii[q]] = static_cast<int64_t>(ii[q] / mult) - (v[cc[q]] << 6);
+          }
+          if (r > 0)
+            A[static_cast<size_t>(ii[q]) * AST + ww[q]] =
+                (S[static_cast<size_t>(r - 1) * n + ww[q]] - u[r]) << 6;
+        }
       }
     }
     __syncthreads();
