@@ -917,315 +917,6 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
     }
     __syncthreads();
     const long long t1 = clock64();
-    c_step += t1 - t0;
-    if (scal[2]) {
-      if (tid == 0) atomicOr(flags + kFlagBadCost, 1);
-      return;
-    }
-    const int64_t Dl = scal[0];
-    const int nu = static_cast<int>(scal[1]);
-    for (int t = tid; t < nu; t += blockDim.x) {  // potentials (assign.hpp:131-138), lazily
-      const int j = ulist[t];
-      const int64_t d = Dl - dlt[j];
-      u[p[j]] += d;
-      v[j] -= d;
-    }
-    __syncthreads();
-    if (tid == 0) {  // augment (assign.hpp:141-145)
-      int jj = ulist[nu - 1];
-      do {
-        const int jp = way[jj];
-        p[jj] = p[jp];
-        jj = jp;
-      } while (jj != 0);
-    }
-    // re-key each touched block's consumed prefix (v changed), one block per warp
-    for (int w = warp; w < n; w += nw) {
-      const int P = cur_s[w];
-      if (P == 0) continue;
-      if (lane == 0) rekeyed += P;
-      int32_t* base = ord + w * mult;
-      int64_t* pv = rk_v + static_cast<size_t>(warp) * mult;
-      int32_t* sorted = rk_i + static_cast<size_t>(warp) * 2 * mult;
-      int32_t* merged = sorted + mult;
-      for (int t = lane; t < P; t += 32) pv[t] = v[base[t]];
-      __syncwarp();
-      for (int t = lane; t < P; t += 32) {
-        const int a = base[t];
-        const int64_t va = pv[t];
-        int rank = 0;
-        for (int s2 = 0; s2 < P; ++s2) {
-          const int64_t vb = pv[s2];
-          rank += (vb > va || (vb == va && base[s2] < a)) ? 1 : 0;
-        }
-        sorted[rank] = a;
-      }
-      __syncwarp();
-      const int Q = mult - P;
-      const int32_t* suf = base + P;
-      for (int t = lane; t < P; t += 32) {
-        const int a = sorted[t];
-        const int64_t va = v[a];
-        int lo2 = 0, hi2 = Q;  // suffix entries ordered before a
-        while (lo2 < hi2) {
-          const int mid = (lo2 + hi2) >> 1;
-          const int b2 = suf[mid];
-          const int64_t vb = v[b2];
-          if (vb > va || (vb == va && b2 < a)) lo2 = mid + 1;
-          else hi2 = mid;
-        }
-        merged[t + lo2] = a;
-      }
-      for (int t = lane; t < Q; t += 32) {
-        const int b2 = suf[t];
-        const int64_t vb = v[b2];
-        int lo2 = 0, hi2 = P;  // prefix entries ordered before b2
-        while (lo2 < hi2) {
-          const int mid = (lo2 + hi2) >> 1;
-          const int a = sorted[mid];
-          const int64_t va = v[a];
-          if (va > vb || (va == vb && a < b2)) lo2 = mid + 1;
-          else hi2 = mid;
-        }
-        merged[t + lo2] = b2;
-      }
-      __syncwarp();
-      for (int t = lane; t < mult; t += 32) base[t] = merged[t];
-      __syncwarp();
-    }
-    __syncthreads();
-    c_end += clock64() - t1;
-  }
-  for (int j = tid + 1; j <= k; j += blockDim.x) {
-    const int r = p[j] - 1;
-    if (col_of_row) col_of_row[r] = static_cast<uint64_t>(j - 1);
-    if (decision) {
-      const uint32_t row = order[r];
-      decision[row_ids ? row_ids[row] : row] = (j - 1) / mult;
-    }
-  }
-  if (tid == 0 && stats) {
-    stats[0] = steps;
-    stats[1] = c_step;
-    stats[2] = c_end;
-    stats[3] = 0;
-    stats[4] = 0;
-    stats[5] = 0;
-    stats[6] = rekeyed;
-    stats[7] = clock64() - c_start;
-  }
-}
-
-// Warp-wide bitonic sort of 32*E (hi, lo) keys held in registers, element
-// index i = e*32 + lane, ascending by (hi, lo).  Used to re-sort a block's
-// columns by (v desc, j asc) = ascending (-v, j) at the end of a row.
-template <int E>
-__device__ __forceinline__ void warp_bitonic_sort(int64_t (&hi)[E], int32_t (&lo)[E], int lane) {
-  constexpr int M = 32 * E;
-#pragma unroll
-  for (int size = 2; size <= M; size <<= 1) {
-#pragma unroll
-    for (int d = size >> 1; d > 0; d >>= 1) {
-      if (d >= 32) {
-        const int de = d >> 5;
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int pe = e ^ de;
-          if (pe > e) {
-            const bool asc = ((e * 32 + lane) & size) == 0;
-            const bool gt = hi[e] > hi[pe] || (hi[e] == hi[pe] && lo[e] > lo[pe]);
-            if (gt == asc) {
-              const int64_t th = hi[e];
-              const int32_t tl = lo[e];
-              hi[e] = hi[pe];
-              lo[e] = lo[pe];
-              hi[pe] = th;
-              lo[pe] = tl;
-            }
-          }
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int64_t oh = __shfl_xor_sync(0xffffffffu, hi[e], d);
-          const int32_t ol = __shfl_xor_sync(0xffffffffu, lo[e], d);
-          const bool asc = ((e * 32 + lane) & size) == 0;
-          const bool lower = (lane & d) == 0;
-          const bool other_less = oh < hi[e] || (oh == hi[e] && ol < lo[e]);
-          if ((lower == asc) ? other_less : !other_less) {
-            hi[e] = oh;
-            lo[e] = ol;
-          }
-        }
-      }
-    }
-  }
-}
-
-// Re-sorts ord[base .. base+mult) by (v desc, j asc) with one warp.
-template <int E>
-__device__ __forceinline__ void warp_resort_block(int32_t* ord, const int64_t* v, int base,
-                                                  int mult, int lane) {
-  int64_t hi[E];
-  int32_t lo[E];
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int i = e * 32 + lane;
-    if (i < mult) {
-      const int c = ord[base + i];
-      lo[e] = c;
-      hi[e] = -v[c];
-    } else {
-      lo[e] = INT_MAX;
-      hi[e] = LLONG_MAX;
-    }
-  }
-  warp_bitonic_sort<E>(hi, lo, lane);
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int i = e * 32 + lane;
-    if (i < mult) ord[base + i] = lo[e];
-  }
-}
-
-__device__ __forceinline__ void warp_resort_dispatch(int32_t* ord, const int64_t* v, int base,
-                                                     int mult, int lane) {
-  if (mult <= 32) warp_resort_block<1>(ord, v, base, mult, lane);
-  else if (mult <= 64) warp_resort_block<2>(ord, v, base, mult, lane);
-  else if (mult <= 128) warp_resort_block<4>(ord, v, base, mult, lane);
-  else if (mult <= 256) warp_resort_block<8>(ord, v, base, mult, lane);
-  else warp_resort_block<16>(ord, v, base, mult, lane);
-}
-
-// --------------------------------------------- K6 tabled (per-row operand table)
-// Fastest variant, used when the operand table fits in shared memory.  At the
-// start of each row (phase) all warps rebuild, for every block x and every
-// position d of its (v desc, j asc) column order,
-//     A[x][d][w] = (S[r][w] - u[r]) << 6,  r = p[ord[x][d]]   (relax operand)
-//     Btab[x][d] = x - (v[ord[x][d]] << 6)                    (key offset)
-//     rtab[x][d] = r                                          (0 = free column)
-// so that during the row a Dijkstra step only needs: key = E + B -> two
-// redux.sync.min.u32 -> one LDS of A[winner][cursor][lane] -> relax.  The
-// winner's bookkeeping uses values prefetched one consumption ahead, and the
-// per-block cursors are packed 8 bits each in one uniform register (n <= 8)
-// or kept in shared memory.  `way` is recorded as a step index (see the
-// fast kernel).  Row end is the same as the fast kernel.
-constexpr int kTabMaxWarps = 8;
-constexpr int kRunMax = 255;  // speculative run length cap of the batched Dijkstra steps
-constexpr int kChunk = 8;     // steps evaluated per speculation chunk
-
-template <int NB, int SMODE, bool PACK>  // SMODE 0: S shared, 1: S global
-__global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
-    k_hungarian_blocks_tab(const int64_t* __restrict__ S_global, int n, int mult, int k,
-                           const uint32_t* __restrict__ order, int32_t* __restrict__ decision,
-                           const uint32_t* __restrict__ row_ids, uint64_t* __restrict__ col_of_row,
-                           unsigned long long* stats, int* flags,
-                           const unsigned long long* __restrict__ max_scaled) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  const size_t K1 = static_cast<size_t>(k) + 1;
-  size_t so = 0;
-  auto stake = [&](size_t bytes) {
-    uint8_t* q = smem + so;
-    so += (bytes + 15) & ~size_t(15);
-    return q;
-  };
-  const int64_t* S;
-  if constexpr (SMODE == 0) {
-    int64_t* Ss = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(k) * n * 8));
-    for (size_t x = tid; x < static_cast<size_t>(k) * n; x += blockDim.x) Ss[x] = S_global[x];
-    S = Ss;
-  } else {
-    S = S_global;
-  }
-  const int AST = PACK ? 8 : n;  // row stride of the operand table
-  int64_t* A = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(k) * AST * 8));
-  int64_t* Btab = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(k) * 8));
-  int64_t* u = reinterpret_cast<int64_t*>(stake(K1 * 8));
-  int64_t* v = reinterpret_cast<int64_t*>(stake(K1 * 8));
-  int64_t* dlt = reinterpret_cast<int64_t*>(stake((K1 + 32) * 8));
-  int32_t* p = reinterpret_cast<int32_t*>(stake(K1 * 4));
-  int32_t* wayi = reinterpret_cast<int32_t*>(stake((K1 + 32) * 4));
-  int32_t* ulist = reinterpret_cast<int32_t*>(stake((K1 + 32) * 4));
-  int32_t* ord = reinterpret_cast<int32_t*>(stake(K1 * 4));
-  int32_t* rtab = reinterpret_cast<int32_t*>(stake(K1 * 4));
-  int32_t* curs = reinterpret_cast<int32_t*>(stake(64 * 4));
-  int64_t* scal = reinterpret_cast<int64_t*>(stake(4 * 8));
-  int64_t* rk_v = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(nw) * mult * 8));
-  int32_t* rk_i = reinterpret_cast<int32_t*>(stake(static_cast<size_t>(nw) * 2 * mult * 4));
-  if (so > dynamic_smem_bytes()) {  // host/device layout mismatch: fail loudly, touch nothing
-    if (tid == 0) atomicOr(flags + kFlagInternal, 1);
-    return;
-  }
-
-  const unsigned long long mx = *max_scaled;
-  const bool packable = mx < (1ULL << 57) / (8ULL * static_cast<unsigned long long>(k + 1));
-  for (size_t x = tid; x < K1; x += blockDim.x) {
-    u[x] = 0;
-    v[x] = 0;
-    p[x] = 0;
-    wayi[x] = 0;
-  }
-  for (int x = tid; x < k; x += blockDim.x) ord[x] = x + 1;
-  if (tid == 0) scal[2] = 0;
-  __syncthreads();
-  if (!packable) {  // wide-range path (see k_hungarian_blocks_wide)
-    if (warp == 0) {
-      BlockArrays Aw{S, u, v, dlt, p, wayi, ulist, ord, rk_i};
-      if (!hungarian_blocks_warp<NB>(Aw, n, mult, k, stats, flags)) return;
-      __syncwarp();
-      for (int j = lane + 1; j <= k; j += 32) {
-        const int r = p[j] - 1;
-        if (col_of_row) col_of_row[r] = static_cast<uint64_t>(j - 1);
-        if (decision) {
-          const uint32_t row = order[r];
-          decision[row_ids ? row_ids[row] : row] = (j - 1) / mult;
-        }
-      }
-    }
-    return;
-  }
-
-  unsigned long long steps = 0;
-  long long c_step = 0, c_end = 0, c_tab = 0, rekeyed = 0, c_pot = 0, p2 = 0, pmax = 0, runs = 0;
-  const long long c_start = clock64();
-  for (int i = 1; i <= k; ++i) {
-    const long long t0 = clock64();
-    // ---- operand tables for this row (all warps).  One thread per (position,
-    // worker) pair, 4 independent pairs in flight per thread: the chain
-    // ord -> p -> (u, S) is 3 dependent loads, so memory-level parallelism
-    // decides the cost.
-    {
-      const int pairs = k * n;
-      for (int e0 = tid; e0 < pairs; e0 += 4 * blockDim.x) {
-        int cc[4], rr[4], ii[4], ww[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int e = e0 + q * blockDim.x;
-          const int ee = e < pairs ? e : 0;
-          ii[q] = ee / n;
-          ww[q] = ee - ii[q] * n;
-          cc[q] = ord[ii[q]];
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) rr[q] = p[cc[q]];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int e = e0 + q * blockDim.x;
-          if (e >= pairs) continue;
-          const int r = rr[q];
-          if (ww[q] == 0) {
-            rtab[ii[q]] = r;
-            Btab[ii[q]] = static_cast<int64_t>(ii[q] / mult) - (v[cc[q]] << 6);
-          }
-          if (r > 0)
-            A[static_cast<size_t>(ii[q]) * AST + ww[q]] =
-                (S[static_cast<size_t>(r - 1) * n + ww[q]] - u[r]) << 6;
-        }
-      }
-    }
-    __syncthreads();
-    const long long t1 = clock64();
     c_tab += t1 - t0;
     if (warp == 0) {
       int64_t E6[NB], B[NB], Bn[NB];
