@@ -1308,6 +1308,331 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
   }
 }
 
+// ------------------------------------------- K6 run kernel (n <= 32, lanes = blocks)
+// The production solver for n <= 32.  Same per-row operand table and row
+// end as the tabled kernel; the Dijkstra steps are evaluated in runs (see the
+// derivation above): the argmin picks block w, then chunks of up to 32
+// consecutive steps are evaluated assuming w keeps winning.  In a chunk the
+// warp first works lanes = steps (load the candidates of w, scan the delta
+// sums P_t), then lanes = blocks: lane x walks the chunk's steps in order,
+// checking F_x + B_x - w > P_t (x would not win step t) and relaxing
+// F_x = min(F_x, A_x(r_t) + P_t), snapshotting F_x per step.  One REDUX gives
+// the first step some block would win; each lane then commits its own step.
+// AMODE 0: S and the table in shared memory; 1: S global; 2: S and table
+// global (L2; each chunk's loads are issued together).
+constexpr int kRunWarps = 8;
+
+template <int AMODE>
+__global__ void __launch_bounds__(kRunWarps * 32, 1)
+    k_hungarian_blocks_run(const int64_t* __restrict__ S_global, int n, int mult, int k,
+                           int64_t* __restrict__ A_global, const uint32_t* __restrict__ order,
+                           int32_t* __restrict__ decision, const uint32_t* __restrict__ row_ids,
+                           uint64_t* __restrict__ col_of_row, unsigned long long* stats,
+                           int* flags, const unsigned long long* __restrict__ max_scaled) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const size_t K1 = static_cast<size_t>(k) + 1;
+  size_t so = 0;
+  auto stake = [&](size_t bytes) {
+    uint8_t* q = smem + so;
+    so += (bytes + 15) & ~size_t(15);
+    return q;
+  };
+  const int64_t* S;
+  if constexpr (AMODE == 0) {
+    int64_t* Ss = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(k) * n * 8));
+    for (size_t x = tid; x < static_cast<size_t>(k) * n; x += blockDim.x) Ss[x] = S_global[x];
+    S = Ss;
+  } else {
+    S = S_global;
+  }
+  int64_t* A;
+  if constexpr (AMODE <= 1) A = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(k) * n * 8));
+  else A = A_global;
+  int64_t* Btab = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(k) * 8));
+  int64_t* u = reinterpret_cast<int64_t*>(stake(K1 * 8));
+  int64_t* v = reinterpret_cast<int64_t*>(stake(K1 * 8));
+  int64_t* dlt = reinterpret_cast<int64_t*>(stake(K1 * 8));
+  int32_t* p = reinterpret_cast<int32_t*>(stake(K1 * 4));
+  int32_t* wayi = reinterpret_cast<int32_t*>(stake(K1 * 4));
+  int32_t* ulist = reinterpret_cast<int32_t*>(stake(K1 * 4));
+  int32_t* ord = reinterpret_cast<int32_t*>(stake(K1 * 4));
+  int32_t* rtab = reinterpret_cast<int32_t*>(stake(K1 * 4));
+  int32_t* curs = reinterpret_cast<int32_t*>(stake(64 * 4));
+  int64_t* Ps = reinterpret_cast<int64_t*>(stake(32 * 8));
+  int64_t* Fsnap = reinterpret_cast<int64_t*>(stake(32 * 32 * 8));
+  int64_t* scal = reinterpret_cast<int64_t*>(stake(4 * 8));
+  int64_t* rk_v = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(nw) * mult * 8));
+  int32_t* rk_i = reinterpret_cast<int32_t*>(stake(static_cast<size_t>(nw) * 2 * mult * 4));
+  if (so > dynamic_smem_bytes()) {  // host/device layout mismatch: fail loudly, touch nothing
+    if (tid == 0) atomicOr(flags + kFlagInternal, 1);
+    return;
+  }
+  const unsigned long long mx = *max_scaled;
+  const bool packable = mx < (1ULL << 57) / (8ULL * static_cast<unsigned long long>(k + 1));
+  for (size_t x = tid; x < K1; x += blockDim.x) {
+    u[x] = 0;
+    v[x] = 0;
+    p[x] = 0;
+    wayi[x] = 0;
+  }
+  for (int x = tid; x < k; x += blockDim.x) ord[x] = x + 1;
+  if (tid == 0) scal[2] = 0;
+  __syncthreads();
+  if (!packable) {  // wide-range path (see k_hungarian_blocks_wide)
+    if (warp == 0) {
+      BlockArrays Aw{S, u, v, dlt, p, wayi, ulist, ord, rk_i};
+      if (!hungarian_blocks_warp<1>(Aw, n, mult, k, stats, flags)) return;
+      __syncwarp();
+      for (int j = lane + 1; j <= k; j += 32) {
+        const int r = p[j] - 1;
+        if (col_of_row) col_of_row[r] = static_cast<uint64_t>(j - 1);
+        if (decision) {
+          const uint32_t row = order[r];
+          decision[row_ids ? row_ids[row] : row] = (j - 1) / mult;
+        }
+      }
+    }
+    return;
+  }
+
+  constexpr int64_t kBig = 1LL << 62;
+  const int xl = lane < n ? lane : 0;  // this lane's block column (clamped for inert lanes)
+  unsigned long long steps = 0;
+  long long c_step = 0, c_end = 0, c_tab = 0, runs = 0;
+  const long long c_start = clock64();
+  for (int i = 1; i <= k; ++i) {
+    const long long t0 = clock64();
+    // ---- operand table (all warps), two positions per thread
+    for (int i0 = tid; i0 < k; i0 += 2 * blockDim.x) {
+      const int i1 = i0 + blockDim.x;
+      const bool h1 = i1 < k;
+      const int c0 = ord[i0], c1 = h1 ? ord[i1] : c0;
+      const int r0 = p[c0], r1 = p[c1];
+      const int64_t u0 = u[r0], u1 = u[r1];
+      rtab[i0] = r0;
+      Btab[i0] = static_cast<int64_t>(i0 / mult) - (v[c0] << 6);
+      if (h1) {
+        rtab[i1] = r1;
+        Btab[i1] = static_cast<int64_t>(i1 / mult) - (v[c1] << 6);
+      }
+      if (r0 > 0)
+        for (int w = 0; w < n; ++w)
+          A[static_cast<size_t>(i0) * n + w] = (S[static_cast<size_t>(r0 - 1) * n + w] - u0) << 6;
+      if (h1 && r1 > 0)
+        for (int w = 0; w < n; ++w)
+          A[static_cast<size_t>(i1) * n + w] = (S[static_cast<size_t>(r1 - 1) * n + w] - u1) << 6;
+    }
+    if constexpr (AMODE == 2) __threadfence_block();
+    __syncthreads();
+    const long long t1 = clock64();
+    c_tab += t1 - t0;
+    if (warp == 0) {
+      // lane x < n owns block x: E = D_x - Δ (<< 6), B = x - (v(candidate) << 6), way index
+      int64_t E6v = 0, Bv = kBig;
+      int wyv = 0;
+      if (lane < n) {
+        E6v = (S[static_cast<size_t>(i - 1) * n + lane] - u[i]) << 6;  // relax from row i
+        Bv = Btab[lane * mult];
+        curs[lane] = 0;
+      }
+      if (lane == 0) {
+        p[0] = i;
+        ulist[0] = 0;
+        dlt[0] = 0;
+      }
+      __syncwarp();
+      int nused = 1;
+      int64_t Dl = 0;
+      bool abort = false;
+      for (;;) {  // runs
+        const uint64_t key = static_cast<uint64_t>(E6v + Bv);
+        const unsigned hi = static_cast<unsigned>(key >> 32), lo = static_cast<unsigned>(key);
+        const unsigned mh = __reduce_min_sync(0xffffffffu, hi);
+        const unsigned ml = __reduce_min_sync(0xffffffffu, hi == mh ? lo : 0xffffffffu);
+        if (ml == 0xffffffffu && mh == 0xffffffffu) {
+          abort = true;
+          break;
+        }
+        const int ws = min(static_cast<int>(ml & 63u), n - 1);
+        const int64_t delta1 = static_cast<int64_t>(((static_cast<uint64_t>(mh) << 32) | ml) & ~63ULL);
+        const int d = curs[ws];
+        const int base = ws * mult + d;
+        const int Tm = mult - d;
+        const int wyw0 = __shfl_sync(0xffffffffu, wyv, ws);
+        const bool check = lane < n && lane != ws;
+        int64_t P = 0, F = E6v, V6prev = 0, Awprev = 0;
+        int sN = 0, wyw = wyw0;
+        bool phase_end = false;
+        const int nused0 = nused;
+        const int64_t Dl0 = Dl;
+        while (sN < Tm) {
+          const int cnt = min(32, Tm - sN);
+          // -- lanes = steps: the winner's candidates and the running delta sums
+          const bool live = lane < cnt;
+          const int pos = base + sN + (live ? lane : 0);
+          const int64_t V6 = static_cast<int64_t>(ws) - Btab[pos];
+          const int64_t Aw = A[static_cast<size_t>(pos) * n + ws];
+          const int r = rtab[pos];
+          const int c = ord[pos];
+          int64_t V6p = __shfl_up_sync(0xffffffffu, V6, 1), Awp = __shfl_up_sync(0xffffffffu, Aw, 1);
+          if (lane == 0) {
+            V6p = V6prev;
+            Awp = Awprev;
+          }
+          const bool first = sN == 0 && lane == 0;
+          int64_t Pt = first ? delta1 : (V6p < Awp ? V6p : Awp) - V6;
+          if (!live) Pt = 0;
+#pragma unroll
+          for (int off = 1; off < 32; off <<= 1) {
+            const int64_t y = __shfl_up_sync(0xffffffffu, Pt, off);
+            if (lane >= off) Pt += y;
+          }
+          Pt += P;
+          Ps[lane] = Pt;
+          const unsigned freem = __ballot_sync(0xffffffffu, live && r == 0);
+          const int freeq = freem ? __ffs(freem) - 1 : 32;
+          const int tl = cnt < freeq + 1 ? cnt : freeq + 1;
+          __syncwarp();
+          // -- lanes = blocks: walk the chunk's steps in order
+          const int64_t F_in = F;
+          int failt = 32;
+          unsigned impm = 0;
+          const int64_t Gb = Bv - ws;  // key offset relative to the winner
+          for (int t0 = 0; t0 < tl; t0 += 8) {
+            int64_t Ax[8], Pq[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const int t = t0 + q < tl ? t0 + q : t0;
+              Ax[q] = A[static_cast<size_t>(base + sN + t) * n + xl];
+              Pq[q] = Ps[t];
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const int t = t0 + q;
+              if (t < tl) {
+                if (check && failt == 32 && !(sN == 0 && t == 0) && !(F + Gb > Pq[q])) failt = t;
+                const int64_t cand = Ax[q] + Pq[q];
+                if (t != freeq && cand < F) {
+                  F = cand;
+                  impm |= 1u << t;
+                }
+                Fsnap[t * 32 + lane] = F;
+              }
+            }
+          }
+          const int fail = static_cast<int>(__reduce_min_sync(0xffffffffu, static_cast<unsigned>(failt)));
+          int vq = fail < cnt ? fail : cnt;
+          if (freeq < vq) {
+            vq = freeq + 1;
+            phase_end = true;
+          }
+          const unsigned impw = __shfl_sync(0xffffffffu, impm, ws);
+          const int wbase = nused0 + sN;
+          if (lane < vq) {  // lanes = steps again: each lane commits its own step
+            const unsigned prev = impw & ((1u << lane) - 1u);
+            wayi[c] = prev ? wbase + 31 - __clz(prev) : wyw;
+            dlt[c] = Dl0 + (Pt >> 6);
+            ulist[wbase + lane] = c;
+          }
+          __syncwarp();
+          if (vq > 0) {
+            P = __shfl_sync(0xffffffffu, Pt, vq - 1);
+            F = Fsnap[(vq - 1) * 32 + lane];
+            const unsigned cm = impm & (vq >= 32 ? 0xffffffffu : ((1u << vq) - 1u));
+            wyv = cm ? wbase + 31 - __clz(cm) : wyv;
+            const unsigned cw = impw & (vq >= 32 ? 0xffffffffu : ((1u << vq) - 1u));
+            wyw = cw ? wbase + 31 - __clz(cw) : wyw;
+          } else {
+            F = F_in;
+          }
+          V6prev = __shfl_sync(0xffffffffu, V6, 31);
+          Awprev = __shfl_sync(0xffffffffu, Aw, 31);
+          sN += vq;
+          if (vq < cnt || phase_end) break;
+        }
+        ++runs;
+        Dl = Dl0 + (P >> 6);
+        nused = nused0 + sN;
+        steps += sN;
+        if (lane < n) E6v = F - P;
+        if (lane == ws) {
+          curs[ws] = d + sN;
+          Bv = d + sN < mult ? Btab[base + sN] : kBig;
+        }
+        __syncwarp();
+        if (phase_end) break;
+      }
+      if (lane == 0) {
+        scal[0] = Dl;
+        scal[1] = nused;
+        if (abort) scal[2] = 1;
+      }
+    }
+    __syncthreads();
+    const long long t2 = clock64();
+    c_step += t2 - t1;
+    if (scal[2]) {
+      if (tid == 0) atomicOr(flags + kFlagBadCost, 1);
+      return;
+    }
+    const int64_t Dl = scal[0];
+    const int nu = static_cast<int>(scal[1]);
+    for (int t = tid; t < nu; t += blockDim.x) {  // potentials (assign.hpp:131-138)
+      const int j = ulist[t];
+      const int64_t dd = Dl - dlt[j];
+      u[p[j]] += dd;
+      v[j] -= dd;
+    }
+    __syncthreads();
+    if (tid == 0) {  // augment (assign.hpp:141-145); way[j] = ulist[wayi[j]]
+      int jj = ulist[nu - 1];
+      do {
+        const int jp = ulist[wayi[jj]];
+        p[jj] = p[jp];
+        jj = jp;
+      } while (jj != 0);
+    }
+    for (int w = warp; w < n; w += nw) {  // re-sort the touched blocks
+      if (curs[w] == 0) continue;
+      warp_resort_dispatch(ord, v, w * mult, mult, lane);
+      __syncwarp();
+    }
+    __syncthreads();
+    c_end += clock64() - t2;
+  }
+  for (int j = tid + 1; j <= k; j += blockDim.x) {
+    const int r = p[j] - 1;
+    if (col_of_row) col_of_row[r] = static_cast<uint64_t>(j - 1);
+    if (decision) {
+      const uint32_t row = order[r];
+      decision[row_ids ? row_ids[row] : row] = (j - 1) / mult;
+    }
+  }
+  if (tid == 0 && stats) {
+    stats[0] = steps;
+    stats[1] = c_step;
+    stats[2] = c_end;
+    stats[3] = c_tab;
+    stats[4] = 0;
+    stats[5] = runs;
+    stats[6] = 0;
+    stats[7] = clock64() - c_start;
+  }
+}
+
+size_t run_smem_bytes(int k, int n, int mult, int nw, int amode) {
+  const size_t K1 = static_cast<size_t>(k) + 1;
+  auto r = [](size_t b) { return (b + 15) & ~size_t(15); };
+  size_t b = 0;
+  if (amode == 0) b += r(static_cast<size_t>(k) * n * 8);
+  if (amode <= 1) b += r(static_cast<size_t>(k) * n * 8);
+  b += r(static_cast<size_t>(k) * 8) + 3 * r(K1 * 8) + 5 * r(K1 * 4) + r(64 * 4) + r(32 * 8) +
+       r(32 * 32 * 8) + r(32) + r(static_cast<size_t>(nw) * mult * 8) +
+       r(static_cast<size_t>(nw) * 2 * mult * 4);
+  return b;
+}
+
 // ----------------------------------------------------------------- K5 dense
 // The reference loop on an arbitrary k x k matrix: one CTA, columns strided
 // over threads, block-wide argmin with the lowest column winning ties.
@@ -1509,6 +1834,30 @@ void launch_hungarian_blocks(HungarianScratch& sc, const double* matrix, int n,
   EDX_LAUNCHED();
   const size_t limit = static_cast<size_t>(max_dyn_smem(device));
   const int nw = std::min(n, kFastMaxWarps);
+  if (n <= 32 && mult <= 512) {  // the run-batched kernel
+    const int nwr = std::min(n, kRunWarps);
+    for (int am = 0; am <= 2; ++am) {
+      const size_t smem = run_smem_bytes(k, n, mult, nwr, am);
+      if (smem > limit) continue;
+      int64_t* Ag = nullptr;
+      if (am == 2) {
+        sc.arena.ensure(static_cast<size_t>(k) * n * 8);
+        Ag = reinterpret_cast<int64_t*>(sc.arena.p);
+      }
+      auto launch = [&](auto kern) {
+        if (smem > 48 * 1024)
+          EDX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem)));
+        kern<<<1, 32 * nwr, smem, s>>>(sc.s64.p, n, mult, k, Ag, order, decision, row_ids,
+                                       col_of_row, sc.steps.p, flags, max_scaled);
+      };
+      if (am == 0) launch(k_hungarian_blocks_run<0>);
+      else if (am == 1) launch(k_hungarian_blocks_run<1>);
+      else launch(k_hungarian_blocks_run<2>);
+      EDX_LAUNCHED();
+      return;
+    }
+  }
   // tabled kernel when its per-row operand table fits in shared memory
   const int nwt = std::min(n, kTabMaxWarps);
   for (int sm = 0; sm <= 1; ++sm) {
