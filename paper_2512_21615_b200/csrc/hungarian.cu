@@ -1349,7 +1349,7 @@ __global__ void __launch_bounds__(kRunWarps * 32, 1)
   int64_t* A;
   if constexpr (AMODE <= 1) A = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(k) * n * 8));
   else A = A_global;
-  int64_t* Btab = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(k) * 8));
+  int64_t* Btab = reinterpret_cast<int64_t*>(stake(K1 * 8));  // by column: block - (v << 6)
   int64_t* u = reinterpret_cast<int64_t*>(stake(K1 * 8));
   int64_t* v = reinterpret_cast<int64_t*>(stake(K1 * 8));
   int64_t* dlt = reinterpret_cast<int64_t*>(stake(K1 * 8));
@@ -1360,6 +1360,7 @@ __global__ void __launch_bounds__(kRunWarps * 32, 1)
   int32_t* rtab = reinterpret_cast<int32_t*>(stake(K1 * 4));
   int32_t* curs = reinterpret_cast<int32_t*>(stake(64 * 4));
   int64_t* Ps = reinterpret_cast<int64_t*>(stake(32 * 8));
+  int32_t* Cs = reinterpret_cast<int32_t*>(stake(32 * 4));
   int64_t* Fsnap = reinterpret_cast<int64_t*>(stake(32 * 32 * 8));
   int64_t* scal = reinterpret_cast<int64_t*>(stake(4 * 8));
   int64_t* rk_v = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(nw) * mult * 8));
@@ -1403,25 +1404,14 @@ __global__ void __launch_bounds__(kRunWarps * 32, 1)
   const long long c_start = clock64();
   for (int i = 1; i <= k; ++i) {
     const long long t0 = clock64();
-    // ---- operand table (all warps), two positions per thread
-    for (int i0 = tid; i0 < k; i0 += 2 * blockDim.x) {
-      const int i1 = i0 + blockDim.x;
-      const bool h1 = i1 < k;
-      const int c0 = ord[i0], c1 = h1 ? ord[i1] : c0;
-      const int r0 = p[c0], r1 = p[c1];
-      const int64_t u0 = u[r0], u1 = u[r1];
-      rtab[i0] = r0;
-      Btab[i0] = static_cast<int64_t>(i0 / mult) - (v[c0] << 6);
-      if (h1) {
-        rtab[i1] = r1;
-        Btab[i1] = static_cast<int64_t>(i1 / mult) - (v[c1] << 6);
+    // Operand tables are indexed by column: A[c] = (S[p[c]] - u[p[c]]) << 6,
+    // B[c] = block(c) - (v[c] << 6), r[c] = p[c].  Only the columns reached in a
+    // row change (see the row end), so they are updated incrementally there.
+    if (i == 1) {
+      for (int c = tid + 1; c <= k; c += blockDim.x) {
+        rtab[c] = 0;
+        Btab[c] = static_cast<int64_t>((c - 1) / mult);
       }
-      if (r0 > 0)
-        for (int w = 0; w < n; ++w)
-          A[static_cast<size_t>(i0) * n + w] = (S[static_cast<size_t>(r0 - 1) * n + w] - u0) << 6;
-      if (h1 && r1 > 0)
-        for (int w = 0; w < n; ++w)
-          A[static_cast<size_t>(i1) * n + w] = (S[static_cast<size_t>(r1 - 1) * n + w] - u1) << 6;
     }
     if constexpr (AMODE == 2) __threadfence_block();
     __syncthreads();
@@ -1433,7 +1423,7 @@ __global__ void __launch_bounds__(kRunWarps * 32, 1)
       int wyv = 0;
       if (lane < n) {
         E6v = (S[static_cast<size_t>(i - 1) * n + lane] - u[i]) << 6;  // relax from row i
-        Bv = Btab[lane * mult];
+        Bv = Btab[ord[lane * mult]];
         curs[lane] = 0;
       }
       if (lane == 0) {
@@ -1471,10 +1461,11 @@ __global__ void __launch_bounds__(kRunWarps * 32, 1)
           // -- lanes = steps: the winner's candidates and the running delta sums
           const bool live = lane < cnt;
           const int pos = base + sN + (live ? lane : 0);
-          const int64_t V6 = static_cast<int64_t>(ws) - Btab[pos];
-          const int64_t Aw = A[static_cast<size_t>(pos) * n + ws];
-          const int r = rtab[pos];
           const int c = ord[pos];
+          const int64_t V6 = static_cast<int64_t>(ws) - Btab[c];
+          const int r = rtab[c];
+          const int64_t Aw = A[static_cast<size_t>(c - 1) * n + ws];
+          Cs[lane] = c;
           int64_t V6p = __shfl_up_sync(0xffffffffu, V6, 1), Awp = __shfl_up_sync(0xffffffffu, Aw, 1);
           if (lane == 0) {
             V6p = V6prev;
@@ -1504,7 +1495,7 @@ __global__ void __launch_bounds__(kRunWarps * 32, 1)
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
               const int t = t0 + q < tl ? t0 + q : t0;
-              Ax[q] = A[static_cast<size_t>(base + sN + t) * n + xl];
+              Ax[q] = A[static_cast<size_t>(Cs[t] - 1) * n + xl];
               Pq[q] = Ps[t];
             }
 #pragma unroll
@@ -1558,7 +1549,7 @@ __global__ void __launch_bounds__(kRunWarps * 32, 1)
         if (lane < n) E6v = F - P;
         if (lane == ws) {
           curs[ws] = d + sN;
-          Bv = d + sN < mult ? Btab[base + sN] : kBig;
+          Bv = d + sN < mult ? Btab[ord[base + sN]] : kBig;
         }
         __syncwarp();
         if (phase_end) break;
@@ -1599,6 +1590,19 @@ __global__ void __launch_bounds__(kRunWarps * 32, 1)
       __syncwarp();
     }
     __syncthreads();
+    // refresh the operand table of the reached columns (their row or its
+    // potential changed; every other column is unchanged)
+    for (int e = tid; e < (nu - 1) * n; e += blockDim.x) {
+      const int c = ulist[1 + e / n], w = e - (e / n) * n;
+      const int r = p[c];
+      if (w == 0) {
+        rtab[c] = r;
+        Btab[c] = static_cast<int64_t>((c - 1) / mult) - (v[c] << 6);
+      }
+      A[static_cast<size_t>(c - 1) * n + w] = (S[static_cast<size_t>(r - 1) * n + w] - u[r]) << 6;
+    }
+    if constexpr (AMODE == 2) __threadfence_block();
+    __syncthreads();
     c_end += clock64() - t2;
   }
   for (int j = tid + 1; j <= k; j += blockDim.x) {
@@ -1627,7 +1631,7 @@ size_t run_smem_bytes(int k, int n, int mult, int nw, int amode) {
   size_t b = 0;
   if (amode == 0) b += r(static_cast<size_t>(k) * n * 8);
   if (amode <= 1) b += r(static_cast<size_t>(k) * n * 8);
-  b += r(static_cast<size_t>(k) * 8) + 3 * r(K1 * 8) + 5 * r(K1 * 4) + r(64 * 4) + r(32 * 8) +
+  b += r(K1 * 8) + 3 * r(K1 * 8) + 5 * r(K1 * 4) + r(64 * 4) + r(32 * 8) + r(32 * 4) +
        r(32 * 32 * 8) + r(32) + r(static_cast<size_t>(nw) * mult * 8) +
        r(static_cast<size_t>(nw) * 2 * mult * 4);
   return b;
