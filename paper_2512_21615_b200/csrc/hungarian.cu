@@ -821,7 +821,7 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
   }
   const int AST = PACK ? 8 : n;  // row stride of the operand table
   int64_t* A = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(k) * AST * 8));
-  int64_t* Btab = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(k) * 8));
+  int64_t* Btab = reinterpret_cast<int64_t*>(stake(K1 * 8));  // by column: block - (v << 6)
   int64_t* u = reinterpret_cast<int64_t*>(stake(K1 * 8));
   int64_t* v = reinterpret_cast<int64_t*>(stake(K1 * 8));
   int64_t* dlt = reinterpret_cast<int64_t*>(stake((K1 + 32) * 8));
@@ -872,47 +872,13 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
   const long long c_start = clock64();
   for (int i = 1; i <= k; ++i) {
     const long long t0 = clock64();
-    // ---- operand tables for this row (all warps): one thread per position,
-    // two positions in flight (the chain ord -> p -> (u, S) is 3 dependent
-    // loads), 16-byte row loads/stores when a row is exactly 8 workers.
-    for (int i0 = tid; i0 < k; i0 += 2 * blockDim.x) {
-      const int i1 = i0 + blockDim.x;
-      const bool h1 = i1 < k;
-      const int c0 = ord[i0], c1 = h1 ? ord[i1] : c0;
-      const int r0 = p[c0], r1 = p[c1];
-      const int64_t u0 = u[r0], u1 = u[r1];
-      rtab[i0] = r0;
-      Btab[i0] = static_cast<int64_t>(i0 / mult) - (v[c0] << 6);
-      if (h1) {
-        rtab[i1] = r1;
-        Btab[i1] = static_cast<int64_t>(i1 / mult) - (v[c1] << 6);
-      }
-      if (AST == 8 && n == 8) {
-        if (r0 > 0) {
-          const longlong2* Sr = reinterpret_cast<const longlong2*>(S + static_cast<size_t>(r0 - 1) * 8);
-          longlong2* Ar = reinterpret_cast<longlong2*>(A + static_cast<size_t>(i0) * 8);
-#pragma unroll
-          for (int h = 0; h < 4; ++h) {
-            const longlong2 sv = Sr[h];
-            Ar[h] = make_longlong2((sv.x - u0) << 6, (sv.y - u0) << 6);
-          }
-        }
-        if (h1 && r1 > 0) {
-          const longlong2* Sr = reinterpret_cast<const longlong2*>(S + static_cast<size_t>(r1 - 1) * 8);
-          longlong2* Ar = reinterpret_cast<longlong2*>(A + static_cast<size_t>(i1) * 8);
-#pragma unroll
-          for (int h = 0; h < 4; ++h) {
-            const longlong2 sv = Sr[h];
-            Ar[h] = make_longlong2((sv.x - u1) << 6, (sv.y - u1) << 6);
-          }
-        }
-      } else {
-        if (r0 > 0)
-          for (int w = 0; w < n; ++w)
-            A[static_cast<size_t>(i0) * AST + w] = (S[static_cast<size_t>(r0 - 1) * n + w] - u0) << 6;
-        if (h1 && r1 > 0)
-          for (int w = 0; w < n; ++w)
-            A[static_cast<size_t>(i1) * AST + w] = (S[static_cast<size_t>(r1 - 1) * n + w] - u1) << 6;
+    // Operand tables are indexed by column (A[c] = (S[p[c]] - u[p[c]]) << 6,
+    // B[c] = block(c) - (v[c] << 6), r[c] = p[c]) and refreshed at row end for
+    // the reached columns only.
+    if (i == 1) {
+      for (int c = tid + 1; c <= k; c += blockDim.x) {
+        rtab[c] = 0;
+        Btab[c] = static_cast<int64_t>((c - 1) / mult);
       }
     }
     __syncthreads();
@@ -934,10 +900,10 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
           curl[b] = 0;
           const int base = w * mult;
           col[b] = ord[base];
-          B[b] = Btab[base];
+          B[b] = Btab[col[b]];
           if (mult > 1) {
             coln[b] = ord[base + 1];
-            Bn[b] = Btab[base + 1];
+            Bn[b] = Btab[coln[b]];
           }
           E6[b] = (S[static_cast<size_t>(i - 1) * n + w] - ui) << 6;  // relax from row i
         }
@@ -1012,13 +978,13 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
             const int cnt = min(32, Tm - sN);
             const bool live = lane < cnt;
             const int pos = base + sN + (live ? lane : 0);
-            const int64_t V6 = static_cast<int64_t>(ws) - Btab[pos];
-            const int r = rtab[pos];
             const int c = ord[pos];
-            const int64_t Aw = A[static_cast<size_t>(pos) * 8 + ws];
+            const int64_t V6 = static_cast<int64_t>(ws) - Btab[c];
+            const int r = rtab[c];
+            const int64_t Aw = A[static_cast<size_t>(c - 1) * 8 + ws];
             int64_t Ax[8];
             {
-              const longlong2* row = reinterpret_cast<const longlong2*>(A + static_cast<size_t>(pos) * 8);
+              const longlong2* row = reinterpret_cast<const longlong2*>(A + static_cast<size_t>(c - 1) * 8);
 #pragma unroll
               for (int h = 0; h < 4; ++h) {
                 const longlong2 v2 = row[h];
@@ -1121,7 +1087,7 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
             const int np = base + sN;
             const bool left = d + sN < mult;
             const int cn = left ? ord[np] : 0;
-            const int64_t bn = left ? Btab[np] : kBig;
+            const int64_t bn = left ? Btab[cn] : kBig;
             colv = mine ? cn : colv;
             Bv = mine ? bn : Bv;
           }
@@ -1130,62 +1096,6 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
         }
         (void)colv;
         curl[0] = lane < n ? static_cast<int>(__byte_perm(cpl, cph, static_cast<unsigned>(lane & 7)) & 255u) : 0;
-      } else {
-      for (;;) {
-        ++steps;
-        uint64_t key = ~0ULL;
-#pragma unroll
-        for (int b = 0; b < NB; ++b) {
-          const uint64_t kb = static_cast<uint64_t>(E6[b] + B[b]);
-          key = (curl[b] < mult && kb < key) ? kb : key;
-        }
-        const unsigned hi = static_cast<unsigned>(key >> 32), lo = static_cast<unsigned>(key);
-        const unsigned mh = __reduce_min_sync(0xffffffffu, hi);
-        const unsigned ml = __reduce_min_sync(0xffffffffu, hi == mh ? lo : 0xffffffffu);
-        const int ws = min(static_cast<int>(ml & 63u), n - 1);  // clamp: corrupt input only
-        const int d = curs[ws];
-        const int idx = ws * mult + d;
-        int64_t a[NB];
-#pragma unroll
-        for (int b = 0; b < NB; ++b) a[b] = A[static_cast<size_t>(idx) * AST + lane + 32 * b];
-        const int r = rtab[idx];
-        if (mh == 0xffffffffu && ml == 0xffffffffu) {  // nothing left: corrupt input only
-          abort = true;
-          break;
-        }
-        const int64_t delta6 = static_cast<int64_t>(((static_cast<uint64_t>(mh) << 32) | ml) & ~63ULL);
-        Dl += delta6 >> 6;
-        const int nxt = idx + 2 < (ws + 1) * mult ? idx + 2 : idx;
-        const int pc = ord[nxt];
-        const int64_t pb = Btab[nxt];
-#pragma unroll
-        for (int b = 0; b < NB; ++b) {
-          const bool mine = lane + 32 * b == ws;
-          if (mine) {
-            const int j1 = col[b];
-            wayi[j1] = wyi[b];
-            dlt[j1] = Dl;
-            ulist[nused] = j1;
-          }
-          curl[b] = mine ? d + 1 : curl[b];
-          col[b] = mine ? coln[b] : col[b];
-          B[b] = mine ? Bn[b] : B[b];
-          coln[b] = mine ? pc : coln[b];
-          Bn[b] = mine ? pb : Bn[b];
-        }
-        __syncwarp();
-        if (lane == 0) curs[ws] = d + 1;
-        __syncwarp();
-        const int s_cur = nused++;
-        if (r == 0) break;  // free column: augmenting path found
-#pragma unroll
-        for (int b = 0; b < NB; ++b) {
-          const int64_t t = E6[b] - delta6;
-          const bool imp = a[b] < t;
-          E6[b] = imp ? a[b] : t;
-          wyi[b] = imp ? s_cur : wyi[b];
-        }
-      }
       }
       if (lane == 0) {
         scal[0] = Dl;
@@ -1284,6 +1194,17 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
       __syncwarp();
       for (int t = lane; t < mult; t += 32) base[t] = merged[t];
       __syncwarp();
+    }
+    __syncthreads();
+    // refresh the operand table of the reached columns
+    for (int e = tid; e < (nu - 1) * n; e += blockDim.x) {
+      const int c = ulist[1 + e / n], w = e - (e / n) * n;
+      const int r = p[c];
+      if (w == 0) {
+        rtab[c] = r;
+        Btab[c] = static_cast<int64_t>((c - 1) / mult) - (v[c] << 6);
+      }
+      A[static_cast<size_t>(c - 1) * AST + w] = (S[static_cast<size_t>(r - 1) * n + w] - u[r]) << 6;
     }
     __syncthreads();
     c_end += clock64() - t2;
@@ -1802,7 +1723,7 @@ size_t tab_smem_bytes(int k, int n, int mult, int nw, int smode) {
   size_t b = 0;
   if (smode == 0) b += r(static_cast<size_t>(k) * n * 8);
   const int ast = (n <= 8 && mult <= 255) ? 8 : n;
-  b += r(static_cast<size_t>(k) * ast * 8) + r(static_cast<size_t>(k) * 8) + 2 * r(K1 * 8) +
+  b += r(static_cast<size_t>(k) * ast * 8) + r(K1 * 8) + 2 * r(K1 * 8) +
        r((K1 + 32) * 8) + 3 * r(K1 * 4) + 2 * r((K1 + 32) * 4) + r(64 * 4) +
        r(32) + r(static_cast<size_t>(nw) * mult * 8) +
        r(static_cast<size_t>(nw) * 2 * mult * 4);
@@ -1838,6 +1759,25 @@ void launch_hungarian_blocks(HungarianScratch& sc, const double* matrix, int n,
   EDX_LAUNCHED();
   const size_t limit = static_cast<size_t>(max_dyn_smem(device));
   const int nw = std::min(n, kFastMaxWarps);
+  // n <= 8: the lanes = steps tabled kernel (fastest there)
+  if (n <= 8 && mult <= 255) {
+    const int nwt = std::min(n, kTabMaxWarps);
+    for (int sm = 0; sm <= 1; ++sm) {
+      const size_t smem = tab_smem_bytes(k, n, mult, nwt, sm);
+      if (smem > limit) continue;
+      auto launch = [&](auto kern) {
+        if (smem > 48 * 1024)
+          EDX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem)));
+        kern<<<1, 32 * nwt, smem, s>>>(sc.s64.p, n, mult, k, order, decision, row_ids, col_of_row,
+                                       sc.steps.p, flags, max_scaled);
+      };
+      if (sm == 0) launch(k_hungarian_blocks_tab<1, 0, true>);
+      else launch(k_hungarian_blocks_tab<1, 1, true>);
+      EDX_LAUNCHED();
+      return;
+    }
+  }
   if (n <= 32 && mult <= 512) {  // the run-batched kernel
     const int nwr = std::min(n, kRunWarps);
     for (int am = 0; am <= 2; ++am) {
@@ -1861,31 +1801,6 @@ void launch_hungarian_blocks(HungarianScratch& sc, const double* matrix, int n,
       EDX_LAUNCHED();
       return;
     }
-  }
-  // tabled kernel when its per-row operand table fits in shared memory
-  const int nwt = std::min(n, kTabMaxWarps);
-  for (int sm = 0; sm <= 1; ++sm) {
-    const size_t smem = tab_smem_bytes(k, n, mult, nwt, sm);
-    if (smem > limit) continue;
-    auto launch = [&](auto kern) {
-      if (smem > 48 * 1024)
-        EDX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem)));
-      kern<<<1, 32 * nwt, smem, s>>>(sc.s64.p, n, mult, k, order, decision, row_ids, col_of_row,
-                                     sc.steps.p, flags, max_scaled);
-    };
-    if (n <= 8 && mult <= 255) {  // 8-bit packed cursors
-      if (sm == 0) launch(k_hungarian_blocks_tab<1, 0, true>);
-      else launch(k_hungarian_blocks_tab<1, 1, true>);
-    } else if (n <= 32) {
-      if (sm == 0) launch(k_hungarian_blocks_tab<1, 0, false>);
-      else launch(k_hungarian_blocks_tab<1, 1, false>);
-    } else {
-      if (sm == 0) launch(k_hungarian_blocks_tab<2, 0, false>);
-      else launch(k_hungarian_blocks_tab<2, 1, false>);
-    }
-    EDX_LAUNCHED();
-    return;
   }
   int mode = -1;
   for (int md = 0; md <= 2 && mode < 0; ++md)
