@@ -868,7 +868,7 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
   }
 
   unsigned long long steps = 0;
-  long long c_step = 0, c_end = 0, c_tab = 0, rekeyed = 0, c_pot = 0, p2 = 0, pmax = 0, runs = 0;
+  long long c_step = 0, c_end = 0, c_tab = 0, rekeyed = 0, c_pot = 0, p2 = 0, pmax = 0, runs = 0, c_ref = 0;
   const long long c_start = clock64();
   for (int i = 1; i <= k; ++i) {
     const long long t0 = clock64();
@@ -1196,17 +1196,29 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
       __syncwarp();
     }
     __syncthreads();
-    // refresh the operand table of the reached columns
-    for (int e = tid; e < (nu - 1) * n; e += blockDim.x) {
-      const int c = ulist[1 + e / n], w = e - (e / n) * n;
+    const long long t3 = clock64();
+    // refresh the operand table of the reached columns (one thread per column)
+    for (int e = tid + 1; e < nu; e += blockDim.x) {
+      const int c = ulist[e];
       const int r = p[c];
-      if (w == 0) {
-        rtab[c] = r;
-        Btab[c] = static_cast<int64_t>((c - 1) / mult) - (v[c] << 6);
+      const int64_t ur = u[r];
+      rtab[c] = r;
+      Btab[c] = static_cast<int64_t>((c - 1) / mult) - (v[c] << 6);
+      if (n == 8) {
+        const longlong2* Sr = reinterpret_cast<const longlong2*>(S + static_cast<size_t>(r - 1) * 8);
+        longlong2* Ar = reinterpret_cast<longlong2*>(A + static_cast<size_t>(c - 1) * 8);
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const longlong2 sv = Sr[h];
+          Ar[h] = make_longlong2((sv.x - ur) << 6, (sv.y - ur) << 6);
+        }
+      } else {
+        for (int w = 0; w < n; ++w)
+          A[static_cast<size_t>(c - 1) * AST + w] = (S[static_cast<size_t>(r - 1) * n + w] - ur) << 6;
       }
-      A[static_cast<size_t>(c - 1) * AST + w] = (S[static_cast<size_t>(r - 1) * n + w] - u[r]) << 6;
     }
     __syncthreads();
+    c_ref += clock64() - t3;
     c_end += clock64() - t2;
   }
   for (int j = tid + 1; j <= k; j += blockDim.x) {
@@ -1224,7 +1236,7 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
     stats[3] = c_tab;
     stats[4] = c_pot;
     stats[5] = runs;
-    stats[6] = rekeyed;
+    stats[6] = c_ref;
     stats[7] = clock64() - c_start;
   }
 }
@@ -1513,14 +1525,28 @@ __global__ void __launch_bounds__(kRunWarps * 32, 1)
     __syncthreads();
     // refresh the operand table of the reached columns (their row or its
     // potential changed; every other column is unchanged)
-    for (int e = tid; e < (nu - 1) * n; e += blockDim.x) {
-      const int c = ulist[1 + e / n], w = e - (e / n) * n;
-      const int r = p[c];
-      if (w == 0) {
+    if (nu - 1 >= (int)blockDim.x / 4) {  // many columns: one thread per column
+      for (int e = tid + 1; e < nu; e += blockDim.x) {
+        const int c = ulist[e];
+        const int r = p[c];
+        const int64_t ur = u[r];
         rtab[c] = r;
         Btab[c] = static_cast<int64_t>((c - 1) / mult) - (v[c] << 6);
+        for (int w = 0; w < n; ++w)
+          A[static_cast<size_t>(c - 1) * n + w] = (S[static_cast<size_t>(r - 1) * n + w] - ur) << 6;
       }
-      A[static_cast<size_t>(c - 1) * n + w] = (S[static_cast<size_t>(r - 1) * n + w] - u[r]) << 6;
+    } else {  // few columns: one warp per column, lanes over workers
+      for (int e = warp + 1; e < nu; e += nw) {
+        const int c = ulist[e];
+        const int r = p[c];
+        const int64_t ur = u[r];
+        if (lane == 0) {
+          rtab[c] = r;
+          Btab[c] = static_cast<int64_t>((c - 1) / mult) - (v[c] << 6);
+        }
+        if (lane < n)
+          A[static_cast<size_t>(c - 1) * n + lane] = (S[static_cast<size_t>(r - 1) * n + lane] - ur) << 6;
+      }
     }
     if constexpr (AMODE == 2) __threadfence_block();
     __syncthreads();
