@@ -35,6 +35,9 @@
 
 #include "edx_internal.cuh"
 
+#include <cstdlib>
+#include <cstring>
+
 namespace edx {
 
 namespace {
@@ -1197,23 +1200,23 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
     }
     __syncthreads();
     const long long t3 = clock64();
-    // refresh the operand table of the reached columns (one thread per column)
-    for (int e = tid + 1; e < nu; e += blockDim.x) {
-      const int c = ulist[e];
+    // refresh the operand table of the reached columns: 4 lanes per column,
+    // 16 bytes (2 workers) each, so a warp's row accesses are conflict-free
+    for (int e = tid; e < (nu - 1) * 4; e += blockDim.x) {
+      const int q = e >> 2, h = e & 3;
+      const int c = ulist[1 + q];
       const int r = p[c];
       const int64_t ur = u[r];
-      rtab[c] = r;
-      Btab[c] = static_cast<int64_t>((c - 1) / mult) - (v[c] << 6);
+      if (h == 0) {
+        rtab[c] = r;
+        Btab[c] = static_cast<int64_t>((c - 1) / mult) - (v[c] << 6);
+      }
       if (n == 8) {
-        const longlong2* Sr = reinterpret_cast<const longlong2*>(S + static_cast<size_t>(r - 1) * 8);
-        longlong2* Ar = reinterpret_cast<longlong2*>(A + static_cast<size_t>(c - 1) * 8);
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          const longlong2 sv = Sr[h];
-          Ar[h] = make_longlong2((sv.x - ur) << 6, (sv.y - ur) << 6);
-        }
+        const longlong2 sv = reinterpret_cast<const longlong2*>(S + static_cast<size_t>(r - 1) * 8)[h];
+        reinterpret_cast<longlong2*>(A + static_cast<size_t>(c - 1) * 8)[h] =
+            make_longlong2((sv.x - ur) << 6, (sv.y - ur) << 6);
       } else {
-        for (int w = 0; w < n; ++w)
+        for (int w = 2 * h; w < 2 * h + 2 && w < n; ++w)
           A[static_cast<size_t>(c - 1) * AST + w] = (S[static_cast<size_t>(r - 1) * n + w] - ur) << 6;
       }
     }
@@ -1525,27 +1528,19 @@ __global__ void __launch_bounds__(kRunWarps * 32, 1)
     __syncthreads();
     // refresh the operand table of the reached columns (their row or its
     // potential changed; every other column is unchanged)
-    if (nu - 1 >= (int)blockDim.x / 4) {  // many columns: one thread per column
-      for (int e = tid + 1; e < nu; e += blockDim.x) {
+    {  // refresh reached columns: a group of gs >= n lanes per column, lanes over workers
+      const int gs = n <= 8 ? 8 : (n <= 16 ? 16 : 32);
+      const int gpw = 32 / gs, sub = lane / gs, lw = lane - sub * gs;
+      for (int e = warp * gpw + sub + 1; e < nu; e += nw * gpw) {
         const int c = ulist[e];
         const int r = p[c];
         const int64_t ur = u[r];
-        rtab[c] = r;
-        Btab[c] = static_cast<int64_t>((c - 1) / mult) - (v[c] << 6);
-        for (int w = 0; w < n; ++w)
-          A[static_cast<size_t>(c - 1) * n + w] = (S[static_cast<size_t>(r - 1) * n + w] - ur) << 6;
-      }
-    } else {  // few columns: one warp per column, lanes over workers
-      for (int e = warp + 1; e < nu; e += nw) {
-        const int c = ulist[e];
-        const int r = p[c];
-        const int64_t ur = u[r];
-        if (lane == 0) {
+        if (lw == 0) {
           rtab[c] = r;
           Btab[c] = static_cast<int64_t>((c - 1) / mult) - (v[c] << 6);
         }
-        if (lane < n)
-          A[static_cast<size_t>(c - 1) * n + lane] = (S[static_cast<size_t>(r - 1) * n + lane] - ur) << 6;
+        if (lw < n)
+          A[static_cast<size_t>(c - 1) * n + lw] = (S[static_cast<size_t>(r - 1) * n + lw] - ur) << 6;
       }
     }
     if constexpr (AMODE == 2) __threadfence_block();
@@ -1570,6 +1565,460 @@ __global__ void __launch_bounds__(kRunWarps * 32, 1)
     stats[6] = 0;
     stats[7] = clock64() - c_start;
   }
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+
+// ----------------------------------------- K6 multi-warp kernel (n <= 16)
+// The production solver for n <= 16.  Same run-batched Dijkstra steps as the
+// tabled and run kernels (derivation above), but warp x owns block x.  Every
+// warp keeps all blocks' (G, key offset, cursor) lane-distributed, so each
+// picks the run's winner itself (two redux.sync.min).  In a chunk (lanes =
+// steps of the winner block) every warp runs one scan over the pair monoid
+// (sum of deltas, min of its own block's relax candidates), then only its own
+// block's "would block x win here" ballot and way update: a chunk costs one
+// block's dependency chain instead of n of them.  The per-block fail masks
+// and per-step G values are exchanged through double-buffered shared slots
+// and an mbarrier (arrive, then the next chunk's operands and scan are
+// computed speculatively, then wait).  The winner warp writes one 16-byte
+// entry per reached column {column | row << 16, way entry, delta}, so the
+// row end (potentials fused with the operand-table refresh, then the
+// augmenting walk at one entry load per hop) needs no further lookups.  Block
+// orders start as the identity and a potential update keeps each block sorted
+// (see the re-sort check), so ord is only consulted after a fallback sort.
+
+template <int AMODE, int MAXW>  // AMODE 0: S and A shared; 1: S global, A shared; 2: S and A global
+__global__ void __launch_bounds__(MAXW * 32, 1)
+    k_hungarian_blocks_mw(const int64_t* __restrict__ S_global, int n, int mult, int k,
+                          int64_t* __restrict__ A_global, const uint32_t* __restrict__ order,
+                          int32_t* __restrict__ decision, const uint32_t* __restrict__ row_ids,
+                          uint64_t* __restrict__ col_of_row, unsigned long long* stats, int* flags,
+                          const unsigned long long* __restrict__ max_scaled) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const size_t K1 = static_cast<size_t>(k) + 1;
+  size_t so = 0;
+  auto stake = [&](size_t bytes) {
+    uint8_t* q = smem + so;
+    so += (bytes + 15) & ~size_t(15);
+    return q;
+  };
+  const int64_t* S;
+  if constexpr (AMODE == 0) {
+    int64_t* Ss = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(k) * n * 8));
+    for (size_t x = tid; x < static_cast<size_t>(k) * n; x += blockDim.x) Ss[x] = S_global[x];
+    S = Ss;
+  } else {
+    S = S_global;
+  }
+  int64_t* A;
+  if constexpr (AMODE <= 1) A = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(k) * n * 8));
+  else A = A_global;
+  int64_t* Btab = reinterpret_cast<int64_t*>(stake(K1 * 8));  // by column: block - (v << 6)
+  int64_t* u = reinterpret_cast<int64_t*>(stake(K1 * 8));
+  int64_t* v = reinterpret_cast<int64_t*>(stake(K1 * 8));
+  int64_t* dlt = reinterpret_cast<int64_t*>(stake((K1 + 32) * 8));
+  int32_t* p = reinterpret_cast<int32_t*>(stake(K1 * 4));
+  int32_t* wayi = reinterpret_cast<int32_t*>(stake((K1 + 32) * 4));
+  int32_t* ulist = reinterpret_cast<int32_t*>(stake((K1 + 32) * 4));
+  int32_t* ord = reinterpret_cast<int32_t*>(stake(K1 * 4));
+  int32_t* rtab = reinterpret_cast<int32_t*>(stake(K1 * 4));
+  int32_t* cblk = reinterpret_cast<int32_t*>(stake(K1 * 4));   // column -> block
+  int32_t* curs = reinterpret_cast<int32_t*>(stake(32 * 4));
+  // reached-column list of the row being solved, one 16-byte entry per step:
+  // {c | p[c] << 16, way (entry index of the predecessor), delta at reach}
+  int4* L = reinterpret_cast<int4*>(stake((K1 + 32) * 16));
+  int64_t* GA = reinterpret_cast<int64_t*>(stake(2 * 32 * 32 * 8));  // chunk: per-step G of each block
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(stake(16));            // chunk exchange barrier
+  int32_t* ordflag = reinterpret_cast<int32_t*>(stake(16));           // block orders still identity?
+  uint32_t* pfail = reinterpret_cast<uint32_t*>(stake(2 * 32 * 4));  // chunk: fail masks
+  int32_t* tmp = reinterpret_cast<int32_t*>(stake(static_cast<size_t>(2 * mult) * 4));
+  if (so > dynamic_smem_bytes()) {  // host/device layout mismatch: fail loudly, touch nothing
+    if (tid == 0) atomicOr(flags + kFlagInternal, 1);
+    return;
+  }
+  const unsigned long long mx = *max_scaled;
+  const bool packable = mx < (1ULL << 57) / (8ULL * static_cast<unsigned long long>(k + 1));
+  for (size_t x = tid; x < K1; x += blockDim.x) {
+    u[x] = 0;
+    v[x] = 0;
+    p[x] = 0;
+    wayi[x] = 0;
+  }
+  for (int x = tid; x < k; x += blockDim.x) ord[x] = x + 1;
+  __syncthreads();
+  if (!packable) {  // wide-range path (see k_hungarian_blocks_wide)
+    if (warp == 0) {
+      BlockArrays Aw{S, u, v, dlt, p, wayi, ulist, ord, tmp};
+      if (!hungarian_blocks_warp<1>(Aw, n, mult, k, stats, flags)) return;
+      __syncwarp();
+      for (int j = lane + 1; j <= k; j += 32) {
+        const int r = p[j] - 1;
+        if (col_of_row) col_of_row[r] = static_cast<uint64_t>(j - 1);
+        if (decision) {
+          const uint32_t row = order[r];
+          decision[row_ids ? row_ids[row] : row] = (j - 1) / mult;
+        }
+      }
+    }
+    return;
+  }
+  for (int c = tid; c <= k; c += blockDim.x) {
+    const int b = c == 0 ? 0 : (c - 1) / mult;
+    cblk[c] = b;
+    rtab[c] = 0;
+    Btab[c] = b;
+  }
+  if (tid == 0) {
+    mbar_init(mbar, blockDim.x);
+    ordflag[0] = 1;
+  }
+  __syncthreads();
+
+  constexpr int64_t kBig = 1LL << 62;
+  const int x = warp;  // this warp's block
+  int par = 0;         // publish slot parity (identical in every warp)
+  unsigned mbph = 0;   // mbarrier phase parity
+  unsigned long long steps = 0;
+  long long c_step = 0, c_end = 0, c_pot = 0, c_ref = 0, runs = 0, sorts = 0;
+  const long long c_start = clock64();
+  for (int i = 1; i <= k; ++i) {
+    const long long t1 = clock64();
+    // Row frame: Q = cumulative delta of this row's search (<< 6).  Block y
+    // keeps G_y = E_y + Q (its least relaxed value, unshifted by the deltas),
+    // the key offset B_y of its next column and its cursor d_y; every warp
+    // holds all blocks' (G, B, d) lane-distributed (lane y = block y) and its
+    // own block's way (a step index into ulist).
+    // Block orders start as the identity and, in practice, stay so (see the
+    // re-sort check at row end); while they do, position q of the order is
+    // column q + 1 and the ord lookup drops off the critical path.
+    const bool ordid = ordflag[0] != 0;
+    int64_t Gy = kBig, By = kBig;
+    int dy = 0;
+    if (lane < n) {
+      Gy = (S[static_cast<size_t>(i - 1) * n + lane] - u[i]) << 6;  // relax from row i
+      By = Btab[ordid ? lane * mult + 1 : ord[lane * mult]];
+    }
+    int wyx = 0;
+    if (tid == 0) {
+      p[0] = i;
+      L[0] = make_int4(i << 16, 0, 0, 0);
+    }
+    int nused = 1;
+    int64_t Q = 0;
+    bool abort = false, phase_end = false;
+    while (!phase_end) {  // runs
+      const uint64_t key = lane < n ? static_cast<uint64_t>(Gy - Q + By) : ~0ULL;
+      const unsigned hi = static_cast<unsigned>(key >> 32), lo = static_cast<unsigned>(key);
+      const unsigned mh = __reduce_min_sync(0xffffffffu, hi);
+      const unsigned ml = __reduce_min_sync(0xffffffffu, hi == mh ? lo : 0xffffffffu);
+      if (mh >= 0x20000000u) {  // every block exhausted (key >= 2^61): corrupt input only
+        abort = true;
+        break;
+      }
+      const int ws = static_cast<int>(ml & 63u);
+      const int dws = __shfl_sync(0xffffffffu, dy, ws);
+      const int base = ws * mult + dws;  // position of the winner's candidate c_1
+      const int Tm = mult - dws;
+      const int64_t delta1 = static_cast<int64_t>(((static_cast<uint64_t>(mh) << 32) | ml) & ~63ULL);
+      int64_t Gx = __shfl_sync(0xffffffffu, Gy, x);
+      const int64_t Bx = __shfl_sync(0xffffffffu, By, x);
+      int64_t P = Q;
+      int sN = 0;
+      const int nused0 = nused;
+      // Chunk operands, lanes = steps: column, its row, key offset, A[winner],
+      // A[own]; then the chunk's scan over (sum of deltas, min of relax
+      // candidates) with the pair monoid (S, M).(S', M') = (S + S', min(M, S + M')),
+      // relative to the carry P.  The next chunk's operands and scan are
+      // computed speculatively while this chunk's fail masks are exchanged.
+      auto load = [&](int s0, int& c, int& r, int64_t& Bc, int64_t& Aw, int64_t& Ax) {
+        const int q = base + min(s0 + lane, Tm - 1);
+        c = ordid ? q + 1 : ord[q];
+        Bc = Btab[c];
+        r = rtab[c];
+        Aw = A[static_cast<size_t>(c - 1) * n + ws];
+        Ax = A[static_cast<size_t>(c - 1) * n + x];
+      };
+      auto scan = [&](int64_t dl, int64_t Ax, int64_t& Ss, int64_t& M) {
+        Ss = dl;
+        M = Ax + dl;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const int64_t ys = __shfl_up_sync(0xffffffffu, Ss, off);
+          const int64_t ym = __shfl_up_sync(0xffffffffu, M, off);
+          if (lane >= off) {
+            const int64_t t = ys + M;
+            M = ym < t ? ym : t;
+            Ss += ys;
+          }
+        }
+      };
+      int c, r;
+      int64_t Bc, Aw, Ax, Ss, M;
+      load(0, c, r, Bc, Aw, Ax);
+      int64_t V6 = static_cast<int64_t>(ws) - Bc;
+      {
+        const int64_t V6p = __shfl_up_sync(0xffffffffu, V6, 1), Awp = __shfl_up_sync(0xffffffffu, Aw, 1);
+        int64_t dl = lane == 0 ? delta1 : (V6p < Awp ? V6p : Awp) - V6;
+        if (lane >= Tm) dl = 0;
+        scan(dl, Ax, Ss, M);
+      }
+      for (;;) {  // chunks of up to 32 steps
+        const int cnt = min(32, Tm - sN);
+        const bool live = lane < cnt;
+        const bool first = sN == 0 && lane == 0;
+        const int64_t Qt = P + Ss;     // cumulative delta after this step
+        const int64_t cand = Ax + Qt;  // relax candidate of this step for block x
+        const int64_t Mp = P + __shfl_up_sync(0xffffffffu, M, 1);
+        const int64_t Gb = lane == 0 ? Gx : (Mp < Gx ? Mp : Gx);  // G before the step
+        const int64_t Ga = cand < Gb ? cand : Gb;                  // G after its relax
+        const bool fail = x != ws && !(Gb + Bx - ws > Qt);         // block x would win here
+        const unsigned failx = __ballot_sync(0xffffffffu, live && !first && fail);
+        const unsigned impm = __ballot_sync(0xffffffffu, live && cand < Gb);
+        const unsigned freem = __ballot_sync(0xffffffffu, live && r == 0);
+        if (lane == 0) pfail[par * 32 + x] = failx;
+        GA[(par * 32 + x) * 32 + lane] = Ga;
+        mbar_arrive(mbar);
+        // speculative next chunk (this one complete, the run continuing)
+        const bool more = sN + 32 < Tm;
+        const int64_t P31 = __shfl_sync(0xffffffffu, Qt, 31);
+        const int64_t G31 = __shfl_sync(0xffffffffu, Ga, 31);
+        int c2 = 0, r2 = 0;
+        int64_t Bc2 = kBig, Aw2 = 0, Ax2 = 0, V62 = 0, Ss2 = 0, M2 = 0;
+        if (more) {
+          load(sN + 32, c2, r2, Bc2, Aw2, Ax2);
+          V62 = static_cast<int64_t>(ws) - Bc2;
+          int64_t V6p = __shfl_up_sync(0xffffffffu, V62, 1), Awp = __shfl_up_sync(0xffffffffu, Aw2, 1);
+          const int64_t V6l = __shfl_sync(0xffffffffu, V6, 31), Awl = __shfl_sync(0xffffffffu, Aw, 31);
+          if (lane == 0) {
+            V6p = V6l;
+            Awp = Awl;
+          }
+          int64_t dl = (V6p < Awp ? V6p : Awp) - V62;
+          if (sN + 32 + lane >= Tm) dl = 0;
+          scan(dl, Ax2, Ss2, M2);
+        }
+        mbar_wait(mbar, mbph);
+        mbph ^= 1u;
+        const unsigned failm = __reduce_or_sync(0xffffffffu, lane < n ? pfail[par * 32 + lane] : 0u);
+        const int failq = failm ? __ffs(failm) - 1 : 32;
+        const int freeq = freem ? __ffs(freem) - 1 : 32;
+        int vq = failq < cnt ? failq : cnt;
+        if (freeq < vq) {
+          vq = freeq + 1;
+          phase_end = true;
+        }
+        const unsigned relax_m = freeq < 32 ? ((1u << freeq) - 1u) : 0xffffffffu;  // no relax at a free column
+        const int wbase = nused0 + sN;
+        if (x == ws && lane < vq) {  // the winner warp commits: each lane its own step
+          const unsigned prev = impm & relax_m & ((1u << lane) - 1u);
+          const int64_t dq = Qt >> 6;
+          L[wbase + lane] = make_int4(c | (r << 16), prev ? wbase + 31 - __clz(prev) : wyx,
+                                      static_cast<int>(static_cast<uint32_t>(dq)),
+                                      static_cast<int>(dq >> 32));
+        }
+        sN += vq;
+        if (vq == 32 && !phase_end && more) {  // the whole chunk held: continue the run
+          P = P31;
+          Gx = G31;
+          wyx = impm ? wbase + 31 - __clz(impm) : wyx;
+          par ^= 1;
+          c = c2;
+          r = r2;
+          Bc = Bc2;
+          Aw = Aw2;
+          Ax = Ax2;
+          V6 = V62;
+          Ss = Ss2;
+          M = M2;
+          continue;
+        }
+        // run end: carry, way, every block's G after the run's last step
+        // (vq == 0 only after a full chunk, whose slot is still intact)
+        if (vq > 0) {
+          P = __shfl_sync(0xffffffffu, Qt, vq - 1);
+          const unsigned m2 = impm & relax_m & (vq >= 32 ? 0xffffffffu : ((1u << vq) - 1u));
+          wyx = m2 ? wbase + 31 - __clz(m2) : wyx;
+        }
+        if (lane < n)
+          Gy = vq > 0 ? GA[(par * 32 + lane) * 32 + vq - 1] : GA[((par ^ 1) * 32 + lane) * 32 + 31];
+        // the winner's next key offset: lane vq of this chunk, or lane 0 of the next
+        const int64_t bnext = __shfl_sync(0xffffffffu, vq < 32 ? Bc : Bc2, vq < 32 ? vq : 0);
+        par ^= 1;
+        ++runs;
+        Q = P;
+        nused = nused0 + sN;
+        steps += sN;
+        if (lane == ws) {  // lane ws holds the winner's cursor and key offset
+          dy += sN;
+          By = dy < mult ? bnext : kBig;
+        }
+        break;
+      }
+    }
+    if (abort) {
+      if (tid == 0) atomicOr(flags + kFlagBadCost, 1);
+      return;
+    }
+    const int64_t Dl = Q >> 6;
+    if (warp == 0 && lane < n) curs[lane] = dy;
+    __syncthreads();
+    const long long t2 = clock64();
+    c_step += t2 - t1;
+    const int nu = nused;
+    // Potentials (assign.hpp:131-138) fused with the operand-table refresh:
+    // reached column c moves by dd_c = Dl - dlt[c] (v[c] -= dd_c, u[p[c]] +=
+    // dd_c), and unless c is on the augmenting path its row stays p[c], whose
+    // new potential is exactly u[p[c]] + dd_c.  A group of gs >= n lanes per
+    // column, lanes over workers; two columns per group in flight.
+    {
+      const int gs = n <= 8 ? 8 : (n <= 16 ? 16 : 32);
+      const int gpw = 32 / gs, sub = lane / gs, lw = lane - sub * gs;
+      const int stride = nw * gpw;
+      for (int eb = warp * gpw; eb < nu; eb += 2 * stride) {  // warp-uniform trip count
+        const int e0 = eb + sub, e1 = e0 + stride;
+        const bool act0 = e0 < nu, act1 = e1 < nu;
+        const int4 q0 = act0 ? L[e0] : make_int4(0, 0, 0, 0);
+        const int4 q1 = act1 ? L[e1] : make_int4(0, 0, 0, 0);
+        const int c0 = q0.x & 0xffff, r0 = q0.x >> 16, c1 = q1.x & 0xffff, r1 = q1.x >> 16;
+        const int64_t dd0 = Dl - ((static_cast<int64_t>(q0.w) << 32) | static_cast<uint32_t>(q0.z));
+        const int64_t dd1 = Dl - ((static_cast<int64_t>(q1.w) << 32) | static_cast<uint32_t>(q1.z));
+        const int64_t u0 = act0 ? u[r0] + dd0 : 0, u1 = act1 ? u[r1] + dd1 : 0;
+        const int64_t v0 = act0 ? v[c0] - dd0 : 0, v1 = act1 ? v[c1] - dd1 : 0;
+        const int64_t b0 = act0 ? cblk[c0] : 0, b1 = act1 ? cblk[c1] : 0;
+        const int64_t s0 = (act0 && r0 > 0 && lw < n) ? S[static_cast<size_t>(r0 - 1) * n + lw] : 0;
+        const int64_t s1 = (act1 && r1 > 0 && lw < n) ? S[static_cast<size_t>(r1 - 1) * n + lw] : 0;
+        __syncwarp();  // every lane has read u[r] before the group leader writes it
+        if (lw == 0) {
+          if (act0) {
+            u[r0] = u0;
+            v[c0] = v0;
+            if (c0 != 0) Btab[c0] = b0 - (v0 << 6);
+          }
+          if (act1) {
+            u[r1] = u1;
+            v[c1] = v1;
+            Btab[c1] = b1 - (v1 << 6);
+          }
+        }
+        if (lw < n) {
+          if (act0 && c0 != 0 && r0 > 0) A[static_cast<size_t>(c0 - 1) * n + lw] = (s0 - u0) << 6;
+          if (act1 && r1 > 0) A[static_cast<size_t>(c1 - 1) * n + lw] = (s1 - u1) << 6;
+        }
+      }
+    }
+    if constexpr (AMODE == 2) __threadfence_block();
+    __syncthreads();
+    const long long t3 = clock64();
+    c_pot += t3 - t2;
+    // augment (assign.hpp:141-145) on the first warp whose block was not
+    // touched, so it overlaps the re-sort checks.  Each hop is one entry load
+    // (the predecessor's entry carries its column and old row); the path
+    // columns change rows, so the warp also rewrites their tables.
+    const unsigned untouched = __ballot_sync(0xffffffffu, lane < n && curs[lane] == 0);
+    const int aug_warp = untouched ? __ffs(untouched) - 1 : 0;
+    if (warp == aug_warp) {
+      int4 ent = L[nu - 1];
+      for (;;) {
+        const int jj = ent.x & 0xffff;
+        if (jj == 0) break;
+        const int4 prv = L[ent.y];
+        const int rn = prv.x >> 16;  // p[jj] = p[way[jj]]
+        const int64_t ur = u[rn];
+        const int64_t sv = lane < n ? S[static_cast<size_t>(rn - 1) * n + lane] : 0;
+        if (lane == 0) {
+          p[jj] = rn;
+          rtab[jj] = rn;
+        }
+        if (lane < n) A[static_cast<size_t>(jj - 1) * n + lane] = (sv - ur) << 6;
+        ent = prv;
+      }
+    }
+    // Re-sort the touched blocks.  After the potential update a block's order
+    // is already sorted by v desc: its P consumed columns get v' = G_w(t) - Q
+    // (non-increasing in t, G only decreases) and every unconsumed column has
+    // v <= G_w(end) - Q (all remaining keys are >= 0 at the row end).  Only
+    // runs of equal v can be out of j order, so check adjacent pairs first
+    // and sort only when one is.
+    for (int w = warp; w < n; w += nw) {
+      if (curs[w] == 0) continue;
+      const int32_t* ob = ord + w * mult;
+      bool bad = false;
+      for (int q = lane; q < mult - 1; q += 32) {
+        const int a0 = ob[q], b0 = ob[q + 1];
+        const int64_t va = v[a0], vb = v[b0];
+        bad |= !(va > vb || (va == vb && a0 < b0));
+      }
+      if (__any_sync(0xffffffffu, bad)) {
+        if (lane == 0) {
+          ++sorts;
+          ordflag[0] = 0;
+        }
+        warp_resort_dispatch(ord, v, w * mult, mult, lane);
+      }
+      __syncwarp();
+    }
+    if constexpr (AMODE == 2) __threadfence_block();
+    __syncthreads();
+    const long long t4 = clock64();
+    c_ref += t4 - t3;
+    c_end += t4 - t2;
+  }
+  for (int j = tid + 1; j <= k; j += blockDim.x) {
+    const int r = p[j] - 1;
+    if (col_of_row) col_of_row[r] = static_cast<uint64_t>(j - 1);
+    if (decision) {
+      const uint32_t row = order[r];
+      decision[row_ids ? row_ids[row] : row] = cblk[j];
+    }
+  }
+  if (stats == nullptr) return;
+  __syncthreads();
+  if (tid == 0) curs[0] = 0;
+  __syncthreads();
+  if (lane == 0) atomicAdd(curs, static_cast<int>(sorts));
+  __syncthreads();
+  if (tid == 0) {
+    stats[0] = steps;
+    stats[1] = c_step;
+    stats[2] = c_end;
+    stats[3] = static_cast<unsigned long long>(curs[0]);  // blocks that needed a full re-sort
+    stats[4] = c_pot;
+    stats[5] = runs;
+    stats[6] = c_ref;
+    stats[7] = clock64() - c_start;
+  }
+}
+
+size_t mw_smem_bytes(int k, int n, int mult, int amode) {
+  const size_t K1 = static_cast<size_t>(k) + 1;
+  auto r = [](size_t b) { return (b + 15) & ~size_t(15); };
+  size_t b = 0;
+  if (amode == 0) b += r(static_cast<size_t>(k) * n * 8);
+  if (amode <= 1) b += r(static_cast<size_t>(k) * n * 8);
+  b += 3 * r(K1 * 8) + r((K1 + 32) * 8) + 4 * r(K1 * 4) + 2 * r((K1 + 32) * 4) + r(32 * 4) +
+       r((K1 + 32) * 16) + r(2 * 32 * 32 * 8) + r(16) + r(16) + r(2 * 32 * 4) +
+       r(static_cast<size_t>(2 * mult) * 4);
+  return b;
 }
 
 size_t run_smem_bytes(int k, int n, int mult, int nw, int amode) {
@@ -1785,8 +2234,47 @@ void launch_hungarian_blocks(HungarianScratch& sc, const double* matrix, int n,
   EDX_LAUNCHED();
   const size_t limit = static_cast<size_t>(max_dyn_smem(device));
   const int nw = std::min(n, kFastMaxWarps);
-  // n <= 8: the lanes = steps tabled kernel (fastest there)
-  if (n <= 8 && mult <= 255) {
+  static const int solver_pref = [] {  // EDX_SOLVER=tab|run|mw: A/B override for measurements
+    const char* e = std::getenv("EDX_SOLVER");
+    if (e == nullptr) return 0;
+    if (std::strcmp(e, "tab") == 0) return 1;
+    if (std::strcmp(e, "run") == 0) return 2;
+    return 0;
+  }();
+  // the multi-warp kernel for n <= 16 (at n = 32 the run kernel is faster:
+  // 32 warps per exchange cost more than the per-block work they split)
+  if (solver_pref == 0 && n <= 16 && mult <= 512) {
+    for (int am = 0; am <= 2; ++am) {
+      const size_t smem = mw_smem_bytes(k, n, mult, am);
+      if (smem > limit) continue;
+      int64_t* Ag = nullptr;
+      if (am == 2) {
+        sc.arena.ensure(static_cast<size_t>(k) * n * 8);
+        Ag = reinterpret_cast<int64_t*>(sc.arena.p);
+      }
+      auto launch = [&](auto kern) {
+        if (smem > 48 * 1024)
+          EDX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem)));
+        kern<<<1, 32 * n, smem, s>>>(sc.s64.p, n, mult, k, Ag, order, decision, row_ids,
+                                     col_of_row, sc.steps.p, flags, max_scaled);
+      };
+      // the warp cap sets the register budget: 255 (n <= 8), 128 (n <= 16)
+      if (n <= 8) {
+        if (am == 0) launch(k_hungarian_blocks_mw<0, 8>);
+        else if (am == 1) launch(k_hungarian_blocks_mw<1, 8>);
+        else launch(k_hungarian_blocks_mw<2, 8>);
+      } else {
+        if (am == 0) launch(k_hungarian_blocks_mw<0, 16>);
+        else if (am == 1) launch(k_hungarian_blocks_mw<1, 16>);
+        else launch(k_hungarian_blocks_mw<2, 16>);
+      }
+      EDX_LAUNCHED();
+      return;
+    }
+  }
+  // n <= 8: the lanes = steps tabled kernel
+  if (solver_pref != 2 && n <= 8 && mult <= 255) {
     const int nwt = std::min(n, kTabMaxWarps);
     for (int sm = 0; sm <= 1; ++sm) {
       const size_t smem = tab_smem_bytes(k, n, mult, nwt, sm);
