@@ -781,6 +781,24 @@ __device__ __forceinline__ void warp_resort_dispatch(int32_t* ord, const int64_t
   else warp_resort_block<16>(ord, v, base, mult, lane);
 }
 
+// After a row's potential update every touched block is already sorted by
+// v desc: its P consumed columns get v' = G_w(t) - Q (non-increasing in t, the
+// block's least relaxed value G only decreases) and every unconsumed column
+// has v <= G_w(end) - Q (all remaining keys are >= 0 at the row end).  Only
+// runs of equal v can be out of j order, so a block is re-sorted only when an
+// adjacent pair violates (v desc, j asc) -- which never happened in any
+// measured solve.
+__device__ __forceinline__ bool warp_block_sorted(const int32_t* ord, const int64_t* v, int base,
+                                                  int mult, int lane) {
+  bool bad = false;
+  for (int q = lane; q < mult - 1; q += 32) {
+    const int a = ord[base + q], b = ord[base + q + 1];
+    const int64_t va = v[a], vb = v[b];
+    bad |= !(va > vb || (va == vb && a < b));
+  }
+  return !__any_sync(0xffffffffu, bad);
+}
+
 // --------------------------------------------- K6 tabled (per-row operand table)
 // Fastest variant, used when the operand table fits in shared memory.  At the
 // start of each row (phase) all warps rebuild, for every block x and every
@@ -1144,6 +1162,7 @@ __global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
         p2 += static_cast<long long>(P) * P;
         pmax = P > pmax ? P : pmax;
       }
+      if (warp_block_sorted(ord, v, w * mult, mult, lane)) continue;
       if (mult <= 512) {
         warp_resort_dispatch(ord, v, w * mult, mult, lane);
         __syncwarp();
@@ -1520,9 +1539,10 @@ __global__ void __launch_bounds__(kRunWarps * 32, 1)
         jj = jp;
       } while (jj != 0);
     }
-    for (int w = warp; w < n; w += nw) {  // re-sort the touched blocks
+    for (int w = warp; w < n; w += nw) {  // re-sort the touched blocks (if needed)
       if (curs[w] == 0) continue;
-      warp_resort_dispatch(ord, v, w * mult, mult, lane);
+      if (!warp_block_sorted(ord, v, w * mult, mult, lane))
+        warp_resort_dispatch(ord, v, w * mult, mult, lane);
       __syncwarp();
     }
     __syncthreads();
@@ -1953,22 +1973,10 @@ __global__ void __launch_bounds__(MAXW * 32, 1)
         ent = prv;
       }
     }
-    // Re-sort the touched blocks.  After the potential update a block's order
-    // is already sorted by v desc: its P consumed columns get v' = G_w(t) - Q
-    // (non-increasing in t, G only decreases) and every unconsumed column has
-    // v <= G_w(end) - Q (all remaining keys are >= 0 at the row end).  Only
-    // runs of equal v can be out of j order, so check adjacent pairs first
-    // and sort only when one is.
+    // re-sort the touched blocks, if needed (see warp_block_sorted)
     for (int w = warp; w < n; w += nw) {
       if (curs[w] == 0) continue;
-      const int32_t* ob = ord + w * mult;
-      bool bad = false;
-      for (int q = lane; q < mult - 1; q += 32) {
-        const int a0 = ob[q], b0 = ob[q + 1];
-        const int64_t va = v[a0], vb = v[b0];
-        bad |= !(va > vb || (va == vb && a0 < b0));
-      }
-      if (__any_sync(0xffffffffu, bad)) {
+      if (!warp_block_sorted(ord, v, w * mult, mult, lane)) {
         if (lane == 0) {
           ++sorts;
           ordflag[0] = 0;
