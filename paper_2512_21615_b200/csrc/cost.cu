@@ -109,6 +109,253 @@ __global__ void __launch_bounds__(kBlockCells)
   }
 }
 
+// ------------------------------------------------ K1, 2 <= n <= 8 (warp rows)
+// A warp holds 32 / NP rows, one group of NP >= n lanes per row (lane j of a
+// group = worker j).  Each lane loads up to 4 of its row's ids and their
+// {owners, latest} masks up front, so every gather of the row is in flight at
+// once.  Ids are then taken 8 at a time: for each, the group expands the
+// id's owner list into shared memory -- owner o's unit cost at position
+// popc(owners below o), -0.0 after the last owner -- and afterwards every
+// lane runs its chains for the 8 ids back to back: += u_j, then += u_o for
+// the owners in ascending order, two per 16-byte broadcast load, entering a
+// fully unrolled run of pairs at the right offset (no loop, no predicate).
+// A lane whose worker holds the latest copy reads an all -0.0 list instead:
+// x + -0.0 == x for every x these chains produce, so padding and inactive
+// lanes are exact no-ops and each cell's add sequence is the reference's.
+// The row gap (two smallest of the row, with multiplicity) is a shuffle
+// reduction, order-independent, then one __dsub_rn.
+constexpr int kWarpRowsThreads = 128;
+constexpr int kIdsPerLane = 4;
+
+template <int NP>
+__global__ void __launch_bounds__(kWarpRowsThreads)
+    k_cost_build_warp(const uint32_t* __restrict__ ids, const uint64_t* __restrict__ offsets,
+                      uint64_t rows, int n, const ulonglong2* __restrict__ ol, uint64_t id_space,
+                      const double* __restrict__ ucost, double* __restrict__ matrix,
+                      uint64_t* __restrict__ gap_keys, uint32_t* __restrict__ row_index,
+                      int* __restrict__ flags) {
+  constexpr int RPW = 32 / NP;
+  constexpr int NW = kWarpRowsThreads / 32;
+  static_assert(NP <= 8, "wide rows use k_cost_build_wide");
+  constexpr int kSub = NP;  // ids per sub-batch: one whole load slot
+  // [warp][buffer][id of the sub-batch][32 lanes' list entries]
+  __shared__ __align__(16) double lists[NW][2][kSub][32];
+  __shared__ __align__(16) double zeros[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x < 32) zeros[threadIdx.x] = -0.0;
+  __syncthreads();
+  const int g = lane / NP, j = lane - g * NP;
+  const uint64_t i = (static_cast<uint64_t>(blockIdx.x) * NW + warp) * RPW + g;
+  const bool rowok = i < rows;
+  const bool cell = rowok && j < n;
+  const double uj = j < n ? ucost[j] : 0.0;
+  uint64_t beg = 0, end = 0;
+  if (rowok) {
+    beg = offsets[i];
+    end = offsets[i + 1];
+  }
+  const int len = static_cast<int>(end - beg);
+  const int maxlen = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(len));
+  const unsigned below_j = (1u << j) - 1u;
+  double c = 0.0;
+  bool bad = false;
+  int sb = 0;  // sub-batch parity
+  for (int t0 = 0; t0 < maxlen; t0 += kIdsPerLane * NP) {
+    unsigned own[kIdsPerLane], lat[kIdsPerLane];
+    uint32_t idv[kIdsPerLane];
+#pragma unroll
+    for (int s = 0; s < kIdsPerLane; ++s) {
+      const int idx = t0 + s * NP + j;
+      idv[s] = idx < len ? __ldg(ids + beg + idx) : 0xffffffffu;
+    }
+#pragma unroll
+    for (int s = 0; s < kIdsPerLane; ++s) {
+      const int idx = t0 + s * NP + j;
+      own[s] = 0u;
+      lat[s] = 0xffffffffu;  // past the row's end: no lane adds
+      if (idx < len) {
+        if (idv[s] < id_space) {
+          const ulonglong2 m = __ldg(ol + idv[s]);
+          own[s] = static_cast<unsigned>(m.x);
+          lat[s] = static_cast<unsigned>(m.y);
+        } else {
+          bad = true;
+        }
+      }
+    }
+    // Ids of slot s are t0 + s * NP + tt, held by lane tt of each group; a
+    // lane past its row's end holds (owners 0, latest all-ones), so ids beyond
+    // a row need no masking -- nobody adds for them.
+#pragma unroll
+    for (int s = 0; s < kIdsPerLane; ++s) {
+      if (t0 + s * NP >= maxlen) break;
+      for (int u0 = 0; u0 < NP; u0 += kSub) {
+        if (t0 + s * NP + u0 >= maxlen) break;
+        double (*buf)[32] = lists[warp][sb];
+        unsigned pm[kSub];
+        bool act[kSub];
+#pragma unroll
+        for (int q = 0; q < kSub; ++q) {
+          const unsigned O = __shfl_sync(0xffffffffu, own[s], u0 + q, NP);
+          const unsigned Lm = __shfl_sync(0xffffffffu, lat[s], u0 + q, NP);
+          const int p = __popc(O);
+          pm[q] = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(p));
+          const bool has = (O >> j) & 1u;
+          const int below = __popc(O & below_j);
+          buf[q][g * NP + (has ? below : p + (j - below))] = has ? uj : -0.0;
+          act[q] = cell && !((Lm >> j) & 1u);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < kSub; ++q) {
+          c = __dadd_rn(c, act[q] ? uj : -0.0);  // miss pull over j's link
+          // pushes, owners ascending, in blocks of 4 pairs: positions past the
+          // last owner hold -0.0, so whole blocks are exact
+          const double* lp = act[q] ? &buf[q][g * NP] : zeros;
+          const int nblk = (static_cast<int>(pm[q]) + 7) >> 3;
+#pragma unroll
+          for (int bk = 0; bk < (NP + 7) / 8; ++bk) {
+            if (bk >= nblk) break;
+            double2 v2[4];
+#pragma unroll
+            for (int h = 0; h < 4; ++h)
+              v2[h] = (8 * bk + 2 * h < NP) ? *reinterpret_cast<const double2*>(lp + 8 * bk + 2 * h)
+                                            : make_double2(-0.0, -0.0);
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              if (8 * bk + 2 * h < NP) {
+                c = __dadd_rn(c, v2[h].x);
+                c = __dadd_rn(c, v2[h].y);
+              }
+            }
+          }
+        }
+        sb ^= 1;
+      }
+    }
+  }
+  if (bad) atomicOr(flags + kFlagIdOutOfRange, 1);
+  if (cell) matrix[i * n + j] = c;
+  if (gap_keys == nullptr) return;
+  // two smallest of the row with multiplicity (row_gap_key, cost.hpp:130-146)
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  double s1 = cell ? c : inf, s2 = inf;
+#pragma unroll
+  for (int off = NP / 2; off > 0; off >>= 1) {
+    const double b1 = __shfl_xor_sync(0xffffffffu, s1, off, NP);
+    const double b2 = __shfl_xor_sync(0xffffffffu, s2, off, NP);
+    const double lo = s1 < b1 ? s1 : b1, hi = s1 < b1 ? b1 : s1;
+    const double m2 = s2 < b2 ? s2 : b2;
+    s1 = lo;
+    s2 = hi < m2 ? hi : m2;
+  }
+  if (rowok && j == 0) {
+    gap_keys[i] = gap_sort_key(__dsub_rn(s2, s1));
+    row_index[i] = static_cast<uint32_t>(i);
+  }
+}
+
+// K1 for wide rows (16 < NP <= 32 lanes per row; issue-bound at scale): the
+// same row layout, loads and list expansion, one id at a time -- list, one
+// __syncwarp, then the chain with every lane reading the same list (a
+// single broadcast per load) and the adds taken only by the lanes whose
+// worker does not hold the latest copy.  A compact loop body keeps the
+// instruction stream in cache.
+template <int NP>
+__global__ void __launch_bounds__(kWarpRowsThreads)
+    k_cost_build_wide(const uint32_t* __restrict__ ids, const uint64_t* __restrict__ offsets,
+                      uint64_t rows, int n, const ulonglong2* __restrict__ ol, uint64_t id_space,
+                      const double* __restrict__ ucost, double* __restrict__ matrix,
+                      uint64_t* __restrict__ gap_keys, uint32_t* __restrict__ row_index,
+                      int* __restrict__ flags) {
+  constexpr int RPW = 32 / NP;
+  __shared__ __align__(16) double lists[kWarpRowsThreads / 32][2][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane / NP, j = lane - g * NP;
+  const uint64_t i = (static_cast<uint64_t>(blockIdx.x) * (kWarpRowsThreads / 32) + warp) * RPW + g;
+  const bool rowok = i < rows;
+  const bool cell = rowok && j < n;
+  const double uj = j < n ? ucost[j] : 0.0;
+  uint64_t beg = 0, end = 0;
+  if (rowok) {
+    beg = offsets[i];
+    end = offsets[i + 1];
+  }
+  const int len = static_cast<int>(end - beg);
+  const int maxlen = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(len));
+  const unsigned below_j = (1u << j) - 1u;
+  double* const mylist = &lists[warp][0][g * NP];
+  double c = 0.0;
+  bool bad = false;
+  int t = 0;
+  for (int t0 = 0; t0 < maxlen; t0 += kIdsPerLane * NP) {
+    unsigned own[kIdsPerLane], lat[kIdsPerLane];
+    uint32_t idv[kIdsPerLane];
+#pragma unroll
+    for (int s = 0; s < kIdsPerLane; ++s) {
+      const int idx = t0 + s * NP + j;
+      idv[s] = idx < len ? __ldg(ids + beg + idx) : 0xffffffffu;
+    }
+#pragma unroll
+    for (int s = 0; s < kIdsPerLane; ++s) {
+      const int idx = t0 + s * NP + j;
+      own[s] = 0u;
+      lat[s] = 0xffffffffu;  // past the row's end: no lane adds
+      if (idx < len) {
+        if (idv[s] < id_space) {
+          const ulonglong2 m = __ldg(ol + idv[s]);
+          own[s] = static_cast<unsigned>(m.x);
+          lat[s] = static_cast<unsigned>(m.y);
+        } else {
+          bad = true;
+        }
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < kIdsPerLane; ++s) {
+      for (int tt = 0; tt < NP; ++tt, ++t) {
+        if (t >= maxlen) break;
+        const unsigned O = __shfl_sync(0xffffffffu, own[s], tt, NP);
+        const unsigned Lm = __shfl_sync(0xffffffffu, lat[s], tt, NP);
+        const int p = __popc(O);
+        const int pmax = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(p)));
+        const bool has = (O >> j) & 1u;
+        const int below = __popc(O & below_j);
+        double* buf = mylist + (t & 1) * 32;
+        buf[has ? below : p + (j - below)] = has ? uj : -0.0;
+        __syncwarp();
+        const bool active = cell && !((Lm >> j) & 1u);
+        if (active) c = __dadd_rn(c, uj);  // miss pull over j's link
+        for (int q = 0; q < pmax; q += 2) {  // one push per other owner, ascending
+          const double2 v2 = *reinterpret_cast<const double2*>(buf + q);
+          if (active) {
+            c = __dadd_rn(c, v2.x);
+            c = __dadd_rn(c, v2.y);
+          }
+        }
+      }
+    }
+  }
+  if (bad) atomicOr(flags + kFlagIdOutOfRange, 1);
+  if (cell) matrix[i * n + j] = c;
+  if (gap_keys == nullptr) return;
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  double s1 = cell ? c : inf, s2 = inf;
+#pragma unroll
+  for (int off = NP / 2; off > 0; off >>= 1) {
+    const double b1 = __shfl_xor_sync(0xffffffffu, s1, off, NP);
+    const double b2 = __shfl_xor_sync(0xffffffffu, s2, off, NP);
+    const double lo = s1 < b1 ? s1 : b1, hi = s1 < b1 ? b1 : s1;
+    const double m2 = s2 < b2 ? s2 : b2;
+    s1 = lo;
+    s2 = hi < m2 ? hi : m2;
+  }
+  if (rowok && j == 0) {
+    gap_keys[i] = gap_sort_key(__dsub_rn(s2, s1));
+    row_index[i] = static_cast<uint32_t>(i);
+  }
+}
+
 __global__ void k_gap_keys(const double* __restrict__ matrix, uint64_t rows, int n,
                            uint64_t* __restrict__ gap_keys, uint32_t* __restrict__ row_index) {
   const uint64_t r = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
@@ -123,6 +370,25 @@ void launch_cost_build(const uint32_t* ids, const uint64_t* offsets, uint64_t ro
                        const ulonglong2* ol, uint64_t id_space, const double* ucost,
                        double* matrix, uint64_t* gap_keys, uint32_t* row_index, int* flags,
                        cudaStream_t s) {
+  if (rows == 0) return;
+  if (n >= 2 && n <= 32) {
+    const int np = n <= 2 ? 2 : n <= 4 ? 4 : n <= 8 ? 8 : n <= 16 ? 16 : 32;
+    const uint64_t rows_per_block = static_cast<uint64_t>(kWarpRowsThreads / 32) * (32 / np);
+    const unsigned blocks = static_cast<unsigned>((rows + rows_per_block - 1) / rows_per_block);
+    auto go = [&](auto kern) {
+      kern<<<blocks, kWarpRowsThreads, 0, s>>>(ids, offsets, rows, n, ol, id_space, ucost, matrix,
+                                               gap_keys, row_index, flags);
+    };
+    switch (np) {
+      case 2: go(k_cost_build_warp<2>); break;
+      case 4: go(k_cost_build_warp<4>); break;
+      case 8: go(k_cost_build_warp<8>); break;
+      case 16: go(k_cost_build_wide<16>); break;
+      default: go(k_cost_build_wide<32>); break;
+    }
+    EDX_LAUNCHED();
+    return;
+  }
   const int rows_per_block = n >= kBlockCells ? 1 : kBlockCells / n;
   const int threads = rows_per_block * n;
   const uint64_t blocks = (rows + rows_per_block - 1) / rows_per_block;

@@ -137,6 +137,35 @@ def test_build_random_snapshots_bitwise(gpu, oracle, pyoracle, n):
     assert got.tobytes() == want.tobytes()
 
 
+@pytest.mark.parametrize("n", [2, 7, 8, 32])
+def test_build_long_and_empty_rows_bitwise(gpu, oracle, pyoracle, n):
+    """Rows longer than one load batch of the warp-row build (4 ids per lane)
+    and empty rows: every cell bitwise, gap order through ecomix."""
+    edx = gpu
+    rng = np.random.default_rng(2000 + n)
+    bw = rng.choice([5e9, 2e9, 5e8, 1e9], size=n)
+    m = 3
+    c = cfg(edx, n, m, bw)
+    oc = pyoracle.Cfg(n, m, bw)
+    snap, osnap = edx.Snapshot(), {}
+    full = (1 << n) - 1
+    for id_ in range(0, 3000, 2):
+        res = int(rng.integers(1, 1 << n)) & full
+        own = res & int(rng.integers(0, 1 << n)) if rng.integers(0, 3) else 0
+        lat = own if own else res & int(rng.integers(0, 1 << n))
+        snap[id_] = edx.EmbeddingState(own, lat, res)
+        osnap[id_] = (own, lat, res)
+    R = n * m
+    lens = rng.integers(0, 400, size=R)
+    lens[0] = 0
+    lens[-1] = 399
+    samples = [list(rng.choice(3000, size=l, replace=False)) for l in lens]
+    got = edx.build_matrix(samples, snap, c).values
+    ids, offs = edx.to_csr(samples)
+    want = oracle.build_matrix_snapshot(oc, osnap, ids, offs)
+    assert got.tobytes() == want.tobytes()
+
+
 # ------------------------------------------------------------- gap / order
 def test_row_gap_key_kat(gpu):
     edx = gpu
