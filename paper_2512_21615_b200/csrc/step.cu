@@ -23,6 +23,7 @@
 // stable sort of (worker, position) keys, counts are integer atomics
 // (order-free), and the realised cost is summed on the host in worker order
 // (sim.hpp:208-216).
+#include <cub/block/block_radix_sort.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -274,7 +275,7 @@ __global__ void k_cand_ranges(const int32_t* __restrict__ wlist, int nw, uint64_
   const int jl = static_cast<int>(x / capacity);
   const uint64_t s = x - static_cast<uint64_t>(jl) * capacity;
   const int j = wlist[jl];
-  if (s >= ws[j * kWS + kWsSize0]) return;
+  if (s >= ws[j * kWS + kWsSize0] || ws[j * kWS + kWsEvict] == 0) return;
   const uint64_t g = static_cast<uint64_t>(j) * capacity + s;
   const uint32_t id = sid[g];
   if (pinned_by(j, id, first_pos, uidx, ucap, need_first)) return;
@@ -308,7 +309,7 @@ __global__ void k_cand_pack(const int32_t* __restrict__ wlist, int nw, uint64_t 
   const uint64_t s = x - static_cast<uint64_t>(jl) * capacity;
   const int j = wlist[jl];
   uint64_t key = ~0ULL;
-  if (s < ws[j * kWS + kWsSize0]) {
+  if (s < ws[j * kWS + kWsSize0] && ws[j * kWS + kWsEvict] != 0) {
     const uint64_t g = static_cast<uint64_t>(j) * capacity + s;
     const uint32_t id = sid[g];
     if (!pinned_by(j, id, first_pos, uidx, ucap, need_first)) {
@@ -339,6 +340,124 @@ __global__ void k_cand_offsets(const int32_t* __restrict__ wlist, int nw, uint32
     run += w[kWsCand];
     if (w[kWsCand] < w[kWsEvict]) atomicOr(flags + kFlagPinned, 1);
   }
+}
+
+// Victim selection for caches of up to kSelCap entries: one CTA per worker.
+// The CTA finds its non-pinned entries, the per-worker value ranges of
+// (mark, frequency, last_access, id), packs each VictimKey (cache.hpp:47-58)
+// order-preservingly -- version (= the worker's latest bit) above mark above
+// frequency above last_access above id -- and block-radix-sorts them in
+// shared memory; non-candidates carry bit W and sort last.  The first E_j
+// sorted slots are the victims, in victim order.  No host round trip and no
+// device-wide sort.
+constexpr int kSelThreads = 1024, kSelItems = 12;
+constexpr uint64_t kSelCap = static_cast<uint64_t>(kSelThreads) * kSelItems;
+using SelSort = cub::BlockRadixSort<uint64_t, kSelThreads, kSelItems, uint32_t>;
+
+__global__ void __launch_bounds__(kSelThreads, 1)
+    k_select_victims(uint64_t capacity, uint32_t* __restrict__ ws, const uint32_t* __restrict__ sid,
+                     const uint32_t* __restrict__ smark, const uint32_t* __restrict__ sfreq,
+                     const uint32_t* __restrict__ slast, const ulonglong2* __restrict__ ol,
+                     const int32_t* __restrict__ first_pos, const uint32_t* __restrict__ uidx,
+                     uint64_t ucap, const int32_t* __restrict__ need_first,
+                     uint32_t* __restrict__ cand_slot_sorted, int* __restrict__ flags) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  auto& temp = *reinterpret_cast<typename SelSort::TempStorage*>(smem);
+  __shared__ uint32_t part[kSelThreads / 32][9];
+  __shared__ uint32_t tot[9];
+  const int j = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t* w = ws + j * kWS;
+  const uint32_t E = w[kWsEvict];
+  const uint64_t gb = static_cast<uint64_t>(j) * capacity;
+  if (E == 0) {
+    if (tid == 0) {
+      w[kWsCand] = 0;
+      w[kWsCandOff] = static_cast<uint32_t>(gb);
+    }
+    return;
+  }
+  const uint32_t size0 = w[kWsSize0];
+  bool cf[kSelItems];
+  // v[0..3] = min of mark, freq, last, id; v[4..7] = max; v[8] = candidates
+  uint32_t v[9] = {UINT_MAX, UINT_MAX, UINT_MAX, UINT_MAX, 0, 0, 0, 0, 0};
+#pragma unroll
+  for (int k = 0; k < kSelItems; ++k) {
+    const uint32_t sl = tid * kSelItems + k;
+    cf[k] = false;
+    if (sl < size0) {
+      const uint32_t id = sid[gb + sl];
+      if (!pinned_by(j, id, first_pos, uidx, ucap, need_first)) {
+        cf[k] = true;
+        const uint32_t f[4] = {smark[gb + sl], sfreq[gb + sl], slast[gb + sl], id};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          v[q] = min(v[q], f[q]);
+          v[4 + q] = max(v[4 + q], f[q]);
+        }
+        ++v[8];
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    v[q] = __reduce_min_sync(0xffffffffu, v[q]);
+    v[4 + q] = __reduce_max_sync(0xffffffffu, v[4 + q]);
+  }
+  v[8] = __reduce_add_sync(0xffffffffu, v[8]);
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < 9; ++q) part[warp][q] = v[q];
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      const uint32_t x = part[lane][q];
+      tot[q] = q < 4 ? __reduce_min_sync(0xffffffffu, x)
+                     : (q < 8 ? __reduce_max_sync(0xffffffffu, x) : __reduce_add_sync(0xffffffffu, x));
+    }
+  }
+  __syncthreads();
+  const uint32_t cnt = tot[8];
+  const int wm = width_of(tot[0], tot[4]), wf = width_of(tot[1], tot[5]);
+  const int wl = width_of(tot[2], tot[6]), wi = width_of(tot[3], tot[7]);
+  const int W = 1 + wm + wf + wl + wi;  // <= 1 + 4 * 32
+  if (W > 63) {
+    if (tid == 0) atomicOr(flags + kFlagKeyRange, 1);
+    return;
+  }
+  uint64_t keys[kSelItems];
+  uint32_t slots[kSelItems];
+#pragma unroll
+  for (int k = 0; k < kSelItems; ++k) {
+    const uint32_t sl = tid * kSelItems + k;
+    slots[k] = sl;
+    keys[k] = 1ULL << W;  // not a candidate: after every candidate
+    if (cf[k]) {
+      const uint32_t id = sid[gb + sl];
+      uint64_t key = (ol[id].y >> j) & 1ULL;  // version: a stale copy goes first
+      key = (key << wm) | (smark[gb + sl] - tot[0]);
+      key = (key << wf) | (sfreq[gb + sl] - tot[1]);
+      key = (key << wl) | (slast[gb + sl] - tot[2]);
+      key = (key << wi) | (id - tot[3]);
+      keys[k] = key;
+    }
+  }
+  SelSort(temp).Sort(keys, slots, 0, W + 1);
+  const uint32_t take = min(E, cnt);
+#pragma unroll
+  for (int k = 0; k < kSelItems; ++k) {
+    const uint32_t r = tid * kSelItems + k;  // blocked arrangement: sorted rank
+    if (r < take) cand_slot_sorted[gb + r] = slots[k];
+  }
+  if (tid == 0) {
+    w[kWsCand] = cnt;
+    w[kWsCandOff] = static_cast<uint32_t>(gb);
+    if (cnt < E) atomicOr(flags + kFlagPinned, 1);
+  }
+}
+
+__global__ void k_init_ranges(uint32_t* __restrict__ ranges) {
+  if (threadIdx.x < 8) ranges[threadIdx.x] = (threadIdx.x & 1) ? 0u : UINT_MAX;
 }
 
 // evicting insert contribution: +1 for the insert, -1 if its victim carries
@@ -570,6 +689,26 @@ void step_init_state(edx_engine* e) {
   s.counters.ensure(3 * n + 4);
   s.wscalars.ensure(n * kWS);
   s.ranges.ensure(8);
+  // victim candidates of every worker (a worker with no evictions skips its share)
+  const uint64_t cand = n * e->capacity;
+  s.cand_slot_sorted.ensure(cand);
+  s.cand_count.ensure(cand);  // the victim-id list
+  if (e->capacity > kSelCap) {
+    s.cand_key.ensure(cand);
+    s.cand_key_sorted.ensure(cand);
+    s.cand_slot.ensure(cand);
+  }
+  s.cand_off.ensure(128);  // [0,64): workers 0..n-1; [64,128): evicting workers (large caches)
+  std::vector<int32_t> wl(n);
+  for (uint64_t j = 0; j < n; ++j) wl[j] = static_cast<int32_t>(j);
+  EDX_CUDA(cudaMemcpyAsync(s.cand_off.p, wl.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice,
+                           e->stream));
+  EDX_CUDA(cudaStreamSynchronize(e->stream));
+  if (e->capacity <= kSelCap) {
+    static const size_t sel_smem = sizeof(typename SelSort::TempStorage);
+    EDX_CUDA(cudaFuncSetAttribute(k_select_victims, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(sel_smem)));
+  }
 }
 
 namespace {
@@ -619,8 +758,10 @@ void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
   int wbits = 1;
   while ((1 << wbits) < n) ++wbits;
   cub_call(e, [&](void* tmp, size_t& b) {
+    // items arrive in position order and the sort is stable: sorting on the
+    // worker field alone leaves each worker's items in first-occurrence order
     return cub::DeviceRadixSort::SortKeys(tmp, b, s.need_key.p, s.need_key_sorted.p,
-                                          static_cast<int>(T), 0, 32 + wbits + 1, st);
+                                          static_cast<int>(T), 32, 32 + wbits + 1, st);
   });
   launches += 4;
   k_phase1<<<grid_for(T), kT, 0, st>>>(s.uniq.p, s.umask.p, s.counters.p, n, e->ol.p, s.counters.p);
@@ -640,68 +781,75 @@ void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
   EDX_LAUNCHED();
   launches += 2;
 
-  // The host needs E_j to size the victim selection (the only mid-step sync).
-  std::vector<uint32_t> ws(static_cast<size_t>(n) * kWS);
-  EDX_CUDA(cudaMemcpyAsync(ws.data(), s.wscalars.p, ws.size() * sizeof(uint32_t),
-                           cudaMemcpyDeviceToHost, st));
-  EDX_CUDA(cudaStreamSynchronize(st));
-  std::vector<int32_t> wl;
-  for (int j = 0; j < n; ++j)
-    if (ws[j * kWS + kWsEvict] > 0) wl.push_back(j);
-  const int nw = static_cast<int>(wl.size());
-
-  int32_t* d_wlist = nullptr;
-  if (nw > 0) {
-    const uint64_t cand = static_cast<uint64_t>(nw) * e->capacity;
-    s.cand_key.ensure(cand);
-    s.cand_key_sorted.ensure(cand);
-    s.cand_slot.ensure(cand);
-    s.cand_slot_sorted.ensure(cand);
-    s.cand_count.ensure(cand);  // reused as the victim-id list
-    s.cand_off.ensure(64);
-    d_wlist = reinterpret_cast<int32_t*>(s.cand_off.p);
-    EDX_CUDA(cudaMemcpyAsync(d_wlist, wl.data(), nw * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-    const uint32_t init[8] = {UINT_MAX, 0, UINT_MAX, 0, UINT_MAX, 0, UINT_MAX, 0};
-    EDX_CUDA(cudaMemcpyAsync(s.ranges.p, init, sizeof init, cudaMemcpyHostToDevice, st));
-    k_cand_ranges<<<grid_for(cand), kT, 0, st>>>(d_wlist, nw, e->capacity, s.wscalars.p, c.sid.p,
-                                                 c.smark.p, c.sfreq.p, c.slast.p, s.first_pos.p,
-                                                 s.uidx_of_pos.p, ucap, s.need_first.p, s.ranges.p);
-    k_cand_pack<<<grid_for(cand), kT, 0, st>>>(d_wlist, nw, e->capacity, s.wscalars.p, c.sid.p,
-                                               c.smark.p, c.sfreq.p, c.slast.p, e->ol.p,
-                                               s.first_pos.p, s.uidx_of_pos.p, ucap, s.need_first.p,
-                                               s.ranges.p, s.cand_key.p, s.cand_slot.p, e->flags.p);
+  // Victim selection (evict_for, cache.hpp:152-170), every worker at once;
+  // workers without evictions drop out on the device.
+  const int32_t* d_wlist = reinterpret_cast<const int32_t*>(s.cand_off.p);
+  int nw = n;  // workers the victim kernels visit
+  if (e->capacity <= kSelCap) {
+    k_select_victims<<<n, kSelThreads, sizeof(typename SelSort::TempStorage), st>>>(
+        e->capacity, s.wscalars.p, c.sid.p, c.smark.p, c.sfreq.p, c.slast.p, e->ol.p,
+        s.first_pos.p, s.uidx_of_pos.p, ucap, s.need_first.p, s.cand_slot_sorted.p, e->flags.p);
     EDX_LAUNCHED();
-    cub_call(e, [&](void* tmp, size_t& b) {
-      return cub::DeviceRadixSort::SortPairs(tmp, b, s.cand_key.p, s.cand_key_sorted.p,
-                                             s.cand_slot.p, s.cand_slot_sorted.p,
-                                             static_cast<int>(cand), 0, 64, st);
-    });
-    k_cand_offsets<<<1, 32, 0, st>>>(d_wlist, nw, s.wscalars.p, e->flags.p);
-    k_evict_contrib<<<grid_for(T), kT, 0, st>>>(s.need_key_sorted.p, s.counters.p, n,
-                                                s.need_type.p, s.ins_rank.p, s.wscalars.p,
-                                                s.cand_slot_sorted.p, c.smark.p, e->capacity,
-                                                c.cur_mark.p, s.need_contrib.p);
-    EDX_LAUNCHED();
-    launches += 3 + 8 + 2;
+    launches += 1;
+  } else {
+    // Large caches: the device-wide sort is sized by the host, so fetch E_j
+    // (one mid-step sync) and sort only the candidates of evicting workers
+    // (none while the caches are still filling).
+    std::vector<uint32_t> ws(static_cast<size_t>(n) * kWS);
+    EDX_CUDA(cudaMemcpyAsync(ws.data(), s.wscalars.p, ws.size() * sizeof(uint32_t),
+                             cudaMemcpyDeviceToHost, st));
+    EDX_CUDA(cudaStreamSynchronize(st));
+    std::vector<int32_t> wl;
+    for (int j = 0; j < n; ++j)
+      if (ws[j * kWS + kWsEvict] > 0) wl.push_back(j);
+    nw = static_cast<int>(wl.size());
+    if (nw > 0) {
+      int32_t* d_wl = reinterpret_cast<int32_t*>(s.cand_off.p) + 64;
+      EDX_CUDA(cudaMemcpyAsync(d_wl, wl.data(), nw * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+      const uint64_t cand = static_cast<uint64_t>(nw) * e->capacity;
+      k_init_ranges<<<1, 32, 0, st>>>(s.ranges.p);
+      k_cand_ranges<<<grid_for(cand), kT, 0, st>>>(d_wl, nw, e->capacity, s.wscalars.p, c.sid.p,
+                                                   c.smark.p, c.sfreq.p, c.slast.p, s.first_pos.p,
+                                                   s.uidx_of_pos.p, ucap, s.need_first.p, s.ranges.p);
+      k_cand_pack<<<grid_for(cand), kT, 0, st>>>(d_wl, nw, e->capacity, s.wscalars.p, c.sid.p,
+                                                 c.smark.p, c.sfreq.p, c.slast.p, e->ol.p,
+                                                 s.first_pos.p, s.uidx_of_pos.p, ucap,
+                                                 s.need_first.p, s.ranges.p, s.cand_key.p,
+                                                 s.cand_slot.p, e->flags.p);
+      EDX_LAUNCHED();
+      cub_call(e, [&](void* tmp, size_t& b) {
+        return cub::DeviceRadixSort::SortPairs(tmp, b, s.cand_key.p, s.cand_key_sorted.p,
+                                               s.cand_slot.p, s.cand_slot_sorted.p,
+                                               static_cast<int>(cand), 0, 64, st);
+      });
+      k_cand_offsets<<<1, 32, 0, st>>>(d_wl, nw, s.wscalars.p, e->flags.p);
+      EDX_LAUNCHED();
+      launches += 4 + 8;
+    }
   }
+  k_evict_contrib<<<grid_for(T), kT, 0, st>>>(s.need_key_sorted.p, s.counters.p, n, s.need_type.p,
+                                              s.ins_rank.p, s.wscalars.p, s.cand_slot_sorted.p,
+                                              c.smark.p, e->capacity, c.cur_mark.p,
+                                              s.need_contrib.p);
+  EDX_LAUNCHED();
   cub_call(e, [&](void* tmp, size_t& b) {
     return cub::DeviceScan::ExclusiveSum(tmp, b, s.need_contrib.p,
                                          reinterpret_cast<int32_t*>(s.flag_scan.p),
                                          static_cast<int>(T + 1), st);
   });
   const int32_t* con_scan = reinterpret_cast<const int32_t*>(s.flag_scan.p);
-  launches += 1;
+  k_find_advance<<<grid_for(T), kT, 0, st>>>(s.need_key_sorted.p, s.counters.p, n, s.need_type.p,
+                                             s.ins_rank.p, con_scan, s.wscalars.p, c.at_cur.p,
+                                             e->capacity);
   if (nw > 0) {
-    k_find_advance<<<grid_for(T), kT, 0, st>>>(s.need_key_sorted.p, s.counters.p, n, s.need_type.p,
-                                               s.ins_rank.p, con_scan, s.wscalars.p, c.at_cur.p,
-                                               e->capacity);
     dim3 g(8, nw);
-    k_evict<<<g, kT, 0, st>>>(d_wlist, nw, s.wscalars.p, s.cand_slot_sorted.p, c.sid.p,
+    const int32_t* wlv = e->capacity <= kSelCap ? d_wlist : d_wlist + 64;
+    k_evict<<<g, kT, 0, st>>>(wlv, nw, s.wscalars.p, s.cand_slot_sorted.p, c.sid.p,
                               e->capacity, e->id_space, e->ol.p, e->res.p, c.slot_of.p,
                               s.cand_count.p, s.counters.p, n);
-    EDX_LAUNCHED();
-    launches += 2;
   }
+  EDX_LAUNCHED();
+  launches += 5;
   k_apply<<<grid_for(T), kT, 0, st>>>(s.need_key_sorted.p, s.counters.p, n, e->cur_ids,
                                       s.need_type.p, s.ins_rank.p, s.wscalars.p,
                                       s.cand_slot_sorted.p, e->capacity, e->id_space, c.cur_mark.p,
@@ -719,7 +867,7 @@ void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
   EDX_CUDA(cudaMemcpyAsync(e->h_counters, s.counters.p, (3 * n + 4) * sizeof(unsigned long long),
                            cudaMemcpyDeviceToHost, st));
   out->launches = launches;
-  out->evicting_workers = nw;
+  out->evicting_workers = e->capacity <= kSelCap ? -1 : nw;  // -1: decided on the device
 }
 
 }  // namespace edx
