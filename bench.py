@@ -141,6 +141,21 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------- product arm
+def fp64_adds(w, ids, glob):
+    """F_alg = sum over (cell, id) with the latest copy not on the
+    cell's worker of (1 + popcount(owners)) -- per id occurrence,
+    (n - popcount(latest)) * (1 + popcount(owners)) -- from the state the build reads."""
+    gid, ow, la, _ = glob
+    order = np.argsort(gid)
+    sid = gid[order]
+    pos = np.minimum(np.searchsorted(sid, ids), max(len(sid) - 1, 0))
+    hit = (sid[pos] == ids) if len(sid) else np.zeros(len(ids), bool)
+    o = np.where(hit, ow[order][pos], 0).astype(np.uint64)
+    l = np.where(hit, la[order][pos], 0).astype(np.uint64)
+    nl = w["n"] - np.bitwise_count(l).astype(np.int64)
+    return int(np.sum(nl * (1 + np.bitwise_count(o).astype(np.int64))))
+
+
 def algorithmic_build_bytes(w, ids):
     """B_alg = 4 R L (ids) + 16 U (owners+latest per unique id)
     + 8 n (unit costs) + 8 R n (matrix write)."""
@@ -206,6 +221,8 @@ def product(args, w, rank, world, local_rank):
 
     for i in range(W):
         one_resident(i)
+    # FP64 adds of the first timed build, from the state it reads (untimed)
+    f_alg = fp64_adds(w, seg[W], eng.global_masks()) if world == 1 else None
     eng.set_profiling(True)
     eng.phase_times(reset=True)
     with ClockSampler(local_rank) as clk:
@@ -241,6 +258,12 @@ def product(args, w, rank, world, local_rank):
         pass
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     achieved = (sum(b_alg) / K) / (t_build_ms * 1e-3) / 1e9 if t_build_ms > 0 else None
+    dadd_peak = None
+    try:
+        dadd_peak = json.load(open(os.path.join(ROOT, "profiles", "r01_dadd_peak.json")))["dadd_per_s"]
+    except (OSError, ValueError, KeyError):
+        pass
+    fp64_rate = f_alg / (t_build_ms * 1e-3) if (f_alg and t_build_ms > 0) else None
     traffic = None
     try:
         traffic = json.load(open(os.path.join(ROOT, "profiles", "k_cost_build_traffic.json")))
@@ -259,13 +282,21 @@ def product(args, w, rank, world, local_rank):
         "e2e": {"value": R / (e2e_step_ms * 1e-3), "unit": "samples/s",
                 "ms_per_step": e2e_step_ms, "h2d_bytes_per_step": R * L * 4 + (R + 1) * 8,
                 "d2h_bytes_per_step": R * 4 + 8 + (3 * n + 4) * 8},
-        "roofline": {"kernel": "k_cost_build (K1, cost.hpp:81-125)", "bound": "hbm",
+        "roofline": {"kernel": ("k_cost_build_warp" if 2 <= n <= 8 else "k_cost_build_wide"
+                                if 8 < n <= 32 else "k_cost_build") + " (K1, cost.hpp:81-125)",
+                     "bound": "hbm",
                      "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": (achieved / hbm_peak) if achieved else None, "traffic": traffic,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else
                      "fallback 6.65 TB/s",
                      "algorithmic_bytes_per_launch": sum(b_alg) / K,
-                     "unique_ids_per_batch": sum(uniq) / K, "launch_ms": t_build_ms},
+                     "unique_ids_per_batch": sum(uniq) / K, "launch_ms": t_build_ms,
+                     "fp64": {"adds_per_launch": f_alg, "achieved_adds_per_s": fp64_rate,
+                              "peak_adds_per_s": dadd_peak,
+                              "frac": (fp64_rate / dadd_peak) if (fp64_rate and dadd_peak) else None,
+                              "peak_source": "profiles/r01_dadd_peak.json (tools/dadd_peak.cu)",
+                              "note": "second roof of the build (sequential fp64 add chains, "
+                                      "SURVEY 8d); adds counted on the first timed batch"}},
         "dominant_kernel": "k_hungarian_blocks (exact EcoMix block; latency-bound single warp)",
         "solver": {"exact_rows": n * int(np.floor(m * w["alpha"] + 1e-9)),
                    "latency_ms_per_batch": phase_ms[2] / K,

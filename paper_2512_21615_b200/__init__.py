@@ -537,6 +537,18 @@ class SimState:
         check(lib().edx_engine_cache_marks(self._h, int(worker), C.byref(cur), C.byref(at)))
         return int(cur.value), int(at.value)
 
+    def global_masks(self):
+        """(ids, owners, latest, resident) of every id with a non-zero state."""
+        cnt = C.c_uint64()
+        check(lib().edx_engine_export_global(self._h, None, None, None, None, 0, C.byref(cnt)))
+        k = cnt.value
+        ids = np.empty(k, np.uint32)
+        ow, la, re = (np.empty(k, np.uint64) for _ in range(3))
+        check(lib().edx_engine_export_global(self._h, _ptr(ids, C.c_uint32), _ptr(ow, C.c_uint64),
+                                             _ptr(la, C.c_uint64), _ptr(re, C.c_uint64), k,
+                                             C.byref(cnt)))
+        return ids, ow, la, re
+
     def canonical_state(self):
         """(global, caches) in the same canonical form as oracle.pyoracle.Sim."""
         cnt = C.c_uint64()
