@@ -237,6 +237,18 @@ def product(args, w, rank, world, local_rank):
     solver_steps = int(counts[1])
     step_ms = sum(ms) / K
 
+    # ---- K8 baseline_hitgreedy latency on the same resident batches (reported
+    # beside the metric), on a copy of the state's clock
+    hg_ms = None
+    if world == 1:
+        def one_hitgreedy(i):
+            eng.load(None, on_device=True, ids_ptr=d_ids[i].data_ptr(),
+                     offsets_ptr=d_offs.data_ptr(), rows=R)
+            eng.dispatch_hitgreedy(want_decision=False)
+        one_hitgreedy(W)
+        hg = timed(one_hitgreedy, range(W, W + K))
+        hg_ms = sum(hg) / K
+
     # ---- e2e: through edx_engine_iterate from pinned host buffers
     seg2 = host[P + W + K:]
     pinned = torch.from_numpy(np.stack(seg2).view(np.int32)).pin_memory()
@@ -309,6 +321,8 @@ def product(args, w, rank, world, local_rank):
                          "unit": "samples/s",
                          "note": "reference timing regions only (matrix_s + decision_s, "
                                  "sim.hpp:423-432)"},
+        "hitgreedy": {"ms_per_batch": hg_ms, "note": "baseline_hitgreedy (assign.hpp:346-392) "
+                      "on the resident batches after the timed region: scores, order, assignment"},
         "clocks": clk.summary(),
         "gpu_launches": launches,
     }

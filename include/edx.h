@@ -119,6 +119,12 @@ int edx_engine_build(edx_engine* e, double* matrix_out);
  * configured alpha.  Either output may be NULL. */
 int edx_engine_dispatch(edx_engine* e, double alpha, int32_t* decision_out,
                         double* expected_cost_out);
+/* baseline_hitgreedy(samples, snapshot, cfg) — assign.hpp:346-392 (the
+ * paper's relevance-score / LAIA-proxy baseline, dispatch_with kHitGreedy,
+ * sim.hpp:390-391) on the loaded batch and the engine's live state.  The
+ * decision stays on device for edx_engine_step(e, NULL, ...); decision_out
+ * may be NULL.  EDX_INVALID_ARGUMENT "sample count must be m*n". */
+int edx_engine_dispatch_hitgreedy(edx_engine* e, int32_t* decision_out);
 /* SimState::step(samples, decision) — sim.hpp:87-218.  decision NULL = the
  * engine's last dispatch (already on device). */
 int edx_engine_step(edx_engine* e, const int32_t* decision, edx_report* rep);
@@ -183,6 +189,12 @@ int edx_build_matrix(const edx_cluster_config* cfg, const uint32_t* snap_ids,
                      const uint64_t* snap_owners, const uint64_t* snap_latest,
                      const uint64_t* snap_resident, uint64_t snap_count, const uint32_t* ids,
                      const uint64_t* offsets, uint64_t num_samples, double* out);
+/* baseline_hitgreedy — assign.hpp:346-392 on a snapshot ({owners, latest}
+ * per id; residency is not consulted).  decision: num_samples entries. */
+int edx_hitgreedy(const edx_cluster_config* cfg, const uint32_t* snap_ids,
+                  const uint64_t* snap_owners, const uint64_t* snap_latest, uint64_t snap_count,
+                  const uint32_t* ids, const uint64_t* offsets, uint64_t num_samples,
+                  int32_t* decision);
 /* expected_cost(sample, j, snapshot, cfg) for every j and every given sample
  * (cost.hpp:81-100) — build_matrix without the m*n sample-count check. */
 int edx_expected_costs(const edx_cluster_config* cfg, const uint32_t* snap_ids,

@@ -1,7 +1,8 @@
 // Drop-in for the reference's assign.hpp hot path: the exact solver, the
 // capacity-bounded greedy, the gap order and the EcoMix hybrid, all executed
-// by libedx kernels (hungarian.cu, dispatch.cu).  The experimental baselines
-// (random / round-robin / hit-greedy) are not part of the device path.
+// by libedx kernels (hungarian.cu, dispatch.cu), and the hit-greedy baseline
+// (hitgreedy.cu).  The random / round-robin baselines are not part of the
+// device path.
 #pragma once
 
 #include <algorithm>
@@ -115,6 +116,29 @@ inline DispatchDecision ecomix(const CostMatrix& matrix, const ClusterConfig& cf
   const edx_cluster_config c = edxc::to_c(cfg);
   edxc::check(edx_ecomix(&c, matrix.rows, matrix.cols, matrix.values.data(),
                          rid.empty() ? nullptr : rid.data(), dec.data()));
+  d.worker_of_sample.assign(dec.begin(), dec.end());
+  return d;
+}
+
+// assign.hpp:346-392 (edx_hitgreedy / edx_engine_dispatch_hitgreedy): the
+// relevance-score baseline on the snapshot -- the live device state when the
+// snapshot is the engine's current one.
+inline DispatchDecision baseline_hitgreedy(const std::vector<EmbeddingSample>& samples,
+                                           const Snapshot& snap, const ClusterConfig& cfg) {
+  if (samples.size() != cfg.samples_per_iteration())
+    throw std::invalid_argument("sample count must be m*n");
+  std::vector<int32_t> dec(samples.size());
+  const edxc::Csr csr(samples);
+  if (snap.engine && edx_engine_clock(snap.engine) == snap.engine_clock) {
+    edxc::check(edx_engine_load_batch(snap.engine, csr.ids.data(), csr.offsets.data(), samples.size(), 0));
+    edxc::check(edx_engine_dispatch_hitgreedy(snap.engine, dec.data()));
+  } else {
+    const edxc::SnapArrays a(snap);
+    const edx_cluster_config c = edxc::to_c(cfg);
+    edxc::check(edx_hitgreedy(&c, a.ids.data(), a.owners.data(), a.latest.data(), a.ids.size(),
+                              csr.ids.data(), csr.offsets.data(), samples.size(), dec.data()));
+  }
+  DispatchDecision d;
   d.worker_of_sample.assign(dec.begin(), dec.end());
   return d;
 }

@@ -182,16 +182,23 @@ class SimState {
   mutable std::vector<WorkerCache> views_;
 };
 
-// sim.hpp:271-318, EcoMix only (the baselines are outside the device path).
+// sim.hpp:271-318 for the mechanisms on the device path: EcoMix and the
+// hit-greedy baseline (random / round-robin are outside it).
 struct Mechanism {
-  enum class Kind { kEcoMix };
+  enum class Kind { kEcoMix, kHitGreedy };
   Kind kind = Kind::kEcoMix;
   double alpha = 1.0;
-  std::string name() const { return "ecomix:" + detail::format_double(alpha); }
+  std::string name() const {
+    return kind == Kind::kHitGreedy ? std::string("hitgreedy") : "ecomix:" + detail::format_double(alpha);
+  }
   bool needs_snapshot() const { return true; }
-  bool needs_matrix() const { return true; }
+  bool needs_matrix() const { return kind == Kind::kEcoMix; }
   static Mechanism parse(const std::string& text) {
     Mechanism mech;
+    if (text == "hitgreedy") {
+      mech.kind = Kind::kHitGreedy;
+      return mech;
+    }
     if (text == "ecomix" || text.rfind("ecomix:", 0) == 0) {
       if (text.size() > 7) {
         try {
@@ -203,7 +210,8 @@ struct Mechanism {
       if (mech.alpha < 0.0 || mech.alpha > 1.0) throw std::invalid_argument("alpha must lie in [0, 1]");
       return mech;
     }
-    throw std::invalid_argument("unknown mechanism '" + text + "' (the device path runs ecomix)");
+    throw std::invalid_argument("unknown mechanism '" + text +
+                                "' (the device path runs ecomix and hitgreedy)");
   }
 };
 
@@ -260,21 +268,23 @@ inline RunResult run(SampleStream& stream, const Mechanism& mech, const ClusterC
       throw std::invalid_argument("stream underrun: iteration is short of samples");
     const edxc::Csr csr(samples);
     edxc::check(edx_engine_load_batch(e, csr.ids.data(), csr.offsets.data(), samples.size(), 0));
+    const bool hybrid = mech.needs_matrix();
     const auto t0 = clk::now();
-    edxc::check(edx_engine_build(e, nullptr));
+    if (hybrid) edxc::check(edx_engine_build(e, nullptr));
     const auto t1 = clk::now();
     double expected = 0.0;
     std::vector<int32_t> dec(samples.size());
-    edxc::check(edx_engine_dispatch(e, mech.alpha, dec.data(), &expected));
+    if (hybrid) edxc::check(edx_engine_dispatch(e, mech.alpha, dec.data(), &expected));
+    else edxc::check(edx_engine_dispatch_hitgreedy(e, dec.data()));
     const auto t2 = clk::now();
     edxc::Report raw(cfg.n);
     edxc::check(edx_engine_step(e, nullptr, &raw.c));
     IterationReport rep = raw.to_report();
     rep.mechanism = mech.name();
-    rep.matrix_s = std::chrono::duration<double>(t1 - t0).count();
+    rep.matrix_s = hybrid ? std::chrono::duration<double>(t1 - t0).count() : 0.0;
     rep.decision_s = std::chrono::duration<double>(t2 - t1).count();
     rep.expected_cost_s = expected;
-    rep.has_expected = true;
+    rep.has_expected = hybrid;
     if (opt.validate_state) state.validate_consistency();
     if (iteration >= opt.warmup) {
       ++s.measured_iterations;
@@ -285,7 +295,7 @@ inline RunResult run(SampleStream& stream, const Mechanism& mech, const ClusterC
       s.lookups += rep.lookups;
       s.cost_s += rep.cost_s;
       s.expected_cost_s += rep.expected_cost_s;
-      s.has_expected = true;
+      s.has_expected = hybrid;
       s.matrix_s_total += rep.matrix_s;
       for (std::size_t j = 0; j < static_cast<std::size_t>(cfg.n); ++j) {
         s.miss_pull_w[j] += rep.miss_pull_w[j];

@@ -376,6 +376,83 @@ int orc_build_matrix_snapshot(const orc_cluster_config* cfg, const uint32_t* sna
   return rc;
 }
 
+/* baseline_hitgreedy — assign.hpp:346-392.  A sample scores worker j by how
+ * many of its ids have their latest copy on j; samples commit in order of
+ * best score (desc), index (asc); each takes its best-scoring worker with
+ * workload left, ties to the larger remaining workload, then the lower index
+ * (strict comparisons over ascending j). */
+typedef struct {
+  int best;
+  uint64_t index;
+} hg_key;
+
+static int hg_cmp(const void* a, const void* b) {
+  const hg_key* x = (const hg_key*)a;
+  const hg_key* y = (const hg_key*)b;
+  if (x->best != y->best) return x->best > y->best ? -1 : 1;
+  return x->index < y->index ? -1 : (x->index > y->index ? 1 : 0);
+}
+
+static int hitgreedy(const orc_cluster_config* cfg, const gstate* g, const uint32_t* ids,
+                     const uint64_t* offsets, uint64_t R, int32_t* decision) {
+  if (R != (uint64_t)cfg->n * (uint64_t)cfg->m)
+    return fail(ORC_INVALID_ARGUMENT, "sample count must be m*n");
+  const int n = cfg->n;
+  int* score = (int*)calloc(R * (uint64_t)n + 1, sizeof(int));
+  hg_key* order = (hg_key*)malloc(sizeof(hg_key) * (R ? R : 1));
+  int* remaining = (int*)malloc(sizeof(int) * (uint64_t)n);
+  for (uint64_t i = 0; i < R; ++i) {
+    int* sc = score + i * (uint64_t)n;
+    for (uint64_t t = offsets[i]; t < offsets[i + 1]; ++t) {
+      int32_t x = idmap_get(&g->map, ids[t]);
+      uint64_t holders = x >= 0 ? g->latest[x] : 0;
+      while (holders) {
+        ++sc[__builtin_ctzll(holders)];
+        holders &= holders - 1;
+      }
+    }
+    int best = sc[0];
+    for (int j = 1; j < n; ++j)
+      if (sc[j] > best) best = sc[j];
+    order[i].best = best;
+    order[i].index = i;
+  }
+  qsort(order, R, sizeof(hg_key), hg_cmp); /* total order: index breaks ties */
+  for (int j = 0; j < n; ++j) remaining[j] = cfg->m;
+  for (uint64_t t = 0; t < R; ++t) {
+    const uint64_t i = order[t].index;
+    const int* sc = score + i * (uint64_t)n;
+    int best = -1;
+    for (int j = 0; j < n; ++j) {
+      if (remaining[j] <= 0) continue;
+      if (best < 0 || sc[j] > sc[best] || (sc[j] == sc[best] && remaining[j] > remaining[best]))
+        best = j;
+    }
+    --remaining[best];
+    decision[i] = best;
+  }
+  free(score);
+  free(order);
+  free(remaining);
+  return ORC_OK;
+}
+
+int orc_hitgreedy_snapshot(const orc_cluster_config* cfg, const uint32_t* snap_ids,
+                           const uint64_t* snap_owners, const uint64_t* snap_latest,
+                           uint64_t snap_count, const uint32_t* ids, const uint64_t* offsets,
+                           uint64_t R, int32_t* decision) {
+  gstate g;
+  gstate_init(&g, snap_count + 16);
+  for (uint64_t s = 0; s < snap_count; ++s) {
+    int64_t x = gstate_ref(&g, snap_ids[s]);
+    g.owners[x] = snap_owners[s];
+    g.latest[x] = snap_latest[s];
+  }
+  int rc = hitgreedy(cfg, &g, ids, offsets, R, decision);
+  gstate_free(&g);
+  return rc;
+}
+
 /* row_gap_key — cost.hpp:130-146 */
 static double gap_of(uint64_t cols, const double* row) {
   if (cols == 1) return 0.0;
@@ -780,6 +857,11 @@ uint64_t orc_sim_clock(orc_sim* s) { return s->clock; }
 int orc_sim_build_matrix(orc_sim* s, const uint32_t* ids, const uint64_t* offsets,
                          uint64_t R, double* out) {
   return build_matrix(&s->cfg, &s->g, ids, offsets, R, out);
+}
+
+int orc_sim_hitgreedy(orc_sim* s, const uint32_t* ids, const uint64_t* offsets, uint64_t R,
+                      int32_t* decision) {
+  return hitgreedy(&s->cfg, &s->g, ids, offsets, R, decision);
 }
 
 /* seed_entry — sim.hpp:252-261 */

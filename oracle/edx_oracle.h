@@ -81,6 +81,11 @@ int orc_build_matrix_snapshot(const orc_cluster_config* cfg, const uint32_t* sna
                               const uint64_t* snap_resident, uint64_t snap_count,
                               const uint32_t* ids, const uint64_t* offsets,
                               uint64_t num_samples, double* out);
+/* baseline_hitgreedy — assign.hpp:346-392 on a snapshot (owners/latest). */
+int orc_hitgreedy_snapshot(const orc_cluster_config* cfg, const uint32_t* snap_ids,
+                           const uint64_t* snap_owners, const uint64_t* snap_latest,
+                           uint64_t snap_count, const uint32_t* ids, const uint64_t* offsets,
+                           uint64_t num_samples, int32_t* decision);
 int orc_row_gap_key(uint64_t rows, uint64_t cols, const double* values, uint64_t row,
                     double* out);
 int orc_rows_by_gap(uint64_t rows, uint64_t cols, const double* values, uint64_t* order);
@@ -99,6 +104,9 @@ int orc_sim_create(const orc_cluster_config* cfg, orc_sim** out);
 void orc_sim_destroy(orc_sim* s);
 int orc_sim_build_matrix(orc_sim* s, const uint32_t* ids, const uint64_t* offsets,
                          uint64_t num_samples, double* out);
+/* baseline_hitgreedy on the simulator's live state (its snapshot). */
+int orc_sim_hitgreedy(orc_sim* s, const uint32_t* ids, const uint64_t* offsets,
+                      uint64_t num_samples, int32_t* decision);
 int orc_sim_step(orc_sim* s, const uint32_t* ids, const uint64_t* offsets,
                  uint64_t num_samples, const int32_t* decision, orc_report* rep);
 int orc_sim_seed_entry(orc_sim* s, uint32_t id, int32_t worker, int latest, int owner);

@@ -112,6 +112,9 @@ class Oracle:
         L.orc_unit_costs.argtypes = [P(ClusterConfigC), P(dbl)]
         L.orc_build_matrix_snapshot.argtypes = [P(ClusterConfigC), P(C.c_uint32), P(u64), P(u64),
                                                 P(u64), u64, P(C.c_uint32), P(u64), u64, P(dbl)]
+        L.orc_hitgreedy_snapshot.argtypes = [P(ClusterConfigC), P(C.c_uint32), P(u64), P(u64), u64,
+                                             P(C.c_uint32), P(u64), u64, P(i32)]
+        L.orc_sim_hitgreedy.argtypes = [vp, P(C.c_uint32), P(u64), u64, P(i32)]
         L.orc_row_gap_key.argtypes = [u64, u64, P(dbl), u64, P(dbl)]
         L.orc_rows_by_gap.argtypes = [u64, u64, P(dbl), P(u64)]
         L.orc_hungarian.argtypes = [u64, P(dbl), P(u64), P(dbl)]
@@ -185,6 +188,20 @@ class Oracle:
             _p(re, C.c_uint64), len(keys), _p(ids, C.c_uint32), _p(offsets, C.c_uint64), R,
             _p(out, C.c_double)))
         return out.reshape(R, cfg.n)
+
+    def hitgreedy_snapshot(self, cfg: Cfg, snap, ids, offsets):
+        """baseline_hitgreedy (assign.hpp:346-392); snap: dict id -> (owners, latest, ...)."""
+        keys = np.array(sorted(snap), np.uint32)
+        ow = np.array([snap[int(k)][0] for k in keys], np.uint64)
+        la = np.array([snap[int(k)][1] for k in keys], np.uint64)
+        ids = np.ascontiguousarray(ids, np.uint32)
+        offsets = np.ascontiguousarray(offsets, np.uint64)
+        R = len(offsets) - 1
+        dec = np.empty(max(R, 1), np.int32)
+        self._check(self.lib.orc_hitgreedy_snapshot(
+            C.byref(cfg.c()), _p(keys, C.c_uint32), _p(ow, C.c_uint64), _p(la, C.c_uint64),
+            len(keys), _p(ids, C.c_uint32), _p(offsets, C.c_uint64), R, _p(dec, C.c_int32)))
+        return dec[:R]
 
     def row_gap_key(self, mat, row):
         mat = np.ascontiguousarray(mat, np.float64)
@@ -267,6 +284,17 @@ class Sim:
                                                       _p(offsets, C.c_uint64), R,
                                                       _p(out, C.c_double)))
         return out.reshape(R, self.cfg.n)
+
+    def hitgreedy(self, ids, offsets):
+        """baseline_hitgreedy on this simulator's live state."""
+        ids = np.ascontiguousarray(ids, np.uint32)
+        offsets = np.ascontiguousarray(offsets, np.uint64)
+        R = len(offsets) - 1
+        dec = np.empty(max(R, 1), np.int32)
+        self.o._check(self.o.lib.orc_sim_hitgreedy(self.h, _p(ids, C.c_uint32),
+                                                   _p(offsets, C.c_uint64), R,
+                                                   _p(dec, C.c_int32)))
+        return dec[:R]
 
     def step(self, ids, offsets, decision):
         ids = np.ascontiguousarray(ids, np.uint32)

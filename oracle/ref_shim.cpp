@@ -203,6 +203,22 @@ int orc_hungarian(uint64_t k, const double* values, uint64_t* col_of_row, double
   });
 }
 
+int orc_hitgreedy_snapshot(const orc_cluster_config* c, const uint32_t* snap_ids,
+                           const uint64_t* owners, const uint64_t* latest, uint64_t count,
+                           const uint32_t* ids, const uint64_t* offsets, uint64_t R,
+                           int32_t* decision) {
+  return guarded([&] {
+    Snapshot snap;
+    for (uint64_t s = 0; s < count; ++s) {
+      EmbeddingState& st = snap.states[snap_ids[s]];
+      st.owners = owners[s];
+      st.latest = latest[s];
+    }
+    const DispatchDecision d = baseline_hitgreedy(to_samples(ids, offsets, R), snap, to_cfg(c));
+    for (std::size_t i = 0; i < d.worker_of_sample.size(); ++i) decision[i] = d.worker_of_sample[i];
+  });
+}
+
 int orc_greedy_dispatch(uint64_t rows, uint64_t cols, const double* values,
                         const uint64_t* order, uint64_t n_order, const int32_t* capacity,
                         uint64_t* out_rows, int32_t* out_workers) {
@@ -249,6 +265,15 @@ int orc_sim_build_matrix(orc_sim* s, const uint32_t* ids, const uint64_t* offset
     const Snapshot snap = s->state.snapshot();
     const CostMatrix m = build_matrix(to_samples(ids, offsets, R), snap, s->cfg);
     std::memcpy(out, m.values.data(), m.values.size() * sizeof(double));
+  });
+}
+
+int orc_sim_hitgreedy(orc_sim* s, const uint32_t* ids, const uint64_t* offsets, uint64_t R,
+                      int32_t* decision) {
+  return guarded([&] {
+    const Snapshot snap = s->state.snapshot();
+    const DispatchDecision d = baseline_hitgreedy(to_samples(ids, offsets, R), snap, s->cfg);
+    for (std::size_t i = 0; i < d.worker_of_sample.size(); ++i) decision[i] = d.worker_of_sample[i];
   });
 }
 

@@ -353,6 +353,24 @@ def ecomix(matrix, cfg: ClusterConfig) -> DispatchDecision:
     return DispatchDecision(dec)
 
 
+def baseline_hitgreedy(samples, snap, cfg: ClusterConfig) -> DispatchDecision:
+    """baseline_hitgreedy — assign.hpp:346-392 (relevance-score baseline): each
+    sample scores a worker by its ids' latest copies there; strongest affinity
+    commits first; ties to the least-loaded, then lowest-indexed worker.
+    `snap` is a Snapshot or a SimState snapshot view (the engine's live state)."""
+    if isinstance(snap, _EngineSnapshot):
+        return snap.engine._hitgreedy_view(samples)
+    ids, offs = to_csr(samples)
+    R = len(offs) - 1
+    keys, ow, la, _ = _snapshot_arrays(snap or {})
+    dec = np.empty(max(R, 1), np.int32)
+    c = cfg._c()
+    check(lib().edx_hitgreedy(C.byref(c), _ptr(keys, C.c_uint32), _ptr(ow, C.c_uint64),
+                              _ptr(la, C.c_uint64), len(keys), _ptr(ids, C.c_uint32),
+                              _ptr(offs, C.c_uint64), R, _ptr(dec, C.c_int32)))
+    return DispatchDecision(dec[:R])
+
+
 def decision_cost(matrix, decision) -> float:
     """decision_cost — assign.hpp:288-298."""
     v = _vals(matrix)
@@ -453,6 +471,10 @@ class SimState:
         check(lib().edx_engine_build(self._h, _ptr(out, C.c_double)))
         return out
 
+    def _hitgreedy_view(self, samples) -> DispatchDecision:
+        self.load(samples)
+        return DispatchDecision(self.dispatch_hitgreedy())
+
     def _dispatch_view(self, alpha) -> DispatchDecision:
         R = self.cfg.samples_per_iteration()
         dec = np.empty(R, np.int32)
@@ -466,6 +488,13 @@ class SimState:
         check(lib().edx_engine_dispatch(self._h, float(alpha), _ptr(dec, C.c_int32),
                                         C.byref(exp) if want_expected else None))
         return dec, (exp.value if want_expected else None)
+
+    def dispatch_hitgreedy(self, want_decision=True):
+        """baseline_hitgreedy (assign.hpp:346-392) on the loaded batch and the live
+        state; the decision stays on device for step()."""
+        dec = np.empty(self.cfg.samples_per_iteration(), np.int32) if want_decision else None
+        check(lib().edx_engine_dispatch_hitgreedy(self._h, _ptr(dec, C.c_int32)))
+        return dec
 
     def step(self, samples=None, decision=None) -> IterationReport:
         """SimState::step(samples, decision) — sim.hpp:87-218.  samples None =

@@ -78,6 +78,7 @@ def _sigs():
         ("edx_engine_load_batch", cint, [vp, vp, vp, u64, cint]),
         ("edx_engine_build", cint, [vp, dblp]),
         ("edx_engine_dispatch", cint, [vp, dbl, i32p, dblp]),
+        ("edx_engine_dispatch_hitgreedy", cint, [vp, i32p]),
         ("edx_engine_step", cint, [vp, i32p, P(ReportC)]),
         ("edx_engine_iterate", cint, [vp, vp, vp, u64, cint, i32p, dblp, P(ReportC)]),
         ("edx_engine_stream", cint, [vp, P(vp)]),
@@ -94,6 +95,7 @@ def _sigs():
         ("edx_engine_phase_times", cint, [vp, dblp, u64p, cint]),
         ("edx_solver_stats", cint, [vp, u64p]),
         ("edx_build_matrix", cint, [cfgp, u32p, u64p, u64p, u64p, u64, u32p, u64p, u64, dblp]),
+        ("edx_hitgreedy", cint, [cfgp, u32p, u64p, u64p, u64, u32p, u64p, u64, i32p]),
         ("edx_expected_costs", cint, [cfgp, u32p, u64p, u64p, u64, u32p, u64p, u64, dblp]),
         ("edx_row_gap_key", cint, [u64, u64, dblp, u64, dblp]),
         ("edx_rows_by_gap", cint, [u64, u64, dblp, u64p]),

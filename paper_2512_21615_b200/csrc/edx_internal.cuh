@@ -146,4 +146,14 @@ void run_ecomix(DispatchScratch& sc, const double* matrix, uint64_t rows, int n,
                 double alpha, bool gap_ready, int32_t* decision, int* flags, cudaStream_t s,
                 int device, const PhaseEvents* ev, int* launches);
 
+// hitgreedy.cu — K8 baseline_hitgreedy (assign.hpp:346-392)
+struct HitScratch {
+  DevBuf<int32_t> scores;
+  DevBuf<uint32_t> keys, keys_sorted, index, index_sorted;
+  DevBuf<uint8_t> temp;
+};
+void launch_hitgreedy(HitScratch& sc, const uint32_t* ids, const uint64_t* offsets, uint64_t rows,
+                      int n, int m, const ulonglong2* ol, uint64_t id_space, int32_t* decision,
+                      int* flags, cudaStream_t s);
+
 }  // namespace edx

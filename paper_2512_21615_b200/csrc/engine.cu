@@ -234,6 +234,7 @@ struct DefaultCtx {
   int device = -1;
   cudaStream_t stream = nullptr;
   edx::DispatchScratch disp;
+  edx::HitScratch hit;
   DevBuf<double> values;
   DevBuf<uint32_t> ids, u32a, u32b;
   DevBuf<uint64_t> offsets, u64a, u64b;
@@ -623,6 +624,27 @@ int edx_engine_dispatch(edx_engine* e, double alpha, int32_t* decision_out,
   });
 }
 
+int edx_engine_dispatch_hitgreedy(edx_engine* e, int32_t* decision_out) {
+  return guard([&] {
+    EDX_CUDA(cudaSetDevice(e->device));
+    if (e->rows == 0) edx::invalid("load a batch before dispatching");
+    if (e->rows != static_cast<uint64_t>(e->n) * static_cast<uint64_t>(e->m))
+      edx::invalid("sample count must be m*n");
+    if (e->m >= (1 << 26)) edx::invalid("at most 2^26 samples per worker");
+    e->decision.ensure(e->rows + 2);
+    // every rank holds the same replica, so every rank decides identically
+    edx::launch_hitgreedy(e->hit, e->cur_ids, e->cur_offsets, e->rows, e->n, e->m, e->ol.p,
+                          e->id_space, e->decision.p, e->flags.p, e->stream);
+    e->launches += 3;
+    e->dispatched = true;
+    if (decision_out) {
+      EDX_CUDA(cudaMemcpyAsync(decision_out, e->decision.p, e->rows * sizeof(int32_t),
+                               cudaMemcpyDeviceToHost, e->stream));
+      engine_sync_check(e);
+    }
+  });
+}
+
 int edx_engine_step(edx_engine* e, const int32_t* decision, edx_report* rep) {
   return guard([&] {
     EDX_CUDA(cudaSetDevice(e->device));
@@ -912,6 +934,51 @@ int edx_build_matrix(const edx_cluster_config* cfg, const uint32_t* snap_ids,
     if (R != want) edx::invalid("expected " + std::to_string(want) + " samples, got " + std::to_string(R));
     (void)snap_resident;  // residency never enters the cost (cost.hpp:81-100)
     stateless_build(cfg, snap_ids, snap_owners, snap_latest, snap_count, ids, offsets, R, out);
+  });
+}
+
+int edx_hitgreedy(const edx_cluster_config* cfg, const uint32_t* snap_ids,
+                  const uint64_t* snap_owners, const uint64_t* snap_latest, uint64_t snap_count,
+                  const uint32_t* ids, const uint64_t* offsets, uint64_t R, int32_t* decision) {
+  return guard([&] {
+    if (!cfg || cfg->n < 1 || cfg->n > 64) edx::invalid(cfg && cfg->n > 64 ? "at most 64 workers supported" : "worker count must be >= 1");
+    if (R != static_cast<uint64_t>(cfg->n) * static_cast<uint64_t>(cfg->m))
+      edx::invalid("sample count must be m*n");
+    if (cfg->m >= (1 << 26)) edx::invalid("at most 2^26 samples per worker");
+    auto& c = dctx();
+    std::lock_guard<std::mutex> lk(c.mu);
+    c.init();
+    const uint64_t base = offsets[0], total = offsets[R] - base;
+    uint64_t max_id = 0;
+    for (uint64_t s = 0; s < snap_count; ++s) max_id = std::max<uint64_t>(max_id, snap_ids[s]);
+    for (uint64_t t = 0; t < total; ++t) max_id = std::max<uint64_t>(max_id, ids[base + t]);
+    const uint64_t space = max_id + 1;
+    if (space > (1ULL << 28)) edx::invalid("ids too large for the stateless dense snapshot table (< 2^28)");
+    std::vector<uint64_t> offs(offsets, offsets + R + 1);
+    for (auto& o : offs) o -= base;
+    c.ol.ensure(space);
+    c.ids.ensure(total);
+    c.offsets.ensure(R + 1);
+    c.i32a.ensure(R);
+    c.reset_flags();
+    EDX_CUDA(cudaMemsetAsync(c.ol.p, 0, space * sizeof(ulonglong2), c.stream));
+    if (total) EDX_CUDA(cudaMemcpyAsync(c.ids.p, ids + base, total * 4, cudaMemcpyHostToDevice, c.stream));
+    EDX_CUDA(cudaMemcpyAsync(c.offsets.p, offs.data(), (R + 1) * 8, cudaMemcpyHostToDevice, c.stream));
+    if (snap_count) {
+      c.u32a.ensure(snap_count);
+      c.snapA.ensure(snap_count);
+      c.snapB.ensure(snap_count);
+      EDX_CUDA(cudaMemcpyAsync(c.u32a.p, snap_ids, snap_count * 4, cudaMemcpyHostToDevice, c.stream));
+      EDX_CUDA(cudaMemcpyAsync(c.snapA.p, snap_owners, snap_count * 8, cudaMemcpyHostToDevice, c.stream));
+      EDX_CUDA(cudaMemcpyAsync(c.snapB.p, snap_latest, snap_count * 8, cudaMemcpyHostToDevice, c.stream));
+      k_import<<<grid_for(snap_count), kT, 0, c.stream>>>(c.u32a.p, c.snapA.p, c.snapB.p, nullptr,
+                                                         snap_count, space, c.ol.p, nullptr, c.flags.p);
+      EDX_LAUNCHED();
+    }
+    edx::launch_hitgreedy(c.hit, c.ids.p, c.offsets.p, R, cfg->n, cfg->m, c.ol.p, space, c.i32a.p,
+                          c.flags.p, c.stream);
+    EDX_CUDA(cudaMemcpyAsync(decision, c.i32a.p, R * 4, cudaMemcpyDeviceToHost, c.stream));
+    c.sync_and_check();
   });
 }
 

@@ -87,6 +87,7 @@ struct edx_engine {
   edx::DevBuf<int32_t> decision;
   edx::DevBuf<double> expected;
   edx::DispatchScratch disp;
+  edx::HitScratch hit;
   bool built = false, gap_ready = false, dispatched = false;
 
   edx::DevBuf<int> flags;

@@ -117,6 +117,59 @@ static void engine_vs_oracle(double alpha) {
   EXPECT(iter == 30, "iterations");
 }
 
+// baseline_hitgreedy (assign.hpp:346-392) on the engine's live snapshot, then
+// the step, against the oracle simulator driven the same way; and run() with
+// the "hitgreedy" mechanism (dispatch_with, sim.hpp:390-391).
+static void hitgreedy_vs_oracle() {
+  ClusterConfig cfg;
+  cfg.n = 8;
+  cfg.m = 16;
+  cfg.cache_capacity = 120;
+  cfg.bandwidths_bps = {5e9, 5e9, 5e9, 5e9, 5e8, 5e8, 5e8, 5e8};
+  WorkloadSpec spec;
+  spec.total_embeddings = 400;
+  spec.sample_len = 6;
+  spec.iterations = 30;
+  spec.seed = 7;
+  ZipfStream stream(spec, cfg);
+  SimState engine(cfg, EngineOptions{0, 400, 8 * 16 * 6});
+  orc_cluster_config oc{cfg.n, cfg.m, cfg.bandwidths_bps.data(), cfg.n, 0, cfg.d_tran_bytes,
+                        cfg.cache_capacity, 0.0};
+  orc_sim* oracle = nullptr;
+  orc_sim_create(&oc, &oracle);
+  std::vector<EmbeddingSample> samples;
+  int iter = 0;
+  while (stream.next_iteration(samples)) {
+    const DispatchDecision decision = baseline_hitgreedy(samples, engine.snapshot(), cfg);
+    const IterationReport rep = engine.step(samples, decision);
+    std::vector<uint32_t> ids;
+    std::vector<uint64_t> offs{0};
+    for (auto& s : samples) {
+      ids.insert(ids.end(), s.ids.begin(), s.ids.end());
+      offs.push_back(ids.size());
+    }
+    std::vector<int32_t> od(samples.size());
+    orc_sim_hitgreedy(oracle, ids.data(), offs.data(), samples.size(), od.data());
+    bool same = true;
+    for (std::size_t i = 0; i < od.size(); ++i) same &= od[i] == decision.worker_of_sample[i];
+    EXPECT(same, "hitgreedy decision iter %d", iter);
+    std::vector<uint64_t> mp(8), up(8), ep(8);
+    std::vector<double> cw(8);
+    orc_report orep{0, 0, 0, 0, 0, 0, 0.0, mp.data(), up.data(), ep.data(), cw.data()};
+    orc_sim_step(oracle, ids.data(), offs.data(), samples.size(), od.data(), &orep);
+    EXPECT(rep.cost_s == orep.cost_s && rep.hits == orep.hits, "hitgreedy cost/hits iter %d", iter);
+    ++iter;
+  }
+  orc_sim_destroy(oracle);
+  EXPECT(iter == 30, "hitgreedy iterations");
+  ZipfStream again(spec, cfg);
+  RunOptions opt;
+  opt.warmup = 0;
+  const RunResult r = run(again, Mechanism::parse("hitgreedy"), cfg, opt, EngineOptions{0, 400, 8 * 16 * 6});
+  EXPECT(r.summary.mechanism == "hitgreedy" && !r.summary.has_expected && r.reports.size() == 30,
+         "run(hitgreedy) bookkeeping");
+}
+
 static void run_loop() {
   ClusterConfig cfg;
   cfg.n = 2;
@@ -141,6 +194,7 @@ int main() {
   engine_vs_oracle(0.5);
   engine_vs_oracle(1.0);
   run_loop();
+  hitgreedy_vs_oracle();
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;
 }

@@ -156,3 +156,26 @@ def test_iterate_equals_stepwise(gpu, oracle, pyoracle):
         assert rep.as_dict() == wrep
         assert rep.expected_cost_s == wexp
     assert not canon_equal(eng.canonical_state(), sim.canonical_state())
+
+
+@pytest.mark.parametrize("name,iters", [("P2", 50), ("P8", 40), ("C1", 15), ("C2", 10)])
+def test_engine_hitgreedy_trajectory(gpu, oracle, pyoracle, name, iters):
+    """run() with the hit-greedy mechanism: decisions on the live device state,
+    then the step, equal to the reference simulator driven the same way."""
+    edx = gpu
+    p = CONFIGS[name]
+    n, m, L = p["n"], p["m"], p["L"]
+    R = n * m
+    c = edx.ClusterConfig(n=n, m=m, bandwidths_bps=p["bw"], d_tran_bytes=2048,
+                          cache_capacity=p["cap"], alpha=0.0)
+    eng = edx.SimState(c, id_space=p["V"], max_batch_ids=R * L)
+    sim = oracle.sim(pyoracle.Cfg(n, m, p["bw"], cap=p["cap"], alpha=0.0))
+    offs = offsets_for(R, L)
+    for it, ids in enumerate(oracle.zipf_batches(p["V"], L, 1.05, iters, 5, R)):
+        want_d = sim.hitgreedy(ids, offs)
+        eng.load((ids, offs))
+        got_d = eng.dispatch_hitgreedy()
+        assert (got_d == want_d).all(), f"iter {it}: decision differs"
+        assert eng.step().as_dict() == sim.step(ids, offs, want_d), f"iter {it}: report"
+    msg = canon_equal(eng.canonical_state(), sim.canonical_state())
+    assert not msg, msg

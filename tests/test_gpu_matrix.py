@@ -306,3 +306,60 @@ def test_ecomix_shape_error(gpu):
     edx = gpu
     with pytest.raises(edx.InvalidArgument, match="matrix shape does not match cluster config"):
         edx.ecomix(np.zeros((3, 2)), cfg(edx, 2, 2, [1e9, 1e9]))
+
+
+# ------------------------------------------------- baseline_hitgreedy (§8f)
+def test_hitgreedy_cold_is_roundrobin_like(gpu, pyoracle):
+    """Cold caches: every score is 0, so ties fall to the least-loaded then the
+    lowest-indexed worker (assign.hpp:341-344)."""
+    edx = gpu
+    c = cfg(edx, 3, 2, [5e9] * 3)
+    d = edx.baseline_hitgreedy([[1], [2], [3], [4], [5], [6]], edx.Snapshot(), c)
+    assert list(d.worker_of_sample) == [0, 1, 2, 0, 1, 2]
+
+
+def test_hitgreedy_shape_error(gpu):
+    edx = gpu
+    with pytest.raises(edx.InvalidArgument, match="sample count must be m\\*n"):
+        edx.baseline_hitgreedy([[1]], edx.Snapshot(), cfg(edx, 2, 2, [5e9, 5e9]))
+
+
+@pytest.mark.parametrize("n,m", [(1, 5), (2, 3), (3, 7), (8, 16), (13, 5), (32, 9), (40, 4), (64, 3)])
+def test_hitgreedy_matches_reference(gpu, oracle, pyoracle, n, m):
+    """Random snapshots with heavy score ties and capacity exhaustion: decisions equal."""
+    edx = gpu
+    rng = np.random.default_rng(3000 + n * 100 + m)
+    c = cfg(edx, n, m, [5e9] * n)
+    oc = pyoracle.Cfg(n, m, [5e9] * n)
+    snap, osnap = edx.Snapshot(), {}
+    full = (1 << n) - 1 if n < 64 else (1 << 64) - 1
+    for id_ in range(60):
+        lat = int(rng.integers(0, 1 << min(n, 62))) & full
+        own = lat if rng.integers(0, 2) else 0
+        snap[id_] = edx.EmbeddingState(own, lat, lat)
+        osnap[id_] = (own, lat, lat)
+    R = n * m
+    lens = rng.integers(0, 12, size=R)
+    samples = [list(rng.choice(70, size=l, replace=False)) for l in lens]
+    got = edx.baseline_hitgreedy(samples, snap, c).worker_of_sample
+    ids, offs = edx.to_csr(samples)
+    want = oracle.hitgreedy_snapshot(oc, osnap, ids, offs)
+    assert (np.asarray(got) == want).all()
+
+
+def test_hitgreedy_many_rows(gpu, oracle, pyoracle):
+    """More rows than one gathered batch of the assignment kernel (256)."""
+    edx = gpu
+    n, m = 8, 300
+    rng = np.random.default_rng(77)
+    c = cfg(edx, n, m, [5e9] * n)
+    oc = pyoracle.Cfg(n, m, [5e9] * n)
+    snap, osnap = edx.Snapshot(), {}
+    for id_ in range(500):
+        lat = int(rng.integers(0, 1 << n))
+        snap[id_] = edx.EmbeddingState(0, lat, lat)
+        osnap[id_] = (0, lat, lat)
+    samples = [list(rng.choice(600, size=int(rng.integers(1, 20)), replace=False)) for _ in range(n * m)]
+    got = edx.baseline_hitgreedy(samples, snap, c).worker_of_sample
+    ids, offs = edx.to_csr(samples)
+    assert (np.asarray(got) == oracle.hitgreedy_snapshot(oc, osnap, ids, offs)).all()

@@ -130,3 +130,19 @@ def test_oracle_solver_equals_reference(port, ref):
         c2, t2 = ref.hungarian(sq)
         assert (c1 == c2).all() and t1 == t2
     assert (port.bench_matrix(16) == ref.bench_matrix(16)).all()
+
+
+@pytest.mark.parametrize("name", ["P2", "P3", "P8"])
+def test_oracle_hitgreedy_equals_reference(port, ref, pyoracle, name):
+    """baseline_hitgreedy restatement vs the compiled reference, driving both
+    simulators with it (assign.hpp:346-392, sim.hpp:390-391)."""
+    p = CONFIGS[name]
+    n, m, L = p["n"], p["m"], p["L"]
+    cfg = pyoracle.Cfg(n, m, p["bw"], cap=p["cap"], alpha=0.0)
+    a, b = port.sim(cfg), ref.sim(cfg)
+    offs = offsets_for(n * m, L)
+    for ids in port.zipf_batches(p["V"], L, 1.05, 40, 11, n * m):
+        da, db = a.hitgreedy(ids, offs), b.hitgreedy(ids, offs)
+        assert (da == db).all()
+        assert a.step(ids, offs, da) == b.step(ids, offs, db)
+    assert not canon_equal(a.canonical_state(), b.canonical_state())
