@@ -43,6 +43,11 @@ WORKLOADS = {
                desc="C3: Criteo-shaped, 10M ids, batch 8192, 16 heterogeneous workers, alpha=0.125"),
     "C4": dict(n=32, m=512, L=100, V=10_000_000, cap=800_000, bw=HET(32), alpha=0.0625, prefill=2,
                desc="C4: Avazu-shaped, 100 ids/sample, batch 16384, 32 workers, alpha=1/16"),
+    # BASELINE configs[4], the scaling sweep (batch 4K-64K x workers 8-64; n=128 has no
+    # oracle, the reference rejects n > 64): default = the corner, override with
+    # --batch / --workers.
+    "C5": dict(n=64, m=1024, L=26, V=10_000_000, cap=800_000, bw=HET(64), alpha=0.0, prefill=1,
+               desc="C5: scaling sweep, 26 Zipf ids, 10M-id vocabulary, greedy (alpha 0)"),
 }
 METRIC = "samples dispatched/sec (cost matrix + hybrid decision + cache update)"
 ZIPF_S, SEED = 1.05, 42
@@ -60,6 +65,8 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=10, help="timed iterations of cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-flush", action="store_true", help="do not flush L2 between iterations")
+    ap.add_argument("--batch", type=int, default=None, help="C5 sweep: samples per iteration")
+    ap.add_argument("--workers", type=int, default=None, help="C5 sweep: workers (<= 64)")
     return ap.parse_args()
 
 
@@ -69,7 +76,19 @@ def workload(args):
         w["alpha"] = args.alpha
     if args.prefill is not None:
         w["prefill"] = args.prefill
+    if args.workers is not None or args.batch is not None:
+        if args.config != "C5":
+            raise SystemExit("--batch/--workers apply to the C5 sweep only")
+        n = args.workers or w["n"]
+        if not 1 <= n <= 64:
+            raise SystemExit("--workers must lie in [1, 64] (the reference rejects n > 64)")
+        R = args.batch or w["n"] * w["m"]
+        if R % n:
+            raise SystemExit("--batch must be a multiple of --workers")
+        w.update(n=n, m=R // n, bw=HET(n))
     w["R"] = w["n"] * w["m"]
+    if args.config == "C5":
+        w["desc"] = f"{w['desc']}: batch {w['R']}, {w['n']} workers"
     return w
 
 

@@ -179,3 +179,30 @@ def test_engine_hitgreedy_trajectory(gpu, oracle, pyoracle, name, iters):
         assert eng.step().as_dict() == sim.step(ids, offs, want_d), f"iter {it}: report"
     msg = canon_equal(eng.canonical_state(), sim.canonical_state())
     assert not msg, msg
+
+
+def test_engine_64_workers(gpu, oracle, pyoracle):
+    """n = 64 (the widest the reference accepts; the C5 sweep corner's worker
+    count): full 64-bit masks through build, EcoMix, step and state."""
+    edx = gpu
+    n, m, L, V, cap = 64, 4, 5, 3000, 40
+    bw = [5e9] * 32 + [5e8] * 32
+    R = n * m
+    for alpha in (0.0, 0.5):
+        c = edx.ClusterConfig(n=n, m=m, bandwidths_bps=bw, d_tran_bytes=2048,
+                              cache_capacity=cap, alpha=alpha)
+        eng = edx.SimState(c, id_space=V, max_batch_ids=R * L)
+        sim = oracle.sim(pyoracle.Cfg(n, m, bw, cap=cap, alpha=alpha))
+        offs = offsets_for(R, L)
+        for it, ids in enumerate(oracle.zipf_batches(V, L, 1.05, 12, 3, R)):
+            want_m = sim.build_matrix(ids, offs)
+            eng.load((ids, offs))
+            got_m = np.empty((R, n))
+            eng.build(got_m)
+            assert got_m.tobytes() == want_m.tobytes(), f"alpha {alpha} iter {it}: matrix"
+            want_d = oracle.ecomix(pyoracle.Cfg(n, m, bw, alpha=alpha), want_m)
+            got_d, _ = eng.dispatch()
+            assert (got_d == want_d).all(), f"alpha {alpha} iter {it}: decision"
+            assert eng.step().as_dict() == sim.step(ids, offs, want_d), f"alpha {alpha} iter {it}"
+        msg = canon_equal(eng.canonical_state(), sim.canonical_state())
+        assert not msg, msg

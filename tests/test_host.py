@@ -146,3 +146,17 @@ def test_oracle_hitgreedy_equals_reference(port, ref, pyoracle, name):
         assert (da == db).all()
         assert a.step(ids, offs, da) == b.step(ids, offs, db)
     assert not canon_equal(a.canonical_state(), b.canonical_state())
+
+
+@pytest.mark.parametrize("V,L,R,iters", [(10_000_000, 26, 2048, 3), (10_000_000, 100, 1024, 2),
+                                         (1000, 30, 64, 40)])
+def test_zipf_stream_large_and_reset(edx, oracle, V, L, R, iters):
+    """Guide-table mapping, chunked draws, hash dedup and the producer thread
+    reproduce the reference's stream at the 10M-id vocabulary and with heavy
+    rejection (L = 30 of 1,000 ids); reset() replays it."""
+    z = edx.ZipfStream(V, L, 1.05, iters, 7, R)
+    want = list(oracle.zipf_batches(V, L, 1.05, iters, 7, R))
+    got = list(z)
+    assert len(got) == iters and all((a == b).all() for a, b in zip(got, want))
+    z.reset()
+    assert (next(iter(z)) == want[0]).all()
