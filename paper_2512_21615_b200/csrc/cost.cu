@@ -15,6 +15,8 @@
 // threads of one row hit the same address (a broadcast), so each id costs
 // one L1/L2 transaction per row.  Loads are batched 4 ids ahead of the add
 // chain to keep memory-level parallelism despite the serial adds.
+#include <type_traits>
+
 #include "edx_internal.cuh"
 
 namespace edx {
@@ -125,6 +127,9 @@ __global__ void __launch_bounds__(kBlockCells)
 // The row gap (two smallest of the row, with multiplicity) is a shuffle
 // reduction, order-independent, then one __dsub_rn.
 constexpr int kWarpRowsThreads = 128;
+
+__device__ __forceinline__ int popc_mask(unsigned x) { return __popc(x); }
+__device__ __forceinline__ int popc_mask(unsigned long long x) { return __popcll(x); }
 constexpr int kIdsPerLane = 4;
 
 template <int NP>
@@ -356,6 +361,176 @@ __global__ void __launch_bounds__(kWarpRowsThreads)
   }
 }
 
+// K1 for 32 < n <= 64 (NP = 64): one row per warp, two cells per lane
+// (workers j and j + 32: two independent chains over the same lists).  A group of G = min(NP, 32) lanes
+// loads G consecutive ids of its row (one per lane) and their masks; a ballot
+// then drops every id whose latest copy is on all n workers (no cell adds
+// anything: at steady state the hot ids -- 43% of occurrences at C4) and the
+// group walks the remaining ids in row order.  An id without owners costs
+// each non-latest cell one pull and needs no list; otherwise the group
+// expands the id's owner-cost list into shared memory (owner o's u_o at
+// position popc(owners below o), -0.0 at every other position), one
+// __syncwarp, and the chains run over it in fully unrolled blocks of 8
+// entries (one 16-byte broadcast load per 2 adds).  x + (-0.0) == x for every
+// value these chains produce, so padding and the lanes holding the latest
+// copy are exact no-ops: every cell's add sequence is the reference's.
+template <int NP>
+__global__ void __launch_bounds__(kWarpRowsThreads)
+    k_cost_build_wide64(const uint32_t* __restrict__ ids, const uint64_t* __restrict__ offsets,
+                      uint64_t rows, int n, const ulonglong2* __restrict__ ol, uint64_t id_space,
+                      const double* __restrict__ ucost, double* __restrict__ matrix,
+                      uint64_t* __restrict__ gap_keys, uint32_t* __restrict__ row_index,
+                      int* __restrict__ flags) {
+  constexpr int G = NP < 32 ? NP : 32;  // lanes per row
+  constexpr int RPW = 32 / G;           // rows per warp
+  constexpr int NC = NP / G;            // cells per lane (1 or 2)
+  constexpr int NW = kWarpRowsThreads / 32;
+  using M = typename std::conditional<(NP > 32), unsigned long long, unsigned>::type;
+  // [warp][buffer][RPW groups x NP list entries]
+  __shared__ __align__(16) double lists[NW][2][RPW * NP];
+  __shared__ __align__(16) double zeros[NP];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x < NP) zeros[threadIdx.x] = -0.0;
+  if constexpr (NP > 32) {
+    if (threadIdx.x < NP - 32) zeros[32 + threadIdx.x] = -0.0;
+  }
+  __syncthreads();
+  const int g = lane / G, jl = lane - g * G;
+  const uint64_t i = (static_cast<uint64_t>(blockIdx.x) * NW + warp) * RPW + g;
+  const bool rowok = i < rows;
+  int jw[NC];
+  bool cell[NC];
+  double uj[NC], c[NC];
+#pragma unroll
+  for (int h = 0; h < NC; ++h) {
+    jw[h] = jl + 32 * h;
+    cell[h] = rowok && jw[h] < n;
+    uj[h] = jw[h] < n ? ucost[jw[h]] : 0.0;
+    c[h] = 0.0;
+  }
+  const M full = n >= static_cast<int>(8 * sizeof(M)) ? ~M(0) : ((M(1) << n) - 1);
+  uint64_t beg = 0, end = 0;
+  if (rowok) {
+    beg = offsets[i];
+    end = offsets[i + 1];
+  }
+  const int len = static_cast<int>(end - beg);
+  const int maxlen = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(len));
+  double* const mylist = &lists[warp][0][g * NP];
+  const unsigned gmask = G == 32 ? 0xffffffffu : ((1u << G) - 1u);
+  bool bad = false;
+  int par = 0;
+  // software pipeline: ids two batches ahead, masks one batch ahead
+  auto load_id = [&](int t0) -> uint32_t {
+    const int idx = t0 + jl;
+    return idx < len ? __ldg(ids + beg + idx) : 0xffffffffu;
+  };
+  auto load_masks = [&](int t0, uint32_t id, M& own, M& lat) {
+    own = 0;
+    lat = ~M(0);  // past the row's end: every worker "holds" it, nobody adds
+    if (t0 + jl < len) {
+      if (id < id_space) {
+        const ulonglong2 m = __ldg(ol + id);
+        own = static_cast<M>(m.x);
+        lat = static_cast<M>(m.y);
+      } else {
+        bad = true;
+      }
+    }
+  };
+  uint32_t id_next = load_id(G);
+  M own_n, lat_n;
+  load_masks(0, load_id(0), own_n, lat_n);
+  for (int t0 = 0; t0 < maxlen; t0 += G) {
+    const M own = own_n, lat = lat_n;
+    if (t0 + G < maxlen) {
+      const uint32_t id1 = id_next;
+      id_next = load_id(t0 + 2 * G);
+      load_masks(t0 + G, id1, own_n, lat_n);
+    }
+    // ids some worker of its row lacks, slot-aligned over the warp's groups
+    unsigned todo = __ballot_sync(0xffffffffu, (lat & full) != full);
+    if constexpr (RPW == 2) todo = (todo | (todo >> 16)) & gmask;
+    while (todo) {
+      const int s = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const M O = __shfl_sync(0xffffffffu, own, s, G);
+      const M Lm = __shfl_sync(0xffffffffu, lat, s, G);
+      bool act[NC];
+#pragma unroll
+      for (int h = 0; h < NC; ++h) act[h] = cell[h] && !((Lm >> jw[h]) & 1u);
+      if (!__any_sync(0xffffffffu, O != 0)) {  // no owners: one pull per non-latest cell
+#pragma unroll
+        for (int h = 0; h < NC; ++h) c[h] = __dadd_rn(c[h], act[h] ? uj[h] : -0.0);
+        continue;
+      }
+      const int p = popc_mask(O);
+      const int pmax = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(p)));
+      double* buf = mylist + par * (RPW * NP);
+      par ^= 1;
+#pragma unroll
+      for (int h = 0; h < NC; ++h) {
+        const M below_mask = (M(1) << jw[h]) - 1;
+        const bool has = (O >> jw[h]) & 1u;
+        const int below = popc_mask(O & below_mask);
+        buf[has ? below : p + (jw[h] - below)] = has ? uj[h] : -0.0;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int h = 0; h < NC; ++h) c[h] = __dadd_rn(c[h], act[h] ? uj[h] : -0.0);  // miss pull
+      const double* lp[NC];
+#pragma unroll
+      for (int h = 0; h < NC; ++h) lp[h] = act[h] ? buf : zeros;
+      // pushes, owners ascending, in blocks of 8 entries; entries past the
+      // last owner hold -0.0
+      const int nblk = (pmax + 7) >> 3;
+#pragma unroll 1
+      for (int bk = 0; bk < nblk; ++bk) {
+        double2 v2[NC][4];
+#pragma unroll
+        for (int h = 0; h < NC; ++h)
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            v2[h][q] = *reinterpret_cast<const double2*>(lp[h] + 8 * bk + 2 * q);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int h = 0; h < NC; ++h) {
+            c[h] = __dadd_rn(c[h], v2[h][q].x);
+            c[h] = __dadd_rn(c[h], v2[h][q].y);
+          }
+      }
+    }
+  }
+  if (bad) atomicOr(flags + kFlagIdOutOfRange, 1);
+#pragma unroll
+  for (int h = 0; h < NC; ++h)
+    if (cell[h]) matrix[i * n + jw[h]] = c[h];
+  if (gap_keys == nullptr) return;
+  // two smallest of the row with multiplicity (row_gap_key, cost.hpp:130-146)
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  double s1 = cell[0] ? c[0] : inf, s2 = inf;
+  if constexpr (NC == 2) {
+    const double b = cell[1] ? c[1] : inf;
+    const double lo = s1 < b ? s1 : b, hi = s1 < b ? b : s1;
+    s1 = lo;
+    s2 = hi;
+  }
+#pragma unroll
+  for (int off = G / 2; off > 0; off >>= 1) {
+    const double b1 = __shfl_xor_sync(0xffffffffu, s1, off, G);
+    const double b2 = __shfl_xor_sync(0xffffffffu, s2, off, G);
+    const double lo = s1 < b1 ? s1 : b1, hi = s1 < b1 ? b1 : s1;
+    const double m2 = s2 < b2 ? s2 : b2;
+    s1 = lo;
+    s2 = hi < m2 ? hi : m2;
+  }
+  if (rowok && jl == 0) {
+    gap_keys[i] = gap_sort_key(__dsub_rn(s2, s1));
+    row_index[i] = static_cast<uint32_t>(i);
+  }
+}
+
 __global__ void k_gap_keys(const double* __restrict__ matrix, uint64_t rows, int n,
                            uint64_t* __restrict__ gap_keys, uint32_t* __restrict__ row_index) {
   const uint64_t r = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
@@ -371,9 +546,9 @@ void launch_cost_build(const uint32_t* ids, const uint64_t* offsets, uint64_t ro
                        double* matrix, uint64_t* gap_keys, uint32_t* row_index, int* flags,
                        cudaStream_t s) {
   if (rows == 0) return;
-  if (n >= 2 && n <= 32) {
-    const int np = n <= 2 ? 2 : n <= 4 ? 4 : n <= 8 ? 8 : n <= 16 ? 16 : 32;
-    const uint64_t rows_per_block = static_cast<uint64_t>(kWarpRowsThreads / 32) * (32 / np);
+  if (n >= 2) {
+    const int np = n <= 2 ? 2 : n <= 4 ? 4 : n <= 8 ? 8 : n <= 16 ? 16 : n <= 32 ? 32 : 64;
+    const uint64_t rows_per_block = static_cast<uint64_t>(kWarpRowsThreads / 32) * (np >= 32 ? 1 : 32 / np);
     const unsigned blocks = static_cast<unsigned>((rows + rows_per_block - 1) / rows_per_block);
     auto go = [&](auto kern) {
       kern<<<blocks, kWarpRowsThreads, 0, s>>>(ids, offsets, rows, n, ol, id_space, ucost, matrix,
@@ -384,11 +559,13 @@ void launch_cost_build(const uint32_t* ids, const uint64_t* offsets, uint64_t ro
       case 4: go(k_cost_build_warp<4>); break;
       case 8: go(k_cost_build_warp<8>); break;
       case 16: go(k_cost_build_wide<16>); break;
-      default: go(k_cost_build_wide<32>); break;
+      case 32: go(k_cost_build_wide<32>); break;
+      default: go(k_cost_build_wide64<64>); break;
     }
     EDX_LAUNCHED();
     return;
   }
+  // n == 1: one thread per cell
   const int rows_per_block = n >= kBlockCells ? 1 : kBlockCells / n;
   const int threads = rows_per_block * n;
   const uint64_t blocks = (rows + rows_per_block - 1) / rows_per_block;

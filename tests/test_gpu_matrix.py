@@ -137,10 +137,11 @@ def test_build_random_snapshots_bitwise(gpu, oracle, pyoracle, n):
     assert got.tobytes() == want.tobytes()
 
 
-@pytest.mark.parametrize("n", [2, 7, 8, 32])
+@pytest.mark.parametrize("n", [2, 7, 8, 12, 16, 24, 32, 33, 48, 64])
 def test_build_long_and_empty_rows_bitwise(gpu, oracle, pyoracle, n):
-    """Rows longer than one load batch of the warp-row build (4 ids per lane)
-    and empty rows: every cell bitwise, gap order through ecomix."""
+    """Rows longer than several load batches of the warp-row builds, empty
+    rows, and the id kinds the wide build treats specially (latest copy on
+    every worker: skipped; no owners: pull only): every cell bitwise."""
     edx = gpu
     rng = np.random.default_rng(2000 + n)
     bw = rng.choice([5e9, 2e9, 5e8, 1e9], size=n)
@@ -149,10 +150,22 @@ def test_build_long_and_empty_rows_bitwise(gpu, oracle, pyoracle, n):
     oc = pyoracle.Cfg(n, m, bw)
     snap, osnap = edx.Snapshot(), {}
     full = (1 << n) - 1
+
+    def bits():
+        return (int(rng.integers(0, 1 << 32)) << 32 | int(rng.integers(0, 1 << 32))) & full
+
     for id_ in range(0, 3000, 2):
-        res = int(rng.integers(1, 1 << n)) & full
-        own = res & int(rng.integers(0, 1 << n)) if rng.integers(0, 3) else 0
-        lat = own if own else res & int(rng.integers(0, 1 << n))
+        kind = rng.integers(0, 6)
+        res = bits() | 1
+        if kind == 0:  # owned by every worker: nobody adds
+            own = lat = res = full
+        elif kind == 1:  # synced on every worker, no owners
+            own, lat, res = 0, full, full
+        elif kind == 2:  # no owners, some stale or missing copies
+            own, lat = 0, res & bits()
+        else:
+            own = res & bits() if rng.integers(0, 3) else 0
+            lat = own if own else res & bits()
         snap[id_] = edx.EmbeddingState(own, lat, res)
         osnap[id_] = (own, lat, res)
     R = n * m
