@@ -352,6 +352,7 @@ __global__ void k_cand_offsets(const int32_t* __restrict__ wlist, int nw, uint32
 // device-wide sort.
 constexpr int kSelThreads = 1024, kSelItems = 12;
 constexpr uint64_t kSelCap = static_cast<uint64_t>(kSelThreads) * kSelItems;
+constexpr uint32_t kSelSmall = 4096;  // victims per worker selected + bitonic-sorted
 using SelSort = cub::BlockRadixSort<uint64_t, kSelThreads, kSelItems, uint32_t>;
 
 __global__ void __launch_bounds__(kSelThreads, 1)
@@ -442,12 +443,95 @@ __global__ void __launch_bounds__(kSelThreads, 1)
       keys[k] = key;
     }
   }
-  SelSort(temp).Sort(keys, slots, 0, W + 1);
   const uint32_t take = min(E, cnt);
+  if (take > kSelSmall) {  // many victims: sort every key
+    SelSort(temp).Sort(keys, slots, 0, W + 1);
 #pragma unroll
-  for (int k = 0; k < kSelItems; ++k) {
-    const uint32_t r = tid * kSelItems + k;  // blocked arrangement: sorted rank
-    if (r < take) cand_slot_sorted[gb + r] = slots[k];
+    for (int k = 0; k < kSelItems; ++k) {
+      const uint32_t r = tid * kSelItems + k;  // blocked arrangement: sorted rank
+      if (r < take) cand_slot_sorted[gb + r] = slots[k];
+    }
+  } else if (take > 0) {
+    // Radix select of the take-th least candidate key (8-bit digits, most
+    // significant first; keys are unique -- they end in the id), then a
+    // bitonic sort of the take keys at or below it.
+    uint32_t* hist = reinterpret_cast<uint32_t*>(smem);
+    uint64_t* sk = reinterpret_cast<uint64_t*>(smem + 256 * sizeof(uint32_t));
+    uint32_t* ss = reinterpret_cast<uint32_t*>(sk + kSelSmall);
+    __shared__ uint32_t s_bin, s_rank, s_cnt;
+    uint64_t prefix = 0;
+    uint32_t rank = take;  // 1-based rank among the keys under `prefix`
+    for (int done = 0; done < W;) {
+      const int nb = min(8, W - done), shift = W - done - nb;
+      for (int x = tid; x < 256; x += kSelThreads) hist[x] = 0;
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < kSelItems; ++k)
+        if (cf[k] && (keys[k] >> (shift + nb)) == prefix)
+          atomicAdd(&hist[(keys[k] >> shift) & ((1u << nb) - 1u)], 1u);
+      __syncthreads();
+      if (warp == 0) {
+        uint32_t h[8], sum = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          h[q] = hist[8 * lane + q];
+          sum += h[q];
+        }
+        uint32_t inc = sum;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, inc, off);
+          if (lane >= off) inc += y;
+        }
+        uint32_t run = inc - sum;
+        if (run < rank && rank <= inc) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            if (run + h[q] >= rank) {
+              s_bin = 8 * lane + q;
+              s_rank = rank - run;
+              break;
+            }
+            run += h[q];
+          }
+        }
+      }
+      __syncthreads();
+      prefix = (prefix << nb) | s_bin;
+      rank = s_rank;
+      done += nb;
+    }
+    if (tid == 0) s_cnt = 0;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kSelItems; ++k) {
+      if (cf[k] && keys[k] <= prefix) {
+        const uint32_t q = atomicAdd(&s_cnt, 1u);
+        sk[q] = keys[k];
+        ss[q] = slots[k];
+      }
+    }
+    uint32_t P = 2;
+    while (P < take) P <<= 1;
+    for (uint32_t x = take + tid; x < P; x += kSelThreads) sk[x] = ~0ULL;
+    __syncthreads();
+    for (uint32_t size = 2; size <= P; size <<= 1) {
+      for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+        for (uint32_t t = tid; t < P / 2; t += kSelThreads) {
+          const uint32_t lo = 2 * t - (t & (stride - 1)), hi = lo + stride;
+          const uint64_t a = sk[lo], b = sk[hi];
+          if ((a > b) == ((lo & size) == 0)) {
+            sk[lo] = b;
+            sk[hi] = a;
+            const uint32_t sa = ss[lo];
+            ss[lo] = ss[hi];
+            ss[hi] = sa;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    for (uint32_t r = tid; r < take; r += kSelThreads) cand_slot_sorted[gb + r] = ss[r];
   }
   if (tid == 0) {
     w[kWsCand] = cnt;
@@ -705,7 +789,9 @@ void step_init_state(edx_engine* e) {
                            e->stream));
   EDX_CUDA(cudaStreamSynchronize(e->stream));
   if (e->capacity <= kSelCap) {
-    static const size_t sel_smem = sizeof(typename SelSort::TempStorage);
+    static const size_t sel_smem =
+        std::max(sizeof(typename SelSort::TempStorage),
+                 256 * sizeof(uint32_t) + kSelSmall * (sizeof(uint64_t) + sizeof(uint32_t)));
     EDX_CUDA(cudaFuncSetAttribute(k_select_victims, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(sel_smem)));
   }

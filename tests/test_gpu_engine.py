@@ -128,6 +128,13 @@ def test_engine_eviction_pressure_p8(gpu, oracle, pyoracle, alpha):
     run_parity(gpu, oracle, pyoracle, "P8", alpha, 40, seed=99)
 
 
+@pytest.mark.parametrize("s", [0.6, 1.05])
+def test_engine_mass_eviction(gpu, oracle, pyoracle, s):
+    """Thousands of victims per worker per step (s = 0.6: > 4096, the full
+    block sort; s = 1.05: the radix-select path), caches refilled every step."""
+    run_parity(gpu, oracle, pyoracle, "PX", 0.0, 6, seed=11, s=s)
+
+
 def test_engine_c1(gpu, oracle, pyoracle):
     """C1: 4 workers, batch 1024, uniform, 10% cache, greedy only."""
     run_parity(gpu, oracle, pyoracle, "C1", 0.0, 30, check_state_every=10)
