@@ -201,6 +201,18 @@ int edx_expected_costs(const edx_cluster_config* cfg, const uint32_t* snap_ids,
                        const uint64_t* snap_owners, const uint64_t* snap_latest,
                        uint64_t snap_count, const uint32_t* ids, const uint64_t* offsets,
                        uint64_t num_samples, double* out);
+/* build_matrix / expected_cost with a SizeLookupFn (cost.hpp:64-73,81-125):
+ * sizes[t] = size_of(ids[t]) in bytes for every id position t of the batch
+ * (parallel to ids, same offsets); each add is then bytes * 8.0 / bw_j of
+ * that id instead of the uniform d_tran unit cost. */
+int edx_build_matrix_sized(const edx_cluster_config* cfg, const uint32_t* snap_ids,
+                           const uint64_t* snap_owners, const uint64_t* snap_latest,
+                           uint64_t snap_count, const uint32_t* ids, const uint64_t* offsets,
+                           uint64_t num_samples, const uint64_t* sizes, double* out);
+int edx_expected_costs_sized(const edx_cluster_config* cfg, const uint32_t* snap_ids,
+                             const uint64_t* snap_owners, const uint64_t* snap_latest,
+                             uint64_t snap_count, const uint32_t* ids, const uint64_t* offsets,
+                             uint64_t num_samples, const uint64_t* sizes, double* out);
 /* row_gap_key — cost.hpp:130-146. */
 int edx_row_gap_key(uint64_t rows, uint64_t cols, const double* values, uint64_t row,
                     double* out);

@@ -43,8 +43,9 @@ struct CostMatrix {
   double& at(std::size_t r, std::size_t c) { return values[r * cols + c]; }
 };
 
-// cost.hpp:64.  Non-uniform sizes are outside the device path:
-// passing one throws instead of silently using d_tran.
+// cost.hpp:64.  Optional per-embedding transfer size in bytes; the device
+// build evaluates it once per id position and charges bytes * 8.0 / bw_j
+// (cost.hpp:68-73) for each add.
 using SizeLookupFn = std::function<std::uint64_t(EmbeddingId)>;
 
 namespace edxc {
@@ -53,6 +54,17 @@ struct SnapArrays {
   std::vector<uint32_t> ids;
   std::vector<uint64_t> owners, latest, resident;
   explicit SnapArrays(const Snapshot& s) {
+    if (s.engine && s.states.empty()) {  // a device view: read the live state back
+      uint64_t count = 0;
+      check(edx_engine_export_global(s.engine, nullptr, nullptr, nullptr, nullptr, 0, &count));
+      ids.resize(count);
+      owners.resize(count);
+      latest.resize(count);
+      resident.resize(count);
+      check(edx_engine_export_global(s.engine, ids.data(), owners.data(), latest.data(),
+                                     resident.data(), count, &count));
+      return;
+    }
     ids.reserve(s.states.size());
     for (const auto& [id, st] : s.states) {
       ids.push_back(id);
@@ -74,8 +86,10 @@ struct Csr {
   }
 };
 
-inline void no_size_hook(const SizeLookupFn& f) {
-  if (f) throw std::invalid_argument("non-uniform embedding sizes are not supported by the device path");
+inline std::vector<uint64_t> sizes_of(const std::vector<uint32_t>& ids, const SizeLookupFn& f) {
+  std::vector<uint64_t> out(ids.size());
+  for (std::size_t t = 0; t < ids.size(); ++t) out[t] = f(ids[t]);
+  return out;
 }
 
 }  // namespace edxc
@@ -84,13 +98,19 @@ inline void no_size_hook(const SizeLookupFn& f) {
 inline double expected_cost(const EmbeddingSample& sample, WorkerId worker, const Snapshot& snap,
                             const ClusterConfig& cfg, const SizeLookupFn& size_of = nullptr) {
   if (worker < 0 || worker >= cfg.n) throw std::invalid_argument("worker id out of range");
-  edxc::no_size_hook(size_of);
   const edxc::SnapArrays a(snap);
   const uint64_t off[2] = {0, sample.ids.size()};
   std::vector<double> row(static_cast<std::size_t>(cfg.n));
   const edx_cluster_config c = edxc::to_c(cfg);
-  edxc::check(edx_expected_costs(&c, a.ids.data(), a.owners.data(), a.latest.data(), a.ids.size(),
-                                 sample.ids.data(), off, 1, row.data()));
+  if (size_of) {
+    const auto sz = edxc::sizes_of(sample.ids, size_of);
+    edxc::check(edx_expected_costs_sized(&c, a.ids.data(), a.owners.data(), a.latest.data(),
+                                         a.ids.size(), sample.ids.data(), off, 1, sz.data(),
+                                         row.data()));
+  } else {
+    edxc::check(edx_expected_costs(&c, a.ids.data(), a.owners.data(), a.latest.data(),
+                                   a.ids.size(), sample.ids.data(), off, 1, row.data()));
+  }
   return row[static_cast<std::size_t>(worker)];
 }
 
@@ -100,7 +120,6 @@ inline CostMatrix build_matrix(const std::vector<EmbeddingSample>& samples, cons
   if (samples.size() != cfg.samples_per_iteration())
     throw std::invalid_argument("expected " + std::to_string(cfg.samples_per_iteration()) +
                                 " samples, got " + std::to_string(samples.size()));
-  edxc::no_size_hook(size_of);
   CostMatrix m;
   m.rows = samples.size();
   m.cols = static_cast<std::size_t>(cfg.n);
@@ -108,13 +127,20 @@ inline CostMatrix build_matrix(const std::vector<EmbeddingSample>& samples, cons
   m.row_ids.resize(m.rows);
   for (std::size_t i = 0; i < m.rows; ++i) m.row_ids[i] = i;
   const edxc::Csr csr(samples);
-  if (snap.engine && edx_engine_clock(snap.engine) == snap.engine_clock) {
+  if (!size_of && snap.engine && edx_engine_clock(snap.engine) == snap.engine_clock) {
     edxc::check(edx_engine_load_batch(snap.engine, csr.ids.data(), csr.offsets.data(), m.rows, 0));
     edxc::check(edx_engine_build(snap.engine, m.values.data()));
     return m;
   }
   const edxc::SnapArrays a(snap);
   const edx_cluster_config c = edxc::to_c(cfg);
+  if (size_of) {
+    const auto sz = edxc::sizes_of(csr.ids, size_of);
+    edxc::check(edx_build_matrix_sized(&c, a.ids.data(), a.owners.data(), a.latest.data(),
+                                       a.ids.size(), csr.ids.data(), csr.offsets.data(), m.rows,
+                                       sz.data(), m.values.data()));
+    return m;
+  }
   edxc::check(edx_build_matrix(&c, a.ids.data(), a.owners.data(), a.latest.data(),
                                a.resident.data(), a.ids.size(), csr.ids.data(), csr.offsets.data(),
                                m.rows, m.values.data()));

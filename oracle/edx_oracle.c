@@ -376,6 +376,42 @@ int orc_build_matrix_snapshot(const orc_cluster_config* cfg, const uint32_t* sna
   return rc;
 }
 
+/* detail::transfer_seconds with a SizeLookupFn (cost.hpp:68-73):
+ * bytes * 8.0 / bw, mul then div; expected_cost's chain is unchanged. */
+int orc_expected_costs_sized(const orc_cluster_config* cfg, const uint32_t* snap_ids,
+                             const uint64_t* snap_owners, const uint64_t* snap_latest,
+                             uint64_t snap_count, const uint32_t* ids, const uint64_t* offsets,
+                             uint64_t R, const uint64_t* sizes, double* out) {
+  gstate g;
+  gstate_init(&g, snap_count + 16);
+  for (uint64_t s = 0; s < snap_count; ++s) {
+    int64_t x = gstate_ref(&g, snap_ids[s]);
+    g.owners[x] = snap_owners[s];
+    g.latest[x] = snap_latest[s];
+  }
+  for (uint64_t i = 0; i < R; ++i) {
+    for (int j = 0; j < cfg->n; ++j) {
+      double cost = 0.0;
+      for (uint64_t t = offsets[i]; t < offsets[i + 1]; ++t) {
+        int32_t x = idmap_get(&g.map, ids[t]);
+        uint64_t owners = x >= 0 ? g.owners[x] : 0, latest = x >= 0 ? g.latest[x] : 0;
+        if ((latest >> j) & 1ULL) continue;
+        const double bytes = (double)sizes[t];
+        cost += bytes * 8.0 / cfg->bandwidths_bps[j];
+        uint64_t others = owners & ~(1ULL << j);
+        while (others) {
+          int o = __builtin_ctzll(others);
+          others &= others - 1;
+          cost += bytes * 8.0 / cfg->bandwidths_bps[o];
+        }
+      }
+      out[i * (uint64_t)cfg->n + (uint64_t)j] = cost;
+    }
+  }
+  gstate_free(&g);
+  return ORC_OK;
+}
+
 /* baseline_hitgreedy — assign.hpp:346-392.  A sample scores worker j by how
  * many of its ids have their latest copy on j; samples commit in order of
  * best score (desc), index (asc); each takes its best-scoring worker with

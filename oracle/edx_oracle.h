@@ -81,6 +81,13 @@ int orc_build_matrix_snapshot(const orc_cluster_config* cfg, const uint32_t* sna
                               const uint64_t* snap_resident, uint64_t snap_count,
                               const uint32_t* ids, const uint64_t* offsets,
                               uint64_t num_samples, double* out);
+/* expected_cost (cost.hpp:81-100) of every (sample, worker) with a
+ * SizeLookupFn (cost.hpp:64-73): sizes[t] = size_of(ids[t]) bytes per id
+ * position; no sample-count check (build_matrix adds only that). */
+int orc_expected_costs_sized(const orc_cluster_config* cfg, const uint32_t* snap_ids,
+                             const uint64_t* snap_owners, const uint64_t* snap_latest,
+                             uint64_t snap_count, const uint32_t* ids, const uint64_t* offsets,
+                             uint64_t num_samples, const uint64_t* sizes, double* out);
 /* baseline_hitgreedy — assign.hpp:346-392 on a snapshot (owners/latest). */
 int orc_hitgreedy_snapshot(const orc_cluster_config* cfg, const uint32_t* snap_ids,
                            const uint64_t* snap_owners, const uint64_t* snap_latest,

@@ -112,6 +112,8 @@ class Oracle:
         L.orc_unit_costs.argtypes = [P(ClusterConfigC), P(dbl)]
         L.orc_build_matrix_snapshot.argtypes = [P(ClusterConfigC), P(C.c_uint32), P(u64), P(u64),
                                                 P(u64), u64, P(C.c_uint32), P(u64), u64, P(dbl)]
+        L.orc_expected_costs_sized.argtypes = [P(ClusterConfigC), P(C.c_uint32), P(u64), P(u64),
+                                               u64, P(C.c_uint32), P(u64), u64, P(u64), P(dbl)]
         L.orc_hitgreedy_snapshot.argtypes = [P(ClusterConfigC), P(C.c_uint32), P(u64), P(u64), u64,
                                              P(C.c_uint32), P(u64), u64, P(i32)]
         L.orc_sim_hitgreedy.argtypes = [vp, P(C.c_uint32), P(u64), u64, P(i32)]
@@ -186,6 +188,22 @@ class Oracle:
         self._check(self.lib.orc_build_matrix_snapshot(
             C.byref(cfg.c()), _p(keys, C.c_uint32), _p(ow, C.c_uint64), _p(la, C.c_uint64),
             _p(re, C.c_uint64), len(keys), _p(ids, C.c_uint32), _p(offsets, C.c_uint64), R,
+            _p(out, C.c_double)))
+        return out.reshape(R, cfg.n)
+
+    def expected_costs_sized(self, cfg: Cfg, snap, ids, offsets, sizes):
+        """Every expected_cost cell with a SizeLookupFn; sizes[t] per id position."""
+        keys = np.array(sorted(snap), np.uint32)
+        ow = np.array([snap[int(k)][0] for k in keys], np.uint64)
+        la = np.array([snap[int(k)][1] for k in keys], np.uint64)
+        ids = np.ascontiguousarray(ids, np.uint32)
+        offsets = np.ascontiguousarray(offsets, np.uint64)
+        sizes = np.ascontiguousarray(sizes, np.uint64)
+        R = len(offsets) - 1
+        out = np.empty(max(R, 0) * cfg.n, np.float64)
+        self._check(self.lib.orc_expected_costs_sized(
+            C.byref(cfg.c()), _p(keys, C.c_uint32), _p(ow, C.c_uint64), _p(la, C.c_uint64),
+            len(keys), _p(ids, C.c_uint32), _p(offsets, C.c_uint64), R, _p(sizes, C.c_uint64),
             _p(out, C.c_double)))
         return out.reshape(R, cfg.n)
 

@@ -20,6 +20,7 @@
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <unordered_map>
 #include <vector>
 
 #include "embdispatch/assign.hpp"
@@ -177,6 +178,29 @@ int orc_build_matrix_snapshot(const orc_cluster_config* c, const uint32_t* snap_
     }
     const CostMatrix m = build_matrix(to_samples(ids, offsets, R), snap, to_cfg(c));
     std::memcpy(out, m.values.data(), m.values.size() * sizeof(double));
+  });
+}
+
+int orc_expected_costs_sized(const orc_cluster_config* c, const uint32_t* snap_ids,
+                             const uint64_t* owners, const uint64_t* latest, uint64_t count,
+                             const uint32_t* ids, const uint64_t* offsets, uint64_t R,
+                             const uint64_t* sizes, double* out) {
+  return guarded([&] {
+    Snapshot snap;
+    for (uint64_t s = 0; s < count; ++s) {
+      EmbeddingState& st = snap.states[snap_ids[s]];
+      st.owners = owners[s];
+      st.latest = latest[s];
+    }
+    std::unordered_map<EmbeddingId, std::uint64_t> table;
+    for (uint64_t t = offsets[0]; t < offsets[R]; ++t) table[ids[t]] = sizes[t];
+    const SizeLookupFn size_of = [&table](EmbeddingId id) { return table.at(id); };
+    const ClusterConfig cfg = to_cfg(c);
+    const auto samples = to_samples(ids, offsets, R);
+    for (uint64_t i = 0; i < R; ++i)
+      for (int j = 0; j < cfg.n; ++j)
+        out[i * static_cast<uint64_t>(cfg.n) + static_cast<uint64_t>(j)] =
+            expected_cost(samples[i], j, snap, cfg, size_of);
   });
 }
 

@@ -38,7 +38,7 @@ from ._lib import (EDX_NUM_PHASES, ClusterConfigC, CudaError, EdxError, EdxRunti
 __all__ = [
     "ClusterConfig", "EmbeddingState", "Snapshot", "CostMatrix", "SquareCost", "AssignmentResult",
     "DispatchDecision", "IterationReport", "SimState", "ZipfStream", "validate", "unit_cost",
-    "make_sample", "to_csr", "build_matrix", "row_gap_key", "rows_by_gap", "hungarian",
+    "make_sample", "to_csr", "build_matrix", "expected_cost", "row_gap_key", "rows_by_gap", "hungarian",
     "hungarian_blocks", "greedy_dispatch", "expand_columns", "ecomix", "decision_cost",
     "exact_multiplicity", "InvalidArgument", "LogicError", "EdxRuntimeError", "CudaError",
     "EdxError", "EDX_NUM_PHASES",
@@ -231,20 +231,60 @@ def _snapshot_arrays(snap):
     return keys, ow, la, re
 
 
-def build_matrix(samples, snap, cfg: ClusterConfig) -> CostMatrix:
-    """build_matrix — cost.hpp:105-125.  `snap` is a Snapshot or a SimState snapshot view."""
+def _sizes_of(ids, size_of):
+    """SizeLookupFn (cost.hpp:64) evaluated once per id position, in order."""
+    return np.fromiter((int(size_of(int(x))) for x in ids), dtype=np.uint64, count=len(ids))
+
+
+def build_matrix(samples, snap, cfg: ClusterConfig, size_of=None) -> CostMatrix:
+    """build_matrix — cost.hpp:105-125.  `snap` is a Snapshot or a SimState
+    snapshot view; `size_of` (optional) maps an id to its transfer size in
+    bytes (SizeLookupFn, cost.hpp:64-73) instead of the uniform d_tran."""
     if isinstance(snap, _EngineSnapshot):
-        return snap.engine._build_view(samples)
+        if size_of is None:
+            return snap.engine._build_view(samples)
+        snap = snap.engine.snapshot_dict()
     ids, offs = to_csr(samples)
     R = len(offs) - 1
     keys, ow, la, re = _snapshot_arrays(snap or {})
     out = np.empty((max(R, 0), cfg.n), np.float64)
     c = cfg._c()
-    check(lib().edx_build_matrix(C.byref(c), _ptr(keys, C.c_uint32), _ptr(ow, C.c_uint64),
-                                 _ptr(la, C.c_uint64), _ptr(re, C.c_uint64), len(keys),
-                                 _ptr(ids, C.c_uint32), _ptr(offs, C.c_uint64), R,
-                                 _ptr(out, C.c_double)))
+    if size_of is None:
+        check(lib().edx_build_matrix(C.byref(c), _ptr(keys, C.c_uint32), _ptr(ow, C.c_uint64),
+                                     _ptr(la, C.c_uint64), _ptr(re, C.c_uint64), len(keys),
+                                     _ptr(ids, C.c_uint32), _ptr(offs, C.c_uint64), R,
+                                     _ptr(out, C.c_double)))
+    else:
+        sz = _sizes_of(ids, size_of)
+        check(lib().edx_build_matrix_sized(C.byref(c), _ptr(keys, C.c_uint32), _ptr(ow, C.c_uint64),
+                                           _ptr(la, C.c_uint64), len(keys), _ptr(ids, C.c_uint32),
+                                           _ptr(offs, C.c_uint64), R, _ptr(sz, C.c_uint64),
+                                           _ptr(out, C.c_double)))
     return CostMatrix(out, np.arange(R, dtype=np.uint64))
+
+
+def expected_cost(sample, worker: int, snap, cfg: ClusterConfig, size_of=None) -> float:
+    """expected_cost — cost.hpp:81-100 (one cell, optional SizeLookupFn)."""
+    if not 0 <= int(worker) < cfg.n:
+        raise InvalidArgument("worker id out of range")
+    if isinstance(snap, _EngineSnapshot):
+        snap = snap.engine.snapshot_dict()
+    ids, offs = to_csr([sample])
+    keys, ow, la, _ = _snapshot_arrays(snap or {})
+    row = np.empty(cfg.n, np.float64)
+    c = cfg._c()
+    if size_of is None:
+        check(lib().edx_expected_costs(C.byref(c), _ptr(keys, C.c_uint32), _ptr(ow, C.c_uint64),
+                                       _ptr(la, C.c_uint64), len(keys), _ptr(ids, C.c_uint32),
+                                       _ptr(offs, C.c_uint64), 1, _ptr(row, C.c_double)))
+    else:
+        sz = _sizes_of(ids, size_of)
+        check(lib().edx_expected_costs_sized(C.byref(c), _ptr(keys, C.c_uint32),
+                                             _ptr(ow, C.c_uint64), _ptr(la, C.c_uint64),
+                                             len(keys), _ptr(ids, C.c_uint32),
+                                             _ptr(offs, C.c_uint64), 1, _ptr(sz, C.c_uint64),
+                                             _ptr(row, C.c_double)))
+    return float(row[int(worker)])
 
 
 def _vals(matrix):
@@ -577,6 +617,14 @@ class SimState:
                                              _ptr(la, C.c_uint64), _ptr(re, C.c_uint64), k,
                                              C.byref(cnt)))
         return ids, ow, la, re
+
+    def snapshot_dict(self) -> "Snapshot":
+        """A host Snapshot (id -> EmbeddingState) of the live device state."""
+        ids, ow, la, re = self.global_masks()
+        snap = Snapshot()
+        for t in range(len(ids)):
+            snap[int(ids[t])] = EmbeddingState(int(ow[t]), int(la[t]), int(re[t]))
+        return snap
 
     def canonical_state(self):
         """(global, caches) in the same canonical form as oracle.pyoracle.Sim."""

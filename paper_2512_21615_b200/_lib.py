@@ -97,6 +97,9 @@ def _sigs():
         ("edx_build_matrix", cint, [cfgp, u32p, u64p, u64p, u64p, u64, u32p, u64p, u64, dblp]),
         ("edx_hitgreedy", cint, [cfgp, u32p, u64p, u64p, u64, u32p, u64p, u64, i32p]),
         ("edx_expected_costs", cint, [cfgp, u32p, u64p, u64p, u64, u32p, u64p, u64, dblp]),
+        ("edx_build_matrix_sized", cint, [cfgp, u32p, u64p, u64p, u64, u32p, u64p, u64, u64p, dblp]),
+        ("edx_expected_costs_sized", cint, [cfgp, u32p, u64p, u64p, u64, u32p, u64p, u64, u64p,
+                                            dblp]),
         ("edx_row_gap_key", cint, [u64, u64, dblp, u64, dblp]),
         ("edx_rows_by_gap", cint, [u64, u64, dblp, u64p]),
         ("edx_hungarian", cint, [u64, dblp, u64p, dblp]),

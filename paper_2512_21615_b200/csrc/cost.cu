@@ -53,11 +53,14 @@ __global__ void __launch_bounds__(kBlockCells)
     k_cost_build(const uint32_t* __restrict__ ids, const uint64_t* __restrict__ offsets,
                  uint64_t rows, int n, int rows_per_block, const ulonglong2* __restrict__ ol,
                  uint64_t id_space, const double* __restrict__ ucost,
+                 const uint64_t* __restrict__ sizes, const double* __restrict__ bw,
                  double* __restrict__ matrix, uint64_t* __restrict__ gap_keys,
                  uint32_t* __restrict__ row_index, int* __restrict__ flags) {
   __shared__ double u_s[kMaxWorkers];
   __shared__ double tile[kBlockCells];
-  if (threadIdx.x < n) u_s[threadIdx.x] = ucost[threadIdx.x];
+  // sizes == nullptr: u_s = unit costs; else u_s = bandwidths and every add is
+  // transfer_seconds (cost.hpp:68-73) of the id's own size: bytes * 8.0 / bw
+  if (threadIdx.x < n) u_s[threadIdx.x] = sizes ? bw[threadIdx.x] : ucost[threadIdx.x];
   __syncthreads();
 
   const int local_row = threadIdx.x / n;
@@ -72,7 +75,22 @@ __global__ void __launch_bounds__(kBlockCells)
     const double uj = u_s[j];
     const uint64_t beg = offsets[i], end = offsets[i + 1];
     bool bad = false;
-    for (uint64_t t = beg; t < end; t += kPrefetch) {
+    for (uint64_t t = beg; sizes && t < end; ++t) {  // SizeLookupFn path (cost.hpp:64-73)
+      const uint32_t id = __ldg(ids + t);
+      ulonglong2 st = make_ulonglong2(0, 0);
+      if (id < id_space) st = __ldg(ol + id);
+      else bad = true;
+      if (st.y & jbit) continue;
+      const double bytes8 = __dmul_rn(__ull2double_rn(sizes[t]), 8.0);
+      c = __dadd_rn(c, __ddiv_rn(bytes8, u_s[j]));
+      uint64_t others = st.x & ~jbit;
+      while (others) {
+        const int o = __ffsll(static_cast<long long>(others)) - 1;
+        others &= others - 1;
+        c = __dadd_rn(c, __ddiv_rn(bytes8, u_s[o]));
+      }
+    }
+    for (uint64_t t = beg; !sizes && t < end; t += kPrefetch) {
       ulonglong2 st[kPrefetch];
 #pragma unroll
       for (int q = 0; q < kPrefetch; ++q) {
@@ -544,9 +562,9 @@ __global__ void k_gap_keys(const double* __restrict__ matrix, uint64_t rows, int
 void launch_cost_build(const uint32_t* ids, const uint64_t* offsets, uint64_t rows, int n,
                        const ulonglong2* ol, uint64_t id_space, const double* ucost,
                        double* matrix, uint64_t* gap_keys, uint32_t* row_index, int* flags,
-                       cudaStream_t s) {
+                       cudaStream_t s, const uint64_t* sizes, const double* bw) {
   if (rows == 0) return;
-  if (n >= 2) {
+  if (n >= 2 && sizes == nullptr) {
     const int np = n <= 2 ? 2 : n <= 4 ? 4 : n <= 8 ? 8 : n <= 16 ? 16 : n <= 32 ? 32 : 64;
     const uint64_t rows_per_block = static_cast<uint64_t>(kWarpRowsThreads / 32) * (np >= 32 ? 1 : 32 / np);
     const unsigned blocks = static_cast<unsigned>((rows + rows_per_block - 1) / rows_per_block);
@@ -565,13 +583,13 @@ void launch_cost_build(const uint32_t* ids, const uint64_t* offsets, uint64_t ro
     EDX_LAUNCHED();
     return;
   }
-  // n == 1: one thread per cell
+  // n == 1 or per-id sizes: one thread per cell
   const int rows_per_block = n >= kBlockCells ? 1 : kBlockCells / n;
   const int threads = rows_per_block * n;
   const uint64_t blocks = (rows + rows_per_block - 1) / rows_per_block;
   k_cost_build<<<static_cast<unsigned>(blocks), threads, 0, s>>>(
-      ids, offsets, rows, n, rows_per_block, ol, id_space, ucost, matrix, gap_keys, row_index,
-      flags);
+      ids, offsets, rows, n, rows_per_block, ol, id_space, ucost, sizes, bw, matrix, gap_keys,
+      row_index, flags);
   EDX_LAUNCHED();
 }
 

@@ -81,7 +81,7 @@ struct DevBuf {
 void launch_cost_build(const uint32_t* ids, const uint64_t* offsets, uint64_t rows, int n,
                        const ulonglong2* ol, uint64_t id_space, const double* ucost,
                        double* matrix, uint64_t* gap_keys, uint32_t* row_index, int* flags,
-                       cudaStream_t s);
+                       cudaStream_t s, const uint64_t* sizes = nullptr, const double* bw = nullptr);
 // gap keys only, for an externally supplied matrix (rows_by_gap on a host matrix)
 void launch_gap_keys(const double* matrix, uint64_t rows, int n, uint64_t* gap_keys,
                      uint32_t* row_index, cudaStream_t s);

@@ -241,7 +241,8 @@ struct DefaultCtx {
   DevBuf<int32_t> i32a, i32b;
   DevBuf<unsigned long long> snapA, snapB, snapC;
   DevBuf<ulonglong2> ol;
-  DevBuf<double> ucost, scalar;
+  DevBuf<double> ucost, scalar, bw;
+  DevBuf<uint64_t> sizes;
   DevBuf<int> flags;
 
   void init() {
@@ -921,7 +922,7 @@ namespace {
 void stateless_build(const edx_cluster_config* cfg, const uint32_t* snap_ids,
                      const uint64_t* snap_owners, const uint64_t* snap_latest,
                      uint64_t snap_count, const uint32_t* ids, const uint64_t* offsets,
-                     uint64_t R, double* out);
+                     uint64_t R, double* out, const uint64_t* sizes = nullptr);
 }  // namespace
 
 int edx_build_matrix(const edx_cluster_config* cfg, const uint32_t* snap_ids,
@@ -995,11 +996,37 @@ int edx_expected_costs(const edx_cluster_config* cfg, const uint32_t* snap_ids,
   });
 }
 
+int edx_build_matrix_sized(const edx_cluster_config* cfg, const uint32_t* snap_ids,
+                           const uint64_t* snap_owners, const uint64_t* snap_latest,
+                           uint64_t snap_count, const uint32_t* ids, const uint64_t* offsets,
+                           uint64_t R, const uint64_t* sizes, double* out) {
+  return guard([&] {
+    if (!cfg || cfg->n < 1 || cfg->n > 64) edx::invalid(cfg && cfg->n > 64 ? "at most 64 workers supported" : "worker count must be >= 1");
+    const uint64_t want = static_cast<uint64_t>(cfg->n) * static_cast<uint64_t>(cfg->m);
+    if (R != want) edx::invalid("expected " + std::to_string(want) + " samples, got " + std::to_string(R));
+    if (cfg->n_bandwidths < cfg->n) edx::invalid("need one bandwidth per worker");
+    stateless_build(cfg, snap_ids, snap_owners, snap_latest, snap_count, ids, offsets, R, out, sizes);
+  });
+}
+
+int edx_expected_costs_sized(const edx_cluster_config* cfg, const uint32_t* snap_ids,
+                             const uint64_t* snap_owners, const uint64_t* snap_latest,
+                             uint64_t snap_count, const uint32_t* ids, const uint64_t* offsets,
+                             uint64_t num_samples, const uint64_t* sizes, double* out) {
+  return guard([&] {
+    if (!cfg || cfg->n < 1 || cfg->n > 64) edx::invalid(cfg && cfg->n > 64 ? "at most 64 workers supported" : "worker count must be >= 1");
+    if (cfg->n_bandwidths < cfg->n) edx::invalid("need one bandwidth per worker");
+    if (num_samples == 0) return;
+    stateless_build(cfg, snap_ids, snap_owners, snap_latest, snap_count, ids, offsets,
+                    num_samples, out, sizes);
+  });
+}
+
 namespace {
 void stateless_build(const edx_cluster_config* cfg, const uint32_t* snap_ids,
                      const uint64_t* snap_owners, const uint64_t* snap_latest,
                      uint64_t snap_count, const uint32_t* ids, const uint64_t* offsets,
-                     uint64_t R, double* out) {
+                     uint64_t R, double* out, const uint64_t* sizes) {
   {
     auto& c = dctx();
     std::lock_guard<std::mutex> lk(c.mu);
@@ -1034,8 +1061,17 @@ void stateless_build(const edx_cluster_config* cfg, const uint32_t* snap_ids,
                                                          snap_count, space, c.ol.p, nullptr, c.flags.p);
       EDX_LAUNCHED();
     }
+    const uint64_t* d_sizes = nullptr;
+    if (sizes) {  // SizeLookupFn values, one per id position
+      c.sizes.ensure(total);
+      c.bw.ensure(cfg->n);
+      if (total)
+        EDX_CUDA(cudaMemcpyAsync(c.sizes.p, sizes + base, total * 8, cudaMemcpyHostToDevice, c.stream));
+      EDX_CUDA(cudaMemcpyAsync(c.bw.p, cfg->bandwidths_bps, cfg->n * 8, cudaMemcpyHostToDevice, c.stream));
+      d_sizes = c.sizes.p;
+    }
     edx::launch_cost_build(c.ids.p, c.offsets.p, R, cfg->n, c.ol.p, space, c.ucost.p, c.values.p,
-                           nullptr, nullptr, c.flags.p, c.stream);
+                           nullptr, nullptr, c.flags.p, c.stream, d_sizes, c.bw.p);
     EDX_CUDA(cudaMemcpyAsync(out, c.values.p, R * cfg->n * 8, cudaMemcpyDeviceToHost, c.stream));
     c.sync_and_check();
   }

@@ -188,7 +188,45 @@ static void run_loop() {
   EXPECT(r.reports.size() == 50 && r.summary.measured_iterations == 40, "run() bookkeeping");
 }
 
+// test_cost.cpp:241-249, then the same hook on a live SimState snapshot
+// against the oracle restatement of the sized chain.
+static void sized_costs() {
+  ClusterConfig cfg;
+  cfg.n = 2;
+  cfg.m = 1;
+  cfg.cache_capacity = 16;
+  cfg.bandwidths_bps = {5e9, 5e9};
+  const Snapshot empty;
+  const SizeLookupFn size_of = [](EmbeddingId id) -> std::uint64_t { return id == 1 ? 4096 : 1024; };
+  const double got = expected_cost(make_sample({1, 2}), 0, empty, cfg, size_of);
+  EXPECT(got == (4096.0 * 8 / 5e9) + (1024.0 * 8 / 5e9), "sized KAT %.17g", got);
+
+  cfg.n = 3;
+  cfg.bandwidths_bps = {5e9, 2e9, 5e8};
+  SimState state(cfg, EngineOptions{0, 64, 64});
+  state.seed_entry(1, 0, true, true);
+  state.seed_entry(2, 1, true, false);
+  state.seed_entry(2, 2, true, false);
+  const std::vector<EmbeddingSample> samples = {make_sample({1, 2, 3}), make_sample({2}),
+                                                make_sample({3, 1})};
+  const SizeLookupFn sz = [](EmbeddingId id) -> std::uint64_t { return 300 + 1000 * id; };
+  const CostMatrix m = build_matrix(samples, state.snapshot(), cfg, sz);
+  const CostMatrix v = build_matrix(samples, state.device_snapshot(), cfg, sz);
+  const uint32_t ids[6] = {1, 2, 3, 2, 3, 1};
+  const uint64_t offs[4] = {0, 3, 4, 6};
+  uint64_t sizes[6];
+  for (int t = 0; t < 6; ++t) sizes[t] = sz(ids[t]);
+  const uint32_t sid[2] = {1, 2};
+  const uint64_t so[2] = {1, 0}, sl[2] = {1, 6};
+  orc_cluster_config oc{3, 1, cfg.bandwidths_bps.data(), 3, 0, 2048, 16, 1.0};
+  double want[9];
+  orc_expected_costs_sized(&oc, sid, so, sl, 2, ids, offs, 3, sizes, want);
+  EXPECT(std::memcmp(m.values.data(), want, sizeof want) == 0, "sized build vs oracle");
+  EXPECT(std::memcmp(v.values.data(), want, sizeof want) == 0, "sized build on a device view");
+}
+
 int main() {
+  sized_costs();
   fig2_walkthrough();
   engine_vs_oracle(0.0);
   engine_vs_oracle(0.5);

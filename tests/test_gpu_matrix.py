@@ -179,6 +179,58 @@ def test_build_long_and_empty_rows_bitwise(gpu, oracle, pyoracle, n):
     assert got.tobytes() == want.tobytes()
 
 
+def test_sized_kat(gpu):
+    """test_cost.cpp:241-249: non-uniform sizes flow through the cost hook."""
+    edx = gpu
+    c = cfg(edx, 2, 1, [5e9, 5e9])
+    size_of = lambda i: 4096 if i == 1 else 1024
+    got = edx.expected_cost([1, 2], 0, edx.Snapshot(), c, size_of)
+    assert got == (4096.0 * 8 / 5e9) + (1024.0 * 8 / 5e9)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 8, 16, 33, 64])
+def test_sized_build_bitwise(gpu, oracle, pyoracle, n):
+    """build_matrix with a SizeLookupFn: every cell bitwise vs the reference."""
+    from test_host import random_sized_case
+    edx = gpu
+    snap, samples, ids, offs, sizes, size_of, bw = random_sized_case(70 + n, n, R=n * 3)
+    c = cfg(edx, n, 3, bw)
+    s = edx.Snapshot()
+    for k, (o, l, r) in snap.items():
+        s[k] = edx.EmbeddingState(o, l, r)
+    got = edx.build_matrix(samples, s, c, size_of=lambda i: size_of[i]).values
+    want = oracle.expected_costs_sized(pyoracle.Cfg(n, 3, bw), snap, ids, offs, sizes)
+    assert got.tobytes() == want.tobytes()
+    # uniform sizes equal to d_tran reproduce the unsized build
+    plain = edx.build_matrix(samples, s, c).values
+    same = edx.build_matrix(samples, s, c, size_of=lambda i: 2048).values
+    assert plain.tobytes() == same.tobytes()
+
+
+def test_sized_build_on_engine_snapshot(gpu, oracle, pyoracle):
+    """A SimState snapshot view with a size hook reads the live device state."""
+    edx = gpu
+    n, m, L, V = 4, 8, 6, 500
+    bw = [5e9, 5e9, 5e8, 5e8]
+    c = edx.ClusterConfig(n=n, m=m, bandwidths_bps=bw, cache_capacity=200, alpha=0.0)
+    eng = edx.SimState(c, id_space=V, max_batch_ids=n * m * L)
+    sim = oracle.sim(pyoracle.Cfg(n, m, bw, cap=200, alpha=0.0))
+    offs = np.arange(n * m + 1, dtype=np.uint64) * np.uint64(L)
+    batches = list(oracle.zipf_batches(V, L, 1.05, 4, 3, n * m))
+    for ids in batches[:3]:
+        dec, _, _, _ = sim.iteration(ids, offs)
+        eng.iterate(ids, offs)
+    ids = batches[3]
+    size_of = lambda i: 512 + 64 * (i % 7)
+    samples = [list(ids[i * L:(i + 1) * L]) for i in range(n * m)]
+    got = edx.build_matrix(samples, eng.snapshot(), c, size_of=size_of).values
+    g = sim.canonical_state()[0]
+    snap = {int(r[0]): (int(r[1]), int(r[2]), int(r[3])) for r in g}
+    sizes = np.array([size_of(int(x)) for x in ids], np.uint64)
+    want = oracle.expected_costs_sized(pyoracle.Cfg(n, m, bw), snap, ids, offs, sizes)
+    assert got.tobytes() == want.tobytes()
+
+
 # ------------------------------------------------------------- gap / order
 def test_row_gap_key_kat(gpu):
     edx = gpu

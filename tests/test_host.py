@@ -160,3 +160,50 @@ def test_zipf_stream_large_and_reset(edx, oracle, V, L, R, iters):
     assert len(got) == iters and all((a == b).all() for a, b in zip(got, want))
     z.reset()
     assert (next(iter(z)) == want[0]).all()
+
+
+def random_sized_case(seed, n, R=12, V=300):
+    """A consistent random snapshot, ragged samples and per-id sizes."""
+    rng = np.random.default_rng(seed)
+    full = (1 << n) - 1
+
+    def bits():
+        return (int(rng.integers(0, 1 << 32)) << 32 | int(rng.integers(0, 1 << 32))) & full
+
+    snap = {}
+    for id_ in range(V):
+        k = rng.integers(0, 4)
+        if k == 0:
+            continue
+        res = bits()
+        own = res & bits() if k == 3 else 0
+        lat = own if own else res & bits()
+        snap[id_] = (own, lat, res)
+    size_of = {i: int(rng.choice([256, 1024, 2048, 4096, 3000, 777])) for i in range(V + 20)}
+    samples = [list(rng.choice(V + 20, size=int(rng.integers(0, 25)), replace=False)) for _ in range(R)]
+    ids = np.array([x for s in samples for x in s], np.uint32)
+    offs = np.zeros(R + 1, np.uint64)
+    offs[1:] = np.cumsum([len(s) for s in samples])
+    sizes = np.array([size_of[int(x)] for x in ids], np.uint64)
+    bw = rng.choice([5e9, 2e9, 5e8, 1e9, 3.3e9], size=n)
+    return snap, samples, ids, offs, sizes, size_of, bw
+
+
+def test_oracle_sized_kat(port, ref, pyoracle):
+    """test_cost.cpp:241-249: non-uniform sizes flow through the cost hook."""
+    cfg = pyoracle.Cfg(2, 1, [5e9, 5e9])
+    ids = np.array([1, 2], np.uint32)
+    offs = np.array([0, 2, 2], np.uint64)
+    sizes = np.array([4096, 1024], np.uint64)
+    for o in (port, ref):
+        got = o.expected_costs_sized(cfg, {}, ids, offs, sizes)
+        assert got[0, 0] == (4096.0 * 8 / 5e9) + (1024.0 * 8 / 5e9)
+
+
+@pytest.mark.parametrize("n", [1, 3, 8, 33, 64])
+def test_oracle_sized_equals_reference(port, ref, pyoracle, n):
+    snap, _, ids, offs, sizes, _, bw = random_sized_case(50 + n, n)
+    cfg = pyoracle.Cfg(n, 1, bw)
+    a = port.expected_costs_sized(cfg, snap, ids, offs, sizes)
+    b = ref.expected_costs_sized(cfg, snap, ids, offs, sizes)
+    assert a.tobytes() == b.tobytes()
