@@ -236,6 +236,36 @@ int edx_ecomix(const edx_cluster_config* cfg, uint64_t rows, uint64_t cols,
 int edx_decision_cost(uint64_t rows, uint64_t cols, const double* values,
                       const int32_t* decision, double* out);
 
+/* --------------------------------------------------- standalone WorkerCache
+ * cache.hpp:73-240, one device-resident cache driven entry by entry (SimState
+ * updates its caches a batch at a time inside edx_engine_step instead).
+ * policy: 0 = VictimPolicy::kMarkVersion, 1 = kPriorityRatio.  footprint is
+ * the FootprintFn value of the id (1.0 without one), used by kPriorityRatio. */
+typedef struct edx_cache edx_cache;
+/* WorkerCache(capacity, policy, footprint) — cache.hpp:79-84 */
+int edx_cache_create(uint64_t capacity, int policy, int device, edx_cache** out);
+void edx_cache_destroy(edx_cache* c);
+/* touch(id, latest, now) — cache.hpp:102-122 */
+int edx_cache_touch(edx_cache* c, uint32_t id, int latest, uint64_t now, double footprint);
+/* set_version(id, latest) — cache.hpp:126-135 */
+int edx_cache_set_version(edx_cache* c, uint32_t id, int latest);
+/* erase(id) — cache.hpp:174-180 */
+int edx_cache_erase(edx_cache* c, uint32_t id);
+/* find(id) — cache.hpp:94-97; *found = 0 when absent */
+int edx_cache_find(edx_cache* c, uint32_t id, int* found, int* version_latest, uint32_t* mark,
+                   uint32_t* frequency, uint64_t* last_access);
+/* select_victim() — cache.hpp:141-148 */
+int edx_cache_select_victim(edx_cache* c, uint32_t* victim);
+/* evict_for(needed, needs_push, pinned) — cache.hpp:152-170: the evicted ids
+ * in eviction order (at most capacity); needs_push is applied by the caller. */
+int edx_cache_evict_for(edx_cache* c, uint64_t needed, const uint32_t* pinned, uint64_t n_pinned,
+                        uint32_t* victims, uint64_t* n_victims);
+/* size(), current_mark() and the at-current-mark count — cache.hpp:86-91 */
+int edx_cache_info(edx_cache* c, uint64_t* size, uint32_t* current_mark, uint64_t* at_current_mark);
+/* entries() — cache.hpp:180-182, as parallel arrays (count first with ids NULL) */
+int edx_cache_export(edx_cache* c, uint32_t* ids, uint8_t* version, uint32_t* mark,
+                     uint32_t* frequency, uint64_t* last_access, uint64_t cap_out, uint64_t* count);
+
 /* ------------------------------------------------- synthetic input stream
  * ZipfStream (workload.hpp:94-133): the benchmark's input producer, host side. */
 typedef struct edx_zipf edx_zipf;

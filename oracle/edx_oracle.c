@@ -760,6 +760,7 @@ typedef struct {
   uint8_t* version;
   uint32_t *mark, *freq;
   uint64_t* last;
+  double* fp; /* standalone caches only: FootprintFn(id) per slot */
 } wcache;
 
 static void wcache_init(wcache* c, uint64_t capacity) {
@@ -773,6 +774,7 @@ static void wcache_init(wcache* c, uint64_t capacity) {
   c->mark = (uint32_t*)malloc(sizeof(uint32_t) * capacity);
   c->freq = (uint32_t*)malloc(sizeof(uint32_t) * capacity);
   c->last = (uint64_t*)malloc(sizeof(uint64_t) * capacity);
+  c->fp = NULL;
 }
 
 static void wcache_free(wcache* c) {
@@ -782,6 +784,7 @@ static void wcache_free(wcache* c) {
   free(c->mark);
   free(c->freq);
   free(c->last);
+  free(c->fp);
 }
 
 /* touch — cache.hpp:102-122 */
@@ -829,6 +832,7 @@ static void wcache_erase(wcache* c, uint32_t id) {
     c->mark[s] = c->mark[last];
     c->freq[s] = c->freq[last];
     c->last[s] = c->last[last];
+    if (c->fp) c->fp[s] = c->fp[last];
     idmap_put(&c->map, c->id[s], s);
   }
   --c->size;
@@ -851,6 +855,136 @@ static int64_t wcache_pick(const wcache* c, const idmap* pinned) {
     if (best < 0 || key_less(c, s, (uint64_t)best)) best = (int64_t)s;
   }
   return best;
+}
+
+/* ---------------------------------------------- standalone WorkerCache */
+
+struct orc_cache {
+  wcache w;
+  int policy;
+};
+
+int orc_cache_create(uint64_t capacity, int policy, orc_cache** out) {
+  if (capacity == 0) return fail(ORC_INVALID_ARGUMENT, "cache capacity must be positive");
+  orc_cache* c = (orc_cache*)calloc(1, sizeof *c);
+  wcache_init(&c->w, capacity);
+  c->w.fp = (double*)malloc(sizeof(double) * capacity);
+  c->policy = policy;
+  *out = c;
+  return ORC_OK;
+}
+
+void orc_cache_destroy(orc_cache* c) {
+  if (!c) return;
+  wcache_free(&c->w);
+  free(c);
+}
+
+int orc_cache_touch(orc_cache* c, uint32_t id, int latest, uint64_t now, double footprint) {
+  int inserting = idmap_get(&c->w.map, id) < 0;
+  int rc = wcache_touch(&c->w, id, latest, now);
+  if (rc == ORC_OK && inserting) c->w.fp[c->w.size - 1] = footprint;
+  return rc;
+}
+
+int orc_cache_set_version(orc_cache* c, uint32_t id, int latest) {
+  return wcache_set_version(&c->w, id, latest);
+}
+
+int orc_cache_erase(orc_cache* c, uint32_t id) {
+  wcache_erase(&c->w, id);
+  return ORC_OK;
+}
+
+/* pick_victim (kPriorityRatio) — cache.hpp:203-230: least
+ * (version ? 2 : 1) * mark * frequency / footprint, then last access, then id */
+static int64_t wcache_pick_ratio(const wcache* c, const idmap* pinned) {
+  int64_t best = -1;
+  double bp = 0.0;
+  for (uint64_t s = 0; s < c->size; ++s) {
+    if (pinned && idmap_get(pinned, c->id[s]) >= 0) continue;
+    const double num = (c->version[s] ? 2.0 : 1.0) * (double)c->mark[s] * (double)c->freq[s];
+    const double pr = num / c->fp[s];
+    int better = best < 0 || pr < bp ||
+                 (pr == bp && (c->last[s] < c->last[best] ||
+                               (c->last[s] == c->last[best] && c->id[s] < c->id[best])));
+    if (better) {
+      best = (int64_t)s;
+      bp = pr;
+    }
+  }
+  return best;
+}
+
+static int64_t cache_pick(const orc_cache* c, const idmap* pinned) {
+  return c->policy ? wcache_pick_ratio(&c->w, pinned) : wcache_pick(&c->w, pinned);
+}
+
+/* select_victim — cache.hpp:141-148 */
+int orc_cache_select_victim(orc_cache* c, uint32_t* victim) {
+  if (c->w.size != c->w.capacity)
+    return fail(ORC_LOGIC_ERROR, "select_victim requires a full cache");
+  int64_t s = cache_pick(c, NULL);
+  if (s < 0) return fail(ORC_LOGIC_ERROR, "no evictable entry");
+  *victim = c->w.id[s];
+  return ORC_OK;
+}
+
+/* evict_for — cache.hpp:152-170 (maybe_advance_mark :187-192 first) */
+int orc_cache_evict_for(orc_cache* c, uint64_t needed, const uint32_t* pinned, uint64_t n_pinned,
+                        uint32_t* victims, uint64_t* n_victims) {
+  wcache* w = &c->w;
+  *n_victims = 0;
+  if (needed > w->capacity)
+    return fail(ORC_INVALID_ARGUMENT, "cannot free more slots than the capacity");
+  if (w->capacity - w->size >= needed) return ORC_OK;
+  if (w->size == w->capacity && w->at_current == w->size) {
+    ++w->current_mark;
+    w->at_current = 0;
+  }
+  idmap pins;
+  idmap_init(&pins, n_pinned + 16);
+  for (uint64_t q = 0; q < n_pinned; ++q) idmap_put(&pins, pinned[q], 1);
+  int rc = ORC_OK;
+  while (w->capacity - w->size < needed) {
+    int64_t s = cache_pick(c, &pins);
+    if (s < 0) {
+      rc = fail(ORC_LOGIC_ERROR, "every cache entry is pinned; cannot evict");
+      break;
+    }
+    victims[(*n_victims)++] = w->id[s];
+    wcache_erase(w, w->id[s]);
+  }
+  idmap_free(&pins);
+  return rc;
+}
+
+void orc_cache_info(orc_cache* c, uint64_t* size, uint32_t* current_mark) {
+  *size = c->w.size;
+  *current_mark = c->w.current_mark;
+}
+
+static const wcache* g_sort_cache;
+static int slot_by_id(const void* a, const void* b) {
+  uint32_t x = g_sort_cache->id[*(const uint64_t*)a], y = g_sort_cache->id[*(const uint64_t*)b];
+  return x < y ? -1 : (x > y ? 1 : 0);
+}
+
+void orc_cache_export(orc_cache* c, uint32_t* ids, uint8_t* version, uint32_t* mark,
+                      uint32_t* freq, uint64_t* last_access) {
+  const wcache* w = &c->w;
+  uint64_t* ord = (uint64_t*)malloc(sizeof(uint64_t) * (w->size + 1));
+  for (uint64_t s = 0; s < w->size; ++s) ord[s] = s;
+  g_sort_cache = w;
+  qsort(ord, w->size, sizeof(uint64_t), slot_by_id);
+  for (uint64_t t = 0; t < w->size; ++t) {
+    ids[t] = w->id[ord[t]];
+    version[t] = w->version[ord[t]];
+    mark[t] = w->mark[ord[t]];
+    freq[t] = w->freq[ord[t]];
+    last_access[t] = w->last[ord[t]];
+  }
+  free(ord);
 }
 
 /* ------------------------------------------------------------ the engine */

@@ -136,6 +136,23 @@ int orc_ref_iteration(orc_sim* s, const uint32_t* ids, const uint64_t* offsets,
                       uint64_t num_samples, int threads, int32_t* decision,
                       double* expected_cost, orc_report* rep, double* times_s);
 
+/* ---- standalone WorkerCache (cache.hpp:73-240) ----
+ * policy 0 = kMarkVersion, 1 = kPriorityRatio; footprint = FootprintFn(id)
+ * of the touched id (kept per id, 1.0 for ids never given one). */
+typedef struct orc_cache orc_cache;
+int orc_cache_create(uint64_t capacity, int policy, orc_cache** out);
+void orc_cache_destroy(orc_cache* c);
+int orc_cache_touch(orc_cache* c, uint32_t id, int latest, uint64_t now, double footprint);
+int orc_cache_set_version(orc_cache* c, uint32_t id, int latest);
+int orc_cache_erase(orc_cache* c, uint32_t id);
+int orc_cache_select_victim(orc_cache* c, uint32_t* victim);
+int orc_cache_evict_for(orc_cache* c, uint64_t needed, const uint32_t* pinned, uint64_t n_pinned,
+                        uint32_t* victims, uint64_t* n_victims);
+void orc_cache_info(orc_cache* c, uint64_t* size, uint32_t* current_mark);
+/* entries sorted by id */
+void orc_cache_export(orc_cache* c, uint32_t* ids, uint8_t* version, uint32_t* mark,
+                      uint32_t* freq, uint64_t* last_access);
+
 /* Cross-check counters: total Dijkstra steps of the last orc_hungarian call. */
 uint64_t orc_last_hungarian_steps(void);
 

@@ -142,6 +142,16 @@ class Oracle:
         L.orc_ref_iteration.argtypes = [vp, P(C.c_uint32), P(u64), u64, C.c_int, P(i32), P(dbl),
                                         P(ReportC), P(dbl)]
         L.orc_last_hungarian_steps.restype = u64
+        L.orc_cache_create.argtypes = [u64, C.c_int, P(vp)]
+        L.orc_cache_destroy.argtypes = [vp]
+        L.orc_cache_touch.argtypes = [vp, C.c_uint32, C.c_int, u64, dbl]
+        L.orc_cache_set_version.argtypes = [vp, C.c_uint32, C.c_int]
+        L.orc_cache_erase.argtypes = [vp, C.c_uint32]
+        L.orc_cache_select_victim.argtypes = [vp, P(C.c_uint32)]
+        L.orc_cache_evict_for.argtypes = [vp, u64, P(C.c_uint32), u64, P(C.c_uint32), P(u64)]
+        L.orc_cache_info.argtypes = [vp, P(u64), P(C.c_uint32)]
+        L.orc_cache_export.argtypes = [vp, P(C.c_uint32), P(C.c_uint8), P(C.c_uint32),
+                                       P(C.c_uint32), P(u64)]
 
     def _check(self, rc):
         if rc != ORC_OK:
@@ -278,6 +288,61 @@ class Oracle:
 
     def sim(self, cfg: Cfg):
         return Sim(self, cfg)
+
+    def cache(self, capacity, policy=0):
+        return Cache(self, capacity, policy)
+
+
+class Cache:
+    """Mirror of a standalone embdispatch::WorkerCache (cache.hpp:73-240)."""
+
+    def __init__(self, o: Oracle, capacity, policy=0):
+        self.o = o
+        self.h = C.c_void_p()
+        o._check(o.lib.orc_cache_create(int(capacity), int(policy), C.byref(self.h)))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.o.lib.orc_cache_destroy(self.h)
+            self.h = None
+
+    def touch(self, id_, latest, now, footprint=1.0):
+        self.o._check(self.o.lib.orc_cache_touch(self.h, int(id_), int(bool(latest)), int(now),
+                                                 float(footprint)))
+
+    def set_version(self, id_, latest):
+        self.o._check(self.o.lib.orc_cache_set_version(self.h, int(id_), int(bool(latest))))
+
+    def erase(self, id_):
+        self.o._check(self.o.lib.orc_cache_erase(self.h, int(id_)))
+
+    def select_victim(self):
+        v = C.c_uint32()
+        self.o._check(self.o.lib.orc_cache_select_victim(self.h, C.byref(v)))
+        return v.value
+
+    def evict_for(self, needed, pinned=()):
+        pins = np.array(sorted(int(x) for x in pinned), np.uint32)
+        out = np.empty(max(int(needed), 1) + 1, np.uint32)
+        cnt = C.c_uint64()
+        self.o._check(self.o.lib.orc_cache_evict_for(self.h, int(needed), _p(pins, C.c_uint32),
+                                                     len(pins), _p(out, C.c_uint32),
+                                                     C.byref(cnt)))
+        return [int(x) for x in out[:cnt.value]]
+
+    def info(self):
+        size, mark = C.c_uint64(), C.c_uint32()
+        self.o.lib.orc_cache_info(self.h, C.byref(size), C.byref(mark))
+        return size.value, mark.value
+
+    def entries(self):
+        """(id, version, mark, freq, last_access) rows sorted by id."""
+        k = self.info()[0]
+        ids, ver = np.empty(k, np.uint32), np.empty(k, np.uint8)
+        mk, fq, la = np.empty(k, np.uint32), np.empty(k, np.uint32), np.empty(k, np.uint64)
+        self.o.lib.orc_cache_export(self.h, _p(ids, C.c_uint32), _p(ver, C.c_uint8),
+                                    _p(mk, C.c_uint32), _p(fq, C.c_uint32), _p(la, C.c_uint64))
+        return [(int(ids[t]), int(ver[t]), int(mk[t]), int(fq[t]), int(la[t])) for t in range(k)]
 
 
 class Sim:

@@ -14,6 +14,7 @@
 // expected_cost (cost.hpp:81); rows are independent, so it is bit-identical
 // ("all host cores" variant).
 
+#include <algorithm>
 #include <chrono>
 #include <cstring>
 #include <exception>
@@ -364,6 +365,65 @@ void orc_sim_cache_marks(orc_sim* s, int32_t worker, uint32_t* current_mark,
 }
 
 uint64_t orc_last_hungarian_steps(void) { return g_steps; }
+
+// Standalone WorkerCache: the reference class itself; the footprint callback
+// reads the value recorded for the id at its touches.
+struct orc_cache {
+  std::unordered_map<EmbeddingId, double> fp;
+  WorkerCache cache;
+  orc_cache(uint64_t cap, int policy)
+      : cache(cap, policy ? VictimPolicy::kPriorityRatio : VictimPolicy::kMarkVersion,
+              [this](EmbeddingId id) {
+                auto it = fp.find(id);
+                return it == fp.end() ? 1.0 : it->second;
+              }) {}
+};
+
+int orc_cache_create(uint64_t capacity, int policy, orc_cache** out) {
+  return guarded([&] { *out = new orc_cache(capacity, policy); });
+}
+void orc_cache_destroy(orc_cache* c) { delete c; }
+int orc_cache_touch(orc_cache* c, uint32_t id, int latest, uint64_t now, double footprint) {
+  return guarded([&] {
+    if (!c->cache.resident(id) && !c->cache.full()) c->fp[id] = footprint;
+    c->cache.touch(id, latest != 0, now);
+  });
+}
+int orc_cache_set_version(orc_cache* c, uint32_t id, int latest) {
+  return guarded([&] { c->cache.set_version(id, latest != 0); });
+}
+int orc_cache_erase(orc_cache* c, uint32_t id) {
+  return guarded([&] { c->cache.erase(id); });
+}
+int orc_cache_select_victim(orc_cache* c, uint32_t* victim) {
+  return guarded([&] { *victim = c->cache.select_victim(); });
+}
+int orc_cache_evict_for(orc_cache* c, uint64_t needed, const uint32_t* pinned, uint64_t n_pinned,
+                        uint32_t* victims, uint64_t* n_victims) {
+  return guarded([&] {
+    WorkerCache::PinnedSet pins(pinned, pinned + n_pinned);
+    const auto ev = c->cache.evict_for(needed, nullptr, n_pinned ? &pins : nullptr);
+    *n_victims = ev.size();
+    for (std::size_t t = 0; t < ev.size(); ++t) victims[t] = ev[t].first;
+  });
+}
+void orc_cache_info(orc_cache* c, uint64_t* size, uint32_t* current_mark) {
+  *size = c->cache.size();
+  *current_mark = c->cache.current_mark();
+}
+void orc_cache_export(orc_cache* c, uint32_t* ids, uint8_t* version, uint32_t* mark,
+                      uint32_t* freq, uint64_t* last_access) {
+  std::vector<CacheEntry> es;
+  for (const auto& [id, e] : c->cache.entries()) es.push_back(e);
+  std::sort(es.begin(), es.end(), [](const CacheEntry& a, const CacheEntry& b) { return a.id < b.id; });
+  for (std::size_t t = 0; t < es.size(); ++t) {
+    ids[t] = es[t].id;
+    version[t] = es[t].version_latest;
+    mark[t] = es[t].mark;
+    freq[t] = es[t].frequency;
+    last_access[t] = es[t].last_access;
+  }
+}
 
 // One reference iteration, timed like run() (sim.hpp:421-441).  times_s gets
 // {snapshot, build, decide, step}; `threads` > 1 partitions build rows.

@@ -41,7 +41,7 @@ __all__ = [
     "make_sample", "to_csr", "build_matrix", "expected_cost", "row_gap_key", "rows_by_gap", "hungarian",
     "hungarian_blocks", "greedy_dispatch", "expand_columns", "ecomix", "decision_cost",
     "exact_multiplicity", "InvalidArgument", "LogicError", "EdxRuntimeError", "CudaError",
-    "EdxError", "EDX_NUM_PHASES",
+    "EdxError", "EDX_NUM_PHASES", "WorkerCache", "VictimPolicy", "CacheEntry",
 ]
 
 _P = C.POINTER
@@ -710,3 +710,97 @@ class ZipfStream:
         if getattr(self, "_h", None):
             lib().edx_zipf_destroy(self._h)
             self._h = None
+
+
+# ------------------------------------------------------- standalone WorkerCache
+class VictimPolicy:
+    """embdispatch::VictimPolicy (cache.hpp:68)."""
+    MARK_VERSION = 0
+    PRIORITY_RATIO = 1
+
+
+@dataclass
+class CacheEntry:
+    """embdispatch::CacheEntry (cache.hpp:36-42)."""
+    id: int
+    version_latest: bool = True
+    mark: int = 1
+    frequency: int = 1
+    last_access: int = 0
+
+
+class WorkerCache:
+    """embdispatch::WorkerCache (cache.hpp:73-240) on the device, driven entry
+    by entry (libedx workercache.cu).  `footprint(id) -> float` feeds the
+    kPriorityRatio policy; `evict_for` returns [(victim, needs_push(victim))]."""
+
+    def __init__(self, capacity: int, policy: int = VictimPolicy.MARK_VERSION, footprint=None,
+                 device: int = 0):
+        self._h = None
+        h = C.c_void_p()
+        check(lib().edx_cache_create(int(capacity), int(policy), int(device), C.byref(h)))
+        self._h = h
+        self._cap = int(capacity)
+        self._footprint = footprint
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().edx_cache_destroy(self._h)
+            self._h = None
+
+    def _info(self):
+        size, mark, at = C.c_uint64(), C.c_uint32(), C.c_uint64()
+        check(lib().edx_cache_info(self._h, C.byref(size), C.byref(mark), C.byref(at)))
+        return size.value, mark.value, at.value
+
+    def capacity(self): return self._cap
+    def size(self): return self._info()[0]
+    def full(self): return self.size() == self._cap
+    def free_slots(self): return self._cap - self.size()
+    def current_mark(self): return self._info()[1]
+    def at_current_mark(self): return self._info()[2]
+    def resident(self, id_): return self.find(id_) is not None
+
+    def find(self, id_):
+        f, v, mk, fq, la = C.c_int(), C.c_int(), C.c_uint32(), C.c_uint32(), C.c_uint64()
+        check(lib().edx_cache_find(self._h, int(id_), C.byref(f), C.byref(v), C.byref(mk),
+                                   C.byref(fq), C.byref(la)))
+        if not f.value:
+            return None
+        return CacheEntry(int(id_), bool(v.value), mk.value, fq.value, la.value)
+
+    def touch(self, id_, latest: bool, now: int):
+        fp = float(self._footprint(int(id_))) if self._footprint else 1.0
+        check(lib().edx_cache_touch(self._h, int(id_), int(bool(latest)), int(now), fp))
+
+    def set_version(self, id_, latest: bool):
+        check(lib().edx_cache_set_version(self._h, int(id_), int(bool(latest))))
+
+    def erase(self, id_):
+        check(lib().edx_cache_erase(self._h, int(id_)))
+
+    def select_victim(self) -> int:
+        out = C.c_uint32()
+        check(lib().edx_cache_select_victim(self._h, C.byref(out)))
+        return out.value
+
+    def evict_for(self, needed: int, needs_push=None, pinned=None):
+        pins = np.array(sorted(int(x) for x in pinned), np.uint32) if pinned else np.zeros(0, np.uint32)
+        out = np.empty(max(self._cap, 1), np.uint32)
+        cnt = C.c_uint64()
+        check(lib().edx_cache_evict_for(self._h, int(needed), _ptr(pins, C.c_uint32), len(pins),
+                                        _ptr(out, C.c_uint32), C.byref(cnt)))
+        return [(int(v), bool(needs_push(int(v))) if needs_push else False)
+                for v in out[:cnt.value]]
+
+    def entries(self):
+        cnt = C.c_uint64()
+        check(lib().edx_cache_export(self._h, None, None, None, None, None, 0, C.byref(cnt)))
+        k = cnt.value
+        ids, ver = np.empty(k, np.uint32), np.empty(k, np.uint8)
+        mk, fq, la = np.empty(k, np.uint32), np.empty(k, np.uint32), np.empty(k, np.uint64)
+        check(lib().edx_cache_export(self._h, _ptr(ids, C.c_uint32), _ptr(ver, C.c_uint8),
+                                     _ptr(mk, C.c_uint32), _ptr(fq, C.c_uint32),
+                                     _ptr(la, C.c_uint64), k, C.byref(cnt)))
+        return {int(ids[t]): CacheEntry(int(ids[t]), bool(ver[t]), int(mk[t]), int(fq[t]),
+                                        int(la[t])) for t in range(k)}

@@ -100,6 +100,16 @@ def _sigs():
         ("edx_build_matrix_sized", cint, [cfgp, u32p, u64p, u64p, u64, u32p, u64p, u64, u64p, dblp]),
         ("edx_expected_costs_sized", cint, [cfgp, u32p, u64p, u64p, u64, u32p, u64p, u64, u64p,
                                             dblp]),
+        ("edx_cache_create", cint, [u64, cint, cint, P(vp)]),
+        ("edx_cache_destroy", None, [vp]),
+        ("edx_cache_touch", cint, [vp, C.c_uint32, cint, u64, C.c_double]),
+        ("edx_cache_set_version", cint, [vp, C.c_uint32, cint]),
+        ("edx_cache_erase", cint, [vp, C.c_uint32]),
+        ("edx_cache_find", cint, [vp, C.c_uint32, P(cint), P(cint), u32p, u32p, u64p]),
+        ("edx_cache_select_victim", cint, [vp, u32p]),
+        ("edx_cache_evict_for", cint, [vp, u64, u32p, u64, u32p, u64p]),
+        ("edx_cache_info", cint, [vp, u64p, u32p, u64p]),
+        ("edx_cache_export", cint, [vp, u32p, P(C.c_uint8), u32p, u32p, u64p, u64, u64p]),
         ("edx_row_gap_key", cint, [u64, u64, dblp, u64, dblp]),
         ("edx_rows_by_gap", cint, [u64, u64, dblp, u64p]),
         ("edx_hungarian", cint, [u64, dblp, u64p, dblp]),

@@ -40,6 +40,27 @@ struct Error : std::runtime_error {
 inline void invalid(const std::string& m) { throw Error(EDX_INVALID_ARGUMENT, m); }
 inline void logic(const std::string& m) { throw Error(EDX_LOGIC_ERROR, m); }
 
+// edx_last_error() storage (engine.cu)
+void set_last_error(const char* m);
+
+// C-ABI wrapper: exceptions -> edx_status + edx_last_error()
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return EDX_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_last_error("out of host memory");
+    return EDX_RUNTIME_ERROR;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return EDX_RUNTIME_ERROR;
+  }
+}
+
 // Device-side error flags (set by kernels, checked by the host after a sync).
 enum DevFlag : int {
   kFlagIdOutOfRange = 0,   // an id >= id_space reached a dense-table kernel

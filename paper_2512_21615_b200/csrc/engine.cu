@@ -41,6 +41,12 @@ int guard(F&& f) {
   }
 }
 
+}  // namespace
+
+void edx::set_last_error(const char* m) { g_err = m; }
+
+namespace {
+
 constexpr int kT = 256;
 unsigned grid_for(uint64_t n) { return static_cast<unsigned>(std::max<uint64_t>(1, (n + kT - 1) / kT)); }
 

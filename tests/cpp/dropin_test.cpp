@@ -225,7 +225,37 @@ static void sized_costs() {
   EXPECT(std::memcmp(v.values.data(), want, sizeof want) == 0, "sized build on a device view");
 }
 
+// test_cache.cpp KATs through the drop-in WorkerCache (device-resident).
+static void worker_cache_kats() {
+  WorkerCache cache(2);
+  cache.touch(1, true, 0);
+  cache.touch(2, true, 0);
+  EXPECT(cache.full() && cache.current_mark() == 1, "full, mark 1");
+  auto ev = cache.evict_for(1, nullptr);
+  EXPECT(cache.current_mark() == 2 && ev.size() == 1, "advance on evict_for");
+  cache.touch(9, true, 1);
+  EXPECT(cache.find(9) && cache.find(9)->mark == 2, "new entry carries mark 2");
+  bool threw = false;
+  try {
+    cache.touch(10, true, 2);
+  } catch (const std::logic_error&) {
+    threw = true;
+  }
+  EXPECT(threw, "touch into a full cache must throw std::logic_error");
+  WorkerCache::PinnedSet pinned{9};
+  ev = cache.evict_for(1, [](EmbeddingId) { return true; }, &pinned);
+  EXPECT(ev.size() == 1 && ev[0].first != 9 && ev[0].second, "pinned skip + needs_push");
+  const auto fp = [](EmbeddingId id) { return id == 1 ? 8.0 : 1.0; };
+  WorkerCache pr(2, VictimPolicy::kPriorityRatio, fp);
+  pr.touch(1, true, 0);
+  pr.touch(2, true, 0);
+  pr.touch(2, true, 0);
+  EXPECT(pr.select_victim() == 1, "priority ratio prefers big cold entries");
+  EXPECT(pr.entries().size() == 2, "entries()");
+}
+
 int main() {
+  worker_cache_kats();
   sized_costs();
   fig2_walkthrough();
   engine_vs_oracle(0.0);

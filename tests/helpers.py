@@ -46,3 +46,65 @@ def random_int_matrix(rows, cols, seed, max_value=100):
     """oracles::random_int_matrix (tests/oracles.hpp:80-95) semantics, numpy RNG."""
     rng = np.random.default_rng(seed)
     return rng.integers(0, max_value + 1, size=(rows, cols)).astype(np.float64)
+
+
+# ------------------------------------------------ standalone WorkerCache ops
+def cache_footprint(id_):
+    """A pure FootprintFn for the kPriorityRatio parity runs."""
+    return 1.0 + float((id_ * 7) % 5) * 0.75
+
+
+def cache_op_stream(seed, capacity, n_ops, id_range):
+    """Random WorkerCache traffic: mostly touches (the reference's own random
+    test, test_cache.cpp:181-191), set_version, erase, select_victim and
+    evict_for with pinned sets -- errors included."""
+    rng = np.random.default_rng(seed)
+    for step in range(n_ops):
+        k = rng.random()
+        id_ = int(rng.integers(0, id_range))
+        if k < 0.55:
+            yield ("touch", id_, bool(rng.integers(0, 2)), int(rng.integers(0, max(step, 1) + 1)))
+        elif k < 0.65:
+            yield ("set_version", id_, bool(rng.integers(0, 2)))
+        elif k < 0.72:
+            yield ("erase", id_)
+        elif k < 0.80:
+            yield ("select_victim",)
+        else:
+            needed = int(rng.integers(0, capacity + 2))
+            pins = [int(x) for x in rng.integers(0, id_range, size=int(rng.integers(0, capacity + 1)))]
+            yield ("evict_for", needed, pins)
+
+
+def _err_kind(e):
+    n = type(e).__name__
+    return ("logic" if "Logic" in n else "invalid" if "Invalid" in n else n, str(e))
+
+
+def apply_cache_op(cache, op, device):
+    """Run one op on a device WorkerCache (device=True) or an oracle Cache;
+    returns its result or ('raised', kind, message)."""
+    try:
+        if op[0] == "touch":
+            if device:
+                return cache.touch(op[1], op[2], op[3])
+            return cache.touch(op[1], op[2], op[3], cache_footprint(op[1]))
+        if op[0] == "set_version":
+            return cache.set_version(op[1], op[2])
+        if op[0] == "erase":
+            return cache.erase(op[1])
+        if op[0] == "select_victim":
+            return cache.select_victim()
+        if op[0] == "evict_for":
+            out = cache.evict_for(op[1], pinned=op[2]) if not device else \
+                cache.evict_for(op[1], None, set(op[2]))
+            return [v[0] for v in out] if device else out
+    except Exception as e:  # noqa: BLE001 - compared against the other side
+        return ("raised",) + _err_kind(e)
+    raise AssertionError(op)
+
+
+def device_cache_rows(cache):
+    es = cache.entries()
+    return [(e.id, int(e.version_latest), e.mark, e.frequency, e.last_access)
+            for _, e in sorted(es.items())]

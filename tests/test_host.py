@@ -207,3 +207,17 @@ def test_oracle_sized_equals_reference(port, ref, pyoracle, n):
     a = port.expected_costs_sized(cfg, snap, ids, offs, sizes)
     b = ref.expected_costs_sized(cfg, snap, ids, offs, sizes)
     assert a.tobytes() == b.tobytes()
+
+
+@pytest.mark.parametrize("policy", [0, 1])
+@pytest.mark.parametrize("seed,capacity,id_range", [(1, 1, 4), (2, 3, 8), (3, 8, 32), (4, 16, 40)])
+def test_oracle_cache_equals_reference(port, ref, policy, seed, capacity, id_range):
+    """The restated standalone WorkerCache (both victim policies) against the
+    reference class on random traffic: every result, error and state."""
+    from helpers import apply_cache_op, cache_op_stream
+    a, b = port.cache(capacity, policy), ref.cache(capacity, policy)
+    for op in cache_op_stream(seed, capacity, 600, id_range):
+        ra, rb = apply_cache_op(a, op, False), apply_cache_op(b, op, False)
+        assert ra == rb, (op, ra, rb)
+        assert a.info() == b.info(), op
+        assert a.entries() == b.entries(), op
