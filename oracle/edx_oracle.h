@@ -153,6 +153,30 @@ void orc_cache_info(orc_cache* c, uint64_t* size, uint32_t* current_mark);
 void orc_cache_export(orc_cache* c, uint32_t* ids, uint8_t* version, uint32_t* mark,
                       uint32_t* freq, uint64_t* last_access);
 
+/* ---- report formats (report_io.hpp; compiled reference only) ---- */
+typedef struct orc_iter_report {
+  uint64_t iteration;
+  const char* mechanism;
+  uint64_t miss_pull, update_push, evict_push, hits, lookups;
+  double cost_s, decision_s, matrix_s, expected_cost_s;
+  int32_t has_expected, n;
+  const uint64_t *miss_pull_w, *update_push_w, *evict_push_w;
+  const double* cost_w;
+} orc_iter_report;
+typedef struct orc_run_summary {
+  const char* mechanism;
+  uint64_t iterations, measured_iterations, miss_pull, update_push, evict_push, hits, lookups;
+  double cost_s, expected_cost_s, decision_s_total, decision_s_max, matrix_s_total;
+  int32_t has_expected, n;
+  uint64_t budget_violations;
+  const uint64_t *miss_pull_w, *update_push_w, *evict_push_w, *ops_w;
+} orc_run_summary;
+/* report_jsonl (report_io.hpp:35-55); *len = bytes needed (out may be NULL) */
+int orc_report_jsonl(const orc_iter_report* rep, char* out, uint64_t cap, uint64_t* len);
+/* comparison_csv (report_io.hpp:89-146) */
+int orc_comparison_csv(const orc_run_summary* runs, uint64_t count, const char* reference,
+                       const orc_cluster_config* cfg, char* out, uint64_t cap, uint64_t* len);
+
 /* Cross-check counters: total Dijkstra steps of the last orc_hungarian call. */
 uint64_t orc_last_hungarian_steps(void);
 

@@ -26,6 +26,7 @@
 
 #include "embdispatch/assign.hpp"
 #include "embdispatch/cost.hpp"
+#include "embdispatch/report_io.hpp"
 #include "embdispatch/sim.hpp"
 #include "embdispatch/workload.hpp"
 
@@ -479,3 +480,65 @@ int orc_ref_iteration(orc_sim* s, const uint32_t* ids, const uint64_t* offsets, 
 }
 
 }  // extern "C"
+
+// report_io.hpp over POD copies of IterationReport / RunSummary.
+namespace {
+void put_string(const std::string& s, char* out, uint64_t cap, uint64_t* len) {
+  *len = s.size();
+  if (out && cap > s.size()) std::memcpy(out, s.c_str(), s.size() + 1);
+}
+}  // namespace
+
+int orc_report_jsonl(const orc_iter_report* r, char* out, uint64_t cap, uint64_t* len) {
+  return guarded([&] {
+    IterationReport rep;
+    rep.iteration = r->iteration;
+    rep.mechanism = r->mechanism;
+    rep.miss_pull = r->miss_pull;
+    rep.update_push = r->update_push;
+    rep.evict_push = r->evict_push;
+    rep.hits = r->hits;
+    rep.lookups = r->lookups;
+    rep.cost_s = r->cost_s;
+    rep.decision_s = r->decision_s;
+    rep.matrix_s = r->matrix_s;
+    rep.expected_cost_s = r->expected_cost_s;
+    rep.has_expected = r->has_expected != 0;
+    rep.miss_pull_w.assign(r->miss_pull_w, r->miss_pull_w + r->n);
+    rep.update_push_w.assign(r->update_push_w, r->update_push_w + r->n);
+    rep.evict_push_w.assign(r->evict_push_w, r->evict_push_w + r->n);
+    rep.cost_w.assign(r->cost_w, r->cost_w + r->n);
+    put_string(report_jsonl(rep), out, cap, len);
+  });
+}
+
+int orc_comparison_csv(const orc_run_summary* runs, uint64_t count, const char* reference,
+                       const orc_cluster_config* c, char* out, uint64_t cap, uint64_t* len) {
+  return guarded([&] {
+    std::vector<RunResult> results(count);
+    for (uint64_t k = 0; k < count; ++k) {
+      const orc_run_summary& r = runs[k];
+      RunSummary& s = results[k].summary;
+      s.mechanism = r.mechanism;
+      s.iterations = r.iterations;
+      s.measured_iterations = r.measured_iterations;
+      s.miss_pull = r.miss_pull;
+      s.update_push = r.update_push;
+      s.evict_push = r.evict_push;
+      s.hits = r.hits;
+      s.lookups = r.lookups;
+      s.cost_s = r.cost_s;
+      s.expected_cost_s = r.expected_cost_s;
+      s.has_expected = r.has_expected != 0;
+      s.decision_s_total = r.decision_s_total;
+      s.decision_s_max = r.decision_s_max;
+      s.matrix_s_total = r.matrix_s_total;
+      s.budget_violations = r.budget_violations;
+      s.miss_pull_w.assign(r.miss_pull_w, r.miss_pull_w + r.n);
+      s.update_push_w.assign(r.update_push_w, r.update_push_w + r.n);
+      s.evict_push_w.assign(r.evict_push_w, r.evict_push_w + r.n);
+      s.ops_w.assign(r.ops_w, r.ops_w + r.n);
+    }
+    put_string(comparison_csv(results, reference, to_cfg(c)), out, cap, len);
+  });
+}
