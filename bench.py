@@ -328,7 +328,7 @@ def product(args, w, rank, world, local_rank):
                               "peak_source": "profiles/r01_dadd_peak.json (tools/dadd_peak.cu)",
                               "note": "second roof of the build (sequential fp64 add chains, "
                                       "SURVEY 8d); adds counted on the first timed batch"}},
-        "dominant_kernel": "k_hungarian_blocks (exact EcoMix block; latency-bound single warp)",
+        "dominant_kernel": ("k_hungarian_blocks_mw (exact EcoMix block; latency-bound, one CTA, warp per block)" if n <= 16 else "k_hungarian_blocks_run (exact EcoMix block; latency-bound, one CTA)"),
         "solver": {"exact_rows": n * int(np.floor(m * w["alpha"] + 1e-9)),
                    "latency_ms_per_batch": phase_ms[2] / K,
                    "dijkstra_steps_last_batch": solver_steps,
