@@ -220,7 +220,7 @@ def product(args, w, rank, world, local_rank):
 
     def one_resident(i):
         eng.load(None, on_device=True, ids_ptr=d_ids[i].data_ptr(), offsets_ptr=d_offs.data_ptr(),
-                 rows=R)
+                 rows=R, total_ids=R * L)
         eng.build(None)
         eng.dispatch(want_decision=False, want_expected=False)
         return eng.step()
@@ -262,7 +262,7 @@ def product(args, w, rank, world, local_rank):
     if world == 1:
         def one_hitgreedy(i):
             eng.load(None, on_device=True, ids_ptr=d_ids[i].data_ptr(),
-                     offsets_ptr=d_offs.data_ptr(), rows=R)
+                     offsets_ptr=d_offs.data_ptr(), rows=R, total_ids=R * L)
             eng.dispatch_hitgreedy(want_decision=False)
         one_hitgreedy(W)
         hg = timed(one_hitgreedy, range(W, W + K))

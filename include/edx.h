@@ -110,6 +110,12 @@ void edx_engine_destroy(edx_engine* e);
  * ids/offsets are device pointers already resident in HBM. */
 int edx_engine_load_batch(edx_engine* e, const uint32_t* ids, const uint64_t* offsets,
                           uint64_t num_samples, int on_device);
+/* A batch already in device memory whose id count the caller knows: no host
+ * round trip (edx_engine_load_batch with on_device=1 reads the offsets back).
+ * offsets[0] == 0 and offsets[num_samples] == total_ids are checked on the
+ * device and reported by the next synchronising call. */
+int edx_engine_load_device_batch(edx_engine* e, const uint32_t* ids, const uint64_t* offsets,
+                                 uint64_t num_samples, uint64_t total_ids);
 /* build_matrix(samples, snapshot(), cfg) — cost.hpp:105-125 over the live
  * device state (SimState::snapshot, sim.hpp:71-82, costs nothing here).
  * matrix_out (rows*n doubles) may be NULL to keep the matrix on device. */

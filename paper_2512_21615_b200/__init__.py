@@ -491,10 +491,18 @@ class SimState:
         return self.cfg
 
     # -- batch-level calls
-    def load(self, samples, on_device: bool = False, ids_ptr=None, offsets_ptr=None, rows=None):
+    def load(self, samples, on_device: bool = False, ids_ptr=None, offsets_ptr=None, rows=None,
+             total_ids=None):
+        """Host samples (CSR or list of id lists), or a device batch by pointer; a
+        device batch with `total_ids` given is loaded without a host round trip."""
         if on_device:
-            check(lib().edx_engine_load_batch(self._h, C.c_void_p(ids_ptr), C.c_void_p(offsets_ptr),
-                                              int(rows), 1))
+            if total_ids is not None:
+                check(lib().edx_engine_load_device_batch(self._h, C.c_void_p(ids_ptr),
+                                                         C.c_void_p(offsets_ptr), int(rows),
+                                                         int(total_ids)))
+            else:
+                check(lib().edx_engine_load_batch(self._h, C.c_void_p(ids_ptr),
+                                                  C.c_void_p(offsets_ptr), int(rows), 1))
             return
         ids, offs = to_csr(samples)
         self._batch = (ids, offs)

@@ -76,6 +76,7 @@ def _sigs():
         ("edx_engine_create", cint, [cfgp, P(EngineOptionsC), P(vp)]),
         ("edx_engine_destroy", None, [vp]),
         ("edx_engine_load_batch", cint, [vp, vp, vp, u64, cint]),
+        ("edx_engine_load_device_batch", cint, [vp, vp, vp, u64, u64]),
         ("edx_engine_build", cint, [vp, dblp]),
         ("edx_engine_dispatch", cint, [vp, dbl, i32p, dblp]),
         ("edx_engine_dispatch_hitgreedy", cint, [vp, i32p]),

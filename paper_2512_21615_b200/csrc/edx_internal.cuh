@@ -69,6 +69,7 @@ enum DevFlag : int {
   kFlagUnbalanced = 3,     // a dispatch decision broke the m-per-worker balance
   kFlagKeyRange = 4,       // victim-key fields exceed the 57-bit packing
   kFlagInternal = 5,       // internal launch-configuration error (bug)
+  kFlagBadBatch = 6,       // a device batch's offsets disagree with its declared id count
   kFlagCount = 8
 };
 

@@ -83,6 +83,15 @@ void check_flags_host(const int* f) {
   if (f[edx::kFlagInternal]) throw Error(EDX_RUNTIME_ERROR, "internal error: solver shared-memory layout");
   if (f[edx::kFlagKeyRange])
     throw Error(EDX_RUNTIME_ERROR, "victim key fields exceed the 57-bit device packing");
+  if (f[edx::kFlagBadBatch])
+    edx::invalid("device offsets must start at 0 and end at the declared id count");
+}
+
+// device batch with a declared id count: offsets[0] == 0 and offsets[R] == total,
+// checked on the device (no host round trip), reported at the next sync
+__global__ void k_check_batch(const uint64_t* __restrict__ offsets, uint64_t R, uint64_t total,
+                              int* flags) {
+  if (offsets[0] != 0 || offsets[R] != total) atomicOr(flags + edx::kFlagBadBatch, 1);
 }
 
 // ------------------------------------------------------- small kernels
@@ -310,10 +319,16 @@ void rec(edx_engine* e, int idx, cudaStream_t s) {
 }
 
 void engine_load(edx_engine* e, const uint32_t* ids, const uint64_t* offsets, uint64_t R,
-                 int on_device) {
+                 int on_device, uint64_t declared_total = UINT64_MAX) {
   if (R == 0) edx::invalid("batch holds no samples");
   uint64_t total;
-  if (on_device) {
+  if (on_device && declared_total != UINT64_MAX) {
+    total = declared_total;
+    k_check_batch<<<1, 1, 0, e->stream>>>(offsets, R, total, e->flags.p);
+    EDX_LAUNCHED();
+    e->cur_ids = ids;
+    e->cur_offsets = offsets;
+  } else if (on_device) {
     uint64_t ends[2];
     EDX_CUDA(cudaMemcpyAsync(&ends[0], offsets, sizeof(uint64_t), cudaMemcpyDeviceToHost, e->stream));
     EDX_CUDA(cudaMemcpyAsync(&ends[1], offsets + R, sizeof(uint64_t), cudaMemcpyDeviceToHost, e->stream));
@@ -598,6 +613,14 @@ int edx_engine_load_batch(edx_engine* e, const uint32_t* ids, const uint64_t* of
   return guard([&] {
     EDX_CUDA(cudaSetDevice(e->device));
     engine_load(e, ids, offsets, num_samples, on_device);
+  });
+}
+
+int edx_engine_load_device_batch(edx_engine* e, const uint32_t* ids, const uint64_t* offsets,
+                                 uint64_t num_samples, uint64_t total_ids) {
+  return guard([&] {
+    EDX_CUDA(cudaSetDevice(e->device));
+    engine_load(e, ids, offsets, num_samples, 1, total_ids);
   });
 }
 

@@ -213,3 +213,39 @@ def test_engine_64_workers(gpu, oracle, pyoracle):
             assert eng.step().as_dict() == sim.step(ids, offs, want_d), f"alpha {alpha} iter {it}"
         msg = canon_equal(eng.canonical_state(), sim.canonical_state())
         assert not msg, msg
+
+
+def test_device_batch_declared_total(gpu, oracle, pyoracle):
+    """edx_engine_load_device_batch: a device-resident batch with its id count
+    declared (no host round trip) gives the same iteration as a host load; a
+    wrong count fails loudly at the next synchronising call."""
+    import torch
+    edx = gpu
+    p = CONFIGS["P8"]
+    n, m, L = p["n"], p["m"], p["L"]
+    R = n * m
+    c = edx.ClusterConfig(n=n, m=m, bandwidths_bps=p["bw"], cache_capacity=p["cap"], alpha=0.5)
+    a = edx.SimState(c, id_space=p["V"], max_batch_ids=R * L)
+    b = edx.SimState(c, id_space=p["V"], max_batch_ids=R * L)
+    offs = offsets_for(R, L)
+    d_offs = torch.from_numpy(offs.view(np.int64)).cuda()
+    for ids in oracle.zipf_batches(p["V"], L, 1.05, 6, 3, R):
+        d_ids = torch.from_numpy(ids.view(np.int32)).cuda()
+        torch.cuda.synchronize()
+        a.load(None, on_device=True, ids_ptr=d_ids.data_ptr(), offsets_ptr=d_offs.data_ptr(), rows=R,
+               total_ids=R * L)
+        ma = np.empty((R, n))
+        a.build(ma)
+        da, _ = a.dispatch()
+        ra = a.step().as_dict()
+        b.load((ids, offs))
+        mb = np.empty((R, n))
+        b.build(mb)
+        db, _ = b.dispatch()
+        rb = b.step().as_dict()
+        assert ma.tobytes() == mb.tobytes() and (da == db).all() and ra == rb
+    torch.cuda.synchronize()
+    a.load(None, on_device=True, ids_ptr=d_ids.data_ptr(), offsets_ptr=d_offs.data_ptr(), rows=R,
+           total_ids=R * L - 1)
+    with pytest.raises(edx.InvalidArgument, match="declared id count"):
+        a.build(np.empty((R, n)))
