@@ -1626,8 +1626,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
 // orders start as the identity and a potential update keeps each block sorted
 // (see the re-sort check), so ord is only consulted after a fallback sort.
 
-template <int AMODE, int MAXW>  // AMODE 0: S and A shared; 1: S global, A shared; 2: S and A global
-__global__ void __launch_bounds__(MAXW * 32, 1)
+template <int AMODE, int MAXW, int BPW>  // AMODE 0: S and A shared; 1: S global, A shared; 2: S and A global
+__global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks per warp (1, or 2 for n <= 32)
     k_hungarian_blocks_mw(const int64_t* __restrict__ S_global, int n, int mult, int k,
                           int64_t* __restrict__ A_global, const uint32_t* __restrict__ order,
                           int32_t* __restrict__ decision, const uint32_t* __restrict__ row_ids,
@@ -1715,7 +1715,16 @@ __global__ void __launch_bounds__(MAXW * 32, 1)
   __syncthreads();
 
   constexpr int64_t kBig = 1LL << 62;
-  const int x = warp;  // this warp's block
+  // this warp's blocks: warp, warp + nw (BPW == 2); xa is a valid table column
+  int xs[BPW], xa[BPW];
+  bool own[BPW];
+#pragma unroll
+  for (int h = 0; h < BPW; ++h) {
+    xs[h] = warp + h * nw;
+    own[h] = xs[h] < n;
+    xa[h] = own[h] ? xs[h] : 0;
+    if (!own[h]) xs[h] = 63;  // matches no winner
+  }
   int par = 0;         // publish slot parity (identical in every warp)
   unsigned mbph = 0;   // mbarrier phase parity
   unsigned long long steps = 0;
@@ -1738,7 +1747,9 @@ __global__ void __launch_bounds__(MAXW * 32, 1)
       Gy = (S[static_cast<size_t>(i - 1) * n + lane] - u[i]) << 6;  // relax from row i
       By = Btab[ordid ? lane * mult + 1 : ord[lane * mult]];
     }
-    int wyx = 0;
+    int wyx[BPW];
+#pragma unroll
+    for (int h = 0; h < BPW; ++h) wyx[h] = 0;
     if (tid == 0) {
       p[0] = i;
       L[0] = make_int4(i << 16, 0, 0, 0);
@@ -1760,40 +1771,52 @@ __global__ void __launch_bounds__(MAXW * 32, 1)
       const int base = ws * mult + dws;  // position of the winner's candidate c_1
       const int Tm = mult - dws;
       const int64_t delta1 = static_cast<int64_t>(((static_cast<uint64_t>(mh) << 32) | ml) & ~63ULL);
-      int64_t Gx = __shfl_sync(0xffffffffu, Gy, x);
-      const int64_t Bx = __shfl_sync(0xffffffffu, By, x);
+      int64_t Gx[BPW], Bx[BPW];
+#pragma unroll
+      for (int h = 0; h < BPW; ++h) {
+        Gx[h] = __shfl_sync(0xffffffffu, Gy, xs[h]);
+        Bx[h] = __shfl_sync(0xffffffffu, By, xs[h]);
+      }
       int64_t P = Q;
       int sN = 0;
       const int nused0 = nused;
       // Chunk operands, lanes = steps: column, its row, key offset, A[winner],
-      // A[own]; then the chunk's scan over (sum of deltas, min of relax
+      // A[own blocks]; then the chunk's scan over (sum of deltas, min of relax
       // candidates) with the pair monoid (S, M).(S', M') = (S + S', min(M, S + M')),
-      // relative to the carry P.  The next chunk's operands and scan are
-      // computed speculatively while this chunk's fail masks are exchanged.
-      auto load = [&](int s0, int& c, int& r, int64_t& Bc, int64_t& Aw, int64_t& Ax) {
+      // relative to the carry P (one S, one M per own block).  The next chunk's
+      // operands and scan are computed speculatively while this chunk's fail masks
+      // are exchanged.
+      auto load = [&](int s0, int& c, int& r, int64_t& Bc, int64_t& Aw, int64_t (&Ax)[BPW]) {
         const int q = base + min(s0 + lane, Tm - 1);
         c = ordid ? q + 1 : ord[q];
         Bc = Btab[c];
         r = rtab[c];
         Aw = A[static_cast<size_t>(c - 1) * n + ws];
-        Ax = A[static_cast<size_t>(c - 1) * n + x];
+#pragma unroll
+        for (int h = 0; h < BPW; ++h) Ax[h] = A[static_cast<size_t>(c - 1) * n + xa[h]];
       };
-      auto scan = [&](int64_t dl, int64_t Ax, int64_t& Ss, int64_t& M) {
+      auto scan = [&](int64_t dl, const int64_t (&Ax)[BPW], int64_t& Ss, int64_t (&M)[BPW]) {
         Ss = dl;
-        M = Ax + dl;
+#pragma unroll
+        for (int h = 0; h < BPW; ++h) M[h] = Ax[h] + dl;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
           const int64_t ys = __shfl_up_sync(0xffffffffu, Ss, off);
-          const int64_t ym = __shfl_up_sync(0xffffffffu, M, off);
+          int64_t ym[BPW];
+#pragma unroll
+          for (int h = 0; h < BPW; ++h) ym[h] = __shfl_up_sync(0xffffffffu, M[h], off);
           if (lane >= off) {
-            const int64_t t = ys + M;
-            M = ym < t ? ym : t;
+#pragma unroll
+            for (int h = 0; h < BPW; ++h) {
+              const int64_t t = ys + M[h];
+              M[h] = ym[h] < t ? ym[h] : t;
+            }
             Ss += ys;
           }
         }
       };
       int c, r;
-      int64_t Bc, Aw, Ax, Ss, M;
+      int64_t Bc, Aw, Ax[BPW], Ss, M[BPW];
       load(0, c, r, Bc, Aw, Ax);
       int64_t V6 = static_cast<int64_t>(ws) - Bc;
       {
@@ -1806,24 +1829,36 @@ __global__ void __launch_bounds__(MAXW * 32, 1)
         const int cnt = min(32, Tm - sN);
         const bool live = lane < cnt;
         const bool first = sN == 0 && lane == 0;
-        const int64_t Qt = P + Ss;     // cumulative delta after this step
-        const int64_t cand = Ax + Qt;  // relax candidate of this step for block x
-        const int64_t Mp = P + __shfl_up_sync(0xffffffffu, M, 1);
-        const int64_t Gb = lane == 0 ? Gx : (Mp < Gx ? Mp : Gx);  // G before the step
-        const int64_t Ga = cand < Gb ? cand : Gb;                  // G after its relax
-        const bool fail = x != ws && !(Gb + Bx - ws > Qt);         // block x would win here
-        const unsigned failx = __ballot_sync(0xffffffffu, live && !first && fail);
-        const unsigned impm = __ballot_sync(0xffffffffu, live && cand < Gb);
+        const int64_t Qt = P + Ss;  // cumulative delta after this step
+        bool failany = false;
+        unsigned impm[BPW];
+        int64_t Ga[BPW];
+#pragma unroll
+        for (int h = 0; h < BPW; ++h) {
+          const int64_t cand = Ax[h] + Qt;  // relax candidate of this step for block xs[h]
+          const int64_t Mp = P + __shfl_up_sync(0xffffffffu, M[h], 1);
+          const int64_t Gb = lane == 0 ? Gx[h] : (Mp < Gx[h] ? Mp : Gx[h]);  // G before the step
+          Ga[h] = cand < Gb ? cand : Gb;                                     // G after its relax
+          failany |= own[h] && xs[h] != ws && !(Gb + Bx[h] - ws > Qt);      // block would win here
+          impm[h] = __ballot_sync(0xffffffffu, live && cand < Gb);
+        }
+        const unsigned failx = __ballot_sync(0xffffffffu, live && !first && failany);
         const unsigned freem = __ballot_sync(0xffffffffu, live && r == 0);
-        if (lane == 0) pfail[par * 32 + x] = failx;
-        GA[(par * 32 + x) * 32 + lane] = Ga;
+        if (lane == 0) pfail[par * 32 + warp] = failx;
+#pragma unroll
+        for (int h = 0; h < BPW; ++h)
+          if (own[h]) GA[(par * 32 + xs[h]) * 32 + lane] = Ga[h];
         mbar_arrive(mbar);
         // speculative next chunk (this one complete, the run continuing)
         const bool more = sN + 32 < Tm;
         const int64_t P31 = __shfl_sync(0xffffffffu, Qt, 31);
-        const int64_t G31 = __shfl_sync(0xffffffffu, Ga, 31);
+        int64_t G31[BPW];
+#pragma unroll
+        for (int h = 0; h < BPW; ++h) G31[h] = __shfl_sync(0xffffffffu, Ga[h], 31);
         int c2 = 0, r2 = 0;
-        int64_t Bc2 = kBig, Aw2 = 0, Ax2 = 0, V62 = 0, Ss2 = 0, M2 = 0;
+        int64_t Bc2 = kBig, Aw2 = 0, Ax2[BPW], V62 = 0, Ss2 = 0, M2[BPW];
+#pragma unroll
+        for (int h = 0; h < BPW; ++h) Ax2[h] = M2[h] = 0;
         if (more) {
           load(sN + 32, c2, r2, Bc2, Aw2, Ax2);
           V62 = static_cast<int64_t>(ws) - Bc2;
@@ -1839,7 +1874,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1)
         }
         mbar_wait(mbar, mbph);
         mbph ^= 1u;
-        const unsigned failm = __reduce_or_sync(0xffffffffu, lane < n ? pfail[par * 32 + lane] : 0u);
+        const unsigned failm = __reduce_or_sync(0xffffffffu, lane < nw ? pfail[par * 32 + lane] : 0u);
         const int failq = failm ? __ffs(failm) - 1 : 32;
         const int freeq = freem ? __ffs(freem) - 1 : 32;
         int vq = failq < cnt ? failq : cnt;
@@ -1849,35 +1884,45 @@ __global__ void __launch_bounds__(MAXW * 32, 1)
         }
         const unsigned relax_m = freeq < 32 ? ((1u << freeq) - 1u) : 0xffffffffu;  // no relax at a free column
         const int wbase = nused0 + sN;
-        if (x == ws && lane < vq) {  // the winner warp commits: each lane its own step
-          const unsigned prev = impm & relax_m & ((1u << lane) - 1u);
-          const int64_t dq = Qt >> 6;
-          L[wbase + lane] = make_int4(c | (r << 16), prev ? wbase + 31 - __clz(prev) : wyx,
-                                      static_cast<int>(static_cast<uint32_t>(dq)),
-                                      static_cast<int>(dq >> 32));
+#pragma unroll
+        for (int h = 0; h < BPW; ++h) {
+          if (xs[h] == ws && lane < vq) {  // the winner's warp commits: each lane its own step
+            const unsigned prev = impm[h] & relax_m & ((1u << lane) - 1u);
+            const int64_t dq = Qt >> 6;
+            L[wbase + lane] = make_int4(c | (r << 16), prev ? wbase + 31 - __clz(prev) : wyx[h],
+                                        static_cast<int>(static_cast<uint32_t>(dq)),
+                                        static_cast<int>(dq >> 32));
+          }
         }
         sN += vq;
         if (vq == 32 && !phase_end && more) {  // the whole chunk held: continue the run
           P = P31;
-          Gx = G31;
-          wyx = impm ? wbase + 31 - __clz(impm) : wyx;
+#pragma unroll
+          for (int h = 0; h < BPW; ++h) {
+            Gx[h] = G31[h];
+            wyx[h] = impm[h] ? wbase + 31 - __clz(impm[h]) : wyx[h];
+            Ax[h] = Ax2[h];
+            M[h] = M2[h];
+          }
           par ^= 1;
           c = c2;
           r = r2;
           Bc = Bc2;
           Aw = Aw2;
-          Ax = Ax2;
           V6 = V62;
           Ss = Ss2;
-          M = M2;
           continue;
         }
         // run end: carry, way, every block's G after the run's last step
         // (vq == 0 only after a full chunk, whose slot is still intact)
         if (vq > 0) {
           P = __shfl_sync(0xffffffffu, Qt, vq - 1);
-          const unsigned m2 = impm & relax_m & (vq >= 32 ? 0xffffffffu : ((1u << vq) - 1u));
-          wyx = m2 ? wbase + 31 - __clz(m2) : wyx;
+          const unsigned lowv = vq >= 32 ? 0xffffffffu : ((1u << vq) - 1u);
+#pragma unroll
+          for (int h = 0; h < BPW; ++h) {
+            const unsigned m2 = impm[h] & relax_m & lowv;
+            wyx[h] = m2 ? wbase + 31 - __clz(m2) : wyx[h];
+          }
         }
         if (lane < n)
           Gy = vq > 0 ? GA[(par * 32 + lane) * 32 + vq - 1] : GA[((par ^ 1) * 32 + lane) * 32 + 31];
@@ -1955,7 +2000,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1)
     // (the predecessor's entry carries its column and old row); the path
     // columns change rows, so the warp also rewrites their tables.
     const unsigned untouched = __ballot_sync(0xffffffffu, lane < n && curs[lane] == 0);
-    const int aug_warp = untouched ? __ffs(untouched) - 1 : 0;
+    const int aug_warp = untouched ? (__ffs(untouched) - 1) % nw : 0;
     if (warp == aug_warp) {
       int4 ent = L[nu - 1];
       for (;;) {
@@ -2249,9 +2294,11 @@ void launch_hungarian_blocks(HungarianScratch& sc, const double* matrix, int n,
     if (std::strcmp(e, "run") == 0) return 2;
     return 0;
   }();
-  // the multi-warp kernel for n <= 16 (at n = 32 the run kernel is faster:
-  // 32 warps per exchange cost more than the per-block work they split)
-  if (solver_pref == 0 && n <= 16 && mult <= 512) {
+  // the multi-warp kernel: one warp per block for n <= 16, one warp per two
+  // blocks (16 warps) for 16 < n <= 32 -- one warp per block at n = 32 costs
+  // more in the 32-way exchange than the per-block work it splits
+  if (solver_pref == 0 && n <= 32 && mult <= 512) {
+    const int nwarps = n <= 16 ? n : 16;
     for (int am = 0; am <= 2; ++am) {
       const size_t smem = mw_smem_bytes(k, n, mult, am);
       if (smem > limit) continue;
@@ -2264,18 +2311,22 @@ void launch_hungarian_blocks(HungarianScratch& sc, const double* matrix, int n,
         if (smem > 48 * 1024)
           EDX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem)));
-        kern<<<1, 32 * n, smem, s>>>(sc.s64.p, n, mult, k, Ag, order, decision, row_ids,
-                                     col_of_row, sc.steps.p, flags, max_scaled);
+        kern<<<1, 32 * nwarps, smem, s>>>(sc.s64.p, n, mult, k, Ag, order, decision, row_ids,
+                                          col_of_row, sc.steps.p, flags, max_scaled);
       };
-      // the warp cap sets the register budget: 255 (n <= 8), 128 (n <= 16)
+      // the warp cap sets the register budget: 255 (n <= 8), 128 (n <= 32)
       if (n <= 8) {
-        if (am == 0) launch(k_hungarian_blocks_mw<0, 8>);
-        else if (am == 1) launch(k_hungarian_blocks_mw<1, 8>);
-        else launch(k_hungarian_blocks_mw<2, 8>);
+        if (am == 0) launch(k_hungarian_blocks_mw<0, 8, 1>);
+        else if (am == 1) launch(k_hungarian_blocks_mw<1, 8, 1>);
+        else launch(k_hungarian_blocks_mw<2, 8, 1>);
+      } else if (n <= 16) {
+        if (am == 0) launch(k_hungarian_blocks_mw<0, 16, 1>);
+        else if (am == 1) launch(k_hungarian_blocks_mw<1, 16, 1>);
+        else launch(k_hungarian_blocks_mw<2, 16, 1>);
       } else {
-        if (am == 0) launch(k_hungarian_blocks_mw<0, 16>);
-        else if (am == 1) launch(k_hungarian_blocks_mw<1, 16>);
-        else launch(k_hungarian_blocks_mw<2, 16>);
+        if (am == 0) launch(k_hungarian_blocks_mw<0, 16, 2>);
+        else if (am == 1) launch(k_hungarian_blocks_mw<1, 16, 2>);
+        else launch(k_hungarian_blocks_mw<2, 16, 2>);
       }
       EDX_LAUNCHED();
       return;

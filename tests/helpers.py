@@ -13,6 +13,9 @@ CONFIGS = {
     "P2": dict(n=2, m=4, bw=[5e9, 5e8], cap=12, V=60, L=3),
     "P3": dict(n=3, m=4, bw=[5e9, 5e9, 5e8], cap=14, V=80, L=3),
     "P8": dict(n=8, m=16, bw=HET(8), cap=120, V=400, L=6),
+    # 16 < n <= 32: the two-blocks-per-warp exact solver
+    "P24": dict(n=24, m=16, bw=HET(24), cap=160, V=1500, L=5),
+    "P32": dict(n=32, m=12, bw=HET(32), cap=120, V=2000, L=4),
     # mass eviction: > 4096 victims per worker per step (the full-sort victim path)
     "PX": dict(n=2, m=64, bw=[5e9, 5e8], cap=12_000, V=500_000, L=100),
 }

@@ -135,6 +135,12 @@ def test_engine_mass_eviction(gpu, oracle, pyoracle, s):
     run_parity(gpu, oracle, pyoracle, "PX", 0.0, 6, seed=11, s=s)
 
 
+@pytest.mark.parametrize("name,alpha", [("P24", 0.5), ("P32", 1.0), ("P32", 0.25)])
+def test_engine_wide_exact_block(gpu, oracle, pyoracle, name, alpha):
+    """16 < n <= 32 engines through the hybrid dispatcher (two blocks per warp)."""
+    run_parity(gpu, oracle, pyoracle, name, alpha, 15, seed=21)
+
+
 def test_engine_c1(gpu, oracle, pyoracle):
     """C1: 4 workers, batch 1024, uniform, 10% cache, greedy only."""
     run_parity(gpu, oracle, pyoracle, "C1", 0.0, 30, check_state_every=10)

@@ -293,6 +293,10 @@ def test_hungarian_bench_matrix(gpu, oracle, k):
                                                (16, 16, 50, 3.2768e-6), (33, 4, 20, 3.2768e-6),
                                                (64, 2, 7, 3.2768e-6), (8, 64, 1000, 3.2768e-6),
                                                (40, 8, 9, 3.2768e-6), (32, 32, 100, 3.2768e-6),
+                                               # two blocks per warp (16 < n <= 32), incl. runs
+                                               # longer than one 32-step chunk
+                                               (17, 8, 30, 3.2768e-6), (24, 16, 5, 3.2768e-6),
+                                               (20, 64, 3, 3.2768e-6), (31, 40, 1000, 3.2768e-6),
                                                # magnitudes beyond the packed-key range: wide path
                                                (8, 16, 1000, 4.0), (40, 4, 50, 100.0)])
 def test_hungarian_blocks_equals_expanded(gpu, oracle, n, mult, maxv, scale):
