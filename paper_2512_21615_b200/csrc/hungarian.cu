@@ -2297,8 +2297,13 @@ void launch_hungarian_blocks(HungarianScratch& sc, const double* matrix, int n,
   // the multi-warp kernel: one warp per block for n <= 16, one warp per two
   // blocks (16 warps) for 16 < n <= 32 -- one warp per block at n = 32 costs
   // more in the 32-way exchange than the per-block work it splits
+  static const int bpw_pref = [] {  // EDX_MW_BPW=2: two blocks per warp also for n <= 16 (A/B)
+    const char* e = std::getenv("EDX_MW_BPW");
+    return e && std::strcmp(e, "2") == 0 ? 2 : 1;
+  }();
   if (solver_pref == 0 && n <= 32 && mult <= 512) {
-    const int nwarps = n <= 16 ? n : 16;
+    const bool pair = n > 16 || (bpw_pref == 2 && n > 1);
+    const int nwarps = pair ? (n + 1) / 2 : n;
     for (int am = 0; am <= 2; ++am) {
       const size_t smem = mw_smem_bytes(k, n, mult, am);
       if (smem > limit) continue;
@@ -2315,7 +2320,11 @@ void launch_hungarian_blocks(HungarianScratch& sc, const double* matrix, int n,
                                           col_of_row, sc.steps.p, flags, max_scaled);
       };
       // the warp cap sets the register budget: 255 (n <= 8), 128 (n <= 32)
-      if (n <= 8) {
+      if (pair && n <= 16) {
+        if (am == 0) launch(k_hungarian_blocks_mw<0, 8, 2>);
+        else if (am == 1) launch(k_hungarian_blocks_mw<1, 8, 2>);
+        else launch(k_hungarian_blocks_mw<2, 8, 2>);
+      } else if (n <= 8) {
         if (am == 0) launch(k_hungarian_blocks_mw<0, 8, 1>);
         else if (am == 1) launch(k_hungarian_blocks_mw<1, 8, 1>);
         else launch(k_hungarian_blocks_mw<2, 8, 1>);
