@@ -73,7 +73,12 @@ __global__ void k_first_pos(const uint32_t* __restrict__ ids, uint64_t T,
                             int32_t* __restrict__ first_pos) {
   const uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (p >= T) return;
-  atomicMin(first_pos + ids[p], static_cast<int32_t>(p));
+  // Zipf-hot ids occur in thousands of samples: test before the atomic.  The
+  // table only decreases, so a stale read is >= the true minimum -- skipping
+  // when it is already <= p is exact -- and CTAs run roughly in position
+  // order, so a hot id's minimum is in place after its first few occurrences.
+  int32_t* slot = first_pos + ids[p];
+  if (*slot > static_cast<int32_t>(p)) atomicMin(slot, static_cast<int32_t>(p));
 }
 
 __global__ void k_unique_flag(const uint32_t* __restrict__ ids, uint64_t T,
@@ -106,9 +111,10 @@ __global__ void k_needs(const uint32_t* __restrict__ ids, uint64_t T,
   const int j = decision[occ_sample[p]];
   const uint32_t u = uidx[first_pos[ids[p]]];
   const uint64_t x = static_cast<uint64_t>(j) * ucap + u;
-  atomicMin(need_first + x, static_cast<int32_t>(p));
+  // test before the atomics (monotone tables, see k_first_pos)
+  if (need_first[x] > static_cast<int32_t>(p)) atomicMin(need_first + x, static_cast<int32_t>(p));
   atomicAdd(need_cnt + x, 1u);
-  atomicOr(umask + u, 1ULL << j);
+  if (!((umask[u] >> j) & 1ULL)) atomicOr(umask + u, 1ULL << j);
 }
 
 // first occurrence of (worker, id) -> sortable key (worker << 32 | position)
@@ -122,12 +128,13 @@ __global__ void k_need_keys(const uint32_t* __restrict__ ids, uint64_t T,
   if (p >= T) return;
   const int j = decision[occ_sample[p]];
   const uint32_t u = uidx[first_pos[ids[p]]];
-  if (need_first[static_cast<uint64_t>(j) * ucap + u] == static_cast<int32_t>(p)) {
-    keys[p] = (static_cast<uint64_t>(j) << 32) | p;
-    atomicAdd(ws + j * kWS + kWsNeeds, 1u);
-  } else {
-    keys[p] = ~0ULL;
-  }
+  const bool first = need_first[static_cast<uint64_t>(j) * ucap + u] == static_cast<int32_t>(p);
+  keys[p] = first ? ((static_cast<uint64_t>(j) << 32) | p) : ~0ULL;
+  // per-worker need count: lanes of one sample share the worker, so one
+  // atomic per (warp, worker) group
+  const unsigned act = __activemask();
+  const unsigned grp = __match_any_sync(act, first ? j : -1 - j);
+  if (first && (threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(ws + j * kWS + kWsNeeds, __popc(grp));
 }
 
 // Phase 1: on-demand update push (sim.hpp:119-153).  set_version(false) on
