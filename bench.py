@@ -218,7 +218,11 @@ def product(args, w, rank, world, local_rank):
     d_offs = torch.from_numpy(offs.view(np.int64)).to(dev)
     torch.cuda.synchronize()
 
-    def one_resident(i):
+    def one_resident(i):  # the reference's run() body as one fused call (a CUDA-graph replay)
+        return eng.iterate_device(d_ids[i].data_ptr(), d_offs.data_ptr(), R, R * L,
+                                  want_decision=False, want_expected=False)
+
+    def one_profiled(i):  # the same iteration phase by phase, CUDA events per phase
         eng.load(None, on_device=True, ids_ptr=d_ids[i].data_ptr(), offsets_ptr=d_offs.data_ptr(),
                  rows=R, total_ids=R * L)
         eng.build(None)
@@ -242,7 +246,6 @@ def product(args, w, rank, world, local_rank):
         one_resident(i)
     # FP64 adds of the first timed build, from the state it reads (untimed)
     f_alg = fp64_adds(w, seg[W], eng.global_masks()) if world == 1 else None
-    eng.set_profiling(True)
     eng.phase_times(reset=True)
     with ClockSampler(local_rank) as clk:
         if world > 1:
@@ -250,9 +253,14 @@ def product(args, w, rank, world, local_rank):
         torch.cuda.synchronize()
         ms = timed(one_resident, range(W, W + K))
         torch.cuda.synchronize()
+    _, counts = eng.phase_times(reset=True)
+    launches = int(counts[0])
+    # phase breakdown (not part of `value`): the next iterations, phase by phase
+    eng.set_profiling(True)
+    eng.phase_times(reset=True)
+    timed(one_profiled, range(W, W + K))
     phase_ms, counts = eng.phase_times(reset=True)
     eng.set_profiling(False)
-    launches = int(counts[0])
     solver_steps = int(counts[1])
     step_ms = sum(ms) / K
 
@@ -333,6 +341,8 @@ def product(args, w, rank, world, local_rank):
                    "latency_ms_per_batch": phase_ms[2] / K,
                    "dijkstra_steps_last_batch": solver_steps,
                    "ns_per_step": (phase_ms[2] / K) * 1e6 / solver_steps if solver_steps else None},
+        "phases_note": "per-phase CUDA events on a separate profiled pass (phase-by-phase calls); "
+                       "the timed value runs each iteration as one CUDA-graph replay",
         "phases_ms_per_step": {"build": phase_ms[0] / K, "gap_sort": phase_ms[1] / K,
                                "exact_solve": phase_ms[2] / K, "greedy": phase_ms[3] / K,
                                "cache_update": phase_ms[4] / K, "dispatch_total": phase_ms[5] / K},

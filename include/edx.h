@@ -144,6 +144,13 @@ int edx_engine_iterate(edx_engine* e, const uint32_t* ids, const uint64_t* offse
 int edx_engine_stream(edx_engine* e, void** stream);
 
 /* SimState::seed_entry — sim.hpp:252-261 (test hook). */
+/* edx_engine_iterate for a batch already in device memory whose id count the
+ * caller knows (see edx_engine_load_device_batch): the batch is staged into the
+ * engine's own buffers and the iteration runs as one CUDA graph replay when the
+ * engine allows it (one GPU, caches of <= 12,288 entries, profiling off). */
+int edx_engine_iterate_device(edx_engine* e, const uint32_t* ids, const uint64_t* offsets,
+                              uint64_t num_samples, uint64_t total_ids, int32_t* decision_out,
+                              double* expected_cost_out, edx_report* rep);
 int edx_engine_seed_entry(edx_engine* e, uint32_t id, int32_t worker, int latest, int owner);
 /* SimState::state_of — sim.hpp:64-67. */
 int edx_engine_state_of(edx_engine* e, uint32_t id, uint64_t* owners, uint64_t* latest,

@@ -574,6 +574,22 @@ class SimState:
         r.expected_cost_s, r.has_expected = exp.value, True
         return dec, r
 
+    def iterate_device(self, ids_ptr, offsets_ptr, rows, total_ids, want_decision=True,
+                       want_expected=True):
+        """One run() iteration on a batch already in device memory (pointers),
+        its id count declared; a CUDA-graph replay when the engine allows it."""
+        dec = np.empty(int(rows), np.int32) if want_decision else None
+        exp = C.c_double()
+        rep = _Report(self.cfg.n)
+        check(lib().edx_engine_iterate_device(self._h, C.c_void_p(ids_ptr), C.c_void_p(offsets_ptr),
+                                              int(rows), int(total_ids), _ptr(dec, C.c_int32),
+                                              C.byref(exp) if want_expected else None,
+                                              C.byref(rep.c)))
+        r = rep.result()
+        if want_expected:
+            r.expected_cost_s, r.has_expected = exp.value, True
+        return dec, r
+
     # -- state access (parity / tests)
     def seed_entry(self, id_, worker, latest, owner):
         check(lib().edx_engine_seed_entry(self._h, int(id_), int(worker), int(bool(latest)),

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <stdexcept>
 #include <string>
 
@@ -76,6 +77,10 @@ enum DevFlag : int {
 constexpr int kMaxWorkers = 64;  // WorkerMask is one uint64 (types.hpp:89,124)
 
 // --------------------------------------------------------- device buffers
+// Bumped on every device (re)allocation: a captured CUDA graph bakes buffer
+// addresses in, so it is only replayed while this is unchanged.
+inline std::atomic<unsigned long long> g_alloc_epoch{0};
+
 template <class T>
 struct DevBuf {
   T* p = nullptr;
@@ -95,6 +100,7 @@ struct DevBuf {
     size_t c = count ? count : 1;
     EDX_CUDA(cudaMalloc(&p, c * sizeof(T)));
     n = c;
+    g_alloc_epoch.fetch_add(1, std::memory_order_relaxed);
   }
 };
 

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -372,7 +373,7 @@ void engine_build(edx_engine* e) {
   e->matrix.ensure(e->rows * e->n);
   e->disp.gap_keys.ensure(e->rows);
   e->disp.row_index.ensure(e->rows);
-  EDX_CUDA(cudaStreamWaitEvent(e->stream, e->cost_done, 0));
+  if (!e->capturing) EDX_CUDA(cudaStreamWaitEvent(e->stream, e->cost_done, 0));
   rec(e, 0, e->stream);
   if (e->world == 1) {
     edx::launch_cost_build(e->cur_ids, e->cur_offsets, e->rows, e->n, e->ol.p, e->id_space,
@@ -463,7 +464,8 @@ void validate_decision_host(const int32_t* w, uint64_t count, int n, int m) {
                    " samples, expected " + std::to_string(m));
 }
 
-void engine_step(edx_engine* e, const int32_t* decision, edx_report* rep) {
+// Enqueues the step for the current batch and decision (no sync).
+void step_enqueue(edx_engine* e, const int32_t* decision) {
   if (!e->cur_ids) edx::invalid("no batch loaded");
   if (decision) {
     validate_decision_host(decision, e->rows, e->n, e->m);
@@ -481,6 +483,10 @@ void engine_step(edx_engine* e, const int32_t* decision, edx_report* rep) {
   rec(e, 9, e->stream);
   e->launches += sr.launches;
   e->pending_step = e->profiling;
+}
+
+// Waits for the iteration and assembles its IterationReport.
+void step_finish(edx_engine* e, edx_report* rep) {
   engine_sync_check(e);
   // IterationReport totals and realised cost, worker order (sim.hpp:206-216)
   const int n = e->n;
@@ -503,6 +509,89 @@ void engine_step(edx_engine* e, const int32_t* decision, edx_report* rep) {
   }
   ++e->clock;
   e->dispatched = false;
+}
+
+void engine_step(edx_engine* e, const int32_t* decision, edx_report* rep) {
+  step_enqueue(e, decision);
+  step_finish(e, rep);
+}
+
+// One fused iteration (build -> dispatch -> step) for an already-loaded
+// batch.  On one GPU with device-decided victims and profiling off it runs as
+// a CUDA graph captured on first use and replayed while (rows, ids, alpha)
+// stay the same -- the ~40 launches of an iteration become one.  Any capture
+// failure disables graphs for the engine and the iteration runs eagerly.
+void engine_iterate_core(edx_engine* e, double alpha) {
+  if (e->graph_mode < 0) {
+    const char* v = std::getenv("EDX_GRAPH");
+    e->graph_mode = (v && std::strcmp(v, "0") == 0) ? 0 : 1;
+  }
+  const bool eligible = e->graph_mode == 1 && e->world == 1 && !e->profiling &&
+                        edx::step_device_only(e) && e->cur_ids == e->ids.p;
+  if (!eligible) {
+    engine_build(e);
+    engine_dispatch(e, alpha);
+    step_enqueue(e, nullptr);
+    return;
+  }
+  const double a = alpha < 0.0 ? e->alpha : alpha;
+  const unsigned long long epoch = edx::g_alloc_epoch.load(std::memory_order_relaxed);
+  if (!e->gexec || e->g_rows != e->rows || e->g_total != e->total_ids || e->g_alpha != a ||
+      e->g_epoch != epoch) {
+    if (e->gexec) {
+      cudaGraphExecDestroy(e->gexec);
+      e->gexec = nullptr;
+    }
+    // first iteration of a shape runs eagerly: every scratch buffer reaches its
+    // final size before the capture (no allocation is recorded)
+    if (e->g_rows != e->rows || e->g_total != e->total_ids || e->g_alpha != a) {
+      e->g_rows = e->rows;
+      e->g_total = e->total_ids;
+      e->g_alpha = a;
+      engine_build(e);
+      engine_dispatch(e, a);
+      step_enqueue(e, nullptr);
+      return;
+    }
+    const uint64_t l0 = e->launches;
+    cudaGraph_t g = nullptr;
+    EDX_CUDA(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeRelaxed));
+    e->capturing = true;
+    bool ok = true;
+    try {
+      engine_build(e);
+      engine_dispatch(e, a);
+      step_enqueue(e, nullptr);
+      EDX_CUDA(cudaStreamWaitEvent(e->stream, e->cost_done, 0));  // join decision_cost
+    } catch (...) {
+      ok = false;
+    }
+    e->capturing = false;
+    const cudaError_t ec = cudaStreamEndCapture(e->stream, &g);
+    if (ok && ec == cudaSuccess && g) ok = cudaGraphInstantiate(&e->gexec, g, 0) == cudaSuccess;
+    else ok = false;
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    if (!ok) {  // not capturable here: eager from now on
+      e->gexec = nullptr;
+      e->graph_mode = 0;
+      e->launches = l0;
+      engine_build(e);
+      engine_dispatch(e, a);
+      step_enqueue(e, nullptr);
+      return;
+    }
+    e->g_launches = e->launches - l0;
+    e->launches = l0;
+    e->g_epoch = edx::g_alloc_epoch.load(std::memory_order_relaxed);
+  }
+  // host-side inputs the graph reads at replay time (pinned; the previous
+  // iteration's copy has completed: every iteration ends with a sync)
+  *e->h_clock = static_cast<uint32_t>(e->clock);
+  EDX_CUDA(cudaGraphLaunch(e->gexec, e->stream));
+  EDX_CUDA(cudaEventRecord(e->cost_done, e->stream));
+  e->launches += e->g_launches;
+  e->built = e->gap_ready = e->dispatched = true;
 }
 
 }  // namespace
@@ -584,6 +673,8 @@ int edx_engine_create(const edx_cluster_config* cfg, const edx_engine_options* o
     EDX_CUDA(cudaMallocHost(&e->h_flags, edx::kFlagCount * sizeof(int)));
     EDX_CUDA(cudaMallocHost(&e->h_counters, (3 * 64 + 8) * sizeof(unsigned long long)));
     EDX_CUDA(cudaMallocHost(&e->h_expected, sizeof(double)));
+    EDX_CUDA(cudaMallocHost(&e->h_clock, sizeof(uint32_t)));
+    e->d_clock.ensure(1);
     e->disp.init(e->device);
     edx::step_init_state(e.get());
     EDX_CUDA(cudaStreamSynchronize(e->stream));
@@ -601,6 +692,8 @@ void edx_engine_destroy(edx_engine* e) {
   if (e->cost_done) cudaEventDestroy(e->cost_done);
   if (e->h_flags) cudaFreeHost(e->h_flags);
   if (e->h_counters) cudaFreeHost(e->h_counters);
+  if (e->h_clock) cudaFreeHost(e->h_clock);
+  if (e->gexec) cudaGraphExecDestroy(e->gexec);
   if (e->h_expected) cudaFreeHost(e->h_expected);
   cudaStream_t s = e->stream;
   if (e->comm) edx::nccl_comm_destroy(e->comm);
@@ -688,12 +781,42 @@ int edx_engine_iterate(edx_engine* e, const uint32_t* ids, const uint64_t* offse
   return guard([&] {
     EDX_CUDA(cudaSetDevice(e->device));
     engine_load(e, ids, offsets, num_samples, on_device);
-    engine_build(e);
-    engine_dispatch(e, -1.0);
+    engine_iterate_core(e, -1.0);
     if (decision_out)
       EDX_CUDA(cudaMemcpyAsync(decision_out, e->decision.p, e->rows * sizeof(int32_t),
                                cudaMemcpyDeviceToHost, e->stream));
-    engine_step(e, nullptr, rep);
+    step_finish(e, rep);
+    if (expected_cost_out) {
+      EDX_CUDA(cudaStreamWaitEvent(e->stream, e->cost_done, 0));
+      EDX_CUDA(cudaMemcpyAsync(e->h_expected, e->expected.p, sizeof(double),
+                               cudaMemcpyDeviceToHost, e->stream));
+      EDX_CUDA(cudaStreamSynchronize(e->stream));
+      *expected_cost_out = *e->h_expected;
+    }
+  });
+}
+
+int edx_engine_iterate_device(edx_engine* e, const uint32_t* ids, const uint64_t* offsets,
+                              uint64_t num_samples, uint64_t total_ids, int32_t* decision_out,
+                              double* expected_cost_out, edx_report* rep) {
+  return guard([&] {
+    EDX_CUDA(cudaSetDevice(e->device));
+    if (total_ids > e->max_ids)
+      edx::invalid("batch holds " + std::to_string(total_ids) + " ids; engine max_batch_ids is " +
+                   std::to_string(e->max_ids));
+    // stage into the engine's own batch buffers: fixed pointers for the graph
+    e->offsets.ensure(num_samples + 1);
+    if (total_ids)
+      EDX_CUDA(cudaMemcpyAsync(e->ids.p, ids, total_ids * sizeof(uint32_t), cudaMemcpyDeviceToDevice,
+                               e->stream));
+    EDX_CUDA(cudaMemcpyAsync(e->offsets.p, offsets, (num_samples + 1) * sizeof(uint64_t),
+                             cudaMemcpyDeviceToDevice, e->stream));
+    engine_load(e, e->ids.p, e->offsets.p, num_samples, 1, total_ids);
+    engine_iterate_core(e, -1.0);
+    if (decision_out)
+      EDX_CUDA(cudaMemcpyAsync(decision_out, e->decision.p, e->rows * sizeof(int32_t),
+                               cudaMemcpyDeviceToHost, e->stream));
+    step_finish(e, rep);
     if (expected_cost_out) {
       EDX_CUDA(cudaStreamWaitEvent(e->stream, e->cost_done, 0));
       EDX_CUDA(cudaMemcpyAsync(e->h_expected, e->expected.p, sizeof(double),

@@ -94,6 +94,19 @@ struct edx_engine {
   int* h_flags = nullptr;            // pinned
   unsigned long long* h_counters = nullptr;  // pinned
   double* h_expected = nullptr;      // pinned
+  uint32_t* h_clock = nullptr;       // pinned: the iteration clock, copied to d_clock in-stream
+  edx::DevBuf<uint32_t> d_clock;
+
+  // CUDA graph of one fused iteration (build -> dispatch -> step), replayed
+  // while the shape is unchanged; eligible on one GPU, with device-decided
+  // victims (caches <= kSelCap) and profiling off
+  int graph_mode = -1;               // -1: undecided (env EDX_GRAPH, default on); 0 off; 1 on
+  cudaGraphExec_t gexec = nullptr;
+  uint64_t g_rows = 0, g_total = 0;
+  double g_alpha = -1.0;
+  uint64_t g_launches = 0;
+  unsigned long long g_epoch = 0;  // edx::g_alloc_epoch at capture
+  bool capturing = false;
 
   // profiling
   bool profiling = false;

@@ -627,11 +627,13 @@ __global__ void k_apply(const uint64_t* __restrict__ items,
                         const uint32_t* __restrict__ ids, const uint8_t* __restrict__ type,
                         const uint32_t* __restrict__ ins_scan, const uint32_t* __restrict__ ws,
                         const uint32_t* __restrict__ cand_slot, uint64_t capacity,
-                        uint64_t id_space, const uint32_t* __restrict__ cur_mark, uint32_t clock,
+                        uint64_t id_space, const uint32_t* __restrict__ cur_mark,
+                        const uint32_t* __restrict__ clock_dev,
                         ulonglong2* __restrict__ ol, unsigned long long* __restrict__ res,
                         int32_t* __restrict__ slot_of, uint32_t* __restrict__ sid,
                         uint32_t* __restrict__ smark, uint32_t* __restrict__ sfreq,
                         uint32_t* __restrict__ slast) {
+  const uint32_t clock = *clock_dev;
   const uint64_t N = counters_ro[3 * n + 2];
   const uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (q >= N) return;
@@ -817,13 +819,18 @@ void cub_call(edx_engine* e, F&& f) {
 
 }  // namespace
 
+bool step_device_only(const edx_engine* e) { return e->capacity <= kSelCap; }
+
 void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
   cudaStream_t st = e->stream;
   auto& s = e->step;
   auto& c = e->cache;
   const int n = e->n;
   const uint64_t T = e->total_ids, R = e->rows, ucap = e->max_ids;
-  const uint32_t clock32 = static_cast<uint32_t>(e->clock);
+  // the clock goes through pinned memory so a captured graph reads each
+  // iteration's value at replay time
+  *e->h_clock = static_cast<uint32_t>(e->clock);
+  EDX_CUDA(cudaMemcpyAsync(e->d_clock.p, e->h_clock, sizeof(uint32_t), cudaMemcpyHostToDevice, st));
   int launches = 0;
 
   EDX_CUDA(cudaMemsetAsync(s.counters.p, 0, (3 * n + 4) * sizeof(unsigned long long), st));
@@ -946,8 +953,8 @@ void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
   k_apply<<<grid_for(T), kT, 0, st>>>(s.need_key_sorted.p, s.counters.p, n, e->cur_ids,
                                       s.need_type.p, s.ins_rank.p, s.wscalars.p,
                                       s.cand_slot_sorted.p, e->capacity, e->id_space, c.cur_mark.p,
-                                      clock32, e->ol.p, e->res.p, c.slot_of.p, c.sid.p, c.smark.p,
-                                      c.sfreq.p, c.slast.p);
+                                      e->d_clock.p, e->ol.p, e->res.p, c.slot_of.p, c.sid.p,
+                                      c.smark.p, c.sfreq.p, c.slast.p);
   k_worker_finalize<<<1, 64, 0, st>>>(n, s.wscalars.p, con_scan, c.size.p, c.cur_mark.p,
                                       c.at_cur.p);
   k_phase3<<<grid_for(T), kT, 0, st>>>(s.uniq.p, s.umask.p, s.counters.p, n, e->ol.p);

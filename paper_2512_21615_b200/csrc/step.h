@@ -16,5 +16,8 @@ void step_init_state(edx_engine* e);
 // return the per-worker counters are being copied to e->h_counters (the
 // caller synchronises the stream).
 void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out);
+// True when step_run decides every victim on the device (no host round trip),
+// i.e. the step can be captured into a CUDA graph.
+bool step_device_only(const edx_engine* e);
 
 }  // namespace edx

@@ -255,3 +255,34 @@ def test_device_batch_declared_total(gpu, oracle, pyoracle):
            total_ids=R * L - 1)
     with pytest.raises(edx.InvalidArgument, match="declared id count"):
         a.build(np.empty((R, n)))
+
+
+@pytest.mark.parametrize("name,alpha", [("C2", 0.5), ("C1", 0.0), ("P8", 1.0)])
+def test_iterate_device_graph_replay(gpu, oracle, pyoracle, name, alpha):
+    """edx_engine_iterate_device: from the third iteration of a shape the
+    iteration is a CUDA-graph replay; every decision, report and the final
+    state equal the reference run() body, also across a shape change."""
+    import torch
+    edx = gpu
+    p = CONFIGS[name]
+    n, m, L = p["n"], p["m"], p["L"]
+    R = n * m
+    c = edx.ClusterConfig(n=n, m=m, bandwidths_bps=p["bw"], cache_capacity=p["cap"], alpha=alpha)
+    eng = edx.SimState(c, id_space=p["V"], max_batch_ids=R * L)
+    sim = oracle.sim(pyoracle.Cfg(n, m, p["bw"], cap=p["cap"], alpha=alpha))
+    offs = offsets_for(R, L)
+    d_offs = torch.from_numpy(offs.view(np.int64)).cuda()
+    batches = list(oracle.zipf_batches(p["V"], L, 1.05, 10, 17, R))
+    for it, ids in enumerate(batches):
+        if it == 6:  # a host-path iteration and a stepwise one in between (graph reuse)
+            dec, rep = eng.iterate(ids, offs)
+        else:
+            d_ids = torch.from_numpy(ids.view(np.int32)).cuda()
+            torch.cuda.synchronize()
+            dec, rep = eng.iterate_device(d_ids.data_ptr(), d_offs.data_ptr(), R, R * L)
+        wdec, wexp, wrep, _ = sim.iteration(ids, offs)
+        assert (dec == wdec).all(), f"iter {it}: decision"
+        assert rep.as_dict() == wrep, f"iter {it}: report"
+        assert rep.expected_cost_s == wexp, f"iter {it}: expected cost"
+    msg = canon_equal(eng.canonical_state(), sim.canonical_state())
+    assert not msg, msg
