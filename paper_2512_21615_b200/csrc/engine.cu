@@ -429,18 +429,19 @@ void engine_dispatch(edx_engine* e, double alpha) {
                               e->disp.side);
     EDX_CUDA(cudaEventRecord(e->cost_done, e->disp.side));
   } else {
-    // rank 0 appends decision_cost's bits to the decision; one broadcast to all
+    // the decision goes out first; rank 0 (the only rank holding the gathered
+    // matrix) computes decision_cost on its side stream, overlapping the step,
+    // and the expected cost is broadcast only when a caller asks for it
+    edx::nccl_broadcast_i32(e->comm, e->decision.p, e->rows, 0, e->stream);
     if (e->rank == 0) {
+      EDX_CUDA(cudaEventRecord(e->disp.fork, e->stream));
+      EDX_CUDA(cudaStreamWaitEvent(e->disp.side, e->disp.fork, 0));
       edx::launch_decision_cost(e->matrix.p, e->decision.p, e->rows, e->n, e->expected.p,
-                                e->stream);
-      EDX_CUDA(cudaMemcpyAsync(e->decision.p + e->rows, e->expected.p, sizeof(double),
-                               cudaMemcpyDeviceToDevice, e->stream));
+                                e->disp.side);
+      EDX_CUDA(cudaEventRecord(e->cost_done, e->disp.side));
+    } else {
+      EDX_CUDA(cudaEventRecord(e->cost_done, e->stream));
     }
-    edx::nccl_broadcast_i32(e->comm, e->decision.p, e->rows + 2, 0, e->stream);
-    if (e->rank != 0)
-      EDX_CUDA(cudaMemcpyAsync(e->expected.p, e->decision.p + e->rows, sizeof(double),
-                               cudaMemcpyDeviceToDevice, e->stream));
-    EDX_CUDA(cudaEventRecord(e->cost_done, e->stream));
   }
   e->launches += launches + 1;
   const int mult = edx::exact_multiplicity(e->m, alpha);
@@ -462,6 +463,18 @@ void validate_decision_host(const int32_t* w, uint64_t count, int n, int m) {
     if (load[j] != m)
       edx::invalid("worker " + std::to_string(j) + " received " + std::to_string(load[j]) +
                    " samples, expected " + std::to_string(m));
+}
+
+// The iteration's expected_cost_s (decision_cost, sim.hpp:439) on the host;
+// multi-GPU engines broadcast rank 0's value (every rank must call this).
+double fetch_expected(edx_engine* e) {
+  EDX_CUDA(cudaStreamWaitEvent(e->stream, e->cost_done, 0));
+  if (e->world > 1)
+    edx::nccl_broadcast_i32(e->comm, reinterpret_cast<int32_t*>(e->expected.p), 2, 0, e->stream);
+  EDX_CUDA(cudaMemcpyAsync(e->h_expected, e->expected.p, sizeof(double), cudaMemcpyDeviceToHost,
+                           e->stream));
+  EDX_CUDA(cudaStreamSynchronize(e->stream));
+  return *e->h_expected;
 }
 
 // Enqueues the step for the current batch and decision (no sync).
@@ -737,13 +750,8 @@ int edx_engine_dispatch(edx_engine* e, double alpha, int32_t* decision_out,
     if (decision_out)
       EDX_CUDA(cudaMemcpyAsync(decision_out, e->decision.p, e->rows * sizeof(int32_t),
                                cudaMemcpyDeviceToHost, e->stream));
-    if (expected_cost_out) {
-      EDX_CUDA(cudaStreamWaitEvent(e->stream, e->cost_done, 0));
-      EDX_CUDA(cudaMemcpyAsync(e->h_expected, e->expected.p, sizeof(double),
-                               cudaMemcpyDeviceToHost, e->stream));
-    }
     if (decision_out || expected_cost_out) engine_sync_check(e);
-    if (expected_cost_out) *expected_cost_out = *e->h_expected;
+    if (expected_cost_out) *expected_cost_out = fetch_expected(e);
   });
 }
 
@@ -786,13 +794,7 @@ int edx_engine_iterate(edx_engine* e, const uint32_t* ids, const uint64_t* offse
       EDX_CUDA(cudaMemcpyAsync(decision_out, e->decision.p, e->rows * sizeof(int32_t),
                                cudaMemcpyDeviceToHost, e->stream));
     step_finish(e, rep);
-    if (expected_cost_out) {
-      EDX_CUDA(cudaStreamWaitEvent(e->stream, e->cost_done, 0));
-      EDX_CUDA(cudaMemcpyAsync(e->h_expected, e->expected.p, sizeof(double),
-                               cudaMemcpyDeviceToHost, e->stream));
-      EDX_CUDA(cudaStreamSynchronize(e->stream));
-      *expected_cost_out = *e->h_expected;
-    }
+    if (expected_cost_out) *expected_cost_out = fetch_expected(e);
   });
 }
 
@@ -817,13 +819,7 @@ int edx_engine_iterate_device(edx_engine* e, const uint32_t* ids, const uint64_t
       EDX_CUDA(cudaMemcpyAsync(decision_out, e->decision.p, e->rows * sizeof(int32_t),
                                cudaMemcpyDeviceToHost, e->stream));
     step_finish(e, rep);
-    if (expected_cost_out) {
-      EDX_CUDA(cudaStreamWaitEvent(e->stream, e->cost_done, 0));
-      EDX_CUDA(cudaMemcpyAsync(e->h_expected, e->expected.p, sizeof(double),
-                               cudaMemcpyDeviceToHost, e->stream));
-      EDX_CUDA(cudaStreamSynchronize(e->stream));
-      *expected_cost_out = *e->h_expected;
-    }
+    if (expected_cost_out) *expected_cost_out = fetch_expected(e);
   });
 }
 
