@@ -277,23 +277,37 @@ __global__ void k_cand_ranges(const int32_t* __restrict__ wlist, int nw, uint64_
                               const int32_t* __restrict__ first_pos, const uint32_t* __restrict__ uidx,
                               uint64_t ucap, const int32_t* __restrict__ need_first,
                               uint32_t* __restrict__ ranges) {
+  // one warp-level reduction per field, then one atomic per warp (the
+  // candidates of every evicting worker -- millions at C4 -- would otherwise
+  // all hit the same eight words)
   const uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  if (x >= static_cast<uint64_t>(nw) * capacity) return;
-  const int jl = static_cast<int>(x / capacity);
-  const uint64_t s = x - static_cast<uint64_t>(jl) * capacity;
-  const int j = wlist[jl];
-  if (s >= ws[j * kWS + kWsSize0] || ws[j * kWS + kWsEvict] == 0) return;
-  const uint64_t g = static_cast<uint64_t>(j) * capacity + s;
-  const uint32_t id = sid[g];
-  if (pinned_by(j, id, first_pos, uidx, ucap, need_first)) return;
-  atomicMin(ranges + 0, smark[g]);
-  atomicMax(ranges + 1, smark[g]);
-  atomicMin(ranges + 2, sfreq[g]);
-  atomicMax(ranges + 3, sfreq[g]);
-  atomicMin(ranges + 4, slast[g]);
-  atomicMax(ranges + 5, slast[g]);
-  atomicMin(ranges + 6, id);
-  atomicMax(ranges + 7, id);
+  uint32_t v[4] = {UINT_MAX, UINT_MAX, UINT_MAX, UINT_MAX}, V[4] = {0, 0, 0, 0};
+  if (x < static_cast<uint64_t>(nw) * capacity) {
+    const int jl = static_cast<int>(x / capacity);
+    const uint64_t s = x - static_cast<uint64_t>(jl) * capacity;
+    const int j = wlist[jl];
+    if (s < ws[j * kWS + kWsSize0] && ws[j * kWS + kWsEvict] != 0) {
+      const uint64_t g = static_cast<uint64_t>(j) * capacity + s;
+      const uint32_t id = sid[g];
+      if (!pinned_by(j, id, first_pos, uidx, ucap, need_first)) {
+        const uint32_t f[4] = {smark[g], sfreq[g], slast[g], id};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] = V[q] = f[q];
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    v[q] = __reduce_min_sync(0xffffffffu, v[q]);
+    V[q] = __reduce_max_sync(0xffffffffu, V[q]);
+  }
+  if ((threadIdx.x & 31) == 0 && V[0] >= v[0] && v[0] != UINT_MAX) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      atomicMin(ranges + 2 * q, v[q]);
+      atomicMax(ranges + 2 * q + 1, V[q]);
+    }
+  }
 }
 
 __device__ __forceinline__ int width_of(uint32_t lo, uint32_t hi) {
@@ -330,9 +344,11 @@ __global__ void k_cand_pack(const int32_t* __restrict__ wlist, int nw, uint64_t 
       k = (k << wl) | (slast[g] - ranges[4]);
       k = (k << wi) | (id - ranges[6]);
       key = (static_cast<uint64_t>(jl) << 58) | k;
-      atomicAdd(ws + j * kWS + kWsCand, 1u);
     }
   }
+  // per-worker candidate count, one atomic per (warp, worker) group
+  const unsigned grp = __match_any_sync(__activemask(), key != ~0ULL ? j : -1 - j);
+  if (key != ~0ULL && (threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(ws + j * kWS + kWsCand, __popc(grp));
   keys[x] = key;
   slots[x] = static_cast<uint32_t>(s);
 }

@@ -18,6 +18,8 @@ CONFIGS = {
     "P32": dict(n=32, m=12, bw=HET(32), cap=120, V=2000, L=4),
     # mass eviction: > 4096 victims per worker per step (the full-sort victim path)
     "PX": dict(n=2, m=64, bw=[5e9, 5e8], cap=12_000, V=500_000, L=100),
+    # caches above the one-CTA selection size: host-sized device-wide victim path
+    "PXL": dict(n=3, m=64, bw=[5e9, 5e9, 5e8], cap=13_000, V=500_000, L=100),
 }
 
 

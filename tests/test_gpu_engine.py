@@ -141,6 +141,13 @@ def test_engine_wide_exact_block(gpu, oracle, pyoracle, name, alpha):
     run_parity(gpu, oracle, pyoracle, name, alpha, 15, seed=21)
 
 
+@pytest.mark.parametrize("s", [0.6, 1.05])
+def test_engine_mass_eviction_large_caches(gpu, oracle, pyoracle, s):
+    """Caches of 13,000 entries (> the one-CTA selection size): victims through
+    the device-wide candidate ranges, packing and sort, thousands per step."""
+    run_parity(gpu, oracle, pyoracle, "PXL", 0.25, 7, seed=13, s=s)
+
+
 def test_engine_c1(gpu, oracle, pyoracle):
     """C1: 4 workers, batch 1024, uniform, 10% cache, greedy only."""
     run_parity(gpu, oracle, pyoracle, "C1", 0.0, 30, check_state_every=10)
