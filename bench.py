@@ -67,6 +67,7 @@ def parse():
     ap.add_argument("--no-flush", action="store_true", help="do not flush L2 between iterations")
     ap.add_argument("--batch", type=int, default=None, help="C5 sweep: samples per iteration")
     ap.add_argument("--workers", type=int, default=None, help="C5 sweep: workers (<= 64)")
+    ap.add_argument("--debug-times", action="store_true", help="per-iteration times in the line")
     return ap.parse_args()
 
 
@@ -355,6 +356,8 @@ def product(args, w, rank, world, local_rank):
         "clocks": clk.summary(),
         "gpu_launches": launches,
     }
+    if args.debug_times:
+        out["debug_times"] = {"value_ms": ms, "e2e_ms": e2e_ms}
     return out, host[:P + W + K], offs
 
 

@@ -270,42 +270,56 @@ __device__ __forceinline__ bool pinned_by(int j, uint32_t id, const int32_t* fir
   return need_first[static_cast<uint64_t>(j) * ucap + uidx[fp]] != INT_MAX;
 }
 
-__global__ void k_cand_ranges(const int32_t* __restrict__ wlist, int nw, uint64_t capacity,
-                              const uint32_t* __restrict__ ws, const uint32_t* __restrict__ sid,
-                              const uint32_t* __restrict__ smark, const uint32_t* __restrict__ sfreq,
-                              const uint32_t* __restrict__ slast,
-                              const int32_t* __restrict__ first_pos, const uint32_t* __restrict__ uidx,
-                              uint64_t ucap, const int32_t* __restrict__ need_first,
-                              uint32_t* __restrict__ ranges) {
-  // one warp-level reduction per field, then one atomic per warp (the
-  // candidates of every evicting worker -- millions at C4 -- would otherwise
-  // all hit the same eight words)
-  const uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+__global__ void __launch_bounds__(256)
+    k_cand_ranges(const int32_t* __restrict__ wlist, int nw, uint64_t capacity,
+                  const uint32_t* __restrict__ ws, const uint32_t* __restrict__ sid,
+                  const uint32_t* __restrict__ smark, const uint32_t* __restrict__ sfreq,
+                  const uint32_t* __restrict__ slast, const int32_t* __restrict__ first_pos,
+                  const uint32_t* __restrict__ uidx, uint64_t ucap,
+                  const int32_t* __restrict__ need_first, uint32_t* __restrict__ ranges) {
+  // grid-stride, then a block reduction and one atomic per block and field
+  // (the candidates of every evicting worker -- millions at C4 -- would
+  // otherwise all hit the same eight words)
+  __shared__ uint32_t part[8][8];
   uint32_t v[4] = {UINT_MAX, UINT_MAX, UINT_MAX, UINT_MAX}, V[4] = {0, 0, 0, 0};
-  if (x < static_cast<uint64_t>(nw) * capacity) {
+  const uint64_t total = static_cast<uint64_t>(nw) * capacity;
+  for (uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; x < total;
+       x += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const int jl = static_cast<int>(x / capacity);
     const uint64_t s = x - static_cast<uint64_t>(jl) * capacity;
     const int j = wlist[jl];
-    if (s < ws[j * kWS + kWsSize0] && ws[j * kWS + kWsEvict] != 0) {
-      const uint64_t g = static_cast<uint64_t>(j) * capacity + s;
-      const uint32_t id = sid[g];
-      if (!pinned_by(j, id, first_pos, uidx, ucap, need_first)) {
-        const uint32_t f[4] = {smark[g], sfreq[g], slast[g], id};
+    if (s >= ws[j * kWS + kWsSize0] || ws[j * kWS + kWsEvict] == 0) continue;
+    const uint64_t g = static_cast<uint64_t>(j) * capacity + s;
+    const uint32_t id = sid[g];
+    if (pinned_by(j, id, first_pos, uidx, ucap, need_first)) continue;
+    const uint32_t f[4] = {smark[g], sfreq[g], slast[g], id};
 #pragma unroll
-        for (int q = 0; q < 4; ++q) v[q] = V[q] = f[q];
-      }
+    for (int q = 0; q < 4; ++q) {
+      v[q] = min(v[q], f[q]);
+      V[q] = max(V[q], f[q]);
     }
   }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     v[q] = __reduce_min_sync(0xffffffffu, v[q]);
     V[q] = __reduce_max_sync(0xffffffffu, V[q]);
   }
-  if ((threadIdx.x & 31) == 0 && V[0] >= v[0] && v[0] != UINT_MAX) {
+  if (lane == 0)
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      atomicMin(ranges + 2 * q, v[q]);
-      atomicMax(ranges + 2 * q + 1, V[q]);
+      part[warp][2 * q] = v[q];
+      part[warp][2 * q + 1] = V[q];
+    }
+  __syncthreads();
+  if (threadIdx.x < 8) {
+    const int f = threadIdx.x;
+    uint32_t r = (f & 1) ? 0u : UINT_MAX;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w)
+      r = (f & 1) ? max(r, part[w][f]) : min(r, part[w][f]);
+    if ((f & 1) ? r != 0u : r != UINT_MAX) {
+      if (f & 1) atomicMax(ranges + f, r);
+      else atomicMin(ranges + f, r);
     }
   }
 }
@@ -315,42 +329,46 @@ __device__ __forceinline__ int width_of(uint32_t lo, uint32_t hi) {
 }
 
 // VictimKey (cache.hpp:47-58) = (version, mark, frequency, last_access, id),
-// packed order-preservingly into 58 bits below a 6-bit worker field.
-__global__ void k_cand_pack(const int32_t* __restrict__ wlist, int nw, uint64_t capacity,
-                            uint32_t* __restrict__ ws, const uint32_t* __restrict__ sid,
-                            const uint32_t* __restrict__ smark, const uint32_t* __restrict__ sfreq,
-                            const uint32_t* __restrict__ slast, const ulonglong2* __restrict__ ol,
-                            const int32_t* __restrict__ first_pos, const uint32_t* __restrict__ uidx,
-                            uint64_t ucap, const int32_t* __restrict__ need_first,
-                            const uint32_t* __restrict__ ranges, uint64_t* __restrict__ keys,
-                            uint32_t* __restrict__ slots, int* __restrict__ flags) {
+// packed order-preservingly into kw = 1 + wm + wf + wl + wi bits (widths of the
+// candidates' value ranges, computed on the host from k_cand_ranges) below the
+// evicting worker's list index; non-candidates are all ones and sort last.
+__global__ void __launch_bounds__(256)
+    k_cand_pack(const int32_t* __restrict__ wlist, int nw, uint64_t capacity,
+                uint32_t* __restrict__ ws, const uint32_t* __restrict__ sid,
+                const uint32_t* __restrict__ smark, const uint32_t* __restrict__ sfreq,
+                const uint32_t* __restrict__ slast, const ulonglong2* __restrict__ ol,
+                const int32_t* __restrict__ first_pos, const uint32_t* __restrict__ uidx,
+                uint64_t ucap, const int32_t* __restrict__ need_first,
+                const uint32_t* __restrict__ ranges, int wm, int wf, int wl, int wi,
+                uint64_t* __restrict__ keys, uint32_t* __restrict__ slots) {
+  __shared__ uint32_t cnt[kMaxWorkers];
+  if (threadIdx.x < kMaxWorkers) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const int kw = 1 + wm + wf + wl + wi;
   const uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  if (x >= static_cast<uint64_t>(nw) * capacity) return;
-  const int jl = static_cast<int>(x / capacity);
-  const uint64_t s = x - static_cast<uint64_t>(jl) * capacity;
-  const int j = wlist[jl];
-  uint64_t key = ~0ULL;
-  if (s < ws[j * kWS + kWsSize0] && ws[j * kWS + kWsEvict] != 0) {
-    const uint64_t g = static_cast<uint64_t>(j) * capacity + s;
-    const uint32_t id = sid[g];
-    if (!pinned_by(j, id, first_pos, uidx, ucap, need_first)) {
-      const int wm = width_of(ranges[0], ranges[1]), wf = width_of(ranges[2], ranges[3]);
-      const int wl = width_of(ranges[4], ranges[5]), wi = width_of(ranges[6], ranges[7]);
-      if (1 + wm + wf + wl + wi > 57) atomicOr(flags + kFlagKeyRange, 1);
-      const uint64_t ver = (ol[id].y >> j) & 1ULL;
-      uint64_t k = ver;
-      k = (k << wm) | (smark[g] - ranges[0]);
-      k = (k << wf) | (sfreq[g] - ranges[2]);
-      k = (k << wl) | (slast[g] - ranges[4]);
-      k = (k << wi) | (id - ranges[6]);
-      key = (static_cast<uint64_t>(jl) << 58) | k;
+  if (x < static_cast<uint64_t>(nw) * capacity) {
+    const int jl = static_cast<int>(x / capacity);
+    const uint64_t s = x - static_cast<uint64_t>(jl) * capacity;
+    const int j = wlist[jl];
+    uint64_t key = ~0ULL;
+    if (s < ws[j * kWS + kWsSize0] && ws[j * kWS + kWsEvict] != 0) {
+      const uint64_t g = static_cast<uint64_t>(j) * capacity + s;
+      const uint32_t id = sid[g];
+      if (!pinned_by(j, id, first_pos, uidx, ucap, need_first)) {
+        uint64_t k = (ol[id].y >> j) & 1ULL;  // version: a stale copy goes first
+        k = (k << wm) | (smark[g] - ranges[0]);
+        k = (k << wf) | (sfreq[g] - ranges[2]);
+        k = (k << wl) | (slast[g] - ranges[4]);
+        k = (k << wi) | (id - ranges[6]);
+        key = (static_cast<uint64_t>(jl) << kw) | k;
+        atomicAdd(&cnt[jl], 1u);
+      }
     }
+    keys[x] = key;
+    slots[x] = static_cast<uint32_t>(s);
   }
-  // per-worker candidate count, one atomic per (warp, worker) group
-  const unsigned grp = __match_any_sync(__activemask(), key != ~0ULL ? j : -1 - j);
-  if (key != ~0ULL && (threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(ws + j * kWS + kWsCand, __popc(grp));
-  keys[x] = key;
-  slots[x] = static_cast<uint32_t>(s);
+  __syncthreads();
+  if (threadIdx.x < nw && cnt[threadIdx.x]) atomicAdd(ws + wlist[threadIdx.x] * kWS + kWsCand, cnt[threadIdx.x]);
 }
 
 __global__ void k_cand_offsets(const int32_t* __restrict__ wlist, int nw, uint32_t* __restrict__ ws,
@@ -806,6 +824,13 @@ void step_init_state(edx_engine* e) {
     s.cand_key.ensure(cand);
     s.cand_key_sorted.ensure(cand);
     s.cand_slot.ensure(cand);
+    // the device-wide victim sort's scratch, sized once here: growing it at
+    // the first evicting step would cost a free + malloc inside the loop
+    size_t bytes = 0;
+    EDX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, s.cand_key.p, s.cand_key_sorted.p,
+                                             s.cand_slot.p, s.cand_slot_sorted.p,
+                                             static_cast<int>(cand), 0, 64, e->stream));
+    s.temp.ensure(bytes);
   }
   s.cand_off.ensure(128);  // [0,64): workers 0..n-1; [64,128): evicting workers (large caches)
   std::vector<int32_t> wl(n);
@@ -924,19 +949,33 @@ void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
       EDX_CUDA(cudaMemcpyAsync(d_wl, wl.data(), nw * sizeof(int32_t), cudaMemcpyHostToDevice, st));
       const uint64_t cand = static_cast<uint64_t>(nw) * e->capacity;
       k_init_ranges<<<1, 32, 0, st>>>(s.ranges.p);
-      k_cand_ranges<<<grid_for(cand), kT, 0, st>>>(d_wl, nw, e->capacity, s.wscalars.p, c.sid.p,
-                                                   c.smark.p, c.sfreq.p, c.slast.p, s.first_pos.p,
-                                                   s.uidx_of_pos.p, ucap, s.need_first.p, s.ranges.p);
+      const unsigned rgrid = static_cast<unsigned>(std::min<uint64_t>(grid_for(cand), 148ull * 8));
+      k_cand_ranges<<<rgrid, kT, 0, st>>>(d_wl, nw, e->capacity, s.wscalars.p, c.sid.p, c.smark.p,
+                                         c.sfreq.p, c.slast.p, s.first_pos.p, s.uidx_of_pos.p, ucap,
+                                         s.need_first.p, s.ranges.p);
+      EDX_LAUNCHED();
+      // key widths on the host (this path already synchronised once): the
+      // sort then covers only the key bits and the worker-index bits
+      uint32_t rg[8];
+      EDX_CUDA(cudaMemcpyAsync(rg, s.ranges.p, sizeof rg, cudaMemcpyDeviceToHost, st));
+      EDX_CUDA(cudaStreamSynchronize(st));
+      auto width = [](uint32_t lo, uint32_t hi) { return hi > lo ? 32 - __builtin_clz(hi - lo) : 0; };
+      const int wm = width(rg[0], rg[1]), wf = width(rg[2], rg[3]);
+      const int wl = width(rg[4], rg[5]), wi = width(rg[6], rg[7]);
+      const int kw = 1 + wm + wf + wl + wi;
+      int wb = 1;  // worker-index bits, one spare so a real key never equals all ones
+      while ((1 << (wb - 1)) < nw) ++wb;
+      if (kw + wb > 64) throw Error(EDX_RUNTIME_ERROR, "victim key fields exceed the 64-bit device packing");
       k_cand_pack<<<grid_for(cand), kT, 0, st>>>(d_wl, nw, e->capacity, s.wscalars.p, c.sid.p,
                                                  c.smark.p, c.sfreq.p, c.slast.p, e->ol.p,
                                                  s.first_pos.p, s.uidx_of_pos.p, ucap,
-                                                 s.need_first.p, s.ranges.p, s.cand_key.p,
-                                                 s.cand_slot.p, e->flags.p);
+                                                 s.need_first.p, s.ranges.p, wm, wf, wl, wi,
+                                                 s.cand_key.p, s.cand_slot.p);
       EDX_LAUNCHED();
       cub_call(e, [&](void* tmp, size_t& b) {
         return cub::DeviceRadixSort::SortPairs(tmp, b, s.cand_key.p, s.cand_key_sorted.p,
                                                s.cand_slot.p, s.cand_slot_sorted.p,
-                                               static_cast<int>(cand), 0, 64, st);
+                                               static_cast<int>(cand), 0, kw + wb, st);
       });
       k_cand_offsets<<<1, 32, 0, st>>>(d_wl, nw, s.wscalars.p, e->flags.p);
       EDX_LAUNCHED();
