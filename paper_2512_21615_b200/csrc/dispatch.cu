@@ -41,44 +41,55 @@ namespace {
 constexpr int kGreedyThreads = 1024;
 constexpr int kGreedyWarps = kGreedyThreads / 32;
 
-// Each position's four best workers among the initially open ones, in
+// Each position's eight best workers among the initially open ones, in
 // (cost, index) order -- strict '<' over ascending j, as the reference's scan
 // (assign.hpp:177-184) -- packed 8 bits each (0xFF = none).  One thread per
 // position, grid-wide: the matrix is read once.
+constexpr int kPrefs = 8;
+
 __global__ void k_greedy_prefs(const double* __restrict__ matrix, int n,
                                const uint32_t* __restrict__ order, uint64_t n_order,
                                const int32_t* __restrict__ capacity_dev, int cap_uniform,
-                               uint32_t* __restrict__ prefs) {
+                               uint64_t* __restrict__ prefs) {
   const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (t >= n_order) return;
   const double* r = matrix + static_cast<uint64_t>(order[t]) * n;
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
-  double c0 = inf, c1 = inf, c2 = inf, c3 = inf;
-  int w0 = 0xFF, w1 = 0xFF, w2 = 0xFF, w3 = 0xFF;
+  double cb[kPrefs];
+  int wb[kPrefs];
+#pragma unroll
+  for (int q = 0; q < kPrefs; ++q) {
+    cb[q] = inf;
+    wb[q] = 0xFF;
+  }
   for (int w = 0; w < n; ++w) {
     if ((capacity_dev ? capacity_dev[w] : cap_uniform) <= 0) continue;
     const double c = r[w];
-    if (c < c3) {  // insertion keeps equal costs in index order
-      if (c < c2) {
-        c3 = c2; w3 = w2;
-        if (c < c1) {
-          c2 = c1; w2 = w1;
-          if (c < c0) {
-            c1 = c0; w1 = w0;
-            c0 = c; w0 = w;
-          } else {
-            c1 = c; w1 = w;
-          }
+    if (!(c < cb[kPrefs - 1])) continue;
+    // insertion keeps equal costs in index order (strict '<')
+    bool placed = false;
+#pragma unroll
+    for (int q = kPrefs - 1; q > 0; --q) {
+      if (!placed) {
+        if (c < cb[q - 1]) {
+          cb[q] = cb[q - 1];
+          wb[q] = wb[q - 1];
         } else {
-          c2 = c; w2 = w;
+          cb[q] = c;
+          wb[q] = w;
+          placed = true;
         }
-      } else {
-        c3 = c; w3 = w;
       }
     }
+    if (!placed) {
+      cb[0] = c;
+      wb[0] = w;
+    }
   }
-  prefs[t] = static_cast<uint32_t>(w0) | (static_cast<uint32_t>(w1) << 8) |
-             (static_cast<uint32_t>(w2) << 16) | (static_cast<uint32_t>(w3) << 24);
+  uint64_t pk = 0;
+#pragma unroll
+  for (int q = 0; q < kPrefs; ++q) pk |= static_cast<uint64_t>(wb[q]) << (8 * q);
+  prefs[t] = pk;
 }
 
 __global__ void __launch_bounds__(kGreedyThreads)
@@ -86,7 +97,7 @@ __global__ void __launch_bounds__(kGreedyThreads)
              uint64_t n_order, const int32_t* __restrict__ capacity_dev, int cap_uniform,
              int32_t* __restrict__ decision, const uint32_t* __restrict__ row_ids,
              int32_t* __restrict__ pair_worker, int* __restrict__ flags,
-             const uint32_t* __restrict__ prefs) {
+             const uint64_t* __restrict__ prefs) {
   __shared__ int remaining[kMaxWorkers];
   __shared__ int used[kMaxWorkers];
   __shared__ int cnt[kGreedyWarps][kMaxWorkers];
@@ -119,12 +130,12 @@ __global__ void __launch_bounds__(kGreedyThreads)
     if (valid) {
       row = order[t];
       const unsigned long long om = open_mask;
-      // The first of the position's four best (initially open) workers that is
+      // The first of the position's eight best (initially open) workers that is
       // still open is its argmin over the open set: every worker ranked before
-      // it is closed.  Only when all four are closed is the row rescanned.
-      const uint32_t pf = prefs[t];
+      // it is closed.  Only when all eight are closed is the row rescanned.
+      const uint64_t pf = prefs[t];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < kPrefs; ++q) {
         const int w = static_cast<int>((pf >> (8 * q)) & 0xFFu);
         if (choice < 0 && w != 0xFF && ((om >> w) & 1ULL)) choice = w;
       }
@@ -221,7 +232,7 @@ __global__ void __launch_bounds__(kCostThreads)
 void launch_greedy(const double* matrix, uint64_t rows, int n, const uint32_t* order,
                    uint64_t n_order, const int32_t* capacity_dev, int cap_uniform,
                    int32_t* decision, const uint32_t* row_ids, int32_t* pair_worker,
-                   int* flags, uint32_t* prefs, cudaStream_t s) {
+                   int* flags, uint64_t* prefs, cudaStream_t s) {
   (void)rows;
   if (n_order == 0) return;
   k_greedy_prefs<<<static_cast<unsigned>((n_order + 255) / 256), 256, 0, s>>>(
