@@ -534,6 +534,21 @@ void engine_step(edx_engine* e, const int32_t* decision, edx_report* rep) {
 // a CUDA graph captured on first use and replayed while (rows, ids, alpha)
 // stay the same -- the ~40 launches of an iteration become one.  Any capture
 // failure disables graphs for the engine and the iteration runs eagerly.
+// build -> dispatch -> step enqueue, with the step's decision-independent
+// head on the side stream overlapping the build and the dispatch
+void iterate_enqueue(edx_engine* e, double alpha) {
+  if (!e->cur_ids) edx::invalid("no batch loaded");
+  if (!e->profiling) edx::step_head(e);  // profiled runs time the whole step in its phase
+  try {
+    engine_build(e);
+    engine_dispatch(e, alpha);
+    step_enqueue(e, nullptr);
+  } catch (...) {
+    edx::step_head_abandon(e);
+    throw;
+  }
+}
+
 void engine_iterate_core(edx_engine* e, double alpha) {
   if (e->graph_mode < 0) {
     const char* v = std::getenv("EDX_GRAPH");
@@ -542,9 +557,7 @@ void engine_iterate_core(edx_engine* e, double alpha) {
   const bool eligible = e->graph_mode == 1 && e->world == 1 && !e->profiling &&
                         edx::step_device_only(e) && e->cur_ids == e->ids.p;
   if (!eligible) {
-    engine_build(e);
-    engine_dispatch(e, alpha);
-    step_enqueue(e, nullptr);
+    iterate_enqueue(e, alpha);
     return;
   }
   const double a = alpha < 0.0 ? e->alpha : alpha;
@@ -561,9 +574,7 @@ void engine_iterate_core(edx_engine* e, double alpha) {
       e->g_rows = e->rows;
       e->g_total = e->total_ids;
       e->g_alpha = a;
-      engine_build(e);
-      engine_dispatch(e, a);
-      step_enqueue(e, nullptr);
+      iterate_enqueue(e, a);
       return;
     }
     const uint64_t l0 = e->launches;
@@ -572,9 +583,7 @@ void engine_iterate_core(edx_engine* e, double alpha) {
     e->capturing = true;
     bool ok = true;
     try {
-      engine_build(e);
-      engine_dispatch(e, a);
-      step_enqueue(e, nullptr);
+      iterate_enqueue(e, a);
       EDX_CUDA(cudaStreamWaitEvent(e->stream, e->cost_done, 0));  // join decision_cost
     } catch (...) {
       ok = false;
@@ -589,9 +598,7 @@ void engine_iterate_core(edx_engine* e, double alpha) {
       e->gexec = nullptr;
       e->graph_mode = 0;
       e->launches = l0;
-      engine_build(e);
-      engine_dispatch(e, a);
-      step_enqueue(e, nullptr);
+      iterate_enqueue(e, a);
       return;
     }
     e->g_launches = e->launches - l0;
@@ -673,6 +680,9 @@ int edx_engine_create(const edx_cluster_config* cfg, const edx_engine_options* o
     EDX_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
     for (auto& ev : e->ev) EDX_CUDA(cudaEventCreate(&ev));
     EDX_CUDA(cudaEventCreateWithFlags(&e->cost_done, cudaEventDisableTiming));
+    EDX_CUDA(cudaStreamCreateWithFlags(&e->step_side, cudaStreamNonBlocking));
+    EDX_CUDA(cudaEventCreateWithFlags(&e->head_fork, cudaEventDisableTiming));
+    EDX_CUDA(cudaEventCreateWithFlags(&e->head_done, cudaEventDisableTiming));
     e->ol.ensure(e->id_space);
     e->res.ensure(e->id_space);
     EDX_CUDA(cudaMemsetAsync(e->ol.p, 0, e->id_space * sizeof(ulonglong2), e->stream));
@@ -703,6 +713,12 @@ void edx_engine_destroy(edx_engine* e) {
   for (auto& ev : e->ev)
     if (ev) cudaEventDestroy(ev);
   if (e->cost_done) cudaEventDestroy(e->cost_done);
+  if (e->head_fork) cudaEventDestroy(e->head_fork);
+  if (e->head_done) cudaEventDestroy(e->head_done);
+  if (e->step_side) {
+    cudaStreamSynchronize(e->step_side);
+    cudaStreamDestroy(e->step_side);
+  }
   if (e->h_flags) cudaFreeHost(e->h_flags);
   if (e->h_counters) cudaFreeHost(e->h_counters);
   if (e->h_clock) cudaFreeHost(e->h_clock);

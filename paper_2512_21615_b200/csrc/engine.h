@@ -96,6 +96,11 @@ struct edx_engine {
   double* h_expected = nullptr;      // pinned
   uint32_t* h_clock = nullptr;       // pinned: the iteration clock, copied to d_clock in-stream
   edx::DevBuf<uint32_t> d_clock;
+  // the decision-independent head of the step runs on its own stream during
+  // a fused iteration's build and dispatch (step_head / step_run)
+  cudaStream_t step_side = nullptr;
+  cudaEvent_t head_fork = nullptr, head_done = nullptr;
+  bool head_pending = false;
 
   // CUDA graph of one fused iteration (build -> dispatch -> step), replayed
   // while the shape is unchanged; eligible on one GPU, with device-decided

@@ -62,23 +62,26 @@ enum WS : int {
   kWS = 11
 };
 
-__global__ void k_occ_sample(const uint64_t* __restrict__ offsets, uint64_t rows,
-                             uint32_t* __restrict__ occ_sample) {
+// Head of the step: zero the counters and per-worker scalars, map each id
+// position to its sample, and the first position of every id.
+__global__ void k_step_begin(const uint64_t* __restrict__ offsets, uint64_t rows,
+                             uint32_t* __restrict__ occ_sample, const uint32_t* __restrict__ ids,
+                             uint64_t T, int32_t* __restrict__ first_pos,
+                             unsigned long long* __restrict__ counters, uint32_t ncnt,
+                             uint32_t* __restrict__ ws, uint32_t nws) {
   const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  if (i >= rows) return;
-  for (uint64_t p = offsets[i]; p < offsets[i + 1]; ++p) occ_sample[p] = static_cast<uint32_t>(i);
-}
-
-__global__ void k_first_pos(const uint32_t* __restrict__ ids, uint64_t T,
-                            int32_t* __restrict__ first_pos) {
-  const uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  if (p >= T) return;
-  // Zipf-hot ids occur in thousands of samples: test before the atomic.  The
-  // table only decreases, so a stale read is >= the true minimum -- skipping
-  // when it is already <= p is exact -- and CTAs run roughly in position
-  // order, so a hot id's minimum is in place after its first few occurrences.
-  int32_t* slot = first_pos + ids[p];
-  if (*slot > static_cast<int32_t>(p)) atomicMin(slot, static_cast<int32_t>(p));
+  if (i < ncnt) counters[i] = 0;
+  if (i < nws) ws[i] = 0;
+  if (i < rows)
+    for (uint64_t p = offsets[i]; p < offsets[i + 1]; ++p) occ_sample[p] = static_cast<uint32_t>(i);
+  if (i < T) {
+    // Zipf-hot ids occur in thousands of samples: test before the atomic.  The
+    // table only decreases, so a stale read is >= the true minimum -- skipping
+    // when it is already <= p is exact -- and CTAs run roughly in position
+    // order, so a hot id's minimum is in place after its first few occurrences.
+    int32_t* slot = first_pos + ids[i];
+    if (*slot > static_cast<int32_t>(i)) atomicMin(slot, static_cast<int32_t>(i));
+  }
 }
 
 __global__ void k_unique_flag(const uint32_t* __restrict__ ids, uint64_t T,
@@ -139,12 +142,27 @@ __global__ void k_need_keys(const uint32_t* __restrict__ ids, uint64_t T,
 
 // Phase 1: on-demand update push (sim.hpp:119-153).  set_version(false) on
 // stale copies is the `latest` mask update itself (version == latest bit).
+// Block 0 also lays out the per-worker need CSR (need items are sorted by
+// worker, then position) and the phase-2 scalars.
 __global__ void k_phase1(const uint32_t* __restrict__ uniq,
                          const unsigned long long* __restrict__ umask,
                          const unsigned long long* counters_ro, int n,
-                         ulonglong2* __restrict__ ol, unsigned long long* counters) {
+                         ulonglong2* __restrict__ ol, unsigned long long* counters,
+                         uint32_t* __restrict__ ws, const uint32_t* __restrict__ size,
+                         uint64_t capacity) {
   __shared__ unsigned int push[kMaxWorkers];
   if (threadIdx.x < kMaxWorkers) push[threadIdx.x] = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    uint32_t run = 0;
+    for (int j = 0; j < n; ++j) {
+      ws[j * kWS + kWsNeedOff] = run;
+      run += ws[j * kWS + kWsNeeds];
+      ws[j * kWS + kWsSize0] = size[j];
+      ws[j * kWS + kWsFree] = static_cast<uint32_t>(capacity - size[j]);
+      ws[j * kWS + kWsAdvance] = UINT_MAX;
+    }
+    counters[3 * n + 2] = run;
+  }
   __syncthreads();
   const uint64_t U = counters_ro[3 * n + 1];
   const uint64_t u = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
@@ -171,21 +189,6 @@ __global__ void k_phase1(const uint32_t* __restrict__ uniq,
   __syncthreads();
   if (threadIdx.x < n && push[threadIdx.x])
     atomicAdd(counters + n + threadIdx.x, static_cast<unsigned long long>(push[threadIdx.x]));
-}
-
-// per-worker need CSR offsets (need items are sorted by worker, then position)
-__global__ void k_need_offsets(int n, uint32_t* __restrict__ ws, const uint32_t* __restrict__ size,
-                               uint64_t capacity, unsigned long long* counters) {
-  if (threadIdx.x != 0) return;
-  uint32_t run = 0;
-  for (int j = 0; j < n; ++j) {
-    ws[j * kWS + kWsNeedOff] = run;
-    run += ws[j * kWS + kWsNeeds];
-    ws[j * kWS + kWsSize0] = size[j];
-    ws[j * kWS + kWsFree] = static_cast<uint32_t>(capacity - size[j]);
-    ws[j * kWS + kWsAdvance] = UINT_MAX;
-  }
-  counters[3 * n + 2] = run;
 }
 
 __device__ __forceinline__ int item_worker(uint64_t key) { return static_cast<int>(key >> 32); }
@@ -383,6 +386,65 @@ __global__ void k_cand_offsets(const int32_t* __restrict__ wlist, int nw, uint32
   }
 }
 
+// Register part of the victims' bitonic sort: thread t holds elements
+// [4t, 4t+4) in (rk, rs); runs the stages (size, stride), (size, stride/2),
+// ... (size, 1) for stride <= 64.
+__device__ __forceinline__ void bitonic_load4(const uint64_t* sk, const uint32_t* ss, int tid,
+                                              uint64_t (&rk)[4], uint32_t (&rs)[4]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    rk[q] = sk[4 * tid + q];
+    rs[q] = ss[4 * tid + q];
+  }
+}
+
+__device__ __forceinline__ void bitonic_store4(uint64_t* sk, uint32_t* ss, int tid,
+                                               const uint64_t (&rk)[4], const uint32_t (&rs)[4]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    sk[4 * tid + q] = rk[q];
+    ss[4 * tid + q] = rs[q];
+  }
+}
+
+template <int S>
+__device__ __forceinline__ void bitonic_in_thread(int tid, uint32_t size, uint64_t (&rk)[4],
+                                                  uint32_t (&rs)[4]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if (q & S) continue;
+    const uint32_t i = 4 * static_cast<uint32_t>(tid) + q;
+    if ((rk[q] > rk[q + S]) == ((i & size) == 0)) {
+      const uint64_t tk = rk[q];
+      rk[q] = rk[q + S];
+      rk[q + S] = tk;
+      const uint32_t ts = rs[q];
+      rs[q] = rs[q + S];
+      rs[q + S] = ts;
+    }
+  }
+}
+
+__device__ __forceinline__ void bitonic_reg_stages(int tid, uint32_t size, uint32_t stride,
+                                                   uint64_t (&rk)[4], uint32_t (&rs)[4]) {
+  for (; stride >= 4; stride >>= 1) {
+    const int lx = static_cast<int>(stride >> 2);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t i = 4 * static_cast<uint32_t>(tid) + q;
+      const uint64_t ok = __shfl_xor_sync(0xffffffffu, rk[q], lx);
+      const uint32_t os = __shfl_xor_sync(0xffffffffu, rs[q], lx);
+      const bool asc = (i & size) == 0, lower = (i & stride) == 0;
+      if (lower == asc ? (ok < rk[q]) : (ok > rk[q])) {
+        rk[q] = ok;
+        rs[q] = os;
+      }
+    }
+  }
+  if (stride >= 2) bitonic_in_thread<2>(tid, size, rk, rs);
+  bitonic_in_thread<1>(tid, size, rk, rs);
+}
+
 // Victim selection for caches of up to kSelCap entries: one CTA per worker.
 // The CTA finds its non-pinned entries, the per-worker value ranges of
 // (mark, frequency, last_access, id), packs each VictimKey (cache.hpp:47-58)
@@ -402,6 +464,7 @@ __global__ void __launch_bounds__(kSelThreads, 1)
                      const uint32_t* __restrict__ slast, const ulonglong2* __restrict__ ol,
                      const int32_t* __restrict__ first_pos, const uint32_t* __restrict__ uidx,
                      uint64_t ucap, const int32_t* __restrict__ need_first,
+                     const uint32_t* __restrict__ ins_scan,
                      uint32_t* __restrict__ cand_slot_sorted, int* __restrict__ flags) {
   extern __shared__ __align__(16) uint8_t smem[];
   auto& temp = *reinterpret_cast<typename SelSort::TempStorage*>(smem);
@@ -409,8 +472,16 @@ __global__ void __launch_bounds__(kSelThreads, 1)
   __shared__ uint32_t tot[9];
   const int j = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint32_t* w = ws + j * kWS;
-  const uint32_t E = w[kWsEvict];
+  // inserts and evictions of worker j (evict_for, cache.hpp:152-170)
+  const uint32_t nb0 = w[kWsNeedOff], ins0 = ins_scan[nb0];
+  const uint32_t ins = ins_scan[nb0 + w[kWsNeeds]] - ins0, fr = w[kWsFree];
+  const uint32_t E = ins > fr ? ins - fr : 0;
   const uint64_t gb = static_cast<uint64_t>(j) * capacity;
+  if (tid == 0) {
+    w[kWsInserts] = ins;
+    w[kWsInsBase] = ins0;
+    w[kWsEvict] = E;
+  }
   if (E == 0) {
     if (tid == 0) {
       w[kWsCand] = 0;
@@ -422,15 +493,33 @@ __global__ void __launch_bounds__(kSelThreads, 1)
   bool cf[kSelItems];
   // v[0..3] = min of mark, freq, last, id; v[4..7] = max; v[8] = candidates
   uint32_t v[9] = {UINT_MAX, UINT_MAX, UINT_MAX, UINT_MAX, 0, 0, 0, 0, 0};
+  {
+    // level by level so all of a thread's items have their loads in flight
+    // together (the pinned test is a chain of four dependent gathers)
+    uint32_t id[kSelItems];
+    int32_t fp[kSelItems];
 #pragma unroll
-  for (int k = 0; k < kSelItems; ++k) {
-    const uint32_t sl = tid * kSelItems + k;
-    cf[k] = false;
-    if (sl < size0) {
-      const uint32_t id = sid[gb + sl];
-      if (!pinned_by(j, id, first_pos, uidx, ucap, need_first)) {
-        cf[k] = true;
-        const uint32_t f[4] = {smark[gb + sl], sfreq[gb + sl], slast[gb + sl], id};
+    for (int k = 0; k < kSelItems; ++k) {
+      const uint32_t sl = tid * kSelItems + k;
+      id[k] = sl < size0 ? sid[gb + sl] : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < kSelItems; ++k)
+      fp[k] = tid * kSelItems + k < size0 ? first_pos[id[k]] : INT_MAX;
+#pragma unroll
+    for (int k = 0; k < kSelItems; ++k)
+      fp[k] = fp[k] != INT_MAX ? static_cast<int32_t>(uidx[fp[k]]) : -1;
+#pragma unroll
+    for (int k = 0; k < kSelItems; ++k) {
+      const bool pinned = fp[k] >= 0 &&
+          need_first[static_cast<uint64_t>(j) * ucap + static_cast<uint32_t>(fp[k])] != INT_MAX;
+      cf[k] = tid * kSelItems + k < size0 && !pinned;
+    }
+#pragma unroll
+    for (int k = 0; k < kSelItems; ++k) {
+      if (cf[k]) {
+        const uint32_t sl = tid * kSelItems + k;
+        const uint32_t f[4] = {smark[gb + sl], sfreq[gb + sl], slast[gb + sl], id[k]};
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           v[q] = min(v[q], f[q]);
@@ -506,10 +595,15 @@ __global__ void __launch_bounds__(kSelThreads, 1)
       const int nb = min(8, W - done), shift = W - done - nb;
       for (int x = tid; x < 256; x += kSelThreads) hist[x] = 0;
       __syncthreads();
+      // the leading digits are shared by most keys: one shared atomic per
+      // (warp, bin) group instead of one per key
 #pragma unroll
-      for (int k = 0; k < kSelItems; ++k)
-        if (cf[k] && (keys[k] >> (shift + nb)) == prefix)
-          atomicAdd(&hist[(keys[k] >> shift) & ((1u << nb) - 1u)], 1u);
+      for (int k = 0; k < kSelItems; ++k) {
+        const bool in = cf[k] && (keys[k] >> (shift + nb)) == prefix;
+        const int bin = in ? static_cast<int>((keys[k] >> shift) & ((1u << nb) - 1u)) : -1;
+        const unsigned grp = __match_any_sync(0xffffffffu, bin);
+        if (in && lane == __ffs(grp) - 1) atomicAdd(&hist[bin], static_cast<uint32_t>(__popc(grp)));
+      }
       __syncthreads();
       if (warp == 0) {
         uint32_t h[8], sum = 0;
@@ -546,18 +640,36 @@ __global__ void __launch_bounds__(kSelThreads, 1)
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < kSelItems; ++k) {
-      if (cf[k] && keys[k] <= prefix) {
-        const uint32_t q = atomicAdd(&s_cnt, 1u);
+      const bool sel = cf[k] && keys[k] <= prefix;
+      const unsigned bal = __ballot_sync(0xffffffffu, sel);
+      uint32_t base = 0;
+      if (lane == 0 && bal) base = atomicAdd(&s_cnt, static_cast<uint32_t>(__popc(bal)));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (sel) {
+        const uint32_t q = base + __popc(bal & ((1u << lane) - 1u));
         sk[q] = keys[k];
         ss[q] = slots[k];
       }
     }
-    uint32_t P = 2;
+    // Bitonic sort of the take keys (padded to P >= 128 with all-ones keys,
+    // which sort last).  Thread t owns elements [4t, 4t+4): strides 1 and 2
+    // are in-register, strides 4..64 are warp shuffles (the partner sits in
+    // lane ^ stride/4, same register), strides >= 128 go through shared memory.
+    uint32_t P = 128;
     while (P < take) P <<= 1;
     for (uint32_t x = take + tid; x < P; x += kSelThreads) sk[x] = ~0ULL;
     __syncthreads();
-    for (uint32_t size = 2; size <= P; size <<= 1) {
-      for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+    const bool owner = 4 * static_cast<uint32_t>(tid) < P;  // warp-uniform (P % 128 == 0)
+    uint64_t rk[4];
+    uint32_t rs[4];
+    if (owner) {
+      bitonic_load4(sk, ss, tid, rk, rs);
+      for (uint32_t size = 2; size <= 128; size <<= 1) bitonic_reg_stages(tid, size, size >> 1, rk, rs);
+      bitonic_store4(sk, ss, tid, rk, rs);
+    }
+    __syncthreads();
+    for (uint32_t size = 256; size <= P; size <<= 1) {
+      for (uint32_t stride = size >> 1; stride >= 128; stride >>= 1) {
         for (uint32_t t = tid; t < P / 2; t += kSelThreads) {
           const uint32_t lo = 2 * t - (t & (stride - 1)), hi = lo + stride;
           const uint64_t a = sk[lo], b = sk[hi];
@@ -571,6 +683,12 @@ __global__ void __launch_bounds__(kSelThreads, 1)
         }
         __syncthreads();
       }
+      if (owner) {
+        bitonic_load4(sk, ss, tid, rk, rs);
+        bitonic_reg_stages(tid, size, 64, rk, rs);
+        bitonic_store4(sk, ss, tid, rk, rs);
+      }
+      __syncthreads();
     }
     for (uint32_t r = tid; r < take; r += kSelThreads) cand_slot_sorted[gb + r] = ss[r];
   }
@@ -608,13 +726,14 @@ __global__ void k_evict_contrib(const uint64_t* __restrict__ items,
 
 // maybe_advance_mark (cache.hpp:187-192) at the first evicting insert whose
 // running at_current_mark equals the capacity.
-__global__ void k_find_advance(const uint64_t* __restrict__ items,
-                               const unsigned long long* counters_ro, int n,
-                               const uint8_t* __restrict__ type, const uint32_t* __restrict__ ins_scan,
-                               const int32_t* __restrict__ con_scan, uint32_t* __restrict__ ws,
-                               const unsigned long long* __restrict__ at_cur, uint64_t capacity) {
+__device__ __forceinline__ void find_advance(uint64_t q, const uint64_t* __restrict__ items,
+                                             const unsigned long long* counters_ro, int n,
+                                             const uint8_t* __restrict__ type,
+                                             const uint32_t* __restrict__ ins_scan,
+                                             const int32_t* __restrict__ con_scan, uint32_t* ws,
+                                             const unsigned long long* __restrict__ at_cur,
+                                             uint64_t capacity) {
   const uint64_t N = counters_ro[3 * n + 2];
-  const uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (q >= N || type[q] != 2) return;
   const int j = item_worker(items[q]);
   uint32_t* w = ws + j * kWS;
@@ -626,19 +745,22 @@ __global__ void k_find_advance(const uint64_t* __restrict__ items,
 }
 
 // evictions: clear the victim's bits of worker j (sim.hpp:177-184)
-__global__ void k_evict(const int32_t* __restrict__ wlist, int nw, const uint32_t* __restrict__ ws,
-                        const uint32_t* __restrict__ cand_slot, const uint32_t* __restrict__ sid,
-                        uint64_t capacity, uint64_t id_space, ulonglong2* __restrict__ ol,
-                        unsigned long long* __restrict__ res, int32_t* __restrict__ slot_of,
-                        uint32_t* __restrict__ victim_id, unsigned long long* counters,
-                        int n) {
-  const int jl = blockIdx.y;
-  if (jl >= nw) return;
+// (bx, jl) = (block within the worker, evicting worker), kEvictBlocks per worker
+constexpr unsigned kEvictBlocks = 8;
+__device__ __forceinline__ void evict_victims(unsigned bx, int jl, const int32_t* __restrict__ wlist,
+                                              const uint32_t* ws,
+                                              const uint32_t* __restrict__ cand_slot,
+                                              const uint32_t* __restrict__ sid, uint64_t capacity,
+                                              uint64_t id_space, ulonglong2* __restrict__ ol,
+                                              unsigned long long* __restrict__ res,
+                                              int32_t* __restrict__ slot_of,
+                                              uint32_t* __restrict__ victim_id,
+                                              unsigned long long* counters, int n) {
   const int j = wlist[jl];
   const uint32_t* w = ws + j * kWS;
   const uint32_t E = min(w[kWsEvict], w[kWsCand]);
   unsigned int pushes = 0;
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < E; t += gridDim.x * blockDim.x) {
+  for (uint32_t t = bx * blockDim.x + threadIdx.x; t < E; t += kEvictBlocks * blockDim.x) {
     const uint32_t vs = cand_slot[w[kWsCandOff] + t];
     const uint64_t g = static_cast<uint64_t>(j) * capacity + vs;
     const uint32_t id = sid[g];
@@ -655,6 +777,30 @@ __global__ void k_evict(const int32_t* __restrict__ wlist, int nw, const uint32_
   if ((threadIdx.x & 31) == 0 && pushes) atomicAdd(counters + 2 * n + j, static_cast<unsigned long long>(pushes));
 }
 
+// The epoch-advance search (blocks [0, ga)) and the evictions (kEvictBlocks
+// blocks per evicting worker after them) are independent: one launch.
+__global__ void k_advance_evict(uint32_t ga, const uint64_t* __restrict__ items,
+                                const unsigned long long* counters_ro, int n,
+                                const uint8_t* __restrict__ type,
+                                const uint32_t* __restrict__ ins_scan,
+                                const int32_t* __restrict__ con_scan, uint32_t* ws,
+                                const unsigned long long* __restrict__ at_cur, uint64_t capacity,
+                                const int32_t* __restrict__ wlist,
+                                const uint32_t* __restrict__ cand_slot,
+                                const uint32_t* __restrict__ sid, uint64_t id_space,
+                                ulonglong2* __restrict__ ol, unsigned long long* __restrict__ res,
+                                int32_t* __restrict__ slot_of, uint32_t* __restrict__ victim_id,
+                                unsigned long long* counters) {
+  if (blockIdx.x < ga) {
+    find_advance(blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x, items, counters_ro, n,
+                 type, ins_scan, con_scan, ws, at_cur, capacity);
+  } else {
+    const unsigned b = blockIdx.x - ga;
+    evict_victims(b % kEvictBlocks, static_cast<int>(b / kEvictBlocks), wlist, ws, cand_slot, sid,
+                  capacity, id_space, ol, res, slot_of, victim_id, counters, n);
+  }
+}
+
 // touches and inserts (WorkerCache::touch, cache.hpp:102-122; sim.hpp:172,186-188)
 __global__ void k_apply(const uint64_t* __restrict__ items,
                         const unsigned long long* counters_ro, int n,
@@ -666,13 +812,24 @@ __global__ void k_apply(const uint64_t* __restrict__ items,
                         ulonglong2* __restrict__ ol, unsigned long long* __restrict__ res,
                         int32_t* __restrict__ slot_of, uint32_t* __restrict__ sid,
                         uint32_t* __restrict__ smark, uint32_t* __restrict__ sfreq,
-                        uint32_t* __restrict__ slast) {
+                        uint32_t* __restrict__ slast, const int32_t* __restrict__ first_pos,
+                        const uint32_t* __restrict__ uidx, uint64_t ucap,
+                        int32_t* __restrict__ need_first, uint32_t* __restrict__ need_cnt) {
   const uint32_t clock = *clock_dev;
   const uint64_t N = counters_ro[3 * n + 2];
   const uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (q >= N) return;
   const int j = item_worker(items[q]);
   const uint32_t id = ids[item_pos(items[q])];
+  {
+    // reset this need item's (worker, id) cell for the next step; nothing
+    // after the victim selection reads the need tables.  uidx at a worker's
+    // first occurrence of the id is the id's unique index only when that is
+    // also the id's first occurrence: go through first_pos.
+    const uint64_t x = static_cast<uint64_t>(j) * ucap + uidx[first_pos[id]];
+    need_first[x] = INT_MAX;
+    need_cnt[x] = 0;
+  }
   const uint32_t* w = ws + j * kWS;
   const uint32_t local = static_cast<uint32_t>(q) - w[kWsNeedOff];
   const uint32_t mark = cur_mark[j] + (local >= w[kWsAdvance] ? 1u : 0u);
@@ -701,68 +858,47 @@ __global__ void k_apply(const uint64_t* __restrict__ items,
   atomicOr(res + id, bit);
 }
 
-__global__ void k_worker_finalize(int n, const uint32_t* __restrict__ ws,
-                                  const int32_t* __restrict__ con_scan, uint32_t* __restrict__ size,
-                                  uint32_t* __restrict__ cur_mark,
-                                  unsigned long long* __restrict__ at_cur) {
-  const int j = threadIdx.x;
-  if (j >= n) return;
-  const uint32_t* w = ws + j * kWS;
-  const uint32_t E = min(w[kWsEvict], w[kWsCand]);
-  size[j] = w[kWsSize0] + w[kWsInserts] - E;
-  const uint32_t b = w[kWsNeedOff], cnt = w[kWsNeeds];
-  if (w[kWsAdvance] != UINT_MAX) {
-    cur_mark[j] += 1;
-    at_cur[j] = cnt - w[kWsAdvance];
-  } else {
-    at_cur[j] += static_cast<unsigned long long>(con_scan[b + cnt] - con_scan[b]);
+// Tail of the step: per-worker sizes and epoch state (block 0), phase 3
+// ownership hand-over (sim.hpp:192-204), and the reset of the per-id tables
+// for the next step.
+__global__ void k_step_tail(int n, const uint32_t* __restrict__ ws,
+                            const int32_t* __restrict__ con_scan, uint32_t* __restrict__ size,
+                            uint32_t* __restrict__ cur_mark, unsigned long long* __restrict__ at_cur,
+                            const uint32_t* __restrict__ uniq,
+                            const unsigned long long* counters_ro, ulonglong2* __restrict__ ol,
+                            int32_t* __restrict__ first_pos, unsigned long long* __restrict__ umask) {
+  if (blockIdx.x == 0 && threadIdx.x < n) {
+    const int j = threadIdx.x;
+    const uint32_t* w = ws + j * kWS;
+    const uint32_t E = min(w[kWsEvict], w[kWsCand]);
+    size[j] = w[kWsSize0] + w[kWsInserts] - E;
+    const uint32_t b = w[kWsNeedOff], cnt = w[kWsNeeds];
+    if (w[kWsAdvance] != UINT_MAX) {
+      cur_mark[j] += 1;
+      at_cur[j] = cnt - w[kWsAdvance];
+    } else {
+      at_cur[j] += static_cast<unsigned long long>(con_scan[b + cnt] - con_scan[b]);
+    }
   }
-}
-
-// Phase 3: ownership hand-over (sim.hpp:192-204)
-__global__ void k_phase3(const uint32_t* __restrict__ uniq,
-                         const unsigned long long* __restrict__ umask,
-                         const unsigned long long* counters_ro, int n,
-                         ulonglong2* __restrict__ ol) {
   const uint64_t U = counters_ro[3 * n + 1];
   const uint64_t u = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (u >= U) return;
   const unsigned long long m = umask[u];
-  ol[uniq[u]] = make_ulonglong2(m, m);
+  const uint32_t id = uniq[u];
+  ol[id] = make_ulonglong2(m, m);
+  first_pos[id] = INT_MAX;
+  umask[u] = 0;
 }
 
-__global__ void k_reset(const uint32_t* __restrict__ uniq,
-                        const unsigned long long* counters_ro, int n,
-                        const uint64_t* __restrict__ items, const uint32_t* __restrict__ ids,
-                        const uint32_t* __restrict__ uidx, uint64_t ucap,
-                        int32_t* __restrict__ first_pos, unsigned long long* __restrict__ umask,
-                        int32_t* __restrict__ need_first, uint32_t* __restrict__ need_cnt) {
-  const uint64_t U = counters_ro[3 * n + 1], N = counters_ro[3 * n + 2];
-  const uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  if (x < N) {
-    const uint64_t key = items[x];
-    const uint32_t p = item_pos(key);
-    // uidx at a worker's first occurrence of the id is the id's unique index
-    // only when that is also the id's first occurrence; go through first_pos.
-    const int j = item_worker(key);
-    const uint32_t u = uidx[first_pos[ids[p]]];
-    need_first[static_cast<uint64_t>(j) * ucap + u] = INT_MAX;
-    need_cnt[static_cast<uint64_t>(j) * ucap + u] = 0;
-  }
-  (void)U;
-  (void)uniq;
-  (void)umask;
-}
-
+// Clears the per-id tables of a batch whose step head ran but whose step
+// never did (the iteration failed in between).
 __global__ void k_reset_unique(const uint32_t* __restrict__ uniq,
                                const unsigned long long* counters_ro, int n,
-                               int32_t* __restrict__ first_pos,
-                               unsigned long long* __restrict__ umask) {
+                               int32_t* __restrict__ first_pos) {
   const uint64_t U = counters_ro[3 * n + 1];
   const uint64_t u = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (u >= U) return;
   first_pos[uniq[u]] = INT_MAX;
-  umask[u] = 0;
 }
 
 __global__ void k_fill_i32(int32_t* p, uint64_t n, int32_t v) {
@@ -862,32 +998,69 @@ void cub_call(edx_engine* e, F&& f) {
 
 bool step_device_only(const edx_engine* e) { return e->capacity <= kSelCap; }
 
-void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
-  cudaStream_t st = e->stream;
+namespace {
+
+// The decision-independent head of the step on stream `st`: the iteration
+// clock, zeroed counters, the sample of every id position, and the unique ids
+// of the batch in first-occurrence order.  Returns the kernels launched.
+int launch_step_head(edx_engine* e, cudaStream_t st) {
   auto& s = e->step;
-  auto& c = e->cache;
   const int n = e->n;
-  const uint64_t T = e->total_ids, R = e->rows, ucap = e->max_ids;
+  const uint64_t T = e->total_ids, R = e->rows;
   // the clock goes through pinned memory so a captured graph reads each
   // iteration's value at replay time
   *e->h_clock = static_cast<uint32_t>(e->clock);
   EDX_CUDA(cudaMemcpyAsync(e->d_clock.p, e->h_clock, sizeof(uint32_t), cudaMemcpyHostToDevice, st));
-  int launches = 0;
-
-  EDX_CUDA(cudaMemsetAsync(s.counters.p, 0, (3 * n + 4) * sizeof(unsigned long long), st));
-  EDX_CUDA(cudaMemsetAsync(s.wscalars.p, 0, n * kWS * sizeof(uint32_t), st));
-
-  k_occ_sample<<<grid_for(R), kT, 0, st>>>(e->cur_offsets, R, s.occ_sample.p);
-  k_first_pos<<<grid_for(T), kT, 0, st>>>(e->cur_ids, T, s.first_pos.p);
+  const uint32_t ncnt = static_cast<uint32_t>(3 * n + 4), nws = static_cast<uint32_t>(n * kWS);
+  const uint64_t span = std::max<uint64_t>(std::max<uint64_t>(R, T), nws);
+  k_step_begin<<<grid_for(span), kT, 0, st>>>(e->cur_offsets, R, s.occ_sample.p, e->cur_ids, T,
+                                              s.first_pos.p, s.counters.p, ncnt, s.wscalars.p, nws);
   k_unique_flag<<<grid_for(T + 1), kT, 0, st>>>(e->cur_ids, T, s.first_pos.p, s.flag_scan.p);
   EDX_LAUNCHED();
-  launches += 3;
   cub_call(e, [&](void* tmp, size_t& b) {
     return cub::DeviceScan::ExclusiveSum(tmp, b, s.flag_scan.p, s.uidx_of_pos.p,
                                          static_cast<int>(T + 1), st);
   });
   k_unique_scatter<<<grid_for(T + 1), kT, 0, st>>>(e->cur_ids, T, s.first_pos.p, s.uidx_of_pos.p,
                                                    s.uniq.p, s.counters.p, n);
+  EDX_LAUNCHED();
+  return 5;
+}
+
+}  // namespace
+
+void step_head(edx_engine* e) {
+  if (e->head_pending) return;
+  EDX_CUDA(cudaEventRecord(e->head_fork, e->stream));
+  EDX_CUDA(cudaStreamWaitEvent(e->step_side, e->head_fork, 0));
+  e->launches += launch_step_head(e, e->step_side);
+  EDX_CUDA(cudaEventRecord(e->head_done, e->step_side));
+  e->head_pending = true;
+}
+
+void step_head_abandon(edx_engine* e) {
+  if (!e->head_pending) return;
+  e->head_pending = false;
+  if (e->capturing) return;  // the captured head never ran
+  EDX_CUDA(cudaStreamWaitEvent(e->stream, e->head_done, 0));
+  k_reset_unique<<<grid_for(e->total_ids), kT, 0, e->stream>>>(e->step.uniq.p, e->step.counters.p,
+                                                               e->n, e->step.first_pos.p);
+  EDX_LAUNCHED();
+}
+
+void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
+  cudaStream_t st = e->stream;
+  auto& s = e->step;
+  auto& c = e->cache;
+  const int n = e->n;
+  const uint64_t T = e->total_ids, ucap = e->max_ids;
+  int launches = 0;
+  if (e->head_pending) {  // launched by the fused iteration, overlapping the dispatch
+    EDX_CUDA(cudaStreamWaitEvent(st, e->head_done, 0));
+    e->head_pending = false;
+  } else {
+    launches += launch_step_head(e, st);
+  }
   k_needs<<<grid_for(T), kT, 0, st>>>(e->cur_ids, T, s.occ_sample.p, d_decision, s.first_pos.p,
                                       s.uidx_of_pos.p, ucap, s.need_first.p, s.need_cnt.p,
                                       s.umask.p);
@@ -895,7 +1068,7 @@ void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
                                           s.uidx_of_pos.p, ucap, s.need_first.p, s.need_key.p,
                                           s.wscalars.p);
   EDX_LAUNCHED();
-  launches += 5;
+  launches += 2;
   int wbits = 1;
   while ((1 << wbits) < n) ++wbits;
   cub_call(e, [&](void* tmp, size_t& b) {
@@ -904,23 +1077,26 @@ void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
     return cub::DeviceRadixSort::SortKeys(tmp, b, s.need_key.p, s.need_key_sorted.p,
                                           static_cast<int>(T), 32, 32 + wbits + 1, st);
   });
-  launches += 4;
-  k_phase1<<<grid_for(T), kT, 0, st>>>(s.uniq.p, s.umask.p, s.counters.p, n, e->ol.p, s.counters.p);
-  k_need_offsets<<<1, 32, 0, st>>>(n, s.wscalars.p, c.size.p, e->capacity, s.counters.p);
+  launches += 3;
+  k_phase1<<<grid_for(T), kT, 0, st>>>(s.uniq.p, s.umask.p, s.counters.p, n, e->ol.p, s.counters.p,
+                                       s.wscalars.p, c.size.p, e->capacity);
   k_classify<<<grid_for(T + 1), kT, 0, st>>>(
       s.need_key_sorted.p, s.counters.p, n, e->cur_ids, s.first_pos.p, s.uidx_of_pos.p, ucap,
       s.need_cnt.p, e->ol.p, e->res.p, e->id_space, c.slot_of.p, e->capacity, c.smark.p,
       c.cur_mark.p, s.need_type.p, s.flag_scan.p, s.need_contrib.p, s.counters.p);
   EDX_LAUNCHED();
-  launches += 3;
+  launches += 2;
   // insert ordinals: exclusive scan over the (worker-grouped) need items
   cub_call(e, [&](void* tmp, size_t& b) {
     return cub::DeviceScan::ExclusiveSum(tmp, b, s.flag_scan.p, s.ins_rank.p,
                                          static_cast<int>(T + 1), st);
   });
-  k_worker_inserts<<<1, 64, 0, st>>>(n, s.ins_rank.p, s.wscalars.p, e->flags.p);
-  EDX_LAUNCHED();
   launches += 2;
+  if (e->capacity > kSelCap) {
+    k_worker_inserts<<<1, 64, 0, st>>>(n, s.ins_rank.p, s.wscalars.p, e->flags.p);
+    EDX_LAUNCHED();
+    launches += 1;
+  }
 
   // Victim selection (evict_for, cache.hpp:152-170), every worker at once;
   // workers without evictions drop out on the device.
@@ -929,7 +1105,8 @@ void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
   if (e->capacity <= kSelCap) {
     k_select_victims<<<n, kSelThreads, sizeof(typename SelSort::TempStorage), st>>>(
         e->capacity, s.wscalars.p, c.sid.p, c.smark.p, c.sfreq.p, c.slast.p, e->ol.p,
-        s.first_pos.p, s.uidx_of_pos.p, ucap, s.need_first.p, s.cand_slot_sorted.p, e->flags.p);
+        s.first_pos.p, s.uidx_of_pos.p, ucap, s.need_first.p, s.ins_rank.p, s.cand_slot_sorted.p,
+        e->flags.p);
     EDX_LAUNCHED();
     launches += 1;
   } else {
@@ -993,32 +1170,27 @@ void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
                                          static_cast<int>(T + 1), st);
   });
   const int32_t* con_scan = reinterpret_cast<const int32_t*>(s.flag_scan.p);
-  k_find_advance<<<grid_for(T), kT, 0, st>>>(s.need_key_sorted.p, s.counters.p, n, s.need_type.p,
-                                             s.ins_rank.p, con_scan, s.wscalars.p, c.at_cur.p,
-                                             e->capacity);
-  if (nw > 0) {
-    dim3 g(8, nw);
+  {
+    const unsigned ga = grid_for(T);
     const int32_t* wlv = e->capacity <= kSelCap ? d_wlist : d_wlist + 64;
-    k_evict<<<g, kT, 0, st>>>(wlv, nw, s.wscalars.p, s.cand_slot_sorted.p, c.sid.p,
-                              e->capacity, e->id_space, e->ol.p, e->res.p, c.slot_of.p,
-                              s.cand_count.p, s.counters.p, n);
+    k_advance_evict<<<ga + kEvictBlocks * static_cast<unsigned>(nw), kT, 0, st>>>(
+        ga, s.need_key_sorted.p, s.counters.p, n, s.need_type.p, s.ins_rank.p, con_scan,
+        s.wscalars.p, c.at_cur.p, e->capacity, wlv, s.cand_slot_sorted.p, c.sid.p, e->id_space,
+        e->ol.p, e->res.p, c.slot_of.p, s.cand_count.p, s.counters.p);
   }
   EDX_LAUNCHED();
-  launches += 5;
+  launches += 3;  // contribution, scan (2), advance + evict
   k_apply<<<grid_for(T), kT, 0, st>>>(s.need_key_sorted.p, s.counters.p, n, e->cur_ids,
                                       s.need_type.p, s.ins_rank.p, s.wscalars.p,
                                       s.cand_slot_sorted.p, e->capacity, e->id_space, c.cur_mark.p,
                                       e->d_clock.p, e->ol.p, e->res.p, c.slot_of.p, c.sid.p,
-                                      c.smark.p, c.sfreq.p, c.slast.p);
-  k_worker_finalize<<<1, 64, 0, st>>>(n, s.wscalars.p, con_scan, c.size.p, c.cur_mark.p,
-                                      c.at_cur.p);
-  k_phase3<<<grid_for(T), kT, 0, st>>>(s.uniq.p, s.umask.p, s.counters.p, n, e->ol.p);
-  k_reset<<<grid_for(T), kT, 0, st>>>(s.uniq.p, s.counters.p, n, s.need_key_sorted.p, e->cur_ids,
-                                      s.uidx_of_pos.p, ucap, s.first_pos.p, s.umask.p,
-                                      s.need_first.p, s.need_cnt.p);
-  k_reset_unique<<<grid_for(T), kT, 0, st>>>(s.uniq.p, s.counters.p, n, s.first_pos.p, s.umask.p);
+                                      c.smark.p, c.sfreq.p, c.slast.p, s.first_pos.p,
+                                      s.uidx_of_pos.p, ucap, s.need_first.p, s.need_cnt.p);
+  k_step_tail<<<grid_for(T), kT, 0, st>>>(n, s.wscalars.p, con_scan, c.size.p, c.cur_mark.p,
+                                          c.at_cur.p, s.uniq.p, s.counters.p, e->ol.p,
+                                          s.first_pos.p, s.umask.p);
   EDX_LAUNCHED();
-  launches += 5;
+  launches += 2;
   EDX_CUDA(cudaMemcpyAsync(e->h_counters, s.counters.p, (3 * n + 4) * sizeof(unsigned long long),
                            cudaMemcpyDeviceToHost, st));
   out->launches = launches;
