@@ -9,6 +9,7 @@
 #include <atomic>
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 #include "edx.h"
 
@@ -37,6 +38,33 @@ struct Error : std::runtime_error {
     cudaError_t _e = cudaGetLastError();                                      \
     if (_e != cudaSuccess) ::edx::throw_cuda(_e, "kernel launch", __FILE__, __LINE__); \
   } while (0)
+
+// Programmatic dependent launch: a kernel launched with launch_pdl may be
+// scheduled while its stream predecessor drains; it must call pdl_wait()
+// before touching memory (the wait returns once the predecessor grid has
+// completed and its writes are visible).  pdl_trigger() lets the successor's
+// CTAs be scheduled early.  Both are no-ops for a normal launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;"); }
+
+// EDX_PDL=0 turns the attribute off (A/B switch)
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  EDX_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
 
 inline void invalid(const std::string& m) { throw Error(EDX_INVALID_ARGUMENT, m); }
 inline void logic(const std::string& m) { throw Error(EDX_LOGIC_ERROR, m); }

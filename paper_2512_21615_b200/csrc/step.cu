@@ -29,12 +29,22 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstring>
 
+#include "bitonic.cuh"
 #include "engine.h"
 #include "step.h"
 
 namespace edx {
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("EDX_PDL");
+    return !(v && std::strcmp(v, "0") == 0);
+  }();
+  return on;
+}
 
 namespace {
 
@@ -69,6 +79,8 @@ __global__ void k_step_begin(const uint64_t* __restrict__ offsets, uint64_t rows
                              uint64_t T, int32_t* __restrict__ first_pos,
                              unsigned long long* __restrict__ counters, uint32_t ncnt,
                              uint32_t* __restrict__ ws, uint32_t nws) {
+  pdl_wait();
+  pdl_trigger();
   const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (i < ncnt) counters[i] = 0;
   if (i < nws) ws[i] = 0;
@@ -86,6 +98,8 @@ __global__ void k_step_begin(const uint64_t* __restrict__ offsets, uint64_t rows
 
 __global__ void k_unique_flag(const uint32_t* __restrict__ ids, uint64_t T,
                               const int32_t* __restrict__ first_pos, uint32_t* __restrict__ flag) {
+  pdl_wait();
+  pdl_trigger();
   const uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (p > T) return;
   flag[p] = (p < T && first_pos[ids[p]] == static_cast<int32_t>(p)) ? 1u : 0u;
@@ -95,6 +109,8 @@ __global__ void k_unique_scatter(const uint32_t* __restrict__ ids, uint64_t T,
                                  const int32_t* __restrict__ first_pos,
                                  const uint32_t* __restrict__ uidx, uint32_t* __restrict__ uniq,
                                  unsigned long long* counters, int n) {
+  pdl_wait();
+  pdl_trigger();
   const uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (p == T) counters[3 * n + 1] = uidx[T];
   if (p >= T) return;
@@ -109,6 +125,8 @@ __global__ void k_needs(const uint32_t* __restrict__ ids, uint64_t T,
                         const uint32_t* __restrict__ uidx, uint64_t ucap,
                         int32_t* __restrict__ need_first, uint32_t* __restrict__ need_cnt,
                         unsigned long long* __restrict__ umask) {
+  pdl_wait();
+  pdl_trigger();
   const uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (p >= T) return;
   const int j = decision[occ_sample[p]];
@@ -127,6 +145,8 @@ __global__ void k_need_keys(const uint32_t* __restrict__ ids, uint64_t T,
                             const int32_t* __restrict__ first_pos, const uint32_t* __restrict__ uidx,
                             uint64_t ucap, const int32_t* __restrict__ need_first,
                             uint64_t* __restrict__ keys, uint32_t* __restrict__ ws) {
+  pdl_wait();
+  pdl_trigger();
   const uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (p >= T) return;
   const int j = decision[occ_sample[p]];
@@ -150,6 +170,8 @@ __global__ void k_phase1(const uint32_t* __restrict__ uniq,
                          ulonglong2* __restrict__ ol, unsigned long long* counters,
                          uint32_t* __restrict__ ws, const uint32_t* __restrict__ size,
                          uint64_t capacity) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ unsigned int push[kMaxWorkers];
   if (threadIdx.x < kMaxWorkers) push[threadIdx.x] = 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -207,6 +229,8 @@ __global__ void k_classify(const uint64_t* __restrict__ items,
                            const uint32_t* __restrict__ smark, const uint32_t* __restrict__ cur_mark,
                            uint8_t* __restrict__ type, uint32_t* __restrict__ ins_flag,
                            int32_t* __restrict__ contrib, unsigned long long* counters) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ unsigned int miss[kMaxWorkers];
   __shared__ unsigned long long hits;
   if (threadIdx.x < kMaxWorkers) miss[threadIdx.x] = 0;
@@ -386,65 +410,6 @@ __global__ void k_cand_offsets(const int32_t* __restrict__ wlist, int nw, uint32
   }
 }
 
-// Register part of the victims' bitonic sort: thread t holds elements
-// [4t, 4t+4) in (rk, rs); runs the stages (size, stride), (size, stride/2),
-// ... (size, 1) for stride <= 64.
-__device__ __forceinline__ void bitonic_load4(const uint64_t* sk, const uint32_t* ss, int tid,
-                                              uint64_t (&rk)[4], uint32_t (&rs)[4]) {
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    rk[q] = sk[4 * tid + q];
-    rs[q] = ss[4 * tid + q];
-  }
-}
-
-__device__ __forceinline__ void bitonic_store4(uint64_t* sk, uint32_t* ss, int tid,
-                                               const uint64_t (&rk)[4], const uint32_t (&rs)[4]) {
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    sk[4 * tid + q] = rk[q];
-    ss[4 * tid + q] = rs[q];
-  }
-}
-
-template <int S>
-__device__ __forceinline__ void bitonic_in_thread(int tid, uint32_t size, uint64_t (&rk)[4],
-                                                  uint32_t (&rs)[4]) {
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    if (q & S) continue;
-    const uint32_t i = 4 * static_cast<uint32_t>(tid) + q;
-    if ((rk[q] > rk[q + S]) == ((i & size) == 0)) {
-      const uint64_t tk = rk[q];
-      rk[q] = rk[q + S];
-      rk[q + S] = tk;
-      const uint32_t ts = rs[q];
-      rs[q] = rs[q + S];
-      rs[q + S] = ts;
-    }
-  }
-}
-
-__device__ __forceinline__ void bitonic_reg_stages(int tid, uint32_t size, uint32_t stride,
-                                                   uint64_t (&rk)[4], uint32_t (&rs)[4]) {
-  for (; stride >= 4; stride >>= 1) {
-    const int lx = static_cast<int>(stride >> 2);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint32_t i = 4 * static_cast<uint32_t>(tid) + q;
-      const uint64_t ok = __shfl_xor_sync(0xffffffffu, rk[q], lx);
-      const uint32_t os = __shfl_xor_sync(0xffffffffu, rs[q], lx);
-      const bool asc = (i & size) == 0, lower = (i & stride) == 0;
-      if (lower == asc ? (ok < rk[q]) : (ok > rk[q])) {
-        rk[q] = ok;
-        rs[q] = os;
-      }
-    }
-  }
-  if (stride >= 2) bitonic_in_thread<2>(tid, size, rk, rs);
-  bitonic_in_thread<1>(tid, size, rk, rs);
-}
-
 // Victim selection for caches of up to kSelCap entries: one CTA per worker.
 // The CTA finds its non-pinned entries, the per-worker value ranges of
 // (mark, frequency, last_access, id), packs each VictimKey (cache.hpp:47-58)
@@ -466,6 +431,8 @@ __global__ void __launch_bounds__(kSelThreads, 1)
                      uint64_t ucap, const int32_t* __restrict__ need_first,
                      const uint32_t* __restrict__ ins_scan,
                      uint32_t* __restrict__ cand_slot_sorted, int* __restrict__ flags) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) uint8_t smem[];
   auto& temp = *reinterpret_cast<typename SelSort::TempStorage*>(smem);
   __shared__ uint32_t part[kSelThreads / 32][9];
@@ -651,45 +618,13 @@ __global__ void __launch_bounds__(kSelThreads, 1)
         ss[q] = slots[k];
       }
     }
-    // Bitonic sort of the take keys (padded to P >= 128 with all-ones keys,
-    // which sort last).  Thread t owns elements [4t, 4t+4): strides 1 and 2
-    // are in-register, strides 4..64 are warp shuffles (the partner sits in
-    // lane ^ stride/4, same register), strides >= 128 go through shared memory.
+    // bitonic sort of the take keys, padded to P >= 128 with all-ones keys
+    // (which sort last); keys are unique
     uint32_t P = 128;
     while (P < take) P <<= 1;
     for (uint32_t x = take + tid; x < P; x += kSelThreads) sk[x] = ~0ULL;
     __syncthreads();
-    const bool owner = 4 * static_cast<uint32_t>(tid) < P;  // warp-uniform (P % 128 == 0)
-    uint64_t rk[4];
-    uint32_t rs[4];
-    if (owner) {
-      bitonic_load4(sk, ss, tid, rk, rs);
-      for (uint32_t size = 2; size <= 128; size <<= 1) bitonic_reg_stages(tid, size, size >> 1, rk, rs);
-      bitonic_store4(sk, ss, tid, rk, rs);
-    }
-    __syncthreads();
-    for (uint32_t size = 256; size <= P; size <<= 1) {
-      for (uint32_t stride = size >> 1; stride >= 128; stride >>= 1) {
-        for (uint32_t t = tid; t < P / 2; t += kSelThreads) {
-          const uint32_t lo = 2 * t - (t & (stride - 1)), hi = lo + stride;
-          const uint64_t a = sk[lo], b = sk[hi];
-          if ((a > b) == ((lo & size) == 0)) {
-            sk[lo] = b;
-            sk[hi] = a;
-            const uint32_t sa = ss[lo];
-            ss[lo] = ss[hi];
-            ss[hi] = sa;
-          }
-        }
-        __syncthreads();
-      }
-      if (owner) {
-        bitonic_load4(sk, ss, tid, rk, rs);
-        bitonic_reg_stages(tid, size, 64, rk, rs);
-        bitonic_store4(sk, ss, tid, rk, rs);
-      }
-      __syncthreads();
-    }
+    block_bitonic_sort(sk, ss, P);
     for (uint32_t r = tid; r < take; r += kSelThreads) cand_slot_sorted[gb + r] = ss[r];
   }
   if (tid == 0) {
@@ -711,6 +646,8 @@ __global__ void k_evict_contrib(const uint64_t* __restrict__ items,
                                 const uint32_t* __restrict__ ws, const uint32_t* __restrict__ cand_slot,
                                 const uint32_t* __restrict__ smark, uint64_t capacity,
                                 const uint32_t* __restrict__ cur_mark, int32_t* __restrict__ contrib) {
+  pdl_wait();
+  pdl_trigger();
   const uint64_t N = counters_ro[3 * n + 2];
   const uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (q >= N || type[q] != 2) return;
@@ -791,6 +728,8 @@ __global__ void k_advance_evict(uint32_t ga, const uint64_t* __restrict__ items,
                                 ulonglong2* __restrict__ ol, unsigned long long* __restrict__ res,
                                 int32_t* __restrict__ slot_of, uint32_t* __restrict__ victim_id,
                                 unsigned long long* counters) {
+  pdl_wait();
+  pdl_trigger();
   if (blockIdx.x < ga) {
     find_advance(blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x, items, counters_ro, n,
                  type, ins_scan, con_scan, ws, at_cur, capacity);
@@ -815,6 +754,8 @@ __global__ void k_apply(const uint64_t* __restrict__ items,
                         uint32_t* __restrict__ slast, const int32_t* __restrict__ first_pos,
                         const uint32_t* __restrict__ uidx, uint64_t ucap,
                         int32_t* __restrict__ need_first, uint32_t* __restrict__ need_cnt) {
+  pdl_wait();
+  pdl_trigger();
   const uint32_t clock = *clock_dev;
   const uint64_t N = counters_ro[3 * n + 2];
   const uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
@@ -867,6 +808,8 @@ __global__ void k_step_tail(int n, const uint32_t* __restrict__ ws,
                             const uint32_t* __restrict__ uniq,
                             const unsigned long long* counters_ro, ulonglong2* __restrict__ ol,
                             int32_t* __restrict__ first_pos, unsigned long long* __restrict__ umask) {
+  pdl_wait();
+  pdl_trigger();
   if (blockIdx.x == 0 && threadIdx.x < n) {
     const int j = threadIdx.x;
     const uint32_t* w = ws + j * kWS;
@@ -1015,13 +958,13 @@ int launch_step_head(edx_engine* e, cudaStream_t st) {
   const uint64_t span = std::max<uint64_t>(std::max<uint64_t>(R, T), nws);
   k_step_begin<<<grid_for(span), kT, 0, st>>>(e->cur_offsets, R, s.occ_sample.p, e->cur_ids, T,
                                               s.first_pos.p, s.counters.p, ncnt, s.wscalars.p, nws);
-  k_unique_flag<<<grid_for(T + 1), kT, 0, st>>>(e->cur_ids, T, s.first_pos.p, s.flag_scan.p);
+  launch_pdl(k_unique_flag, grid_for(T + 1), kT, 0, st, e->cur_ids, T, s.first_pos.p, s.flag_scan.p);
   EDX_LAUNCHED();
   cub_call(e, [&](void* tmp, size_t& b) {
     return cub::DeviceScan::ExclusiveSum(tmp, b, s.flag_scan.p, s.uidx_of_pos.p,
                                          static_cast<int>(T + 1), st);
   });
-  k_unique_scatter<<<grid_for(T + 1), kT, 0, st>>>(e->cur_ids, T, s.first_pos.p, s.uidx_of_pos.p,
+  launch_pdl(k_unique_scatter, grid_for(T + 1), kT, 0, st, e->cur_ids, T, s.first_pos.p, s.uidx_of_pos.p,
                                                    s.uniq.p, s.counters.p, n);
   EDX_LAUNCHED();
   return 5;
@@ -1064,7 +1007,7 @@ void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
   k_needs<<<grid_for(T), kT, 0, st>>>(e->cur_ids, T, s.occ_sample.p, d_decision, s.first_pos.p,
                                       s.uidx_of_pos.p, ucap, s.need_first.p, s.need_cnt.p,
                                       s.umask.p);
-  k_need_keys<<<grid_for(T), kT, 0, st>>>(e->cur_ids, T, s.occ_sample.p, d_decision, s.first_pos.p,
+  launch_pdl(k_need_keys, grid_for(T), kT, 0, st, e->cur_ids, T, s.occ_sample.p, d_decision, s.first_pos.p,
                                           s.uidx_of_pos.p, ucap, s.need_first.p, s.need_key.p,
                                           s.wscalars.p);
   EDX_LAUNCHED();
@@ -1078,9 +1021,9 @@ void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
                                           static_cast<int>(T), 32, 32 + wbits + 1, st);
   });
   launches += 3;
-  k_phase1<<<grid_for(T), kT, 0, st>>>(s.uniq.p, s.umask.p, s.counters.p, n, e->ol.p, s.counters.p,
+  launch_pdl(k_phase1, grid_for(T), kT, 0, st, s.uniq.p, s.umask.p, s.counters.p, n, e->ol.p, s.counters.p,
                                        s.wscalars.p, c.size.p, e->capacity);
-  k_classify<<<grid_for(T + 1), kT, 0, st>>>(
+  launch_pdl(k_classify, grid_for(T + 1), kT, 0, st, 
       s.need_key_sorted.p, s.counters.p, n, e->cur_ids, s.first_pos.p, s.uidx_of_pos.p, ucap,
       s.need_cnt.p, e->ol.p, e->res.p, e->id_space, c.slot_of.p, e->capacity, c.smark.p,
       c.cur_mark.p, s.need_type.p, s.flag_scan.p, s.need_contrib.p, s.counters.p);
@@ -1103,7 +1046,7 @@ void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
   const int32_t* d_wlist = reinterpret_cast<const int32_t*>(s.cand_off.p);
   int nw = n;  // workers the victim kernels visit
   if (e->capacity <= kSelCap) {
-    k_select_victims<<<n, kSelThreads, sizeof(typename SelSort::TempStorage), st>>>(
+    launch_pdl(k_select_victims, n, kSelThreads, sizeof(typename SelSort::TempStorage), st, 
         e->capacity, s.wscalars.p, c.sid.p, c.smark.p, c.sfreq.p, c.slast.p, e->ol.p,
         s.first_pos.p, s.uidx_of_pos.p, ucap, s.need_first.p, s.ins_rank.p, s.cand_slot_sorted.p,
         e->flags.p);
@@ -1159,7 +1102,7 @@ void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
       launches += 4 + 8;
     }
   }
-  k_evict_contrib<<<grid_for(T), kT, 0, st>>>(s.need_key_sorted.p, s.counters.p, n, s.need_type.p,
+  launch_pdl(k_evict_contrib, grid_for(T), kT, 0, st, s.need_key_sorted.p, s.counters.p, n, s.need_type.p,
                                               s.ins_rank.p, s.wscalars.p, s.cand_slot_sorted.p,
                                               c.smark.p, e->capacity, c.cur_mark.p,
                                               s.need_contrib.p);
@@ -1173,20 +1116,20 @@ void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
   {
     const unsigned ga = grid_for(T);
     const int32_t* wlv = e->capacity <= kSelCap ? d_wlist : d_wlist + 64;
-    k_advance_evict<<<ga + kEvictBlocks * static_cast<unsigned>(nw), kT, 0, st>>>(
+    launch_pdl(k_advance_evict, ga + kEvictBlocks * static_cast<unsigned>(nw), kT, 0, st, 
         ga, s.need_key_sorted.p, s.counters.p, n, s.need_type.p, s.ins_rank.p, con_scan,
         s.wscalars.p, c.at_cur.p, e->capacity, wlv, s.cand_slot_sorted.p, c.sid.p, e->id_space,
         e->ol.p, e->res.p, c.slot_of.p, s.cand_count.p, s.counters.p);
   }
   EDX_LAUNCHED();
   launches += 3;  // contribution, scan (2), advance + evict
-  k_apply<<<grid_for(T), kT, 0, st>>>(s.need_key_sorted.p, s.counters.p, n, e->cur_ids,
+  launch_pdl(k_apply, grid_for(T), kT, 0, st, s.need_key_sorted.p, s.counters.p, n, e->cur_ids,
                                       s.need_type.p, s.ins_rank.p, s.wscalars.p,
                                       s.cand_slot_sorted.p, e->capacity, e->id_space, c.cur_mark.p,
                                       e->d_clock.p, e->ol.p, e->res.p, c.slot_of.p, c.sid.p,
                                       c.smark.p, c.sfreq.p, c.slast.p, s.first_pos.p,
                                       s.uidx_of_pos.p, ucap, s.need_first.p, s.need_cnt.p);
-  k_step_tail<<<grid_for(T), kT, 0, st>>>(n, s.wscalars.p, con_scan, c.size.p, c.cur_mark.p,
+  launch_pdl(k_step_tail, grid_for(T), kT, 0, st, n, s.wscalars.p, con_scan, c.size.p, c.cur_mark.p,
                                           c.at_cur.p, s.uniq.p, s.counters.p, e->ol.p,
                                           s.first_pos.p, s.umask.p);
   EDX_LAUNCHED();
