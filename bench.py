@@ -191,7 +191,7 @@ def product(args, w, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     n, m, L, R = w["n"], w["m"], w["L"], w["R"]
     K, W, P = args.steps, args.warmup, w["prefill"]
-    total = P + 2 * (W + K)
+    total = P + 2 * (W + K) + 1  # +1: the batch the last timed e2e step prefetches
     host = batches(w, total)
     offs = np.arange(R + 1, dtype=np.uint64) * np.uint64(L)
     cfg = edx.ClusterConfig(n=n, m=m, bandwidths_bps=w["bw"], d_tran_bytes=2048,
@@ -283,9 +283,17 @@ def product(args, w, rank, world, local_rank):
     pinned_offs = torch.from_numpy(offs.view(np.int64)).pin_memory()
     pin_np = pinned.numpy().view(np.uint32)
     poffs_np = pinned_offs.numpy().view(np.uint64)
+    # batch i+1's host->device copy is issued (edx_engine_prefetch, copy stream,
+    # double-buffered) before iteration i runs -- the paper's pipelined input
+    # loading; every step still copies its own batch inside the timed region
+    def one_e2e(i):
+        nxt = (pin_np[i + 1], poffs_np) if i + 1 < len(pin_np) else None
+        return eng.iterate(pin_np[i], poffs_np, prefetch_next=nxt)
+
+    eng.prefetch(pin_np[0], poffs_np)
     for i in range(W):
-        eng.iterate(pin_np[i], poffs_np)
-    e2e_ms = timed(lambda i: eng.iterate(pin_np[i], poffs_np), range(W, W + K))
+        one_e2e(i)
+    e2e_ms = timed(one_e2e, range(W, W + K))
     e2e_step_ms = sum(e2e_ms) / K
 
     # ---- roofline of the cost build (K1), per launch
@@ -320,7 +328,10 @@ def product(args, w, rank, world, local_rank):
                                         "NCCL gather to rank 0, rank-0 solve, decision broadcast, "
                                         "replicated cache update" if world > 1 else "1 GPU"}),
         "e2e": {"value": R / (e2e_step_ms * 1e-3), "unit": "samples/s",
-                "ms_per_step": e2e_step_ms, "h2d_bytes_per_step": R * L * 4 + (R + 1) * 8,
+                "ms_per_step": e2e_step_ms,
+                "note": "edx_engine_iterate from pinned host buffers; the next batch's H2D is "
+                        "prefetched on the engine's copy stream during each iteration",
+                "h2d_bytes_per_step": R * L * 4 + (R + 1) * 8,
                 "d2h_bytes_per_step": R * 4 + 8 + (3 * n + 4) * 8},
         "roofline": {"kernel": ("k_cost_build_warp" if 2 <= n <= 8 else "k_cost_build_wide"
                                 if 8 < n <= 32 else "k_cost_build") + " (K1, cost.hpp:81-125)",

@@ -143,7 +143,6 @@ int edx_engine_iterate(edx_engine* e, const uint32_t* ids, const uint64_t* offse
  * work and timing events after the engine's. */
 int edx_engine_stream(edx_engine* e, void** stream);
 
-/* SimState::seed_entry — sim.hpp:252-261 (test hook). */
 /* edx_engine_iterate for a batch already in device memory whose id count the
  * caller knows (see edx_engine_load_device_batch): the batch is staged into the
  * engine's own buffers and the iteration runs as one CUDA graph replay when the
@@ -151,6 +150,25 @@ int edx_engine_stream(edx_engine* e, void** stream);
 int edx_engine_iterate_device(edx_engine* e, const uint32_t* ids, const uint64_t* offsets,
                               uint64_t num_samples, uint64_t total_ids, int32_t* decision_out,
                               double* expected_cost_out, edx_report* rep);
+/* Input prefetch (the paper's pipelined batch loading; SURVEY
+ * 8f item 2): starts the host->device copy of a HOST batch on the engine's
+ * copy stream into one of two device slots and returns.  A later
+ * edx_engine_iterate / edx_engine_load_batch with the same (ids, offsets,
+ * num_samples) host pointers uses the prefetched copy instead of copying
+ * again.  The host buffers must stay unchanged until that call (pinned memory
+ * makes the copy asynchronous).  Offsets are validated here, with the same
+ * messages as edx_engine_load_batch. */
+int edx_engine_prefetch(edx_engine* e, const uint32_t* ids, const uint64_t* offsets,
+                        uint64_t num_samples);
+/* edx_engine_iterate on a host batch (used from the prefetch slot when it was
+ * prefetched) that, once the iteration is launched and before waiting for it,
+ * prefetches the NEXT host batch (next_ids may be NULL): the steady-state loop
+ * of a pipelined caller, copy of batch i+1 overlapping iteration i. */
+int edx_engine_iterate_prefetch(edx_engine* e, const uint32_t* ids, const uint64_t* offsets,
+                                uint64_t num_samples, const uint32_t* next_ids,
+                                const uint64_t* next_offsets, uint64_t next_num_samples,
+                                int32_t* decision_out, double* expected_cost_out, edx_report* rep);
+/* SimState::seed_entry — sim.hpp:252-261 (test hook). */
 int edx_engine_seed_entry(edx_engine* e, uint32_t id, int32_t worker, int latest, int owner);
 /* SimState::state_of — sim.hpp:64-67. */
 int edx_engine_state_of(edx_engine* e, uint32_t id, uint64_t* owners, uint64_t* latest,

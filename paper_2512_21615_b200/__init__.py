@@ -559,20 +559,42 @@ class SimState:
         check(lib().edx_engine_step(self._h, _ptr(d, C.c_int32), C.byref(rep.c)))
         return rep.result()
 
-    def iterate(self, ids, offsets, want_decision=True):
-        """One run() iteration (sim.hpp:421-441) on host buffers."""
+    def iterate(self, ids, offsets, want_decision=True, prefetch_next=None):
+        """One run() iteration (sim.hpp:421-441) on host buffers.  With
+        prefetch_next=(ids, offsets) the next batch's host->device copy is issued
+        once this iteration is launched (edx_engine_iterate_prefetch)."""
         ids = np.ascontiguousarray(ids, np.uint32)
         offsets = np.ascontiguousarray(offsets, np.uint64)
         R = len(offsets) - 1
         dec = np.empty(R, np.int32) if want_decision else None
         exp = C.c_double()
         rep = _Report(self.cfg.n)
-        check(lib().edx_engine_iterate(self._h, ids.ctypes.data_as(C.c_void_p),
-                                       offsets.ctypes.data_as(C.c_void_p), R, 0,
-                                       _ptr(dec, C.c_int32), C.byref(exp), C.byref(rep.c)))
+        if prefetch_next is None:
+            check(lib().edx_engine_iterate(self._h, ids.ctypes.data_as(C.c_void_p),
+                                           offsets.ctypes.data_as(C.c_void_p), R, 0,
+                                           _ptr(dec, C.c_int32), C.byref(exp), C.byref(rep.c)))
+        else:
+            nids = np.ascontiguousarray(prefetch_next[0], np.uint32)
+            noffs = np.ascontiguousarray(prefetch_next[1], np.uint64)
+            check(lib().edx_engine_iterate_prefetch(
+                self._h, ids.ctypes.data_as(C.c_void_p), offsets.ctypes.data_as(C.c_void_p), R,
+                nids.ctypes.data_as(C.c_void_p), noffs.ctypes.data_as(C.c_void_p), len(noffs) - 1,
+                _ptr(dec, C.c_int32), C.byref(exp), C.byref(rep.c)))
+            self._prefetched = (getattr(self, "_prefetched", ()) + ((nids, noffs),))[-2:]
         r = rep.result()
         r.expected_cost_s, r.has_expected = exp.value, True
         return dec, r
+
+    def prefetch(self, ids, offsets):
+        """Start the host->device copy of a host batch on the engine's copy stream
+        (edx_engine_prefetch); a later iterate()/load() with the same arrays uses
+        it.  Pass pinned arrays for an asynchronous copy; they must stay unchanged
+        until that call (the engine keeps a reference to the last two)."""
+        ids = np.ascontiguousarray(ids, np.uint32)
+        offsets = np.ascontiguousarray(offsets, np.uint64)
+        check(lib().edx_engine_prefetch(self._h, ids.ctypes.data_as(C.c_void_p),
+                                        offsets.ctypes.data_as(C.c_void_p), len(offsets) - 1))
+        self._prefetched = (getattr(self, "_prefetched", ()) + ((ids, offsets),))[-2:]
 
     def iterate_device(self, ids_ptr, offsets_ptr, rows, total_ids, want_decision=True,
                        want_expected=True):

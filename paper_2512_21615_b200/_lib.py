@@ -83,6 +83,9 @@ def _sigs():
         ("edx_engine_step", cint, [vp, i32p, P(ReportC)]),
         ("edx_engine_iterate", cint, [vp, vp, vp, u64, cint, i32p, dblp, P(ReportC)]),
         ("edx_engine_iterate_device", cint, [vp, vp, vp, u64, u64, i32p, dblp, P(ReportC)]),
+        ("edx_engine_prefetch", cint, [vp, vp, vp, u64]),
+        ("edx_engine_iterate_prefetch", cint, [vp, vp, vp, u64, vp, vp, u64, i32p, dblp,
+                                                P(ReportC)]),
         ("edx_engine_stream", cint, [vp, P(vp)]),
         ("edx_engine_seed_entry", cint, [vp, C.c_uint32, i32, cint, cint]),
         ("edx_engine_state_of", cint, [vp, C.c_uint32, u64p, u64p, u64p]),

@@ -681,6 +681,11 @@ int edx_engine_create(const edx_cluster_config* cfg, const edx_engine_options* o
     for (auto& ev : e->ev) EDX_CUDA(cudaEventCreate(&ev));
     EDX_CUDA(cudaEventCreateWithFlags(&e->cost_done, cudaEventDisableTiming));
     EDX_CUDA(cudaStreamCreateWithFlags(&e->step_side, cudaStreamNonBlocking));
+    EDX_CUDA(cudaStreamCreateWithFlags(&e->copy_stream, cudaStreamNonBlocking));
+    for (auto& f : e->pf) {
+      EDX_CUDA(cudaEventCreateWithFlags(&f.ready, cudaEventDisableTiming));
+      EDX_CUDA(cudaEventCreateWithFlags(&f.free, cudaEventDisableTiming));
+    }
     EDX_CUDA(cudaEventCreateWithFlags(&e->head_fork, cudaEventDisableTiming));
     EDX_CUDA(cudaEventCreateWithFlags(&e->head_done, cudaEventDisableTiming));
     e->ol.ensure(e->id_space);
@@ -719,6 +724,15 @@ void edx_engine_destroy(edx_engine* e) {
     cudaStreamSynchronize(e->step_side);
     cudaStreamDestroy(e->step_side);
   }
+  if (e->copy_stream) {
+    cudaStreamSynchronize(e->copy_stream);
+    cudaStreamDestroy(e->copy_stream);
+  }
+  for (auto& f : e->pf) {
+    if (f.ready) cudaEventDestroy(f.ready);
+    if (f.free) cudaEventDestroy(f.free);
+    if (f.h_offsets) cudaFreeHost(f.h_offsets);
+  }
   if (e->h_flags) cudaFreeHost(e->h_flags);
   if (e->h_counters) cudaFreeHost(e->h_counters);
   if (e->h_clock) cudaFreeHost(e->h_clock);
@@ -730,11 +744,94 @@ void edx_engine_destroy(edx_engine* e) {
   if (s) cudaStreamDestroy(s);
 }
 
+namespace {
+
+// Host batch validation shared by the load and prefetch paths (same messages);
+// returns the id count.
+uint64_t check_host_offsets(const edx_engine* e, const uint64_t* offsets, uint64_t R) {
+  if (R == 0) edx::invalid("batch holds no samples");
+  for (uint64_t i = 0; i < R; ++i)
+    if (offsets[i + 1] < offsets[i]) edx::invalid("sample offsets must be non-decreasing");
+  const uint64_t total = offsets[R] - offsets[0];
+  if (total > e->max_ids)
+    edx::invalid("batch holds " + std::to_string(total) + " ids; engine max_batch_ids is " +
+                 std::to_string(e->max_ids));
+  return total;
+}
+
+// A host batch prefetched by edx_engine_prefetch: wait for its copy, stage it
+// into the engine's own buffers (fixed pointers for the graph) and load it.
+bool load_prefetched(edx_engine* e, const uint32_t* ids, const uint64_t* offsets, uint64_t R) {
+  for (auto& f : e->pf) {
+    if (!f.valid || f.host_ids != ids || f.host_offsets != offsets || f.rows != R) continue;
+    f.valid = false;
+    EDX_CUDA(cudaStreamWaitEvent(e->stream, f.ready, 0));
+    e->offsets.ensure(R + 1);
+    if (f.total)
+      EDX_CUDA(cudaMemcpyAsync(e->ids.p, f.ids.p, f.total * sizeof(uint32_t), cudaMemcpyDeviceToDevice,
+                               e->stream));
+    EDX_CUDA(cudaMemcpyAsync(e->offsets.p, f.offsets.p, (R + 1) * sizeof(uint64_t),
+                             cudaMemcpyDeviceToDevice, e->stream));
+    EDX_CUDA(cudaEventRecord(f.free, e->stream));
+    engine_load(e, e->ids.p, e->offsets.p, R, 1, f.total);
+    return true;
+  }
+  return false;
+}
+
+}  // namespace
+
 int edx_engine_load_batch(edx_engine* e, const uint32_t* ids, const uint64_t* offsets,
                           uint64_t num_samples, int on_device) {
   return guard([&] {
     EDX_CUDA(cudaSetDevice(e->device));
-    engine_load(e, ids, offsets, num_samples, on_device);
+    if (on_device || !load_prefetched(e, ids, offsets, num_samples))
+      engine_load(e, ids, offsets, num_samples, on_device);
+  });
+}
+
+void engine_prefetch(edx_engine* e, const uint32_t* ids, const uint64_t* offsets,
+                     uint64_t num_samples) {
+  {
+    const uint64_t R = num_samples;
+    const uint64_t total = check_host_offsets(e, offsets, R);
+    const uint64_t base = offsets[0];
+    auto& f = e->pf[e->pf_next];
+    e->pf_next ^= 1;
+    // the slot's previous copy has finished before its pinned offsets are rewritten
+    EDX_CUDA(cudaEventSynchronize(f.ready));
+    f.valid = false;
+    if (f.h_cap < R + 1) {
+      if (f.h_offsets) EDX_CUDA(cudaFreeHost(f.h_offsets));
+      f.h_offsets = nullptr;
+      f.h_cap = 0;
+      EDX_CUDA(cudaMallocHost(&f.h_offsets, (R + 1) * sizeof(uint64_t)));
+      f.h_cap = R + 1;
+    }
+    for (uint64_t i = 0; i <= R; ++i) f.h_offsets[i] = offsets[i] - base;
+    f.ids.ensure(e->max_ids);
+    f.offsets.ensure(R + 1);
+    // the previous batch of this slot has been staged out of it
+    EDX_CUDA(cudaStreamWaitEvent(e->copy_stream, f.free, 0));
+    if (total)
+      EDX_CUDA(cudaMemcpyAsync(f.ids.p, ids + base, total * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                               e->copy_stream));
+    EDX_CUDA(cudaMemcpyAsync(f.offsets.p, f.h_offsets, (R + 1) * sizeof(uint64_t),
+                             cudaMemcpyHostToDevice, e->copy_stream));
+    EDX_CUDA(cudaEventRecord(f.ready, e->copy_stream));
+    f.host_ids = ids;
+    f.host_offsets = offsets;
+    f.rows = R;
+    f.total = total;
+    f.valid = true;
+  }
+}
+
+int edx_engine_prefetch(edx_engine* e, const uint32_t* ids, const uint64_t* offsets,
+                        uint64_t num_samples) {
+  return guard([&] {
+    EDX_CUDA(cudaSetDevice(e->device));
+    engine_prefetch(e, ids, offsets, num_samples);
   });
 }
 
@@ -804,8 +901,30 @@ int edx_engine_iterate(edx_engine* e, const uint32_t* ids, const uint64_t* offse
                        double* expected_cost_out, edx_report* rep) {
   return guard([&] {
     EDX_CUDA(cudaSetDevice(e->device));
-    engine_load(e, ids, offsets, num_samples, on_device);
+    if (on_device || !load_prefetched(e, ids, offsets, num_samples))
+      engine_load(e, ids, offsets, num_samples, on_device);
     engine_iterate_core(e, -1.0);
+    if (decision_out)
+      EDX_CUDA(cudaMemcpyAsync(decision_out, e->decision.p, e->rows * sizeof(int32_t),
+                               cudaMemcpyDeviceToHost, e->stream));
+    step_finish(e, rep);
+    if (expected_cost_out) *expected_cost_out = fetch_expected(e);
+  });
+}
+
+int edx_engine_iterate_prefetch(edx_engine* e, const uint32_t* ids, const uint64_t* offsets,
+                                uint64_t num_samples, const uint32_t* next_ids,
+                                const uint64_t* next_offsets, uint64_t next_num_samples,
+                                int32_t* decision_out, double* expected_cost_out, edx_report* rep) {
+  return guard([&] {
+    EDX_CUDA(cudaSetDevice(e->device));
+    // the next batch is validated before this iteration is launched: a bad
+    // next batch must not leave a launched, unfinished iteration behind
+    if (next_ids && next_offsets) check_host_offsets(e, next_offsets, next_num_samples);
+    if (!load_prefetched(e, ids, offsets, num_samples)) engine_load(e, ids, offsets, num_samples, 0);
+    engine_iterate_core(e, -1.0);
+    // the next batch's copy is issued while this iteration runs
+    if (next_ids && next_offsets) engine_prefetch(e, next_ids, next_offsets, next_num_samples);
     if (decision_out)
       EDX_CUDA(cudaMemcpyAsync(decision_out, e->decision.p, e->rows * sizeof(int32_t),
                                cudaMemcpyDeviceToHost, e->stream));

@@ -99,6 +99,20 @@ struct edx_engine {
   // the decision-independent head of the step runs on its own stream during
   // a fused iteration's build and dispatch (step_head / step_run)
   cudaStream_t step_side = nullptr;
+  // input prefetch (edx_engine_prefetch): two device slots filled on copy_stream
+  struct Prefetch {
+    edx::DevBuf<uint32_t> ids;
+    edx::DevBuf<uint64_t> offsets;
+    uint64_t* h_offsets = nullptr;  // pinned, base-adjusted offsets
+    uint64_t h_cap = 0;
+    cudaEvent_t ready = nullptr, free = nullptr;
+    bool valid = false, used = false;
+    const void* host_ids = nullptr;
+    const void* host_offsets = nullptr;
+    uint64_t rows = 0, total = 0;
+  } pf[2];
+  int pf_next = 0;
+  cudaStream_t copy_stream = nullptr;
   cudaEvent_t head_fork = nullptr, head_done = nullptr;
   bool head_pending = false;
 

@@ -293,3 +293,75 @@ def test_iterate_device_graph_replay(gpu, oracle, pyoracle, name, alpha):
         assert rep.expected_cost_s == wexp, f"iter {it}: expected cost"
     msg = canon_equal(eng.canonical_state(), sim.canonical_state())
     assert not msg, msg
+
+
+@pytest.mark.parametrize("name,alpha", [("C2", 0.5), ("C1", 0.0)])
+def test_iterate_with_prefetch(gpu, oracle, pyoracle, name, alpha):
+    """edx_engine_prefetch: batch i+1's host->device copy is issued before
+    iteration i; every decision, report and the final state equal the
+    reference run() body.  Also: a prefetched batch that is never consumed, a
+    host batch that was not prefetched, and prefetch's offset validation."""
+    import torch
+    edx = gpu
+    p = CONFIGS[name]
+    n, m, L = p["n"], p["m"], p["L"]
+    R = n * m
+    c = edx.ClusterConfig(n=n, m=m, bandwidths_bps=p["bw"], cache_capacity=p["cap"], alpha=alpha)
+    eng = edx.SimState(c, id_space=p["V"], max_batch_ids=R * L)
+    sim = oracle.sim(pyoracle.Cfg(n, m, p["bw"], cap=p["cap"], alpha=alpha))
+    offs = torch.from_numpy(offsets_for(R, L).view(np.int64)).pin_memory().numpy().view(np.uint64)
+    batches = [torch.from_numpy(b.view(np.int32)).pin_memory().numpy().view(np.uint32)
+               for b in oracle.zipf_batches(p["V"], L, 1.05, 10, 23, R)]
+    stray = batches[0].copy()
+    eng.prefetch(batches[0], offs)
+    for it, ids in enumerate(batches):
+        if it == 4:
+            eng.prefetch(stray, offs)  # never consumed: batch 5 is not prefetched
+        elif it + 1 < len(batches) and it != 4:
+            eng.prefetch(batches[it + 1], offs)
+        dec, rep = eng.iterate(ids, offs)
+        wdec, wexp, wrep, _ = sim.iteration(ids, offs)
+        assert (dec == wdec).all(), f"iter {it}: decision"
+        assert rep.as_dict() == wrep, f"iter {it}: report"
+        assert rep.expected_cost_s == wexp, f"iter {it}: expected cost"
+    msg = canon_equal(eng.canonical_state(), sim.canonical_state())
+    assert not msg, msg
+    bad = offs.copy()
+    bad[1], bad[2] = bad[2], bad[1]
+    with pytest.raises(edx.InvalidArgument, match="non-decreasing"):
+        eng.prefetch(batches[0], bad)
+    with pytest.raises(edx.InvalidArgument, match="no samples"):
+        eng.prefetch(batches[0], offs[:1])
+
+
+def test_iterate_prefetch_next(gpu, oracle, pyoracle):
+    """edx_engine_iterate_prefetch: the loop bench.py's e2e leg runs (batch
+    i+1 prefetched once iteration i is launched) equals the reference; a bad
+    next batch is rejected before the iteration starts (clock unchanged)."""
+    import torch
+    edx = gpu
+    p = CONFIGS["C2"]
+    n, m, L = p["n"], p["m"], p["L"]
+    R = n * m
+    c = edx.ClusterConfig(n=n, m=m, bandwidths_bps=p["bw"], cache_capacity=p["cap"], alpha=0.5)
+    eng = edx.SimState(c, id_space=p["V"], max_batch_ids=R * L)
+    sim = oracle.sim(pyoracle.Cfg(n, m, p["bw"], cap=p["cap"], alpha=0.5))
+    offs = torch.from_numpy(offsets_for(R, L).view(np.int64)).pin_memory().numpy().view(np.uint64)
+    batches = [torch.from_numpy(b.view(np.int32)).pin_memory().numpy().view(np.uint32)
+               for b in oracle.zipf_batches(p["V"], L, 1.05, 8, 29, R)]
+    eng.prefetch(batches[0], offs)
+    for it, ids in enumerate(batches):
+        nxt = (batches[it + 1], offs) if it + 1 < len(batches) else None
+        dec, rep = eng.iterate(ids, offs, prefetch_next=nxt)
+        wdec, wexp, wrep, _ = sim.iteration(ids, offs)
+        assert (dec == wdec).all(), f"iter {it}: decision"
+        assert rep.as_dict() == wrep, f"iter {it}: report"
+        assert rep.expected_cost_s == wexp, f"iter {it}: expected cost"
+    bad = offs.copy()
+    bad[1], bad[2] = bad[2], bad[1]
+    clock = eng.clock()
+    with pytest.raises(edx.InvalidArgument, match="non-decreasing"):
+        eng.iterate(batches[0], offs, prefetch_next=(batches[1], bad))
+    assert eng.clock() == clock
+    msg = canon_equal(eng.canonical_state(), sim.canonical_state())
+    assert not msg, msg
