@@ -308,6 +308,25 @@ int edx_zipf_next(edx_zipf* z, uint32_t* ids);
 void edx_zipf_reset(edx_zipf* z);
 void edx_zipf_destroy(edx_zipf* z);
 
+/* ------------------------------------------------------------ trace input
+ * TraceStream (workload.hpp:176-268): a plain-text trace, one sample per line,
+ * read once and held as per-iteration CSR (offsets rebased to 0) for the
+ * engine's batch entry points.  n_tables = 0: no schema; otherwise the
+ * schema's table sizes and names (TraceSchema, workload.hpp:137-150).  Errors
+ * are EDX_RUNTIME_ERROR with the reference's messages; the dropped trailing
+ * partial iteration is reported by edx_trace_info (the caller warns). */
+typedef struct edx_trace edx_trace;
+int edx_trace_load(const char* path, uint64_t n_tables, const uint64_t* table_sizes,
+                   const char* const* table_names, uint64_t samples_per_iteration,
+                   uint64_t cache_capacity, uint64_t m, edx_trace** out);
+void edx_trace_info(const edx_trace* t, uint64_t* iterations, uint64_t* dropped,
+                    uint64_t* max_sample_len, uint64_t* samples);
+/* Iteration it (< iterations): ids, offsets[samples_per_iteration + 1] and the
+ * id count, pointing into the trace (valid until edx_trace_destroy). */
+int edx_trace_iteration(const edx_trace* t, uint64_t it, const uint32_t** ids,
+                        const uint64_t** offsets, uint64_t* num_ids);
+void edx_trace_destroy(edx_trace* t);
+
 #ifdef __cplusplus
 }
 #endif

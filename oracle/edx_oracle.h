@@ -177,6 +177,11 @@ int orc_report_jsonl(const orc_iter_report* rep, char* out, uint64_t cap, uint64
 int orc_comparison_csv(const orc_run_summary* runs, uint64_t count, const char* reference,
                        const orc_cluster_config* cfg, char* out, uint64_t cap, uint64_t* len);
 
+/* TraceStream dump (workload.hpp:176-268; compiled reference only):
+ * "iterations I dropped D max M\n", kept samples one per line, warnings. */
+int orc_trace_dump(const char* path, const char* schema_path, int32_t n, int32_t m,
+                   uint64_t capacity, char* out, uint64_t cap, uint64_t* len);
+
 /* Cross-check counters: total Dijkstra steps of the last orc_hungarian call. */
 uint64_t orc_last_hungarian_steps(void);
 

@@ -171,6 +171,18 @@ class Oracle:
         finally:
             self.lib.orc_zipf_destroy(h)
 
+    def trace_dump(self, path, schema_path, n, m, capacity):
+        """Compiled reference only: TraceStream(path, cfg, schema) dumped as
+        text by oracle/_ref/trace_dump (its own process: the reference's
+        iostreams and numpy's C++ runtime do not share one safely); returns
+        (True, text) or (False, message)."""
+        import subprocess
+        exe = os.path.join(os.path.dirname(REF_SO), "trace_dump")
+        r = subprocess.run([exe, path, schema_path or "-", str(n), str(m), str(capacity)],
+                           capture_output=True, check=True)
+        head, _, body = r.stdout.partition(b"\n")
+        return head == b"OK", body.decode("latin-1")
+
     def bench_matrix(self, k):
         out = np.empty(k * k, np.float64)
         self.lib.orc_bench_matrix(k, _p(out, C.c_double))

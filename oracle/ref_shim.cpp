@@ -18,6 +18,7 @@
 #include <chrono>
 #include <cstring>
 #include <exception>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -540,5 +541,33 @@ int orc_comparison_csv(const orc_run_summary* runs, uint64_t count, const char* 
       s.ops_w.assign(r.ops_w, r.ops_w + r.n);
     }
     put_string(comparison_csv(results, reference, to_cfg(c)), out, cap, len);
+  });
+}
+
+/* TraceStream / load_schema (workload.hpp:152-268) through the reference:
+ * "iterations I dropped D max M\n", one line per kept sample, then the
+ * warning text the reference wrote. */
+int orc_trace_dump(const char* path, const char* schema_path, int32_t n, int32_t m,
+                   uint64_t capacity, char* out, uint64_t cap, uint64_t* len) {
+  return guarded([&] {
+    ClusterConfig cfg;
+    cfg.n = n;
+    cfg.m = m;
+    cfg.cache_capacity = capacity;
+    TraceSchema schema;
+    if (schema_path) schema = load_schema(schema_path);
+    std::ostringstream warn;
+    TraceStream ts(path, cfg, schema_path ? &schema : nullptr, &warn);
+    std::ostringstream os;
+    os << "iterations " << ts.iterations() << " dropped " << ts.dropped_samples() << " max "
+       << ts.max_sample_len() << "\n";
+    std::vector<EmbeddingSample> batch;
+    while (ts.next_iteration(batch))
+      for (const auto& smp : batch) {
+        for (std::size_t i = 0; i < smp.ids.size(); ++i) os << (i ? " " : "") << smp.ids[i];
+        os << "\n";
+      }
+    os << warn.str();
+    put_string(os.str(), out, cap, len);
   });
 }

@@ -19,6 +19,8 @@ reference so parity tests read like its own tests:
     decision_cost          assign.hpp:288  decision_cost
     SimState                  sim.hpp:54   SimState (state resident on the GPU)
     ZipfStream           workload.hpp:94   ZipfStream
+    TraceSchema/load_schema   :137-172    TraceSchema / load_schema
+    TraceStream          workload.hpp:176  TraceStream (CSR batches)
 
 std::invalid_argument -> InvalidArgument (a ValueError), std::logic_error ->
 LogicError.  Every computation runs in the CUDA kernels of libedx.so; this
@@ -37,7 +39,8 @@ from ._lib import (EDX_NUM_PHASES, ClusterConfigC, CudaError, EdxError, EdxRunti
 
 __all__ = [
     "ClusterConfig", "EmbeddingState", "Snapshot", "CostMatrix", "SquareCost", "AssignmentResult",
-    "DispatchDecision", "IterationReport", "SimState", "ZipfStream", "validate", "unit_cost",
+    "DispatchDecision", "IterationReport", "SimState", "ZipfStream",
+    "TraceSchema", "load_schema", "TraceStream", "validate", "unit_cost",
     "make_sample", "to_csr", "build_matrix", "expected_cost", "row_gap_key", "rows_by_gap", "hungarian",
     "hungarian_blocks", "greedy_dispatch", "expand_columns", "ecomix", "decision_cost",
     "exact_multiplicity", "InvalidArgument", "LogicError", "EdxRuntimeError", "CudaError",
@@ -755,6 +758,113 @@ class ZipfStream:
     def __del__(self):
         if getattr(self, "_h", None):
             lib().edx_zipf_destroy(self._h)
+            self._h = None
+
+
+@dataclass
+class TraceSchema:
+    """TraceSchema (workload.hpp:137-150): (name, size) per table; row ids
+    flatten into one id space by the cumulative table sizes."""
+    tables: List[tuple] = field(default_factory=list)
+
+    def total_embeddings(self) -> int:
+        return sum(size for _, size in self.tables)
+
+
+_WS = b" \t\n\v\f\r"
+
+
+def load_schema(path: str) -> TraceSchema:
+    """load_schema (workload.hpp:152-172): "name size" per line, blank lines
+    skipped; `size` read as `istream >> size_t` does (optional sign, decimal
+    prefix, < 2**64, '-' wrapping) and must be non-zero."""
+    try:
+        raw = open(path, "rb").read()
+    except OSError:
+        raise EdxRuntimeError(f"cannot open schema file: {path}") from None
+    import re
+    schema = TraceSchema()
+    lines = raw.split(b"\n")
+    if lines and lines[-1] == b"":
+        lines.pop()
+    for no, line in enumerate(lines, 1):
+        parts = line.lstrip(_WS)
+        if not parts:
+            continue
+        name_end = next((i for i, ch in enumerate(parts) if ch in _WS), len(parts))
+        name, rest = parts[:name_end], parts[name_end:].lstrip(_WS)
+        mt = re.match(rb"([+-]?)([0-9]+)", rest)
+        size = None
+        if mt and int(mt.group(2)) < 2 ** 64:
+            size = int(mt.group(2))
+            if mt.group(1) == b"-":
+                size = (-size) % 2 ** 64
+        if not size:
+            raise EdxRuntimeError(f"{path}:{no}: expected 'table_name size'")
+        schema.tables.append((name.decode("latin-1"), size))
+    if not schema.tables:
+        raise EdxRuntimeError(f"schema file declares no tables: {path}")
+    return schema
+
+
+class TraceStream:
+    """TraceStream (workload.hpp:176-268): one sample per line of decimal ids,
+    m*n samples per iteration, a trailing partial iteration dropped with a
+    warning.  Parsed once by libedx on all host threads; each iteration is the
+    engine's CSR batch `(ids uint32, offsets uint64[R+1])`, ready for
+    `SimState.load` / `iterate` / `prefetch`."""
+
+    def __init__(self, path: str, cfg: ClusterConfig, schema: Optional[TraceSchema] = None,
+                 warnings=None):
+        import sys
+        self._h = C.c_void_p()
+        names = [n.encode("latin-1") for n, _ in (schema.tables if schema else [])]
+        sizes = np.array([sz for _, sz in (schema.tables if schema else [])], np.uint64)
+        name_arr = (C.c_char_p * max(1, len(names)))(*names)
+        check(lib().edx_trace_load(path.encode(), len(names), _ptr(sizes, C.c_uint64), name_arr,
+                                   cfg.samples_per_iteration(), int(cfg.cache_capacity),
+                                   int(cfg.m), C.byref(self._h)))
+        it, dropped, mx = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        lib().edx_trace_info(self._h, C.byref(it), C.byref(dropped), C.byref(mx), None)
+        self._iterations, self._dropped, self._max = it.value, dropped.value, mx.value
+        self.R = cfg.samples_per_iteration()
+        self._cursor = 0
+        out = sys.stderr if warnings is None else warnings
+        if self._dropped and out is not False:
+            out.write(f"warning: {path}: dropping {self._dropped} trailing sample(s) "
+                      "of a partial iteration\n")
+
+    def iterations(self) -> int: return self._iterations
+    def dropped_samples(self) -> int: return self._dropped
+    def max_sample_len(self) -> int: return self._max
+
+    def batch_csr(self, it: int):
+        ids_p, offs_p, n = _P(C.c_uint32)(), _P(C.c_uint64)(), C.c_uint64()
+        check(lib().edx_trace_iteration(self._h, int(it), C.byref(ids_p), C.byref(offs_p),
+                                        C.byref(n)))
+        ids = np.ctypeslib.as_array(ids_p, (n.value,)).copy() if n.value else \
+            np.empty(0, np.uint32)
+        return ids, np.ctypeslib.as_array(offs_p, (self.R + 1,)).copy()
+
+    def next_iteration(self):
+        if self._cursor >= self._iterations:
+            return None
+        self._cursor += 1
+        return self.batch_csr(self._cursor - 1)
+
+    def __iter__(self):
+        while True:
+            b = self.next_iteration()
+            if b is None:
+                return
+            yield b
+
+    def reset(self):
+        self._cursor = 0
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().edx_trace_destroy(self._h)
             self._h = None
 
 

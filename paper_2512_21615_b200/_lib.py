@@ -126,6 +126,10 @@ def _sigs():
         ("edx_zipf_next", cint, [vp, u32p]),
         ("edx_zipf_reset", None, [vp]),
         ("edx_zipf_destroy", None, [vp]),
+        ("edx_trace_load", cint, [C.c_char_p, u64, u64p, P(C.c_char_p), u64, u64, u64, P(vp)]),
+        ("edx_trace_info", None, [vp, u64p, u64p, u64p, u64p]),
+        ("edx_trace_iteration", cint, [vp, u64, P(u32p), P(u64p), u64p]),
+        ("edx_trace_destroy", None, [vp]),
     ]
 
 

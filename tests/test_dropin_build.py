@@ -23,3 +23,13 @@ def test_report_formats_match_reference():
                        timeout=300)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     assert "OK" in r.stdout
+
+
+def test_trace_stream_dropin():
+    """TraceStream / load_schema / write_trace through the drop-in C++ headers:
+    the reference's trace tests (test_workload.cpp:179-281), host only."""
+    subprocess.run(["make", "-s", "-C", HERE, "trace_test"], check=True)
+    r = subprocess.run([os.path.join(HERE, "trace_test")], capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    assert "OK" in r.stdout
