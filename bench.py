@@ -447,8 +447,17 @@ def reference_arm(args, w, rank, world):
     }
 
 
+def emit(out, fd):
+    os.write(fd, (json.dumps(out) + "\n").encode())
+
+
 def main():
     args = parse()
+    # native libraries write to fd 1 (NCCL's version banner at communicator
+    # init): route everything else to stderr, keep stdout for the one JSON line
+    sys.stdout.flush()
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
@@ -456,7 +465,7 @@ def main():
     if args.impl == "reference":
         out = reference_arm(args, w, rank, world)
         if out is not None:
-            print(json.dumps(out), flush=True)
+            emit(out, json_fd)
         return
     if world > 1:
         import torch
@@ -475,7 +484,7 @@ def main():
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(w, host, offs, args.cpu_sample)
-        print(json.dumps(out), flush=True)
+        emit(out, json_fd)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

@@ -530,7 +530,7 @@ void engine_step(edx_engine* e, const int32_t* decision, edx_report* rep) {
 }
 
 // One fused iteration (build -> dispatch -> step) for an already-loaded
-// batch.  On one GPU with device-decided victims and profiling off it runs as
+// batch.  With device-decided victims and profiling off it runs as
 // a CUDA graph captured on first use and replayed while (rows, ids, alpha)
 // stay the same -- the ~40 launches of an iteration become one.  Any capture
 // failure disables graphs for the engine and the iteration runs eagerly.
@@ -553,8 +553,13 @@ void engine_iterate_core(edx_engine* e, double alpha) {
   if (e->graph_mode < 0) {
     const char* v = std::getenv("EDX_GRAPH");
     e->graph_mode = (v && std::strcmp(v, "0") == 0) ? 0 : 1;
+    // sharded engines capture their NCCL gather / broadcast into the graph too
+    // (every rank replays the same collective sequence); EDX_MULTI_GRAPH=0 keeps
+    // them eager
+    const char* mv = std::getenv("EDX_MULTI_GRAPH");
+    if (e->world > 1 && mv && std::strcmp(mv, "0") == 0) e->graph_mode = 0;
   }
-  const bool eligible = e->graph_mode == 1 && e->world == 1 && !e->profiling &&
+  const bool eligible = e->graph_mode == 1 && !e->profiling &&
                         edx::step_device_only(e) && e->cur_ids == e->ids.p;
   if (!eligible) {
     iterate_enqueue(e, alpha);
