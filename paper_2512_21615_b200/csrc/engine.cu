@@ -553,11 +553,12 @@ void engine_iterate_core(edx_engine* e, double alpha) {
   if (e->graph_mode < 0) {
     const char* v = std::getenv("EDX_GRAPH");
     e->graph_mode = (v && std::strcmp(v, "0") == 0) ? 0 : 1;
-    // sharded engines capture their NCCL gather / broadcast into the graph too
-    // (every rank replays the same collective sequence); EDX_MULTI_GRAPH=0 keeps
-    // them eager
+    // sharded engines can capture their NCCL gather / broadcast into the graph
+    // too (EDX_MULTI_GRAPH=1; every rank replays the same collective sequence).
+    // Parity-green at 2 and 4 ranks, but within noise of eager (C2 / C5 at
+    // N = 2, 4: +0.0..0.8%), so eager stays the default there.
     const char* mv = std::getenv("EDX_MULTI_GRAPH");
-    if (e->world > 1 && mv && std::strcmp(mv, "0") == 0) e->graph_mode = 0;
+    if (e->world > 1 && !(mv && std::strcmp(mv, "1") == 0)) e->graph_mode = 0;
   }
   const bool eligible = e->graph_mode == 1 && !e->profiling &&
                         edx::step_device_only(e) && e->cur_ids == e->ids.p;
