@@ -348,7 +348,7 @@ def product(args, w, rank, world, local_rank):
                               "peak_source": "profiles/r01_dadd_peak.json (tools/dadd_peak.cu)",
                               "note": "second roof of the build (sequential fp64 add chains, "
                                       "SURVEY 8d); adds counted on the first timed batch"}},
-        "dominant_kernel": ("k_hungarian_blocks_mw (exact EcoMix block; latency-bound, one CTA, warp per block)" if n <= 16 else "k_hungarian_blocks_run (exact EcoMix block; latency-bound, one CTA)"),
+        "dominant_kernel": dominant_kernel(n, phase_ms),
         "solver": {"exact_rows": n * int(np.floor(m * w["alpha"] + 1e-9)),
                    "latency_ms_per_batch": phase_ms[2] / K,
                    "dijkstra_steps_last_batch": solver_steps,
@@ -445,6 +445,18 @@ def reference_arm(args, w, rank, world):
                 "d2h_bytes_per_step": 0},
         "build_decide": {"value": w["R"] / (sum(bd) / len(bd)), "unit": "samples/s"},
     }
+
+
+def dominant_kernel(n, phase_ms):
+    """The phase with the largest device time (profiled pass) and its main kernel."""
+    names = {
+        0: "k_cost_build (K1 cost build, cost.hpp:81-125)",
+        2: ("k_hungarian_blocks_mw (exact EcoMix block; latency-bound, one CTA, warp per block)"
+            if n <= 16 else "k_hungarian_blocks_run (exact EcoMix block; latency-bound, one CTA)"),
+        3: "k_greedy (EcoMix greedy, assign.hpp:162-192; one CTA, rows in gap order)",
+        4: "K7 step kernels (cache update, sim.hpp:87-218; k_select_victims the largest)",
+    }
+    return names[max(names, key=lambda i: phase_ms[i])]
 
 
 def emit(out, fd):
