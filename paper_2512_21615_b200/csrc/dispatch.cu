@@ -142,15 +142,22 @@ __global__ void __launch_bounds__(kGreedyThreads)
       if (choice < 0) {
         const double* r = matrix + static_cast<uint64_t>(row) * n;
         double best = __longlong_as_double(0x7ff0000000000000LL);
-        unsigned long long it = om;
-        while (it) {
-          const int w = __ffsll(static_cast<long long>(it)) - 1;
-          it &= it - 1;
-          const double c = r[w];
-          if (c < best) {
-            best = c;
-            choice = w;
+        // sixteen workers per group, all of a group's loads in flight before
+        // the ascending strict-'<' compares (closed workers read as +inf,
+        // which never beats `best`)
+        for (int base = 0; base < n; base += 16) {
+          double c[16];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            const int w = base + k;
+            c[k] = (w < n && ((om >> w) & 1ULL)) ? r[w] : best;
           }
+#pragma unroll
+          for (int k = 0; k < 16; ++k)
+            if (c[k] < best) {
+              best = c[k];
+              choice = base + k;
+            }
         }
       }
       if (choice < 0) atomicOr(flags + kFlagUnbalanced, 1);  // "capacities exhausted"
