@@ -311,8 +311,8 @@ void edx_zipf_destroy(edx_zipf* z);
 /* ------------------------------------------------------------ trace input
  * TraceStream (workload.hpp:176-268): a plain-text trace, one sample per line,
  * read once and held as per-iteration CSR (offsets rebased to 0) for the
- * engine's batch entry points.  n_tables = 0: no schema; otherwise the
- * schema's table sizes and names (TraceSchema, workload.hpp:137-150).  Errors
+ * engine's batch entry points.  table_sizes = NULL: no schema; otherwise the
+ * schema's n_tables table sizes and names (TraceSchema, workload.hpp:137-150).  Errors
  * are EDX_RUNTIME_ERROR with the reference's messages; the dropped trailing
  * partial iteration is reported by edx_trace_info (the caller warns). */
 typedef struct edx_trace edx_trace;

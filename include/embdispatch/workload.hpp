@@ -117,7 +117,10 @@ class TraceStream final : public SampleStream {
         names.push_back(t.name.c_str());
       }
     edx_trace* t = nullptr;
-    edxc::check(edx_trace_load(path.c_str(), sizes.size(), sizes.data(), names.data(),
+    static const std::uint64_t kNoTables = 0;  // a schema without tables is still a schema
+    const std::uint64_t* sizes_p =
+        schema == nullptr ? nullptr : (sizes.empty() ? &kNoTables : sizes.data());
+    edxc::check(edx_trace_load(path.c_str(), sizes.size(), sizes_p, names.data(),
                                cfg.samples_per_iteration(), cfg.cache_capacity,
                                static_cast<std::uint64_t>(cfg.m), &t));
     t_.reset(t);

@@ -821,7 +821,10 @@ class TraceStream:
         names = [n.encode("latin-1") for n, _ in (schema.tables if schema else [])]
         sizes = np.array([sz for _, sz in (schema.tables if schema else [])], np.uint64)
         name_arr = (C.c_char_p * max(1, len(names)))(*names)
-        check(lib().edx_trace_load(path.encode(), len(names), _ptr(sizes, C.c_uint64), name_arr,
+        no_tables = (C.c_uint64 * 1)()  # a schema without tables is still a schema
+        sizes_p = (None if schema is None else
+                   _ptr(sizes, C.c_uint64) if len(sizes) else C.cast(no_tables, _P(C.c_uint64)))
+        check(lib().edx_trace_load(path.encode(), len(names), sizes_p, name_arr,
                                    cfg.samples_per_iteration(), int(cfg.cache_capacity),
                                    int(cfg.m), C.byref(self._h)))
         it, dropped, mx = C.c_uint64(), C.c_uint64(), C.c_uint64()

@@ -82,6 +82,7 @@ struct Chunk {
 };
 
 struct Params {
+  bool schema;  // table_sizes != NULL: a schema, possibly with no tables
   uint64_t n_tables;
   const uint64_t* table_sizes;
   std::vector<uint64_t> table_offsets;
@@ -114,7 +115,7 @@ void parse_chunk(Chunk& c, const Params& p) {
     }
     s = nl ? nl + 1 : c.end;
     if (raw.empty()) continue;
-    if (p.n_tables != 0) {
+    if (p.schema) {
       if (raw.size() != p.n_tables) {
         c.err = {Error::kFieldCount, line, {}, p.n_tables, raw.size()};
         return;
@@ -176,7 +177,7 @@ int edx_trace_load(const char* path, uint64_t n_tables, const uint64_t* table_si
     std::fclose(f);
   }
 
-  Params p{n_tables, table_sizes, {}, cache_capacity / m};
+  Params p{table_sizes != nullptr, n_tables, table_sizes, {}, cache_capacity / m};
   uint64_t acc = 0;
   for (uint64_t i = 0; i < n_tables; ++i) {
     p.table_offsets.push_back(acc);

@@ -78,6 +78,14 @@ def test_schema_offsets_flatten(edx, tmp_path):
         edx.TraceStream(bad, cfg_of(edx, 2, 1), schema)
 
 
+def test_schema_without_tables(edx, tmp_path):
+    """A TraceSchema with no tables is still a schema: every id line has too
+    many fields (workload.hpp:227-232 with an empty offset list)."""
+    p = write(tmp_path, "z.txt", "\n1 2 3\n")
+    with pytest.raises(edx.EdxRuntimeError, match=":2: expected 0 fields per schema, got 3"):
+        edx.TraceStream(p, cfg_of(edx, 2, 1), edx.TraceSchema())
+
+
 def test_oversized_sample_rejected(edx, tmp_path):
     p = write(tmp_path, "i.txt", "1 2 3\n4 5 6\n7 8 9\n10 11 12\n")
     with pytest.raises(edx.EdxRuntimeError,
