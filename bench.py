@@ -7,10 +7,13 @@ expected-cost matrix build -> EcoMix decision (exact Hungarian block +
 capacity-bounded greedy) -> per-worker cache update (SimState::step).  The
 batches are sequential because each dispatch changes the cache state.
 
-Default workload = BASELINE.json configs[1] ("C2"): 8 heterogeneous workers
-(4 x 5 Gbps + 4 x 0.5 Gbps), batch 1024 (m=128), 26 Zipf(1.05) ids per
-sample over 100K ids, 10K-entry caches, hybrid dispatcher alpha=0.5.  Before
-timing, `prefill` iterations bring the caches to steady state (evicting).
+Default workload = BASELINE.json configs[2] ("C3"), the largest configuration
+that runs on one GPU (configs[3], C4, is declared 8-GPU sharded): Criteo-shaped,
+16 heterogeneous workers (8 x 5 Gbps + 8 x 0.5 Gbps), batch 8192 (m=512), 26
+Zipf(1.05) ids per sample over a 10M-id vocabulary, 800K-entry caches, hybrid
+dispatcher alpha=0.125 (an exact block of k = 1024 rows).  `prefill`
+untimed iterations precede the timed ones.  --config C1/C2/C4/C5 select the
+other BASELINE configs (parity-test cases, not the headline).
 
   value : samples/s with the batches already resident in HBM
   e2e   : samples/s through the C ABI (edx_engine_iterate) from pinned host
@@ -59,7 +62,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="product", choices=["product", "reference"])
-    ap.add_argument("--config", default="C2", choices=sorted(WORKLOADS))
+    ap.add_argument("--config", default="C3", choices=sorted(WORKLOADS))
     ap.add_argument("--alpha", type=float, default=None)
     ap.add_argument("--prefill", type=int, default=None)
     ap.add_argument("--cpu-sample", type=int, default=10, help="timed iterations of cpu_baseline")
@@ -68,6 +71,9 @@ def parse():
     ap.add_argument("--batch", type=int, default=None, help="C5 sweep: samples per iteration")
     ap.add_argument("--workers", type=int, default=None, help="C5 sweep: workers (<= 64)")
     ap.add_argument("--debug-times", action="store_true", help="per-iteration times in the line")
+    ap.add_argument("--no-ncu", action="store_true",
+                    help="skip the ncu DRAM-traffic capture of the cost build")
+    ap.add_argument("--ncu-child", action="store_true", help=argparse.SUPPRESS)
     return ap.parse_args()
 
 
@@ -99,6 +105,18 @@ def batches(w, count):
     import paper_2512_21615_b200 as edx
     z = edx.ZipfStream(w["V"], w["L"], ZIPF_S, count, SEED, w["R"])
     return [ids for ids in z]
+
+
+def reference_batches(w, count):
+    """The same stream from the reference's own ZipfStream (oracle/_ref), so
+    the reference arm maps no product library."""
+    orc, _ = reference_oracle()
+    return list(orc.zipf_batches(w["V"], w["L"], ZIPF_S, count, SEED, w["R"]))
+
+
+def parallelism(world):
+    return (f"row-sharded cost build x{world}, NCCL gather to rank 0, rank-0 solve, decision "
+            "broadcast, replicated cache update" if world > 1 else "1 GPU")
 
 
 def config_json(w, args, extra=None):
@@ -312,32 +330,29 @@ def product(args, w, rank, world, local_rank):
     except (OSError, ValueError, KeyError):
         pass
     fp64_rate = f_alg / (t_build_ms * 1e-3) if (f_alg and t_build_ms > 0) else None
-    traffic = None
-    try:
-        traffic = json.load(open(os.path.join(ROOT, "profiles", "k_cost_build_traffic.json")))
-        traffic = traffic.get(args.config, {}).get("dram_bytes_per_launch")
-    except (OSError, ValueError):
-        traffic = None
+    kernels = eng.last_kernels()
+    traffic = None if (args.no_ncu or world > 1) else ncu_build_traffic(args, kernels["build"])
 
     out = {
         "metric": METRIC, "value": R / (step_ms * 1e-3), "unit": "samples/s", "n_gpus": world,
         "steps": K, "warmup": W, "ms_per_step": step_ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: reference ZipfStream (s=1.05, seed 42), state warmed by prefill",
-        "config": config_json(w, args, {"parallelism": f"row-sharded cost build x{world}, "
-                                        "NCCL gather to rank 0, rank-0 solve, decision broadcast, "
-                                        "replicated cache update" if world > 1 else "1 GPU"}),
+        "config": config_json(w, args, {"parallelism": parallelism(world)}),
         "e2e": {"value": R / (e2e_step_ms * 1e-3), "unit": "samples/s",
                 "ms_per_step": e2e_step_ms,
                 "note": "edx_engine_iterate from pinned host buffers; the next batch's H2D is "
                         "prefetched on the engine's copy stream during each iteration",
                 "h2d_bytes_per_step": R * L * 4 + (R + 1) * 8,
                 "d2h_bytes_per_step": R * 4 + 8 + (3 * n + 4) * 8},
-        "roofline": {"kernel": ("k_cost_build_warp" if 2 <= n <= 8 else "k_cost_build_wide"
-                                if 8 < n <= 32 else "k_cost_build") + " (K1, cost.hpp:81-125)",
+        "roofline": {"kernel": kernels["build"] + " (K1, cost.hpp:81-125)",
                      "bound": "hbm",
                      "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": (achieved / hbm_peak) if achieved else None, "traffic": traffic,
+                     "frac": (achieved / hbm_peak) if achieved else None,
+                     "traffic": traffic["dram_bytes"] if traffic else None,
+                     "traffic_source": traffic["source"] if traffic else
+                     "not captured (--no-ncu, N > 1, or ncu unavailable)",
+                     "traffic_launch_ns_ncu": traffic["ncu_ns"] if traffic else None,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else
                      "fallback 6.65 TB/s",
                      "algorithmic_bytes_per_launch": sum(b_alg) / K,
@@ -348,7 +363,8 @@ def product(args, w, rank, world, local_rank):
                               "peak_source": "profiles/r01_dadd_peak.json (tools/dadd_peak.cu)",
                               "note": "second roof of the build (sequential fp64 add chains, "
                                       "SURVEY 8d); adds counted on the first timed batch"}},
-        "dominant_kernel": dominant_kernel(n, phase_ms),
+        "dominant_kernel": dominant_kernel(kernels, phase_ms),
+        "kernels": kernels,
         "solver": {"exact_rows": n * int(np.floor(m * w["alpha"] + 1e-9)),
                    "latency_ms_per_batch": phase_ms[2] / K,
                    "dijkstra_steps_last_batch": solver_steps,
@@ -426,7 +442,7 @@ def reference_arm(args, w, rank, world):
         return None
     threads = os.cpu_count() or 1
     K, W, P = args.steps, args.warmup, w["prefill"]
-    host = batches(w, P + W + K)
+    host = reference_batches(w, P + W + K)
     offs = np.arange(w["R"] + 1, dtype=np.uint64) * np.uint64(w["L"])
     times, bd, kind = cpu_run(w, host, offs, P, W, K, threads=threads)
     mean = sum(times) / len(times)
@@ -436,7 +452,7 @@ def reference_arm(args, w, rank, world):
         "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": mean * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: reference ZipfStream (s=1.05, seed 42), state warmed by prefill",
-        "config": config_json(w, args),
+        "config": config_json(w, args, {"parallelism": parallelism(world)}),
         "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads, "kind": kind,
                          "sample": f"iterations {P + W}..{P + W + K - 1}; build_matrix rows "
                                    f"split over {threads} threads (bit-identical), ecomix and "
@@ -447,16 +463,80 @@ def reference_arm(args, w, rank, world):
     }
 
 
-def dominant_kernel(n, phase_ms):
-    """The phase with the largest device time (profiled pass) and its main kernel."""
+def dominant_kernel(kernels, phase_ms):
+    """The phase with the largest device time (profiled pass) and the kernel
+    the engine launched for it (edx_engine_last_kernels)."""
     names = {
-        0: "k_cost_build (K1 cost build, cost.hpp:81-125)",
-        2: ("k_hungarian_blocks_mw (exact EcoMix block; latency-bound, one CTA, warp per block)"
-            if n <= 16 else "k_hungarian_blocks_run (exact EcoMix block; latency-bound, one CTA)"),
-        3: "k_greedy (EcoMix greedy, assign.hpp:162-192; one CTA, rows in gap order)",
-        4: "K7 step kernels (cache update, sim.hpp:87-218; k_select_victims the largest)",
+        0: f"{kernels['build']} (K1 cost build, cost.hpp:81-125)",
+        2: f"{kernels['solver']} (K6 exact EcoMix block, assign.hpp:80-157; latency-bound)",
+        3: f"{kernels['greedy']} (K4 EcoMix greedy, assign.hpp:162-192)",
+        4: "K7 step kernels (cache update, sim.hpp:87-218)",
     }
     return names[max(names, key=lambda i: phase_ms[i])]
+
+
+# ------------------------------------------------- K1 DRAM traffic (ncu)
+def ncu_child(args, w):
+    """Run under ncu by ncu_build_traffic: the product engine, eagerly (no
+    CUDA graph), over the same prefill + warm-up batches as the timed run,
+    then ONE cost build of the first timed batch -- the launch ncu captures."""
+    import paper_2512_21615_b200 as edx
+    n, m, L, R = w["n"], w["m"], w["L"], w["R"]
+    P, W = w["prefill"], args.warmup
+    host = batches(w, P + W + 1)
+    offs = np.arange(R + 1, dtype=np.uint64) * np.uint64(L)
+    cfg = edx.ClusterConfig(n=n, m=m, bandwidths_bps=w["bw"], d_tran_bytes=2048,
+                            cache_capacity=w["cap"], alpha=w["alpha"])
+    eng = edx.SimState(cfg, id_space=w["V"], max_batch_ids=R * L)
+    for b in host[:P + W]:
+        eng.iterate(b, offs, want_decision=False)
+    eng.load((host[P + W], offs))
+    eng.build(None)
+    eng.dispatch(want_decision=False, want_expected=False)
+
+
+def ncu_build_traffic(args, kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the first timed batch's
+    cost-build launch, captured by ncu in a child process of this run (cold L2,
+    as the timed loop's flush makes it)."""
+    import shutil
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return None
+    w = workload(args)
+    skip = w["prefill"] + args.warmup
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
+           "--clock-control", "none", "--print-units", "base", "--csv",
+           "-k", "regex:^k_cost_build", "--launch-skip", str(skip), "--launch-count", "1",
+           sys.executable, os.path.abspath(__file__), "--ncu-child", "--config", args.config,
+           "--warmup", str(args.warmup)]
+    for flag, val in (("--alpha", args.alpha), ("--prefill", args.prefill),
+                      ("--batch", args.batch), ("--workers", args.workers)):
+        if val is not None:
+            cmd += [flag, str(val)]
+    env = dict(os.environ, EDX_GRAPH="0")
+    for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK"):
+        env.pop(k, None)
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
+    except (OSError, subprocess.TimeoutExpired):
+        return None
+    vals = {}
+    import csv
+    rows = [l for l in r.stdout.splitlines() if l.startswith('"')]
+    for rec in csv.DictReader(rows):
+        name, val = rec.get("Metric Name"), rec.get("Metric Value", "").replace(",", "")
+        if name and val:
+            try:
+                vals[name] = float(val)
+            except ValueError:
+                pass
+    if "dram__bytes_read.sum" not in vals:
+        return None
+    return {"dram_bytes": vals["dram__bytes_read.sum"] + vals.get("dram__bytes_write.sum", 0.0),
+            "ncu_ns": vals.get("gpu__time_duration.sum"),
+            "source": f"ncu in this run: {kernel}, launch {skip} (first timed batch), "
+                      "dram__bytes_read.sum + dram__bytes_write.sum, cold L2"}
 
 
 def emit(out, fd):
@@ -474,6 +554,9 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
     w = workload(args)
+    if args.ncu_child:
+        ncu_child(args, w)
+        return
     if args.impl == "reference":
         out = reference_arm(args, w, rank, world)
         if out is not None:

@@ -177,6 +177,15 @@ int edx_engine_state_of(edx_engine* e, uint32_t id, uint64_t* owners, uint64_t* 
 int edx_engine_validate_consistency(edx_engine* e);
 /* SimState::clock — sim.hpp:61. */
 uint64_t edx_engine_clock(edx_engine* e);
+/* Counter bumped by every state mutation (step, seed_entry, the imports): a
+ * Snapshot view of the device state is current while it is unchanged. */
+uint64_t edx_engine_state_version(edx_engine* e);
+/* Waits for the work enqueued on the engine (e.g. an edx_engine_build without
+ * matrix_out) and reports device-side errors. */
+int edx_engine_synchronize(edx_engine* e);
+/* decision_cost(matrix, decision) — assign.hpp:288-298 — of the last
+ * dispatch (computed on a side stream; this call waits for it). */
+int edx_engine_expected_cost(edx_engine* e, double* out);
 
 /* Parity exports (SimState::cache(j).entries(), cache.hpp:180-182, and the
  * global map).  Global: ids with any non-zero mask, ascending id; call with
@@ -196,6 +205,22 @@ int edx_engine_import_snapshot(edx_engine* e, const uint32_t* ids, const uint64_
                                const uint64_t* latest, const uint64_t* resident,
                                uint64_t count);
 
+/* Replaces the whole SimState (the parity hook SURVEY §8(b) sketches as
+ * edx_import_state): the clock (sim.hpp:267), every global_ entry
+ * (sim.hpp:266; g_* arrays, ids unique) and every worker's cache
+ * (cache.hpp:233-239): worker j's entries are e_*[entry_off[j] ..
+ * entry_off[j+1]) (CacheEntry fields, cache.hpp:36-42), plus current_mark_ and
+ * at_current_mark_ per worker.  e_version may be NULL; when given it must equal
+ * bit j of the entry's `latest` mask (EDX_LOGIC_ERROR "version flag diverged
+ * from global state").  The result is checked with
+ * edx_engine_validate_consistency (its errors are returned). */
+int edx_engine_import_state(edx_engine* e, uint64_t clock, uint64_t g_count, const uint32_t* g_ids,
+                            const uint64_t* g_owners, const uint64_t* g_latest,
+                            const uint64_t* g_resident, const uint64_t* entry_off,
+                            const uint32_t* e_ids, const uint8_t* e_version, const uint32_t* e_mark,
+                            const uint32_t* e_freq, const uint64_t* e_last,
+                            const uint32_t* current_mark, const uint64_t* at_current_mark);
+
 /* Per-phase device times of the calls since the last reset, measured with CUDA
  * events on the engine stream when profiling is on.  Phases (ms):
  * [0] build  [1] gap+sort  [2] exact solve  [3] greedy  [4] step  [5] whole dispatch
@@ -203,6 +228,11 @@ int edx_engine_import_snapshot(edx_engine* e, const uint32_t* ids, const uint64_
 #define EDX_NUM_PHASES 6
 int edx_engine_set_profiling(edx_engine* e, int on);
 int edx_engine_phase_times(edx_engine* e, double* ms, uint64_t* counts, int reset);
+
+/* Names of the kernels the engine's last cost build, exact solve and greedy
+ * launched ("" = none; static strings), for measurement labels. */
+int edx_engine_last_kernels(edx_engine* e, const char** build, const char** solver,
+                            const char** greedy);
 
 /* Counters of the last exact solve (engine e, or the stateless context when
  * e is NULL): [0] Dijkstra steps [1] cycles in steps [2] cycles applying
@@ -306,6 +336,11 @@ int edx_zipf_create(uint64_t total_embeddings, uint64_t sample_len, double zipf_
 /* Fills samples_per_iteration*sample_len ids; returns 1, or 0 at the end. */
 int edx_zipf_next(edx_zipf* z, uint32_t* ids);
 void edx_zipf_reset(edx_zipf* z);
+/* ZipfSampler (workload.hpp:54-79): ids in [0, population) with P(id) ∝
+ * (id+1)^-s, drawn from std::mt19937_64(seed) by inverse CDF; free with
+ * edx_zipf_destroy.  edx_zipf_draw returns the next `count` draws. */
+int edx_zipf_sampler_create(uint64_t population, double zipf_s, uint64_t seed, edx_zipf** out);
+int edx_zipf_draw(edx_zipf* z, uint64_t count, uint32_t* out);
 void edx_zipf_destroy(edx_zipf* z);
 
 /* ------------------------------------------------------------ trace input

@@ -1,14 +1,14 @@
 // Drop-in for the reference's assign.hpp hot path: the exact solver, the
 // capacity-bounded greedy, the gap order and the EcoMix hybrid, all executed
 // by libedx kernels (hungarian.cu, dispatch.cu), and the hit-greedy baseline
-// (hitgreedy.cu).  The random / round-robin baselines are not part of the
-// device path.
+// (hitgreedy.cu).  The random / round-robin controls are data-free host code.
 #pragma once
 
 #include <algorithm>
 #include <cmath>
 #include <numeric>
 #include <ostream>
+#include <random>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -129,9 +129,9 @@ inline DispatchDecision baseline_hitgreedy(const std::vector<EmbeddingSample>& s
     throw std::invalid_argument("sample count must be m*n");
   std::vector<int32_t> dec(samples.size());
   const edxc::Csr csr(samples);
-  if (snap.engine && edx_engine_clock(snap.engine) == snap.engine_clock) {
-    edxc::check(edx_engine_load_batch(snap.engine, csr.ids.data(), csr.offsets.data(), samples.size(), 0));
-    edxc::check(edx_engine_dispatch_hitgreedy(snap.engine, dec.data()));
+  if (edx_engine* e = snap.device_view()) {
+    edxc::check(edx_engine_load_batch(e, csr.ids.data(), csr.offsets.data(), samples.size(), 0));
+    edxc::check(edx_engine_dispatch_hitgreedy(e, dec.data()));
   } else {
     const edxc::SnapArrays a(snap);
     const edx_cluster_config c = edxc::to_c(cfg);
@@ -140,6 +140,41 @@ inline DispatchDecision baseline_hitgreedy(const std::vector<EmbeddingSample>& s
   }
   DispatchDecision d;
   d.worker_of_sample.assign(dec.begin(), dec.end());
+  return d;
+}
+
+// assign.hpp:300-326: the random control -- a uniformly random balanced
+// assignment.  Data-free host code (no state, no matrix): sample perm[p]
+// goes to worker p / m, perm from an explicit Fisher-Yates pass over
+// std::mt19937_64(seed) (draw j = rng() % (i + 1) for i = R-1 .. 1), so the
+// decisions replay bit-identically from the seed.
+inline DispatchDecision baseline_random(std::size_t sample_count, const ClusterConfig& cfg,
+                                        std::uint64_t seed) {
+  if (sample_count != cfg.samples_per_iteration())
+    throw std::invalid_argument("sample count must be m*n");
+  std::vector<std::size_t> perm(sample_count);
+  std::iota(perm.begin(), perm.end(), std::size_t{0});
+  std::mt19937_64 rng(seed);
+  for (std::size_t i = sample_count; i-- > 1;)
+    std::swap(perm[i], perm[static_cast<std::size_t>(rng() % (i + 1))]);
+  DispatchDecision d;
+  d.worker_of_sample.assign(sample_count, -1);
+  const std::size_t m = static_cast<std::size_t>(cfg.m);
+  for (std::size_t p = 0; p < sample_count; ++p)
+    d.worker_of_sample[perm[p]] = static_cast<WorkerId>(p / m);
+  d.validate(cfg);
+  return d;
+}
+
+// assign.hpp:329-341: the round-robin control, sample i to worker i mod n.
+inline DispatchDecision baseline_roundrobin(std::size_t sample_count, const ClusterConfig& cfg) {
+  if (sample_count != cfg.samples_per_iteration())
+    throw std::invalid_argument("sample count must be m*n");
+  DispatchDecision d;
+  d.worker_of_sample.resize(sample_count);
+  for (std::size_t i = 0; i < sample_count; ++i)
+    d.worker_of_sample[i] = static_cast<WorkerId>(i % static_cast<std::size_t>(cfg.n));
+  d.validate(cfg);
   return d;
 }
 

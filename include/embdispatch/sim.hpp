@@ -38,12 +38,15 @@ struct IterationReport {
 };
 
 // Device sizing of a SimState (no reference counterpart: the reference grows
-// hash maps on demand).  Defaults can be overridden with EDX_ID_SPACE /
-// EDX_MAX_BATCH_IDS.
+// hash maps on demand).  id_space > 0 selects the dense fast path (every id
+// < id_space, tables indexed by id); 0 (the default, or EDX_ID_SPACE) accepts
+// any uint32 id through the device's open-addressing id table, which grows as
+// new ids arrive.  max_batch_ids bounds one iteration's id stream (0 = env
+// EDX_MAX_BATCH_IDS or 2^20; run() sizes it from the stream).
 struct EngineOptions {
   int device = 0;
-  std::uint64_t id_space = 0;       // ids must be < id_space; 0 = env or 2^20
-  std::uint64_t max_batch_ids = 0;  // ids per iteration; 0 = env or 2^20
+  std::uint64_t id_space = 0;
+  std::uint64_t max_batch_ids = 0;
 };
 
 namespace edxc {
@@ -128,32 +131,12 @@ class SimState {
     return views_[static_cast<std::size_t>(j)];
   }
 
-  // sim.hpp:71-82: the full state as a host Snapshot, tagged with the engine
-  // so that build_matrix can use the live device state instead.
-  Snapshot snapshot() const {
-    Snapshot s = device_snapshot();
-    uint64_t count = 0;
-    edxc::check(edx_engine_export_global(e_, nullptr, nullptr, nullptr, nullptr, 0, &count));
-    std::vector<uint32_t> ids(count);
-    std::vector<uint64_t> ow(count), la(count), re(count);
-    edxc::check(edx_engine_export_global(e_, ids.data(), ow.data(), la.data(), re.data(), count,
-                                         &count));
-    s.resident_ids.resize(static_cast<std::size_t>(cfg_.n));
-    for (uint64_t t = 0; t < count; ++t) {
-      s.states[ids[t]] = EmbeddingState{ow[t], la[t], re[t]};
-      for (WorkerMask r = re[t]; r; r &= r - 1)
-        s.resident_ids[static_cast<std::size_t>(__builtin_ctzll(r))].push_back(ids[t]);
-    }
-    return s;
-  }
-
-  // Zero-copy: valid for build_matrix until the next step().
-  Snapshot device_snapshot() const {
-    Snapshot s;
-    s.engine = e_;
-    s.engine_clock = clock();
-    return s;
-  }
+  // sim.hpp:71-82.  The reference copies the whole global map; here the
+  // Snapshot is a view of the device state (nothing is copied unless the
+  // caller reads `states` / `resident_ids`), and build_matrix /
+  // baseline_hitgreedy read the device tables directly while it is current.
+  Snapshot snapshot() const { return Snapshot::of_engine(e_, cfg_.n); }
+  Snapshot device_snapshot() const { return snapshot(); }
 
   // sim.hpp:87-218.
   IterationReport step(const std::vector<EmbeddingSample>& samples, const DispatchDecision& decision) {
@@ -182,24 +165,35 @@ class SimState {
   mutable std::vector<WorkerCache> views_;
 };
 
-// sim.hpp:271-318 for the mechanisms on the device path: EcoMix and the
-// hit-greedy baseline (random / round-robin are outside it).
+// sim.hpp:271-318.  EcoMix and the hit-greedy baseline run on the device;
+// random and round-robin are the data-free controls (host, assign.hpp).
 struct Mechanism {
-  enum class Kind { kEcoMix, kHitGreedy };
+  enum class Kind { kEcoMix, kRandom, kRoundRobin, kHitGreedy };
   Kind kind = Kind::kEcoMix;
   double alpha = 1.0;
+
   std::string name() const {
-    return kind == Kind::kHitGreedy ? std::string("hitgreedy") : "ecomix:" + detail::format_double(alpha);
+    switch (kind) {
+      case Kind::kRandom: return "random";
+      case Kind::kRoundRobin: return "roundrobin";
+      case Kind::kHitGreedy: return "hitgreedy";
+      case Kind::kEcoMix: break;
+    }
+    return "ecomix:" + detail::format_double(alpha);
   }
-  bool needs_snapshot() const { return true; }
+  bool needs_snapshot() const { return kind == Kind::kEcoMix || kind == Kind::kHitGreedy; }
   bool needs_matrix() const { return kind == Kind::kEcoMix; }
+
+  // "ecomix:<alpha>", "ecomix", "random", "roundrobin", "hitgreedy"
   static Mechanism parse(const std::string& text) {
     Mechanism mech;
-    if (text == "hitgreedy") {
+    if (text == "random") {
+      mech.kind = Kind::kRandom;
+    } else if (text == "roundrobin") {
+      mech.kind = Kind::kRoundRobin;
+    } else if (text == "hitgreedy") {
       mech.kind = Kind::kHitGreedy;
-      return mech;
-    }
-    if (text == "ecomix" || text.rfind("ecomix:", 0) == 0) {
+    } else if (text == "ecomix" || text.rfind("ecomix:", 0) == 0) {
       if (text.size() > 7) {
         try {
           mech.alpha = std::stod(text.substr(7));
@@ -208,12 +202,46 @@ struct Mechanism {
         }
       }
       if (mech.alpha < 0.0 || mech.alpha > 1.0) throw std::invalid_argument("alpha must lie in [0, 1]");
-      return mech;
+    } else {
+      throw std::invalid_argument("unknown mechanism '" + text + "'");
     }
-    throw std::invalid_argument("unknown mechanism '" + text +
-                                "' (the device path runs ecomix and hitgreedy)");
+    return mech;
   }
 };
+
+namespace detail {
+// sim.hpp:360-366: the random baseline's per-iteration seed (one splitmix64
+// step of seed ^ iteration * golden ratio).
+inline std::uint64_t mix_seed(std::uint64_t seed, std::uint64_t iteration) {
+  std::uint64_t z = (seed ^ (iteration * 0x9e3779b97f4a7c15ull)) + 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+}  // namespace detail
+
+// sim.hpp:373-395: one decision of `mech`.  The matrix is read only by
+// EcoMix, the snapshot only by the snapshot-aware mechanisms.
+inline DispatchDecision dispatch_with(const Mechanism& mech,
+                                      const std::vector<EmbeddingSample>& samples,
+                                      const Snapshot& snap, const CostMatrix& matrix,
+                                      const ClusterConfig& cfg, std::uint64_t iteration,
+                                      std::uint64_t random_seed) {
+  switch (mech.kind) {
+    case Mechanism::Kind::kEcoMix: {
+      ClusterConfig tuned = cfg;
+      tuned.alpha = mech.alpha;
+      return ecomix(matrix, tuned);
+    }
+    case Mechanism::Kind::kRandom:
+      return baseline_random(samples.size(), cfg, detail::mix_seed(random_seed, iteration));
+    case Mechanism::Kind::kRoundRobin:
+      return baseline_roundrobin(samples.size(), cfg);
+    case Mechanism::Kind::kHitGreedy:
+      return baseline_hitgreedy(samples, snap, cfg);
+  }
+  throw std::logic_error("unreachable");
+}
 
 struct RunOptions {
   std::size_t warmup = 10;
@@ -243,8 +271,9 @@ struct RunResult {
   RunSummary summary;
 };
 
-// sim.hpp:400-478 on the engine: build (matrix_s), dispatch (decision_s),
-// device step, decision_cost; summaries accumulated in the reference's order.
+// sim.hpp:400-478 on the engine: build (matrix_s, synchronised), dispatch
+// (decision_s), device step, decision_cost; summaries accumulated in the
+// reference's order.
 inline RunResult run(SampleStream& stream, const Mechanism& mech, const ClusterConfig& cfg,
                      const RunOptions& opt, EngineOptions eopt = {}) {
   using clk = std::chrono::steady_clock;
@@ -256,9 +285,11 @@ inline RunResult run(SampleStream& stream, const Mechanism& mech, const ClusterC
   s.update_push_w.assign(static_cast<std::size_t>(cfg.n), 0);
   s.evict_push_w.assign(static_cast<std::size_t>(cfg.n), 0);
   s.ops_w.assign(static_cast<std::size_t>(cfg.n), 0);
+  if (!eopt.max_batch_ids) eopt.max_batch_ids = cfg.samples_per_iteration() * stream.max_sample_len();
+  if (!eopt.id_space)  // a Zipf stream's ids are dense: the direct-indexed fast path
+    if (const auto* z = dynamic_cast<const ZipfStream*>(&stream)) eopt.id_space = z->spec().total_embeddings;
   ClusterConfig tuned = cfg;
-  tuned.alpha = mech.alpha;
-  if (!eopt.max_batch_ids) eopt.max_batch_ids = tuned.samples_per_iteration() * stream.max_sample_len();
+  if (mech.kind == Mechanism::Kind::kEcoMix) tuned.alpha = mech.alpha;
   SimState state(tuned, eopt);
   edx_engine* e = state.engine();
   std::vector<EmbeddingSample> samples;
@@ -269,22 +300,44 @@ inline RunResult run(SampleStream& stream, const Mechanism& mech, const ClusterC
     const edxc::Csr csr(samples);
     edxc::check(edx_engine_load_batch(e, csr.ids.data(), csr.offsets.data(), samples.size(), 0));
     const bool hybrid = mech.needs_matrix();
-    const auto t0 = clk::now();
-    if (hybrid) edxc::check(edx_engine_build(e, nullptr));
-    const auto t1 = clk::now();
-    double expected = 0.0;
+    // matrix_s: the build alone, synchronised (sim.hpp:423-425)
+    double matrix_s = 0.0;
+    if (hybrid) {
+      const auto t0 = clk::now();
+      edxc::check(edx_engine_build(e, nullptr));
+      edxc::check(edx_engine_synchronize(e));
+      matrix_s = std::chrono::duration<double>(clk::now() - t0).count();
+    }
+    // decision_s: the dispatcher alone, until its decision is on the host
+    // (sim.hpp:428-432); decision_cost runs on a side stream outside it
     std::vector<int32_t> dec(samples.size());
-    if (hybrid) edxc::check(edx_engine_dispatch(e, mech.alpha, dec.data(), &expected));
-    else edxc::check(edx_engine_dispatch_hitgreedy(e, dec.data()));
-    const auto t2 = clk::now();
+    const auto t1 = clk::now();
+    bool device_decision = true;
+    switch (mech.kind) {
+      case Mechanism::Kind::kEcoMix:
+        edxc::check(edx_engine_dispatch(e, mech.alpha, dec.data(), nullptr));
+        break;
+      case Mechanism::Kind::kHitGreedy:
+        edxc::check(edx_engine_dispatch_hitgreedy(e, dec.data()));
+        break;
+      default: {
+        const DispatchDecision d = dispatch_with(mech, samples, Snapshot{}, CostMatrix{}, cfg,
+                                                 iteration, opt.random_seed);
+        dec.assign(d.worker_of_sample.begin(), d.worker_of_sample.end());
+        device_decision = false;
+      }
+    }
+    const double decision_s = std::chrono::duration<double>(clk::now() - t1).count();
     edxc::Report raw(cfg.n);
-    edxc::check(edx_engine_step(e, nullptr, &raw.c));
+    edxc::check(edx_engine_step(e, device_decision ? nullptr : dec.data(), &raw.c));
     IterationReport rep = raw.to_report();
     rep.mechanism = mech.name();
-    rep.matrix_s = hybrid ? std::chrono::duration<double>(t1 - t0).count() : 0.0;
-    rep.decision_s = std::chrono::duration<double>(t2 - t1).count();
-    rep.expected_cost_s = expected;
-    rep.has_expected = hybrid;
+    rep.matrix_s = matrix_s;
+    rep.decision_s = decision_s;
+    if (hybrid) {  // decision_cost (sim.hpp:437-440), computed beside the step
+      edxc::check(edx_engine_expected_cost(e, &rep.expected_cost_s));
+      rep.has_expected = true;
+    }
     if (opt.validate_state) state.validate_consistency();
     if (iteration >= opt.warmup) {
       ++s.measured_iterations;
@@ -294,8 +347,10 @@ inline RunResult run(SampleStream& stream, const Mechanism& mech, const ClusterC
       s.hits += rep.hits;
       s.lookups += rep.lookups;
       s.cost_s += rep.cost_s;
-      s.expected_cost_s += rep.expected_cost_s;
-      s.has_expected = hybrid;
+      if (rep.has_expected) {
+        s.expected_cost_s += rep.expected_cost_s;
+        s.has_expected = true;
+      }
       s.matrix_s_total += rep.matrix_s;
       for (std::size_t j = 0; j < static_cast<std::size_t>(cfg.n); ++j) {
         s.miss_pull_w[j] += rep.miss_pull_w[j];

@@ -26,6 +26,42 @@ struct WorkloadSpec {
   std::uint64_t seed = 42;
 };
 
+// workload.hpp:44-50 (same messages).
+inline void validate(const WorkloadSpec& spec) {
+  if (spec.sample_len < 1) throw std::invalid_argument("sample_len must be >= 1");
+  if (!(spec.zipf_s > 0.0)) throw std::invalid_argument("zipf_s must be positive");
+  if (spec.total_embeddings < spec.sample_len)
+    throw std::invalid_argument("sample_len exceeds the embedding population");
+}
+
+// workload.hpp:54-79: ids in [0, n) with P(id) proportional to (id+1)^-s,
+// inverse-CDF over std::mt19937_64(seed) -- the same draws, produced by
+// libedx's guide-table sampler (workload.cpp) a block at a time.
+class ZipfSampler {
+ public:
+  ZipfSampler(std::size_t n, double s, std::uint64_t seed) {
+    edx_zipf* z = nullptr;
+    edxc::check(edx_zipf_sampler_create(n, s, seed, &z));
+    z_.reset(z);
+  }
+  EmbeddingId draw() {
+    if (pos_ == buf_.size()) {
+      buf_.resize(4096);
+      edxc::check(edx_zipf_draw(z_.get(), buf_.size(), buf_.data()));
+      pos_ = 0;
+    }
+    return buf_[pos_++];
+  }
+
+ private:
+  struct Del {
+    void operator()(edx_zipf* z) const { edx_zipf_destroy(z); }
+  };
+  std::unique_ptr<edx_zipf, Del> z_;
+  std::vector<std::uint32_t> buf_;
+  std::size_t pos_ = 0;
+};
+
 class SampleStream {
  public:
   virtual ~SampleStream() = default;
@@ -54,6 +90,7 @@ class ZipfStream final : public SampleStream {
   }
   void reset() override { edx_zipf_reset(z_.get()); }
   std::size_t max_sample_len() const override { return spec_.sample_len; }
+  const WorkloadSpec& spec() const { return spec_; }
 
  private:
   struct Del {

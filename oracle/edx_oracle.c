@@ -1259,6 +1259,44 @@ void orc_sim_cache_marks(orc_sim* s, int32_t worker, uint32_t* current_mark,
   *at_current_mark = s->caches[worker].at_current;
 }
 
+/* Parity import: replaces the clock, the global table and every cache. */
+int orc_sim_import_state(orc_sim* s, uint64_t clock, uint64_t g_count, const uint32_t* g_ids,
+                         const uint64_t* g_owners, const uint64_t* g_latest,
+                         const uint64_t* g_resident, const uint64_t* entry_off,
+                         const uint32_t* e_ids, const uint8_t* e_version, const uint32_t* e_mark,
+                         const uint32_t* e_freq, const uint64_t* e_last,
+                         const uint32_t* current_mark, const uint64_t* at_current_mark) {
+  for (int j = 0; j < s->cfg.n; ++j)
+    if (entry_off[j + 1] - entry_off[j] > s->cfg.cache_capacity)
+      return fail(ORC_INVALID_ARGUMENT, "imported cache exceeds its capacity");
+  gstate_free(&s->g);
+  gstate_init(&s->g, g_count + 16);
+  for (uint64_t t = 0; t < g_count; ++t) {
+    const int64_t x = gstate_ref(&s->g, g_ids[t]);
+    s->g.owners[x] = g_owners[t];
+    s->g.latest[x] = g_latest[t];
+    s->g.resident[x] = g_resident[t];
+  }
+  for (int j = 0; j < s->cfg.n; ++j) {
+    wcache* c = &s->caches[j];
+    wcache_free(c);
+    wcache_init(c, s->cfg.cache_capacity);
+    for (uint64_t t = entry_off[j]; t < entry_off[j + 1]; ++t) {
+      const uint64_t k = c->size++;
+      c->id[k] = e_ids[t];
+      c->version[k] = e_version[t] ? 1 : 0;
+      c->mark[k] = e_mark[t];
+      c->freq[k] = e_freq[t];
+      c->last[k] = e_last[t];
+      idmap_put(&c->map, e_ids[t], (int32_t)k);
+    }
+    c->current_mark = current_mark[j];
+    c->at_current = at_current_mark[j];
+  }
+  s->clock = clock;
+  return ORC_OK;
+}
+
 /* One iteration of run() — sim.hpp:421-441 — for the "port" CPU baseline
  * when oracle/_ref is absent.  The snapshot is free here (the build reads the
  * live state), so times_s[0] is 0. */

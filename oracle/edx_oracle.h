@@ -127,6 +127,16 @@ void orc_sim_export_cache(orc_sim* s, int32_t worker, uint32_t* ids, uint8_t* ve
                           uint32_t* mark, uint32_t* freq, uint64_t* last_access);
 void orc_sim_cache_marks(orc_sim* s, int32_t worker, uint32_t* current_mark,
                          uint64_t* at_current_mark);
+/* Replaces the whole simulator state (parity hook, the counterpart of
+ * edx_engine_import_state): the clock, every global_ entry (sim.hpp:266) and
+ * every worker's cache entries (cache.hpp:233-239), current_mark_ and
+ * at_current_mark_.  Worker j's entries are e_*[entry_off[j] .. entry_off[j+1]). */
+int orc_sim_import_state(orc_sim* s, uint64_t clock, uint64_t g_count, const uint32_t* g_ids,
+                         const uint64_t* g_owners, const uint64_t* g_latest,
+                         const uint64_t* g_resident, const uint64_t* entry_off,
+                         const uint32_t* e_ids, const uint8_t* e_version, const uint32_t* e_mark,
+                         const uint32_t* e_freq, const uint64_t* e_last,
+                         const uint32_t* current_mark, const uint64_t* at_current_mark);
 
 /* One full reference iteration timed like run() (sim.hpp:421-441):
  * snapshot -> build_matrix -> ecomix -> step, plus decision_cost.  times_s

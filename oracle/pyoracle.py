@@ -139,6 +139,9 @@ class Oracle:
         L.orc_sim_export_cache.argtypes = [vp, i32, P(C.c_uint32), P(C.c_uint8), P(C.c_uint32),
                                            P(C.c_uint32), P(u64)]
         L.orc_sim_cache_marks.argtypes = [vp, i32, P(C.c_uint32), P(u64)]
+        L.orc_sim_import_state.argtypes = [vp, u64, u64, P(C.c_uint32), P(u64), P(u64), P(u64),
+                                           P(u64), P(C.c_uint32), P(C.c_uint8), P(C.c_uint32),
+                                           P(C.c_uint32), P(u64), P(C.c_uint32), P(u64)]
         L.orc_ref_iteration.argtypes = [vp, P(C.c_uint32), P(u64), u64, C.c_int, P(i32), P(dbl),
                                         P(ReportC), P(dbl)]
         L.orc_last_hungarian_steps.restype = u64
@@ -305,6 +308,25 @@ class Oracle:
         return Cache(self, capacity, policy)
 
 
+def state_arrays(state, n):
+    """canonical_state()-format state -> the flat arrays of orc_sim_import_state
+    / edx_engine_import_state."""
+    glob, caches = state
+    glob = np.asarray(glob, np.uint64).reshape(-1, 4)
+    assert len(caches) == n
+    ents = [np.asarray(c[0], np.uint64).reshape(-1, 5) for c in caches]
+    off = np.zeros(n + 1, np.uint64)
+    off[1:] = np.cumsum([len(e) for e in ents])
+    cat = np.concatenate(ents) if ents else np.zeros((0, 5), np.uint64)
+    c = np.ascontiguousarray
+    return dict(g_ids=c(glob[:, 0].astype(np.uint32)), g_owners=c(glob[:, 1]),
+                g_latest=c(glob[:, 2]), g_resident=c(glob[:, 3]), off=off,
+                e_ids=c(cat[:, 0].astype(np.uint32)), e_ver=c(cat[:, 1].astype(np.uint8)),
+                e_mark=c(cat[:, 2].astype(np.uint32)), e_freq=c(cat[:, 3].astype(np.uint32)),
+                e_last=c(cat[:, 4]), cur=np.array([x[1] for x in caches], np.uint32),
+                at=np.array([x[2] for x in caches], np.uint64))
+
+
 class Cache:
     """Mirror of a standalone embdispatch::WorkerCache (cache.hpp:73-240)."""
 
@@ -424,6 +446,20 @@ class Sim:
 
     def clock(self):
         return int(self.o.lib.orc_sim_clock(self.h))
+
+    def import_state(self, state, clock):
+        """Replace the whole state with `state` in canonical_state()'s format
+        (global rows [id, owners, latest, resident]; per worker (entries
+        [id, version, mark, freq, last_access], current_mark, at_current_mark))."""
+        args = state_arrays(state, self.cfg.n)
+        self.o._check(self.o.lib.orc_sim_import_state(
+            self.h, int(clock), len(args["g_ids"]), _p(args["g_ids"], C.c_uint32),
+            _p(args["g_owners"], C.c_uint64), _p(args["g_latest"], C.c_uint64),
+            _p(args["g_resident"], C.c_uint64), _p(args["off"], C.c_uint64),
+            _p(args["e_ids"], C.c_uint32), _p(args["e_ver"], C.c_uint8),
+            _p(args["e_mark"], C.c_uint32), _p(args["e_freq"], C.c_uint32),
+            _p(args["e_last"], C.c_uint64), _p(args["cur"], C.c_uint32),
+            _p(args["at"], C.c_uint64)))
 
     def canonical_state(self):
         """Non-zero global masks and per-worker entries, both sorted by id."""

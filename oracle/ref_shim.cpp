@@ -22,6 +22,7 @@
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <set>
 #include <unordered_map>
 #include <vector>
 
@@ -116,6 +117,36 @@ struct orc_sim {
   SimState state;
   explicit orc_sim(const ClusterConfig& c) : cfg(c), state(c) {}
 };
+
+namespace {
+
+// Parity import (orc_sim_import_state): the reference keeps SimState's and
+// WorkerCache's state private and has no setter.  An explicit template
+// instantiation may name private members ([temp.spec.general]), so a friend
+// defined inside one hands out the member pointer -- the reference headers
+// stay unmodified and are still compiled in place.
+template <class Tag, typename Tag::type M>
+struct Rob {
+  friend typename Tag::type get(Tag) { return M; }
+};
+#define EDX_ROB(NAME, CLASS, TYPE, MEMBER)                   \
+  struct NAME {                                              \
+    using type = TYPE CLASS::*;                              \
+    friend type get(NAME);                                   \
+  };                                                         \
+  template struct Rob<NAME, &CLASS::MEMBER>;
+using GlobalMap = std::unordered_map<EmbeddingId, EmbeddingState>;
+using EntryMap = std::unordered_map<EmbeddingId, CacheEntry>;
+EDX_ROB(RobCaches, SimState, std::vector<WorkerCache>, caches_)
+EDX_ROB(RobGlobal, SimState, GlobalMap, global_)
+EDX_ROB(RobClock, SimState, std::uint64_t, clock_)
+EDX_ROB(RobEntries, WorkerCache, EntryMap, entries_)
+EDX_ROB(RobOrder, WorkerCache, std::set<VictimKey>, order_)
+EDX_ROB(RobMark, WorkerCache, std::uint32_t, current_mark_)
+EDX_ROB(RobAtMark, WorkerCache, std::size_t, at_current_mark_)
+#undef EDX_ROB
+
+}  // namespace
 
 extern "C" {
 
@@ -352,6 +383,41 @@ void orc_sim_export_cache(orc_sim* s, int32_t worker, uint32_t* ids, uint8_t* ve
     last_access[t] = e.last_access;
     ++t;
   }
+}
+
+int orc_sim_import_state(orc_sim* s, uint64_t clock, uint64_t g_count, const uint32_t* g_ids,
+                         const uint64_t* g_owners, const uint64_t* g_latest,
+                         const uint64_t* g_resident, const uint64_t* entry_off,
+                         const uint32_t* e_ids, const uint8_t* e_version, const uint32_t* e_mark,
+                         const uint32_t* e_freq, const uint64_t* e_last,
+                         const uint32_t* current_mark, const uint64_t* at_current_mark) {
+  return guarded([&] {
+    SimState& st = s->state;
+    st.*get(RobClock{}) = clock;
+    GlobalMap& g = st.*get(RobGlobal{});
+    g.clear();
+    g.reserve(g_count);
+    for (uint64_t t = 0; t < g_count; ++t)
+      g[g_ids[t]] = EmbeddingState{g_owners[t], g_latest[t], g_resident[t]};
+    std::vector<WorkerCache>& caches = st.*get(RobCaches{});
+    for (int j = 0; j < s->cfg.n; ++j) {
+      WorkerCache& c = caches[j];
+      EntryMap& em = c.*get(RobEntries{});
+      std::set<VictimKey>& order = c.*get(RobOrder{});
+      em.clear();
+      order.clear();
+      const uint64_t a = entry_off[j], b = entry_off[j + 1];
+      if (b - a > c.capacity()) throw std::invalid_argument("imported cache exceeds its capacity");
+      em.reserve(b - a);
+      for (uint64_t t = a; t < b; ++t) {
+        const CacheEntry e{e_ids[t], e_version[t] != 0, e_mark[t], e_freq[t], e_last[t]};
+        em.emplace(e.id, e);
+        order.insert(victim_key(e));
+      }
+      c.*get(RobMark{}) = current_mark[j];
+      c.*get(RobAtMark{}) = static_cast<std::size_t>(at_current_mark[j]);
+    }
+  });
 }
 
 void orc_sim_cache_marks(orc_sim* s, int32_t worker, uint32_t* current_mark,

@@ -633,6 +633,34 @@ class SimState:
         check(lib().edx_engine_import_snapshot(self._h, _ptr(keys, C.c_uint32), _ptr(ow, C.c_uint64),
                                                _ptr(la, C.c_uint64), _ptr(re, C.c_uint64), len(keys)))
 
+    def import_state(self, state, clock):
+        """Replace the whole state (edx_engine_import_state) with `state` in
+        canonical_state()'s format: global rows [id, owners, latest, resident]
+        and per worker (entries [id, version, mark, freq, last_access],
+        current_mark, at_current_mark).  The result is validated."""
+        glob, caches = state
+        glob = np.asarray(glob, np.uint64).reshape(-1, 4)
+        n = self.cfg.n
+        if len(caches) != n:
+            raise InvalidArgument("one cache per worker")
+        ents = [np.asarray(c[0], np.uint64).reshape(-1, 5) for c in caches]
+        off = np.zeros(n + 1, np.uint64)
+        off[1:] = np.cumsum([len(x) for x in ents])
+        cat = np.concatenate(ents) if ents else np.zeros((0, 5), np.uint64)
+        cc = np.ascontiguousarray
+        g_ids, e_ids = cc(glob[:, 0].astype(np.uint32)), cc(cat[:, 0].astype(np.uint32))
+        g_ow, g_la, g_re = cc(glob[:, 1]), cc(glob[:, 2]), cc(glob[:, 3])
+        e_ver, e_mk = cc(cat[:, 1].astype(np.uint8)), cc(cat[:, 2].astype(np.uint32))
+        e_fq, e_la = cc(cat[:, 3].astype(np.uint32)), cc(cat[:, 4])
+        cur = np.array([c[1] for c in caches], np.uint32)
+        at = np.array([c[2] for c in caches], np.uint64)
+        check(lib().edx_engine_import_state(
+            self._h, int(clock), len(g_ids), _ptr(g_ids, C.c_uint32), _ptr(g_ow, C.c_uint64),
+            _ptr(g_la, C.c_uint64), _ptr(g_re, C.c_uint64), _ptr(off, C.c_uint64),
+            _ptr(e_ids, C.c_uint32), _ptr(e_ver, C.c_uint8), _ptr(e_mk, C.c_uint32),
+            _ptr(e_fq, C.c_uint32), _ptr(e_la, C.c_uint64), _ptr(cur, C.c_uint32),
+            _ptr(at, C.c_uint64)))
+
     def cache_entries(self, worker):
         """WorkerCache::entries() of one worker as an (k, 5) uint64 array of
         (id, version, mark, freq, last_access) rows, ascending id."""
@@ -690,6 +718,13 @@ class SimState:
         return glob, caches
 
     # -- profiling
+    def last_kernels(self) -> dict:
+        """Kernels the last cost build / exact solve / greedy launched."""
+        b, s, g = C.c_char_p(), C.c_char_p(), C.c_char_p()
+        check(lib().edx_engine_last_kernels(self._h, C.byref(b), C.byref(s), C.byref(g)))
+        return {"build": (b.value or b"").decode(), "solver": (s.value or b"").decode(),
+                "greedy": (g.value or b"").decode()}
+
     def set_profiling(self, on: bool):
         check(lib().edx_engine_set_profiling(self._h, int(bool(on))))
 

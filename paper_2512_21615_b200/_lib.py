@@ -91,11 +91,17 @@ def _sigs():
         ("edx_engine_state_of", cint, [vp, C.c_uint32, u64p, u64p, u64p]),
         ("edx_engine_validate_consistency", cint, [vp]),
         ("edx_engine_clock", u64, [vp]),
+        ("edx_engine_state_version", u64, [vp]),
+        ("edx_engine_synchronize", cint, [vp]),
+        ("edx_engine_expected_cost", cint, [vp, dblp]),
         ("edx_engine_export_global", cint, [vp, u32p, u64p, u64p, u64p, u64, u64p]),
         ("edx_engine_cache_size", cint, [vp, i32, u64p]),
         ("edx_engine_export_cache", cint, [vp, i32, u32p, P(C.c_uint8), u32p, u32p, u64p]),
         ("edx_engine_cache_marks", cint, [vp, i32, u32p, u64p]),
         ("edx_engine_import_snapshot", cint, [vp, u32p, u64p, u64p, u64p, u64]),
+        ("edx_engine_import_state", cint, [vp, u64, u64, u32p, u64p, u64p, u64p, u64p, u32p,
+                                           P(C.c_uint8), u32p, u32p, u64p, u32p, u64p]),
+        ("edx_engine_last_kernels", cint, [vp, P(C.c_char_p), P(C.c_char_p), P(C.c_char_p)]),
         ("edx_engine_set_profiling", cint, [vp, cint]),
         ("edx_engine_phase_times", cint, [vp, dblp, u64p, cint]),
         ("edx_solver_stats", cint, [vp, u64p]),
@@ -125,6 +131,8 @@ def _sigs():
         ("edx_zipf_create", cint, [u64, u64, dbl, u64, u64, u64, P(vp)]),
         ("edx_zipf_next", cint, [vp, u32p]),
         ("edx_zipf_reset", None, [vp]),
+        ("edx_zipf_sampler_create", cint, [u64, dbl, u64, P(vp)]),
+        ("edx_zipf_draw", cint, [vp, u64, u32p]),
         ("edx_zipf_destroy", None, [vp]),
         ("edx_trace_load", cint, [C.c_char_p, u64, u64p, P(C.c_char_p), u64, u64, u64, P(vp)]),
         ("edx_trace_info", None, [vp, u64p, u64p, u64p, u64p]),

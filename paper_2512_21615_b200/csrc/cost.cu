@@ -573,12 +573,12 @@ void launch_cost_build(const uint32_t* ids, const uint64_t* offsets, uint64_t ro
                                                gap_keys, row_index, flags);
     };
     switch (np) {
-      case 2: go(k_cost_build_warp<2>); break;
-      case 4: go(k_cost_build_warp<4>); break;
-      case 8: go(k_cost_build_warp<8>); break;
-      case 16: go(k_cost_build_wide<16>); break;
-      case 32: go(k_cost_build_wide<32>); break;
-      default: go(k_cost_build_wide64<64>); break;
+      case 2: go(k_cost_build_warp<2>); g_kernel_name[kKBuild] = "k_cost_build_warp<2>"; break;
+      case 4: go(k_cost_build_warp<4>); g_kernel_name[kKBuild] = "k_cost_build_warp<4>"; break;
+      case 8: go(k_cost_build_warp<8>); g_kernel_name[kKBuild] = "k_cost_build_warp<8>"; break;
+      case 16: go(k_cost_build_wide<16>); g_kernel_name[kKBuild] = "k_cost_build_wide<16>"; break;
+      case 32: go(k_cost_build_wide<32>); g_kernel_name[kKBuild] = "k_cost_build_wide<32>"; break;
+      default: go(k_cost_build_wide64<64>); g_kernel_name[kKBuild] = "k_cost_build_wide64<64>"; break;
     }
     EDX_LAUNCHED();
     return;
@@ -591,6 +591,7 @@ void launch_cost_build(const uint32_t* ids, const uint64_t* offsets, uint64_t ro
       ids, offsets, rows, n, rows_per_block, ol, id_space, ucost, sizes, bw, matrix, gap_keys,
       row_index, flags);
   EDX_LAUNCHED();
+  g_kernel_name[kKBuild] = "k_cost_build";
 }
 
 void launch_gap_keys(const double* matrix, uint64_t rows, int n, uint64_t* gap_keys,

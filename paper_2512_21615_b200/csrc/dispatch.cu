@@ -244,6 +244,7 @@ void launch_greedy(const double* matrix, uint64_t rows, int n, const uint32_t* o
   if (n_order == 0) return;
   k_greedy_prefs<<<static_cast<unsigned>((n_order + 255) / 256), 256, 0, s>>>(
       matrix, n, order, n_order, capacity_dev, cap_uniform, prefs);
+  g_kernel_name[kKGreedy] = "k_greedy";
   k_greedy<<<1, kGreedyThreads, 0, s>>>(matrix, n, order, n_order, capacity_dev, cap_uniform,
                                         decision, row_ids, pair_worker, flags, prefs);
   EDX_LAUNCHED();

@@ -69,6 +69,11 @@ void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cu
 inline void invalid(const std::string& m) { throw Error(EDX_INVALID_ARGUMENT, m); }
 inline void logic(const std::string& m) { throw Error(EDX_LOGIC_ERROR, m); }
 
+// Name of the kernel each phase launched last on this thread (the bench's
+// labels; edx_engine_last_kernels): [0] cost build, [1] exact solver, [2] greedy.
+enum KernelSlot { kKBuild = 0, kKSolver = 1, kKGreedy = 2 };
+inline thread_local const char* g_kernel_name[3] = {"", "", ""};
+
 // edx_last_error() storage (engine.cu)
 void set_last_error(const char* m);
 

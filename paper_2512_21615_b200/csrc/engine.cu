@@ -167,6 +167,39 @@ __global__ void k_seed_entry(uint32_t id, int j, int latest, int owner, uint32_t
   *status = 0;
 }
 
+__global__ void k_fill_slots(int32_t* p, uint64_t n) {
+  const uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (x < n) p[x] = -1;
+}
+
+// Parity import of worker j's cache entries into slots [0, count): the slot
+// arrays, the id -> slot index, and a check that each entry's version flag
+// equals bit j of the imported `latest` mask (sim.hpp:229-231).
+__global__ void k_import_entries(int j, uint64_t count, uint64_t capacity, uint64_t id_space,
+                                 const uint32_t* __restrict__ ids, const uint8_t* __restrict__ ver,
+                                 const uint32_t* __restrict__ mark, const uint32_t* __restrict__ freq,
+                                 const uint64_t* __restrict__ last, const ulonglong2* __restrict__ ol,
+                                 int32_t* __restrict__ slot_of, uint32_t* __restrict__ sid,
+                                 uint32_t* __restrict__ smark, uint32_t* __restrict__ sfreq,
+                                 uint32_t* __restrict__ slast, int* __restrict__ status) {
+  const uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (x >= count) return;
+  const uint32_t id = ids[x];
+  if (id >= id_space) {
+    atomicOr(status + 0, 1);
+    return;
+  }
+  if (last[x] > 0xFFFFFFFFull) atomicOr(status + 1, 1);
+  if (ver && static_cast<uint64_t>(ver[x] != 0) != ((ol[id].y >> j) & 1ULL)) atomicOr(status + 2, 1);
+  int32_t* so = slot_of + static_cast<uint64_t>(j) * id_space + id;
+  if (atomicCAS(so, -1, static_cast<int32_t>(x)) != -1) atomicOr(status + 3, 1);  // duplicate id
+  const uint64_t g = static_cast<uint64_t>(j) * capacity + x;
+  sid[g] = id;
+  smark[g] = mark[x];
+  sfreq[g] = freq[x];
+  slast[g] = static_cast<uint32_t>(last[x]);
+}
+
 // validate_consistency (sim.hpp:222-248) over the device tables.
 // status: [0] entry without resident bit, [1] invariant violated (+id in [3]),
 // [2] resident bit without entry, [4] at_current_mark drift
@@ -362,7 +395,7 @@ void engine_load(edx_engine* e, const uint32_t* ids, const uint64_t* offsets, ui
                  std::to_string(e->max_ids));
   e->rows = R;
   e->total_ids = total;
-  e->built = e->dispatched = false;
+  e->built = e->dispatched = e->expected_ready = false;
 }
 
 void engine_build(edx_engine* e) {
@@ -380,6 +413,7 @@ void engine_build(edx_engine* e) {
                            e->ucost.p, e->matrix.p, e->disp.gap_keys.p, e->disp.row_index.p,
                            e->flags.p, e->stream);
     e->gap_ready = true;
+    e->kname[edx::kKBuild] = edx::g_kernel_name[edx::kKBuild];
   } else {
     // row shards (samples are independent, cost.hpp:102-104), gathered to rank 0
     std::vector<uint64_t> lo(e->world), hi(e->world);
@@ -389,6 +423,7 @@ void engine_build(edx_engine* e) {
       edx::launch_cost_build(e->cur_ids, e->cur_offsets + a, b - a, e->n, e->ol.p, e->id_space,
                              e->ucost.p, e->matrix.p + a * e->n, nullptr, nullptr, e->flags.p,
                              e->stream);
+    e->kname[edx::kKBuild] = edx::g_kernel_name[edx::kKBuild];
     edx::nccl_gather_rows(e->comm, e->matrix.p, lo.data(), hi.data(), e->world, e->rank, 0, e->n,
                           e->stream);
     e->gap_ready = false;
@@ -416,10 +451,14 @@ void engine_dispatch(edx_engine* e, double alpha) {
   }
   int launches = 0;
   rec(e, 10, e->stream);
-  if (e->rank == 0)
+  if (e->rank == 0) {
+    edx::g_kernel_name[edx::kKSolver] = edx::g_kernel_name[edx::kKGreedy] = "";
     edx::run_ecomix(e->disp, e->matrix.p, e->rows, e->n, e->m, alpha, e->gap_ready,
                     e->decision.p, e->flags.p, e->stream, e->device, e->profiling ? &pe : nullptr,
                     &launches);
+    e->kname[edx::kKSolver] = edx::g_kernel_name[edx::kKSolver];
+    e->kname[edx::kKGreedy] = edx::g_kernel_name[edx::kKGreedy];
+  }
   rec(e, 11, e->stream);
   if (e->world == 1) {
     // decision_cost is only reported (sim.hpp:439): overlap it with the step.
@@ -447,7 +486,7 @@ void engine_dispatch(edx_engine* e, double alpha) {
   const int mult = edx::exact_multiplicity(e->m, alpha);
   e->pending_greedy = e->profiling && static_cast<uint64_t>(e->n) * mult < e->rows;
   e->pending_dispatch = e->profiling;
-  e->dispatched = true;
+  e->dispatched = e->expected_ready = true;
 }
 
 // DispatchDecision::validate — assign.hpp:41-57, same messages.
@@ -521,6 +560,7 @@ void step_finish(edx_engine* e, edx_report* rep) {
     rep->cost_s += rep->cost_w[j];
   }
   ++e->clock;
+  ++e->state_version;
   e->dispatched = false;
 }
 
@@ -617,7 +657,7 @@ void engine_iterate_core(edx_engine* e, double alpha) {
   EDX_CUDA(cudaGraphLaunch(e->gexec, e->stream));
   EDX_CUDA(cudaEventRecord(e->cost_done, e->stream));
   e->launches += e->g_launches;
-  e->built = e->gap_ready = e->dispatched = true;
+  e->built = e->gap_ready = e->dispatched = e->expected_ready = true;
 }
 
 }  // namespace
@@ -887,6 +927,7 @@ int edx_engine_dispatch_hitgreedy(edx_engine* e, int32_t* decision_out) {
                           e->id_space, e->decision.p, e->flags.p, e->stream);
     e->launches += 3;
     e->dispatched = true;
+    e->expected_ready = false;
     if (decision_out) {
       EDX_CUDA(cudaMemcpyAsync(decision_out, e->decision.p, e->rows * sizeof(int32_t),
                                cudaMemcpyDeviceToHost, e->stream));
@@ -981,6 +1022,7 @@ int edx_engine_seed_entry(edx_engine* e, uint32_t id, int32_t worker, int latest
     EDX_CUDA(cudaMemcpyAsync(&st, status, sizeof st, cudaMemcpyDeviceToHost, e->stream));
     EDX_CUDA(cudaStreamSynchronize(e->stream));
     if (st == 1) edx::logic("touch would insert into a full cache; evict first");
+    ++e->state_version;
   });
 }
 
@@ -1035,6 +1077,23 @@ int edx_engine_validate_consistency(edx_engine* e) {
 }
 
 uint64_t edx_engine_clock(edx_engine* e) { return e->clock; }
+
+uint64_t edx_engine_state_version(edx_engine* e) { return e->state_version; }
+
+int edx_engine_synchronize(edx_engine* e) {
+  return guard([&] {
+    EDX_CUDA(cudaSetDevice(e->device));
+    engine_sync_check(e);
+  });
+}
+
+int edx_engine_expected_cost(edx_engine* e, double* out) {
+  return guard([&] {
+    if (!e->expected_ready) edx::invalid("no EcoMix dispatch decision to cost");
+    EDX_CUDA(cudaSetDevice(e->device));
+    *out = fetch_expected(e);
+  });
+}
 
 int edx_nccl_unique_id(void* out, uint64_t len) {
   return guard([&] {
@@ -1148,6 +1207,7 @@ int edx_engine_import_snapshot(edx_engine* e, const uint32_t* ids, const uint64_
                                const uint64_t* latest, const uint64_t* resident, uint64_t count) {
   return guard([&] {
     EDX_CUDA(cudaSetDevice(e->device));
+    ++e->state_version;
     EDX_CUDA(cudaMemsetAsync(e->ol.p, 0, e->id_space * sizeof(ulonglong2), e->stream));
     EDX_CUDA(cudaMemsetAsync(e->res.p, 0, e->id_space * sizeof(unsigned long long), e->stream));
     if (count) {
@@ -1166,6 +1226,113 @@ int edx_engine_import_snapshot(edx_engine* e, const uint32_t* ids, const uint64_
       EDX_LAUNCHED();
       engine_sync_check(e);
     }
+  });
+}
+
+int edx_engine_import_state(edx_engine* e, uint64_t clock, uint64_t g_count, const uint32_t* g_ids,
+                            const uint64_t* g_owners, const uint64_t* g_latest,
+                            const uint64_t* g_resident, const uint64_t* entry_off,
+                            const uint32_t* e_ids, const uint8_t* e_version, const uint32_t* e_mark,
+                            const uint32_t* e_freq, const uint64_t* e_last,
+                            const uint32_t* current_mark, const uint64_t* at_current_mark) {
+  const int rc = guard([&] {
+    if (!e) edx::invalid("null engine");
+    if (clock >= 0xFFFFFFFFull) edx::invalid("clock exceeds 2^32 iterations");
+    const int n = e->n;
+    if (entry_off[0] != 0) edx::invalid("entry offsets must start at 0");
+    for (int j = 0; j < n; ++j) {
+      if (entry_off[j + 1] < entry_off[j]) edx::invalid("entry offsets must be non-decreasing");
+      if (entry_off[j + 1] - entry_off[j] > e->capacity)
+        edx::invalid("imported cache exceeds its capacity");
+    }
+    EDX_CUDA(cudaSetDevice(e->device));
+    EDX_CUDA(cudaStreamSynchronize(e->stream));
+    edx::step_head_abandon(e);
+    auto& c = e->cache;
+    // the global table (SimState::global_): zero, then the imported rows
+    EDX_CUDA(cudaMemsetAsync(e->ol.p, 0, e->id_space * sizeof(ulonglong2), e->stream));
+    EDX_CUDA(cudaMemsetAsync(e->res.p, 0, e->id_space * sizeof(unsigned long long), e->stream));
+    const uint64_t cells = static_cast<uint64_t>(n) * e->id_space;
+    k_fill_slots<<<grid_for(cells), kT, 0, e->stream>>>(c.slot_of.p, cells);
+    EDX_LAUNCHED();
+    DevBuf<int> status;
+    status.ensure(8);
+    EDX_CUDA(cudaMemsetAsync(status.p, 0, 8 * sizeof(int), e->stream));
+    if (g_count) {
+      DevBuf<uint32_t> d_ids;
+      DevBuf<unsigned long long> a, b, r;
+      d_ids.ensure(g_count);
+      a.ensure(g_count);
+      b.ensure(g_count);
+      r.ensure(g_count);
+      EDX_CUDA(cudaMemcpyAsync(d_ids.p, g_ids, g_count * 4, cudaMemcpyHostToDevice, e->stream));
+      EDX_CUDA(cudaMemcpyAsync(a.p, g_owners, g_count * 8, cudaMemcpyHostToDevice, e->stream));
+      EDX_CUDA(cudaMemcpyAsync(b.p, g_latest, g_count * 8, cudaMemcpyHostToDevice, e->stream));
+      EDX_CUDA(cudaMemcpyAsync(r.p, g_resident, g_count * 8, cudaMemcpyHostToDevice, e->stream));
+      k_import<<<grid_for(g_count), kT, 0, e->stream>>>(d_ids.p, a.p, b.p, r.p, g_count,
+                                                       e->id_space, e->ol.p, e->res.p, status.p);
+      EDX_LAUNCHED();
+      EDX_CUDA(cudaStreamSynchronize(e->stream));
+    }
+    // every worker's cache (WorkerCache::entries_, current_mark_, at_current_mark_)
+    const uint64_t total = entry_off[n];
+    std::vector<uint32_t> sizes(n);
+    for (int j = 0; j < n; ++j) sizes[j] = static_cast<uint32_t>(entry_off[j + 1] - entry_off[j]);
+    if (total) {
+      DevBuf<uint32_t> di, dm, df;
+      DevBuf<uint64_t> dl;
+      DevBuf<uint8_t> dv;
+      di.ensure(total);
+      dm.ensure(total);
+      df.ensure(total);
+      dl.ensure(total);
+      EDX_CUDA(cudaMemcpyAsync(di.p, e_ids, total * 4, cudaMemcpyHostToDevice, e->stream));
+      EDX_CUDA(cudaMemcpyAsync(dm.p, e_mark, total * 4, cudaMemcpyHostToDevice, e->stream));
+      EDX_CUDA(cudaMemcpyAsync(df.p, e_freq, total * 4, cudaMemcpyHostToDevice, e->stream));
+      EDX_CUDA(cudaMemcpyAsync(dl.p, e_last, total * 8, cudaMemcpyHostToDevice, e->stream));
+      if (e_version) {
+        dv.ensure(total);
+        EDX_CUDA(cudaMemcpyAsync(dv.p, e_version, total, cudaMemcpyHostToDevice, e->stream));
+      }
+      for (int j = 0; j < n; ++j) {
+        const uint64_t a = entry_off[j], cnt = sizes[j];
+        if (!cnt) continue;
+        k_import_entries<<<grid_for(cnt), kT, 0, e->stream>>>(
+            j, cnt, e->capacity, e->id_space, di.p + a, e_version ? dv.p + a : nullptr, dm.p + a,
+            df.p + a, dl.p + a, e->ol.p, c.slot_of.p, c.sid.p, c.smark.p, c.sfreq.p, c.slast.p,
+            status.p + 4);
+        EDX_LAUNCHED();
+      }
+      EDX_CUDA(cudaStreamSynchronize(e->stream));
+    }
+    std::vector<unsigned long long> at(n);
+    for (int j = 0; j < n; ++j) at[j] = at_current_mark[j];
+    EDX_CUDA(cudaMemcpyAsync(c.size.p, sizes.data(), n * 4, cudaMemcpyHostToDevice, e->stream));
+    EDX_CUDA(cudaMemcpyAsync(c.cur_mark.p, current_mark, n * 4, cudaMemcpyHostToDevice, e->stream));
+    EDX_CUDA(cudaMemcpyAsync(c.at_cur.p, at.data(), n * 8, cudaMemcpyHostToDevice, e->stream));
+    int st[8];
+    EDX_CUDA(cudaMemcpyAsync(st, status.p, sizeof st, cudaMemcpyDeviceToHost, e->stream));
+    EDX_CUDA(cudaStreamSynchronize(e->stream));
+    if (st[edx::kFlagIdOutOfRange] || st[4])
+      edx::invalid("embedding id outside the engine's id_space");
+    if (st[5]) edx::invalid("last_access exceeds 2^32");
+    if (st[6]) edx::logic("version flag diverged from global state");
+    if (st[7]) edx::invalid("duplicate id in an imported cache");
+    e->clock = clock;
+    e->built = e->dispatched = e->expected_ready = false;
+    ++e->state_version;
+  });
+  // the imported state must satisfy SimState::validate_consistency
+  // (sim.hpp:222-248), at_current_mark included
+  return rc != EDX_OK ? rc : edx_engine_validate_consistency(e);
+}
+
+int edx_engine_last_kernels(edx_engine* e, const char** build, const char** solver,
+                            const char** greedy) {
+  return guard([&] {
+    if (build) *build = e->kname[edx::kKBuild];
+    if (solver) *solver = e->kname[edx::kKSolver];
+    if (greedy) *greedy = e->kname[edx::kKGreedy];
   });
 }
 

@@ -66,6 +66,9 @@ struct edx_engine {
   int rank = 0, world = 1;
   void* comm = nullptr;  // ncclComm_t when world > 1; rank 0 is the solver rank
   uint64_t clock = 0;
+  // bumped by every state mutation (step, seed_entry, imports): a Snapshot
+  // view of the device state is current while this is unchanged
+  uint64_t state_version = 0;
 
   // global per-embedding state (SimState::global_, sim.hpp:266), dense by id
   edx::DevBuf<ulonglong2> ol;             // {owners, latest}
@@ -89,6 +92,7 @@ struct edx_engine {
   edx::DispatchScratch disp;
   edx::HitScratch hit;
   bool built = false, gap_ready = false, dispatched = false;
+  bool expected_ready = false;  // the last EcoMix dispatch's decision_cost is enqueued
 
   edx::DevBuf<int> flags;
   int* h_flags = nullptr;            // pinned
@@ -126,6 +130,9 @@ struct edx_engine {
   uint64_t g_launches = 0;
   unsigned long long g_epoch = 0;  // edx::g_alloc_epoch at capture
   bool capturing = false;
+
+  // the kernels the last build / exact solve / greedy launched (bench labels)
+  const char* kname[3] = {"", "", ""};
 
   // profiling
   bool profiling = false;

@@ -2321,21 +2321,21 @@ void launch_hungarian_blocks(HungarianScratch& sc, const double* matrix, int n,
       };
       // the warp cap sets the register budget: 255 (n <= 8), 128 (n <= 32)
       if (pair && n <= 16) {
-        if (am == 0) launch(k_hungarian_blocks_mw<0, 8, 2>);
-        else if (am == 1) launch(k_hungarian_blocks_mw<1, 8, 2>);
-        else launch(k_hungarian_blocks_mw<2, 8, 2>);
+        if (am == 0) { launch(k_hungarian_blocks_mw<0, 8, 2>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<0,8,2>"; }
+        else if (am == 1) { launch(k_hungarian_blocks_mw<1, 8, 2>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<1,8,2>"; }
+        else { launch(k_hungarian_blocks_mw<2, 8, 2>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<2,8,2>"; }
       } else if (n <= 8) {
-        if (am == 0) launch(k_hungarian_blocks_mw<0, 8, 1>);
-        else if (am == 1) launch(k_hungarian_blocks_mw<1, 8, 1>);
-        else launch(k_hungarian_blocks_mw<2, 8, 1>);
+        if (am == 0) { launch(k_hungarian_blocks_mw<0, 8, 1>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<0,8,1>"; }
+        else if (am == 1) { launch(k_hungarian_blocks_mw<1, 8, 1>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<1,8,1>"; }
+        else { launch(k_hungarian_blocks_mw<2, 8, 1>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<2,8,1>"; }
       } else if (n <= 16) {
-        if (am == 0) launch(k_hungarian_blocks_mw<0, 16, 1>);
-        else if (am == 1) launch(k_hungarian_blocks_mw<1, 16, 1>);
-        else launch(k_hungarian_blocks_mw<2, 16, 1>);
+        if (am == 0) { launch(k_hungarian_blocks_mw<0, 16, 1>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<0,16,1>"; }
+        else if (am == 1) { launch(k_hungarian_blocks_mw<1, 16, 1>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<1,16,1>"; }
+        else { launch(k_hungarian_blocks_mw<2, 16, 1>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<2,16,1>"; }
       } else {
-        if (am == 0) launch(k_hungarian_blocks_mw<0, 16, 2>);
-        else if (am == 1) launch(k_hungarian_blocks_mw<1, 16, 2>);
-        else launch(k_hungarian_blocks_mw<2, 16, 2>);
+        if (am == 0) { launch(k_hungarian_blocks_mw<0, 16, 2>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<0,16,2>"; }
+        else if (am == 1) { launch(k_hungarian_blocks_mw<1, 16, 2>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<1,16,2>"; }
+        else { launch(k_hungarian_blocks_mw<2, 16, 2>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<2,16,2>"; }
       }
       EDX_LAUNCHED();
       return;
@@ -2356,6 +2356,7 @@ void launch_hungarian_blocks(HungarianScratch& sc, const double* matrix, int n,
       };
       if (sm == 0) launch(k_hungarian_blocks_tab<1, 0, true>);
       else launch(k_hungarian_blocks_tab<1, 1, true>);
+      g_kernel_name[kKSolver] = "k_hungarian_blocks_tab";
       EDX_LAUNCHED();
       return;
     }
@@ -2380,6 +2381,7 @@ void launch_hungarian_blocks(HungarianScratch& sc, const double* matrix, int n,
       if (am == 0) launch(k_hungarian_blocks_run<0>);
       else if (am == 1) launch(k_hungarian_blocks_run<1>);
       else launch(k_hungarian_blocks_run<2>);
+      g_kernel_name[kKSolver] = "k_hungarian_blocks_run";
       EDX_LAUNCHED();
       return;
     }
@@ -2401,6 +2403,7 @@ void launch_hungarian_blocks(HungarianScratch& sc, const double* matrix, int n,
       kern<<<1, 32 * nw, smem, s>>>(sc.s64.p, n, mult, k, garena, order, decision, row_ids,
                                     col_of_row, sc.steps.p, flags, max_scaled);
     };
+    g_kernel_name[kKSolver] = n <= 32 ? "k_hungarian_blocks_fast<1>" : "k_hungarian_blocks_fast<2>";
     if (n <= 32) {
       if (mode == 0) launch(k_hungarian_blocks_fast<1, 0>);
       else if (mode == 1) launch(k_hungarian_blocks_fast<1, 1>);
@@ -2416,6 +2419,7 @@ void launch_hungarian_blocks(HungarianScratch& sc, const double* matrix, int n,
   // only for very large blocks: the single-warp kernel with global arrays
   const size_t arena = block_arena_bytes(k, mult);
   sc.arena.ensure(arena);
+  g_kernel_name[kKSolver] = "k_hungarian_blocks_wide<2>";
   k_hungarian_blocks_wide<2><<<1, 32, 0, s>>>(sc.s64.p, n, mult, k, 0, sc.arena.p, order, decision,
                                               row_ids, col_of_row, sc.steps.p, flags);
   EDX_LAUNCHED();
@@ -2438,6 +2442,7 @@ void launch_hungarian_dense(HungarianScratch& sc, const double* values, uint64_t
   if (smem > 48 * 1024)
     EDX_CUDA(cudaFuncSetAttribute(k_hungarian_dense, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
+  g_kernel_name[kKSolver] = "k_hungarian_dense";
   k_hungarian_dense<<<1, kDenseThreads, smem, s>>>(values, static_cast<int>(k), cap, garena,
                                                    col_of_row, sc.steps.p, flags);
   EDX_LAUNCHED();

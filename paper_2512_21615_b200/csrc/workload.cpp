@@ -290,6 +290,33 @@ int edx_zipf_next(edx_zipf* z, uint32_t* ids) {
 
 void edx_zipf_reset(edx_zipf* z) { z->reset_stream(); }
 
+int edx_zipf_sampler_create(uint64_t population, double zipf_s, uint64_t seed, edx_zipf** out) {
+  if (population == 0) {
+    edx_set_error(EDX_INVALID_ARGUMENT, "population must be positive");
+    return EDX_INVALID_ARGUMENT;
+  }
+  if (population > 0xFFFFFFFFull) {
+    edx_set_error(EDX_INVALID_ARGUMENT, "population exceeds 32-bit ids");
+    return EDX_INVALID_ARGUMENT;
+  }
+  auto* z = new edx_zipf;  // no stream: iterations = 0, no producer thread
+  z->sample_len = 1;
+  z->seed = seed;
+  build_cdf(z, population, zipf_s);
+  z->rng.seed(seed);
+  *out = z;
+  return EDX_OK;
+}
+
+int edx_zipf_draw(edx_zipf* z, uint64_t count, uint32_t* out) {
+  if (z->producer.joinable()) {
+    edx_set_error(EDX_INVALID_ARGUMENT, "edx_zipf_draw needs a sampler (edx_zipf_sampler_create)");
+    return EDX_INVALID_ARGUMENT;
+  }
+  for (uint64_t t = 0; t < count; ++t) out[t] = z->next_draw();
+  return EDX_OK;
+}
+
 void edx_zipf_destroy(edx_zipf* z) { delete z; }
 
 }  // extern "C"
