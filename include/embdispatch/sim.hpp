@@ -89,7 +89,7 @@ class SimState {
   explicit SimState(const ClusterConfig& cfg, EngineOptions opt = {}) : cfg_(cfg) {
     edx_engine_options o{};
     o.device = opt.device;
-    o.id_space = opt.id_space ? opt.id_space : edxc::env_or("EDX_ID_SPACE", 1ULL << 20);
+    o.id_space = opt.id_space ? opt.id_space : edxc::env_or("EDX_ID_SPACE", 0);
     o.max_batch_ids = opt.max_batch_ids ? opt.max_batch_ids : edxc::env_or("EDX_MAX_BATCH_IDS", 1ULL << 20);
     o.world_size = 1;
     const edx_cluster_config c = edxc::to_c(cfg_);

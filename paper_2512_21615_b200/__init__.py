@@ -448,10 +448,13 @@ class SimState:
     """embdispatch::SimState (sim.hpp:54-268) with its global state and per-
     worker caches resident on a B200.
 
-    id_space: ids must lie in [0, id_space) (dense device tables).
+    id_space: > 0 selects the dense fast path (ids in [0, id_space), tables
+    indexed by id); 0 accepts any uint32 id through the device id table
+    (ids.cu), which grows as new ids arrive.
     max_batch_ids: capacity of one batch's id stream (sum of sample lengths)."""
 
-    def __init__(self, cfg: ClusterConfig, id_space: int, max_batch_ids: int, device: int = 0,
+    def __init__(self, cfg: ClusterConfig, id_space: int = 0, max_batch_ids: int = 1 << 20,
+                 device: int = 0,
                  rank: int = 0, world_size: int = 1, nccl_id: Optional[bytes] = None):
         self.cfg = cfg
         self._h = C.c_void_p()

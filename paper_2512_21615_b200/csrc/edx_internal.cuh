@@ -135,6 +135,11 @@ struct DevBuf {
     n = c;
     g_alloc_epoch.fetch_add(1, std::memory_order_relaxed);
   }
+  void swap(DevBuf& o) {
+    std::swap(p, o.p);
+    std::swap(n, o.n);
+    g_alloc_epoch.fetch_add(1, std::memory_order_relaxed);
+  }
 };
 
 // ------------------------------------------------------ kernel launchers

@@ -114,6 +114,7 @@ __global__ void k_import(const uint32_t* __restrict__ ids, const unsigned long l
 
 __global__ void k_export_global(const ulonglong2* __restrict__ ol,
                                 const unsigned long long* __restrict__ res, uint64_t id_space,
+                                const uint32_t* __restrict__ slot2id,
                                 uint32_t* __restrict__ ids, unsigned long long* __restrict__ out,
                                 uint64_t cap, unsigned long long* __restrict__ count) {
   const uint64_t id = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
@@ -123,7 +124,7 @@ __global__ void k_export_global(const ulonglong2* __restrict__ ol,
   if ((st.x | st.y | r) == 0) return;
   const unsigned long long at = atomicAdd(count, 1ULL);
   if (at < cap) {
-    ids[at] = static_cast<uint32_t>(id);
+    ids[at] = slot2id ? slot2id[id] : static_cast<uint32_t>(id);
     out[3 * at] = st.x;
     out[3 * at + 1] = st.y;
     out[3 * at + 2] = r;
@@ -170,6 +171,11 @@ __global__ void k_seed_entry(uint32_t id, int j, int latest, int owner, uint32_t
 __global__ void k_fill_slots(int32_t* p, uint64_t n) {
   const uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (x < n) p[x] = -1;
+}
+
+__global__ void k_fill_value(int32_t* p, uint64_t n, int32_t v) {
+  const uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (x < n) p[x] = v;
 }
 
 // Parity import of worker j's cache entries into slots [0, count): the slot
@@ -222,14 +228,16 @@ __global__ void k_validate_slots(int n, uint64_t capacity, uint64_t id_space,
 
 __global__ void k_validate_ids(int n, uint64_t id_space, const ulonglong2* __restrict__ ol,
                                const unsigned long long* __restrict__ res,
-                               const int32_t* __restrict__ slot_of, int* status) {
+                               const int32_t* __restrict__ slot_of,
+                               const uint32_t* __restrict__ slot2id, int* status) {
   const uint64_t id = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (id >= id_space) return;
   const ulonglong2 st = ol[id];
   const unsigned long long r = res[id];
   const bool ok = ((st.x & ~st.y) == 0) && ((st.y & ~r) == 0) && !(st.x != 0 && st.y != st.x);
   if (!ok) {
-    if (atomicOr(status + 1, 1) == 0) status[3] = static_cast<int>(id);
+    if (atomicOr(status + 1, 1) == 0)
+      status[3] = static_cast<int>(slot2id ? slot2id[id] : static_cast<uint32_t>(id));
   }
   for (unsigned long long it = r; it; it &= it - 1) {
     const int w = __ffsll(static_cast<long long>(it)) - 1;
@@ -239,10 +247,13 @@ __global__ void k_validate_ids(int n, uint64_t id_space, const ulonglong2* __res
 
 __global__ void k_export_cache(int j, uint64_t capacity, uint32_t count,
                                const uint32_t* __restrict__ sid, const ulonglong2* __restrict__ ol,
-                               uint8_t* __restrict__ ver) {
+                               const uint32_t* __restrict__ slot2id, uint8_t* __restrict__ ver,
+                               uint32_t* __restrict__ ids) {
   const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= count) return;
-  ver[s] = static_cast<uint8_t>((ol[sid[static_cast<uint64_t>(j) * capacity + s]].y >> j) & 1ULL);
+  const uint32_t slot = sid[static_cast<uint64_t>(j) * capacity + s];
+  ver[s] = static_cast<uint8_t>((ol[slot].y >> j) & 1ULL);
+  ids[s] = slot2id ? slot2id[slot] : slot;
 }
 
 // sum_i values[i*stride + col[i]] left to right (hungarian total, assign.hpp:153-155)
@@ -396,11 +407,96 @@ void engine_load(edx_engine* e, const uint32_t* ids, const uint64_t* offsets, ui
   e->rows = R;
   e->total_ids = total;
   e->built = e->dispatched = e->expected_ready = false;
+  e->cur_raw = e->cur_ids;
+  if (e->hashed) {  // kernels read the slot stream, translated before first use
+    e->cur_ids = e->kslots.p;
+    e->translated = false;
+  }
+}
+
+// ---------------------------------------------------- arbitrary ids (ids.cu)
+// Reallocates the slot-indexed tables (global masks, per-worker cache index,
+// the step's first-occurrence table) for `cap` slots, keeping the first
+// `used` slots, and rebuilds the id table.  Between iterations only.
+void grow_slots(edx_engine* e, uint64_t need) {
+  const uint64_t kMax = 0xFFFFFFF0ull;
+  if (need > kMax) edx::invalid("more than 2^32 - 16 distinct embedding ids");
+  const uint64_t old = e->id_space, used = e->idt.used;
+  const uint64_t cap = std::min(kMax, std::max(2 * old, need + need / 2));
+  EDX_CUDA(cudaStreamSynchronize(e->step_side));
+  EDX_CUDA(cudaStreamSynchronize(e->stream));
+  const int n = e->n;
+  DevBuf<ulonglong2> ol;
+  DevBuf<unsigned long long> res;
+  DevBuf<int32_t> so, fp;
+  ol.ensure(cap);
+  res.ensure(cap);
+  so.ensure(static_cast<uint64_t>(n) * cap);
+  fp.ensure(cap);
+  EDX_CUDA(cudaMemsetAsync(ol.p, 0, cap * sizeof(ulonglong2), e->stream));
+  EDX_CUDA(cudaMemsetAsync(res.p, 0, cap * sizeof(unsigned long long), e->stream));
+  k_fill_slots<<<grid_for(static_cast<uint64_t>(n) * cap), kT, 0, e->stream>>>(so.p, static_cast<uint64_t>(n) * cap);
+  k_fill_value<<<grid_for(cap), kT, 0, e->stream>>>(fp.p, cap, INT_MAX);
+  EDX_LAUNCHED();
+  if (used) {
+    EDX_CUDA(cudaMemcpyAsync(ol.p, e->ol.p, used * sizeof(ulonglong2), cudaMemcpyDeviceToDevice, e->stream));
+    EDX_CUDA(cudaMemcpyAsync(res.p, e->res.p, used * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, e->stream));
+    EDX_CUDA(cudaMemcpy2DAsync(so.p, cap * sizeof(int32_t), e->cache.slot_of.p, old * sizeof(int32_t),
+                               used * sizeof(int32_t), n, cudaMemcpyDeviceToDevice, e->stream));
+  }
+  e->ol.swap(ol);
+  e->res.swap(res);
+  e->cache.slot_of.swap(so);
+  e->step.first_pos.swap(fp);
+  edx::id_table_grow(e->idt, cap, e->stream);
+  e->id_space = cap;
+}
+
+// Makes room for `T` new ids before a translation (exact count read back
+// only when the running bound says the table might be short).
+void reserve_slots(edx_engine* e, uint64_t T) {
+  if (e->used_bound + T <= e->idt.cap) return;
+  if (e->capturing) edx::invalid("id table full during graph capture");
+  EDX_CUDA(cudaStreamSynchronize(e->stream));
+  unsigned long long used = 0;
+  EDX_CUDA(cudaMemcpy(&used, e->idt.count.p, sizeof used, cudaMemcpyDeviceToHost));
+  e->idt.used = used;
+  e->used_bound = used;
+  if (used + T > e->idt.cap) grow_slots(e, used + T);
+}
+
+// Translates the loaded batch to slots (hashed mode) before its first consumer.
+void ensure_translated(edx_engine* e) {
+  if (!e->hashed || e->translated) return;
+  reserve_slots(e, e->total_ids);
+  edx::id_table_translate(e->idt, e->cur_raw, e->total_ids, e->kslots.p, true, e->flags.p,
+                          e->stream);
+  e->used_bound += e->total_ids;
+  e->translated = true;
+  e->launches += 1;
+}
+
+// Slots of host ids (dense mode: the ids), inserting new ids when `insert`;
+// absent ids map to 0xFFFFFFFF when not inserting.
+std::vector<uint32_t> host_slots(edx_engine* e, const uint32_t* ids, uint64_t count, bool insert) {
+  std::vector<uint32_t> out(ids, ids + count);
+  if (!e->hashed || count == 0) return out;
+  if (insert) reserve_slots(e, count);
+  DevBuf<uint32_t> din, dout;
+  din.ensure(count);
+  dout.ensure(count);
+  EDX_CUDA(cudaMemcpyAsync(din.p, ids, count * 4, cudaMemcpyHostToDevice, e->stream));
+  edx::id_table_translate(e->idt, din.p, count, dout.p, insert, e->flags.p, e->stream);
+  EDX_CUDA(cudaMemcpyAsync(out.data(), dout.p, count * 4, cudaMemcpyDeviceToHost, e->stream));
+  engine_sync_check(e);
+  if (insert) e->used_bound += count;
+  return out;
 }
 
 void engine_build(edx_engine* e) {
   const uint64_t want = static_cast<uint64_t>(e->n) * static_cast<uint64_t>(e->m);
   if (!e->cur_ids) edx::invalid("no batch loaded");
+  ensure_translated(e);
   if (e->rows != want)
     edx::invalid("expected " + std::to_string(want) + " samples, got " + std::to_string(e->rows));
   e->matrix.ensure(e->rows * e->n);
@@ -519,6 +615,7 @@ double fetch_expected(edx_engine* e) {
 // Enqueues the step for the current batch and decision (no sync).
 void step_enqueue(edx_engine* e, const int32_t* decision) {
   if (!e->cur_ids) edx::invalid("no batch loaded");
+  ensure_translated(e);
   if (decision) {
     validate_decision_host(decision, e->rows, e->n, e->m);
     e->decision.ensure(e->rows);
@@ -532,6 +629,9 @@ void step_enqueue(edx_engine* e, const int32_t* decision) {
   edx::StepResult sr;
   rec(e, 8, e->stream);
   edx::step_run(e, e->decision.p, &sr);
+  if (e->hashed)  // the slots in use, read back with the iteration's counters
+    EDX_CUDA(cudaMemcpyAsync(e->h_used, e->idt.count.p, sizeof(unsigned long long),
+                             cudaMemcpyDeviceToHost, e->stream));
   rec(e, 9, e->stream);
   e->launches += sr.launches;
   e->pending_step = e->profiling;
@@ -540,6 +640,7 @@ void step_enqueue(edx_engine* e, const int32_t* decision) {
 // Waits for the iteration and assembles its IterationReport.
 void step_finish(edx_engine* e, edx_report* rep) {
   engine_sync_check(e);
+  if (e->hashed) e->used_bound = e->idt.used = *e->h_used;
   // IterationReport totals and realised cost, worker order (sim.hpp:206-216)
   const int n = e->n;
   const unsigned long long* c = e->h_counters;
@@ -578,6 +679,7 @@ void engine_step(edx_engine* e, const int32_t* decision, edx_report* rep) {
 // head on the side stream overlapping the build and the dispatch
 void iterate_enqueue(edx_engine* e, double alpha) {
   if (!e->cur_ids) edx::invalid("no batch loaded");
+  ensure_translated(e);
   if (!e->profiling) edx::step_head(e);  // profiled runs time the whole step in its phase
   try {
     engine_build(e);
@@ -601,12 +703,13 @@ void engine_iterate_core(edx_engine* e, double alpha) {
     if (e->world > 1 && !(mv && std::strcmp(mv, "1") == 0)) e->graph_mode = 0;
   }
   const bool eligible = e->graph_mode == 1 && !e->profiling &&
-                        edx::step_device_only(e) && e->cur_ids == e->ids.p;
+                        edx::step_device_only(e) && e->cur_raw == e->ids.p;
   if (!eligible) {
     iterate_enqueue(e, alpha);
     return;
   }
   const double a = alpha < 0.0 ? e->alpha : alpha;
+  if (e->hashed) reserve_slots(e, e->total_ids);  // the graph translates in-stream
   const unsigned long long epoch = edx::g_alloc_epoch.load(std::memory_order_relaxed);
   if (!e->gexec || e->g_rows != e->rows || e->g_total != e->total_ids || e->g_alpha != a ||
       e->g_epoch != epoch) {
@@ -657,6 +760,10 @@ void engine_iterate_core(edx_engine* e, double alpha) {
   EDX_CUDA(cudaGraphLaunch(e->gexec, e->stream));
   EDX_CUDA(cudaEventRecord(e->cost_done, e->stream));
   e->launches += e->g_launches;
+  if (e->hashed) {
+    e->used_bound += e->total_ids;
+    e->translated = true;
+  }
   e->built = e->gap_ready = e->dispatched = e->expected_ready = true;
 }
 
@@ -699,7 +806,7 @@ int edx_engine_create(const edx_cluster_config* cfg, const edx_engine_options* o
       if (!(cfg->bandwidths_bps[j] > 0.0)) edx::invalid("bandwidths must be positive");
     if (cfg->cache_capacity == 0) edx::invalid("cache capacity must be positive");
     if (cfg->alpha < 0.0 || cfg->alpha > 1.0) edx::invalid("alpha must lie in [0, 1]");
-    if (opt->id_space == 0 || opt->id_space > (1ULL << 32)) edx::invalid("id_space must be in [1, 2^32]");
+    if (opt->id_space > (1ULL << 32)) edx::invalid("id_space must be at most 2^32 (0 = any uint32 id)");
     if (opt->max_batch_ids == 0 || opt->max_batch_ids >= (1ULL << 31))
       edx::invalid("max_batch_ids must be in [1, 2^31)");
     if (opt->world_size > 1) {
@@ -719,8 +826,12 @@ int edx_engine_create(const edx_cluster_config* cfg, const edx_engine_options* o
     e->d_tran = cfg->d_tran_bytes;
     e->bw.assign(cfg->bandwidths_bps, cfg->bandwidths_bps + cfg->n);
     e->ucost_h = unit_costs(cfg);
-    e->id_space = opt->id_space;
     e->max_ids = opt->max_batch_ids;
+    // id_space 0: any uint32 id through the device id table, starting with
+    // room for a few batches of new ids (the tables grow on demand)
+    e->hashed = opt->id_space == 0;
+    e->id_space = e->hashed ? std::min<uint64_t>(0xFFFFFFF0ull, std::max<uint64_t>(1ULL << 16, 4 * e->max_ids))
+                            : opt->id_space;
     e->rank = opt->rank;
     e->world = opt->world_size < 1 ? 1 : opt->world_size;
     EDX_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
@@ -749,6 +860,12 @@ int edx_engine_create(const edx_cluster_config* cfg, const edx_engine_options* o
     EDX_CUDA(cudaMallocHost(&e->h_expected, sizeof(double)));
     EDX_CUDA(cudaMallocHost(&e->h_clock, sizeof(uint32_t)));
     e->d_clock.ensure(1);
+    if (e->hashed) {
+      edx::id_table_init(e->idt, e->id_space, e->stream);
+      e->kslots.ensure(e->max_ids);
+      EDX_CUDA(cudaMallocHost(&e->h_used, sizeof(unsigned long long)));
+      *e->h_used = 0;
+    }
     e->disp.init(e->device);
     edx::step_init_state(e.get());
     EDX_CUDA(cudaStreamSynchronize(e->stream));
@@ -784,6 +901,7 @@ void edx_engine_destroy(edx_engine* e) {
   if (e->h_clock) cudaFreeHost(e->h_clock);
   if (e->gexec) cudaGraphExecDestroy(e->gexec);
   if (e->h_expected) cudaFreeHost(e->h_expected);
+  if (e->h_used) cudaFreeHost(e->h_used);
   cudaStream_t s = e->stream;
   if (e->comm) edx::nccl_comm_destroy(e->comm);
   delete e;
@@ -808,9 +926,13 @@ uint64_t check_host_offsets(const edx_engine* e, const uint64_t* offsets, uint64
 // A host batch prefetched by edx_engine_prefetch: wait for its copy, stage it
 // into the engine's own buffers (fixed pointers for the graph) and load it.
 bool load_prefetched(edx_engine* e, const uint32_t* ids, const uint64_t* offsets, uint64_t R) {
-  for (auto& f : e->pf) {
-    if (!f.valid || f.host_ids != ids || f.host_offsets != offsets || f.rows != R) continue;
-    f.valid = false;
+  // only the most recent prefetch can be consumed (the steady-state pairing of
+  // edx_engine_iterate_prefetch); every other load invalidates the slots
+  {
+    auto& f = e->pf[e->pf_next ^ 1];
+    const bool match = f.valid && f.host_ids == ids && f.host_offsets == offsets && f.rows == R;
+    for (auto& g : e->pf) g.valid = false;
+    if (!match) return false;
     EDX_CUDA(cudaStreamWaitEvent(e->stream, f.ready, 0));
     e->offsets.ensure(R + 1);
     if (f.total)
@@ -822,7 +944,10 @@ bool load_prefetched(edx_engine* e, const uint32_t* ids, const uint64_t* offsets
     engine_load(e, e->ids.p, e->offsets.p, R, 1, f.total);
     return true;
   }
-  return false;
+}
+
+void drop_prefetched(edx_engine* e) {
+  for (auto& f : e->pf) f.valid = false;
 }
 
 }  // namespace
@@ -831,8 +956,8 @@ int edx_engine_load_batch(edx_engine* e, const uint32_t* ids, const uint64_t* of
                           uint64_t num_samples, int on_device) {
   return guard([&] {
     EDX_CUDA(cudaSetDevice(e->device));
-    if (on_device || !load_prefetched(e, ids, offsets, num_samples))
-      engine_load(e, ids, offsets, num_samples, on_device);
+    drop_prefetched(e);
+    engine_load(e, ids, offsets, num_samples, on_device);
   });
 }
 
@@ -885,6 +1010,7 @@ int edx_engine_load_device_batch(edx_engine* e, const uint32_t* ids, const uint6
                                  uint64_t num_samples, uint64_t total_ids) {
   return guard([&] {
     EDX_CUDA(cudaSetDevice(e->device));
+    drop_prefetched(e);
     engine_load(e, ids, offsets, num_samples, 1, total_ids);
   });
 }
@@ -922,6 +1048,7 @@ int edx_engine_dispatch_hitgreedy(edx_engine* e, int32_t* decision_out) {
       edx::invalid("sample count must be m*n");
     if (e->m >= (1 << 26)) edx::invalid("at most 2^26 samples per worker");
     e->decision.ensure(e->rows + 2);
+    ensure_translated(e);
     // every rank holds the same replica, so every rank decides identically
     edx::launch_hitgreedy(e->hit, e->cur_ids, e->cur_offsets, e->rows, e->n, e->m, e->ol.p,
                           e->id_space, e->decision.p, e->flags.p, e->stream);
@@ -948,8 +1075,8 @@ int edx_engine_iterate(edx_engine* e, const uint32_t* ids, const uint64_t* offse
                        double* expected_cost_out, edx_report* rep) {
   return guard([&] {
     EDX_CUDA(cudaSetDevice(e->device));
-    if (on_device || !load_prefetched(e, ids, offsets, num_samples))
-      engine_load(e, ids, offsets, num_samples, on_device);
+    drop_prefetched(e);
+    engine_load(e, ids, offsets, num_samples, on_device);
     engine_iterate_core(e, -1.0);
     if (decision_out)
       EDX_CUDA(cudaMemcpyAsync(decision_out, e->decision.p, e->rows * sizeof(int32_t),
@@ -988,6 +1115,7 @@ int edx_engine_iterate_device(edx_engine* e, const uint32_t* ids, const uint64_t
     if (total_ids > e->max_ids)
       edx::invalid("batch holds " + std::to_string(total_ids) + " ids; engine max_batch_ids is " +
                    std::to_string(e->max_ids));
+    drop_prefetched(e);
     // stage into the engine's own batch buffers: fixed pointers for the graph
     e->offsets.ensure(num_samples + 1);
     if (total_ids)
@@ -1009,11 +1137,12 @@ int edx_engine_seed_entry(edx_engine* e, uint32_t id, int32_t worker, int latest
   return guard([&] {
     if (owner && !latest) edx::invalid("an owner's copy is always latest");
     if (worker < 0 || worker >= e->n) edx::invalid("worker out of range");
-    if (id >= e->id_space) edx::invalid("embedding id outside the engine's id_space");
+    if (!e->hashed && id >= e->id_space) edx::invalid("embedding id outside the engine's id_space");
     EDX_CUDA(cudaSetDevice(e->device));
+    const uint32_t slot = host_slots(e, &id, 1, true)[0];
     auto& c = e->cache;
     int* status = reinterpret_cast<int*>(e->step.wscalars.p);
-    k_seed_entry<<<1, 1, 0, e->stream>>>(id, worker, latest, owner, static_cast<uint32_t>(e->clock),
+    k_seed_entry<<<1, 1, 0, e->stream>>>(slot, worker, latest, owner, static_cast<uint32_t>(e->clock),
                                          e->capacity, e->id_space, e->ol.p, e->res.p, c.slot_of.p,
                                          c.sid.p, c.smark.p, c.sfreq.p, c.slast.p, c.size.p,
                                          c.cur_mark.p, c.at_cur.p, status);
@@ -1030,14 +1159,15 @@ int edx_engine_state_of(edx_engine* e, uint32_t id, uint64_t* owners, uint64_t* 
                         uint64_t* resident) {
   return guard([&] {
     EDX_CUDA(cudaSetDevice(e->device));
-    if (id >= e->id_space) {  // unknown embeddings are {0,0,0} (sim.hpp:64-67)
+    const uint32_t slot = e->hashed ? host_slots(e, &id, 1, false)[0] : id;
+    if (slot >= e->id_space) {  // unknown embeddings are {0,0,0} (sim.hpp:64-67)
       *owners = *latest = *resident = 0;
       return;
     }
     ulonglong2 st;
     unsigned long long r;
-    EDX_CUDA(cudaMemcpyAsync(&st, e->ol.p + id, sizeof st, cudaMemcpyDeviceToHost, e->stream));
-    EDX_CUDA(cudaMemcpyAsync(&r, e->res.p + id, sizeof r, cudaMemcpyDeviceToHost, e->stream));
+    EDX_CUDA(cudaMemcpyAsync(&st, e->ol.p + slot, sizeof st, cudaMemcpyDeviceToHost, e->stream));
+    EDX_CUDA(cudaMemcpyAsync(&r, e->res.p + slot, sizeof r, cudaMemcpyDeviceToHost, e->stream));
     EDX_CUDA(cudaStreamSynchronize(e->stream));
     *owners = st.x;
     *latest = st.y;
@@ -1059,8 +1189,9 @@ int edx_engine_validate_consistency(edx_engine* e) {
     k_validate_slots<<<grid_for(cells), kT, 0, e->stream>>>(e->n, e->capacity, e->id_space, c.size.p,
                                                            c.sid.p, e->res.p, c.slot_of.p, c.smark.p,
                                                            c.cur_mark.p, at.p, status.p);
-    k_validate_ids<<<grid_for(e->id_space), kT, 0, e->stream>>>(e->n, e->id_space, e->ol.p, e->res.p,
-                                                               c.slot_of.p, status.p);
+    k_validate_ids<<<grid_for(e->id_space), kT, 0, e->stream>>>(
+        e->n, e->id_space, e->ol.p, e->res.p, c.slot_of.p, e->hashed ? e->idt.slot2id.p : nullptr,
+        status.p);
     EDX_LAUNCHED();
     int st[8];
     std::vector<unsigned long long> at_h(e->n), at_d(e->n);
@@ -1117,8 +1248,9 @@ int edx_engine_export_global(edx_engine* e, uint32_t* ids, uint64_t* owners, uin
     d_ids.ensure(cap);
     d_m.ensure(3 * cap);
     EDX_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), e->stream));
-    k_export_global<<<grid_for(e->id_space), kT, 0, e->stream>>>(e->ol.p, e->res.p, e->id_space,
-                                                                d_ids.p, d_m.p, cap, cnt.p);
+    k_export_global<<<grid_for(e->id_space), kT, 0, e->stream>>>(
+        e->ol.p, e->res.p, e->id_space, e->hashed ? e->idt.slot2id.p : nullptr, d_ids.p, d_m.p, cap,
+        cnt.p);
     EDX_LAUNCHED();
     unsigned long long total = 0;
     EDX_CUDA(cudaMemcpyAsync(&total, cnt.p, sizeof total, cudaMemcpyDeviceToHost, e->stream));
@@ -1167,10 +1299,14 @@ int edx_engine_export_cache(edx_engine* e, int32_t worker, uint32_t* ids, uint8_
     std::vector<uint32_t> hid(sz), hm(sz), hf(sz), hl(sz);
     std::vector<uint8_t> hv(sz);
     DevBuf<uint8_t> dv;
+    DevBuf<uint32_t> di;
     dv.ensure(sz);
-    k_export_cache<<<grid_for(sz), kT, 0, e->stream>>>(worker, e->capacity, sz, c.sid.p, e->ol.p, dv.p);
+    di.ensure(sz);
+    k_export_cache<<<grid_for(sz), kT, 0, e->stream>>>(worker, e->capacity, sz, c.sid.p, e->ol.p,
+                                                       e->hashed ? e->idt.slot2id.p : nullptr, dv.p,
+                                                       di.p);
     EDX_LAUNCHED();
-    EDX_CUDA(cudaMemcpyAsync(hid.data(), c.sid.p + g, sz * 4, cudaMemcpyDeviceToHost, e->stream));
+    EDX_CUDA(cudaMemcpyAsync(hid.data(), di.p, sz * 4, cudaMemcpyDeviceToHost, e->stream));
     EDX_CUDA(cudaMemcpyAsync(hm.data(), c.smark.p + g, sz * 4, cudaMemcpyDeviceToHost, e->stream));
     EDX_CUDA(cudaMemcpyAsync(hf.data(), c.sfreq.p + g, sz * 4, cudaMemcpyDeviceToHost, e->stream));
     EDX_CUDA(cudaMemcpyAsync(hl.data(), c.slast.p + g, sz * 4, cudaMemcpyDeviceToHost, e->stream));
@@ -1208,6 +1344,8 @@ int edx_engine_import_snapshot(edx_engine* e, const uint32_t* ids, const uint64_
   return guard([&] {
     EDX_CUDA(cudaSetDevice(e->device));
     ++e->state_version;
+    const std::vector<uint32_t> slots = host_slots(e, ids, count, true);
+    ids = slots.data();
     EDX_CUDA(cudaMemsetAsync(e->ol.p, 0, e->id_space * sizeof(ulonglong2), e->stream));
     EDX_CUDA(cudaMemsetAsync(e->res.p, 0, e->id_space * sizeof(unsigned long long), e->stream));
     if (count) {
@@ -1248,6 +1386,11 @@ int edx_engine_import_state(edx_engine* e, uint64_t clock, uint64_t g_count, con
     EDX_CUDA(cudaSetDevice(e->device));
     EDX_CUDA(cudaStreamSynchronize(e->stream));
     edx::step_head_abandon(e);
+    // ids -> slots (hashed mode) before any table is cleared: growth copies them
+    const std::vector<uint32_t> gslots = host_slots(e, g_ids, g_count, true);
+    const std::vector<uint32_t> eslots = host_slots(e, e_ids, entry_off[n], true);
+    g_ids = gslots.data();
+    e_ids = eslots.data();
     auto& c = e->cache;
     // the global table (SimState::global_): zero, then the imported rows
     EDX_CUDA(cudaMemsetAsync(e->ol.p, 0, e->id_space * sizeof(ulonglong2), e->stream));
@@ -1255,6 +1398,8 @@ int edx_engine_import_state(edx_engine* e, uint64_t clock, uint64_t g_count, con
     const uint64_t cells = static_cast<uint64_t>(n) * e->id_space;
     k_fill_slots<<<grid_for(cells), kT, 0, e->stream>>>(c.slot_of.p, cells);
     EDX_LAUNCHED();
+    if (c.pin.p)  // pin stamps are iteration clocks: the imported clock may be lower
+      EDX_CUDA(cudaMemsetAsync(c.pin.p, 0, c.pin.n * sizeof(uint32_t), e->stream));
     DevBuf<int> status;
     status.ensure(8);
     EDX_CUDA(cudaMemsetAsync(status.p, 0, 8 * sizeof(int), e->stream));

@@ -5,6 +5,7 @@
 #include <vector>
 
 #include "edx_internal.cuh"
+#include "ids.h"
 
 namespace edx {
 
@@ -23,6 +24,7 @@ struct CacheState {
   DevBuf<uint32_t> size;     // n
   DevBuf<uint32_t> cur_mark; // n (current_mark_, cache.hpp:236)
   DevBuf<unsigned long long> at_cur;  // n (at_current_mark_, cache.hpp:237)
+  DevBuf<uint32_t> pin;      // n * capacity, large caches: iteration stamp of pinned entries
 };
 
 // Scratch of one SimState::step (sim.hpp:87-218).
@@ -43,12 +45,16 @@ struct StepScratch {
   DevBuf<int32_t> need_contrib;  // epoch-scan contribution
   DevBuf<uint32_t> ins_rank;     // insert ordinal within the worker
   DevBuf<unsigned long long> counters;  // per-worker counters + totals
-  DevBuf<uint64_t> cand_key, cand_key_sorted;  // victim candidates
-  DevBuf<uint32_t> cand_slot, cand_slot_sorted;
-  DevBuf<uint32_t> cand_count;   // n
-  DevBuf<uint32_t> cand_off;     // n + 1
+  DevBuf<uint32_t> cand_slot_sorted;  // victims per worker (sorted for small caches)
+  DevBuf<uint32_t> cand_count;   // victim ids
+  DevBuf<uint32_t> cand_off;     // worker list
   DevBuf<uint32_t> wscalars;     // per-worker scalars of the step
-  DevBuf<uint32_t> ranges;       // key-packing ranges
+  // large caches: the cooperative victim selection (k_big_select)
+  DevBuf<uint8_t> big_state;     // n BigState
+  DevBuf<uint32_t> big_hist;     // n * 4096
+  DevBuf<uint8_t> big_key[2];    // n * capacity 128-bit keys (undecided, ping-pong)
+  DevBuf<uint32_t> big_slot[2];  // n * capacity
+  uint64_t big_grid = 0;
   DevBuf<uint8_t> temp;          // CUB temp storage
   DevBuf<uint32_t> ucount;       // number of unique ids
 };
@@ -62,7 +68,18 @@ struct edx_engine {
   double alpha = 1.0;
   uint64_t capacity = 0, d_tran = 0;
   std::vector<double> bw, ucost_h;
+  // id_space = the slot count of the dense per-embedding tables.  Dense mode
+  // (created with id_space > 0): slot = id, ids must be < id_space.  Hashed
+  // mode (created with id_space 0): any uint32 id, mapped to a slot by the
+  // device id table (ids.cu) at the start of each iteration; the tables grow.
   uint64_t id_space = 0, max_ids = 0;
+  bool hashed = false;
+  edx::IdTable idt;
+  edx::DevBuf<uint32_t> kslots;        // the current batch as slots (hashed mode)
+  const uint32_t* cur_raw = nullptr;   // the current batch's ids as loaded
+  bool translated = true;
+  uint64_t used_bound = 0;             // >= slots in use (exact after each sync)
+  unsigned long long* h_used = nullptr;  // pinned copy of idt.count
   int rank = 0, world = 1;
   void* comm = nullptr;  // ncclComm_t when world > 1; rank 0 is the solver rank
   uint64_t clock = 0;

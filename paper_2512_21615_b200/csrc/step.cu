@@ -23,6 +23,7 @@
 // stable sort of (worker, position) keys, counts are integer atomics
 // (order-free), and the realised cost is summed on the host in worker order
 // (sim.hpp:208-216).
+#include <cooperative_groups.h>
 #include <cub/block/block_radix_sort.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
@@ -69,7 +70,10 @@ enum WS : int {
   kWsCandOff = 8,  // start of the worker's sorted candidates
   kWsInsBase = 9,  // exclusive insert-scan value at the worker's first item
   kWsConBase = 10, // exclusive contribution-scan value at the worker's first item
-  kWS = 11
+  kWsVa = 11,      // large caches: victims with version 0, mark != current
+  kWsVb = 12,      //   version 0, mark == current
+  kWsVc = 13,      //   version 1, mark != current (the rest: version 1, current)
+  kWS = 14
 };
 
 // Head of the step: zero the counters and per-worker scalars, map each id
@@ -228,7 +232,8 @@ __global__ void k_classify(const uint64_t* __restrict__ items,
                            const int32_t* __restrict__ slot_of, uint64_t capacity,
                            const uint32_t* __restrict__ smark, const uint32_t* __restrict__ cur_mark,
                            uint8_t* __restrict__ type, uint32_t* __restrict__ ins_flag,
-                           int32_t* __restrict__ contrib, unsigned long long* counters) {
+                           int32_t* __restrict__ contrib, unsigned long long* counters,
+                           uint32_t* __restrict__ pin, const uint32_t* __restrict__ clock_dev) {
   pdl_wait();
   pdl_trigger();
   __shared__ unsigned int miss[kMaxWorkers];
@@ -258,6 +263,8 @@ __global__ void k_classify(const uint64_t* __restrict__ items,
     if (t != 2) {
       const int32_t s = slot_of[static_cast<uint64_t>(j) * id_space + id];
       c = smark[static_cast<uint64_t>(j) * capacity + s] != cur_mark[j] ? 1 : 0;
+      // pinned for this iteration's victim selection (large caches)
+      if (pin) pin[static_cast<uint64_t>(j) * capacity + s] = *clock_dev + 1u;
     }
     type[q] = t;
     ins_flag[q] = t == 2 ? 1u : 0u;
@@ -287,127 +294,414 @@ __global__ void k_worker_inserts(int n, const uint32_t* __restrict__ ins_scan,
   (void)flags;
 }
 
-// --- victim candidates: non-pinned entries of evicting workers -----------
-// ranges[0..7] = {mark lo, mark hi, freq lo, freq hi, last lo, last hi, id lo, id hi}
-__device__ __forceinline__ bool pinned_by(int j, uint32_t id, const int32_t* first_pos,
-                                          const uint32_t* uidx, uint64_t ucap,
-                                          const int32_t* need_first) {
-  const int32_t fp = first_pos[id];
-  if (fp == INT_MAX) return false;
-  return need_first[static_cast<uint64_t>(j) * ucap + uidx[fp]] != INT_MAX;
+// --- victim selection for large caches (> kSelCap entries) ---------------
+// One cooperative kernel (grid-wide syncs, no host round trip, capturable in
+// the iteration's CUDA graph) selects, for every evicting worker j, its E_j
+// least VictimKeys among the non-pinned entries (cache.hpp:47-58) -- an MSB
+// radix select over the whole cache:
+//  * ranges: per-worker min/max of mark, frequency, last access and id over
+//    the candidates, so the key (version | mark | freq | last | id, each field
+//    minus its minimum) packs into W <= 128 bits, MSB-aligned in a 128-bit word;
+//  * level 0: a 4096-bin histogram of the key's top 12 bits (keys built from
+//    the entry fields); the bin holding the E_j-th key is found with a block
+//    scan; keys in lower bins are victims, keys in that bin stay undecided and
+//    are compacted (key, slot) for the next level unless the whole bin is
+//    needed; later levels run on the compacted keys only.
+// Keys are unique (they end in the id), so the victims are exactly the keys
+// <= the E_j-th.  They are written unsorted: the only order-dependent use,
+// the epoch scan's "does the t-th victim carry the current mark", follows
+// from four counts -- in key order the victims are [version 0, mark !=
+// current][version 0, mark == current][version 1, mark != current][version 1,
+// mark == current], since every mark is <= the current mark (a touch stamps
+// the current one, which only grows) -- so k_evict_contrib derives it from
+// kWsVa/kWsVb/kWsVc.  Pinned entries (needed by j this iteration) are the
+// ones k_classify stamped with the iteration's stamp.
+namespace big {
+constexpr int kThreads = 512;
+constexpr int kDigit = 12, kBins = 1 << kDigit;
+constexpr uint32_t kChunk = 4096;  // entries per work unit
+}  // namespace big
+
+typedef unsigned __int128 u128;
+
+// per-worker selection state (global)
+struct BigState {
+  uint32_t lo[4], hi[4];  // mark, frequency, last access, id over the candidates
+  uint32_t cand, need, bin, take_all, active, level, nv, pinned_err;
+  uint32_t vc[3];  // victims: version 0 non-current, version 0 current, version 1 non-current
+  uint32_t nu[2];  // undecided keys per ping-pong buffer
+  int w[5];        // field widths: version, mark, freq, last, id
+  int W;
+  uint32_t pad[2];
+};
+
+__device__ __forceinline__ uint32_t key_digit(u128 k, uint32_t level) {
+  const int sh = 128 - big::kDigit * static_cast<int>(level + 1);
+  return sh >= 0 ? static_cast<uint32_t>(k >> sh) & (big::kBins - 1)
+                 : (static_cast<uint32_t>(k) << (-sh)) & (big::kBins - 1);
 }
 
-__global__ void __launch_bounds__(256)
-    k_cand_ranges(const int32_t* __restrict__ wlist, int nw, uint64_t capacity,
-                  const uint32_t* __restrict__ ws, const uint32_t* __restrict__ sid,
-                  const uint32_t* __restrict__ smark, const uint32_t* __restrict__ sfreq,
-                  const uint32_t* __restrict__ slast, const int32_t* __restrict__ first_pos,
-                  const uint32_t* __restrict__ uidx, uint64_t ucap,
-                  const int32_t* __restrict__ need_first, uint32_t* __restrict__ ranges) {
-  // grid-stride, then a block reduction and one atomic per block and field
-  // (the candidates of every evicting worker -- millions at C4 -- would
-  // otherwise all hit the same eight words)
-  __shared__ uint32_t part[8][8];
-  uint32_t v[4] = {UINT_MAX, UINT_MAX, UINT_MAX, UINT_MAX}, V[4] = {0, 0, 0, 0};
-  const uint64_t total = static_cast<uint64_t>(nw) * capacity;
-  for (uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; x < total;
-       x += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const int jl = static_cast<int>(x / capacity);
-    const uint64_t s = x - static_cast<uint64_t>(jl) * capacity;
-    const int j = wlist[jl];
-    if (s >= ws[j * kWS + kWsSize0] || ws[j * kWS + kWsEvict] == 0) continue;
-    const uint64_t g = static_cast<uint64_t>(j) * capacity + s;
-    const uint32_t id = sid[g];
-    if (pinned_by(j, id, first_pos, uidx, ucap, need_first)) continue;
-    const uint32_t f[4] = {smark[g], sfreq[g], slast[g], id};
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      v[q] = min(v[q], f[q]);
-      V[q] = max(V[q], f[q]);
-    }
+__device__ __forceinline__ u128 victim_key(const BigState& st, uint32_t ver, uint32_t mark,
+                                           uint32_t freq, uint32_t last, uint32_t rid) {
+  u128 k = ver;
+  k = (k << st.w[1]) | (mark - st.lo[0]);
+  k = (k << st.w[2]) | (freq - st.lo[1]);
+  k = (k << st.w[3]) | (last - st.lo[2]);
+  k = (k << st.w[4]) | (rid - st.lo[3]);
+  return k << (128 - st.W);
+}
+
+// warp-aggregated append to a per-worker counter; every lane of `mask` calls it
+__device__ __forceinline__ uint32_t warp_append(uint32_t* ctr, bool take, unsigned mask) {
+  const unsigned bal = __ballot_sync(mask, take);
+  const int lane = threadIdx.x & 31, leader = __ffs(mask) - 1;
+  uint32_t base = 0;
+  if (lane == leader && bal) base = atomicAdd(ctr, static_cast<uint32_t>(__popc(bal)));
+  base = __shfl_sync(mask, base, leader);
+  return base + __popc(bal & ((1u << lane) - 1u));
+}
+
+struct BigArgs {
+  int n;
+  uint64_t capacity;
+  uint32_t* ws;
+  const uint32_t* sid;
+  const uint32_t* smark;
+  const uint32_t* sfreq;
+  const uint32_t* slast;
+  const uint32_t* pin;
+  const ulonglong2* ol;
+  const uint32_t* slot2id;
+  const uint32_t* cur_mark;
+  const uint32_t* clock_dev;
+  BigState* st;
+  uint32_t* hist;          // n * kBins
+  u128* ukey[2];           // n * capacity each
+  uint32_t* uslot[2];
+  uint32_t* victims;       // n * capacity: worker j's victims from j * capacity
+  int* flags;
+};
+
+// One candidate entry of worker j: its key (valid when the entry is a
+// non-pinned resident entry), version and current-mark flag.
+struct BigEntry {
+  bool cand;
+  uint32_t ver, mark, freq, last, rid;
+};
+
+__device__ __forceinline__ BigEntry big_entry(const BigArgs& a, int j, uint32_t s, uint32_t size0,
+                                              uint32_t stamp) {
+  BigEntry e{};
+  const uint64_t g = static_cast<uint64_t>(j) * a.capacity + s;
+  e.cand = s < size0 && a.pin[g] != stamp;
+  if (e.cand) {
+    const uint32_t slot = a.sid[g];
+    e.ver = static_cast<uint32_t>((a.ol[slot].y >> j) & 1ULL);
+    e.mark = a.smark[g];
+    e.freq = a.sfreq[g];
+    e.last = a.slast[g];
+    e.rid = a.slot2id ? a.slot2id[slot] : slot;
   }
+  return e;
+}
+
+// block-wide sum of two counters into shared memory
+__device__ void big_block_hist_flush(uint32_t* sh, uint32_t* gh) {
+  for (int b = threadIdx.x; b < big::kBins; b += blockDim.x) {
+    const uint32_t v = sh[b];
+    if (v) atomicAdd(gh + b, v);
+    sh[b] = 0;
+  }
+}
+
+// the bin holding the need-th key of worker j's histogram (block-wide)
+__device__ void big_select(const BigArgs& a, int j, uint32_t* scan_sh) {
+  BigState& st = a.st[j];
+  uint32_t* h = a.hist + static_cast<uint64_t>(j) * big::kBins;
+  constexpr int per = big::kBins / big::kThreads;  // 8 bins per thread
+  uint32_t v[per], sum = 0;
+#pragma unroll
+  for (int q = 0; q < per; ++q) {
+    v[q] = h[threadIdx.x * per + q];
+    h[threadIdx.x * per + q] = 0;  // ready for the next level
+    sum += v[q];
+  }
+  // block exclusive scan of the per-thread sums
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t inc = sum;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    v[q] = __reduce_min_sync(0xffffffffu, v[q]);
-    V[q] = __reduce_max_sync(0xffffffffu, V[q]);
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
   }
-  if (lane == 0)
+  if (lane == 31) scan_sh[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t x = lane < big::kThreads / 32 ? scan_sh[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane < big::kThreads / 32) scan_sh[32 + lane] = x - scan_sh[lane];
+  }
+  __syncthreads();
+  const uint32_t need = st.need;
+  uint32_t run = scan_sh[32 + warp] + inc - sum;  // exclusive prefix of this thread
+  if (run < need && need <= run + sum) {
+#pragma unroll
+    for (int q = 0; q < per; ++q) {
+      if (run + v[q] >= need) {
+        st.bin = threadIdx.x * per + q;
+        st.need = need - run;
+        st.take_all = (need - run == v[q]) ? 1u : 0u;
+        break;
+      }
+      run += v[q];
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(big::kThreads)
+    k_big_select(BigArgs a) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ uint32_t hsh[big::kBins];
+  __shared__ uint32_t red[big::kThreads / 32][9];
+  __shared__ uint32_t scan_sh[64];
+  const int n = a.n;
+  const uint32_t stamp = *a.clock_dev + 1u;
+  const uint32_t chunks = static_cast<uint32_t>((a.capacity + big::kChunk - 1) / big::kChunk);
+  const uint64_t gtid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int b = threadIdx.x; b < big::kBins; b += blockDim.x) hsh[b] = 0;
+
+  // ---- init
+  if (gtid < static_cast<uint64_t>(n)) {
+    BigState& st = a.st[gtid];
+    const uint32_t* w = a.ws + gtid * kWS;
+    for (int q = 0; q < 4; ++q) {
+      st.lo[q] = UINT_MAX;
+      st.hi[q] = 0;
+    }
+    st.cand = st.nv = st.level = st.bin = st.take_all = st.pinned_err = 0;
+    st.vc[0] = st.vc[1] = st.vc[2] = 0;
+    st.nu[0] = st.nu[1] = 0;
+    st.need = w[kWsEvict];
+    st.active = w[kWsEvict] > 0 ? 1u : 0u;
+  }
+  for (uint64_t x = gtid; x < static_cast<uint64_t>(n) * big::kBins;
+       x += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    a.hist[x] = 0;
+  grid.sync();
+
+  // ---- ranges of the candidates' fields
+  for (uint32_t u = blockIdx.x; u < static_cast<uint32_t>(n) * chunks; u += gridDim.x) {
+    const int j = static_cast<int>(u / chunks);
+    if (!a.st[j].active) continue;
+    const uint32_t size0 = a.ws[j * kWS + kWsSize0], base = (u % chunks) * big::kChunk;
+    if (base >= size0) continue;
+    uint32_t v[9] = {UINT_MAX, UINT_MAX, UINT_MAX, UINT_MAX, 0, 0, 0, 0, 0};
+    for (uint32_t s = base + threadIdx.x; s < base + big::kChunk && s < size0; s += blockDim.x) {
+      const BigEntry e = big_entry(a, j, s, size0, stamp);
+      if (!e.cand) continue;
+      const uint32_t f[4] = {e.mark, e.freq, e.last, e.rid};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        v[q] = min(v[q], f[q]);
+        v[4 + q] = max(v[4 + q], f[q]);
+      }
+      ++v[8];
+    }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      part[warp][2 * q] = v[q];
-      part[warp][2 * q + 1] = V[q];
+      v[q] = __reduce_min_sync(0xffffffffu, v[q]);
+      v[4 + q] = __reduce_max_sync(0xffffffffu, v[4 + q]);
     }
-  __syncthreads();
-  if (threadIdx.x < 8) {
-    const int f = threadIdx.x;
-    uint32_t r = (f & 1) ? 0u : UINT_MAX;
-    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w)
-      r = (f & 1) ? max(r, part[w][f]) : min(r, part[w][f]);
-    if ((f & 1) ? r != 0u : r != UINT_MAX) {
-      if (f & 1) atomicMax(ranges + f, r);
-      else atomicMin(ranges + f, r);
+    v[8] = __reduce_add_sync(0xffffffffu, v[8]);
+    if (lane == 0)
+#pragma unroll
+      for (int q = 0; q < 9; ++q) red[warp][q] = v[q];
+    __syncthreads();
+    if (threadIdx.x < 9) {
+      const int q = threadIdx.x;
+      uint32_t r = q < 4 ? UINT_MAX : 0u;
+      for (int x = 0; x < big::kThreads / 32; ++x)
+        r = q < 4 ? min(r, red[x][q]) : (q < 8 ? max(r, red[x][q]) : r + red[x][q]);
+      BigState& st = a.st[j];
+      if (q < 4) {
+        if (r != UINT_MAX) atomicMin(&st.lo[q], r);
+      } else if (q < 8) {
+        if (r) atomicMax(&st.hi[q - 4], r);
+      } else if (r) {
+        atomicAdd(&st.cand, r);
+      }
     }
+    __syncthreads();
+  }
+  grid.sync();
+
+  // ---- field widths (every block keeps its own copy in the state it reads)
+  if (gtid < static_cast<uint64_t>(n)) {
+    BigState& st = a.st[gtid];
+    if (st.active) {
+      st.w[0] = 1;
+      int W = 1;
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t span = st.hi[q] > st.lo[q] ? st.hi[q] - st.lo[q] : 0u;
+        st.w[1 + q] = span ? 32 - __clz(span) : 0;
+        W += st.w[1 + q];
+      }
+      st.W = W;
+      if (st.cand < st.need) {  // every remaining entry is pinned (cache.hpp:164)
+        st.pinned_err = 1;
+        atomicOr(a.flags + kFlagPinned, 1);
+        st.active = 0;
+      } else if (W > 128) {  // only reachable at ~2^32 epochs
+        atomicOr(a.flags + kFlagKeyRange, 1);
+        st.active = 0;
+      }
+    }
+  }
+  grid.sync();
+
+  // ---- radix select, level by level
+  for (uint32_t level = 0;; ++level) {
+    // any worker still selecting?  (uniform: every block reads the same state)
+    bool any = false;
+    for (int j = 0; j < n; ++j) any |= a.st[j].active != 0;
+    if (!any) break;
+    const int in = (level + 1) & 1, out = level & 1;  // U buffers: level L reads in, writes out
+    // histogram of this level's digit
+    if (level == 0) {
+      for (uint32_t u = blockIdx.x; u < static_cast<uint32_t>(n) * chunks; u += gridDim.x) {
+        const int j = static_cast<int>(u / chunks);
+        const BigState& st = a.st[j];
+        if (!st.active) continue;
+        const uint32_t size0 = a.ws[j * kWS + kWsSize0], base = (u % chunks) * big::kChunk;
+        if (base >= size0) continue;
+        for (uint32_t s = base + threadIdx.x; s < base + big::kChunk && s < size0; s += blockDim.x) {
+          const BigEntry e = big_entry(a, j, s, size0, stamp);
+          if (e.cand)
+            atomicAdd(&hsh[key_digit(victim_key(st, e.ver, e.mark, e.freq, e.last, e.rid), 0)], 1u);
+        }
+        __syncthreads();
+        big_block_hist_flush(hsh, a.hist + static_cast<uint64_t>(j) * big::kBins);
+        __syncthreads();
+      }
+    } else {
+      for (int j = 0; j < n; ++j) {
+        const BigState& st = a.st[j];
+        if (!st.active) continue;
+        const uint32_t cnt = st.nu[in];
+        const uint32_t units = (cnt + big::kChunk - 1) / big::kChunk;
+        const u128* K = a.ukey[in] + static_cast<uint64_t>(j) * a.capacity;
+        for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
+          const uint32_t base = u * big::kChunk;
+          for (uint32_t t = base + threadIdx.x; t < base + big::kChunk && t < cnt; t += blockDim.x)
+            atomicAdd(&hsh[key_digit(K[t], level)], 1u);
+          __syncthreads();
+          big_block_hist_flush(hsh, a.hist + static_cast<uint64_t>(j) * big::kBins);
+          __syncthreads();
+        }
+      }
+    }
+    grid.sync();
+    // the bin of each worker's need-th key
+    for (int j = blockIdx.x; j < n; j += gridDim.x) {
+      if (!a.st[j].active) continue;
+      big_select(a, j, scan_sh);
+      if (threadIdx.x == 0) a.st[j].nu[out] = 0;
+    }
+    grid.sync();
+    // compaction: lower bins are victims, the bin itself is undecided
+    // (unless it is taken whole), higher bins drop out
+    auto place = [&](const BigState& stc, BigState& st, int j, bool live, u128 key, uint32_t slot,
+                     uint32_t ver, bool cur, unsigned mask) {
+      const uint32_t d = live ? key_digit(key, level) : 0u;
+      const bool victim = live && (d < stc.bin || (d == stc.bin && stc.take_all));
+      const bool undecided = live && d == stc.bin && !stc.take_all;
+      const uint32_t vi = warp_append(&st.nv, victim, mask);
+      if (victim) {
+        a.victims[static_cast<uint64_t>(j) * a.capacity + vi] = slot;
+        if (!(ver == 1 && cur)) atomicAdd(&st.vc[ver ? 2 : (cur ? 1 : 0)], 1u);
+      }
+      const uint32_t ui = warp_append(&st.nu[out], undecided, mask);
+      if (undecided) {
+        a.ukey[out][static_cast<uint64_t>(j) * a.capacity + ui] = key;
+        a.uslot[out][static_cast<uint64_t>(j) * a.capacity + ui] = slot;
+      }
+    };
+    if (level == 0) {
+      for (uint32_t u = blockIdx.x; u < static_cast<uint32_t>(n) * chunks; u += gridDim.x) {
+        const int j = static_cast<int>(u / chunks);
+        BigState& st = a.st[j];
+        if (!st.active) continue;
+        const BigState stc = st;
+        const uint32_t size0 = a.ws[j * kWS + kWsSize0], base = (u % chunks) * big::kChunk;
+        if (base >= size0) continue;
+        const uint32_t cm = a.cur_mark[j];
+        for (uint32_t s0 = base; s0 < base + big::kChunk && s0 < size0; s0 += blockDim.x) {
+          const uint32_t s = s0 + threadIdx.x;
+          const bool in_range = s < base + big::kChunk && s < size0;
+          const unsigned mask = __ballot_sync(0xffffffffu, in_range);
+          if (!in_range) continue;
+          const BigEntry e = big_entry(a, j, s, size0, stamp);
+          const u128 key = e.cand ? victim_key(stc, e.ver, e.mark, e.freq, e.last, e.rid) : u128(0);
+          place(stc, st, j, e.cand, key, s, e.ver, e.mark == cm, mask);
+        }
+      }
+    } else {
+      for (int j = 0; j < n; ++j) {
+        BigState& st = a.st[j];
+        if (!st.active) continue;
+        const BigState stc = st;
+        const uint32_t cnt = stc.nu[in];
+        const uint32_t units = (cnt + big::kChunk - 1) / big::kChunk;
+        const uint64_t gb = static_cast<uint64_t>(j) * a.capacity;
+        const uint32_t cm = a.cur_mark[j];
+        for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
+          const uint32_t base = u * big::kChunk;
+          for (uint32_t t0 = base; t0 < base + big::kChunk && t0 < cnt; t0 += blockDim.x) {
+            const uint32_t t = t0 + threadIdx.x;
+            const bool live = t < base + big::kChunk && t < cnt;
+            const unsigned mask = __ballot_sync(0xffffffffu, live);
+            if (!live) continue;
+            const u128 key = a.ukey[in][gb + t];
+            const uint32_t slot = a.uslot[in][gb + t];
+            const uint32_t ver = static_cast<uint32_t>(key >> 127);
+            const bool cur = a.smark[gb + slot] == cm;
+            place(stc, st, j, true, key, slot, ver, cur, mask);
+          }
+        }
+      }
+    }
+    grid.sync();
+    if (gtid < static_cast<uint64_t>(n)) {
+      BigState& st = a.st[gtid];
+      if (st.active && (st.take_all || level >= (128 + big::kDigit - 1) / big::kDigit - 1)) {
+        if (!st.take_all) atomicOr(a.flags + kFlagInternal, 1);  // unique keys: unreachable
+        st.active = 0;
+      }
+    }
+    grid.sync();
+  }
+
+  // ---- results in the per-worker scalars
+  if (gtid < static_cast<uint64_t>(n)) {
+    const BigState& st = a.st[gtid];
+    uint32_t* w = a.ws + gtid * kWS;
+    w[kWsCand] = w[kWsEvict] > 0 ? (st.pinned_err ? st.cand : w[kWsEvict]) : 0u;
+    w[kWsCandOff] = static_cast<uint32_t>(gtid * a.capacity);
+    w[kWsVa] = st.vc[0];
+    w[kWsVb] = st.vc[1];
+    w[kWsVc] = st.vc[2];
   }
 }
 
 __device__ __forceinline__ int width_of(uint32_t lo, uint32_t hi) {
   return hi > lo ? 32 - __clz(hi - lo) : 0;
-}
-
-// VictimKey (cache.hpp:47-58) = (version, mark, frequency, last_access, id),
-// packed order-preservingly into kw = 1 + wm + wf + wl + wi bits (widths of the
-// candidates' value ranges, computed on the host from k_cand_ranges) below the
-// evicting worker's list index; non-candidates are all ones and sort last.
-__global__ void __launch_bounds__(256)
-    k_cand_pack(const int32_t* __restrict__ wlist, int nw, uint64_t capacity,
-                uint32_t* __restrict__ ws, const uint32_t* __restrict__ sid,
-                const uint32_t* __restrict__ smark, const uint32_t* __restrict__ sfreq,
-                const uint32_t* __restrict__ slast, const ulonglong2* __restrict__ ol,
-                const int32_t* __restrict__ first_pos, const uint32_t* __restrict__ uidx,
-                uint64_t ucap, const int32_t* __restrict__ need_first,
-                const uint32_t* __restrict__ ranges, int wm, int wf, int wl, int wi,
-                uint64_t* __restrict__ keys, uint32_t* __restrict__ slots) {
-  __shared__ uint32_t cnt[kMaxWorkers];
-  if (threadIdx.x < kMaxWorkers) cnt[threadIdx.x] = 0;
-  __syncthreads();
-  const int kw = 1 + wm + wf + wl + wi;
-  const uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  if (x < static_cast<uint64_t>(nw) * capacity) {
-    const int jl = static_cast<int>(x / capacity);
-    const uint64_t s = x - static_cast<uint64_t>(jl) * capacity;
-    const int j = wlist[jl];
-    uint64_t key = ~0ULL;
-    if (s < ws[j * kWS + kWsSize0] && ws[j * kWS + kWsEvict] != 0) {
-      const uint64_t g = static_cast<uint64_t>(j) * capacity + s;
-      const uint32_t id = sid[g];
-      if (!pinned_by(j, id, first_pos, uidx, ucap, need_first)) {
-        uint64_t k = (ol[id].y >> j) & 1ULL;  // version: a stale copy goes first
-        k = (k << wm) | (smark[g] - ranges[0]);
-        k = (k << wf) | (sfreq[g] - ranges[2]);
-        k = (k << wl) | (slast[g] - ranges[4]);
-        k = (k << wi) | (id - ranges[6]);
-        key = (static_cast<uint64_t>(jl) << kw) | k;
-        atomicAdd(&cnt[jl], 1u);
-      }
-    }
-    keys[x] = key;
-    slots[x] = static_cast<uint32_t>(s);
-  }
-  __syncthreads();
-  if (threadIdx.x < nw && cnt[threadIdx.x]) atomicAdd(ws + wlist[threadIdx.x] * kWS + kWsCand, cnt[threadIdx.x]);
-}
-
-__global__ void k_cand_offsets(const int32_t* __restrict__ wlist, int nw, uint32_t* __restrict__ ws,
-                               int* __restrict__ flags) {
-  if (threadIdx.x != 0) return;
-  uint32_t run = 0;
-  for (int jl = 0; jl < nw; ++jl) {
-    uint32_t* w = ws + wlist[jl] * kWS;
-    w[kWsCandOff] = run;
-    run += w[kWsCand];
-    if (w[kWsCand] < w[kWsEvict]) atomicOr(flags + kFlagPinned, 1);
-  }
 }
 
 // Victim selection for caches of up to kSelCap entries: one CTA per worker.
@@ -427,6 +721,7 @@ __global__ void __launch_bounds__(kSelThreads, 1)
     k_select_victims(uint64_t capacity, uint32_t* __restrict__ ws, const uint32_t* __restrict__ sid,
                      const uint32_t* __restrict__ smark, const uint32_t* __restrict__ sfreq,
                      const uint32_t* __restrict__ slast, const ulonglong2* __restrict__ ol,
+                     const uint32_t* __restrict__ slot2id,
                      const int32_t* __restrict__ first_pos, const uint32_t* __restrict__ uidx,
                      uint64_t ucap, const int32_t* __restrict__ need_first,
                      const uint32_t* __restrict__ ins_scan,
@@ -486,7 +781,9 @@ __global__ void __launch_bounds__(kSelThreads, 1)
     for (int k = 0; k < kSelItems; ++k) {
       if (cf[k]) {
         const uint32_t sl = tid * kSelItems + k;
-        const uint32_t f[4] = {smark[gb + sl], sfreq[gb + sl], slast[gb + sl], id[k]};
+        // VictimKey's id is the embedding id (slot2id in hashed-id engines)
+        const uint32_t rid = slot2id ? slot2id[id[k]] : id[k];
+        const uint32_t f[4] = {smark[gb + sl], sfreq[gb + sl], slast[gb + sl], rid};
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           v[q] = min(v[q], f[q]);
@@ -532,11 +829,12 @@ __global__ void __launch_bounds__(kSelThreads, 1)
     keys[k] = 1ULL << W;  // not a candidate: after every candidate
     if (cf[k]) {
       const uint32_t id = sid[gb + sl];
+      const uint32_t rid = slot2id ? slot2id[id] : id;
       uint64_t key = (ol[id].y >> j) & 1ULL;  // version: a stale copy goes first
       key = (key << wm) | (smark[gb + sl] - tot[0]);
       key = (key << wf) | (sfreq[gb + sl] - tot[1]);
       key = (key << wl) | (slast[gb + sl] - tot[2]);
-      key = (key << wi) | (id - tot[3]);
+      key = (key << wi) | (rid - tot[3]);
       keys[k] = key;
     }
   }
@@ -634,9 +932,6 @@ __global__ void __launch_bounds__(kSelThreads, 1)
   }
 }
 
-__global__ void k_init_ranges(uint32_t* __restrict__ ranges) {
-  if (threadIdx.x < 8) ranges[threadIdx.x] = (threadIdx.x & 1) ? 0u : UINT_MAX;
-}
 
 // evicting insert contribution: +1 for the insert, -1 if its victim carries
 // the current mark (cache.hpp:111,175), evaluated before any advance.
@@ -645,7 +940,8 @@ __global__ void k_evict_contrib(const uint64_t* __restrict__ items,
                                 const uint8_t* __restrict__ type, const uint32_t* __restrict__ ins_scan,
                                 const uint32_t* __restrict__ ws, const uint32_t* __restrict__ cand_slot,
                                 const uint32_t* __restrict__ smark, uint64_t capacity,
-                                const uint32_t* __restrict__ cur_mark, int32_t* __restrict__ contrib) {
+                                const uint32_t* __restrict__ cur_mark, int by_counts,
+                                int32_t* __restrict__ contrib) {
   pdl_wait();
   pdl_trigger();
   const uint64_t N = counters_ro[3 * n + 2];
@@ -657,8 +953,15 @@ __global__ void k_evict_contrib(const uint64_t* __restrict__ items,
   if (e < w[kWsFree]) return;
   const uint32_t t = e - w[kWsFree];
   if (t >= w[kWsCand]) return;  // reported through kFlagPinned
-  const uint32_t vs = cand_slot[w[kWsCandOff] + t];
-  contrib[q] = smark[static_cast<uint64_t>(j) * capacity + vs] == cur_mark[j] ? 0 : 1;
+  bool cur;
+  if (by_counts) {  // unsorted victims of a large cache: the class of the t-th
+    const uint32_t a = w[kWsVa], b = a + w[kWsVb], c = b + w[kWsVc];
+    cur = (t >= a && t < b) || t >= c;
+  } else {
+    const uint32_t vs = cand_slot[w[kWsCandOff] + t];
+    cur = smark[static_cast<uint64_t>(j) * capacity + vs] == cur_mark[j];
+  }
+  contrib[q] = cur ? 0 : 1;
 }
 
 // maybe_advance_mark (cache.hpp:187-192) at the first evicting insert whose
@@ -849,6 +1152,17 @@ __global__ void k_fill_i32(int32_t* p, uint64_t n, int32_t v) {
   if (x < n) p[x] = v;
 }
 
+// The one-CTA-per-worker selection (sorted victims, keys <= 63 bits) for
+// caches of <= kSelCap entries: EDX_VICTIMS=cta (A/B measurement only; the
+// cooperative selection handles every size and key width).
+bool use_cta_select(const edx_engine* e) {
+  static const bool cta = [] {
+    const char* v = std::getenv("EDX_VICTIMS");
+    return v && std::strcmp(v, "cta") == 0;
+  }();
+  return cta && e->capacity <= kSelCap;
+}
+
 }  // namespace
 
 void step_init_state(edx_engine* e) {
@@ -894,22 +1208,25 @@ void step_init_state(edx_engine* e) {
   s.ins_rank.ensure(T + 1);
   s.counters.ensure(3 * n + 4);
   s.wscalars.ensure(n * kWS);
-  s.ranges.ensure(8);
-  // victim candidates of every worker (a worker with no evictions skips its share)
+  // victims of every worker (a worker with no evictions skips its share)
   const uint64_t cand = n * e->capacity;
   s.cand_slot_sorted.ensure(cand);
   s.cand_count.ensure(cand);  // the victim-id list
-  if (e->capacity > kSelCap) {
-    s.cand_key.ensure(cand);
-    s.cand_key_sorted.ensure(cand);
-    s.cand_slot.ensure(cand);
-    // the device-wide victim sort's scratch, sized once here: growing it at
-    // the first evicting step would cost a free + malloc inside the loop
-    size_t bytes = 0;
-    EDX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, s.cand_key.p, s.cand_key_sorted.p,
-                                             s.cand_slot.p, s.cand_slot_sorted.p,
-                                             static_cast<int>(cand), 0, 64, e->stream));
-    s.temp.ensure(bytes);
+  if (!use_cta_select(e)) {
+    // pin stamps per entry and the cooperative selection's scratch
+    c.pin.ensure(cand);
+    EDX_CUDA(cudaMemsetAsync(c.pin.p, 0, cand * sizeof(uint32_t), e->stream));
+    s.big_state.ensure(n * sizeof(BigState));
+    s.big_hist.ensure(n * big::kBins);
+    for (int b = 0; b < 2; ++b) {
+      s.big_key[b].ensure(cand * sizeof(u128));
+      s.big_slot[b].ensure(cand);
+    }
+    int per_sm = 0, sms = 0;
+    EDX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_big_select, big::kThreads, 0));
+    EDX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device));
+    if (per_sm < 1) throw Error(EDX_CUDA_ERROR, "victim selection kernel cannot be resident");
+    s.big_grid = static_cast<uint64_t>(std::min(per_sm, 2)) * static_cast<uint64_t>(sms);
   }
   s.cand_off.ensure(128);  // [0,64): workers 0..n-1; [64,128): evicting workers (large caches)
   std::vector<int32_t> wl(n);
@@ -917,7 +1234,7 @@ void step_init_state(edx_engine* e) {
   EDX_CUDA(cudaMemcpyAsync(s.cand_off.p, wl.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice,
                            e->stream));
   EDX_CUDA(cudaStreamSynchronize(e->stream));
-  if (e->capacity <= kSelCap) {
+  if (use_cta_select(e)) {
     static const size_t sel_smem =
         std::max(sizeof(typename SelSort::TempStorage),
                  256 * sizeof(uint32_t) + kSelSmall * (sizeof(uint64_t) + sizeof(uint32_t)));
@@ -939,7 +1256,7 @@ void cub_call(edx_engine* e, F&& f) {
 
 }  // namespace
 
-bool step_device_only(const edx_engine* e) { return e->capacity <= kSelCap; }
+bool step_device_only(const edx_engine*) { return true; }
 
 namespace {
 
@@ -1026,7 +1343,8 @@ void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
   launch_pdl(k_classify, grid_for(T + 1), kT, 0, st, 
       s.need_key_sorted.p, s.counters.p, n, e->cur_ids, s.first_pos.p, s.uidx_of_pos.p, ucap,
       s.need_cnt.p, e->ol.p, e->res.p, e->id_space, c.slot_of.p, e->capacity, c.smark.p,
-      c.cur_mark.p, s.need_type.p, s.flag_scan.p, s.need_contrib.p, s.counters.p);
+      c.cur_mark.p, s.need_type.p, s.flag_scan.p, s.need_contrib.p, s.counters.p,
+      use_cta_select(e) ? nullptr : c.pin.p, e->d_clock.p);
   EDX_LAUNCHED();
   launches += 2;
   // insert ordinals: exclusive scan over the (worker-grouped) need items
@@ -1035,7 +1353,7 @@ void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
                                          static_cast<int>(T + 1), st);
   });
   launches += 2;
-  if (e->capacity > kSelCap) {
+  if (!use_cta_select(e)) {
     k_worker_inserts<<<1, 64, 0, st>>>(n, s.ins_rank.p, s.wscalars.p, e->flags.p);
     EDX_LAUNCHED();
     launches += 1;
@@ -1045,67 +1363,55 @@ void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
   // workers without evictions drop out on the device.
   const int32_t* d_wlist = reinterpret_cast<const int32_t*>(s.cand_off.p);
   int nw = n;  // workers the victim kernels visit
-  if (e->capacity <= kSelCap) {
+  if (use_cta_select(e)) {
     launch_pdl(k_select_victims, n, kSelThreads, sizeof(typename SelSort::TempStorage), st, 
         e->capacity, s.wscalars.p, c.sid.p, c.smark.p, c.sfreq.p, c.slast.p, e->ol.p,
+        e->hashed ? e->idt.slot2id.p : nullptr,
         s.first_pos.p, s.uidx_of_pos.p, ucap, s.need_first.p, s.ins_rank.p, s.cand_slot_sorted.p,
         e->flags.p);
     EDX_LAUNCHED();
     launches += 1;
   } else {
-    // Large caches: the device-wide sort is sized by the host, so fetch E_j
-    // (one mid-step sync) and sort only the candidates of evicting workers
-    // (none while the caches are still filling).
-    std::vector<uint32_t> ws(static_cast<size_t>(n) * kWS);
-    EDX_CUDA(cudaMemcpyAsync(ws.data(), s.wscalars.p, ws.size() * sizeof(uint32_t),
-                             cudaMemcpyDeviceToHost, st));
-    EDX_CUDA(cudaStreamSynchronize(st));
-    std::vector<int32_t> wl;
-    for (int j = 0; j < n; ++j)
-      if (ws[j * kWS + kWsEvict] > 0) wl.push_back(j);
-    nw = static_cast<int>(wl.size());
-    if (nw > 0) {
-      int32_t* d_wl = reinterpret_cast<int32_t*>(s.cand_off.p) + 64;
-      EDX_CUDA(cudaMemcpyAsync(d_wl, wl.data(), nw * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-      const uint64_t cand = static_cast<uint64_t>(nw) * e->capacity;
-      k_init_ranges<<<1, 32, 0, st>>>(s.ranges.p);
-      const unsigned rgrid = static_cast<unsigned>(std::min<uint64_t>(grid_for(cand), 148ull * 8));
-      k_cand_ranges<<<rgrid, kT, 0, st>>>(d_wl, nw, e->capacity, s.wscalars.p, c.sid.p, c.smark.p,
-                                         c.sfreq.p, c.slast.p, s.first_pos.p, s.uidx_of_pos.p, ucap,
-                                         s.need_first.p, s.ranges.p);
-      EDX_LAUNCHED();
-      // key widths on the host (this path already synchronised once): the
-      // sort then covers only the key bits and the worker-index bits
-      uint32_t rg[8];
-      EDX_CUDA(cudaMemcpyAsync(rg, s.ranges.p, sizeof rg, cudaMemcpyDeviceToHost, st));
-      EDX_CUDA(cudaStreamSynchronize(st));
-      auto width = [](uint32_t lo, uint32_t hi) { return hi > lo ? 32 - __builtin_clz(hi - lo) : 0; };
-      const int wm = width(rg[0], rg[1]), wf = width(rg[2], rg[3]);
-      const int wl = width(rg[4], rg[5]), wi = width(rg[6], rg[7]);
-      const int kw = 1 + wm + wf + wl + wi;
-      int wb = 1;  // worker-index bits, one spare so a real key never equals all ones
-      while ((1 << (wb - 1)) < nw) ++wb;
-      if (kw + wb > 64) throw Error(EDX_RUNTIME_ERROR, "victim key fields exceed the 64-bit device packing");
-      k_cand_pack<<<grid_for(cand), kT, 0, st>>>(d_wl, nw, e->capacity, s.wscalars.p, c.sid.p,
-                                                 c.smark.p, c.sfreq.p, c.slast.p, e->ol.p,
-                                                 s.first_pos.p, s.uidx_of_pos.p, ucap,
-                                                 s.need_first.p, s.ranges.p, wm, wf, wl, wi,
-                                                 s.cand_key.p, s.cand_slot.p);
-      EDX_LAUNCHED();
-      cub_call(e, [&](void* tmp, size_t& b) {
-        return cub::DeviceRadixSort::SortPairs(tmp, b, s.cand_key.p, s.cand_key_sorted.p,
-                                               s.cand_slot.p, s.cand_slot_sorted.p,
-                                               static_cast<int>(cand), 0, kw + wb, st);
-      });
-      k_cand_offsets<<<1, 32, 0, st>>>(d_wl, nw, s.wscalars.p, e->flags.p);
-      EDX_LAUNCHED();
-      launches += 4 + 8;
-    }
+    // One cooperative kernel selects every evicting worker's victims on the
+    // device (k_big_select); no host round trip, any key width.
+    BigArgs ba;
+    ba.n = n;
+    ba.capacity = e->capacity;
+    ba.ws = s.wscalars.p;
+    ba.sid = c.sid.p;
+    ba.smark = c.smark.p;
+    ba.sfreq = c.sfreq.p;
+    ba.slast = c.slast.p;
+    ba.pin = c.pin.p;
+    ba.ol = e->ol.p;
+    ba.slot2id = e->hashed ? e->idt.slot2id.p : nullptr;
+    ba.cur_mark = c.cur_mark.p;
+    ba.clock_dev = e->d_clock.p;
+    ba.st = reinterpret_cast<BigState*>(s.big_state.p);
+    ba.hist = s.big_hist.p;
+    ba.ukey[0] = reinterpret_cast<u128*>(s.big_key[0].p);
+    ba.ukey[1] = reinterpret_cast<u128*>(s.big_key[1].p);
+    ba.uslot[0] = s.big_slot[0].p;
+    ba.uslot[1] = s.big_slot[1].p;
+    ba.victims = s.cand_slot_sorted.p;
+    ba.flags = e->flags.p;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(s.big_grid));
+    cfg.blockDim = dim3(big::kThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    EDX_CUDA(cudaLaunchKernelEx(&cfg, k_big_select, ba));
+    launches += 1;
   }
   launch_pdl(k_evict_contrib, grid_for(T), kT, 0, st, s.need_key_sorted.p, s.counters.p, n, s.need_type.p,
                                               s.ins_rank.p, s.wscalars.p, s.cand_slot_sorted.p,
                                               c.smark.p, e->capacity, c.cur_mark.p,
-                                              s.need_contrib.p);
+                                              use_cta_select(e) ? 0 : 1, s.need_contrib.p);
   EDX_LAUNCHED();
   cub_call(e, [&](void* tmp, size_t& b) {
     return cub::DeviceScan::ExclusiveSum(tmp, b, s.need_contrib.p,
@@ -1115,7 +1421,7 @@ void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
   const int32_t* con_scan = reinterpret_cast<const int32_t*>(s.flag_scan.p);
   {
     const unsigned ga = grid_for(T);
-    const int32_t* wlv = e->capacity <= kSelCap ? d_wlist : d_wlist + 64;
+    const int32_t* wlv = d_wlist;
     launch_pdl(k_advance_evict, ga + kEvictBlocks * static_cast<unsigned>(nw), kT, 0, st, 
         ga, s.need_key_sorted.p, s.counters.p, n, s.need_type.p, s.ins_rank.p, con_scan,
         s.wscalars.p, c.at_cur.p, e->capacity, wlv, s.cand_slot_sorted.p, c.sid.p, e->id_space,
@@ -1137,7 +1443,7 @@ void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
   EDX_CUDA(cudaMemcpyAsync(e->h_counters, s.counters.p, (3 * n + 4) * sizeof(unsigned long long),
                            cudaMemcpyDeviceToHost, st));
   out->launches = launches;
-  out->evicting_workers = e->capacity <= kSelCap ? -1 : nw;  // -1: decided on the device
+  out->evicting_workers = -1;  // decided on the device
 }
 
 }  // namespace edx

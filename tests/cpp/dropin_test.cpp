@@ -254,7 +254,76 @@ static void worker_cache_kats() {
   EXPECT(pr.entries().size() == 2, "entries()");
 }
 
+// acceptance.cpp:196-218 (criterion 4's loop) verbatim in shape: the
+// reference's ExperimentConfig::defaults() cluster (config.hpp:149-163: 8
+// workers 4x5 + 4x0.5 Gbps, m = 128, 8% of 50,000 ids cached, Zipf(1.05), 26
+// ids, 200 iterations, seed 42) for the five mechanisms, each iteration's
+// decision and report checked against the oracle simulator driven with the
+// same decision (the acceptance binary itself times this loop against a 60 s
+// limit that its CPU replay oracle alone exceeds; this isolates equivalence).
+static void acceptance_default_loop() {
+  ClusterConfig cfg;
+  cfg.n = 8;
+  cfg.m = 128;
+  cfg.bandwidths_bps = {5e9, 5e9, 5e9, 5e9, 5e8, 5e8, 5e8, 5e8};
+  cfg.d_tran_bytes = 512 * 4;
+  cfg.alpha = 1.0;
+  WorkloadSpec spec;
+  cfg.cache_capacity = static_cast<std::size_t>(0.08 * static_cast<double>(spec.total_embeddings));
+  const char* names[] = {"ecomix:1", "ecomix:0.5", "ecomix:0", "random", "hitgreedy"};
+  for (const char* name : names) {
+    const Mechanism mech = Mechanism::parse(name);
+    SimState engine(cfg);  // the reference's constructor: any uint32 id
+    orc_cluster_config oc{cfg.n, cfg.m, cfg.bandwidths_bps.data(), cfg.n, 0, cfg.d_tran_bytes,
+                          cfg.cache_capacity, mech.alpha};
+    orc_sim* oracle = nullptr;
+    orc_sim_create(&oc, &oracle);
+    ZipfStream stream(spec, cfg);
+    std::vector<EmbeddingSample> samples;
+    std::uint64_t iter = 0;
+    int bad = 0;
+    while (stream.next_iteration(samples)) {
+      Snapshot snap;
+      CostMatrix matrix;
+      if (mech.needs_snapshot()) snap = engine.snapshot();
+      if (mech.needs_matrix()) matrix = build_matrix(samples, snap, cfg);
+      const DispatchDecision decision =
+          dispatch_with(mech, samples, snap, matrix, cfg, iter, spec.seed);
+      const IterationReport rep = engine.step(samples, decision);
+      std::vector<uint32_t> ids;
+      std::vector<uint64_t> offs{0};
+      for (auto& x : samples) {
+        ids.insert(ids.end(), x.ids.begin(), x.ids.end());
+        offs.push_back(ids.size());
+      }
+      std::vector<int32_t> od(samples.size());
+      if (mech.kind == Mechanism::Kind::kEcoMix) {
+        std::vector<double> om(samples.size() * cfg.n);
+        orc_sim_build_matrix(oracle, ids.data(), offs.data(), samples.size(), om.data());
+        bad += std::memcmp(om.data(), matrix.values.data(), om.size() * 8) != 0;
+        orc_ecomix(&oc, samples.size(), cfg.n, om.data(), nullptr, od.data());
+      } else if (mech.kind == Mechanism::Kind::kHitGreedy) {
+        orc_sim_hitgreedy(oracle, ids.data(), offs.data(), samples.size(), od.data());
+      } else {
+        od.assign(decision.worker_of_sample.begin(), decision.worker_of_sample.end());
+      }
+      for (std::size_t i = 0; i < od.size(); ++i) bad += od[i] != decision.worker_of_sample[i];
+      std::vector<uint64_t> mp(8), up(8), ep(8);
+      std::vector<double> cw(8);
+      orc_report orep{0, 0, 0, 0, 0, 0, 0.0, mp.data(), up.data(), ep.data(), cw.data()};
+      orc_sim_step(oracle, ids.data(), offs.data(), samples.size(), od.data(), &orep);
+      bad += !(rep.miss_pull_w == mp && rep.update_push_w == up && rep.evict_push_w == ep &&
+               rep.cost_s == orep.cost_s && rep.hits == orep.hits);
+      ++iter;
+    }
+    orc_sim_destroy(oracle);
+    EXPECT(bad == 0 && iter == 200, "acceptance loop %s: %d mismatches over %d iterations", name, bad,
+           static_cast<int>(iter));
+  }
+}
+
 int main() {
+  acceptance_default_loop();
   worker_cache_kats();
   sized_costs();
   fig2_walkthrough();

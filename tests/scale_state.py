@@ -15,7 +15,7 @@ first eviction (cache.hpp:187-192)."""
 import numpy as np
 
 
-def synthetic_full_state(n, cap, V, clock, seed, all_current_every=4):
+def synthetic_full_state(n, cap, V, clock, seed, all_current_every=4, freq_hi=60):
     rng = np.random.default_rng(seed)
     per_worker = []
     for j in range(n):
@@ -52,8 +52,30 @@ def synthetic_full_state(n, cap, V, clock, seed, all_current_every=4):
             mark = np.full(len(ids), cur, np.uint64)  # the epoch advances at the first eviction
         else:
             mark = np.uint64(cur) - rng.integers(0, min(3, cur), len(ids)).astype(np.uint64)
-        freq = rng.integers(1, 60, len(ids)).astype(np.uint64)
+        freq = rng.integers(1, freq_hi, len(ids)).astype(np.uint64)
         last = rng.integers(0, clock, len(ids)).astype(np.uint64)
         ent = np.stack([ids.astype(np.uint64), ver, mark, freq, last], 1)
         caches.append((ent, cur, int((mark == cur).sum())))
     return glob, caches
+
+
+def spread_id(ids):
+    """A bijection of uint32 (odd multiplier mod 2^32): maps the dense Zipf ids
+    onto the whole [0, 2^32) range, order scrambled."""
+    x = np.asarray(ids, np.uint64)
+    return ((x * np.uint64(0x9E3779B1) + np.uint64(0x7F4A7C15)) & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+
+
+def spread_state(state):
+    """synthetic_full_state() output with every id mapped through spread_id,
+    rows re-sorted by the new ids (canonical order)."""
+    glob, caches = state
+    g = glob.copy()
+    g[:, 0] = spread_id(g[:, 0])
+    g = g[np.argsort(g[:, 0], kind="stable")]
+    out = []
+    for ent, cur, at in caches:
+        e = ent.copy()
+        e[:, 0] = spread_id(e[:, 0])
+        out.append((e[np.argsort(e[:, 0], kind="stable")], cur, at))
+    return g, out

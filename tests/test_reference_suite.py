@@ -5,14 +5,26 @@ tests/cpp/refcompat/ (tests/cpp/Makefile `reftests`).  The binaries are built
 where the reference sources exist (this container) and travel to the GPU box
 with the snapshot; the host-only suites (core types, workload generators,
 config parsing) also run on CPU."""
+import json
 import os
 import re
 import subprocess
+import sys
 
 import pytest
 
 HERE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cpp")
 BIN = os.path.join(HERE, "reftests")
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden"))
+from make_reference_suite import summarize  # noqa: E402
+
+# The reference's own results under the same Catch2 stand-in (built against
+# the reference headers): two checks fail IN THE REFERENCE -- test_cost.cpp:136
+# (a 10x slower link is not exactly 10x after three chained fp64 adds) and the
+# greedy-ties case of test_assign.cpp (capacities {0,1,1} for one row, which
+# greedy_dispatch itself rejects).  The drop-in must fail exactly there too.
+GOLDEN = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                                     "reference_suite.json")))
 
 
 def _binary(name):
@@ -24,19 +36,19 @@ def _binary(name):
     return path
 
 
-def _run(name, timeout=900):
-    r = subprocess.run([_binary(name)], capture_output=True, text=True, timeout=timeout)
+def _check_suite(name):
+    r = subprocess.run([_binary(name)], capture_output=True, text=True, timeout=900)
     out = r.stdout + r.stderr
-    m = re.search(r"(\d+) test cases, (\d+) failed; (\d+) checks, (\d+) failed", out)
-    assert m, out[-4000:]
-    return r.returncode, int(m.group(1)), int(m.group(2)), out
+    got = summarize(out)
+    want = GOLDEN[name]
+    # same cases, same number of checks, the same failing checks as the reference
+    assert got == want, f"drop-in {got} vs reference {want}\n" + out[-3000:]
 
 
 @pytest.mark.parametrize("suite", ["test_core", "test_workload", "test_config"])
 def test_reference_host_suite(suite):
     """types.hpp / workload.hpp / config.hpp suites: host code only."""
-    rc, cases, failed, out = _run(suite)
-    assert rc == 0 and failed == 0 and cases > 0, out[-4000:]
+    _check_suite(suite)
 
 
 @pytest.mark.gpu
@@ -44,8 +56,7 @@ def test_reference_host_suite(suite):
                                    "test_experiment"])
 def test_reference_device_suite(suite):
     """cache / cost / assign / sim / experiment suites on the device path."""
-    rc, cases, failed, out = _run(suite)
-    assert rc == 0 and failed == 0 and cases > 0, out[-4000:]
+    _check_suite(suite)
 
 
 # Criteria the reference itself fails here (SURVEY §0): 5 (3.26% < 10%
