@@ -160,11 +160,18 @@ struct SortScratch {
 };
 void sort_rows_by_gap(SortScratch& sc, const uint64_t* keys_in, const uint32_t* idx_in,
                       uint32_t* idx_out, uint64_t rows, cudaStream_t s);
-// prefs: n_order 64-bit words of scratch (each row's eight best initially-open workers)
+// K4 scratch: each position's eight best initially-open workers, its current
+// choice, and the cooperative rounds' per-tile counts
+struct GreedyScratch {
+  DevBuf<uint64_t> prefs;
+  DevBuf<int32_t> choice;
+  DevBuf<uint32_t> cnt;
+  int sms = 0;
+};
 void launch_greedy(const double* matrix, uint64_t rows, int n, const uint32_t* order,
                    uint64_t n_order, const int32_t* capacity_dev, int cap_uniform,
                    int32_t* decision, const uint32_t* row_ids, int32_t* pair_worker,
-                   int* flags, uint64_t* prefs, cudaStream_t s);
+                   int* flags, GreedyScratch& g, cudaStream_t s);
 void launch_check_balance(const int32_t* decision, uint64_t rows, int n, int m, int* flags,
                           cudaStream_t s);
 void launch_decision_cost(const double* matrix, const int32_t* decision, uint64_t rows, int n,
@@ -196,7 +203,7 @@ struct DispatchScratch {
   HungarianScratch hung;
   DevBuf<uint64_t> gap_keys;
   DevBuf<uint32_t> row_index, order;
-  DevBuf<uint64_t> prefs;
+  GreedyScratch greedy;
   DevBuf<double> cost;
   cudaStream_t side = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;

@@ -1815,9 +1815,8 @@ int edx_greedy_dispatch(uint64_t rows, uint64_t cols, const double* values, cons
     EDX_CUDA(cudaMemcpyAsync(c.i32a.p, capacity, cols * 4, cudaMemcpyHostToDevice, c.stream));
     k_u64_to_u32<<<grid_for(n_order), kT, 0, c.stream>>>(c.u64a.p, n_order, c.u32a.p);
     EDX_LAUNCHED();
-    c.disp.prefs.ensure(n_order);
     edx::launch_greedy(c.values.p, rows, static_cast<int>(cols), c.u32a.p, n_order, c.i32a.p, 0,
-                       nullptr, nullptr, c.i32b.p, c.flags.p, c.disp.prefs.p, c.stream);
+                       nullptr, nullptr, c.i32b.p, c.flags.p, c.disp.greedy, c.stream);
     EDX_CUDA(cudaMemcpyAsync(out_workers, c.i32b.p, n_order * 4, cudaMemcpyDeviceToHost, c.stream));
     c.sync_and_check();
     std::copy(order, order + n_order, out_rows);

@@ -799,794 +799,6 @@ __device__ __forceinline__ bool warp_block_sorted(const int32_t* ord, const int6
   return !__any_sync(0xffffffffu, bad);
 }
 
-// --------------------------------------------- K6 tabled (per-row operand table)
-// Fastest variant, used when the operand table fits in shared memory.  At the
-// start of each row (phase) all warps rebuild, for every block x and every
-// position d of its (v desc, j asc) column order,
-//     A[x][d][w] = (S[r][w] - u[r]) << 6,  r = p[ord[x][d]]   (relax operand)
-//     Btab[x][d] = x - (v[ord[x][d]] << 6)                    (key offset)
-//     rtab[x][d] = r                                          (0 = free column)
-// so that during the row a Dijkstra step only needs: key = E + B -> two
-// redux.sync.min.u32 -> one LDS of A[winner][cursor][lane] -> relax.  The
-// winner's bookkeeping uses values prefetched one consumption ahead, and the
-// per-block cursors are packed 8 bits each in one uniform register (n <= 8)
-// or kept in shared memory.  `way` is recorded as a step index (see the
-// fast kernel).  Row end is the same as the fast kernel.
-constexpr int kTabMaxWarps = 8;
-constexpr int kRunMax = 255;  // speculative run length cap of the batched Dijkstra steps
-constexpr int kChunk = 8;     // steps evaluated per speculation chunk
-
-template <int NB, int SMODE, bool PACK>  // SMODE 0: S shared, 1: S global
-__global__ void __launch_bounds__(kTabMaxWarps * 32, 1)
-    k_hungarian_blocks_tab(const int64_t* __restrict__ S_global, int n, int mult, int k,
-                           const uint32_t* __restrict__ order, int32_t* __restrict__ decision,
-                           const uint32_t* __restrict__ row_ids, uint64_t* __restrict__ col_of_row,
-                           unsigned long long* stats, int* flags,
-                           const unsigned long long* __restrict__ max_scaled) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  const size_t K1 = static_cast<size_t>(k) + 1;
-  size_t so = 0;
-  auto stake = [&](size_t bytes) {
-    uint8_t* q = smem + so;
-    so += (bytes + 15) & ~size_t(15);
-    return q;
-  };
-  const int64_t* S;
-  if constexpr (SMODE == 0) {
-    int64_t* Ss = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(k) * n * 8));
-    for (size_t x = tid; x < static_cast<size_t>(k) * n; x += blockDim.x) Ss[x] = S_global[x];
-    S = Ss;
-  } else {
-    S = S_global;
-  }
-  const int AST = PACK ? 8 : n;  // row stride of the operand table
-  int64_t* A = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(k) * AST * 8));
-  int64_t* Btab = reinterpret_cast<int64_t*>(stake(K1 * 8));  // by column: block - (v << 6)
-  int64_t* u = reinterpret_cast<int64_t*>(stake(K1 * 8));
-  int64_t* v = reinterpret_cast<int64_t*>(stake(K1 * 8));
-  int64_t* dlt = reinterpret_cast<int64_t*>(stake((K1 + 32) * 8));
-  int32_t* p = reinterpret_cast<int32_t*>(stake(K1 * 4));
-  int32_t* wayi = reinterpret_cast<int32_t*>(stake((K1 + 32) * 4));
-  int32_t* ulist = reinterpret_cast<int32_t*>(stake((K1 + 32) * 4));
-  int32_t* ord = reinterpret_cast<int32_t*>(stake(K1 * 4));
-  int32_t* rtab = reinterpret_cast<int32_t*>(stake(K1 * 4));
-  int32_t* curs = reinterpret_cast<int32_t*>(stake(64 * 4));
-  int64_t* scal = reinterpret_cast<int64_t*>(stake(4 * 8));
-  int64_t* rk_v = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(nw) * mult * 8));
-  int32_t* rk_i = reinterpret_cast<int32_t*>(stake(static_cast<size_t>(nw) * 2 * mult * 4));
-  if (so > dynamic_smem_bytes()) {  // host/device layout mismatch: fail loudly, touch nothing
-    if (tid == 0) atomicOr(flags + kFlagInternal, 1);
-    return;
-  }
-
-  const unsigned long long mx = *max_scaled;
-  const bool packable = mx < (1ULL << 57) / (8ULL * static_cast<unsigned long long>(k + 1));
-  for (size_t x = tid; x < K1; x += blockDim.x) {
-    u[x] = 0;
-    v[x] = 0;
-    p[x] = 0;
-    wayi[x] = 0;
-  }
-  for (int x = tid; x < k; x += blockDim.x) ord[x] = x + 1;
-  if (tid == 0) scal[2] = 0;
-  __syncthreads();
-  if (!packable) {  // wide-range path (see k_hungarian_blocks_wide)
-    if (warp == 0) {
-      BlockArrays Aw{S, u, v, dlt, p, wayi, ulist, ord, rk_i};
-      if (!hungarian_blocks_warp<NB>(Aw, n, mult, k, stats, flags)) return;
-      __syncwarp();
-      for (int j = lane + 1; j <= k; j += 32) {
-        const int r = p[j] - 1;
-        if (col_of_row) col_of_row[r] = static_cast<uint64_t>(j - 1);
-        if (decision) {
-          const uint32_t row = order[r];
-          decision[row_ids ? row_ids[row] : row] = (j - 1) / mult;
-        }
-      }
-    }
-    return;
-  }
-
-  unsigned long long steps = 0;
-  long long c_step = 0, c_end = 0, c_tab = 0, rekeyed = 0, c_pot = 0, p2 = 0, pmax = 0, runs = 0, c_ref = 0;
-  const long long c_start = clock64();
-  for (int i = 1; i <= k; ++i) {
-    const long long t0 = clock64();
-    // Operand tables are indexed by column (A[c] = (S[p[c]] - u[p[c]]) << 6,
-    // B[c] = block(c) - (v[c] << 6), r[c] = p[c]) and refreshed at row end for
-    // the reached columns only.
-    if (i == 1) {
-      for (int c = tid + 1; c <= k; c += blockDim.x) {
-        rtab[c] = 0;
-        Btab[c] = static_cast<int64_t>((c - 1) / mult);
-      }
-    }
-    __syncthreads();
-    const long long t1 = clock64();
-    c_tab += t1 - t0;
-    if (warp == 0) {
-      int64_t E6[NB], B[NB], Bn[NB];
-      int wyi[NB], curl[NB], col[NB], coln[NB];
-      const int64_t ui = u[i];
-#pragma unroll
-      for (int b = 0; b < NB; ++b) {
-        const int w = lane + 32 * b;
-        curl[b] = mult;  // lanes without a block never offer a key
-        E6[b] = 0;
-        B[b] = Bn[b] = 0;
-        col[b] = coln[b] = 0;
-        wyi[b] = 0;
-        if (w < n) {
-          curl[b] = 0;
-          const int base = w * mult;
-          col[b] = ord[base];
-          B[b] = Btab[col[b]];
-          if (mult > 1) {
-            coln[b] = ord[base + 1];
-            Bn[b] = Btab[coln[b]];
-          }
-          E6[b] = (S[static_cast<size_t>(i - 1) * n + w] - ui) << 6;  // relax from row i
-        }
-      }
-      if constexpr (!PACK) {
-        if (lane < n) curs[lane] = 0;
-        if (NB > 1 && lane + 32 < n) curs[lane + 32] = 0;
-      }
-      if (lane == 0) {
-        p[0] = i;
-        ulist[0] = 0;
-        dlt[0] = 0;
-      }
-      __syncwarp();
-      int nused = 1;
-      int64_t Dl = 0;
-      bool abort = false;
-      if constexpr (PACK) {
-        // n <= 8: lane w owns block w; cursors are 8-bit fields of (cpl, cph);
-        // an exhausted block (or a lane without one) carries B = 2^62, above
-        // every real key (< 2^57), so no per-step validity select is needed.
-        //
-        // Run-batched steps.  After the argmin picks block w, the next steps
-        // are evaluated speculatively assuming w keeps winning (in practice
-        // ~97% of consecutive steps share the winner block).  While w wins,
-        // its key sequence is closed form: with V6_t = v(c_t) << 6,
-        //     delta6_t = min(V6_{t-1}, A_w(r_{t-1})) - V6_t      (t >= 2),
-        // and every block's relaxed value obeys E^{t+1} = min(E^t - delta6_t,
-        // A(r_t)), i.e. with P_t = sum of delta6 up to t and F = E + P_{t-1},
-        //     F^{t+1} = min(F^t, A(r_t) + P_t)      (a prefix min).
-        // Step t is the sequential step iff no other block has a smaller key:
-        // F_x^t + (B_x - w) > P_t for every x != w (keys carry the block index
-        // in their low bits, so they are never equal across blocks).  The
-        // first failing t over all lanes (one REDUX) bounds the valid prefix,
-        // which is then committed exactly as the one-step loop would.
-        constexpr int64_t kBig = 1LL << 62;
-        int64_t E6v = E6[0], Bv = (lane < n && mult > 0) ? B[0] : kBig;
-        int colv = col[0], wyv = wyi[0];
-        uint32_t cpl = 0, cph = 0;
-        const int64_t* Alane = A + lane;
-        const int dummy = k + 1 + lane;
-        for (;;) {
-          const uint64_t key = static_cast<uint64_t>(E6v + Bv);
-          const unsigned hi = static_cast<unsigned>(key >> 32), lo = static_cast<unsigned>(key);
-          const unsigned mh = __reduce_min_sync(0xffffffffu, hi);
-          const unsigned ml = __reduce_min_sync(0xffffffffu, hi == mh ? lo : 0xffffffffu);
-          if (ml == 0xffffffffu && mh == 0xffffffffu) {  // nothing left: corrupt input only
-            abort = true;
-            break;
-          }
-          const int ws = static_cast<int>(ml & 7u);
-          const int d = static_cast<int>(__byte_perm(cpl, cph, static_cast<unsigned>(ws)) & 255u);
-          const int base = ws * mult + d;  // position of the winner's candidate c_1
-          const int Tm = mult - d;
-          const int64_t delta1 = static_cast<int64_t>(((static_cast<uint64_t>(mh) << 32) | ml) & ~63ULL);
-          // Block state broadcast to every lane: F (= E + P), key offset B, way.
-          int64_t Fx[8], Bx[8];
-          int wyx[8];
-#pragma unroll
-          for (int x = 0; x < 8; ++x) {
-            Fx[x] = __shfl_sync(0xffffffffu, E6v, x);
-            Bx[x] = __shfl_sync(0xffffffffu, Bv, x);
-            wyx[x] = __shfl_sync(0xffffffffu, wyv, x);
-          }
-          // Lanes = steps: lane q evaluates step sN+q+1 of the run for all blocks.
-          int64_t P = 0, V6prev = 0, Awprev = 0;
-          int sN = 0;
-          bool phase_end = false;
-          const int nused0 = nused;
-          const int64_t Dl0 = Dl;
-          while (sN < Tm) {
-            const int cnt = min(32, Tm - sN);
-            const bool live = lane < cnt;
-            const int pos = base + sN + (live ? lane : 0);
-            const int c = ord[pos];
-            const int64_t V6 = static_cast<int64_t>(ws) - Btab[c];
-            const int r = rtab[c];
-            const int64_t Aw = A[static_cast<size_t>(c - 1) * 8 + ws];
-            int64_t Ax[8];
-            {
-              const longlong2* row = reinterpret_cast<const longlong2*>(A + static_cast<size_t>(c - 1) * 8);
-#pragma unroll
-              for (int h = 0; h < 4; ++h) {
-                const longlong2 v2 = row[h];
-                Ax[2 * h] = v2.x;
-                Ax[2 * h + 1] = v2.y;
-              }
-            }
-            int64_t V6p = __shfl_up_sync(0xffffffffu, V6, 1), Awp = __shfl_up_sync(0xffffffffu, Aw, 1);
-            if (lane == 0) {
-              V6p = V6prev;
-              Awp = Awprev;
-            }
-            const bool first = sN == 0 && lane == 0;
-            int64_t Pt = first ? delta1 : (V6p < Awp ? V6p : Awp) - V6;
-            if (!live) Pt = 0;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {  // inclusive prefix sum of the deltas
-              const int64_t y = __shfl_up_sync(0xffffffffu, Pt, off);
-              if (lane >= off) Pt += y;
-            }
-            Pt += P;
-            bool fail = false;
-            unsigned impw = 0;
-            unsigned impm[8];
-            int64_t Fa[8];
-#pragma unroll
-            for (int x = 0; x < 8; ++x) {
-              const int64_t cand = Ax[x] + Pt;  // relax candidate of this step for block x
-              int64_t incl = cand;
-#pragma unroll
-              for (int off = 1; off < 32; off <<= 1) {  // inclusive prefix min over steps
-                const int64_t y = __shfl_up_sync(0xffffffffu, incl, off);
-                if (lane >= off) incl = y < incl ? y : incl;
-              }
-              int64_t excl = __shfl_up_sync(0xffffffffu, incl, 1);
-              const int64_t Fb = lane == 0 ? Fx[x] : (excl < Fx[x] ? excl : Fx[x]);  // F before the step
-              Fa[x] = cand < Fb ? cand : Fb;                                            // F after its relax
-              if (x < n && x != ws && !(Fb + Bx[x] - ws > Pt)) fail = true;           // x would win here
-              impm[x] = __ballot_sync(0xffffffffu, live && cand < Fb);
-              impw = x == ws ? impm[x] : impw;
-            }
-            const unsigned failm = __ballot_sync(0xffffffffu, live && !first && fail);
-            const unsigned freem = __ballot_sync(0xffffffffu, live && r == 0);
-            const int failq = failm ? __ffs(failm) - 1 : 32;
-            const int freeq = freem ? __ffs(freem) - 1 : 32;
-            int vq = failq < cnt ? failq : cnt;
-            if (freeq < vq) {
-              vq = freeq + 1;
-              phase_end = true;
-            }
-            const unsigned relax_m = freeq < 32 ? ((1u << freeq) - 1u) : 0xffffffffu;  // no relax at a free column
-            int wyw = wyx[0];
-#pragma unroll
-            for (int x = 1; x < 8; ++x) wyw = x == ws ? wyx[x] : wyw;
-            const int wbase = nused0 + sN;
-            if (lane < vq) {  // each lane commits its own step
-              const unsigned prev = impw & relax_m & ((1u << lane) - 1u);
-              wayi[c] = prev ? wbase + 31 - __clz(prev) : wyw;
-              dlt[c] = Dl0 + (Pt >> 6);
-              ulist[wbase + lane] = c;
-            }
-            if (vq > 0) {
-              P = __shfl_sync(0xffffffffu, Pt, vq - 1);
-              const unsigned cm = relax_m & (vq >= 32 ? 0xffffffffu : ((1u << vq) - 1u));
-#pragma unroll
-              for (int x = 0; x < 8; ++x) {
-                Fx[x] = __shfl_sync(0xffffffffu, Fa[x], vq - 1);
-                const unsigned mx2 = impm[x] & cm;
-                wyx[x] = mx2 ? wbase + 31 - __clz(mx2) : wyx[x];
-              }
-            }
-            V6prev = __shfl_sync(0xffffffffu, V6, 31);
-            Awprev = __shfl_sync(0xffffffffu, Aw, 31);
-            sN += vq;
-            if (vq < cnt || phase_end) break;
-          }
-          const int64_t Ps = P;
-          ++runs;
-          Dl = Dl0 + (Ps >> 6);
-          nused = nused0 + sN;
-          steps += sN;
-          {
-            int64_t fme = Fx[0];
-            int wme = wyx[0];
-#pragma unroll
-            for (int x = 1; x < 8; ++x) {
-              fme = x == lane ? Fx[x] : fme;
-              wme = x == lane ? wyx[x] : wme;
-            }
-            if (lane < n) {
-              E6v = fme - Ps;
-              wyv = wme;
-            }
-          }
-          const bool mine = lane == ws;
-          {  // advance block ws by sN columns
-            const uint32_t inc = static_cast<uint32_t>(sN) << ((ws & 3) * 8);
-            cpl += ws < 4 ? inc : 0u;
-            cph += ws < 4 ? 0u : inc;
-            const int np = base + sN;
-            const bool left = d + sN < mult;
-            const int cn = left ? ord[np] : 0;
-            const int64_t bn = left ? Btab[cn] : kBig;
-            colv = mine ? cn : colv;
-            Bv = mine ? bn : Bv;
-          }
-          __syncwarp();
-          if (phase_end) break;
-        }
-        (void)colv;
-        curl[0] = lane < n ? static_cast<int>(__byte_perm(cpl, cph, static_cast<unsigned>(lane & 7)) & 255u) : 0;
-      }
-      if (lane == 0) {
-        scal[0] = Dl;
-        scal[1] = nused;
-        if (abort) scal[2] = 1;
-      }
-#pragma unroll
-      for (int b = 0; b < NB; ++b) {
-        const int w = lane + 32 * b;
-        if (w < n) curs[w] = curl[b];
-      }
-    }
-    __syncthreads();
-    const long long t2 = clock64();
-    c_step += t2 - t1;
-    if (scal[2]) {
-      if (tid == 0) atomicOr(flags + kFlagBadCost, 1);
-      return;
-    }
-    const int64_t Dl = scal[0];
-    const int nu = static_cast<int>(scal[1]);
-    for (int t = tid; t < nu; t += blockDim.x) {  // potentials (assign.hpp:131-138)
-      const int j = ulist[t];
-      const int64_t dd = Dl - dlt[j];
-      u[p[j]] += dd;
-      v[j] -= dd;
-    }
-    __syncthreads();
-    c_pot += clock64() - t2;
-    if (tid == 0) {  // augment (assign.hpp:141-145); way[j] = ulist[wayi[j]]
-      int jj = ulist[nu - 1];
-      do {
-        const int jp = ulist[wayi[jj]];
-        p[jj] = p[jp];
-        jj = jp;
-      } while (jj != 0);
-    }
-    for (int w = warp; w < n; w += nw) {  // re-key touched blocks
-      const int P = curs[w];
-      if (P == 0) continue;
-      if (lane == 0) rekeyed += P;
-      if (lane == 0 && warp == 0) {
-        p2 += static_cast<long long>(P) * P;
-        pmax = P > pmax ? P : pmax;
-      }
-      if (warp_block_sorted(ord, v, w * mult, mult, lane)) continue;
-      if (mult <= 512) {
-        warp_resort_dispatch(ord, v, w * mult, mult, lane);
-        __syncwarp();
-        continue;
-      }
-      int32_t* base = ord + w * mult;
-      int64_t* pv = rk_v + static_cast<size_t>(warp) * mult;
-      int32_t* sorted = rk_i + static_cast<size_t>(warp) * 2 * mult;
-      int32_t* merged = sorted + mult;
-      for (int t = lane; t < P; t += 32) pv[t] = v[base[t]];
-      __syncwarp();
-      for (int t = lane; t < P; t += 32) {
-        const int a = base[t];
-        const int64_t va = pv[t];
-        int rank = 0;
-        for (int s2 = 0; s2 < P; ++s2) {
-          const int64_t vb = pv[s2];
-          rank += (vb > va || (vb == va && base[s2] < a)) ? 1 : 0;
-        }
-        sorted[rank] = a;
-      }
-      __syncwarp();
-      const int Q = mult - P;
-      const int32_t* suf = base + P;
-      for (int t = lane; t < P; t += 32) {
-        const int a = sorted[t];
-        const int64_t va = v[a];
-        int lo2 = 0, hi2 = Q;
-        while (lo2 < hi2) {
-          const int mid = (lo2 + hi2) >> 1;
-          const int b2 = suf[mid];
-          const int64_t vb = v[b2];
-          if (vb > va || (vb == va && b2 < a)) lo2 = mid + 1;
-          else hi2 = mid;
-        }
-        merged[t + lo2] = a;
-      }
-      for (int t = lane; t < Q; t += 32) {
-        const int b2 = suf[t];
-        const int64_t vb = v[b2];
-        int lo2 = 0, hi2 = P;
-        while (lo2 < hi2) {
-          const int mid = (lo2 + hi2) >> 1;
-          const int a = sorted[mid];
-          const int64_t va = v[a];
-          if (va > vb || (va == vb && a < b2)) lo2 = mid + 1;
-          else hi2 = mid;
-        }
-        merged[t + lo2] = b2;
-      }
-      __syncwarp();
-      for (int t = lane; t < mult; t += 32) base[t] = merged[t];
-      __syncwarp();
-    }
-    __syncthreads();
-    const long long t3 = clock64();
-    // refresh the operand table of the reached columns: 4 lanes per column,
-    // 16 bytes (2 workers) each, so a warp's row accesses are conflict-free
-    for (int e = tid; e < (nu - 1) * 4; e += blockDim.x) {
-      const int q = e >> 2, h = e & 3;
-      const int c = ulist[1 + q];
-      const int r = p[c];
-      const int64_t ur = u[r];
-      if (h == 0) {
-        rtab[c] = r;
-        Btab[c] = static_cast<int64_t>((c - 1) / mult) - (v[c] << 6);
-      }
-      if (n == 8) {
-        const longlong2 sv = reinterpret_cast<const longlong2*>(S + static_cast<size_t>(r - 1) * 8)[h];
-        reinterpret_cast<longlong2*>(A + static_cast<size_t>(c - 1) * 8)[h] =
-            make_longlong2((sv.x - ur) << 6, (sv.y - ur) << 6);
-      } else {
-        for (int w = 2 * h; w < 2 * h + 2 && w < n; ++w)
-          A[static_cast<size_t>(c - 1) * AST + w] = (S[static_cast<size_t>(r - 1) * n + w] - ur) << 6;
-      }
-    }
-    __syncthreads();
-    c_ref += clock64() - t3;
-    c_end += clock64() - t2;
-  }
-  for (int j = tid + 1; j <= k; j += blockDim.x) {
-    const int r = p[j] - 1;
-    if (col_of_row) col_of_row[r] = static_cast<uint64_t>(j - 1);
-    if (decision) {
-      const uint32_t row = order[r];
-      decision[row_ids ? row_ids[row] : row] = (j - 1) / mult;
-    }
-  }
-  if (tid == 0 && stats) {
-    stats[0] = steps;
-    stats[1] = c_step;
-    stats[2] = c_end;
-    stats[3] = c_tab;
-    stats[4] = c_pot;
-    stats[5] = runs;
-    stats[6] = c_ref;
-    stats[7] = clock64() - c_start;
-  }
-}
-
-// ------------------------------------------- K6 run kernel (n <= 32, lanes = blocks)
-// The production solver for n <= 32.  Same per-row operand table and row
-// end as the tabled kernel; the Dijkstra steps are evaluated in runs (see the
-// derivation above): the argmin picks block w, then chunks of up to 32
-// consecutive steps are evaluated assuming w keeps winning.  In a chunk the
-// warp first works lanes = steps (load the candidates of w, scan the delta
-// sums P_t), then lanes = blocks: lane x walks the chunk's steps in order,
-// checking F_x + B_x - w > P_t (x would not win step t) and relaxing
-// F_x = min(F_x, A_x(r_t) + P_t), snapshotting F_x per step.  One REDUX gives
-// the first step some block would win; each lane then commits its own step.
-// AMODE 0: S and the table in shared memory; 1: S global; 2: S and table
-// global (L2; each chunk's loads are issued together).
-constexpr int kRunWarps = 8;
-
-template <int AMODE>
-__global__ void __launch_bounds__(kRunWarps * 32, 1)
-    k_hungarian_blocks_run(const int64_t* __restrict__ S_global, int n, int mult, int k,
-                           int64_t* __restrict__ A_global, const uint32_t* __restrict__ order,
-                           int32_t* __restrict__ decision, const uint32_t* __restrict__ row_ids,
-                           uint64_t* __restrict__ col_of_row, unsigned long long* stats,
-                           int* flags, const unsigned long long* __restrict__ max_scaled) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  const size_t K1 = static_cast<size_t>(k) + 1;
-  size_t so = 0;
-  auto stake = [&](size_t bytes) {
-    uint8_t* q = smem + so;
-    so += (bytes + 15) & ~size_t(15);
-    return q;
-  };
-  const int64_t* S;
-  if constexpr (AMODE == 0) {
-    int64_t* Ss = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(k) * n * 8));
-    for (size_t x = tid; x < static_cast<size_t>(k) * n; x += blockDim.x) Ss[x] = S_global[x];
-    S = Ss;
-  } else {
-    S = S_global;
-  }
-  int64_t* A;
-  if constexpr (AMODE <= 1) A = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(k) * n * 8));
-  else A = A_global;
-  int64_t* Btab = reinterpret_cast<int64_t*>(stake(K1 * 8));  // by column: block - (v << 6)
-  int64_t* u = reinterpret_cast<int64_t*>(stake(K1 * 8));
-  int64_t* v = reinterpret_cast<int64_t*>(stake(K1 * 8));
-  int64_t* dlt = reinterpret_cast<int64_t*>(stake(K1 * 8));
-  int32_t* p = reinterpret_cast<int32_t*>(stake(K1 * 4));
-  int32_t* wayi = reinterpret_cast<int32_t*>(stake(K1 * 4));
-  int32_t* ulist = reinterpret_cast<int32_t*>(stake(K1 * 4));
-  int32_t* ord = reinterpret_cast<int32_t*>(stake(K1 * 4));
-  int32_t* rtab = reinterpret_cast<int32_t*>(stake(K1 * 4));
-  int32_t* curs = reinterpret_cast<int32_t*>(stake(64 * 4));
-  int64_t* Ps = reinterpret_cast<int64_t*>(stake(32 * 8));
-  int32_t* Cs = reinterpret_cast<int32_t*>(stake(32 * 4));
-  int64_t* Fsnap = reinterpret_cast<int64_t*>(stake(32 * 32 * 8));
-  int64_t* scal = reinterpret_cast<int64_t*>(stake(4 * 8));
-  int64_t* rk_v = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(nw) * mult * 8));
-  int32_t* rk_i = reinterpret_cast<int32_t*>(stake(static_cast<size_t>(nw) * 2 * mult * 4));
-  if (so > dynamic_smem_bytes()) {  // host/device layout mismatch: fail loudly, touch nothing
-    if (tid == 0) atomicOr(flags + kFlagInternal, 1);
-    return;
-  }
-  const unsigned long long mx = *max_scaled;
-  const bool packable = mx < (1ULL << 57) / (8ULL * static_cast<unsigned long long>(k + 1));
-  for (size_t x = tid; x < K1; x += blockDim.x) {
-    u[x] = 0;
-    v[x] = 0;
-    p[x] = 0;
-    wayi[x] = 0;
-  }
-  for (int x = tid; x < k; x += blockDim.x) ord[x] = x + 1;
-  if (tid == 0) scal[2] = 0;
-  __syncthreads();
-  if (!packable) {  // wide-range path (see k_hungarian_blocks_wide)
-    if (warp == 0) {
-      BlockArrays Aw{S, u, v, dlt, p, wayi, ulist, ord, rk_i};
-      if (!hungarian_blocks_warp<1>(Aw, n, mult, k, stats, flags)) return;
-      __syncwarp();
-      for (int j = lane + 1; j <= k; j += 32) {
-        const int r = p[j] - 1;
-        if (col_of_row) col_of_row[r] = static_cast<uint64_t>(j - 1);
-        if (decision) {
-          const uint32_t row = order[r];
-          decision[row_ids ? row_ids[row] : row] = (j - 1) / mult;
-        }
-      }
-    }
-    return;
-  }
-
-  constexpr int64_t kBig = 1LL << 62;
-  const int xl = lane < n ? lane : 0;  // this lane's block column (clamped for inert lanes)
-  unsigned long long steps = 0;
-  long long c_step = 0, c_end = 0, c_tab = 0, runs = 0;
-  const long long c_start = clock64();
-  for (int i = 1; i <= k; ++i) {
-    const long long t0 = clock64();
-    // Operand tables are indexed by column: A[c] = (S[p[c]] - u[p[c]]) << 6,
-    // B[c] = block(c) - (v[c] << 6), r[c] = p[c].  Only the columns reached in a
-    // row change (see the row end), so they are updated incrementally there.
-    if (i == 1) {
-      for (int c = tid + 1; c <= k; c += blockDim.x) {
-        rtab[c] = 0;
-        Btab[c] = static_cast<int64_t>((c - 1) / mult);
-      }
-    }
-    if constexpr (AMODE == 2) __threadfence_block();
-    __syncthreads();
-    const long long t1 = clock64();
-    c_tab += t1 - t0;
-    if (warp == 0) {
-      // lane x < n owns block x: E = D_x - Δ (<< 6), B = x - (v(candidate) << 6), way index
-      int64_t E6v = 0, Bv = kBig;
-      int wyv = 0;
-      if (lane < n) {
-        E6v = (S[static_cast<size_t>(i - 1) * n + lane] - u[i]) << 6;  // relax from row i
-        Bv = Btab[ord[lane * mult]];
-        curs[lane] = 0;
-      }
-      if (lane == 0) {
-        p[0] = i;
-        ulist[0] = 0;
-        dlt[0] = 0;
-      }
-      __syncwarp();
-      int nused = 1;
-      int64_t Dl = 0;
-      bool abort = false;
-      for (;;) {  // runs
-        const uint64_t key = static_cast<uint64_t>(E6v + Bv);
-        const unsigned hi = static_cast<unsigned>(key >> 32), lo = static_cast<unsigned>(key);
-        const unsigned mh = __reduce_min_sync(0xffffffffu, hi);
-        const unsigned ml = __reduce_min_sync(0xffffffffu, hi == mh ? lo : 0xffffffffu);
-        if (ml == 0xffffffffu && mh == 0xffffffffu) {
-          abort = true;
-          break;
-        }
-        const int ws = min(static_cast<int>(ml & 63u), n - 1);
-        const int64_t delta1 = static_cast<int64_t>(((static_cast<uint64_t>(mh) << 32) | ml) & ~63ULL);
-        const int d = curs[ws];
-        const int base = ws * mult + d;
-        const int Tm = mult - d;
-        const int wyw0 = __shfl_sync(0xffffffffu, wyv, ws);
-        const bool check = lane < n && lane != ws;
-        int64_t P = 0, F = E6v, V6prev = 0, Awprev = 0;
-        int sN = 0, wyw = wyw0;
-        bool phase_end = false;
-        const int nused0 = nused;
-        const int64_t Dl0 = Dl;
-        while (sN < Tm) {
-          const int cnt = min(32, Tm - sN);
-          // -- lanes = steps: the winner's candidates and the running delta sums
-          const bool live = lane < cnt;
-          const int pos = base + sN + (live ? lane : 0);
-          const int c = ord[pos];
-          const int64_t V6 = static_cast<int64_t>(ws) - Btab[c];
-          const int r = rtab[c];
-          const int64_t Aw = A[static_cast<size_t>(c - 1) * n + ws];
-          Cs[lane] = c;
-          int64_t V6p = __shfl_up_sync(0xffffffffu, V6, 1), Awp = __shfl_up_sync(0xffffffffu, Aw, 1);
-          if (lane == 0) {
-            V6p = V6prev;
-            Awp = Awprev;
-          }
-          const bool first = sN == 0 && lane == 0;
-          int64_t Pt = first ? delta1 : (V6p < Awp ? V6p : Awp) - V6;
-          if (!live) Pt = 0;
-#pragma unroll
-          for (int off = 1; off < 32; off <<= 1) {
-            const int64_t y = __shfl_up_sync(0xffffffffu, Pt, off);
-            if (lane >= off) Pt += y;
-          }
-          Pt += P;
-          Ps[lane] = Pt;
-          const unsigned freem = __ballot_sync(0xffffffffu, live && r == 0);
-          const int freeq = freem ? __ffs(freem) - 1 : 32;
-          const int tl = cnt < freeq + 1 ? cnt : freeq + 1;
-          __syncwarp();
-          // -- lanes = blocks: walk the chunk's steps in order
-          const int64_t F_in = F;
-          int failt = 32;
-          unsigned impm = 0;
-          const int64_t Gb = Bv - ws;  // key offset relative to the winner
-          for (int t0 = 0; t0 < tl; t0 += 8) {
-            int64_t Ax[8], Pq[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const int t = t0 + q < tl ? t0 + q : t0;
-              Ax[q] = A[static_cast<size_t>(Cs[t] - 1) * n + xl];
-              Pq[q] = Ps[t];
-            }
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const int t = t0 + q;
-              if (t < tl) {
-                if (check && failt == 32 && !(sN == 0 && t == 0) && !(F + Gb > Pq[q])) failt = t;
-                const int64_t cand = Ax[q] + Pq[q];
-                if (t != freeq && cand < F) {
-                  F = cand;
-                  impm |= 1u << t;
-                }
-                Fsnap[t * 32 + lane] = F;
-              }
-            }
-          }
-          const int fail = static_cast<int>(__reduce_min_sync(0xffffffffu, static_cast<unsigned>(failt)));
-          int vq = fail < cnt ? fail : cnt;
-          if (freeq < vq) {
-            vq = freeq + 1;
-            phase_end = true;
-          }
-          const unsigned impw = __shfl_sync(0xffffffffu, impm, ws);
-          const int wbase = nused0 + sN;
-          if (lane < vq) {  // lanes = steps again: each lane commits its own step
-            const unsigned prev = impw & ((1u << lane) - 1u);
-            wayi[c] = prev ? wbase + 31 - __clz(prev) : wyw;
-            dlt[c] = Dl0 + (Pt >> 6);
-            ulist[wbase + lane] = c;
-          }
-          __syncwarp();
-          if (vq > 0) {
-            P = __shfl_sync(0xffffffffu, Pt, vq - 1);
-            F = Fsnap[(vq - 1) * 32 + lane];
-            const unsigned cm = impm & (vq >= 32 ? 0xffffffffu : ((1u << vq) - 1u));
-            wyv = cm ? wbase + 31 - __clz(cm) : wyv;
-            const unsigned cw = impw & (vq >= 32 ? 0xffffffffu : ((1u << vq) - 1u));
-            wyw = cw ? wbase + 31 - __clz(cw) : wyw;
-          } else {
-            F = F_in;
-          }
-          V6prev = __shfl_sync(0xffffffffu, V6, 31);
-          Awprev = __shfl_sync(0xffffffffu, Aw, 31);
-          sN += vq;
-          if (vq < cnt || phase_end) break;
-        }
-        ++runs;
-        Dl = Dl0 + (P >> 6);
-        nused = nused0 + sN;
-        steps += sN;
-        if (lane < n) E6v = F - P;
-        if (lane == ws) {
-          curs[ws] = d + sN;
-          Bv = d + sN < mult ? Btab[ord[base + sN]] : kBig;
-        }
-        __syncwarp();
-        if (phase_end) break;
-      }
-      if (lane == 0) {
-        scal[0] = Dl;
-        scal[1] = nused;
-        if (abort) scal[2] = 1;
-      }
-    }
-    __syncthreads();
-    const long long t2 = clock64();
-    c_step += t2 - t1;
-    if (scal[2]) {
-      if (tid == 0) atomicOr(flags + kFlagBadCost, 1);
-      return;
-    }
-    const int64_t Dl = scal[0];
-    const int nu = static_cast<int>(scal[1]);
-    for (int t = tid; t < nu; t += blockDim.x) {  // potentials (assign.hpp:131-138)
-      const int j = ulist[t];
-      const int64_t dd = Dl - dlt[j];
-      u[p[j]] += dd;
-      v[j] -= dd;
-    }
-    __syncthreads();
-    if (tid == 0) {  // augment (assign.hpp:141-145); way[j] = ulist[wayi[j]]
-      int jj = ulist[nu - 1];
-      do {
-        const int jp = ulist[wayi[jj]];
-        p[jj] = p[jp];
-        jj = jp;
-      } while (jj != 0);
-    }
-    for (int w = warp; w < n; w += nw) {  // re-sort the touched blocks (if needed)
-      if (curs[w] == 0) continue;
-      if (!warp_block_sorted(ord, v, w * mult, mult, lane))
-        warp_resort_dispatch(ord, v, w * mult, mult, lane);
-      __syncwarp();
-    }
-    __syncthreads();
-    // refresh the operand table of the reached columns (their row or its
-    // potential changed; every other column is unchanged)
-    {  // refresh reached columns: a group of gs >= n lanes per column, lanes over workers
-      const int gs = n <= 8 ? 8 : (n <= 16 ? 16 : 32);
-      const int gpw = 32 / gs, sub = lane / gs, lw = lane - sub * gs;
-      for (int e = warp * gpw + sub + 1; e < nu; e += nw * gpw) {
-        const int c = ulist[e];
-        const int r = p[c];
-        const int64_t ur = u[r];
-        if (lw == 0) {
-          rtab[c] = r;
-          Btab[c] = static_cast<int64_t>((c - 1) / mult) - (v[c] << 6);
-        }
-        if (lw < n)
-          A[static_cast<size_t>(c - 1) * n + lw] = (S[static_cast<size_t>(r - 1) * n + lw] - ur) << 6;
-      }
-    }
-    if constexpr (AMODE == 2) __threadfence_block();
-    __syncthreads();
-    c_end += clock64() - t2;
-  }
-  for (int j = tid + 1; j <= k; j += blockDim.x) {
-    const int r = p[j] - 1;
-    if (col_of_row) col_of_row[r] = static_cast<uint64_t>(j - 1);
-    if (decision) {
-      const uint32_t row = order[r];
-      decision[row_ids ? row_ids[row] : row] = (j - 1) / mult;
-    }
-  }
-  if (tid == 0 && stats) {
-    stats[0] = steps;
-    stats[1] = c_step;
-    stats[2] = c_end;
-    stats[3] = c_tab;
-    stats[4] = 0;
-    stats[5] = runs;
-    stats[6] = 0;
-    stats[7] = clock64() - c_start;
-  }
-}
-
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
   const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
@@ -1608,9 +820,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       : "memory");
 }
 
-// ----------------------------------------- K6 multi-warp kernel (n <= 16)
-// The production solver for n <= 16.  Same run-batched Dijkstra steps as the
-// tabled and run kernels (derivation above), but warp x owns block x.  Every
+// ----------------------------------------- K6 multi-warp kernel (n <= 32)
+// The production solver for n <= 32 (one warp per block for n <= 16, one warp
+// per two blocks above).  Run-batched Dijkstra steps: after the argmin picks
+// block w, the next steps are evaluated speculatively assuming w keeps
+// winning (~97% of consecutive steps share the winner block).  While w wins,
+// its key sequence is closed form: with V6_t = v(c_t) << 6,
+//     delta6_t = min(V6_{t-1}, A_w(r_{t-1})) - V6_t      (t >= 2),
+// and every block's relaxed value obeys E^{t+1} = min(E^t - delta6_t, A(r_t)),
+// i.e. with P_t = the sum of delta6 up to t and F = E + P_{t-1},
+//     F^{t+1} = min(F^t, A(r_t) + P_t)      (a prefix min).
+// Step t is the sequential step iff no other block has a smaller key:
+// F_x^t + (B_x - w) > P_t for every x != w (keys carry the block index in
+// their low bits, so they are never equal across blocks).  The first failing
+// t over all blocks bounds the valid prefix, which is then committed exactly
+// as the one-step loop would.  Warp x owns block x.  Every
 // warp keeps all blocks' (G, key offset, cursor) lane-distributed, so each
 // picks the run's winner itself (two redux.sync.min).  In a chunk (lanes =
 // steps of the winner block) every warp runs one scan over the pair monoid
@@ -2074,17 +1298,6 @@ size_t mw_smem_bytes(int k, int n, int mult, int amode) {
   return b;
 }
 
-size_t run_smem_bytes(int k, int n, int mult, int nw, int amode) {
-  const size_t K1 = static_cast<size_t>(k) + 1;
-  auto r = [](size_t b) { return (b + 15) & ~size_t(15); };
-  size_t b = 0;
-  if (amode == 0) b += r(static_cast<size_t>(k) * n * 8);
-  if (amode <= 1) b += r(static_cast<size_t>(k) * n * 8);
-  b += r(K1 * 8) + 3 * r(K1 * 8) + 5 * r(K1 * 4) + r(64 * 4) + r(32 * 8) + r(32 * 4) +
-       r(32 * 32 * 8) + r(32) + r(static_cast<size_t>(nw) * mult * 8) +
-       r(static_cast<size_t>(nw) * 2 * mult * 4);
-  return b;
-}
 
 // ----------------------------------------------------------------- K5 dense
 // The reference loop on an arbitrary k x k matrix: one CTA, columns strided
@@ -2245,18 +1458,6 @@ int max_dyn_smem(int device) {
 
 }  // namespace
 
-size_t tab_smem_bytes(int k, int n, int mult, int nw, int smode) {
-  const size_t K1 = static_cast<size_t>(k) + 1;
-  auto r = [](size_t b) { return (b + 15) & ~size_t(15); };
-  size_t b = 0;
-  if (smode == 0) b += r(static_cast<size_t>(k) * n * 8);
-  const int ast = (n <= 8 && mult <= 255) ? 8 : n;
-  b += r(static_cast<size_t>(k) * ast * 8) + r(K1 * 8) + 2 * r(K1 * 8) +
-       r((K1 + 32) * 8) + 3 * r(K1 * 4) + 2 * r((K1 + 32) * 4) + r(64 * 4) +
-       r(32) + r(static_cast<size_t>(nw) * mult * 8) +
-       r(static_cast<size_t>(nw) * 2 * mult * 4);
-  return b;
-}
 
 size_t fast_smem_bytes(int k, int n, int mult, int nw, int mode) {
   const size_t K1 = static_cast<size_t>(k) + 1;
@@ -2287,13 +1488,6 @@ void launch_hungarian_blocks(HungarianScratch& sc, const double* matrix, int n,
   EDX_LAUNCHED();
   const size_t limit = static_cast<size_t>(max_dyn_smem(device));
   const int nw = std::min(n, kFastMaxWarps);
-  static const int solver_pref = [] {  // EDX_SOLVER=tab|run|mw: A/B override for measurements
-    const char* e = std::getenv("EDX_SOLVER");
-    if (e == nullptr) return 0;
-    if (std::strcmp(e, "tab") == 0) return 1;
-    if (std::strcmp(e, "run") == 0) return 2;
-    return 0;
-  }();
   // the multi-warp kernel: one warp per block for n <= 16, one warp per two
   // blocks (16 warps) for 16 < n <= 32 -- one warp per block at n = 32 costs
   // more in the 32-way exchange than the per-block work it splits
@@ -2301,7 +1495,7 @@ void launch_hungarian_blocks(HungarianScratch& sc, const double* matrix, int n,
     const char* e = std::getenv("EDX_MW_BPW");
     return e && std::strcmp(e, "2") == 0 ? 2 : 1;
   }();
-  if (solver_pref == 0 && n <= 32 && mult <= 512) {
+  if (n <= 32 && mult <= 512) {
     const bool pair = n > 16 || (bpw_pref == 2 && n > 1);
     const int nwarps = pair ? (n + 1) / 2 : n;
     for (int am = 0; am <= 2; ++am) {
@@ -2337,51 +1531,6 @@ void launch_hungarian_blocks(HungarianScratch& sc, const double* matrix, int n,
         else if (am == 1) { launch(k_hungarian_blocks_mw<1, 16, 2>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<1,16,2>"; }
         else { launch(k_hungarian_blocks_mw<2, 16, 2>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<2,16,2>"; }
       }
-      EDX_LAUNCHED();
-      return;
-    }
-  }
-  // n <= 8: the lanes = steps tabled kernel
-  if (solver_pref != 2 && n <= 8 && mult <= 255) {
-    const int nwt = std::min(n, kTabMaxWarps);
-    for (int sm = 0; sm <= 1; ++sm) {
-      const size_t smem = tab_smem_bytes(k, n, mult, nwt, sm);
-      if (smem > limit) continue;
-      auto launch = [&](auto kern) {
-        if (smem > 48 * 1024)
-          EDX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(smem)));
-        kern<<<1, 32 * nwt, smem, s>>>(sc.s64.p, n, mult, k, order, decision, row_ids, col_of_row,
-                                       sc.steps.p, flags, max_scaled);
-      };
-      if (sm == 0) launch(k_hungarian_blocks_tab<1, 0, true>);
-      else launch(k_hungarian_blocks_tab<1, 1, true>);
-      g_kernel_name[kKSolver] = "k_hungarian_blocks_tab";
-      EDX_LAUNCHED();
-      return;
-    }
-  }
-  if (n <= 32 && mult <= 512) {  // the run-batched kernel
-    const int nwr = std::min(n, kRunWarps);
-    for (int am = 0; am <= 2; ++am) {
-      const size_t smem = run_smem_bytes(k, n, mult, nwr, am);
-      if (smem > limit) continue;
-      int64_t* Ag = nullptr;
-      if (am == 2) {
-        sc.arena.ensure(static_cast<size_t>(k) * n * 8);
-        Ag = reinterpret_cast<int64_t*>(sc.arena.p);
-      }
-      auto launch = [&](auto kern) {
-        if (smem > 48 * 1024)
-          EDX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(smem)));
-        kern<<<1, 32 * nwr, smem, s>>>(sc.s64.p, n, mult, k, Ag, order, decision, row_ids,
-                                       col_of_row, sc.steps.p, flags, max_scaled);
-      };
-      if (am == 0) launch(k_hungarian_blocks_run<0>);
-      else if (am == 1) launch(k_hungarian_blocks_run<1>);
-      else launch(k_hungarian_blocks_run<2>);
-      g_kernel_name[kKSolver] = "k_hungarian_blocks_run";
       EDX_LAUNCHED();
       return;
     }

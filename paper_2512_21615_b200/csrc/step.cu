@@ -24,7 +24,6 @@
 // (order-free), and the realised cost is summed on the host in worker order
 // (sim.hpp:208-216).
 #include <cooperative_groups.h>
-#include <cub/block/block_radix_sort.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
@@ -33,7 +32,6 @@
 #include <cstdlib>
 #include <cstring>
 
-#include "bitonic.cuh"
 #include "engine.h"
 #include "step.h"
 
@@ -486,6 +484,7 @@ __global__ void __launch_bounds__(big::kThreads)
       st.hi[q] = 0;
     }
     st.cand = st.nv = st.level = st.bin = st.take_all = st.pinned_err = 0;
+    st.pad[0] = UINT_MAX;  // level at which the worker's selection finished
     st.vc[0] = st.vc[1] = st.vc[2] = 0;
     st.nu[0] = st.nu[1] = 0;
     st.need = w[kWsEvict];
@@ -570,7 +569,7 @@ __global__ void __launch_bounds__(big::kThreads)
   for (uint32_t level = 0;; ++level) {
     // any worker still selecting?  (uniform: every block reads the same state)
     bool any = false;
-    for (int j = 0; j < n; ++j) any |= a.st[j].active != 0;
+    for (int j = 0; j < n; ++j) any |= a.st[j].active != 0 && a.st[j].pad[0] == UINT_MAX;
     if (!any) break;
     const int in = (level + 1) & 1, out = level & 1;  // U buffers: level L reads in, writes out
     // histogram of this level's digit
@@ -578,7 +577,7 @@ __global__ void __launch_bounds__(big::kThreads)
       for (uint32_t u = blockIdx.x; u < static_cast<uint32_t>(n) * chunks; u += gridDim.x) {
         const int j = static_cast<int>(u / chunks);
         const BigState& st = a.st[j];
-        if (!st.active) continue;
+        if (!st.active || st.pad[0] != UINT_MAX) continue;
         const uint32_t size0 = a.ws[j * kWS + kWsSize0], base = (u % chunks) * big::kChunk;
         if (base >= size0) continue;
         for (uint32_t s = base + threadIdx.x; s < base + big::kChunk && s < size0; s += blockDim.x) {
@@ -593,7 +592,7 @@ __global__ void __launch_bounds__(big::kThreads)
     } else {
       for (int j = 0; j < n; ++j) {
         const BigState& st = a.st[j];
-        if (!st.active) continue;
+        if (!st.active || st.pad[0] != UINT_MAX) continue;
         const uint32_t cnt = st.nu[in];
         const uint32_t units = (cnt + big::kChunk - 1) / big::kChunk;
         const u128* K = a.ukey[in] + static_cast<uint64_t>(j) * a.capacity;
@@ -610,9 +609,17 @@ __global__ void __launch_bounds__(big::kThreads)
     grid.sync();
     // the bin of each worker's need-th key
     for (int j = blockIdx.x; j < n; j += gridDim.x) {
-      if (!a.st[j].active) continue;
+      if (!a.st[j].active || a.st[j].pad[0] != UINT_MAX) continue;
       big_select(a, j, scan_sh);
-      if (threadIdx.x == 0) a.st[j].nu[out] = 0;
+      if (threadIdx.x == 0) {
+        BigState& st = a.st[j];
+        st.nu[out] = 0;
+        if (!st.take_all && level >= (128 + big::kDigit - 1) / big::kDigit - 1) {
+          atomicOr(a.flags + kFlagInternal, 1);  // unique keys: unreachable
+          st.take_all = 1;
+        }
+        if (st.take_all) st.pad[0] = level;
+      }
     }
     grid.sync();
     // compaction: lower bins are victims, the bin itself is undecided
@@ -637,7 +644,7 @@ __global__ void __launch_bounds__(big::kThreads)
       for (uint32_t u = blockIdx.x; u < static_cast<uint32_t>(n) * chunks; u += gridDim.x) {
         const int j = static_cast<int>(u / chunks);
         BigState& st = a.st[j];
-        if (!st.active) continue;
+        if (!st.active || (st.pad[0] != UINT_MAX && st.pad[0] != level)) continue;
         const BigState stc = st;
         const uint32_t size0 = a.ws[j * kWS + kWsSize0], base = (u % chunks) * big::kChunk;
         if (base >= size0) continue;
@@ -655,7 +662,7 @@ __global__ void __launch_bounds__(big::kThreads)
     } else {
       for (int j = 0; j < n; ++j) {
         BigState& st = a.st[j];
-        if (!st.active) continue;
+        if (!st.active || (st.pad[0] != UINT_MAX && st.pad[0] != level)) continue;
         const BigState stc = st;
         const uint32_t cnt = stc.nu[in];
         const uint32_t units = (cnt + big::kChunk - 1) / big::kChunk;
@@ -678,14 +685,6 @@ __global__ void __launch_bounds__(big::kThreads)
       }
     }
     grid.sync();
-    if (gtid < static_cast<uint64_t>(n)) {
-      BigState& st = a.st[gtid];
-      if (st.active && (st.take_all || level >= (128 + big::kDigit - 1) / big::kDigit - 1)) {
-        if (!st.take_all) atomicOr(a.flags + kFlagInternal, 1);  // unique keys: unreachable
-        st.active = 0;
-      }
-    }
-    grid.sync();
   }
 
   // ---- results in the per-worker scalars
@@ -704,34 +703,40 @@ __device__ __forceinline__ int width_of(uint32_t lo, uint32_t hi) {
   return hi > lo ? 32 - __clz(hi - lo) : 0;
 }
 
-// Victim selection for caches of up to kSelCap entries: one CTA per worker.
-// The CTA finds its non-pinned entries, the per-worker value ranges of
-// (mark, frequency, last_access, id), packs each VictimKey (cache.hpp:47-58)
-// order-preservingly -- version (= the worker's latest bit) above mark above
-// frequency above last_access above id -- and block-radix-sorts them in
-// shared memory; non-candidates carry bit W and sort last.  The first E_j
-// sorted slots are the victims, in victim order.  No host round trip and no
-// device-wide sort.
+// Victim selection for caches of up to kSelCap entries: one CTA per worker,
+// every entry in registers (kSelItems per thread), no grid-wide sync.  The
+// CTA classifies its entries (pinned = stamped by k_classify this
+// iteration), reduces the candidates' field ranges, builds each VictimKey
+// (cache.hpp:47-58) as a W <= 128-bit MSB-aligned integer (version | mark |
+// freq | last | id, fields minus their minima) and radix-selects the E_j-th
+// least key 8 bits at a time (keys are unique -- they end in the id); the
+// victims are the keys at or below it, written unsorted with the class
+// counts k_evict_contrib needs (see k_big_select).  Any key width works.
 constexpr int kSelThreads = 1024, kSelItems = 12;
 constexpr uint64_t kSelCap = static_cast<uint64_t>(kSelThreads) * kSelItems;
-constexpr uint32_t kSelSmall = 4096;  // victims per worker selected + bitonic-sorted
-using SelSort = cub::BlockRadixSort<uint64_t, kSelThreads, kSelItems, uint32_t>;
+
+__device__ __forceinline__ uint32_t digit8(u128 k, int done) {
+  return static_cast<uint32_t>(k >> (120 - done)) & 0xFFu;
+}
+__device__ __forceinline__ u128 top_bits(u128 k, int done) {
+  return done == 0 ? u128(0) : (k >> (128 - done));
+}
 
 __global__ void __launch_bounds__(kSelThreads, 1)
     k_select_victims(uint64_t capacity, uint32_t* __restrict__ ws, const uint32_t* __restrict__ sid,
                      const uint32_t* __restrict__ smark, const uint32_t* __restrict__ sfreq,
                      const uint32_t* __restrict__ slast, const ulonglong2* __restrict__ ol,
-                     const uint32_t* __restrict__ slot2id,
-                     const int32_t* __restrict__ first_pos, const uint32_t* __restrict__ uidx,
-                     uint64_t ucap, const int32_t* __restrict__ need_first,
-                     const uint32_t* __restrict__ ins_scan,
-                     uint32_t* __restrict__ cand_slot_sorted, int* __restrict__ flags) {
+                     const uint32_t* __restrict__ slot2id, const uint32_t* __restrict__ pin,
+                     const uint32_t* __restrict__ clock_dev, const uint32_t* __restrict__ cur_mark,
+                     const uint32_t* __restrict__ ins_scan, uint32_t* __restrict__ victims,
+                     int* __restrict__ flags) {
   pdl_wait();
   pdl_trigger();
-  extern __shared__ __align__(16) uint8_t smem[];
-  auto& temp = *reinterpret_cast<typename SelSort::TempStorage*>(smem);
+  extern __shared__ u128 skey[];  // kSelItems * kSelThreads keys, item-major
   __shared__ uint32_t part[kSelThreads / 32][9];
   __shared__ uint32_t tot[9];
+  __shared__ uint32_t hist[256];
+  __shared__ uint32_t s_bin, s_rank, s_take, s_nv, s_vc[3];
   const int j = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint32_t* w = ws + j * kWS;
   // inserts and evictions of worker j (evict_for, cache.hpp:152-170)
@@ -743,54 +748,41 @@ __global__ void __launch_bounds__(kSelThreads, 1)
     w[kWsInserts] = ins;
     w[kWsInsBase] = ins0;
     w[kWsEvict] = E;
+    w[kWsCandOff] = static_cast<uint32_t>(gb);
+    w[kWsVa] = w[kWsVb] = w[kWsVc] = 0;
   }
   if (E == 0) {
-    if (tid == 0) {
-      w[kWsCand] = 0;
-      w[kWsCandOff] = static_cast<uint32_t>(gb);
-    }
+    if (tid == 0) w[kWsCand] = 0;
     return;
   }
-  const uint32_t size0 = w[kWsSize0];
-  bool cf[kSelItems];
+  const uint32_t size0 = w[kWsSize0], stamp = *clock_dev + 1u, cm = cur_mark[j];
+  unsigned cfm = 0;  // candidate items of this thread (bit k)
+  // an item's (version, mark, freq, last, id); read twice -- for the ranges,
+  // then for the keys -- rather than held in registers across the reduction
+  auto fields = [&](int k, uint32_t (&fo)[5]) {
+    const uint32_t sl = tid * kSelItems + k;
+    const uint32_t slot = sid[gb + sl];
+    fo[0] = static_cast<uint32_t>((ol[slot].y >> j) & 1ULL);
+    fo[1] = smark[gb + sl];
+    fo[2] = sfreq[gb + sl];
+    fo[3] = slast[gb + sl];
+    fo[4] = slot2id ? slot2id[slot] : slot;  // VictimKey's id: the embedding id
+  };
   // v[0..3] = min of mark, freq, last, id; v[4..7] = max; v[8] = candidates
   uint32_t v[9] = {UINT_MAX, UINT_MAX, UINT_MAX, UINT_MAX, 0, 0, 0, 0, 0};
-  {
-    // level by level so all of a thread's items have their loads in flight
-    // together (the pinned test is a chain of four dependent gathers)
-    uint32_t id[kSelItems];
-    int32_t fp[kSelItems];
 #pragma unroll
-    for (int k = 0; k < kSelItems; ++k) {
-      const uint32_t sl = tid * kSelItems + k;
-      id[k] = sl < size0 ? sid[gb + sl] : 0u;
-    }
+  for (int k = 0; k < kSelItems; ++k) {
+    const uint32_t sl = tid * kSelItems + k;
+    if (sl < size0 && pin[gb + sl] != stamp) {
+      cfm |= 1u << k;
+      uint32_t fo[5];
+      fields(k, fo);
 #pragma unroll
-    for (int k = 0; k < kSelItems; ++k)
-      fp[k] = tid * kSelItems + k < size0 ? first_pos[id[k]] : INT_MAX;
-#pragma unroll
-    for (int k = 0; k < kSelItems; ++k)
-      fp[k] = fp[k] != INT_MAX ? static_cast<int32_t>(uidx[fp[k]]) : -1;
-#pragma unroll
-    for (int k = 0; k < kSelItems; ++k) {
-      const bool pinned = fp[k] >= 0 &&
-          need_first[static_cast<uint64_t>(j) * ucap + static_cast<uint32_t>(fp[k])] != INT_MAX;
-      cf[k] = tid * kSelItems + k < size0 && !pinned;
-    }
-#pragma unroll
-    for (int k = 0; k < kSelItems; ++k) {
-      if (cf[k]) {
-        const uint32_t sl = tid * kSelItems + k;
-        // VictimKey's id is the embedding id (slot2id in hashed-id engines)
-        const uint32_t rid = slot2id ? slot2id[id[k]] : id[k];
-        const uint32_t f[4] = {smark[gb + sl], sfreq[gb + sl], slast[gb + sl], rid};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          v[q] = min(v[q], f[q]);
-          v[4 + q] = max(v[4 + q], f[q]);
-        }
-        ++v[8];
+      for (int q = 0; q < 4; ++q) {
+        v[q] = min(v[q], fo[1 + q]);
+        v[4 + q] = max(v[4 + q], fo[1 + q]);
       }
+      ++v[8];
     }
   }
 #pragma unroll
@@ -813,135 +805,130 @@ __global__ void __launch_bounds__(kSelThreads, 1)
   }
   __syncthreads();
   const uint32_t cnt = tot[8];
-  const int wm = width_of(tot[0], tot[4]), wf = width_of(tot[1], tot[5]);
-  const int wl = width_of(tot[2], tot[6]), wi = width_of(tot[3], tot[7]);
-  const int W = 1 + wm + wf + wl + wi;  // <= 1 + 4 * 32
-  if (W > 63) {
+  if (cnt < E) {  // every remaining entry is pinned (cache.hpp:164)
+    if (tid == 0) {
+      w[kWsCand] = cnt;
+      atomicOr(flags + kFlagPinned, 1);
+    }
+    return;
+  }
+  int wd[4], W = 1;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    wd[q] = width_of(tot[q], tot[4 + q]);
+    W += wd[q];
+  }
+  if (W > 128) {  // only reachable at ~2^32 epochs
     if (tid == 0) atomicOr(flags + kFlagKeyRange, 1);
     return;
   }
-  uint64_t keys[kSelItems];
-  uint32_t slots[kSelItems];
-#pragma unroll
+#pragma unroll 4
   for (int k = 0; k < kSelItems; ++k) {
-    const uint32_t sl = tid * kSelItems + k;
-    slots[k] = sl;
-    keys[k] = 1ULL << W;  // not a candidate: after every candidate
-    if (cf[k]) {
-      const uint32_t id = sid[gb + sl];
-      const uint32_t rid = slot2id ? slot2id[id] : id;
-      uint64_t key = (ol[id].y >> j) & 1ULL;  // version: a stale copy goes first
-      key = (key << wm) | (smark[gb + sl] - tot[0]);
-      key = (key << wf) | (sfreq[gb + sl] - tot[1]);
-      key = (key << wl) | (slast[gb + sl] - tot[2]);
-      key = (key << wi) | (rid - tot[3]);
-      keys[k] = key;
-    }
+    if (!((cfm >> k) & 1u)) continue;
+    uint32_t fo[5];
+    fields(k, fo);
+    u128 x = fo[0];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) x = (x << wd[q]) | (fo[1 + q] - tot[q]);
+    skey[k * kSelThreads + tid] = x << (128 - W);
   }
-  const uint32_t take = min(E, cnt);
-  if (take > kSelSmall) {  // many victims: sort every key
-    SelSort(temp).Sort(keys, slots, 0, W + 1);
+  // MSB radix select of the E-th least key, 8 bits per level
+  u128 prefix = 0;
+  uint32_t rank = E;
+  int done = 0;
+  bool take_all = false;
+  while (!take_all && done < W) {
+    for (int x = tid; x < 256; x += kSelThreads) hist[x] = 0;
+    __syncthreads();
 #pragma unroll
     for (int k = 0; k < kSelItems; ++k) {
-      const uint32_t r = tid * kSelItems + k;  // blocked arrangement: sorted rank
-      if (r < take) cand_slot_sorted[gb + r] = slots[k];
+      const u128 key = skey[k * kSelThreads + tid];
+      const bool in = ((cfm >> k) & 1u) && top_bits(key, done) == prefix;
+      const int bin = in ? static_cast<int>(digit8(key, done)) : -1;
+      const unsigned grp = __match_any_sync(0xffffffffu, bin);
+      if (in && lane == __ffs(grp) - 1) atomicAdd(&hist[bin], static_cast<uint32_t>(__popc(grp)));
     }
-  } else if (take > 0) {
-    // Radix select of the take-th least candidate key (8-bit digits, most
-    // significant first; keys are unique -- they end in the id), then a
-    // bitonic sort of the take keys at or below it.
-    uint32_t* hist = reinterpret_cast<uint32_t*>(smem);
-    uint64_t* sk = reinterpret_cast<uint64_t*>(smem + 256 * sizeof(uint32_t));
-    uint32_t* ss = reinterpret_cast<uint32_t*>(sk + kSelSmall);
-    __shared__ uint32_t s_bin, s_rank, s_cnt;
-    uint64_t prefix = 0;
-    uint32_t rank = take;  // 1-based rank among the keys under `prefix`
-    for (int done = 0; done < W;) {
-      const int nb = min(8, W - done), shift = W - done - nb;
-      for (int x = tid; x < 256; x += kSelThreads) hist[x] = 0;
-      __syncthreads();
-      // the leading digits are shared by most keys: one shared atomic per
-      // (warp, bin) group instead of one per key
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t h[8], sum = 0;
 #pragma unroll
-      for (int k = 0; k < kSelItems; ++k) {
-        const bool in = cf[k] && (keys[k] >> (shift + nb)) == prefix;
-        const int bin = in ? static_cast<int>((keys[k] >> shift) & ((1u << nb) - 1u)) : -1;
-        const unsigned grp = __match_any_sync(0xffffffffu, bin);
-        if (in && lane == __ffs(grp) - 1) atomicAdd(&hist[bin], static_cast<uint32_t>(__popc(grp)));
+      for (int q = 0; q < 8; ++q) {
+        h[q] = hist[8 * lane + q];
+        sum += h[q];
       }
-      __syncthreads();
-      if (warp == 0) {
-        uint32_t h[8], sum = 0;
+      uint32_t inc = sum;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, off);
+        if (lane >= off) inc += y;
+      }
+      uint32_t run = inc - sum;
+      if (run < rank && rank <= inc) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          h[q] = hist[8 * lane + q];
-          sum += h[q];
-        }
-        uint32_t inc = sum;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, inc, off);
-          if (lane >= off) inc += y;
-        }
-        uint32_t run = inc - sum;
-        if (run < rank && rank <= inc) {
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            if (run + h[q] >= rank) {
-              s_bin = 8 * lane + q;
-              s_rank = rank - run;
-              break;
-            }
-            run += h[q];
+          if (run + h[q] >= rank) {
+            s_bin = 8 * lane + q;
+            s_rank = rank - run;
+            s_take = (rank - run == h[q]) ? 1u : 0u;
+            break;
           }
+          run += h[q];
         }
       }
-      __syncthreads();
-      prefix = (prefix << nb) | s_bin;
-      rank = s_rank;
-      done += nb;
     }
-    if (tid == 0) s_cnt = 0;
     __syncthreads();
-#pragma unroll
-    for (int k = 0; k < kSelItems; ++k) {
-      const bool sel = cf[k] && keys[k] <= prefix;
-      const unsigned bal = __ballot_sync(0xffffffffu, sel);
-      uint32_t base = 0;
-      if (lane == 0 && bal) base = atomicAdd(&s_cnt, static_cast<uint32_t>(__popc(bal)));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (sel) {
-        const uint32_t q = base + __popc(bal & ((1u << lane) - 1u));
-        sk[q] = keys[k];
-        ss[q] = slots[k];
-      }
-    }
-    // bitonic sort of the take keys, padded to P >= 128 with all-ones keys
-    // (which sort last); keys are unique
-    uint32_t P = 128;
-    while (P < take) P <<= 1;
-    for (uint32_t x = take + tid; x < P; x += kSelThreads) sk[x] = ~0ULL;
+    prefix = (prefix << 8) | s_bin;
+    rank = s_rank;
+    take_all = s_take != 0;
+    done += 8;
     __syncthreads();
-    block_bitonic_sort(sk, ss, P);
-    for (uint32_t r = tid; r < take; r += kSelThreads) cand_slot_sorted[gb + r] = ss[r];
   }
+  // victims: keys whose top `done` bits are at or below the prefix
   if (tid == 0) {
-    w[kWsCand] = cnt;
-    w[kWsCandOff] = static_cast<uint32_t>(gb);
-    if (cnt < E) atomicOr(flags + kFlagPinned, 1);
+    s_nv = 0;
+    s_vc[0] = s_vc[1] = s_vc[2] = 0;
+  }
+  __syncthreads();
+  uint32_t vc[3] = {0, 0, 0};
+  const int mshift = 128 - 1 - wd[0];  // the mark field's position in a key
+#pragma unroll
+  for (int k = 0; k < kSelItems; ++k) {
+    const u128 key = skey[k * kSelThreads + tid];
+    const bool sel = ((cfm >> k) & 1u) && top_bits(key, done) <= prefix;
+    const unsigned bal = __ballot_sync(0xffffffffu, sel);
+    uint32_t base = 0;
+    if (lane == 0 && bal) base = atomicAdd(&s_nv, static_cast<uint32_t>(__popc(bal)));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (sel) {
+      victims[gb + base + __popc(bal & ((1u << lane) - 1u))] = tid * kSelItems + k;
+      const uint32_t vr = static_cast<uint32_t>(key >> 127);
+      const uint32_t mk = wd[0] ? static_cast<uint32_t>(key >> mshift) & ((wd[0] == 32) ? 0xFFFFFFFFu : ((1u << wd[0]) - 1u)) : 0u;
+      const bool cur = mk + tot[0] == cm;
+      if (vr == 0) ++vc[cur ? 1 : 0];
+      else if (!cur) ++vc[2];
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    vc[q] = __reduce_add_sync(0xffffffffu, vc[q]);
+    if (lane == 0 && vc[q]) atomicAdd(&s_vc[q], vc[q]);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (s_nv != E) atomicOr(flags + kFlagInternal, 1);  // unique keys: exactly E
+    w[kWsCand] = E;
+    w[kWsVa] = s_vc[0];
+    w[kWsVb] = s_vc[1];
+    w[kWsVc] = s_vc[2];
   }
 }
-
 
 // evicting insert contribution: +1 for the insert, -1 if its victim carries
 // the current mark (cache.hpp:111,175), evaluated before any advance.
 __global__ void k_evict_contrib(const uint64_t* __restrict__ items,
                                 const unsigned long long* counters_ro, int n,
                                 const uint8_t* __restrict__ type, const uint32_t* __restrict__ ins_scan,
-                                const uint32_t* __restrict__ ws, const uint32_t* __restrict__ cand_slot,
-                                const uint32_t* __restrict__ smark, uint64_t capacity,
-                                const uint32_t* __restrict__ cur_mark, int by_counts,
-                                int32_t* __restrict__ contrib) {
+                                const uint32_t* __restrict__ ws, int32_t* __restrict__ contrib) {
   pdl_wait();
   pdl_trigger();
   const uint64_t N = counters_ro[3 * n + 2];
@@ -953,14 +940,9 @@ __global__ void k_evict_contrib(const uint64_t* __restrict__ items,
   if (e < w[kWsFree]) return;
   const uint32_t t = e - w[kWsFree];
   if (t >= w[kWsCand]) return;  // reported through kFlagPinned
-  bool cur;
-  if (by_counts) {  // unsorted victims of a large cache: the class of the t-th
-    const uint32_t a = w[kWsVa], b = a + w[kWsVb], c = b + w[kWsVc];
-    cur = (t >= a && t < b) || t >= c;
-  } else {
-    const uint32_t vs = cand_slot[w[kWsCandOff] + t];
-    cur = smark[static_cast<uint64_t>(j) * capacity + vs] == cur_mark[j];
-  }
+  // the t-th least victim's class (the victims themselves are unsorted)
+  const uint32_t a = w[kWsVa], b = a + w[kWsVb], c = b + w[kWsVc];
+  const bool cur = (t >= a && t < b) || t >= c;
   contrib[q] = cur ? 0 : 1;
 }
 
@@ -1152,16 +1134,9 @@ __global__ void k_fill_i32(int32_t* p, uint64_t n, int32_t v) {
   if (x < n) p[x] = v;
 }
 
-// The one-CTA-per-worker selection (sorted victims, keys <= 63 bits) for
-// caches of <= kSelCap entries: EDX_VICTIMS=cta (A/B measurement only; the
-// cooperative selection handles every size and key width).
-bool use_cta_select(const edx_engine* e) {
-  static const bool cta = [] {
-    const char* v = std::getenv("EDX_VICTIMS");
-    return v && std::strcmp(v, "cta") == 0;
-  }();
-  return cta && e->capacity <= kSelCap;
-}
+// Caches of <= kSelCap entries select in one CTA per worker (k_select_victims);
+// larger ones with the cooperative grid kernel (k_big_select).
+bool use_cta_select(const edx_engine* e) { return e->capacity <= kSelCap; }
 
 }  // namespace
 
@@ -1212,10 +1187,13 @@ void step_init_state(edx_engine* e) {
   const uint64_t cand = n * e->capacity;
   s.cand_slot_sorted.ensure(cand);
   s.cand_count.ensure(cand);  // the victim-id list
-  if (!use_cta_select(e)) {
-    // pin stamps per entry and the cooperative selection's scratch
-    c.pin.ensure(cand);
-    EDX_CUDA(cudaMemsetAsync(c.pin.p, 0, cand * sizeof(uint32_t), e->stream));
+  // pin stamps per entry (k_classify marks this iteration's working set)
+  c.pin.ensure(cand);
+  EDX_CUDA(cudaMemsetAsync(c.pin.p, 0, cand * sizeof(uint32_t), e->stream));
+  if (use_cta_select(e)) {
+    EDX_CUDA(cudaFuncSetAttribute(k_select_victims, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kSelItems * kSelThreads * sizeof(u128))));
+  } else {  // the cooperative selection's scratch
     s.big_state.ensure(n * sizeof(BigState));
     s.big_hist.ensure(n * big::kBins);
     for (int b = 0; b < 2; ++b) {
@@ -1226,7 +1204,9 @@ void step_init_state(edx_engine* e) {
     EDX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_big_select, big::kThreads, 0));
     EDX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device));
     if (per_sm < 1) throw Error(EDX_CUDA_ERROR, "victim selection kernel cannot be resident");
-    s.big_grid = static_cast<uint64_t>(std::min(per_sm, 2)) * static_cast<uint64_t>(sms);
+    // enough CTAs for the work units, at most two per SM
+    const uint64_t units = n * ((e->capacity + big::kChunk - 1) / big::kChunk);
+    s.big_grid = std::max<uint64_t>(1, std::min<uint64_t>(units, static_cast<uint64_t>(std::min(per_sm, 2)) * sms));
   }
   s.cand_off.ensure(128);  // [0,64): workers 0..n-1; [64,128): evicting workers (large caches)
   std::vector<int32_t> wl(n);
@@ -1234,13 +1214,6 @@ void step_init_state(edx_engine* e) {
   EDX_CUDA(cudaMemcpyAsync(s.cand_off.p, wl.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice,
                            e->stream));
   EDX_CUDA(cudaStreamSynchronize(e->stream));
-  if (use_cta_select(e)) {
-    static const size_t sel_smem =
-        std::max(sizeof(typename SelSort::TempStorage),
-                 256 * sizeof(uint32_t) + kSelSmall * (sizeof(uint64_t) + sizeof(uint32_t)));
-    EDX_CUDA(cudaFuncSetAttribute(k_select_victims, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(sel_smem)));
-  }
 }
 
 namespace {
@@ -1344,7 +1317,7 @@ void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
       s.need_key_sorted.p, s.counters.p, n, e->cur_ids, s.first_pos.p, s.uidx_of_pos.p, ucap,
       s.need_cnt.p, e->ol.p, e->res.p, e->id_space, c.slot_of.p, e->capacity, c.smark.p,
       c.cur_mark.p, s.need_type.p, s.flag_scan.p, s.need_contrib.p, s.counters.p,
-      use_cta_select(e) ? nullptr : c.pin.p, e->d_clock.p);
+      c.pin.p, e->d_clock.p);
   EDX_LAUNCHED();
   launches += 2;
   // insert ordinals: exclusive scan over the (worker-grouped) need items
@@ -1364,11 +1337,11 @@ void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
   const int32_t* d_wlist = reinterpret_cast<const int32_t*>(s.cand_off.p);
   int nw = n;  // workers the victim kernels visit
   if (use_cta_select(e)) {
-    launch_pdl(k_select_victims, n, kSelThreads, sizeof(typename SelSort::TempStorage), st, 
-        e->capacity, s.wscalars.p, c.sid.p, c.smark.p, c.sfreq.p, c.slast.p, e->ol.p,
-        e->hashed ? e->idt.slot2id.p : nullptr,
-        s.first_pos.p, s.uidx_of_pos.p, ucap, s.need_first.p, s.ins_rank.p, s.cand_slot_sorted.p,
-        e->flags.p);
+    launch_pdl(k_select_victims, n, kSelThreads, kSelItems * kSelThreads * sizeof(u128), st,
+               e->capacity, s.wscalars.p, c.sid.p,
+               c.smark.p, c.sfreq.p, c.slast.p, e->ol.p, e->hashed ? e->idt.slot2id.p : nullptr,
+               c.pin.p, e->d_clock.p, c.cur_mark.p, s.ins_rank.p, s.cand_slot_sorted.p,
+               e->flags.p);
     EDX_LAUNCHED();
     launches += 1;
   } else {
@@ -1408,10 +1381,8 @@ void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
     EDX_CUDA(cudaLaunchKernelEx(&cfg, k_big_select, ba));
     launches += 1;
   }
-  launch_pdl(k_evict_contrib, grid_for(T), kT, 0, st, s.need_key_sorted.p, s.counters.p, n, s.need_type.p,
-                                              s.ins_rank.p, s.wscalars.p, s.cand_slot_sorted.p,
-                                              c.smark.p, e->capacity, c.cur_mark.p,
-                                              use_cta_select(e) ? 0 : 1, s.need_contrib.p);
+  launch_pdl(k_evict_contrib, grid_for(T), kT, 0, st, s.need_key_sorted.p, s.counters.p, n,
+             s.need_type.p, s.ins_rank.p, s.wscalars.p, s.need_contrib.p);
   EDX_LAUNCHED();
   cub_call(e, [&](void* tmp, size_t& b) {
     return cub::DeviceScan::ExclusiveSum(tmp, b, s.need_contrib.p,
