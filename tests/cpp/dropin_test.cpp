@@ -3,6 +3,9 @@
 // against include/embdispatch/ + libedx.so, checked against the oracle
 // (oracle/edx_oracle.c, the plain-C restatement of the reference) on the
 // same inputs.  Exit code 0 = every iteration bit-identical.
+#include <dlfcn.h>
+#include <unistd.h>
+
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -261,7 +264,45 @@ static void worker_cache_kats() {
 // decision and report checked against the oracle simulator driven with the
 // same decision (the acceptance binary itself times this loop against a 60 s
 // limit that its CPU replay oracle alone exceeds; this isolates equivalence).
+// The oracle entry points the acceptance loop uses: the compiled reference
+// (oracle/_ref/libedx_ref.so, std::set victim order) when it is present --
+// the plain-C restatement's linear victim scan is slow at 4,000-entry caches.
+struct Orc {
+  int (*sim_create)(const orc_cluster_config*, orc_sim**) = orc_sim_create;
+  void (*sim_destroy)(orc_sim*) = orc_sim_destroy;
+  int (*sim_build_matrix)(orc_sim*, const uint32_t*, const uint64_t*, uint64_t, double*) =
+      orc_sim_build_matrix;
+  int (*sim_hitgreedy)(orc_sim*, const uint32_t*, const uint64_t*, uint64_t, int32_t*) =
+      orc_sim_hitgreedy;
+  int (*sim_step)(orc_sim*, const uint32_t*, const uint64_t*, uint64_t, const int32_t*,
+                  orc_report*) = orc_sim_step;
+  int (*ecomix)(const orc_cluster_config*, uint64_t, uint64_t, const double*, const uint64_t*,
+                int32_t*) = orc_ecomix;
+  const char* kind = "restatement";
+};
+
+static Orc load_reference_oracle() {
+  Orc o;
+  char exe[4096] = {0};
+  const ssize_t len = readlink("/proc/self/exe", exe, sizeof exe - 1);
+  if (len <= 0) return o;
+  std::string dir(exe, static_cast<size_t>(len));
+  dir = dir.substr(0, dir.rfind('/'));
+  void* h = dlopen((dir + "/../../oracle/_ref/libedx_ref.so").c_str(), RTLD_NOW | RTLD_LOCAL);
+  if (!h) return o;
+  o.sim_create = reinterpret_cast<decltype(o.sim_create)>(dlsym(h, "orc_sim_create"));
+  o.sim_destroy = reinterpret_cast<decltype(o.sim_destroy)>(dlsym(h, "orc_sim_destroy"));
+  o.sim_build_matrix = reinterpret_cast<decltype(o.sim_build_matrix)>(dlsym(h, "orc_sim_build_matrix"));
+  o.sim_hitgreedy = reinterpret_cast<decltype(o.sim_hitgreedy)>(dlsym(h, "orc_sim_hitgreedy"));
+  o.sim_step = reinterpret_cast<decltype(o.sim_step)>(dlsym(h, "orc_sim_step"));
+  o.ecomix = reinterpret_cast<decltype(o.ecomix)>(dlsym(h, "orc_ecomix"));
+  o.kind = "compiled reference";
+  return o;
+}
+
 static void acceptance_default_loop() {
+  const Orc orc = load_reference_oracle();
+  std::printf("acceptance loop oracle: %s\n", orc.kind);
   ClusterConfig cfg;
   cfg.n = 8;
   cfg.m = 128;
@@ -277,7 +318,7 @@ static void acceptance_default_loop() {
     orc_cluster_config oc{cfg.n, cfg.m, cfg.bandwidths_bps.data(), cfg.n, 0, cfg.d_tran_bytes,
                           cfg.cache_capacity, mech.alpha};
     orc_sim* oracle = nullptr;
-    orc_sim_create(&oc, &oracle);
+    orc.sim_create(&oc, &oracle);
     ZipfStream stream(spec, cfg);
     std::vector<EmbeddingSample> samples;
     std::uint64_t iter = 0;
@@ -299,11 +340,11 @@ static void acceptance_default_loop() {
       std::vector<int32_t> od(samples.size());
       if (mech.kind == Mechanism::Kind::kEcoMix) {
         std::vector<double> om(samples.size() * cfg.n);
-        orc_sim_build_matrix(oracle, ids.data(), offs.data(), samples.size(), om.data());
+        orc.sim_build_matrix(oracle, ids.data(), offs.data(), samples.size(), om.data());
         bad += std::memcmp(om.data(), matrix.values.data(), om.size() * 8) != 0;
-        orc_ecomix(&oc, samples.size(), cfg.n, om.data(), nullptr, od.data());
+        orc.ecomix(&oc, samples.size(), cfg.n, om.data(), nullptr, od.data());
       } else if (mech.kind == Mechanism::Kind::kHitGreedy) {
-        orc_sim_hitgreedy(oracle, ids.data(), offs.data(), samples.size(), od.data());
+        orc.sim_hitgreedy(oracle, ids.data(), offs.data(), samples.size(), od.data());
       } else {
         od.assign(decision.worker_of_sample.begin(), decision.worker_of_sample.end());
       }
@@ -311,12 +352,12 @@ static void acceptance_default_loop() {
       std::vector<uint64_t> mp(8), up(8), ep(8);
       std::vector<double> cw(8);
       orc_report orep{0, 0, 0, 0, 0, 0, 0.0, mp.data(), up.data(), ep.data(), cw.data()};
-      orc_sim_step(oracle, ids.data(), offs.data(), samples.size(), od.data(), &orep);
+      orc.sim_step(oracle, ids.data(), offs.data(), samples.size(), od.data(), &orep);
       bad += !(rep.miss_pull_w == mp && rep.update_push_w == up && rep.evict_push_w == ep &&
                rep.cost_s == orep.cost_s && rep.hits == orep.hits);
       ++iter;
     }
-    orc_sim_destroy(oracle);
+    orc.sim_destroy(oracle);
     EXPECT(bad == 0 && iter == 200, "acceptance loop %s: %d mismatches over %d iterations", name, bad,
            static_cast<int>(iter));
   }

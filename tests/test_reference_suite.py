@@ -59,23 +59,38 @@ def test_reference_device_suite(suite):
     _check_suite(suite)
 
 
-# Criteria the reference itself fails here: 5 (3.26% < 10%
-# reduction) and 6 (2/50 monotone matrices) are properties of the algorithm,
-# not of the implementation, so the drop-in must reproduce those outcomes too.
-REFERENCE_FAILS = {5, 6}
+# acceptance.cpp as the reference itself runs it (tests/golden/reference_acceptance.txt:
+# reftests_ref/acceptance, built against the reference headers, on this
+# container's host): criteria 4 (its CPU replay oracle alone exceeds the 60 s
+# limit: 744 s there), 5 (3.26% < 10%) and 6 (2/50 monotone) FAIL in the
+# reference.  The drop-in must reach the same verdict on every criterion and
+# the same numbers wherever they are results rather than timings.
+GOLDEN_ACCEPTANCE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                                 "reference_acceptance.txt")
+TIMED = {1: r"[\d.e+-]+ s$", 4: r"[\d.e+-]+ s$", 8: None}  # criterion -> timing field (None: all)
+
+
+def _criteria(text):
+    return {int(c): (v, d.strip()) for v, c, d in
+            re.findall(r"^(PASS|FAIL)  criterion (\d+)\s+(.*)$", text, re.M)}
 
 
 @pytest.mark.gpu
 def test_reference_acceptance():
     """acceptance.cpp criteria 1-9 against the drop-in; the
     default-config 200-iteration runs of 5 mechanisms are checked against the
-    reference's naive replay oracle inside criterion 4."""
+    reference's naive replay oracle inside criterion 4 (and iteration by
+    iteration against the compiled reference in tests/cpp/dropin_test)."""
     path = _binary("acceptance")
     r = subprocess.run([path], capture_output=True, text=True, timeout=1500)
-    lines = re.findall(r"^(PASS|FAIL)  criterion (\d+)\s+(.*)$", r.stdout, re.M)
-    assert len(lines) == 9, r.stdout[-4000:] + r.stderr[-2000:]
-    for verdict, crit, detail in lines:
-        crit = int(crit)
-        if crit in REFERENCE_FAILS:
-            continue
-        assert verdict == "PASS", f"criterion {crit}: {detail}"
+    got = _criteria(r.stdout)
+    want = _criteria(open(GOLDEN_ACCEPTANCE).read())
+    assert sorted(got) == list(range(1, 10)), r.stdout[-4000:] + r.stderr[-2000:]
+    for c in range(1, 10):
+        (gv, gd), (wv, wd) = got[c], want[c]
+        assert gv == wv, f"criterion {c}: drop-in {gv} ({gd}) vs reference {wv} ({wd})"
+        if c in TIMED:
+            if TIMED[c] is None:
+                continue
+            gd, wd = re.sub(TIMED[c], "<t>", gd), re.sub(TIMED[c], "<t>", wd)
+        assert gd == wd, f"criterion {c}: drop-in '{gd}' vs reference '{wd}'"
