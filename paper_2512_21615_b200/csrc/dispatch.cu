@@ -1,6 +1,5 @@
 // K3 row ordering, K4 capacity-bounded greedy, decision checks, and the
 // EcoMix orchestration (assign.hpp:162-298).
-#include <cooperative_groups.h>
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
@@ -36,7 +35,11 @@ void sort_rows_by_gap(SortScratch& sc, const uint64_t* keys_in, const uint32_t* 
 // close and the next round starts at that row.  Rows after an exhaustion that
 // did not pick the exhausted worker keep their argmin (removing a worker that
 // is not the minimum does not move the minimum), so the first over-capacity
-// row is the first divergence.  Each round closes >= 1 worker: <= n rounds.
+// row is the first divergence.  Each round closes >= 1 worker: <= n rounds
+// plus one pass per 1024 rows.  One CTA: the matrix slice is L2-resident.
+// (A grid-wide version -- one cooperative CTA per tile of 1024 rows, one
+// grid-wide sync per round -- measured slower at every config: C5 greedy
+// 0.60 -> 1.03 ms, ~15 us per round against ~5 us per 1024-row chunk here.)
 namespace {
 
 
@@ -91,248 +94,109 @@ __global__ void k_greedy_prefs(const double* __restrict__ matrix, int n,
   prefs[t] = pk;
 }
 
-// The rounds on the whole GPU: one cooperative kernel, tile b of positions
-// owned by CTA b.  A round (one grid-wide sync) is
-//  A: every position >= q0 whose stored choice is unset or now closed takes
-//     its argmin over the open set (first open of its eight preferences, else
-//     a rescan); each CTA publishes its per-worker counts of positions >= q0;
-//  B: every CTA, redundantly and identically, scans those counts over the
-//     tiles to find for each worker w the tile holding its (remaining_w+1)-th
-//     pick -- the earliest such tile holds the round's first over-capacity
-//     position qm, found exactly from that tile's stored choices -- then
-//     finalises its own positions in [q0, qm), subtracts every worker's picks
-//     in [q0, qm) from its remaining capacity, closes exhausted workers and
-//     moves q0 to qm.
-// Positions before qm never change again, so a CTA still in phase B of round
-// r reads only settled choices while others already rewrite choices >= qm in
-// round r+1; the counts are double-buffered by round parity.  Rows whose
-// choice stays open keep it across rounds (closing a worker that is not a
-// row's minimum does not move that minimum).
-constexpr int kGGThreads = 1024;
+constexpr int kGreedyThreads = 1024;
+constexpr int kGreedyWarps = kGreedyThreads / 32;
 
-struct GreedyGridArgs {
-  const double* matrix;
-  int n;
-  const uint32_t* order;
-  uint64_t n_order;
-  const int32_t* capacity_dev;
-  int cap_uniform;
-  int32_t* decision;
-  const uint32_t* row_ids;
-  int32_t* pair_worker;
-  int* flags;
-  const uint64_t* prefs;
-  int32_t* choice;  // n_order
-  uint32_t* cnt;    // 2 * gridDim.x * kMaxWorkers
-  int ppt;          // positions per thread
-};
+__global__ void __launch_bounds__(kGreedyThreads)
+    k_greedy(const double* __restrict__ matrix, int n, const uint32_t* __restrict__ order,
+             uint64_t n_order, const int32_t* __restrict__ capacity_dev, int cap_uniform,
+             int32_t* __restrict__ decision, const uint32_t* __restrict__ row_ids,
+             int32_t* __restrict__ pair_worker, int* __restrict__ flags,
+             const uint64_t* __restrict__ prefs) {
+  __shared__ int remaining[kMaxWorkers];
+  __shared__ int used[kMaxWorkers];
+  __shared__ int cnt[kGreedyWarps][kMaxWorkers];
+  __shared__ unsigned long long open_mask;
+  __shared__ int qmin;
 
-// argmin over the open workers (assign.hpp:177-184: ascending j, strict '<')
-__device__ __forceinline__ int greedy_pick(const GreedyGridArgs& a, uint64_t t,
-                                           unsigned long long om) {
-  const uint64_t pf = a.prefs[t];
-#pragma unroll
-  for (int q = 0; q < kPrefs; ++q) {
-    const int w = static_cast<int>((pf >> (8 * q)) & 0xFFu);
-    if (w != 0xFF && ((om >> w) & 1ULL)) return w;
-  }
-  const double* r = a.matrix + static_cast<uint64_t>(a.order[t]) * a.n;
-  double best = __longlong_as_double(0x7ff0000000000000LL);
-  int choice = -1;
-  for (int base = 0; base < a.n; base += 16) {
-    double c[16];
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      const int w = base + k;
-      c[k] = (w < a.n && ((om >> w) & 1ULL)) ? r[w] : best;
-    }
-#pragma unroll
-    for (int k = 0; k < 16; ++k)
-      if (c[k] < best) {
-        best = c[k];
-        choice = base + k;
-      }
-  }
-  return choice;
-}
-
-__global__ void __launch_bounds__(kGGThreads)
-    k_greedy_grid(GreedyGridArgs a) {
-  namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
-  __shared__ int rem[kMaxWorkers];
-  __shared__ uint32_t cntL[kMaxWorkers];
-  __shared__ int cw[kMaxWorkers];        // tile of each worker's over-capacity pick
-  __shared__ uint32_t kw[kMaxWorkers];   // its rank inside that tile
-  __shared__ uint32_t used[kMaxWorkers];
-  __shared__ uint32_t wsum[kGGThreads / 32];
-  __shared__ unsigned long long open_s;
-  __shared__ int cstar_s;
-  __shared__ uint32_t chunk_hits;
-  __shared__ unsigned long long qm_s;
-  const int n = a.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int G = gridDim.x;
-  const uint64_t tile = static_cast<uint64_t>(kGGThreads) * a.ppt;
-  const uint64_t tb = blockIdx.x * tile;
-  const uint64_t te = min(a.n_order, tb + tile);
-  if (tid < kMaxWorkers) rem[tid] = tid < n ? (a.capacity_dev ? a.capacity_dev[tid] : a.cap_uniform) : 0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < n) remaining[tid] = capacity_dev ? capacity_dev[tid] : cap_uniform;
   __syncthreads();
   if (tid == 0) {
     unsigned long long om = 0;
     for (int w = 0; w < n; ++w)
-      if (rem[w] > 0) om |= 1ULL << w;
-    open_s = om;
+      if (remaining[w] > 0) om |= 1ULL << w;
+    open_mask = om;
   }
   __syncthreads();
-  uint64_t q0 = 0;
-  int par = 0;
-  bool first = true;
-  for (;;) {
-    // ---- A: choices of the unsettled positions, per-CTA counts
-    if (tid < kMaxWorkers) cntL[tid] = 0;
-    __syncthreads();
-    const unsigned long long om = open_s;
-    for (int j = 0; j < a.ppt; ++j) {
-      const uint64_t t = tb + tid + static_cast<uint64_t>(j) * kGGThreads;
-      const bool live = t < te && t >= q0;
-      int c = -1;
-      if (live) {
-        c = first ? -1 : a.choice[t];
-        if (c < 0 || !((om >> c) & 1ULL)) {
-          c = greedy_pick(a, t, om);
-          if (c < 0) atomicOr(a.flags + kFlagUnbalanced, 1);  // capacities exhausted
-          a.choice[t] = c;
-        }
-      }
-      const unsigned grp = __match_any_sync(0xffffffffu, c);
-      if (c >= 0 && lane == __ffs(grp) - 1) atomicAdd(&cntL[c], static_cast<uint32_t>(__popc(grp)));
-    }
-    __syncthreads();
-    uint32_t* cnt = a.cnt + static_cast<uint64_t>(par) * G * kMaxWorkers;
-    if (tid < n) cnt[blockIdx.x * kMaxWorkers + tid] = cntL[tid];
-    grid.sync();
-    // ---- B: the first over-capacity position, identically in every CTA
-    const int c0 = static_cast<int>(q0 / tile);
-    for (int w = warp; w < n; w += kGGThreads / 32) {
-      uint32_t carry = 0;
-      int found = G;
-      uint32_t kk = 0;
-      for (int cb = c0; cb < G && found == G; cb += 32) {
-        const int c = cb + lane;
-        const uint32_t v = c < G ? cnt[c * kMaxWorkers + w] : 0u;
-        uint32_t inc = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-          if (lane >= o) inc += y;
-        }
-        const uint32_t cum = carry + inc;
-        const unsigned over = __ballot_sync(0xffffffffu, c < G && cum > static_cast<uint32_t>(rem[w]));
-        if (over) {
-          const int l = __ffs(over) - 1;
-          found = cb + l;
-          kk = static_cast<uint32_t>(rem[w]) - (__shfl_sync(0xffffffffu, cum, l) -
-                                                __shfl_sync(0xffffffffu, v, l)) + 1u;
-        }
-        carry = __shfl_sync(0xffffffffu, cum, 31);
-      }
-      if (lane == 0) {
-        cw[w] = found;
-        kw[w] = kk;
-      }
-    }
-    __syncthreads();
-    if (warp == 0) {
-      int m = G;
-      for (int w = lane; w < n; w += 32) m = min(m, cw[w]);
-      m = __reduce_min_sync(0xffffffffu, m);
-      if (lane == 0) {
-        cstar_s = m;
-        qm_s = a.n_order;
-      }
-    }
-    __syncthreads();
-    const int cstar = cstar_s;
-    if (cstar < G) {
-      // exact position of each over-capacity pick in tile cstar (usually one worker)
-      const uint64_t sb = cstar * tile, se = min(a.n_order, sb + tile);
-      for (int w = 0; w < n; ++w) {
-        if (cw[w] != cstar) continue;  // uniform
-        uint32_t need = kw[w];  // rank of the pick among tile cstar's picks of w at >= q0
-        for (int j = 0; j < a.ppt && need > 0; ++j) {  // `need` is block-uniform
-          const uint64_t t = sb + tid + static_cast<uint64_t>(j) * kGGThreads;
-          const bool hit = t < se && t >= q0 && a.choice[t] == w;
-          const unsigned bal = __ballot_sync(0xffffffffu, hit);
-          if (lane == 0) wsum[warp] = __popc(bal);
-          __syncthreads();
-          if (warp == 0) {
-            const uint32_t x = wsum[lane];
-            uint32_t inc = x;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-              const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-              if (lane >= o) inc += y;
-            }
-            wsum[lane] = inc - x;  // exclusive over warps
-            if (lane == 31) chunk_hits = inc;
-          }
-          __syncthreads();
-          const uint32_t before = wsum[warp] + __popc(bal & ((1u << lane) - 1u));
-          if (hit && before + 1 == need) atomicMin(&qm_s, static_cast<unsigned long long>(t));
-          need = need > chunk_hits ? need - chunk_hits : 0u;
-          __syncthreads();
-        }
-      }
-    }
-    __syncthreads();
-    const uint64_t qm = qm_s;
-    // picks per worker in [q0, qm): whole tiles before cstar from the counts,
-    // the part of tile cstar from its choices
+
+  uint64_t start = 0;
+  while (start < n_order) {
+    for (int x = tid; x < kGreedyWarps * kMaxWorkers; x += kGreedyThreads)
+      (&cnt[0][0])[x] = 0;
     if (tid < kMaxWorkers) used[tid] = 0;
+    if (tid == 0) qmin = kGreedyThreads;
     __syncthreads();
-    const int cend = cstar < G ? cstar : G;
-    for (int w = warp; w < n; w += kGGThreads / 32) {
-      uint32_t sum = 0;
-      for (int c = c0 + lane; c < cend; c += 32) sum += cnt[c * kMaxWorkers + w];
-      sum = __reduce_add_sync(0xffffffffu, sum);
-      if (lane == 0) used[w] = sum;
-    }
-    __syncthreads();
-    if (cstar < G) {
-      const uint64_t sb = cstar * tile;
-      for (int j = 0; j < a.ppt; ++j) {
-        const uint64_t t = sb + tid + static_cast<uint64_t>(j) * kGGThreads;
-        const int c = (t >= q0 && t < qm) ? a.choice[t] : -1;
-        const unsigned grp = __match_any_sync(0xffffffffu, c);
-        if (c >= 0 && lane == __ffs(grp) - 1) atomicAdd(&used[c], static_cast<uint32_t>(__popc(grp)));
+
+    const uint64_t t = start + tid;
+    const bool valid = t < n_order;
+    int choice = -1;
+    uint32_t row = 0;
+    if (valid) {
+      row = order[t];
+      const unsigned long long om = open_mask;
+      // The first of the position's eight best (initially open) workers that is
+      // still open is its argmin over the open set: every worker ranked before
+      // it is closed.  Only when all eight are closed is the row rescanned.
+      const uint64_t pf = prefs[t];
+#pragma unroll
+      for (int q = 0; q < kPrefs; ++q) {
+        const int w = static_cast<int>((pf >> (8 * q)) & 0xFFu);
+        if (choice < 0 && w != 0xFF && ((om >> w) & 1ULL)) choice = w;
       }
-    }
-    // this CTA's settled positions
-    for (int j = 0; j < a.ppt; ++j) {
-      const uint64_t t = tb + tid + static_cast<uint64_t>(j) * kGGThreads;
-      if (t < te && t >= q0 && t < qm) {
-        const int c = a.choice[t];
-        if (a.decision) {
-          const uint32_t row = a.order[t];
-          a.decision[a.row_ids ? a.row_ids[row] : row] = c;
+      if (choice < 0) {
+        const double* r = matrix + static_cast<uint64_t>(row) * n;
+        double best = __longlong_as_double(0x7ff0000000000000LL);
+        // sixteen workers per group, all of a group's loads in flight before
+        // the ascending strict-'<' compares (closed workers read as +inf,
+        // which never beats `best`)
+        for (int base = 0; base < n; base += 16) {
+          double c[16];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            const int w = base + k;
+            c[k] = (w < n && ((om >> w) & 1ULL)) ? r[w] : best;
+          }
+#pragma unroll
+          for (int k = 0; k < 16; ++k)
+            if (c[k] < best) {
+              best = c[k];
+              choice = base + k;
+            }
         }
-        if (a.pair_worker) a.pair_worker[t] = c;
+      }
+      if (choice < 0) atomicOr(flags + kFlagUnbalanced, 1);  // "capacities exhausted"
+    }
+    // rank of this position among earlier same-choice positions of the chunk
+    const unsigned peers = __match_any_sync(0xffffffffu, choice);
+    const int rank_in_warp = __popc(peers & ((1u << lane) - 1));
+    if (choice >= 0 && rank_in_warp == 0) cnt[warp][choice] = __popc(peers);
+    __syncthreads();
+    if (tid < n) {  // exclusive scan over warps, per worker
+      int run = 0;
+      for (int wp = 0; wp < kGreedyWarps; ++wp) {
+        const int v = cnt[wp][tid];
+        cnt[wp][tid] = run;
+        run += v;
       }
     }
     __syncthreads();
-    if (qm >= a.n_order) break;
-    if (tid < n) rem[tid] -= static_cast<int>(used[tid]);
+    if (choice >= 0 && cnt[warp][choice] + rank_in_warp >= remaining[choice])
+      atomicMin(&qmin, tid);
     __syncthreads();
-    if (tid == 0) {
-      unsigned long long o = 0;
-      for (int w = 0; w < n; ++w)
-        if (rem[w] > 0) o |= 1ULL << w;
-      open_s = o;
+    const int limit = qmin;
+    if (valid && choice >= 0 && tid < limit) {
+      atomicAdd(&used[choice], 1);
+      if (decision) decision[row_ids ? row_ids[row] : row] = choice;
+      if (pair_worker) pair_worker[t] = choice;
     }
     __syncthreads();
-    q0 = qm;
-    par ^= 1;
-    first = false;
+    if (tid < n) {
+      remaining[tid] -= used[tid];
+      if (remaining[tid] <= 0) atomicAnd(&open_mask, ~(1ULL << tid));
+    }
+    start += static_cast<uint64_t>(limit);
+    __syncthreads();
   }
 }
 
@@ -383,36 +247,13 @@ void launch_greedy(const double* matrix, uint64_t rows, int n, const uint32_t* o
                    int* flags, GreedyScratch& g, cudaStream_t s) {
   (void)rows;
   if (n_order == 0) return;
-  if (g.sms == 0) {
-    int dev = 0;
-    EDX_CUDA(cudaGetDevice(&dev));
-    EDX_CUDA(cudaDeviceGetAttribute(&g.sms, cudaDevAttrMultiProcessorCount, dev));
-  }
-  // one tile of >= 1024 positions per CTA, at most one CTA per SM but one (the
-  // exact solver, running concurrently on its own SM, holds a whole SM)
-  const uint64_t want = (n_order + kGGThreads - 1) / kGGThreads;
-  const int G = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(want, g.sms > 1 ? g.sms - 1 : 1)));
-  const int ppt = static_cast<int>((n_order + static_cast<uint64_t>(G) * kGGThreads - 1) /
-                                   (static_cast<uint64_t>(G) * kGGThreads));
   g.prefs.ensure(n_order);
-  g.choice.ensure(n_order);
-  g.cnt.ensure(2 * static_cast<size_t>(G) * kMaxWorkers);
   k_greedy_prefs<<<static_cast<unsigned>((n_order + 255) / 256), 256, 0, s>>>(
       matrix, n, order, n_order, capacity_dev, cap_uniform, g.prefs.p);
+  g_kernel_name[kKGreedy] = "k_greedy";
+  k_greedy<<<1, kGreedyThreads, 0, s>>>(matrix, n, order, n_order, capacity_dev, cap_uniform,
+                                        decision, row_ids, pair_worker, flags, g.prefs.p);
   EDX_LAUNCHED();
-  GreedyGridArgs a{matrix, n, order, n_order, capacity_dev, cap_uniform, decision, row_ids,
-                   pair_worker, flags, g.prefs.p, g.choice.p, g.cnt.p, ppt};
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(G));
-  cfg.blockDim = dim3(kGGThreads);
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  EDX_CUDA(cudaLaunchKernelEx(&cfg, k_greedy_grid, a));
-  g_kernel_name[kKGreedy] = "k_greedy_grid";
 }
 
 void launch_check_balance(const int32_t* decision, uint64_t rows, int n, int m, int* flags,

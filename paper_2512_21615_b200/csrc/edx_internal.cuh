@@ -160,13 +160,9 @@ struct SortScratch {
 };
 void sort_rows_by_gap(SortScratch& sc, const uint64_t* keys_in, const uint32_t* idx_in,
                       uint32_t* idx_out, uint64_t rows, cudaStream_t s);
-// K4 scratch: each position's eight best initially-open workers, its current
-// choice, and the cooperative rounds' per-tile counts
+// K4 scratch: each position's eight best initially-open workers
 struct GreedyScratch {
   DevBuf<uint64_t> prefs;
-  DevBuf<int32_t> choice;
-  DevBuf<uint32_t> cnt;
-  int sms = 0;
 };
 void launch_greedy(const double* matrix, uint64_t rows, int n, const uint32_t* order,
                    uint64_t n_order, const int32_t* capacity_dev, int cap_uniform,

@@ -1444,6 +1444,167 @@ size_t block_arena_bytes(int k, int mult) {
          r(static_cast<size_t>(2 * mult) * 4);
 }
 
+// ------------------------------------------------ K5 dense, lazy potentials
+// The same e-maxx steps with the O(k) potential pass of every step removed:
+// within a row's search, every used column j's potentials move by each later
+// delta, so they are applied once at the row end from D (the running sum of
+// deltas) at the moment j was reached; an unused column's minv is kept as
+// minv + D (one shift for all of them, so their order -- and the argmin with
+// the lowest index on ties -- is unchanged), and a relaxation from row i0 =
+// p[j0] compares a[i0][j] - u[i0] - v[j] + D(j0) with it, where D(j0) = D at
+// the step j0 was reached (u[i0] has not moved yet then).  Exact in int64.
+// One CTA, thread t owning columns t + 1 + c * 1024 (c < C) in registers
+// (stored minv, v, reached flag and D at reach); one barrier per step: warps
+// publish their (minv, j) minimum, every warp reduces the 32 of them.  The
+// scaled costs (llround(v * 1e12), capped; assign.hpp:92-100) are computed
+// once into an int64 k x k table the steps read row by row.
+constexpr int kDense2Threads = 1024;
+
+__global__ void k_scale_dense(const double* __restrict__ values, uint64_t count, int64_t cap,
+                              int64_t* __restrict__ S) {
+  const uint64_t x = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (x < count) S[x] = scale_cost(values[x], cap);
+}
+
+__device__ __forceinline__ void argmin_pair(int64_t& v, int& j) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const int64_t ov = __shfl_xor_sync(0xffffffffu, v, o);
+    const int oj = __shfl_xor_sync(0xffffffffu, j, o);
+    if (ov < v || (ov == v && oj < j)) {
+      v = ov;
+      j = oj;
+    }
+  }
+}
+
+template <int C, int T>
+__global__ void __launch_bounds__(T, 1)
+    k_hungarian_dense2(const int64_t* __restrict__ S, int k, uint64_t* __restrict__ col_of_row,
+                       unsigned long long* stats, int* __restrict__ flags) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ int64_t red_v[2][32];
+  __shared__ int red_j[2][32];
+  const size_t K1 = static_cast<size_t>(k) + 1;
+  int64_t* u = reinterpret_cast<int64_t*>(smem);                 // by row
+  int32_t* p = reinterpret_cast<int32_t*>(u + ((K1 + 1) & ~size_t(1)));  // by column
+  int32_t* way = p + K1;                                          // by column
+  int64_t* dreach = reinterpret_cast<int64_t*>(way + ((K1 + 1) & ~size_t(1)));  // D at reach
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  unsigned long long t_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+  for (size_t x = tid; x < K1; x += T) {
+    u[x] = 0;
+    p[x] = 0;
+    way[x] = 0;
+  }
+  int64_t v[C], ms[C];
+  int jc[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    v[c] = 0;
+    jc[c] = tid + 1 + c * T;  // column (valid when <= k)
+  }
+  __syncthreads();
+  unsigned long long steps = 0;
+  int par = 0;
+  for (int i = 1; i <= k; ++i) {
+#pragma unroll
+    for (int c = 0; c < C; ++c) ms[c] = kInf;
+    unsigned reached = 0;  // bit c: column jc[c] reached (used) in this row
+    if (tid == 0) p[0] = i;
+    __syncthreads();
+    int j0 = 0, i0 = i;
+    int64_t dj0 = 0;          // D when j0 was reached
+    int64_t ui0 = u[i];
+    int64_t D = 0;
+    for (;;) {
+      ++steps;
+      // relax the unreached columns from row i0, local argmin (ascending j)
+      const int64_t* Srow = S + static_cast<size_t>(i0 - 1) * k;
+      const int64_t shift = dj0 - ui0;
+      int64_t a[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) a[c] = (jc[c] <= k && !((reached >> c) & 1u)) ? Srow[jc[c] - 1] : 0;
+      int64_t best = kInf;
+      int bj = INT_MAX;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        if (jc[c] > k || ((reached >> c) & 1u)) continue;
+        const int64_t x = a[c] + shift - v[c];
+        if (x < ms[c]) {
+          ms[c] = x;
+          way[jc[c]] = j0;
+        }
+        if (ms[c] < best) {
+          best = ms[c];
+          bj = jc[c];
+        }
+      }
+      argmin_pair(best, bj);
+      if (lane == 0) {
+        red_v[par][warp] = best;
+        red_j[par][warp] = bj;
+      }
+      __syncthreads();
+      best = lane < T / 32 ? red_v[par][lane] : kInf;
+      bj = lane < T / 32 ? red_j[par][lane] : INT_MAX;
+      argmin_pair(best, bj);
+      par ^= 1;
+      if (bj == INT_MAX) {  // no unused column: only reachable on corrupt input
+        if (tid == 0) atomicOr(flags + kFlagBadCost, 1);
+        return;
+      }
+      // the column reached at this step: D moves to its stored minv
+      D = best;
+      j0 = bj;
+      dj0 = D;
+      {
+        const int c = (j0 - 1 - tid) / T;
+        if ((j0 - 1) % T == tid) {
+          reached |= 1u << c;
+          dreach[j0] = D;
+        }
+      }
+      i0 = p[j0];
+      if (i0 == 0) break;  // a free column: the augmenting path ends here
+      ui0 = u[i0];
+    }
+    // row end: potentials of the reached columns (assign.hpp:131-138 summed
+    // over the row's steps), the free column's excluded (it moved by 0)
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      if (!((reached >> c) & 1u)) continue;
+      const int64_t dd = D - dreach[jc[c]];
+      v[c] -= dd;
+      if (p[jc[c]] != 0) u[p[jc[c]]] += dd;
+    }
+    if (tid == 0) u[i] += D;  // column 0 (row i) was reached at D = 0
+    __syncthreads();
+    if (tid == 0) {  // augment (assign.hpp:141-145)
+      int jj = j0;
+      do {
+        const int jp = way[jj];
+        p[jj] = p[jp];
+        jj = jp;
+      } while (jj != 0);
+    }
+    __syncthreads();
+  }
+  for (int j = tid + 1; j <= k; j += T) col_of_row[p[j] - 1] = static_cast<uint64_t>(j - 1);
+  if (tid == 0 && stats) {
+    unsigned long long t_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    stats[0] = steps;
+    stats[6] = t_end - t_start;  // ns on the device
+  }
+}
+
+size_t dense2_smem_bytes(int k) {
+  const size_t K1 = static_cast<size_t>(k) + 1, K1e = (K1 + 1) & ~size_t(1);
+  return K1e * 8 + K1 * 4 + K1e * 4 + K1 * 8;  // u, p, way, dreach
+}
+
 size_t dense_arena_bytes(int k) {
   const size_t K1 = static_cast<size_t>(k) + 1;
   auto r = [](size_t b) { return (b + 15) & ~size_t(15); };
@@ -1577,9 +1738,31 @@ void launch_hungarian_blocks(HungarianScratch& sc, const double* matrix, int n,
 void launch_hungarian_dense(HungarianScratch& sc, const double* values, uint64_t k,
                             uint64_t* col_of_row, int* flags, cudaStream_t s, int device) {
   const int64_t cap = LLONG_MAX / (8 * static_cast<int64_t>(k + 1));
-  sc.steps.ensure(8);
-  const size_t arena = dense_arena_bytes(static_cast<int>(k));
+  sc.steps.ensure(9);
+  EDX_CUDA(cudaMemsetAsync(sc.steps.p, 0, 8 * sizeof(unsigned long long), s));
   const size_t limit = static_cast<size_t>(max_dyn_smem(device)) - 1024;  // static smem
+  const size_t smem2 = dense2_smem_bytes(static_cast<int>(k));
+  if (k <= 8 * static_cast<uint64_t>(kDense2Threads) && smem2 <= limit) {
+    // scaled costs once, then the lazy-potential steps
+    sc.s64.ensure(k * k);
+    k_scale_dense<<<static_cast<unsigned>((k * k + 255) / 256), 256, 0, s>>>(values, k * k, cap,
+                                                                           sc.s64.p);
+    EDX_LAUNCHED();
+    auto go = [&](auto kern, int threads) {
+      EDX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem2)));
+      kern<<<1, threads, smem2, s>>>(sc.s64.p, static_cast<int>(k), col_of_row, sc.steps.p, flags);
+    };
+    // columns per thread in registers: 1024 threads up to 4 each, 512 x 16 above
+    if (k <= 1024) go(k_hungarian_dense2<1, 1024>, 1024);
+    else if (k <= 2048) go(k_hungarian_dense2<2, 1024>, 1024);
+    else if (k <= 4096) go(k_hungarian_dense2<4, 1024>, 1024);
+    else go(k_hungarian_dense2<16, 512>, 512);
+    EDX_LAUNCHED();
+    g_kernel_name[kKSolver] = "k_hungarian_dense2";
+    return;
+  }
+  const size_t arena = dense_arena_bytes(static_cast<int>(k));
   size_t smem = 0;
   uint8_t* garena = nullptr;
   if (arena <= limit) {

@@ -473,6 +473,21 @@ __global__ void __launch_bounds__(big::kThreads)
   const uint32_t chunks = static_cast<uint32_t>((a.capacity + big::kChunk - 1) / big::kChunk);
   const uint64_t gtid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // no evicting worker (every step while the caches fill): nothing to select,
+  // and no grid-wide sync -- every block sees the same E_j and returns
+  {
+    bool any = false;
+    for (int j = 0; j < n; ++j) any |= a.ws[j * kWS + kWsEvict] > 0;
+    if (!any) {
+      if (gtid < static_cast<uint64_t>(n)) {
+        uint32_t* w = a.ws + gtid * kWS;
+        w[kWsCand] = 0;
+        w[kWsCandOff] = static_cast<uint32_t>(gtid * a.capacity);
+        w[kWsVa] = w[kWsVb] = w[kWsVc] = 0;
+      }
+      return;
+    }
+  }
   for (int b = threadIdx.x; b < big::kBins; b += blockDim.x) hsh[b] = 0;
 
   // ---- init

