@@ -74,6 +74,9 @@ def parse():
     ap.add_argument("--no-ncu", action="store_true",
                     help="skip the ncu DRAM-traffic capture of the cost build")
     ap.add_argument("--ncu-child", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--spread-ids", action="store_true",
+                    help="map every id through a bijection onto [0, 2^32) and run the engine "
+                         "without an id bound (the device id table; SimState(cfg) semantics)")
     return ap.parse_args()
 
 
@@ -94,9 +97,19 @@ def workload(args):
             raise SystemExit("--batch must be a multiple of --workers")
         w.update(n=n, m=R // n, bw=HET(n))
     w["R"] = w["n"] * w["m"]
+    w["spread"] = bool(getattr(args, "spread_ids", False))
+    if w["spread"]:
+        w["desc"] += "; ids spread over [0, 2^32) (bijection), engine without an id bound"
     if args.config == "C5":
         w["desc"] = f"{w['desc']}: batch {w['R']}, {w['n']} workers"
     return w
+
+
+def spread(ids):
+    """uint32 bijection (odd multiplier mod 2^32): the Zipf ids spread over the
+    whole 32-bit range, as hashed feature ids are (tests/scale_state.py)."""
+    x = ids.astype(np.uint64)
+    return ((x * np.uint64(0x9E3779B1) + np.uint64(0x7F4A7C15)) & np.uint64(0xFFFFFFFF)).astype(np.uint32)
 
 
 def batches(w, count):
@@ -104,14 +117,16 @@ def batches(w, count):
     own host generator (bit-identical; tests/test_host.py pins it)."""
     import paper_2512_21615_b200 as edx
     z = edx.ZipfStream(w["V"], w["L"], ZIPF_S, count, SEED, w["R"])
-    return [ids for ids in z]
+    out = [ids for ids in z]
+    return [spread(b) for b in out] if w.get("spread") else out
 
 
 def reference_batches(w, count):
     """The same stream from the reference's own ZipfStream (oracle/_ref), so
     the reference arm maps no product library."""
     orc, _ = reference_oracle()
-    return list(orc.zipf_batches(w["V"], w["L"], ZIPF_S, count, SEED, w["R"]))
+    out = list(orc.zipf_batches(w["V"], w["L"], ZIPF_S, count, SEED, w["R"]))
+    return [spread(b) for b in out] if w.get("spread") else out
 
 
 def parallelism(world):
@@ -222,7 +237,8 @@ def product(args, w, rank, world, local_rank):
             buf.copy_(torch.frombuffer(bytearray(edx.nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(buf, 0)
         nccl_id = bytes(buf.cpu().numpy().tobytes())
-    eng = edx.SimState(cfg, id_space=w["V"], max_batch_ids=R * L, device=local_rank, rank=rank,
+    eng = edx.SimState(cfg, id_space=0 if w["spread"] else w["V"], max_batch_ids=R * L,
+                       device=local_rank, rank=rank,
                        world_size=world, nccl_id=nccl_id)
     stream = torch.cuda.ExternalStream(eng.stream_handle(), device=dev)
     flush = None if args.no_flush else torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -487,7 +503,7 @@ def ncu_child(args, w):
     offs = np.arange(R + 1, dtype=np.uint64) * np.uint64(L)
     cfg = edx.ClusterConfig(n=n, m=m, bandwidths_bps=w["bw"], d_tran_bytes=2048,
                             cache_capacity=w["cap"], alpha=w["alpha"])
-    eng = edx.SimState(cfg, id_space=w["V"], max_batch_ids=R * L)
+    eng = edx.SimState(cfg, id_space=0 if w["spread"] else w["V"], max_batch_ids=R * L)
     for b in host[:P + W]:
         eng.iterate(b, offs, want_decision=False)
     eng.load((host[P + W], offs))
@@ -514,6 +530,8 @@ def ncu_build_traffic(args, kernel):
                       ("--batch", args.batch), ("--workers", args.workers)):
         if val is not None:
             cmd += [flag, str(val)]
+    if args.spread_ids:
+        cmd.append("--spread-ids")
     env = dict(os.environ, EDX_GRAPH="0")
     for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK"):
         env.pop(k, None)

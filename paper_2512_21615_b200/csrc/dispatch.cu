@@ -319,6 +319,7 @@ void run_ecomix(DispatchScratch& sc, const double* matrix, uint64_t rows, int n,
     EDX_CUDA(cudaEventRecord(sc.fork, s));
     EDX_CUDA(cudaStreamWaitEvent(sc.side, sc.fork, 0));
     if (ev && ev->greedy0) EDX_CUDA(cudaEventRecord(ev->greedy0, sc.side));
+    const NvtxRange nv("edx.greedy (K4 assign.hpp:162-192)");
     launch_greedy(matrix, rows, n, sc.order.p + k, rows - k, nullptr, m - mult, decision,
                   nullptr, nullptr, flags, sc.greedy, sc.side);
     if (launches) ++*launches;
@@ -327,6 +328,7 @@ void run_ecomix(DispatchScratch& sc, const double* matrix, uint64_t rows, int n,
   }
   if (ev && ev->exact0) EDX_CUDA(cudaEventRecord(ev->exact0, s));
   if (mult > 0) {
+    const NvtxRange nv("edx.exact_solve (K6 assign.hpp:80-157)");
     launch_hungarian_blocks(sc.hung, matrix, n, sc.order.p, mult, decision, nullptr, nullptr,
                             flags, s, device);
     if (launches) ++*launches;

@@ -11,9 +11,21 @@
 #include <string>
 #include <utility>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "edx.h"
 
 namespace edx {
+
+// NVTX range for the host-side enqueue of one phase (build, gap sort, exact
+// solve, greedy, step): header-only NVTX v3, a no-op unless a tool (ncu
+// --nvtx, Nsight Systems) is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // ---------------------------------------------------------------- errors
 // Host-side exceptions carry an edx_status; the C ABI boundary converts them.

@@ -468,6 +468,7 @@ void reserve_slots(edx_engine* e, uint64_t T) {
 // Translates the loaded batch to slots (hashed mode) before its first consumer.
 void ensure_translated(edx_engine* e) {
   if (!e->hashed || e->translated) return;
+  const edx::NvtxRange nv("edx.translate (ids.cu)");
   reserve_slots(e, e->total_ids);
   edx::id_table_translate(e->idt, e->cur_raw, e->total_ids, e->kslots.p, true, e->flags.p,
                           e->stream);
@@ -494,6 +495,7 @@ std::vector<uint32_t> host_slots(edx_engine* e, const uint32_t* ids, uint64_t co
 }
 
 void engine_build(edx_engine* e) {
+  const edx::NvtxRange nv("edx.build (K1 cost.hpp:105-125)");
   const uint64_t want = static_cast<uint64_t>(e->n) * static_cast<uint64_t>(e->m);
   if (!e->cur_ids) edx::invalid("no batch loaded");
   ensure_translated(e);
@@ -531,6 +533,7 @@ void engine_build(edx_engine* e) {
 }
 
 void engine_dispatch(edx_engine* e, double alpha) {
+  const edx::NvtxRange nv("edx.dispatch (ecomix assign.hpp:247-285)");
   if (!e->built) edx::invalid("build the cost matrix before dispatching");
   if (alpha < 0.0) alpha = e->alpha;
   if (alpha > 1.0) edx::invalid("alpha must lie in [0, 1]");
@@ -614,6 +617,7 @@ double fetch_expected(edx_engine* e) {
 
 // Enqueues the step for the current batch and decision (no sync).
 void step_enqueue(edx_engine* e, const int32_t* decision) {
+  const edx::NvtxRange nv("edx.step (K7 sim.hpp:87-218)");
   if (!e->cur_ids) edx::invalid("no batch loaded");
   ensure_translated(e);
   if (decision) {

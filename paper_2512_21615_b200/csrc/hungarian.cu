@@ -778,7 +778,24 @@ __device__ __forceinline__ void warp_resort_dispatch(int32_t* ord, const int64_t
   else if (mult <= 64) warp_resort_block<2>(ord, v, base, mult, lane);
   else if (mult <= 128) warp_resort_block<4>(ord, v, base, mult, lane);
   else if (mult <= 256) warp_resort_block<8>(ord, v, base, mult, lane);
-  else warp_resort_block<16>(ord, v, base, mult, lane);
+  else if (mult <= 512) warp_resort_block<16>(ord, v, base, mult, lane);
+  else if (lane == 0) {
+    // mult > 512: an insertion sort on one lane, scalar registers only (the
+    // re-sort never ran in a measured solve; see warp_block_sorted)
+    for (int i = 1; i < mult; ++i) {
+      const int c = ord[base + i];
+      const int64_t vc = v[c];
+      int q = i - 1;
+      while (q >= 0) {
+        const int d = ord[base + q];
+        if (!(v[d] < vc || (v[d] == vc && d > c))) break;
+        ord[base + q + 1] = d;
+        --q;
+      }
+      ord[base + q + 1] = c;
+    }
+  }
+  __syncwarp();
 }
 
 // After a row's potential update every touched block is already sorted by
@@ -850,7 +867,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
 // orders start as the identity and a potential update keeps each block sorted
 // (see the re-sort check), so ord is only consulted after a fallback sort.
 
-template <int AMODE, int MAXW, int BPW>  // AMODE 0: S and A shared; 1: S global, A shared; 2: S and A global
+template <int AMODE, int MAXW, int BPW>  // AMODE 0: S and A shared; 1: S global, A shared; 2: S and A global; 3: + tables global
 __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks per warp (1, or 2 for n <= 32)
     k_hungarian_blocks_mw(const int64_t* __restrict__ S_global, int n, int mult, int k,
                           int64_t* __restrict__ A_global, const uint32_t* __restrict__ order,
@@ -874,28 +891,38 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
   } else {
     S = S_global;
   }
+  // AMODE 3 (large blocks): A and every per-column table the Dijkstra steps
+  // do not read -- potentials, ways, orders, the reached list -- live in the
+  // global arena after A; only the key offsets and rows stay shared.
+  size_t go = 0;
+  auto gtake = [&](size_t bytes) {
+    uint8_t* q = reinterpret_cast<uint8_t*>(A_global) + go;
+    go += (bytes + 15) & ~size_t(15);
+    return q;
+  };
+  auto table = [&](size_t bytes) { return AMODE == 3 ? gtake(bytes) : stake(bytes); };
   int64_t* A;
   if constexpr (AMODE <= 1) A = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(k) * n * 8));
-  else A = A_global;
+  else A = reinterpret_cast<int64_t*>(gtake(static_cast<size_t>(k) * n * 8));
   int64_t* Btab = reinterpret_cast<int64_t*>(stake(K1 * 8));  // by column: block - (v << 6)
-  int64_t* u = reinterpret_cast<int64_t*>(stake(K1 * 8));
-  int64_t* v = reinterpret_cast<int64_t*>(stake(K1 * 8));
-  int64_t* dlt = reinterpret_cast<int64_t*>(stake((K1 + 32) * 8));
-  int32_t* p = reinterpret_cast<int32_t*>(stake(K1 * 4));
-  int32_t* wayi = reinterpret_cast<int32_t*>(stake((K1 + 32) * 4));
-  int32_t* ulist = reinterpret_cast<int32_t*>(stake((K1 + 32) * 4));
-  int32_t* ord = reinterpret_cast<int32_t*>(stake(K1 * 4));
+  int64_t* u = reinterpret_cast<int64_t*>(table(K1 * 8));
+  int64_t* v = reinterpret_cast<int64_t*>(table(K1 * 8));
+  int64_t* dlt = reinterpret_cast<int64_t*>(table((K1 + 32) * 8));
+  int32_t* p = reinterpret_cast<int32_t*>(table(K1 * 4));
+  int32_t* wayi = reinterpret_cast<int32_t*>(table((K1 + 32) * 4));
+  int32_t* ulist = reinterpret_cast<int32_t*>(table((K1 + 32) * 4));
+  int32_t* ord = reinterpret_cast<int32_t*>(table(K1 * 4));
   int32_t* rtab = reinterpret_cast<int32_t*>(stake(K1 * 4));
-  int32_t* cblk = reinterpret_cast<int32_t*>(stake(K1 * 4));   // column -> block
+  int32_t* cblk = reinterpret_cast<int32_t*>(table(K1 * 4));   // column -> block
   int32_t* curs = reinterpret_cast<int32_t*>(stake(32 * 4));
   // reached-column list of the row being solved, one 16-byte entry per step:
   // {c | p[c] << 16, way (entry index of the predecessor), delta at reach}
-  int4* L = reinterpret_cast<int4*>(stake((K1 + 32) * 16));
+  int4* L = reinterpret_cast<int4*>(table((K1 + 32) * 16));
   int64_t* GA = reinterpret_cast<int64_t*>(stake(2 * 32 * 32 * 8));  // chunk: per-step G of each block
   uint64_t* mbar = reinterpret_cast<uint64_t*>(stake(16));            // chunk exchange barrier
   int32_t* ordflag = reinterpret_cast<int32_t*>(stake(16));           // block orders still identity?
   uint32_t* pfail = reinterpret_cast<uint32_t*>(stake(2 * 32 * 4));  // chunk: fail masks
-  int32_t* tmp = reinterpret_cast<int32_t*>(stake(static_cast<size_t>(2 * mult) * 4));
+  int32_t* tmp = reinterpret_cast<int32_t*>(table(static_cast<size_t>(2 * mult) * 4));
   if (so > dynamic_smem_bytes()) {  // host/device layout mismatch: fail loudly, touch nothing
     if (tid == 0) atomicOr(flags + kFlagInternal, 1);
     return;
@@ -1116,6 +1143,11 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
             L[wbase + lane] = make_int4(c | (r << 16), prev ? wbase + 31 - __clz(prev) : wyx[h],
                                         static_cast<int>(static_cast<uint32_t>(dq)),
                                         static_cast<int>(dq >> 32));
+            // the row end re-reads this row's scaled costs (potentials and
+            // the operand-table refresh): start pulling them into L1 now
+            if constexpr (AMODE >= 1)
+              if (r > 0)
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(S + static_cast<size_t>(r - 1) * n));
           }
         }
         sN += vq;
@@ -1215,7 +1247,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
         }
       }
     }
-    if constexpr (AMODE == 2) __threadfence_block();
+    if constexpr (AMODE >= 2) __threadfence_block();
     __syncthreads();
     const long long t3 = clock64();
     c_pot += t3 - t2;
@@ -1254,7 +1286,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
       }
       __syncwarp();
     }
-    if constexpr (AMODE == 2) __threadfence_block();
+    if constexpr (AMODE >= 2) __threadfence_block();
     __syncthreads();
     const long long t4 = clock64();
     c_ref += t4 - t3;
@@ -1292,9 +1324,21 @@ size_t mw_smem_bytes(int k, int n, int mult, int amode) {
   size_t b = 0;
   if (amode == 0) b += r(static_cast<size_t>(k) * n * 8);
   if (amode <= 1) b += r(static_cast<size_t>(k) * n * 8);
-  b += 3 * r(K1 * 8) + r((K1 + 32) * 8) + 4 * r(K1 * 4) + 2 * r((K1 + 32) * 4) + r(32 * 4) +
-       r((K1 + 32) * 16) + r(2 * 32 * 32 * 8) + r(16) + r(16) + r(2 * 32 * 4) +
-       r(static_cast<size_t>(2 * mult) * 4);
+  b += r(K1 * 8) + r(K1 * 4) + r(32 * 4) + r(2 * 32 * 32 * 8) + r(16) + r(16) + r(2 * 32 * 4);
+  if (amode <= 2)  // the tables AMODE 3 keeps in the global arena
+    b += 2 * r(K1 * 8) + r((K1 + 32) * 8) + 3 * r(K1 * 4) + 2 * r((K1 + 32) * 4) +
+         r((K1 + 32) * 16) + r(static_cast<size_t>(2 * mult) * 4);
+  return b;
+}
+
+// global arena of AMODE 2 (A) and 3 (A + the per-column tables)
+size_t mw_arena_bytes(int k, int n, int mult, int amode) {
+  const size_t K1 = static_cast<size_t>(k) + 1;
+  auto r = [](size_t b) { return (b + 15) & ~size_t(15); };
+  size_t b = r(static_cast<size_t>(k) * n * 8);
+  if (amode == 3)
+    b += 2 * r(K1 * 8) + r((K1 + 32) * 8) + 3 * r(K1 * 4) + 2 * r((K1 + 32) * 4) +
+         r((K1 + 32) * 16) + r(static_cast<size_t>(2 * mult) * 4);
   return b;
 }
 
@@ -1486,10 +1530,11 @@ __global__ void __launch_bounds__(T, 1)
   __shared__ int64_t red_v[2][32];
   __shared__ int red_j[2][32];
   const size_t K1 = static_cast<size_t>(k) + 1;
-  int64_t* u = reinterpret_cast<int64_t*>(smem);                 // by row
-  int32_t* p = reinterpret_cast<int32_t*>(u + ((K1 + 1) & ~size_t(1)));  // by column
-  int32_t* way = p + K1;                                          // by column
-  int64_t* dreach = reinterpret_cast<int64_t*>(way + ((K1 + 1) & ~size_t(1)));  // D at reach
+  const size_t K1e = (K1 + 1) & ~size_t(1);  // even: every array below stays 8-byte aligned
+  int64_t* u = reinterpret_cast<int64_t*>(smem);        // by row
+  int32_t* p = reinterpret_cast<int32_t*>(u + K1e);     // by column
+  int32_t* way = p + K1e;                               // by column
+  int64_t* dreach = reinterpret_cast<int64_t*>(way + K1e);  // by column: D when reached
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   unsigned long long t_start;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
@@ -1602,7 +1647,7 @@ __global__ void __launch_bounds__(T, 1)
 
 size_t dense2_smem_bytes(int k) {
   const size_t K1 = static_cast<size_t>(k) + 1, K1e = (K1 + 1) & ~size_t(1);
-  return K1e * 8 + K1 * 4 + K1e * 4 + K1 * 8;  // u, p, way, dreach
+  return K1e * (8 + 4 + 4 + 8);  // u, p, way, dreach
 }
 
 size_t dense_arena_bytes(int k) {
@@ -1656,15 +1701,19 @@ void launch_hungarian_blocks(HungarianScratch& sc, const double* matrix, int n,
     const char* e = std::getenv("EDX_MW_BPW");
     return e && std::strcmp(e, "2") == 0 ? 2 : 1;
   }();
-  if (n <= 32 && mult <= 512) {
+  static const int amode_min = [] {  // EDX_MW_GLOBAL=1: the global-table layout (tests)
+    const char* e = std::getenv("EDX_MW_GLOBAL");
+    return e && std::strcmp(e, "1") == 0 ? 3 : 0;
+  }();
+  if (n <= 32 && mult <= 1024) {
     const bool pair = n > 16 || (bpw_pref == 2 && n > 1);
     const int nwarps = pair ? (n + 1) / 2 : n;
-    for (int am = 0; am <= 2; ++am) {
+    for (int am = amode_min; am <= 3; ++am) {
       const size_t smem = mw_smem_bytes(k, n, mult, am);
       if (smem > limit) continue;
       int64_t* Ag = nullptr;
-      if (am == 2) {
-        sc.arena.ensure(static_cast<size_t>(k) * n * 8);
+      if (am >= 2) {
+        sc.arena.ensure(mw_arena_bytes(k, n, mult, am));
         Ag = reinterpret_cast<int64_t*>(sc.arena.p);
       }
       auto launch = [&](auto kern) {
@@ -1678,19 +1727,23 @@ void launch_hungarian_blocks(HungarianScratch& sc, const double* matrix, int n,
       if (pair && n <= 16) {
         if (am == 0) { launch(k_hungarian_blocks_mw<0, 8, 2>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<0,8,2>"; }
         else if (am == 1) { launch(k_hungarian_blocks_mw<1, 8, 2>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<1,8,2>"; }
-        else { launch(k_hungarian_blocks_mw<2, 8, 2>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<2,8,2>"; }
+        else if (am == 2) { launch(k_hungarian_blocks_mw<2, 8, 2>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<2,8,2>"; }
+        else { launch(k_hungarian_blocks_mw<3, 8, 2>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<3,8,2>"; }
       } else if (n <= 8) {
         if (am == 0) { launch(k_hungarian_blocks_mw<0, 8, 1>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<0,8,1>"; }
         else if (am == 1) { launch(k_hungarian_blocks_mw<1, 8, 1>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<1,8,1>"; }
-        else { launch(k_hungarian_blocks_mw<2, 8, 1>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<2,8,1>"; }
+        else if (am == 2) { launch(k_hungarian_blocks_mw<2, 8, 1>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<2,8,1>"; }
+        else { launch(k_hungarian_blocks_mw<3, 8, 1>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<3,8,1>"; }
       } else if (n <= 16) {
         if (am == 0) { launch(k_hungarian_blocks_mw<0, 16, 1>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<0,16,1>"; }
         else if (am == 1) { launch(k_hungarian_blocks_mw<1, 16, 1>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<1,16,1>"; }
-        else { launch(k_hungarian_blocks_mw<2, 16, 1>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<2,16,1>"; }
+        else if (am == 2) { launch(k_hungarian_blocks_mw<2, 16, 1>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<2,16,1>"; }
+        else { launch(k_hungarian_blocks_mw<3, 16, 1>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<3,16,1>"; }
       } else {
         if (am == 0) { launch(k_hungarian_blocks_mw<0, 16, 2>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<0,16,2>"; }
         else if (am == 1) { launch(k_hungarian_blocks_mw<1, 16, 2>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<1,16,2>"; }
-        else { launch(k_hungarian_blocks_mw<2, 16, 2>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<2,16,2>"; }
+        else if (am == 2) { launch(k_hungarian_blocks_mw<2, 16, 2>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<2,16,2>"; }
+        else { launch(k_hungarian_blocks_mw<3, 16, 2>); g_kernel_name[kKSolver] = "k_hungarian_blocks_mw<3,16,2>"; }
       }
       EDX_LAUNCHED();
       return;

@@ -1,0 +1,45 @@
+"""The exact solver's large-block layout (k_hungarian_blocks_mw AMODE 3:
+A and the per-column tables in global memory, used when a block's tables
+outgrow shared memory -- the paper's Table 2 sizes k = 4096, 8192) forced on
+small blocks (EDX_MW_GLOBAL=1, read once per process: run in a child) and
+compared column for column with the compiled reference."""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CHILD = r"""
+import json, sys, numpy as np
+sys.path.insert(0, %r)
+import paper_2512_21615_b200 as edx
+d = np.load(%r)
+res = edx.hungarian_blocks(d["mat"], d["rows"], int(d["mult"]))
+print(json.dumps({"cols": [int(x) for x in res.col_of_row], "total": res.total_cost}))
+"""
+
+
+@pytest.mark.parametrize("n,mult,seed", [(8, 64, 1), (16, 32, 2), (24, 16, 3), (2, 600, 4)])
+def test_global_table_layout(gpu, oracle, tmp_path, n, mult, seed):
+    rng = np.random.default_rng(seed)
+    k = n * mult
+    # cost rows shaped like EcoMix's: a few units of two link speeds, many ties
+    u = np.where(np.arange(n) < max(n // 2, 1), 3.2768e-6, 3.2768e-5)
+    mat = rng.integers(0, 30, size=(k + 17, n)) * u[None, :]
+    rows = rng.permutation(k + 17)[:k].astype(np.uint64)
+    path = str(tmp_path / "case.npz")
+    np.savez(path, mat=mat, rows=rows, mult=mult)
+    env = dict(os.environ, EDX_MW_GLOBAL="1")
+    r = subprocess.run([sys.executable, "-c", CHILD % (ROOT, path)], capture_output=True,
+                       text=True, env=env, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    got = json.loads(r.stdout.strip().splitlines()[-1])
+    sq = np.ascontiguousarray(mat[rows.astype(np.int64)][:, np.arange(k) // mult])
+    cols, total = oracle.hungarian(sq)
+    assert got["cols"] == [int(x) for x in cols]
+    assert got["total"] == total
