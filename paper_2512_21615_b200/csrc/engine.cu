@@ -422,7 +422,7 @@ void grow_slots(edx_engine* e, uint64_t need) {
   const uint64_t kMax = 0xFFFFFFF0ull;
   if (need > kMax) edx::invalid("more than 2^32 - 16 distinct embedding ids");
   const uint64_t old = e->id_space, used = e->idt.used;
-  const uint64_t cap = std::min(kMax, std::max(2 * old, need + need / 2));
+  const uint64_t cap = std::min(kMax, std::max(4 * old, 2 * need));
   EDX_CUDA(cudaStreamSynchronize(e->step_side));
   EDX_CUDA(cudaStreamSynchronize(e->stream));
   const int n = e->n;
@@ -832,9 +832,9 @@ int edx_engine_create(const edx_cluster_config* cfg, const edx_engine_options* o
     e->ucost_h = unit_costs(cfg);
     e->max_ids = opt->max_batch_ids;
     // id_space 0: any uint32 id through the device id table, starting with
-    // room for a few batches of new ids (the tables grow on demand)
+    // room for 16 batches of new ids (the tables grow 4x on demand)
     e->hashed = opt->id_space == 0;
-    e->id_space = e->hashed ? std::min<uint64_t>(0xFFFFFFF0ull, std::max<uint64_t>(1ULL << 16, 4 * e->max_ids))
+    e->id_space = e->hashed ? std::min<uint64_t>(0xFFFFFFF0ull, std::max<uint64_t>(1ULL << 16, 16 * e->max_ids))
                             : opt->id_space;
     e->rank = opt->rank;
     e->world = opt->world_size < 1 ? 1 : opt->world_size;

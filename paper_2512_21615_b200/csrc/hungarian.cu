@@ -960,7 +960,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
     Btab[c] = b;
   }
   if (tid == 0) {
-    mbar_init(mbar, blockDim.x);
+    mbar_init(mbar, nw);  // one arrival per warp
     ordflag[0] = 1;
   }
   __syncthreads();
@@ -1099,7 +1099,10 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
 #pragma unroll
         for (int h = 0; h < BPW; ++h)
           if (own[h]) GA[(par * 32 + xs[h]) * 32 + lane] = Ga[h];
-        mbar_arrive(mbar);
+        // one arrival per warp (lane 0, after the warp's shared writes):
+        // 512 per-thread arrivals on one barrier word serialise at n = 16
+        __syncwarp();
+        if (lane == 0) mbar_arrive(mbar);
         // speculative next chunk (this one complete, the run continuing)
         const bool more = sN + 32 < Tm;
         const int64_t P31 = __shfl_sync(0xffffffffu, Qt, 31);
@@ -1143,11 +1146,6 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
             L[wbase + lane] = make_int4(c | (r << 16), prev ? wbase + 31 - __clz(prev) : wyx[h],
                                         static_cast<int>(static_cast<uint32_t>(dq)),
                                         static_cast<int>(dq >> 32));
-            // the row end re-reads this row's scaled costs (potentials and
-            // the operand-table refresh): start pulling them into L1 now
-            if constexpr (AMODE >= 1)
-              if (r > 0)
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(S + static_cast<size_t>(r - 1) * n));
           }
         }
         sN += vq;

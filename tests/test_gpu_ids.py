@@ -78,7 +78,7 @@ def test_spread_ids_trajectory(gpu, pyoracle, oracle, name, alpha, iters, seed):
 
 @pytest.mark.parametrize("name", ["PX", "PXL"])
 def test_spread_ids_table_growth(gpu, pyoracle, oracle, name):
-    """500K-id vocabularies through a table that starts at 65,536 slots:
+    """500K-id vocabularies through a table that starts at 16 batches (102,400 slots):
     several growths, with thousands of evictions per worker per step."""
     p = CONFIGS[name]
     eng, sim = _pair(gpu, pyoracle, oracle, p, 0.25 if name == "PXL" else 0.0)
