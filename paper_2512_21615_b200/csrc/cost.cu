@@ -15,8 +15,6 @@
 // threads of one row hit the same address (a broadcast), so each id costs
 // one L1/L2 transaction per row.  Loads are batched 4 ids ahead of the add
 // chain to keep memory-level parallelism despite the serial adds.
-#include <cstdlib>
-#include <cstring>
 #include <type_traits>
 
 #include "edx_internal.cuh"
@@ -381,130 +379,6 @@ __global__ void __launch_bounds__(kWarpRowsThreads)
   }
 }
 
-// K1, 2 <= n <= 32, lane chains: a group of NP >= n lanes per row (lane j =
-// worker j), but every lane walks ITS OWN cell's add sequence instead of the
-// group stepping through the ids in lockstep.  The row's ids and their
-// {owners, latest} masks are staged in shared memory (16 per group lane, at
-// most 128, at a time); each lane
-// keeps a bitmask of the staged ids whose latest copy is not on its worker
-// (its active ids) and runs one add per loop iteration: u_j on entering an
-// active id, then u_o for its owners in ascending order, the operand fetched
-// from lane o of the group with a warp shuffle (lane o holds u_o), so the
-// warp's lanes are busy with adds whatever their latest patterns are.  Every
-// cell's adds are the reference's sequence (cost.hpp:88-98), left to right.
-constexpr int kLaneThreads = 128;
-
-template <int NP>
-__global__ void __launch_bounds__(kLaneThreads)
-    k_cost_build_lane(const uint32_t* __restrict__ ids, const uint64_t* __restrict__ offsets,
-                      uint64_t rows, int n, const ulonglong2* __restrict__ ol, uint64_t id_space,
-                      const double* __restrict__ ucost, double* __restrict__ matrix,
-                      uint64_t* __restrict__ gap_keys, uint32_t* __restrict__ row_index,
-                      int* __restrict__ flags) {
-  // ids staged per chunk: 16 per lane of a group, at most 128
-  constexpr int kLaneChunk = 16 * NP < 128 ? 16 * NP : 128;
-  constexpr int RPW = 32 / NP, NW = kLaneThreads / 32, CW = kLaneChunk / 32;
-  // +1: the groups' copies of one position fall in different banks
-  __shared__ uint32_t own_s[NW][RPW][kLaneChunk + 1];
-  __shared__ uint32_t lat_s[NW][RPW][kLaneChunk + 1];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane / NP, j = lane - g * NP;
-  const uint64_t i = (static_cast<uint64_t>(blockIdx.x) * NW + warp) * RPW + g;
-  const bool rowok = i < rows;
-  const bool cell = rowok && j < n;
-  const double uj = j < n ? ucost[j] : 0.0;  // lane o of a group holds u_o
-  uint64_t beg = 0, end = 0;
-  if (rowok) {
-    beg = offsets[i];
-    end = offsets[i + 1];
-  }
-  const int len = static_cast<int>(end - beg);
-  const int maxlen = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(len)));
-  uint32_t* own = own_s[warp][g];
-  uint32_t* lat = lat_s[warp][g];
-  double c = 0.0;
-  bool bad = false;
-  for (int base = 0; base < maxlen; base += kLaneChunk) {
-    // stage this chunk's ids and masks (positions past the row: owners 0, all latest)
-#pragma unroll 4
-    for (int x = j; x < kLaneChunk; x += NP) {
-      const int t = base + x;
-      uint32_t o = 0u, l = 0xffffffffu;
-      if (t < len) {
-        const uint32_t id = __ldg(ids + beg + t);
-        if (id < id_space) {
-          const ulonglong2 m = __ldg(ol + id);
-          o = static_cast<uint32_t>(m.x);
-          l = static_cast<uint32_t>(m.y);
-        } else {
-          bad = true;
-        }
-      }
-      own[x] = o;
-      lat[x] = l;
-    }
-    __syncwarp();
-    // this lane's active ids of the chunk (latest copy not on worker j)
-    uint32_t act[CW];
-#pragma unroll
-    for (int w = 0; w < CW; ++w) {
-      uint32_t m = 0;
-#pragma unroll 8
-      for (int b = 0; b < 32; ++b) m |= ((~lat[32 * w + b] >> j) & 1u) << b;
-      act[w] = cell ? m : 0u;
-    }
-    // next active position after t (kLaneChunk when none)
-    auto next = [&](int t) {
-      const int s = t + 1;
-#pragma unroll
-      for (int w = 0; w < CW; ++w) {
-        const uint32_t m = s <= 32 * w ? act[w] : (s >= 32 * (w + 1) ? 0u : act[w] & (~0u << (s - 32 * w)));
-        if (m) return 32 * w + __ffs(m) - 1;
-      }
-      return kLaneChunk;
-    };
-    int t = next(-1);
-    bool pull = t < kLaneChunk;
-    uint32_t om = pull ? own[t] : 0u;
-    while (__any_sync(0xffffffffu, t < kLaneChunk)) {
-      const bool live = t < kLaneChunk;
-      const int src = live ? (pull ? j : __ffs(om) - 1) : 0;
-      const double v = __shfl_sync(0xffffffffu, uj, g * NP + src);
-      if (live) {
-        c = __dadd_rn(c, v);  // a pull over j's link, or one owner's push
-        if (pull) pull = false;
-        else om &= om - 1;
-        if (!pull && om == 0) {
-          t = next(t);
-          if (t < kLaneChunk) {
-            om = own[t];
-            pull = true;
-          }
-        }
-      }
-    }
-    __syncwarp();
-  }
-  if (bad) atomicOr(flags + kFlagIdOutOfRange, 1);
-  if (cell) matrix[i * n + j] = c;
-  if (gap_keys == nullptr) return;
-  const double inf = __longlong_as_double(0x7ff0000000000000LL);
-  double s1 = cell ? c : inf, s2 = inf;
-#pragma unroll
-  for (int off = NP / 2; off > 0; off >>= 1) {
-    const double b1 = __shfl_xor_sync(0xffffffffu, s1, off, NP);
-    const double b2 = __shfl_xor_sync(0xffffffffu, s2, off, NP);
-    const double lo = s1 < b1 ? s1 : b1, hi = s1 < b1 ? b1 : s1;
-    const double m2 = s2 < b2 ? s2 : b2;
-    s1 = lo;
-    s2 = hi < m2 ? hi : m2;
-  }
-  if (rowok && j == 0) {
-    gap_keys[i] = gap_sort_key(__dsub_rn(s2, s1));
-    row_index[i] = static_cast<uint32_t>(i);
-  }
-}
-
 // K1 for 32 < n <= 64 (NP = 64): one row per warp, two cells per lane
 // (workers j and j + 32: two independent chains over the same lists).  A group of G = min(NP, 32) lanes
 // loads G consecutive ids of its row (one per lane) and their masks; a ballot
@@ -698,28 +572,6 @@ void launch_cost_build(const uint32_t* ids, const uint64_t* offsets, uint64_t ro
       kern<<<blocks, kWarpRowsThreads, 0, s>>>(ids, offsets, rows, n, ol, id_space, ucost, matrix,
                                                gap_keys, row_index, flags);
     };
-    static const bool lane_chains = [] {  // EDX_K1=lane: the lane-chain kernel (A/B)
-      const char* v = std::getenv("EDX_K1");
-      return v && std::strcmp(v, "lane") == 0;
-    }();
-    if (lane_chains && np <= 32) {
-      const uint64_t rpb = static_cast<uint64_t>(kLaneThreads / 32) * (32 / np);
-      const unsigned lb = static_cast<unsigned>((rows + rpb - 1) / rpb);
-      auto gl = [&](auto kern, const char* name) {
-        kern<<<lb, kLaneThreads, 0, s>>>(ids, offsets, rows, n, ol, id_space, ucost, matrix,
-                                         gap_keys, row_index, flags);
-        g_kernel_name[kKBuild] = name;
-      };
-      switch (np) {
-        case 2: gl(k_cost_build_lane<2>, "k_cost_build_lane<2>"); break;
-        case 4: gl(k_cost_build_lane<4>, "k_cost_build_lane<4>"); break;
-        case 8: gl(k_cost_build_lane<8>, "k_cost_build_lane<8>"); break;
-        case 16: gl(k_cost_build_lane<16>, "k_cost_build_lane<16>"); break;
-        default: gl(k_cost_build_lane<32>, "k_cost_build_lane<32>"); break;
-      }
-      EDX_LAUNCHED();
-      return;
-    }
     switch (np) {
       case 2: go(k_cost_build_warp<2>); g_kernel_name[kKBuild] = "k_cost_build_warp<2>"; break;
       case 4: go(k_cost_build_warp<4>); g_kernel_name[kKBuild] = "k_cost_build_warp<4>"; break;

@@ -901,9 +901,14 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
     return q;
   };
   auto table = [&](size_t bytes) { return AMODE == 3 ? gtake(bytes) : stake(bytes); };
+  // the operand table A, block-major: A[w * Kp + c - 1] = (S[p[c]][w] - u[p[c]]) << 6, so
+  // a chunk's lanes (consecutive columns) read consecutive words -- the column-major
+  // layout put every lane of a chunk in one shared-memory bank; Kp odd for the row
+  // end's column-wise writes
+  const size_t Kp = static_cast<size_t>(k) | 1;
   int64_t* A;
-  if constexpr (AMODE <= 1) A = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(k) * n * 8));
-  else A = reinterpret_cast<int64_t*>(gtake(static_cast<size_t>(k) * n * 8));
+  if constexpr (AMODE <= 1) A = reinterpret_cast<int64_t*>(stake(static_cast<size_t>(n) * Kp * 8));
+  else A = reinterpret_cast<int64_t*>(gtake(static_cast<size_t>(n) * Kp * 8));
   int64_t* Btab = reinterpret_cast<int64_t*>(stake(K1 * 8));  // by column: block - (v << 6)
   int64_t* u = reinterpret_cast<int64_t*>(table(K1 * 8));
   int64_t* v = reinterpret_cast<int64_t*>(table(K1 * 8));
@@ -918,7 +923,9 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
   // reached-column list of the row being solved, one 16-byte entry per step:
   // {c | p[c] << 16, way (entry index of the predecessor), delta at reach}
   int4* L = reinterpret_cast<int4*>(table((K1 + 32) * 16));
-  int64_t* GA = reinterpret_cast<int64_t*>(stake(2 * 32 * 32 * 8));  // chunk: per-step G of each block
+  // chunk: per-step G of each block, rows padded to 33 so the run end's read
+  // across blocks (one step, lanes = blocks) hits distinct banks
+  int64_t* GA = reinterpret_cast<int64_t*>(stake(2 * 32 * 33 * 8));
   uint64_t* mbar = reinterpret_cast<uint64_t*>(stake(16));            // chunk exchange barrier
   int32_t* ordflag = reinterpret_cast<int32_t*>(stake(16));           // block orders still identity?
   uint32_t* pfail = reinterpret_cast<uint32_t*>(stake(2 * 32 * 4));  // chunk: fail masks
@@ -1042,9 +1049,9 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
         c = ordid ? q + 1 : ord[q];
         Bc = Btab[c];
         r = rtab[c];
-        Aw = A[static_cast<size_t>(c - 1) * n + ws];
+        Aw = A[static_cast<size_t>(ws) * Kp + (c - 1)];
 #pragma unroll
-        for (int h = 0; h < BPW; ++h) Ax[h] = A[static_cast<size_t>(c - 1) * n + xa[h]];
+        for (int h = 0; h < BPW; ++h) Ax[h] = A[static_cast<size_t>(xa[h]) * Kp + (c - 1)];
       };
       auto scan = [&](int64_t dl, const int64_t (&Ax)[BPW], int64_t& Ss, int64_t (&M)[BPW]) {
         Ss = dl;
@@ -1098,9 +1105,8 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
         if (lane == 0) pfail[par * 32 + warp] = failx;
 #pragma unroll
         for (int h = 0; h < BPW; ++h)
-          if (own[h]) GA[(par * 32 + xs[h]) * 32 + lane] = Ga[h];
-        // one arrival per warp (lane 0, after the warp's shared writes):
-        // 512 per-thread arrivals on one barrier word serialise at n = 16
+          if (own[h]) GA[(par * 32 + xs[h]) * 33 + lane] = Ga[h];
+        // one arrival per warp (lane 0, after the warp's shared writes)
         __syncwarp();
         if (lane == 0) mbar_arrive(mbar);
         // speculative next chunk (this one complete, the run continuing)
@@ -1179,7 +1185,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
           }
         }
         if (lane < n)
-          Gy = vq > 0 ? GA[(par * 32 + lane) * 32 + vq - 1] : GA[((par ^ 1) * 32 + lane) * 32 + 31];
+          Gy = vq > 0 ? GA[(par * 32 + lane) * 33 + vq - 1] : GA[((par ^ 1) * 32 + lane) * 33 + 31];
         // the winner's next key offset: lane vq of this chunk, or lane 0 of the next
         const int64_t bnext = __shfl_sync(0xffffffffu, vq < 32 ? Bc : Bc2, vq < 32 ? vq : 0);
         par ^= 1;
@@ -1240,8 +1246,8 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
           }
         }
         if (lw < n) {
-          if (act0 && c0 != 0 && r0 > 0) A[static_cast<size_t>(c0 - 1) * n + lw] = (s0 - u0) << 6;
-          if (act1 && r1 > 0) A[static_cast<size_t>(c1 - 1) * n + lw] = (s1 - u1) << 6;
+          if (act0 && c0 != 0 && r0 > 0) A[static_cast<size_t>(lw) * Kp + (c0 - 1)] = (s0 - u0) << 6;
+          if (act1 && r1 > 0) A[static_cast<size_t>(lw) * Kp + (c1 - 1)] = (s1 - u1) << 6;
         }
       }
     }
@@ -1268,7 +1274,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
           p[jj] = rn;
           rtab[jj] = rn;
         }
-        if (lane < n) A[static_cast<size_t>(jj - 1) * n + lane] = (sv - ur) << 6;
+        if (lane < n) A[static_cast<size_t>(lane) * Kp + (jj - 1)] = (sv - ur) << 6;
         ent = prv;
       }
     }
@@ -1321,8 +1327,8 @@ size_t mw_smem_bytes(int k, int n, int mult, int amode) {
   auto r = [](size_t b) { return (b + 15) & ~size_t(15); };
   size_t b = 0;
   if (amode == 0) b += r(static_cast<size_t>(k) * n * 8);
-  if (amode <= 1) b += r(static_cast<size_t>(k) * n * 8);
-  b += r(K1 * 8) + r(K1 * 4) + r(32 * 4) + r(2 * 32 * 32 * 8) + r(16) + r(16) + r(2 * 32 * 4);
+  if (amode <= 1) b += r(static_cast<size_t>(n) * (static_cast<size_t>(k) | 1) * 8);
+  b += r(K1 * 8) + r(K1 * 4) + r(32 * 4) + r(2 * 32 * 33 * 8) + r(16) + r(16) + r(2 * 32 * 4);
   if (amode <= 2)  // the tables AMODE 3 keeps in the global arena
     b += 2 * r(K1 * 8) + r((K1 + 32) * 8) + 3 * r(K1 * 4) + 2 * r((K1 + 32) * 4) +
          r((K1 + 32) * 16) + r(static_cast<size_t>(2 * mult) * 4);
@@ -1333,7 +1339,7 @@ size_t mw_smem_bytes(int k, int n, int mult, int amode) {
 size_t mw_arena_bytes(int k, int n, int mult, int amode) {
   const size_t K1 = static_cast<size_t>(k) + 1;
   auto r = [](size_t b) { return (b + 15) & ~size_t(15); };
-  size_t b = r(static_cast<size_t>(k) * n * 8);
+  size_t b = r(static_cast<size_t>(n) * (static_cast<size_t>(k) | 1) * 8);
   if (amode == 3)
     b += 2 * r(K1 * 8) + r((K1 + 32) * 8) + 3 * r(K1 * 4) + 2 * r((K1 + 32) * 4) +
          r((K1 + 32) * 16) + r(static_cast<size_t>(2 * mult) * 4);

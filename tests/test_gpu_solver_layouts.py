@@ -43,15 +43,3 @@ def test_global_table_layout(gpu, oracle, tmp_path, n, mult, seed):
     cols, total = oracle.hungarian(sq)
     assert got["cols"] == [int(x) for x in cols]
     assert got["total"] == total
-
-
-def test_lane_chain_cost_build(gpu):
-    """K1's lane-chain kernel (EDX_K1=lane, read once per process) through the
-    bitwise build tests of test_gpu_matrix.py and the engine parity runs."""
-    env = dict(os.environ, EDX_K1="lane")
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-m", "gpu",
-                        os.path.join(ROOT, "tests", "test_gpu_matrix.py"),
-                        os.path.join(ROOT, "tests", "test_gpu_engine.py"), "-k",
-                        "build or c1 or c2 or pressure"],
-                       capture_output=True, text=True, env=env, timeout=1200, cwd=ROOT)
-    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
