@@ -43,55 +43,71 @@ void sort_rows_by_gap(SortScratch& sc, const uint64_t* keys_in, const uint32_t* 
 namespace {
 
 
-// Each position's eight best workers among the initially open ones, in
-// (cost, index) order -- strict '<' over ascending j, as the reference's scan
-// (assign.hpp:177-184) -- packed 8 bits each (0xFF = none).  One thread per
-// position, grid-wide: the matrix is read once.
-constexpr int kPrefs = 8;
+// Each position's whole preference list: its initially open workers in
+// (cost, index) order -- the order in which the reference's scan
+// (assign.hpp:177-184: ascending j, strict '<') would pick them as workers
+// close -- one byte each, 0xFF past the last.  One warp per position, a
+// 64-element bitonic sort in registers (two elements per lane).  The greedy
+// then takes the first still-open entry: no rescan of the row's costs.
+constexpr int kListBytes = 64;
+
+__device__ __forceinline__ bool pref_less(double ca, int ia, double cb, int ib) {
+  return ca < cb || (!(cb < ca) && ia < ib);
+}
 
 __global__ void k_greedy_prefs(const double* __restrict__ matrix, int n,
                                const uint32_t* __restrict__ order, uint64_t n_order,
                                const int32_t* __restrict__ capacity_dev, int cap_uniform,
-                               uint64_t* __restrict__ prefs) {
-  const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  if (t >= n_order) return;
+                               uint8_t* __restrict__ prefs) {
+  const uint64_t t = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= n_order) return;  // warp-uniform
   const double* r = matrix + static_cast<uint64_t>(order[t]) * n;
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
-  double cb[kPrefs];
-  int wb[kPrefs];
+  double c[2];
+  int id[2];
 #pragma unroll
-  for (int q = 0; q < kPrefs; ++q) {
-    cb[q] = inf;
-    wb[q] = 0xFF;
+  for (int h = 0; h < 2; ++h) {
+    const int w = h * 32 + lane;
+    const bool open = w < n && (capacity_dev ? capacity_dev[w] : cap_uniform) > 0;
+    c[h] = open ? r[w] : inf;
+    id[h] = open ? w : 0xFF;
   }
-  for (int w = 0; w < n; ++w) {
-    if ((capacity_dev ? capacity_dev[w] : cap_uniform) <= 0) continue;
-    const double c = r[w];
-    if (!(c < cb[kPrefs - 1])) continue;
-    // insertion keeps equal costs in index order (strict '<')
-    bool placed = false;
+  // bitonic sort of element e = h * 32 + lane, ascending by (cost, index)
 #pragma unroll
-    for (int q = kPrefs - 1; q > 0; --q) {
-      if (!placed) {
-        if (c < cb[q - 1]) {
-          cb[q] = cb[q - 1];
-          wb[q] = wb[q - 1];
-        } else {
-          cb[q] = c;
-          wb[q] = w;
-          placed = true;
+  for (int size = 2; size <= 64; size <<= 1) {
+#pragma unroll
+    for (int d = size >> 1; d > 0; d >>= 1) {
+      if (d == 32) {
+        const bool asc = (lane & size) == 0;  // size == 64: always ascending
+        const bool gt = pref_less(c[1], id[1], c[0], id[0]);
+        if (gt == asc) {
+          const double tc = c[0];
+          const int ti = id[0];
+          c[0] = c[1];
+          id[0] = id[1];
+          c[1] = tc;
+          id[1] = ti;
+        }
+      } else {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const double oc = __shfl_xor_sync(0xffffffffu, c[h], d);
+          const int oi = __shfl_xor_sync(0xffffffffu, id[h], d);
+          const bool asc = ((h * 32 + lane) & size) == 0;
+          const bool lower = (lane & d) == 0;
+          const bool other_less = pref_less(oc, oi, c[h], id[h]);
+          if ((lower == asc) ? other_less : !other_less) {
+            c[h] = oc;
+            id[h] = oi;
+          }
         }
       }
     }
-    if (!placed) {
-      cb[0] = c;
-      wb[0] = w;
-    }
   }
-  uint64_t pk = 0;
-#pragma unroll
-  for (int q = 0; q < kPrefs; ++q) pk |= static_cast<uint64_t>(wb[q]) << (8 * q);
-  prefs[t] = pk;
+  uint8_t* out = prefs + t * kListBytes;
+  out[lane] = static_cast<uint8_t>(id[0]);
+  out[32 + lane] = static_cast<uint8_t>(id[1]);
 }
 
 constexpr int kGreedyThreads = 1024;
@@ -102,10 +118,10 @@ __global__ void __launch_bounds__(kGreedyThreads)
              uint64_t n_order, const int32_t* __restrict__ capacity_dev, int cap_uniform,
              int32_t* __restrict__ decision, const uint32_t* __restrict__ row_ids,
              int32_t* __restrict__ pair_worker, int* __restrict__ flags,
-             const uint64_t* __restrict__ prefs) {
+             const uint8_t* __restrict__ prefs) {
   __shared__ int remaining[kMaxWorkers];
   __shared__ int used[kMaxWorkers];
-  __shared__ int cnt[kGreedyWarps][kMaxWorkers];
+  __shared__ int cnt[kGreedyWarps][kMaxWorkers + 1];  // +1: a column read is conflict-free
   __shared__ unsigned long long open_mask;
   __shared__ int qmin;
 
@@ -122,7 +138,7 @@ __global__ void __launch_bounds__(kGreedyThreads)
 
   uint64_t start = 0;
   while (start < n_order) {
-    for (int x = tid; x < kGreedyWarps * kMaxWorkers; x += kGreedyThreads)
+    for (int x = tid; x < kGreedyWarps * (kMaxWorkers + 1); x += kGreedyThreads)
       (&cnt[0][0])[x] = 0;
     if (tid < kMaxWorkers) used[tid] = 0;
     if (tid == 0) qmin = kGreedyThreads;
@@ -135,34 +151,17 @@ __global__ void __launch_bounds__(kGreedyThreads)
     if (valid) {
       row = order[t];
       const unsigned long long om = open_mask;
-      // The first of the position's eight best (initially open) workers that is
-      // still open is its argmin over the open set: every worker ranked before
-      // it is closed.  Only when all eight are closed is the row rescanned.
-      const uint64_t pf = prefs[t];
+      // the first still-open worker of the position's preference list is its
+      // argmin over the open set: every worker ranked before it is closed
+      const uint4* lst = reinterpret_cast<const uint4*>(prefs + t * kListBytes);
+      const int nv = (n + 15) >> 4;
+      for (int q = 0; q < nv && choice < 0; ++q) {
+        const uint4 v4 = lst[q];
+        const uint32_t wd[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
-      for (int q = 0; q < kPrefs; ++q) {
-        const int w = static_cast<int>((pf >> (8 * q)) & 0xFFu);
-        if (choice < 0 && w != 0xFF && ((om >> w) & 1ULL)) choice = w;
-      }
-      if (choice < 0) {
-        const double* r = matrix + static_cast<uint64_t>(row) * n;
-        double best = __longlong_as_double(0x7ff0000000000000LL);
-        // sixteen workers per group, all of a group's loads in flight before
-        // the ascending strict-'<' compares (closed workers read as +inf,
-        // which never beats `best`)
-        for (int base = 0; base < n; base += 16) {
-          double c[16];
-#pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            const int w = base + k;
-            c[k] = (w < n && ((om >> w) & 1ULL)) ? r[w] : best;
-          }
-#pragma unroll
-          for (int k = 0; k < 16; ++k)
-            if (c[k] < best) {
-              best = c[k];
-              choice = base + k;
-            }
+        for (int b = 0; b < 16; ++b) {
+          const int w = static_cast<int>((wd[b >> 2] >> (8 * (b & 3))) & 0xFFu);
+          if (choice < 0 && w != 0xFF && ((om >> w) & 1ULL)) choice = w;
         }
       }
       if (choice < 0) atomicOr(flags + kFlagUnbalanced, 1);  // "capacities exhausted"
@@ -172,12 +171,20 @@ __global__ void __launch_bounds__(kGreedyThreads)
     const int rank_in_warp = __popc(peers & ((1u << lane) - 1));
     if (choice >= 0 && rank_in_warp == 0) cnt[warp][choice] = __popc(peers);
     __syncthreads();
-    if (tid < n) {  // exclusive scan over warps, per worker
-      int run = 0;
-      for (int wp = 0; wp < kGreedyWarps; ++wp) {
-        const int v = cnt[wp][tid];
-        cnt[wp][tid] = run;
-        run += v;
+    // exclusive scan over warps, per worker: warp x scans workers x and x + 32,
+    // lanes = warps (one shuffle scan instead of a 32-step serial walk)
+#pragma unroll
+    for (int h = 0; h < kMaxWorkers / kGreedyWarps; ++h) {
+      const int w = warp + h * kGreedyWarps;
+      if (w < n) {  // warp-uniform
+        const int v = cnt[lane][w];
+        int inc = v;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, inc, off);
+          if (lane >= off) inc += y;
+        }
+        cnt[lane][w] = inc - v;
       }
     }
     __syncthreads();
@@ -247,8 +254,8 @@ void launch_greedy(const double* matrix, uint64_t rows, int n, const uint32_t* o
                    int* flags, GreedyScratch& g, cudaStream_t s) {
   (void)rows;
   if (n_order == 0) return;
-  g.prefs.ensure(n_order);
-  k_greedy_prefs<<<static_cast<unsigned>((n_order + 255) / 256), 256, 0, s>>>(
+  g.prefs.ensure(n_order * kListBytes);
+  k_greedy_prefs<<<static_cast<unsigned>((n_order * 32 + 255) / 256), 256, 0, s>>>(
       matrix, n, order, n_order, capacity_dev, cap_uniform, g.prefs.p);
   g_kernel_name[kKGreedy] = "k_greedy";
   k_greedy<<<1, kGreedyThreads, 0, s>>>(matrix, n, order, n_order, capacity_dev, cap_uniform,

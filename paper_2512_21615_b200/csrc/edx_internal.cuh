@@ -172,9 +172,9 @@ struct SortScratch {
 };
 void sort_rows_by_gap(SortScratch& sc, const uint64_t* keys_in, const uint32_t* idx_in,
                       uint32_t* idx_out, uint64_t rows, cudaStream_t s);
-// K4 scratch: each position's eight best initially-open workers
+// K4 scratch: each position's preference list (64 bytes)
 struct GreedyScratch {
-  DevBuf<uint64_t> prefs;
+  DevBuf<uint8_t> prefs;
 };
 void launch_greedy(const double* matrix, uint64_t rows, int n, const uint32_t* order,
                    uint64_t n_order, const int32_t* capacity_dev, int cap_uniform,
