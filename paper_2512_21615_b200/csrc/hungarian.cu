@@ -985,11 +985,17 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
   }
   int par = 0;         // publish slot parity (identical in every warp)
   unsigned mbph = 0;   // mbarrier phase parity
-  unsigned long long steps = 0;
-  long long c_step = 0, c_end = 0, c_pot = 0, c_ref = 0, runs = 0, sorts = 0;
-  const long long c_start = clock64();
+  // solver statistics, kept by thread 0 in shared memory (no registers live
+  // across the loop): [0] steps [1] run cycles [2] row-end cycles [3] re-sorts
+  // [4] potential cycles [5] runs [6] re-sort-check cycles [7] start
+  // [8] row start [9] t2 [10] t3
+  __shared__ unsigned long long sst[11];
+  if (tid == 0) {
+    for (int q = 0; q < 11; ++q) sst[q] = 0;
+    sst[7] = clock64();
+  }
   for (int i = 1; i <= k; ++i) {
-    const long long t1 = clock64();
+    if (tid == 0) sst[8] = clock64();
     // Row frame: Q = cumulative delta of this row's search (<< 6).  Block y
     // keeps G_y = E_y + Q (its least relaxed value, unshifted by the deltas),
     // the key offset B_y of its next column and its cursor d_y; every warp
@@ -1189,10 +1195,12 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
         // the winner's next key offset: lane vq of this chunk, or lane 0 of the next
         const int64_t bnext = __shfl_sync(0xffffffffu, vq < 32 ? Bc : Bc2, vq < 32 ? vq : 0);
         par ^= 1;
-        ++runs;
+        if (tid == 0) {
+          sst[0] += sN;
+          sst[5] += 1;
+        }
         Q = P;
         nused = nused0 + sN;
-        steps += sN;
         if (lane == ws) {  // lane ws holds the winner's cursor and key offset
           dy += sN;
           By = dy < mult ? bnext : kBig;
@@ -1207,8 +1215,11 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
     const int64_t Dl = Q >> 6;
     if (warp == 0 && lane < n) curs[lane] = dy;
     __syncthreads();
-    const long long t2 = clock64();
-    c_step += t2 - t1;
+    if (tid == 0) {
+      const unsigned long long t2 = clock64();
+      sst[1] += t2 - sst[8];
+      sst[9] = t2;
+    }
     const int nu = nused;
     // Potentials (assign.hpp:131-138) fused with the operand-table refresh:
     // reached column c moves by dd_c = Dl - dlt[c] (v[c] -= dd_c, u[p[c]] +=
@@ -1253,8 +1264,11 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
     }
     if constexpr (AMODE >= 2) __threadfence_block();
     __syncthreads();
-    const long long t3 = clock64();
-    c_pot += t3 - t2;
+    if (tid == 0) {
+      const unsigned long long t3 = clock64();
+      sst[4] += t3 - sst[9];
+      sst[10] = t3;
+    }
     // augment (assign.hpp:141-145) on the first warp whose block was not
     // touched, so it overlaps the re-sort checks.  Each hop is one entry load
     // (the predecessor's entry carries its column and old row); the path
@@ -1283,7 +1297,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
       if (curs[w] == 0) continue;
       if (!warp_block_sorted(ord, v, w * mult, mult, lane)) {
         if (lane == 0) {
-          ++sorts;
+          atomicAdd(&sst[3], 1ULL);
           ordflag[0] = 0;
         }
         warp_resort_dispatch(ord, v, w * mult, mult, lane);
@@ -1292,9 +1306,11 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
     }
     if constexpr (AMODE >= 2) __threadfence_block();
     __syncthreads();
-    const long long t4 = clock64();
-    c_ref += t4 - t3;
-    c_end += t4 - t2;
+    if (tid == 0) {
+      const unsigned long long t4 = clock64();
+      sst[6] += t4 - sst[10];
+      sst[2] += t4 - sst[9];
+    }
   }
   for (int j = tid + 1; j <= k; j += blockDim.x) {
     const int r = p[j] - 1;
@@ -1306,19 +1322,9 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
   }
   if (stats == nullptr) return;
   __syncthreads();
-  if (tid == 0) curs[0] = 0;
-  __syncthreads();
-  if (lane == 0) atomicAdd(curs, static_cast<int>(sorts));
-  __syncthreads();
   if (tid == 0) {
-    stats[0] = steps;
-    stats[1] = c_step;
-    stats[2] = c_end;
-    stats[3] = static_cast<unsigned long long>(curs[0]);  // blocks that needed a full re-sort
-    stats[4] = c_pot;
-    stats[5] = runs;
-    stats[6] = c_ref;
-    stats[7] = clock64() - c_start;
+    for (int q = 0; q < 7; ++q) stats[q] = sst[q];  // [3]: blocks that needed a full re-sort
+    stats[7] = clock64() - sst[7];
   }
 }
 

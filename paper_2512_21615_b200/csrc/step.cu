@@ -1219,9 +1219,11 @@ void step_init_state(edx_engine* e) {
     EDX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_big_select, big::kThreads, 0));
     EDX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device));
     if (per_sm < 1) throw Error(EDX_CUDA_ERROR, "victim selection kernel cannot be resident");
-    // enough CTAs for the work units, at most two per SM
+    // enough CTAs for the work units, one per SM and two SMs' worth of room:
+    // a cooperative grid starts only when all its CTAs are resident, and the
+    // step runs beside decision_cost (a 1024-thread CTA on the side stream)
     const uint64_t units = n * ((e->capacity + big::kChunk - 1) / big::kChunk);
-    s.big_grid = std::max<uint64_t>(1, std::min<uint64_t>(units, static_cast<uint64_t>(std::min(per_sm, 2)) * sms));
+    s.big_grid = std::max<uint64_t>(1, std::min<uint64_t>(units, sms > 2 ? sms - 2 : 1));
   }
   s.cand_off.ensure(128);  // [0,64): workers 0..n-1; [64,128): evicting workers (large caches)
   std::vector<int32_t> wl(n);
