@@ -873,7 +873,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
                           int64_t* __restrict__ A_global, const uint32_t* __restrict__ order,
                           int32_t* __restrict__ decision, const uint32_t* __restrict__ row_ids,
                           uint64_t* __restrict__ col_of_row, unsigned long long* stats, int* flags,
-                          const unsigned long long* __restrict__ max_scaled) {
+                          const unsigned long long* __restrict__ max_scaled, int timing) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const size_t K1 = static_cast<size_t>(k) + 1;
@@ -988,14 +988,15 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
   // solver statistics, kept by thread 0 in shared memory (no registers live
   // across the loop): [0] steps [1] run cycles [2] row-end cycles [3] re-sorts
   // [4] potential cycles [5] runs [6] re-sort-check cycles [7] start
-  // [8] row start [9] t2 [10] t3
+  // [8] row start [9] t2 [10] t3; the cycle counters only when `timing`
+  // (EDX_SOLVER_TIMING=1, tools/solver_profile.py)
   __shared__ unsigned long long sst[11];
   if (tid == 0) {
     for (int q = 0; q < 11; ++q) sst[q] = 0;
     sst[7] = clock64();
   }
   for (int i = 1; i <= k; ++i) {
-    if (tid == 0) sst[8] = clock64();
+    if (tid == 0 && timing) sst[8] = clock64();
     // Row frame: Q = cumulative delta of this row's search (<< 6).  Block y
     // keeps G_y = E_y + Q (its least relaxed value, unshifted by the deltas),
     // the key offset B_y of its next column and its cursor d_y; every warp
@@ -1215,7 +1216,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
     const int64_t Dl = Q >> 6;
     if (warp == 0 && lane < n) curs[lane] = dy;
     __syncthreads();
-    if (tid == 0) {
+    if (tid == 0 && timing) {
       const unsigned long long t2 = clock64();
       sst[1] += t2 - sst[8];
       sst[9] = t2;
@@ -1264,7 +1265,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
     }
     if constexpr (AMODE >= 2) __threadfence_block();
     __syncthreads();
-    if (tid == 0) {
+    if (tid == 0 && timing) {
       const unsigned long long t3 = clock64();
       sst[4] += t3 - sst[9];
       sst[10] = t3;
@@ -1306,7 +1307,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
     }
     if constexpr (AMODE >= 2) __threadfence_block();
     __syncthreads();
-    if (tid == 0) {
+    if (tid == 0 && timing) {
       const unsigned long long t4 = clock64();
       sst[6] += t4 - sst[10];
       sst[2] += t4 - sst[9];
@@ -1711,6 +1712,10 @@ void launch_hungarian_blocks(HungarianScratch& sc, const double* matrix, int n,
     const char* e = std::getenv("EDX_MW_BPW");
     return e && std::strcmp(e, "2") == 0 ? 2 : 1;
   }();
+  static const int timing = [] {  // EDX_SOLVER_TIMING=1: per-phase cycle counters
+    const char* e = std::getenv("EDX_SOLVER_TIMING");
+    return e && std::strcmp(e, "1") == 0 ? 1 : 0;
+  }();
   static const int amode_min = [] {  // EDX_MW_GLOBAL=1: the global-table layout (tests)
     const char* e = std::getenv("EDX_MW_GLOBAL");
     return e && std::strcmp(e, "1") == 0 ? 3 : 0;
@@ -1731,7 +1736,7 @@ void launch_hungarian_blocks(HungarianScratch& sc, const double* matrix, int n,
           EDX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(smem)));
         kern<<<1, 32 * nwarps, smem, s>>>(sc.s64.p, n, mult, k, Ag, order, decision, row_ids,
-                                          col_of_row, sc.steps.p, flags, max_scaled);
+                                          col_of_row, sc.steps.p, flags, max_scaled, timing);
       };
       // the warp cap sets the register budget: 255 (n <= 8), 128 (n <= 32)
       if (pair && n <= 16) {

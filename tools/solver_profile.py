@@ -11,6 +11,7 @@ import time
 
 import numpy as np
 
+os.environ.setdefault("EDX_SOLVER_TIMING", "1")  # the solver's per-phase cycle counters
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import bench  # noqa: E402
