@@ -1006,10 +1006,13 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
     // re-sort check at row end); while they do, position q of the order is
     // column q + 1 and the ord lookup drops off the critical path.
     const bool ordid = ordflag[0] != 0;
-    int64_t Gy = kBig, By = kBig;
+    // Row i enters with u[i] = 0 (rows are solved in order); its costs stay
+    // in a register for the augment's hop from column 0.
+    int64_t Gy = kBig, By = kBig, srow = 0;
     int dy = 0;
     if (lane < n) {
-      Gy = (S[static_cast<size_t>(i - 1) * n + lane] - u[i]) << 6;  // relax from row i
+      srow = S[static_cast<size_t>(i - 1) * n + lane];
+      Gy = srow << 6;  // relax from row i
       By = Btab[ordid ? lane * mult + 1 : ord[lane * mult]];
     }
     int wyx[BPW];
@@ -1224,9 +1227,11 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
     const int nu = nused;
     // Potentials (assign.hpp:131-138) fused with the operand-table refresh:
     // reached column c moves by dd_c = Dl - dlt[c] (v[c] -= dd_c, u[p[c]] +=
-    // dd_c), and unless c is on the augmenting path its row stays p[c], whose
-    // new potential is exactly u[p[c]] + dd_c.  A group of gs >= n lanes per
-    // column, lanes over workers; two columns per group in flight.
+    // dd_c).  Unless c is on the augmenting path its row stays p[c], so its
+    // operand words A[w][c] = (S[p[c]][w] - u[p[c]]) << 6 just drop by
+    // dd_c << 6 -- no cost-matrix read.  u itself is never read again (a row's
+    // potential lives only in its column's A words), so it is not kept.  A group
+    // of gs >= n lanes per column, lanes over workers; two columns per group.
     {
       const int gs = n <= 8 ? 8 : (n <= 16 ? 16 : 32);
       const int gpw = 32 / gs, sub = lane / gs, lw = lane - sub * gs;
@@ -1239,27 +1244,22 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
         const int c0 = q0.x & 0xffff, r0 = q0.x >> 16, c1 = q1.x & 0xffff, r1 = q1.x >> 16;
         const int64_t dd0 = Dl - ((static_cast<int64_t>(q0.w) << 32) | static_cast<uint32_t>(q0.z));
         const int64_t dd1 = Dl - ((static_cast<int64_t>(q1.w) << 32) | static_cast<uint32_t>(q1.z));
-        const int64_t u0 = act0 ? u[r0] + dd0 : 0, u1 = act1 ? u[r1] + dd1 : 0;
-        const int64_t v0 = act0 ? v[c0] - dd0 : 0, v1 = act1 ? v[c1] - dd1 : 0;
-        const int64_t b0 = act0 ? cblk[c0] : 0, b1 = act1 ? cblk[c1] : 0;
-        const int64_t s0 = (act0 && r0 > 0 && lw < n) ? S[static_cast<size_t>(r0 - 1) * n + lw] : 0;
-        const int64_t s1 = (act1 && r1 > 0 && lw < n) ? S[static_cast<size_t>(r1 - 1) * n + lw] : 0;
-        __syncwarp();  // every lane has read u[r] before the group leader writes it
+        const bool a0 = act0 && c0 != 0, a1 = act1;  // entry 0 (column 0) is at e == 0 only
         if (lw == 0) {
-          if (act0) {
-            u[r0] = u0;
+          if (a0) {
+            const int64_t v0 = v[c0] - dd0;
             v[c0] = v0;
-            if (c0 != 0) Btab[c0] = b0 - (v0 << 6);
+            Btab[c0] = cblk[c0] - (v0 << 6);
           }
-          if (act1) {
-            u[r1] = u1;
+          if (a1) {
+            const int64_t v1 = v[c1] - dd1;
             v[c1] = v1;
-            Btab[c1] = b1 - (v1 << 6);
+            Btab[c1] = cblk[c1] - (v1 << 6);
           }
         }
         if (lw < n) {
-          if (act0 && c0 != 0 && r0 > 0) A[static_cast<size_t>(lw) * Kp + (c0 - 1)] = (s0 - u0) << 6;
-          if (act1 && r1 > 0) A[static_cast<size_t>(lw) * Kp + (c1 - 1)] = (s1 - u1) << 6;
+          if (a0 && r0 > 0) A[static_cast<size_t>(lw) * Kp + (c0 - 1)] -= dd0 << 6;
+          if (a1 && r1 > 0) A[static_cast<size_t>(lw) * Kp + (c1 - 1)] -= dd1 << 6;
         }
       }
     }
@@ -1277,19 +1277,24 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
     const unsigned untouched = __ballot_sync(0xffffffffu, lane < n && curs[lane] == 0);
     const int aug_warp = untouched ? (__ffs(untouched) - 1) % nw : 0;
     if (warp == aug_warp) {
+      // the operand words move with the rows: jj takes its predecessor's row
+      // and so that column's (already updated) words, read before the next hop
+      // overwrites them; from column 0 it takes row i, (S[i] - Dl) << 6
+      const int64_t wi = (srow - Dl) << 6;
       int4 ent = L[nu - 1];
       for (;;) {
         const int jj = ent.x & 0xffff;
         if (jj == 0) break;
         const int4 prv = L[ent.y];
-        const int rn = prv.x >> 16;  // p[jj] = p[way[jj]]
-        const int64_t ur = u[rn];
-        const int64_t sv = lane < n ? S[static_cast<size_t>(rn - 1) * n + lane] : 0;
+        const int rn = prv.x >> 16, pc = prv.x & 0xffff;  // p[jj] = p[way[jj]]
         if (lane == 0) {
           p[jj] = rn;
           rtab[jj] = rn;
         }
-        if (lane < n) A[static_cast<size_t>(lane) * Kp + (jj - 1)] = (sv - ur) << 6;
+        if (lane < n) {
+          const int64_t w = pc == 0 ? wi : A[static_cast<size_t>(lane) * Kp + (pc - 1)];
+          A[static_cast<size_t>(lane) * Kp + (jj - 1)] = w;
+        }
         ent = prv;
       }
     }
