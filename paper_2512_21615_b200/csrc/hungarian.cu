@@ -1227,11 +1227,14 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
     const int nu = nused;
     // Potentials (assign.hpp:131-138) fused with the operand-table refresh:
     // reached column c moves by dd_c = Dl - dlt[c] (v[c] -= dd_c, u[p[c]] +=
-    // dd_c).  Unless c is on the augmenting path its row stays p[c], so its
-    // operand words A[w][c] = (S[p[c]][w] - u[p[c]]) << 6 just drop by
-    // dd_c << 6 -- no cost-matrix read.  u itself is never read again (a row's
-    // potential lives only in its column's A words), so it is not kept.  A group
-    // of gs >= n lanes per column, lanes over workers; two columns per group.
+    // dd_c).  Unless c is on the augmenting path its row stays p[c], so with A
+    // in shared memory its words A[w][c] = (S[p[c]][w] - u[p[c]]) << 6 just
+    // drop by dd_c << 6 -- no cost-matrix read, and u is never read again (a
+    // row's potential lives only in its column's words).  With A in global
+    // memory (AMODE >= 2) a read-modify-write would wait on L2, while S is
+    // read-only (cached): the words are rewritten from S and u is kept.  A
+    // group of gs >= n lanes per column, lanes over workers; two columns per
+    // group, every load issued before the first store.
     {
       const int gs = n <= 8 ? 8 : (n <= 16 ? 16 : 32);
       const int gpw = 32 / gs, sub = lane / gs, lw = lane - sub * gs;
@@ -1244,23 +1247,38 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
         const int c0 = q0.x & 0xffff, r0 = q0.x >> 16, c1 = q1.x & 0xffff, r1 = q1.x >> 16;
         const int64_t dd0 = Dl - ((static_cast<int64_t>(q0.w) << 32) | static_cast<uint32_t>(q0.z));
         const int64_t dd1 = Dl - ((static_cast<int64_t>(q1.w) << 32) | static_cast<uint32_t>(q1.z));
-        const bool a0 = act0 && c0 != 0, a1 = act1;  // entry 0 (column 0) is at e == 0 only
-        if (lw == 0) {
-          if (a0) {
-            const int64_t v0 = v[c0] - dd0;
-            v[c0] = v0;
-            Btab[c0] = cblk[c0] - (v0 << 6);
-          }
-          if (a1) {
-            const int64_t v1 = v[c1] - dd1;
-            v[c1] = v1;
-            Btab[c1] = cblk[c1] - (v1 << 6);
+        // entry 0 (column 0, row i) sits at e == 0 only; the free column (r == 0) has no words
+        const bool a0 = act0 && c0 != 0, a1 = act1;
+        const bool w0 = a0 && r0 > 0 && lw < n, w1 = a1 && r1 > 0 && lw < n;
+        const bool l0 = lw == 0 && a0, l1 = lw == 0 && a1;
+        const int64_t v0 = l0 ? v[c0] - dd0 : 0, v1 = l1 ? v[c1] - dd1 : 0;
+        const int64_t b0 = l0 ? cblk[c0] : 0, b1 = l1 ? cblk[c1] : 0;
+        int64_t* A0 = A + static_cast<size_t>(lw) * Kp + (c0 - 1);
+        int64_t* A1 = A + static_cast<size_t>(lw) * Kp + (c1 - 1);
+        int64_t x0 = 0, x1 = 0;
+        if constexpr (AMODE <= 1) {
+          x0 = w0 ? *A0 - (dd0 << 6) : 0;
+          x1 = w1 ? *A1 - (dd1 << 6) : 0;
+        } else {
+          const int64_t u0 = act0 ? u[r0] + dd0 : 0, u1 = act1 ? u[r1] + dd1 : 0;
+          x0 = w0 ? (S[static_cast<size_t>(r0 - 1) * n + lw] - u0) << 6 : 0;
+          x1 = w1 ? (S[static_cast<size_t>(r1 - 1) * n + lw] - u1) << 6 : 0;
+          __syncwarp();  // every lane has read u[r] before the group leader writes it
+          if (lw == 0) {
+            if (act0) u[r0] = u0;
+            if (act1) u[r1] = u1;
           }
         }
-        if (lw < n) {
-          if (a0 && r0 > 0) A[static_cast<size_t>(lw) * Kp + (c0 - 1)] -= dd0 << 6;
-          if (a1 && r1 > 0) A[static_cast<size_t>(lw) * Kp + (c1 - 1)] -= dd1 << 6;
+        if (l0) {
+          v[c0] = v0;
+          Btab[c0] = b0 - (v0 << 6);
         }
+        if (l1) {
+          v[c1] = v1;
+          Btab[c1] = b1 - (v1 << 6);
+        }
+        if (w0) *A0 = x0;
+        if (w1) *A1 = x1;
       }
     }
     if constexpr (AMODE >= 2) __threadfence_block();
@@ -1280,6 +1298,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
       // the operand words move with the rows: jj takes its predecessor's row
       // and so that column's (already updated) words, read before the next hop
       // overwrites them; from column 0 it takes row i, (S[i] - Dl) << 6
+      // (AMODE >= 2: rebuilt from S and u, see the potentials above)
       const int64_t wi = (srow - Dl) << 6;
       int4 ent = L[nu - 1];
       for (;;) {
@@ -1292,7 +1311,11 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
           rtab[jj] = rn;
         }
         if (lane < n) {
-          const int64_t w = pc == 0 ? wi : A[static_cast<size_t>(lane) * Kp + (pc - 1)];
+          int64_t w;
+          if constexpr (AMODE <= 1)
+            w = pc == 0 ? wi : A[static_cast<size_t>(lane) * Kp + (pc - 1)];
+          else
+            w = (S[static_cast<size_t>(rn - 1) * n + lane] - (pc == 0 ? Dl : u[rn])) << 6;
           A[static_cast<size_t>(lane) * Kp + (jj - 1)] = w;
         }
         ent = prv;
