@@ -15,6 +15,8 @@
 // threads of one row hit the same address (a broadcast), so each id costs
 // one L1/L2 transaction per row.  Loads are batched 4 ids ahead of the add
 // chain to keep memory-level parallelism despite the serial adds.
+#include <cstdlib>
+#include <cstring>
 #include <type_traits>
 
 #include "edx_internal.cuh"
@@ -406,13 +408,7 @@ __global__ void __launch_bounds__(kWarpRowsThreads)
   using M = typename std::conditional<(NP > 32), unsigned long long, unsigned>::type;
   // [warp][buffer][RPW groups x NP list entries]
   __shared__ __align__(16) double lists[NW][2][RPW * NP];
-  __shared__ __align__(16) double zeros[NP];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x < NP) zeros[threadIdx.x] = -0.0;
-  if constexpr (NP > 32) {
-    if (threadIdx.x < NP - 32) zeros[32 + threadIdx.x] = -0.0;
-  }
-  __syncthreads();
   const int g = lane / G, jl = lane - g * G;
   const uint64_t i = (static_cast<uint64_t>(blockIdx.x) * NW + warp) * RPW + g;
   const bool rowok = i < rows;
@@ -495,27 +491,35 @@ __global__ void __launch_bounds__(kWarpRowsThreads)
       }
       __syncwarp();
 #pragma unroll
-      for (int h = 0; h < NC; ++h) c[h] = __dadd_rn(c[h], act[h] ? uj[h] : -0.0);  // miss pull
-      const double* lp[NC];
-#pragma unroll
-      for (int h = 0; h < NC; ++h) lp[h] = act[h] ? buf : zeros;
-      // pushes, owners ascending, in blocks of 8 entries; entries past the
-      // last owner hold -0.0
-      const int nblk = (pmax + 7) >> 3;
+      for (int h = 0; h < NC; ++h)
+        if (act[h]) c[h] = __dadd_rn(c[h], uj[h]);  // miss pull
+      // pushes, owners ascending: every lane of a group reads the same list
+      // (one broadcast 16-byte load feeds two adds of each of its cells) and
+      // a cell holding the latest copy skips the add; blocks of 8 entries,
+      // then pairs; entries past the last owner hold -0.0
+      int q = 0;
 #pragma unroll 1
-      for (int bk = 0; bk < nblk; ++bk) {
-        double2 v2[NC][4];
+      for (; q + 8 <= pmax; q += 8) {
+        double2 v2[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v2[e] = *reinterpret_cast<const double2*>(buf + q + 2 * e);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+#pragma unroll
+          for (int h = 0; h < NC; ++h)
+            if (act[h]) {
+              c[h] = __dadd_rn(c[h], v2[e].x);
+              c[h] = __dadd_rn(c[h], v2[e].y);
+            }
+      }
+#pragma unroll 1
+      for (; q < pmax; q += 2) {
+        const double2 v2 = *reinterpret_cast<const double2*>(buf + q);
 #pragma unroll
         for (int h = 0; h < NC; ++h)
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            v2[h][q] = *reinterpret_cast<const double2*>(lp[h] + 8 * bk + 2 * q);
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-#pragma unroll
-          for (int h = 0; h < NC; ++h) {
-            c[h] = __dadd_rn(c[h], v2[h][q].x);
-            c[h] = __dadd_rn(c[h], v2[h][q].y);
+          if (act[h]) {
+            c[h] = __dadd_rn(c[h], v2.x);
+            c[h] = __dadd_rn(c[h], v2.y);
           }
       }
     }
@@ -568,6 +572,10 @@ void launch_cost_build(const uint32_t* ids, const uint64_t* offsets, uint64_t ro
     const int np = n <= 2 ? 2 : n <= 4 ? 4 : n <= 8 ? 8 : n <= 16 ? 16 : n <= 32 ? 32 : 64;
     const uint64_t rows_per_block = static_cast<uint64_t>(kWarpRowsThreads / 32) * (np >= 32 ? 1 : 32 / np);
     const unsigned blocks = static_cast<unsigned>((rows + rows_per_block - 1) / rows_per_block);
+    static const bool wide_pref = [] {  // EDX_K1_WIDE=1: the lockstep wide kernel (A/B)
+      const char* e = std::getenv("EDX_K1_WIDE");
+      return e && std::strcmp(e, "1") == 0;
+    }();
     auto go = [&](auto kern) {
       kern<<<blocks, kWarpRowsThreads, 0, s>>>(ids, offsets, rows, n, ol, id_space, ucost, matrix,
                                                gap_keys, row_index, flags);
@@ -576,8 +584,14 @@ void launch_cost_build(const uint32_t* ids, const uint64_t* offsets, uint64_t ro
       case 2: go(k_cost_build_warp<2>); g_kernel_name[kKBuild] = "k_cost_build_warp<2>"; break;
       case 4: go(k_cost_build_warp<4>); g_kernel_name[kKBuild] = "k_cost_build_warp<4>"; break;
       case 8: go(k_cost_build_warp<8>); g_kernel_name[kKBuild] = "k_cost_build_warp<8>"; break;
-      case 16: go(k_cost_build_wide<16>); g_kernel_name[kKBuild] = "k_cost_build_wide<16>"; break;
-      case 32: go(k_cost_build_wide<32>); g_kernel_name[kKBuild] = "k_cost_build_wide<32>"; break;
+      case 16:
+        if (wide_pref) { go(k_cost_build_wide<16>); g_kernel_name[kKBuild] = "k_cost_build_wide<16>"; }
+        else { go(k_cost_build_wide64<16>); g_kernel_name[kKBuild] = "k_cost_build_wide64<16>"; }
+        break;
+      case 32:
+        if (wide_pref) { go(k_cost_build_wide<32>); g_kernel_name[kKBuild] = "k_cost_build_wide<32>"; }
+        else { go(k_cost_build_wide64<32>); g_kernel_name[kKBuild] = "k_cost_build_wide64<32>"; }
+        break;
       default: go(k_cost_build_wide64<64>); g_kernel_name[kKBuild] = "k_cost_build_wide64<64>"; break;
     }
     EDX_LAUNCHED();
