@@ -15,8 +15,6 @@
 // threads of one row hit the same address (a broadcast), so each id costs
 // one L1/L2 transaction per row.  Loads are batched 4 ids ahead of the add
 // chain to keep memory-level parallelism despite the serial adds.
-#include <cstdlib>
-#include <cstring>
 #include <type_traits>
 
 #include "edx_internal.cuh"
@@ -280,7 +278,7 @@ __global__ void __launch_bounds__(kWarpRowsThreads)
   }
 }
 
-// K1 for wide rows (16 < NP <= 32 lanes per row; issue-bound at scale): the
+// K1 for 16 workers (NP = 16, two rows per warp): the
 // same row layout, loads and list expansion, one id at a time -- list, one
 // __syncwarp, then the chain with every lane reading the same list (a
 // single broadcast per load) and the adds taken only by the lanes whose
@@ -381,8 +379,9 @@ __global__ void __launch_bounds__(kWarpRowsThreads)
   }
 }
 
-// K1 for 32 < n <= 64 (NP = 64): one row per warp, two cells per lane
-// (workers j and j + 32: two independent chains over the same lists).  A group of G = min(NP, 32) lanes
+// K1 for 16 < n <= 64 (NP = 32: one row per warp; NP = 64: one row per warp,
+// two cells per lane -- workers j and j + 32, two independent chains over the
+// same lists).  A group of G = min(NP, 32) lanes
 // loads G consecutive ids of its row (one per lane) and their masks; a ballot
 // then drops every id whose latest copy is on all n workers (no cell adds
 // anything: at steady state the hot ids -- 43% of occurrences at C4) and the
@@ -572,10 +571,6 @@ void launch_cost_build(const uint32_t* ids, const uint64_t* offsets, uint64_t ro
     const int np = n <= 2 ? 2 : n <= 4 ? 4 : n <= 8 ? 8 : n <= 16 ? 16 : n <= 32 ? 32 : 64;
     const uint64_t rows_per_block = static_cast<uint64_t>(kWarpRowsThreads / 32) * (np >= 32 ? 1 : 32 / np);
     const unsigned blocks = static_cast<unsigned>((rows + rows_per_block - 1) / rows_per_block);
-    static const bool wide_pref = [] {  // EDX_K1_WIDE=1: the lockstep wide kernel (A/B)
-      const char* e = std::getenv("EDX_K1_WIDE");
-      return e && std::strcmp(e, "1") == 0;
-    }();
     auto go = [&](auto kern) {
       kern<<<blocks, kWarpRowsThreads, 0, s>>>(ids, offsets, rows, n, ol, id_space, ucost, matrix,
                                                gap_keys, row_index, flags);
@@ -584,14 +579,10 @@ void launch_cost_build(const uint32_t* ids, const uint64_t* offsets, uint64_t ro
       case 2: go(k_cost_build_warp<2>); g_kernel_name[kKBuild] = "k_cost_build_warp<2>"; break;
       case 4: go(k_cost_build_warp<4>); g_kernel_name[kKBuild] = "k_cost_build_warp<4>"; break;
       case 8: go(k_cost_build_warp<8>); g_kernel_name[kKBuild] = "k_cost_build_warp<8>"; break;
-      case 16:
-        if (wide_pref) { go(k_cost_build_wide<16>); g_kernel_name[kKBuild] = "k_cost_build_wide<16>"; }
-        else { go(k_cost_build_wide64<16>); g_kernel_name[kKBuild] = "k_cost_build_wide64<16>"; }
-        break;
-      case 32:
-        if (wide_pref) { go(k_cost_build_wide<32>); g_kernel_name[kKBuild] = "k_cost_build_wide<32>"; }
-        else { go(k_cost_build_wide64<32>); g_kernel_name[kKBuild] = "k_cost_build_wide64<32>"; }
-        break;
+      // 16 workers: lockstep over every id (C3: 1.7 us faster than the skip
+      // kernel at 8,192 rows); above: all-latest ids skipped by ballot
+      case 16: go(k_cost_build_wide<16>); g_kernel_name[kKBuild] = "k_cost_build_wide<16>"; break;
+      case 32: go(k_cost_build_wide64<32>); g_kernel_name[kKBuild] = "k_cost_build_wide64<32>"; break;
       default: go(k_cost_build_wide64<64>); g_kernel_name[kKBuild] = "k_cost_build_wide64<64>"; break;
     }
     EDX_LAUNCHED();

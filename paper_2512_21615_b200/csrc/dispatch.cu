@@ -58,11 +58,14 @@ __device__ __forceinline__ bool pref_less(double ca, int ia, double cb, int ib) 
 __global__ void k_greedy_prefs(const double* __restrict__ matrix, int n,
                                const uint32_t* __restrict__ order, uint64_t n_order,
                                const int32_t* __restrict__ capacity_dev, int cap_uniform,
-                               uint8_t* __restrict__ prefs) {
+                               const uint32_t* __restrict__ row_ids, uint8_t* __restrict__ prefs,
+                               uint32_t* __restrict__ dest) {
   const uint64_t t = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (t >= n_order) return;  // warp-uniform
-  const double* r = matrix + static_cast<uint64_t>(order[t]) * n;
+  const uint32_t row = order[t];
+  if (lane == 0) dest[t] = row_ids ? row_ids[row] : row;
+  const double* r = matrix + static_cast<uint64_t>(row) * n;
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
   double c[2];
   int id[2];
@@ -112,21 +115,50 @@ __global__ void k_greedy_prefs(const double* __restrict__ matrix, int n,
 
 constexpr int kGreedyThreads = 1024;
 constexpr int kGreedyWarps = kGreedyThreads / 32;
+constexpr int kGreedySlots = 3;  // staged chunks of kGreedyThreads positions
+constexpr size_t kGreedySmem =
+    static_cast<size_t>(kGreedySlots) * kGreedyThreads * (kListBytes + sizeof(uint32_t));
 
+// One CTA walks the positions in rounds of up to 1024.  Positions are staged
+// in shared memory by 1D bulk copies (TMA) three chunks of 1024 deep -- each
+// position's preference list and its decision index -- so a round reads no
+// global memory: the copies of chunks c + 1, c + 2 are in flight while chunk
+// c is consumed, and a round that starts mid-chunk finds the next one ready.
 __global__ void __launch_bounds__(kGreedyThreads)
-    k_greedy(const double* __restrict__ matrix, int n, const uint32_t* __restrict__ order,
-             uint64_t n_order, const int32_t* __restrict__ capacity_dev, int cap_uniform,
-             int32_t* __restrict__ decision, const uint32_t* __restrict__ row_ids,
-             int32_t* __restrict__ pair_worker, int* __restrict__ flags,
-             const uint8_t* __restrict__ prefs) {
+    k_greedy(int n, uint64_t n_order, const int32_t* __restrict__ capacity_dev, int cap_uniform,
+             int32_t* __restrict__ decision, int32_t* __restrict__ pair_worker,
+             int* __restrict__ flags, const uint8_t* __restrict__ prefs,
+             const uint32_t* __restrict__ dest) {
+  extern __shared__ __align__(128) uint8_t gsm[];
+  uint8_t* const plist = gsm;  // [slot][position][kListBytes]
+  uint32_t* const pdest = reinterpret_cast<uint32_t*>(gsm + static_cast<size_t>(kGreedySlots) *
+                                                                kGreedyThreads * kListBytes);
   __shared__ int remaining[kMaxWorkers];
   __shared__ int used[kMaxWorkers];
   __shared__ int cnt[kGreedyWarps][kMaxWorkers + 1];  // +1: a column read is conflict-free
   __shared__ unsigned long long open_mask;
   __shared__ int qmin;
+  __shared__ __align__(8) uint64_t bars[kGreedySlots];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t nch = (n_order + kGreedyThreads - 1) / kGreedyThreads;
+  auto stage = [&](uint64_t c) {  // thread 0: chunk c -> slot c % kGreedySlots
+    const int sl = static_cast<int>(c % kGreedySlots);
+    const uint64_t p0 = c * kGreedyThreads;
+    const uint64_t cntp = n_order - p0 < kGreedyThreads ? n_order - p0 : kGreedyThreads;
+    const unsigned lb = static_cast<unsigned>(cntp * kListBytes);
+    const unsigned db = static_cast<unsigned>(((cntp + 3) & ~uint64_t(3)) * sizeof(uint32_t));
+    mbar_expect_tx(&bars[sl], lb + db);
+    bulk_g2s(plist + static_cast<size_t>(sl) * kGreedyThreads * kListBytes, prefs + p0 * kListBytes,
+             lb, &bars[sl]);
+    bulk_g2s(pdest + static_cast<size_t>(sl) * kGreedyThreads, dest + p0, db, &bars[sl]);
+  };
   if (tid < n) remaining[tid] = capacity_dev ? capacity_dev[tid] : cap_uniform;
+  if (tid == 0) {
+    for (int q = 0; q < kGreedySlots; ++q) mbar_init(&bars[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (uint64_t c = 0; c < nch && c < kGreedySlots; ++c) stage(c);
+  }
   __syncthreads();
   if (tid == 0) {
     unsigned long long om = 0;
@@ -134,26 +166,33 @@ __global__ void __launch_bounds__(kGreedyThreads)
       if (remaining[w] > 0) om |= 1ULL << w;
     open_mask = om;
   }
-  __syncthreads();
 
   uint64_t start = 0;
+  uint64_t ready = 0;  // chunks [0, ready) are known to have landed
   while (start < n_order) {
     for (int x = tid; x < kGreedyWarps * (kMaxWorkers + 1); x += kGreedyThreads)
       (&cnt[0][0])[x] = 0;
     if (tid < kMaxWorkers) used[tid] = 0;
     if (tid == 0) qmin = kGreedyThreads;
+    // this round covers chunks start / 1024 and (unless aligned) the next
+    const uint64_t cl = (start + kGreedyThreads - 1) / kGreedyThreads;
+    const uint64_t need = (cl + 1 < nch ? cl + 1 : nch);
+    for (; ready < need; ++ready)
+      mbar_wait(&bars[ready % kGreedySlots], static_cast<unsigned>((ready / kGreedySlots) & 1));
     __syncthreads();
 
     const uint64_t t = start + tid;
     const bool valid = t < n_order;
     int choice = -1;
-    uint32_t row = 0;
+    uint32_t dst = 0;
     if (valid) {
-      row = order[t];
+      const int sl = static_cast<int>((t / kGreedyThreads) % kGreedySlots);
+      const size_t off = static_cast<size_t>(sl) * kGreedyThreads + (t % kGreedyThreads);
+      dst = pdest[off];
       const unsigned long long om = open_mask;
       // the first still-open worker of the position's preference list is its
       // argmin over the open set: every worker ranked before it is closed
-      const uint4* lst = reinterpret_cast<const uint4*>(prefs + t * kListBytes);
+      const uint4* lst = reinterpret_cast<const uint4*>(plist + off * kListBytes);
       const int nv = (n + 15) >> 4;
       for (int q = 0; q < nv && choice < 0; ++q) {
         const uint4 v4 = lst[q];
@@ -194,7 +233,7 @@ __global__ void __launch_bounds__(kGreedyThreads)
     const int limit = qmin;
     if (valid && choice >= 0 && tid < limit) {
       atomicAdd(&used[choice], 1);
-      if (decision) decision[row_ids ? row_ids[row] : row] = choice;
+      if (decision) decision[dst] = choice;
       if (pair_worker) pair_worker[t] = choice;
     }
     __syncthreads();
@@ -202,8 +241,18 @@ __global__ void __launch_bounds__(kGreedyThreads)
       remaining[tid] -= used[tid];
       if (remaining[tid] <= 0) atomicAnd(&open_mask, ~(1ULL << tid));
     }
-    start += static_cast<uint64_t>(limit);
+    const uint64_t next = start + static_cast<uint64_t>(limit);
+    // chunks wholly before `next` are consumed: their slots take the chunks
+    // kGreedySlots further on (every thread's reads of them precede the
+    // barrier below; the proxy fence orders them before the bulk writes)
+    const uint64_t c_old = start / kGreedyThreads, c_new = next / kGreedyThreads;
     __syncthreads();
+    if (tid == 0 && c_new > c_old) {
+      fence_proxy_async_smem();
+      for (uint64_t c = c_old; c < c_new; ++c)
+        if (c + kGreedySlots < nch) stage(c + kGreedySlots);
+    }
+    start = next;
   }
 }
 
@@ -255,11 +304,18 @@ void launch_greedy(const double* matrix, uint64_t rows, int n, const uint32_t* o
   (void)rows;
   if (n_order == 0) return;
   g.prefs.ensure(n_order * kListBytes);
+  g.dest.ensure((n_order + kGreedyThreads - 1) / kGreedyThreads * kGreedyThreads);
   k_greedy_prefs<<<static_cast<unsigned>((n_order * 32 + 255) / 256), 256, 0, s>>>(
-      matrix, n, order, n_order, capacity_dev, cap_uniform, g.prefs.p);
+      matrix, n, order, n_order, capacity_dev, cap_uniform, row_ids, g.prefs.p, g.dest.p);
   g_kernel_name[kKGreedy] = "k_greedy";
-  k_greedy<<<1, kGreedyThreads, 0, s>>>(matrix, n, order, n_order, capacity_dev, cap_uniform,
-                                        decision, row_ids, pair_worker, flags, g.prefs.p);
+  static bool attr = [] {
+    EDX_CUDA(cudaFuncSetAttribute(k_greedy, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kGreedySmem)));
+    return true;
+  }();
+  (void)attr;
+  k_greedy<<<1, kGreedyThreads, kGreedySmem, s>>>(n, n_order, capacity_dev, cap_uniform, decision,
+                                                  pair_worker, flags, g.prefs.p, g.dest.p);
   EDX_LAUNCHED();
 }
 

@@ -17,6 +17,49 @@
 
 namespace edx {
 
+// ---- shared-memory mbarriers and 1D bulk (TMA) copies, CTA scope
+#ifdef __CUDACC__
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+// Arms `bar` for `bytes` of bulk-copy traffic (one arrival of its count).
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes)
+               : "memory");
+}
+// Global -> shared bulk copy completing on `bar` (16-byte aligned, size % 16 == 0).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+      "l"(src), "r"(bytes), "r"(b)
+      : "memory");
+}
+// Orders this thread's earlier generic shared-memory accesses before later async-proxy (bulk copy) writes.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+#endif
+
 // NVTX range for the host-side enqueue of one phase (build, gap sort, exact
 // solve, greedy, step): header-only NVTX v3, a no-op unless a tool (ncu
 // --nvtx, Nsight Systems) is attached.
@@ -175,6 +218,7 @@ void sort_rows_by_gap(SortScratch& sc, const uint64_t* keys_in, const uint32_t* 
 // K4 scratch: each position's preference list (64 bytes)
 struct GreedyScratch {
   DevBuf<uint8_t> prefs;
+  DevBuf<uint32_t> dest;  // per position: its decision index (row_ids[order[t]])
 };
 void launch_greedy(const double* matrix, uint64_t rows, int n, const uint32_t* order,
                    uint64_t n_order, const int32_t* capacity_dev, int cap_uniform,

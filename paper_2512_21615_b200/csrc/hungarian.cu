@@ -816,27 +816,6 @@ __device__ __forceinline__ bool warp_block_sorted(const int32_t* ord, const int6
   return !__any_sync(0xffffffffu, bad);
 }
 
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(a),
-      "r"(parity)
-      : "memory");
-}
-
 // ----------------------------------------- K6 multi-warp kernel (n <= 32)
 // The production solver for n <= 32 (one warp per block for n <= 16, one warp
 // per two blocks above).  Run-batched Dijkstra steps: after the argmin picks
