@@ -192,16 +192,27 @@ __global__ void __launch_bounds__(kGreedyThreads)
       const unsigned long long om = open_mask;
       // the first still-open worker of the position's preference list is its
       // argmin over the open set: every worker ranked before it is closed
+      // (early exit: until workers close, the first entry is the answer)
       const uint4* lst = reinterpret_cast<const uint4*>(plist + off * kListBytes);
       const int nv = (n + 15) >> 4;
-      for (int q = 0; q < nv && choice < 0; ++q) {
+      for (int q = 0; q < nv; ++q) {
         const uint4 v4 = lst[q];
         const uint32_t wd[4] = {v4.x, v4.y, v4.z, v4.w};
+        bool stop = false;
 #pragma unroll
         for (int b = 0; b < 16; ++b) {
           const int w = static_cast<int>((wd[b >> 2] >> (8 * (b & 3))) & 0xFFu);
-          if (choice < 0 && w != 0xFF && ((om >> w) & 1ULL)) choice = w;
+          if (w == 0xFF) {  // past the last initially open worker
+            stop = true;
+            break;
+          }
+          if ((om >> w) & 1ULL) {
+            choice = w;
+            stop = true;
+            break;
+          }
         }
+        if (stop) break;
       }
       if (choice < 0) atomicOr(flags + kFlagUnbalanced, 1);  // "capacities exhausted"
     }
