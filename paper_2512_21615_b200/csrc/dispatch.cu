@@ -119,11 +119,19 @@ constexpr int kGreedySlots = 3;  // staged chunks of kGreedyThreads positions
 constexpr size_t kGreedySmem =
     static_cast<size_t>(kGreedySlots) * kGreedyThreads * (kListBytes + sizeof(uint32_t));
 
-// One CTA walks the positions in rounds of up to 1024.  Positions are staged
-// in shared memory by 1D bulk copies (TMA) three chunks of 1024 deep -- each
-// position's preference list and its decision index -- so a round reads no
-// global memory: the copies of chunks c + 1, c + 2 are in flight while chunk
-// c is consumed, and a round that starts mid-chunk finds the next one ready.
+// One CTA walks the positions in rounds of up to 1024, three barriers each:
+//  A  every position of the round takes the first open worker of its
+//     preference list; per warp and worker, the leader of the positions that
+//     chose it records their count (stamped with the round) and lane mask and
+//     adds the count to the worker's round total;
+//  B  a worker whose total reaches its remaining capacity r cuts the round at
+//     its r-th occurrence (0-based): one warp scans the per-warp counts, the
+//     crossing warp's mask gives the lane; the earliest cut wins;
+//  C  positions before the cut commit; each worker takes its count before
+//     the cut off its capacity and closes at zero.
+// Positions are staged in shared memory by 1D bulk copies (TMA) three chunks
+// of 1024 deep -- each position's preference list and its decision index --
+// so a round reads no global memory.
 __global__ void __launch_bounds__(kGreedyThreads)
     k_greedy(int n, uint64_t n_order, const int32_t* __restrict__ capacity_dev, int cap_uniform,
              int32_t* __restrict__ decision, int32_t* __restrict__ pair_worker,
@@ -134,10 +142,11 @@ __global__ void __launch_bounds__(kGreedyThreads)
   uint32_t* const pdest = reinterpret_cast<uint32_t*>(gsm + static_cast<size_t>(kGreedySlots) *
                                                                 kGreedyThreads * kListBytes);
   __shared__ int remaining[kMaxWorkers];
-  __shared__ int used[kMaxWorkers];
-  __shared__ int cnt[kGreedyWarps][kMaxWorkers + 1];  // +1: a column read is conflict-free
+  __shared__ int total[kMaxWorkers];
+  __shared__ unsigned stamp[kGreedyWarps][kMaxWorkers + 1];  // round << 8 | count
+  __shared__ unsigned lanes[kGreedyWarps][kMaxWorkers + 1];  // which lanes chose the worker
   __shared__ unsigned long long open_mask;
-  __shared__ int qmin;
+  __shared__ int qmin[2];
   __shared__ __align__(8) uint64_t bars[kGreedySlots];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -153,8 +162,14 @@ __global__ void __launch_bounds__(kGreedyThreads)
              lb, &bars[sl]);
     bulk_g2s(pdest + static_cast<size_t>(sl) * kGreedyThreads, dest + p0, db, &bars[sl]);
   };
-  if (tid < n) remaining[tid] = capacity_dev ? capacity_dev[tid] : cap_uniform;
+  if (tid < n) {
+    remaining[tid] = capacity_dev ? capacity_dev[tid] : cap_uniform;
+    total[tid] = 0;
+  }
+  for (int x = tid; x < kGreedyWarps * (kMaxWorkers + 1); x += kGreedyThreads)
+    (&stamp[0][0])[x] = 0xFFFFFFFFu;  // no round
   if (tid == 0) {
+    qmin[0] = qmin[1] = kGreedyThreads;
     for (int q = 0; q < kGreedySlots; ++q) mbar_init(&bars[q], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (uint64_t c = 0; c < nch && c < kGreedySlots; ++c) stage(c);
@@ -169,18 +184,17 @@ __global__ void __launch_bounds__(kGreedyThreads)
 
   uint64_t start = 0;
   uint64_t ready = 0;  // chunks [0, ready) are known to have landed
-  while (start < n_order) {
-    for (int x = tid; x < kGreedyWarps * (kMaxWorkers + 1); x += kGreedyThreads)
-      (&cnt[0][0])[x] = 0;
-    if (tid < kMaxWorkers) used[tid] = 0;
-    if (tid == 0) qmin = kGreedyThreads;
+  for (unsigned round = 0; start < n_order; ++round) {
+    const unsigned rs = (round & 0xFFFFFFu) << 8;
     // this round covers chunks start / 1024 and (unless aligned) the next
     const uint64_t cl = (start + kGreedyThreads - 1) / kGreedyThreads;
     const uint64_t need = (cl + 1 < nch ? cl + 1 : nch);
     for (; ready < need; ++ready)
       mbar_wait(&bars[ready % kGreedySlots], static_cast<unsigned>((ready / kGreedySlots) & 1));
-    __syncthreads();
+    if (tid == 0) qmin[(round + 1) & 1] = kGreedyThreads;  // last read before the previous barrier C
+    __syncthreads();  // open_mask and the staged chunks are visible
 
+    // ---- A
     const uint64_t t = start + tid;
     const bool valid = t < n_order;
     int choice = -1;
@@ -216,41 +230,60 @@ __global__ void __launch_bounds__(kGreedyThreads)
       }
       if (choice < 0) atomicOr(flags + kFlagUnbalanced, 1);  // "capacities exhausted"
     }
-    // rank of this position among earlier same-choice positions of the chunk
     const unsigned peers = __match_any_sync(0xffffffffu, choice);
-    const int rank_in_warp = __popc(peers & ((1u << lane) - 1));
-    if (choice >= 0 && rank_in_warp == 0) cnt[warp][choice] = __popc(peers);
+    if (choice >= 0 && lane == __ffs(peers) - 1) {
+      const int c = __popc(peers);
+      stamp[warp][choice] = rs | static_cast<unsigned>(c);
+      lanes[warp][choice] = peers;
+      atomicAdd(&total[choice], c);
+    }
     __syncthreads();
-    // exclusive scan over warps, per worker: warp x scans workers x and x + 32,
-    // lanes = warps (one shuffle scan instead of a 32-step serial walk)
+
+    // ---- B: cuts of the workers the round would overfill
 #pragma unroll
     for (int h = 0; h < kMaxWorkers / kGreedyWarps; ++h) {
       const int w = warp + h * kGreedyWarps;
-      if (w < n) {  // warp-uniform
-        const int v = cnt[lane][w];
+      if (w < n && total[w] >= remaining[w]) {  // warp-uniform
+        const int k = remaining[w];  // >= 1: only open workers are chosen
+        const unsigned e = stamp[lane][w];
+        const int v = (e & ~0xFFu) == rs ? static_cast<int>(e & 0xFFu) : 0;
         int inc = v;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
           const int y = __shfl_up_sync(0xffffffffu, inc, off);
           if (lane >= off) inc += y;
         }
-        cnt[lane][w] = inc - v;
+        const unsigned cross = __ballot_sync(0xffffffffu, inc - v <= k && k < inc);
+        if (lane == __ffs(cross) - 1) {
+          unsigned m = lanes[lane][w];
+          for (int j = k - (inc - v); j > 0; --j) m &= m - 1;  // drop the earlier occurrences
+          atomicMin(&qmin[round & 1], lane * 32 + __ffs(m) - 1);
+        }
       }
     }
     __syncthreads();
-    if (choice >= 0 && cnt[warp][choice] + rank_in_warp >= remaining[choice])
-      atomicMin(&qmin, tid);
-    __syncthreads();
-    const int limit = qmin;
+
+    // ---- C
+    const int limit = qmin[round & 1];
     if (valid && choice >= 0 && tid < limit) {
-      atomicAdd(&used[choice], 1);
       if (decision) decision[dst] = choice;
       if (pair_worker) pair_worker[t] = choice;
     }
-    __syncthreads();
     if (tid < n) {
-      remaining[tid] -= used[tid];
-      if (remaining[tid] <= 0) atomicAnd(&open_mask, ~(1ULL << tid));
+      int used = total[tid];
+      if (limit < kGreedyThreads && used > 0) {  // occurrences before the cut only
+        const int lw = limit >> 5, ll = limit & 31;
+        used = 0;
+        for (int x = 0; x <= lw && x < kGreedyWarps; ++x) {
+          const unsigned e = stamp[x][tid];
+          if ((e & ~0xFFu) != rs) continue;
+          used += x < lw ? static_cast<int>(e & 0xFFu)
+                         : __popc(lanes[x][tid] & ((1u << ll) - 1u));
+        }
+      }
+      total[tid] = 0;
+      remaining[tid] -= used;
+      if (used > 0 && remaining[tid] <= 0) atomicAnd(&open_mask, ~(1ULL << tid));
     }
     const uint64_t next = start + static_cast<uint64_t>(limit);
     // chunks wholly before `next` are consumed: their slots take the chunks
