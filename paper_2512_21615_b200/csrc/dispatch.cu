@@ -119,19 +119,23 @@ constexpr int kGreedySlots = 3;  // staged chunks of kGreedyThreads positions
 constexpr size_t kGreedySmem =
     static_cast<size_t>(kGreedySlots) * kGreedyThreads * (kListBytes + sizeof(uint32_t));
 
-// One CTA walks the positions in rounds of up to 1024, three barriers each:
-//  A  every position of the round takes the first open worker of its
-//     preference list; per warp and worker, the leader of the positions that
-//     chose it records their count (stamped with the round) and lane mask and
-//     adds the count to the worker's round total;
+// One CTA walks the positions in windows of 1024 (one thread per position),
+// each window in rounds of three barriers until all of it is committed:
+//  A  every pending position whose worker is not (or no longer) open takes
+//     the first open worker of its preference list -- the others keep theirs:
+//     closing a worker that is not a position's minimum does not move it;
+//     per warp and worker, the leader of the pending positions that chose it
+//     records their count (stamped with the round) and lane mask and adds the
+//     count to the worker's round total;
 //  B  a worker whose total reaches its remaining capacity r cuts the round at
-//     its r-th occurrence (0-based): one warp scans the per-warp counts, the
-//     crossing warp's mask gives the lane; the earliest cut wins;
-//  C  positions before the cut commit; each worker takes its count before
-//     the cut off its capacity and closes at zero.
-// Positions are staged in shared memory by 1D bulk copies (TMA) three chunks
-// of 1024 deep -- each position's preference list and its decision index --
-// so a round reads no global memory.
+//     its r-th pending occurrence (0-based): one warp scans the per-warp
+//     counts, the crossing warp's mask gives the lane; the earliest cut wins;
+//  C  pending positions before the cut commit; each worker takes their count
+//     off its capacity and closes at zero; a round without a cut ends the
+//     window.
+// Windows are staged in shared memory by 1D bulk copies (TMA) three deep --
+// each position's preference list and its decision index -- so a round reads
+// no global memory.
 __global__ void __launch_bounds__(kGreedyThreads)
     k_greedy(int n, uint64_t n_order, const int32_t* __restrict__ capacity_dev, int cap_uniform,
              int32_t* __restrict__ decision, int32_t* __restrict__ pair_worker,
@@ -151,7 +155,7 @@ __global__ void __launch_bounds__(kGreedyThreads)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t nch = (n_order + kGreedyThreads - 1) / kGreedyThreads;
-  auto stage = [&](uint64_t c) {  // thread 0: chunk c -> slot c % kGreedySlots
+  auto stage = [&](uint64_t c) {  // thread 0: window c -> slot c % kGreedySlots
     const int sl = static_cast<int>(c % kGreedySlots);
     const uint64_t p0 = c * kGreedyThreads;
     const uint64_t cntp = n_order - p0 < kGreedyThreads ? n_order - p0 : kGreedyThreads;
@@ -182,121 +186,117 @@ __global__ void __launch_bounds__(kGreedyThreads)
     open_mask = om;
   }
 
-  uint64_t start = 0;
-  uint64_t ready = 0;  // chunks [0, ready) are known to have landed
-  for (unsigned round = 0; start < n_order; ++round) {
-    const unsigned rs = (round & 0xFFFFFFu) << 8;
-    // this round covers chunks start / 1024 and (unless aligned) the next
-    const uint64_t cl = (start + kGreedyThreads - 1) / kGreedyThreads;
-    const uint64_t need = (cl + 1 < nch ? cl + 1 : nch);
-    for (; ready < need; ++ready)
-      mbar_wait(&bars[ready % kGreedySlots], static_cast<unsigned>((ready / kGreedySlots) & 1));
-    if (tid == 0) qmin[(round + 1) & 1] = kGreedyThreads;  // last read before the previous barrier C
-    __syncthreads();  // open_mask and the staged chunks are visible
-
-    // ---- A
-    const uint64_t t = start + tid;
+  unsigned round = 0;
+  for (uint64_t c = 0; c < nch; ++c) {
+    const int sl = static_cast<int>(c % kGreedySlots);
+    const uint64_t t = c * kGreedyThreads + tid;
     const bool valid = t < n_order;
+    mbar_wait(&bars[sl], static_cast<unsigned>((c / kGreedySlots) & 1));
+    const size_t off = static_cast<size_t>(sl) * kGreedyThreads + tid;
+    const uint32_t dst = valid ? pdest[off] : 0;
+    const uint4* lst = reinterpret_cast<const uint4*>(plist + off * kListBytes);
     int choice = -1;
-    uint32_t dst = 0;
-    if (valid) {
-      const int sl = static_cast<int>((t / kGreedyThreads) % kGreedySlots);
-      const size_t off = static_cast<size_t>(sl) * kGreedyThreads + (t % kGreedyThreads);
-      dst = pdest[off];
+    int q0 = 0;  // positions of the window before q0 are committed
+    for (;; ++round) {
+      const unsigned rs = (round & 0xFFFFFFu) << 8;
+      __syncthreads();  // open_mask is current; the previous round's reads of qmin are done
+      if (tid == 0) qmin[(round + 1) & 1] = kGreedyThreads;  // the next round's cut
+      // ---- A
+      const bool pending = valid && tid >= q0;
       const unsigned long long om = open_mask;
-      // the first still-open worker of the position's preference list is its
-      // argmin over the open set: every worker ranked before it is closed
-      // (early exit: until workers close, the first entry is the answer)
-      const uint4* lst = reinterpret_cast<const uint4*>(plist + off * kListBytes);
-      const int nv = (n + 15) >> 4;
-      for (int q = 0; q < nv; ++q) {
-        const uint4 v4 = lst[q];
-        const uint32_t wd[4] = {v4.x, v4.y, v4.z, v4.w};
-        bool stop = false;
+      if (pending && (choice < 0 || !((om >> choice) & 1ULL))) {
+        // the first still-open worker of the position's preference list is
+        // its argmin over the open set: every worker ranked before it is closed
+        choice = -1;
+        const int nv = (n + 15) >> 4;
+        for (int q = 0; q < nv; ++q) {
+          const uint4 v4 = lst[q];
+          const uint32_t wd[4] = {v4.x, v4.y, v4.z, v4.w};
+          bool stop = false;
 #pragma unroll
-        for (int b = 0; b < 16; ++b) {
-          const int w = static_cast<int>((wd[b >> 2] >> (8 * (b & 3))) & 0xFFu);
-          if (w == 0xFF) {  // past the last initially open worker
-            stop = true;
-            break;
+          for (int b = 0; b < 16; ++b) {
+            const int w = static_cast<int>((wd[b >> 2] >> (8 * (b & 3))) & 0xFFu);
+            if (w == 0xFF) {  // past the last initially open worker
+              stop = true;
+              break;
+            }
+            if ((om >> w) & 1ULL) {
+              choice = w;
+              stop = true;
+              break;
+            }
           }
-          if ((om >> w) & 1ULL) {
-            choice = w;
-            stop = true;
-            break;
+          if (stop) break;
+        }
+        if (choice < 0) atomicOr(flags + kFlagUnbalanced, 1);  // "capacities exhausted"
+      }
+      const int key = pending ? choice : -1;
+      const unsigned peers = __match_any_sync(0xffffffffu, key);
+      if (key >= 0 && lane == __ffs(peers) - 1) {
+        const int cnt = __popc(peers);
+        stamp[warp][key] = rs | static_cast<unsigned>(cnt);
+        lanes[warp][key] = peers;
+        atomicAdd(&total[key], cnt);
+      }
+      __syncthreads();
+
+      // ---- B: cuts of the workers the round would overfill
+#pragma unroll
+      for (int h = 0; h < kMaxWorkers / kGreedyWarps; ++h) {
+        const int w = warp + h * kGreedyWarps;
+        if (w < n && total[w] >= remaining[w]) {  // warp-uniform
+          const int k = remaining[w];  // >= 1: only open workers are chosen
+          const unsigned e = stamp[lane][w];
+          const int v = (e & ~0xFFu) == rs ? static_cast<int>(e & 0xFFu) : 0;
+          int inc = v;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+          }
+          const unsigned cross = __ballot_sync(0xffffffffu, inc - v <= k && k < inc);
+          if (lane == __ffs(cross) - 1) {
+            unsigned m = lanes[lane][w];
+            for (int j = k - (inc - v); j > 0; --j) m &= m - 1;  // drop the earlier occurrences
+            atomicMin(&qmin[round & 1], lane * 32 + __ffs(m) - 1);
           }
         }
-        if (stop) break;
       }
-      if (choice < 0) atomicOr(flags + kFlagUnbalanced, 1);  // "capacities exhausted"
-    }
-    const unsigned peers = __match_any_sync(0xffffffffu, choice);
-    if (choice >= 0 && lane == __ffs(peers) - 1) {
-      const int c = __popc(peers);
-      stamp[warp][choice] = rs | static_cast<unsigned>(c);
-      lanes[warp][choice] = peers;
-      atomicAdd(&total[choice], c);
-    }
-    __syncthreads();
+      __syncthreads();
 
-    // ---- B: cuts of the workers the round would overfill
-#pragma unroll
-    for (int h = 0; h < kMaxWorkers / kGreedyWarps; ++h) {
-      const int w = warp + h * kGreedyWarps;
-      if (w < n && total[w] >= remaining[w]) {  // warp-uniform
-        const int k = remaining[w];  // >= 1: only open workers are chosen
-        const unsigned e = stamp[lane][w];
-        const int v = (e & ~0xFFu) == rs ? static_cast<int>(e & 0xFFu) : 0;
-        int inc = v;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, inc, off);
-          if (lane >= off) inc += y;
-        }
-        const unsigned cross = __ballot_sync(0xffffffffu, inc - v <= k && k < inc);
-        if (lane == __ffs(cross) - 1) {
-          unsigned m = lanes[lane][w];
-          for (int j = k - (inc - v); j > 0; --j) m &= m - 1;  // drop the earlier occurrences
-          atomicMin(&qmin[round & 1], lane * 32 + __ffs(m) - 1);
-        }
+      // ---- C
+      const int limit = qmin[round & 1];
+      if (pending && choice >= 0 && tid < limit) {
+        if (decision) decision[dst] = choice;
+        if (pair_worker) pair_worker[t] = choice;
       }
-    }
-    __syncthreads();
-
-    // ---- C
-    const int limit = qmin[round & 1];
-    if (valid && choice >= 0 && tid < limit) {
-      if (decision) decision[dst] = choice;
-      if (pair_worker) pair_worker[t] = choice;
-    }
-    if (tid < n) {
-      int used = total[tid];
-      if (limit < kGreedyThreads && used > 0) {  // occurrences before the cut only
-        const int lw = limit >> 5, ll = limit & 31;
-        used = 0;
-        for (int x = 0; x <= lw && x < kGreedyWarps; ++x) {
-          const unsigned e = stamp[x][tid];
-          if ((e & ~0xFFu) != rs) continue;
-          used += x < lw ? static_cast<int>(e & 0xFFu)
-                         : __popc(lanes[x][tid] & ((1u << ll) - 1u));
+      if (tid < n) {
+        int used = total[tid];
+        if (limit < kGreedyThreads && used > 0) {  // pending occurrences before the cut only
+          const int lw = limit >> 5, ll = limit & 31;
+          used = 0;
+          for (int x = 0; x <= lw && x < kGreedyWarps; ++x) {
+            const unsigned e = stamp[x][tid];
+            if ((e & ~0xFFu) != rs) continue;
+            used += x < lw ? static_cast<int>(e & 0xFFu)
+                           : __popc(lanes[x][tid] & ((1u << ll) - 1u));
+          }
         }
+        total[tid] = 0;
+        remaining[tid] -= used;
+        if (used > 0 && remaining[tid] <= 0) atomicAnd(&open_mask, ~(1ULL << tid));
       }
-      total[tid] = 0;
-      remaining[tid] -= used;
-      if (used > 0 && remaining[tid] <= 0) atomicAnd(&open_mask, ~(1ULL << tid));
+      if (limit >= kGreedyThreads) break;  // uniform: the window is committed
+      q0 = limit;
     }
-    const uint64_t next = start + static_cast<uint64_t>(limit);
-    // chunks wholly before `next` are consumed: their slots take the chunks
-    // kGreedySlots further on (every thread's reads of them precede the
-    // barrier below; the proxy fence orders them before the bulk writes)
-    const uint64_t c_old = start / kGreedyThreads, c_new = next / kGreedyThreads;
+    ++round;
+    // every read of this window's slot precedes the barrier at the next
+    // round's start; the slot then takes the window kGreedySlots further on
     __syncthreads();
-    if (tid == 0 && c_new > c_old) {
+    if (tid == 0 && c + kGreedySlots < nch) {
       fence_proxy_async_smem();
-      for (uint64_t c = c_old; c < c_new; ++c)
-        if (c + kGreedySlots < nch) stage(c + kGreedySlots);
+      stage(c + kGreedySlots);
     }
-    start = next;
   }
 }
 
