@@ -231,7 +231,13 @@ __global__ void __launch_bounds__(kGreedyThreads)
         if (choice < 0) atomicOr(flags + kFlagUnbalanced, 1);  // "capacities exhausted"
       }
       const int key = pending ? choice : -1;
-      const unsigned peers = __match_any_sync(0xffffffffu, key);
+      // lanes with the same key: six ballots over its bits (cheaper than match.any)
+      unsigned peers = __ballot_sync(0xffffffffu, key >= 0);
+#pragma unroll
+      for (int bit = 0; bit < 6; ++bit) {
+        const unsigned bm = __ballot_sync(0xffffffffu, (key >> bit) & 1);
+        peers &= ((key >> bit) & 1) ? bm : ~bm;
+      }
       if (key >= 0 && lane == __ffs(peers) - 1) {
         const int cnt = __popc(peers);
         stamp[warp][key] = rs | static_cast<unsigned>(cnt);
