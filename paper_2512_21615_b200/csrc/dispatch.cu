@@ -4,6 +4,9 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
 
 #include "edx_internal.cuh"
 
@@ -140,7 +143,7 @@ __global__ void __launch_bounds__(kGreedyThreads)
     k_greedy(int n, uint64_t n_order, const int32_t* __restrict__ capacity_dev, int cap_uniform,
              int32_t* __restrict__ decision, int32_t* __restrict__ pair_worker,
              int* __restrict__ flags, const uint8_t* __restrict__ prefs,
-             const uint32_t* __restrict__ dest) {
+             const uint32_t* __restrict__ dest, unsigned long long* __restrict__ stats) {
   extern __shared__ __align__(128) uint8_t gsm[];
   uint8_t* const plist = gsm;  // [slot][position][kListBytes]
   uint32_t* const pdest = reinterpret_cast<uint32_t*>(gsm + static_cast<size_t>(kGreedySlots) *
@@ -187,11 +190,29 @@ __global__ void __launch_bounds__(kGreedyThreads)
   }
 
   unsigned round = 0;
+  // stats (EDX_GREEDY_STATS=1): [0] rounds [1] cycles waiting for windows
+  // [2] A [3] B [4] C [5] rescans [6] total
+  // (kept by thread 0 in shared memory: nothing stays live in registers)
+  __shared__ unsigned long long st[8];  // [7]: last lap
+  if (stats && tid == 0) {
+    for (int q = 0; q < 7; ++q) st[q] = 0;
+    st[7] = clock64();
+    st[6] = st[7];
+  }
+  auto lap = [&](int slot) {
+    if (stats && tid == 0) {
+      const unsigned long long now = clock64();
+      st[slot] += now - st[7];
+      st[7] = now;
+    }
+  };
   for (uint64_t c = 0; c < nch; ++c) {
     const int sl = static_cast<int>(c % kGreedySlots);
     const uint64_t t = c * kGreedyThreads + tid;
     const bool valid = t < n_order;
+    lap(4);
     mbar_wait(&bars[sl], static_cast<unsigned>((c / kGreedySlots) & 1));
+    lap(1);
     const size_t off = static_cast<size_t>(sl) * kGreedyThreads + tid;
     const uint32_t dst = valid ? pdest[off] : 0;
     const uint4* lst = reinterpret_cast<const uint4*>(plist + off * kListBytes);
@@ -205,6 +226,7 @@ __global__ void __launch_bounds__(kGreedyThreads)
       const bool pending = valid && tid >= q0;
       const unsigned long long om = open_mask;
       if (pending && (choice < 0 || !((om >> choice) & 1ULL))) {
+        if (stats && choice >= 0) atomicAdd(stats + 5, 1ULL);
         // the first still-open worker of the position's preference list is
         // its argmin over the open set: every worker ranked before it is closed
         choice = -1;
@@ -245,6 +267,7 @@ __global__ void __launch_bounds__(kGreedyThreads)
         atomicAdd(&total[key], cnt);
       }
       __syncthreads();
+      lap(2);
 
       // ---- B: cuts of the workers the round would overfill
 #pragma unroll
@@ -269,6 +292,8 @@ __global__ void __launch_bounds__(kGreedyThreads)
         }
       }
       __syncthreads();
+      lap(3);
+      if (stats && tid == 0) ++st[0];
 
       // ---- C
       const int limit = qmin[round & 1];
@@ -303,6 +328,11 @@ __global__ void __launch_bounds__(kGreedyThreads)
       fence_proxy_async_smem();
       stage(c + kGreedySlots);
     }
+  }
+  if (stats && tid == 0) {
+    st[6] = clock64() - st[6];
+    for (int q = 0; q < 7; ++q)
+      if (q != 5) atomicAdd(stats + q, st[q]);
   }
 }
 
@@ -364,8 +394,26 @@ void launch_greedy(const double* matrix, uint64_t rows, int n, const uint32_t* o
     return true;
   }();
   (void)attr;
+  static const bool want_stats = [] {  // EDX_GREEDY_STATS=1: round counters on stderr (tools)
+    const char* e = std::getenv("EDX_GREEDY_STATS");
+    return e && std::strcmp(e, "1") == 0;
+  }();
+  if (want_stats) {
+    g.stats.ensure(8);
+    EDX_CUDA(cudaMemsetAsync(g.stats.p, 0, 8 * sizeof(unsigned long long), s));
+  }
   k_greedy<<<1, kGreedyThreads, kGreedySmem, s>>>(n, n_order, capacity_dev, cap_uniform, decision,
-                                                  pair_worker, flags, g.prefs.p, g.dest.p);
+                                                  pair_worker, flags, g.prefs.p, g.dest.p,
+                                                  want_stats ? g.stats.p : nullptr);
+  if (want_stats) {
+    unsigned long long h[8];
+    EDX_CUDA(cudaMemcpyAsync(h, g.stats.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    EDX_CUDA(cudaStreamSynchronize(s));
+    std::fprintf(stderr,
+                 "{\"greedy_stats\": {\"positions\": %llu, \"rounds\": %llu, \"wait\": %llu, "
+                 "\"A\": %llu, \"B\": %llu, \"C\": %llu, \"rescans\": %llu, \"total\": %llu}}\n",
+                 static_cast<unsigned long long>(n_order), h[0], h[1], h[2], h[3], h[4], h[5], h[6]);
+  }
   EDX_LAUNCHED();
 }
 
