@@ -193,7 +193,9 @@ __global__ void __launch_bounds__(kGreedyThreads)
   // stats (EDX_GREEDY_STATS=1): [0] rounds [1] cycles waiting for windows
   // [2] A [3] B [4] C [5] rescans [6] total
   // (kept by thread 0 in shared memory: nothing stays live in registers)
-  __shared__ unsigned long long st[8];  // [7]: last lap
+  // [0] rounds [1] top barrier + window wait [2] A until the scans are done
+  // (thread 0) [3] A barrier [4] B [5] C (thread 0) [6] total [7] last lap
+  __shared__ unsigned long long st[8];
   if (stats && tid == 0) {
     for (int q = 0; q < 7; ++q) st[q] = 0;
     st[7] = clock64();
@@ -210,9 +212,7 @@ __global__ void __launch_bounds__(kGreedyThreads)
     const int sl = static_cast<int>(c % kGreedySlots);
     const uint64_t t = c * kGreedyThreads + tid;
     const bool valid = t < n_order;
-    lap(4);
     mbar_wait(&bars[sl], static_cast<unsigned>((c / kGreedySlots) & 1));
-    lap(1);
     const size_t off = static_cast<size_t>(sl) * kGreedyThreads + tid;
     const uint32_t dst = valid ? pdest[off] : 0;
     const uint4* lst = reinterpret_cast<const uint4*>(plist + off * kListBytes);
@@ -221,12 +221,13 @@ __global__ void __launch_bounds__(kGreedyThreads)
     for (;; ++round) {
       const unsigned rs = (round & 0xFFFFFFu) << 8;
       __syncthreads();  // open_mask is current; the previous round's reads of qmin are done
+      lap(1);
       if (tid == 0) qmin[(round + 1) & 1] = kGreedyThreads;  // the next round's cut
       // ---- A
       const bool pending = valid && tid >= q0;
       const unsigned long long om = open_mask;
       if (pending && (choice < 0 || !((om >> choice) & 1ULL))) {
-        if (stats && choice >= 0) atomicAdd(stats + 5, 1ULL);
+        if (stats && choice >= 0) atomicAdd(stats + 8, 1ULL);
         // the first still-open worker of the position's preference list is
         // its argmin over the open set: every worker ranked before it is closed
         choice = -1;
@@ -252,6 +253,7 @@ __global__ void __launch_bounds__(kGreedyThreads)
         }
         if (choice < 0) atomicOr(flags + kFlagUnbalanced, 1);  // "capacities exhausted"
       }
+      lap(2);
       const int key = pending ? choice : -1;
       // lanes with the same key: six ballots over its bits (cheaper than match.any)
       unsigned peers = __ballot_sync(0xffffffffu, key >= 0);
@@ -267,7 +269,7 @@ __global__ void __launch_bounds__(kGreedyThreads)
         atomicAdd(&total[key], cnt);
       }
       __syncthreads();
-      lap(2);
+      lap(3);
 
       // ---- B: cuts of the workers the round would overfill
 #pragma unroll
@@ -292,7 +294,7 @@ __global__ void __launch_bounds__(kGreedyThreads)
         }
       }
       __syncthreads();
-      lap(3);
+      lap(4);
       if (stats && tid == 0) ++st[0];
 
       // ---- C
@@ -317,6 +319,7 @@ __global__ void __launch_bounds__(kGreedyThreads)
         remaining[tid] -= used;
         if (used > 0 && remaining[tid] <= 0) atomicAnd(&open_mask, ~(1ULL << tid));
       }
+      lap(5);
       if (limit >= kGreedyThreads) break;  // uniform: the window is committed
       q0 = limit;
     }
@@ -332,7 +335,7 @@ __global__ void __launch_bounds__(kGreedyThreads)
   if (stats && tid == 0) {
     st[6] = clock64() - st[6];
     for (int q = 0; q < 7; ++q)
-      if (q != 5) atomicAdd(stats + q, st[q]);
+      atomicAdd(stats + q, st[q]);
   }
 }
 
@@ -399,20 +402,22 @@ void launch_greedy(const double* matrix, uint64_t rows, int n, const uint32_t* o
     return e && std::strcmp(e, "1") == 0;
   }();
   if (want_stats) {
-    g.stats.ensure(8);
-    EDX_CUDA(cudaMemsetAsync(g.stats.p, 0, 8 * sizeof(unsigned long long), s));
+    g.stats.ensure(9);
+    EDX_CUDA(cudaMemsetAsync(g.stats.p, 0, 9 * sizeof(unsigned long long), s));
   }
   k_greedy<<<1, kGreedyThreads, kGreedySmem, s>>>(n, n_order, capacity_dev, cap_uniform, decision,
                                                   pair_worker, flags, g.prefs.p, g.dest.p,
                                                   want_stats ? g.stats.p : nullptr);
   if (want_stats) {
-    unsigned long long h[8];
+    unsigned long long h[9];
     EDX_CUDA(cudaMemcpyAsync(h, g.stats.p, sizeof(h), cudaMemcpyDeviceToHost, s));
     EDX_CUDA(cudaStreamSynchronize(s));
     std::fprintf(stderr,
-                 "{\"greedy_stats\": {\"positions\": %llu, \"rounds\": %llu, \"wait\": %llu, "
-                 "\"A\": %llu, \"B\": %llu, \"C\": %llu, \"rescans\": %llu, \"total\": %llu}}\n",
-                 static_cast<unsigned long long>(n_order), h[0], h[1], h[2], h[3], h[4], h[5], h[6]);
+                 "{\"greedy_stats\": {\"positions\": %llu, \"rounds\": %llu, \"top\": %llu, "
+                 "\"A_scan0\": %llu, \"A_bar\": %llu, \"B\": %llu, \"C0\": %llu, \"total\": %llu, "
+                 "\"rescans\": %llu}}\n",
+                 static_cast<unsigned long long>(n_order), h[0], h[1], h[2], h[3], h[4], h[5], h[6],
+                 h[8]);
   }
   EDX_LAUNCHED();
 }
