@@ -286,11 +286,9 @@ __global__ void __launch_bounds__(kGreedyThreads)
             if (lane >= o) inc += y;
           }
           const unsigned cross = __ballot_sync(0xffffffffu, inc - v <= k && k < inc);
-          if (lane == __ffs(cross) - 1) {
-            unsigned m = lanes[lane][w];
-            for (int j = k - (inc - v); j > 0; --j) m &= m - 1;  // drop the earlier occurrences
-            atomicMin(&qmin[round & 1], lane * 32 + __ffs(m) - 1);
-          }
+          if (lane == __ffs(cross) - 1)  // the (k - excl)-th (0-based) lane of the crossing warp
+            atomicMin(&qmin[round & 1],
+                      lane * 32 + static_cast<int>(__fns(lanes[lane][w], 0, k - (inc - v) + 1)));
         }
       }
       __syncthreads();
@@ -303,21 +301,30 @@ __global__ void __launch_bounds__(kGreedyThreads)
         if (decision) decision[dst] = choice;
         if (pair_worker) pair_worker[t] = choice;
       }
-      if (tid < n) {
-        int used = total[tid];
-        if (limit < kGreedyThreads && used > 0) {  // pending occurrences before the cut only
-          const int lw = limit >> 5, ll = limit & 31;
-          used = 0;
-          for (int x = 0; x <= lw && x < kGreedyWarps; ++x) {
-            const unsigned e = stamp[x][tid];
-            if ((e & ~0xFFu) != rs) continue;
-            used += x < lw ? static_cast<int>(e & 0xFFu)
-                           : __popc(lanes[x][tid] & ((1u << ll) - 1u));
+      // capacities: a worker's pending occurrences before the cut -- all of
+      // them without a cut, else a warp per worker sums the per-warp counts
+      // (lanes = warps) of the warps before the cut's and its lanes below it
+#pragma unroll
+      for (int h = 0; h < kMaxWorkers / kGreedyWarps; ++h) {
+        const int w = warp + h * kGreedyWarps;
+        if (w < n) {  // warp-uniform
+          int used = total[w];
+          if (limit < kGreedyThreads && used > 0) {  // warp-uniform
+            const int lw = limit >> 5, ll = limit & 31;
+            const unsigned e = stamp[lane][w];
+            int v = 0;
+            if ((e & ~0xFFu) == rs)
+              v = lane < lw ? static_cast<int>(e & 0xFFu)
+                            : (lane == lw ? __popc(lanes[lane][w] & ((1u << ll) - 1u)) : 0);
+            used = static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(v)));
+          }
+          if (lane == 0) {
+            total[w] = 0;
+            const int rem = remaining[w] - used;
+            remaining[w] = rem;
+            if (used > 0 && rem <= 0) atomicAnd(&open_mask, ~(1ULL << w));
           }
         }
-        total[tid] = 0;
-        remaining[tid] -= used;
-        if (used > 0 && remaining[tid] <= 0) atomicAnd(&open_mask, ~(1ULL << tid));
       }
       lap(5);
       if (limit >= kGreedyThreads) break;  // uniform: the window is committed
