@@ -119,8 +119,7 @@ __global__ void k_greedy_prefs(const double* __restrict__ matrix, int n,
 constexpr int kGreedyThreads = 1024;
 constexpr int kGreedyWarps = kGreedyThreads / 32;
 constexpr int kGreedySlots = 3;  // staged chunks of kGreedyThreads positions
-constexpr size_t kGreedySmem =
-    static_cast<size_t>(kGreedySlots) * kGreedyThreads * (kListBytes + sizeof(uint32_t));
+constexpr size_t kGreedySmem = static_cast<size_t>(kGreedySlots) * kGreedyThreads * kListBytes;
 
 // One CTA walks the positions in windows of 1024 (one thread per position),
 // each window in rounds of three barriers until all of it is committed:
@@ -136,18 +135,15 @@ constexpr size_t kGreedySmem =
 //  C  pending positions before the cut commit; each worker takes their count
 //     off its capacity and closes at zero; a round without a cut ends the
 //     window.
-// Windows are staged in shared memory by 1D bulk copies (TMA) three deep --
-// each position's preference list and its decision index -- so a round reads
-// no global memory.
+// Windows' preference lists are staged in shared memory by 1D bulk copies
+// (TMA) three deep, so a round reads no global memory; choices are written in
+// position order (coalesced) and scattered to the decision by k_greedy_scatter.
 __global__ void __launch_bounds__(kGreedyThreads)
     k_greedy(int n, uint64_t n_order, const int32_t* __restrict__ capacity_dev, int cap_uniform,
-             int32_t* __restrict__ decision, int32_t* __restrict__ pair_worker,
-             int* __restrict__ flags, const uint8_t* __restrict__ prefs,
-             const uint32_t* __restrict__ dest, unsigned long long* __restrict__ stats) {
+             int32_t* __restrict__ pair_worker, int* __restrict__ flags,
+             const uint8_t* __restrict__ prefs, unsigned long long* __restrict__ stats) {
   extern __shared__ __align__(128) uint8_t gsm[];
   uint8_t* const plist = gsm;  // [slot][position][kListBytes]
-  uint32_t* const pdest = reinterpret_cast<uint32_t*>(gsm + static_cast<size_t>(kGreedySlots) *
-                                                                kGreedyThreads * kListBytes);
   __shared__ int remaining[kMaxWorkers];
   __shared__ int total[kMaxWorkers];
   __shared__ unsigned stamp[kGreedyWarps][kMaxWorkers + 1];  // round << 8 | count
@@ -163,11 +159,9 @@ __global__ void __launch_bounds__(kGreedyThreads)
     const uint64_t p0 = c * kGreedyThreads;
     const uint64_t cntp = n_order - p0 < kGreedyThreads ? n_order - p0 : kGreedyThreads;
     const unsigned lb = static_cast<unsigned>(cntp * kListBytes);
-    const unsigned db = static_cast<unsigned>(((cntp + 3) & ~uint64_t(3)) * sizeof(uint32_t));
-    mbar_expect_tx(&bars[sl], lb + db);
+    mbar_expect_tx(&bars[sl], lb);
     bulk_g2s(plist + static_cast<size_t>(sl) * kGreedyThreads * kListBytes, prefs + p0 * kListBytes,
              lb, &bars[sl]);
-    bulk_g2s(pdest + static_cast<size_t>(sl) * kGreedyThreads, dest + p0, db, &bars[sl]);
   };
   if (tid < n) {
     remaining[tid] = capacity_dev ? capacity_dev[tid] : cap_uniform;
@@ -214,7 +208,6 @@ __global__ void __launch_bounds__(kGreedyThreads)
     const bool valid = t < n_order;
     mbar_wait(&bars[sl], static_cast<unsigned>((c / kGreedySlots) & 1));
     const size_t off = static_cast<size_t>(sl) * kGreedyThreads + tid;
-    const uint32_t dst = valid ? pdest[off] : 0;
     const uint4* lst = reinterpret_cast<const uint4*>(plist + off * kListBytes);
     int choice = -1;
     int q0 = 0;  // positions of the window before q0 are committed
@@ -297,10 +290,8 @@ __global__ void __launch_bounds__(kGreedyThreads)
 
       // ---- C
       const int limit = qmin[round & 1];
-      if (pending && choice >= 0 && tid < limit) {
-        if (decision) decision[dst] = choice;
-        if (pair_worker) pair_worker[t] = choice;
-      }
+      // in position order (coalesced); the scatter to rows is a separate grid
+      if (pending && choice >= 0 && tid < limit) pair_worker[t] = choice;
       // capacities: a worker's pending occurrences before the cut -- all of
       // them without a cut, else a warp per worker sums the per-warp counts
       // (lanes = warps) of the warps before the cut's and its lanes below it
@@ -344,6 +335,14 @@ __global__ void __launch_bounds__(kGreedyThreads)
     for (int q = 0; q < 7; ++q)
       atomicAdd(stats + q, st[q]);
   }
+}
+
+// decision[dest[t]] = pair_worker[t]: the greedy's choices, from position
+// order to rows (a position left without a worker raised kFlagUnbalanced).
+__global__ void k_greedy_scatter(const int32_t* __restrict__ pw, const uint32_t* __restrict__ dest,
+                                 uint64_t n_order, int32_t* __restrict__ decision) {
+  const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (t < n_order && pw[t] >= 0) decision[dest[t]] = pw[t];
 }
 
 __global__ void k_check_balance(const int32_t* __restrict__ decision, uint64_t rows, int n,
@@ -394,7 +393,14 @@ void launch_greedy(const double* matrix, uint64_t rows, int n, const uint32_t* o
   (void)rows;
   if (n_order == 0) return;
   g.prefs.ensure(n_order * kListBytes);
-  g.dest.ensure((n_order + kGreedyThreads - 1) / kGreedyThreads * kGreedyThreads);
+  g.dest.ensure(n_order);
+  int32_t* pw = pair_worker;
+  if (!pw) {
+    g.pw.ensure(n_order);
+    pw = g.pw.p;
+  }
+  if (decision)  // positions left without a worker keep -1 (and raise kFlagUnbalanced)
+    EDX_CUDA(cudaMemsetAsync(pw, 0xFF, n_order * sizeof(int32_t), s));
   k_greedy_prefs<<<static_cast<unsigned>((n_order * 32 + 255) / 256), 256, 0, s>>>(
       matrix, n, order, n_order, capacity_dev, cap_uniform, row_ids, g.prefs.p, g.dest.p);
   g_kernel_name[kKGreedy] = "k_greedy";
@@ -412,9 +418,11 @@ void launch_greedy(const double* matrix, uint64_t rows, int n, const uint32_t* o
     g.stats.ensure(9);
     EDX_CUDA(cudaMemsetAsync(g.stats.p, 0, 9 * sizeof(unsigned long long), s));
   }
-  k_greedy<<<1, kGreedyThreads, kGreedySmem, s>>>(n, n_order, capacity_dev, cap_uniform, decision,
-                                                  pair_worker, flags, g.prefs.p, g.dest.p,
-                                                  want_stats ? g.stats.p : nullptr);
+  k_greedy<<<1, kGreedyThreads, kGreedySmem, s>>>(n, n_order, capacity_dev, cap_uniform, pw, flags,
+                                                  g.prefs.p, want_stats ? g.stats.p : nullptr);
+  if (decision)
+    k_greedy_scatter<<<static_cast<unsigned>((n_order + 255) / 256), 256, 0, s>>>(pw, g.dest.p,
+                                                                                 n_order, decision);
   if (want_stats) {
     unsigned long long h[9];
     EDX_CUDA(cudaMemcpyAsync(h, g.stats.p, sizeof(h), cudaMemcpyDeviceToHost, s));

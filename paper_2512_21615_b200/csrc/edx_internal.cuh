@@ -219,6 +219,7 @@ void sort_rows_by_gap(SortScratch& sc, const uint64_t* keys_in, const uint32_t* 
 struct GreedyScratch {
   DevBuf<uint8_t> prefs;
   DevBuf<uint32_t> dest;  // per position: its decision index (row_ids[order[t]])
+  DevBuf<int32_t> pw;     // per position: its worker (when the caller wants rows only)
   DevBuf<unsigned long long> stats;  // EDX_GREEDY_STATS=1 only
 };
 void launch_greedy(const double* matrix, uint64_t rows, int n, const uint32_t* order,
