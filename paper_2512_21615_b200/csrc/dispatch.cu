@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(kGreedyThreads)
     mbar_wait(&bars[sl], static_cast<unsigned>((c / kGreedySlots) & 1));
     const size_t off = static_cast<size_t>(sl) * kGreedyThreads + tid;
     const uint4* lst = reinterpret_cast<const uint4*>(plist + off * kListBytes);
-    int choice = -1;
+    int choice = -1, depth = 0;
     int q0 = 0;  // positions of the window before q0 are committed
     for (;; ++round) {
       const unsigned rs = (round & 0xFFFFFFu) << 8;
@@ -238,6 +238,7 @@ __global__ void __launch_bounds__(kGreedyThreads)
             }
             if ((om >> w) & 1ULL) {
               choice = w;
+              if (stats) depth = q * 16 + b + 1;
               stop = true;
               break;
             }
@@ -245,6 +246,16 @@ __global__ void __launch_bounds__(kGreedyThreads)
           if (stop) break;
         }
         if (choice < 0) atomicOr(flags + kFlagUnbalanced, 1);  // "capacities exhausted"
+      }
+      if (stats) {
+        const unsigned mx = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(depth));
+        const unsigned sm = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(depth));
+        if (lane == 0 && mx) {
+          atomicAdd(stats + 9, static_cast<unsigned long long>(sm));
+          atomicAdd(stats + 10, static_cast<unsigned long long>(mx));
+          atomicAdd(stats + 11, 1ULL);
+        }
+        depth = 0;
       }
       lap(2);
       const int key = pending ? choice : -1;
@@ -415,8 +426,8 @@ void launch_greedy(const double* matrix, uint64_t rows, int n, const uint32_t* o
     return e && std::strcmp(e, "1") == 0;
   }();
   if (want_stats) {
-    g.stats.ensure(9);
-    EDX_CUDA(cudaMemsetAsync(g.stats.p, 0, 9 * sizeof(unsigned long long), s));
+    g.stats.ensure(12);
+    EDX_CUDA(cudaMemsetAsync(g.stats.p, 0, 12 * sizeof(unsigned long long), s));
   }
   k_greedy<<<1, kGreedyThreads, kGreedySmem, s>>>(n, n_order, capacity_dev, cap_uniform, pw, flags,
                                                   g.prefs.p, want_stats ? g.stats.p : nullptr);
@@ -424,15 +435,16 @@ void launch_greedy(const double* matrix, uint64_t rows, int n, const uint32_t* o
     k_greedy_scatter<<<static_cast<unsigned>((n_order + 255) / 256), 256, 0, s>>>(pw, g.dest.p,
                                                                                  n_order, decision);
   if (want_stats) {
-    unsigned long long h[9];
+    unsigned long long h[12];
     EDX_CUDA(cudaMemcpyAsync(h, g.stats.p, sizeof(h), cudaMemcpyDeviceToHost, s));
     EDX_CUDA(cudaStreamSynchronize(s));
     std::fprintf(stderr,
                  "{\"greedy_stats\": {\"positions\": %llu, \"rounds\": %llu, \"top\": %llu, "
                  "\"A_scan0\": %llu, \"A_bar\": %llu, \"B\": %llu, \"C0\": %llu, \"total\": %llu, "
-                 "\"rescans\": %llu}}\n",
+                 "\"rescans\": %llu, \"scan_entries\": %llu, \"warp_max_entries\": %llu, "
+                 "\"warp_scans\": %llu}}\n",
                  static_cast<unsigned long long>(n_order), h[0], h[1], h[2], h[3], h[4], h[5], h[6],
-                 h[8]);
+                 h[8], h[9], h[10], h[11]);
   }
   EDX_LAUNCHED();
 }
