@@ -359,40 +359,76 @@ __global__ void k_greedy_scatter(const int32_t* __restrict__ pw, const uint32_t*
 __global__ void k_check_balance(const int32_t* __restrict__ decision, uint64_t rows, int n,
                                 int m, int* __restrict__ flags) {
   __shared__ int load[kMaxWorkers];
+  const int lane = threadIdx.x & 31;
   if (threadIdx.x < kMaxWorkers) load[threadIdx.x] = 0;
   __syncthreads();
-  for (uint64_t i = threadIdx.x; i < rows; i += blockDim.x) {
-    const int w = decision[i];
-    if (w < 0 || w >= n) atomicOr(flags + kFlagUnbalanced, 1);
-    else atomicAdd(&load[w], 1);
+  // warp-aggregated: the lanes holding the same worker (six ballots over its
+  // bits) add their count once
+  for (uint64_t b = threadIdx.x - lane; b < rows; b += blockDim.x) {
+    const uint64_t i = b + lane;
+    int w = i < rows ? decision[i] : -2;
+    if (i < rows && (w < 0 || w >= n)) {
+      atomicOr(flags + kFlagUnbalanced, 1);
+      w = -2;
+    }
+    const int key = w >= 0 ? w : 0x7F;  // 0x7F: no worker
+    unsigned peers = 0xffffffffu;
+#pragma unroll
+    for (int bit = 0; bit < 7; ++bit) {
+      const unsigned bm = __ballot_sync(0xffffffffu, (key >> bit) & 1);
+      peers &= ((key >> bit) & 1) ? bm : ~bm;
+    }
+    if (key != 0x7F && lane == __ffs(peers) - 1) atomicAdd(&load[key], __popc(peers));
   }
   __syncthreads();
   if (threadIdx.x < n && load[threadIdx.x] != m) atomicOr(flags + kFlagUnbalanced, 1);
 }
 
 // decision_cost (assign.hpp:288-298): a left-to-right fp64 sum in sample
-// order.  The order is part of the result, so one thread adds; the gather of
-// C[i, w_i] (the latency) is done by the whole block into shared memory
-// first, chunk by chunk.
-constexpr int kCostThreads = 1024, kCostChunk = 4096;
+// order.  The order is part of the result, so one thread adds (a chain of
+// dependent DADDs, ~8 cycles each); the other warps gather the next chunk of
+// C[i, w_i] into the second buffer meanwhile.
+constexpr int kCostThreads = 1024, kCostChunk = 2048;
 
 __global__ void __launch_bounds__(kCostThreads)
     k_decision_cost(const double* __restrict__ matrix, const int32_t* __restrict__ decision,
                     uint64_t rows, int n, double* __restrict__ out) {
-  __shared__ double vals[kCostChunk];
-  double total = 0.0;
-  for (uint64_t base = 0; base < rows; base += kCostChunk) {
+  __shared__ __align__(16) double vals[2][kCostChunk];
+  const int tid = threadIdx.x;
+  auto gather = [&](uint64_t base, double* dst, int first, int stride) {
     const int cnt = rows - base < kCostChunk ? static_cast<int>(rows - base) : kCostChunk;
-    for (int t = threadIdx.x; t < cnt; t += kCostThreads) {
+    for (int t = first; t < cnt; t += stride) {
       const uint64_t i = base + t;
-      vals[t] = matrix[i * n + decision[i]];
+      dst[t] = matrix[i * n + decision[i]];
+    }
+  };
+  double total = 0.0;
+  if (rows > 0) gather(0, vals[0], tid, kCostThreads);
+  __syncthreads();
+  int par = 0;
+  for (uint64_t base = 0; base < rows; base += kCostChunk, par ^= 1) {
+    if (tid >= 32) {
+      if (base + kCostChunk < rows) gather(base + kCostChunk, vals[par ^ 1], tid - 32, kCostThreads - 32);
+    } else if (tid == 0) {
+      const int cnt = rows - base < kCostChunk ? static_cast<int>(rows - base) : kCostChunk;
+      const double2* v2 = reinterpret_cast<const double2*>(vals[par]);
+      int t = 0;
+      for (; t + 8 <= cnt; t += 8) {
+        const double2 a = v2[t / 2], b = v2[t / 2 + 1], c = v2[t / 2 + 2], d = v2[t / 2 + 3];
+        total = __dadd_rn(total, a.x);
+        total = __dadd_rn(total, a.y);
+        total = __dadd_rn(total, b.x);
+        total = __dadd_rn(total, b.y);
+        total = __dadd_rn(total, c.x);
+        total = __dadd_rn(total, c.y);
+        total = __dadd_rn(total, d.x);
+        total = __dadd_rn(total, d.y);
+      }
+      for (; t < cnt; ++t) total = __dadd_rn(total, vals[par][t]);
     }
     __syncthreads();
-    if (threadIdx.x == 0)
-      for (int t = 0; t < cnt; ++t) total = __dadd_rn(total, vals[t]);
-    __syncthreads();
   }
-  if (threadIdx.x == 0) *out = total;
+  if (tid == 0) *out = total;
 }
 
 }  // namespace
