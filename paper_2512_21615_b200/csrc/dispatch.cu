@@ -356,32 +356,35 @@ __global__ void k_greedy_scatter(const int32_t* __restrict__ pw, const uint32_t*
   if (t < n_order && pw[t] >= 0) decision[dest[t]] = pw[t];
 }
 
-__global__ void k_check_balance(const int32_t* __restrict__ decision, uint64_t rows, int n,
-                                int m, int* __restrict__ flags) {
+// DispatchDecision::validate on the device (assign.hpp:41-57): per block a
+// shared histogram, added to the global counts; the last block to finish
+// compares them with m and clears them for the next call.
+constexpr int kBalanceThreads = 256, kBalanceRows = 2048;
+__global__ void __launch_bounds__(kBalanceThreads)
+    k_check_balance(const int32_t* __restrict__ decision, uint64_t rows, int n, int m,
+                    int* __restrict__ flags, int* __restrict__ counts) {
   __shared__ int load[kMaxWorkers];
-  const int lane = threadIdx.x & 31;
+  __shared__ bool last;
   if (threadIdx.x < kMaxWorkers) load[threadIdx.x] = 0;
   __syncthreads();
-  // warp-aggregated: the lanes holding the same worker (six ballots over its
-  // bits) add their count once
-  for (uint64_t b = threadIdx.x - lane; b < rows; b += blockDim.x) {
-    const uint64_t i = b + lane;
-    int w = i < rows ? decision[i] : -2;
-    if (i < rows && (w < 0 || w >= n)) {
-      atomicOr(flags + kFlagUnbalanced, 1);
-      w = -2;
-    }
-    const int key = w >= 0 ? w : 0x7F;  // 0x7F: no worker
-    unsigned peers = 0xffffffffu;
-#pragma unroll
-    for (int bit = 0; bit < 7; ++bit) {
-      const unsigned bm = __ballot_sync(0xffffffffu, (key >> bit) & 1);
-      peers &= ((key >> bit) & 1) ? bm : ~bm;
-    }
-    if (key != 0x7F && lane == __ffs(peers) - 1) atomicAdd(&load[key], __popc(peers));
+  const uint64_t b0 = static_cast<uint64_t>(blockIdx.x) * kBalanceRows;
+  for (uint64_t i = b0 + threadIdx.x; i < rows && i < b0 + kBalanceRows; i += kBalanceThreads) {
+    const int w = decision[i];
+    if (w < 0 || w >= n) atomicOr(flags + kFlagUnbalanced, 1);
+    else atomicAdd(&load[w], 1);
   }
   __syncthreads();
-  if (threadIdx.x < n && load[threadIdx.x] != m) atomicOr(flags + kFlagUnbalanced, 1);
+  if (threadIdx.x < n && load[threadIdx.x]) atomicAdd(&counts[threadIdx.x], load[threadIdx.x]);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&counts[kMaxWorkers], 1) == static_cast<int>(gridDim.x) - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < n) {
+    if (atomicExch(&counts[threadIdx.x], 0) != m) atomicOr(flags + kFlagUnbalanced, 1);
+  }
+  if (threadIdx.x == 0) counts[kMaxWorkers] = 0;
 }
 
 // decision_cost (assign.hpp:288-298): a left-to-right fp64 sum in sample
@@ -486,8 +489,13 @@ void launch_greedy(const double* matrix, uint64_t rows, int n, const uint32_t* o
 }
 
 void launch_check_balance(const int32_t* decision, uint64_t rows, int n, int m, int* flags,
-                          cudaStream_t s) {
-  k_check_balance<<<1, 1024, 0, s>>>(decision, rows, n, m, flags);
+                          DevBuf<int>& counts, cudaStream_t s) {
+  if (counts.n < kMaxWorkers + 1) {  // zeroed once; every call leaves them zero
+    counts.ensure(kMaxWorkers + 1);
+    EDX_CUDA(cudaMemsetAsync(counts.p, 0, (kMaxWorkers + 1) * sizeof(int), s));
+  }
+  const unsigned blocks = static_cast<unsigned>(rows ? (rows + kBalanceRows - 1) / kBalanceRows : 1);
+  k_check_balance<<<blocks, kBalanceThreads, 0, s>>>(decision, rows, n, m, flags, counts.p);
   EDX_LAUNCHED();
 }
 
@@ -564,7 +572,7 @@ void run_ecomix(DispatchScratch& sc, const double* matrix, uint64_t rows, int n,
   }
   if (ev && ev->exact1) EDX_CUDA(cudaEventRecord(ev->exact1, s));
   if (greedy) EDX_CUDA(cudaStreamWaitEvent(s, sc.join, 0));
-  launch_check_balance(decision, rows, n, m, flags, s);
+  launch_check_balance(decision, rows, n, m, flags, sc.balance, s);
   if (launches) ++*launches;
 }
 

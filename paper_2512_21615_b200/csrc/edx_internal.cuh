@@ -227,7 +227,7 @@ void launch_greedy(const double* matrix, uint64_t rows, int n, const uint32_t* o
                    int32_t* decision, const uint32_t* row_ids, int32_t* pair_worker,
                    int* flags, GreedyScratch& g, cudaStream_t s);
 void launch_check_balance(const int32_t* decision, uint64_t rows, int n, int m, int* flags,
-                          cudaStream_t s);
+                          DevBuf<int>& counts, cudaStream_t s);
 void launch_decision_cost(const double* matrix, const int32_t* decision, uint64_t rows, int n,
                           double* out, cudaStream_t s);
 
@@ -254,6 +254,7 @@ void last_hungarian_stats(HungarianScratch& sc, cudaStream_t s, unsigned long lo
 // The EcoMix pipeline on a device matrix (assign.hpp:247-285).
 struct DispatchScratch {
   SortScratch sort;
+  DevBuf<int> balance;  // k_check_balance: per-worker counts + finished blocks
   HungarianScratch hung;
   DevBuf<uint64_t> gap_keys;
   DevBuf<uint32_t> row_index, order;
