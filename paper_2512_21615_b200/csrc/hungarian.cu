@@ -974,6 +974,9 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
     for (int q = 0; q < 11; ++q) sst[q] = 0;
     sst[7] = clock64();
   }
+  // row i's costs (lane = worker) are fetched one row ahead: the global
+  // load's latency hides behind the previous row's search
+  int64_t snext = (lane < n) ? S[lane] : 0;
   for (int i = 1; i <= k; ++i) {
     if (tid == 0 && timing) sst[8] = clock64();
     // Row frame: Q = cumulative delta of this row's search (<< 6).  Block y
@@ -987,10 +990,11 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
     const bool ordid = ordflag[0] != 0;
     // Row i enters with u[i] = 0 (rows are solved in order); its costs stay
     // in a register for the augment's hop from column 0.
-    int64_t Gy = kBig, By = kBig, srow = 0;
+    int64_t Gy = kBig, By = kBig;
+    const int64_t srow = snext;
+    if (lane < n && i < k) snext = S[static_cast<size_t>(i) * n + lane];
     int dy = 0;
     if (lane < n) {
-      srow = S[static_cast<size_t>(i - 1) * n + lane];
       Gy = srow << 6;  // relax from row i
       By = Btab[ordid ? lane * mult + 1 : ord[lane * mult]];
     }
