@@ -97,6 +97,28 @@ typedef struct edx_engine_options {
  * share the bytes with the other ranks, e.g. through torch.distributed). */
 int edx_nccl_unique_id(void* out, uint64_t len);
 
+/* The multi-GPU exchange steps over a caller's transport (host buffers).
+ * The engine runs exactly this bookkeeping -- which rank builds which rows,
+ * who sends what to whom, what is broadcast -- over NCCL on device memory;
+ * these entry points let a host harness (tests: torch.distributed gloo)
+ * drive it without a GPU.  Callbacks return 0 on success. */
+typedef struct edx_transport {
+  void* ctx;
+  int (*send)(void* ctx, const void* buf, uint64_t bytes, int32_t peer);
+  int (*recv)(void* ctx, void* buf, uint64_t bytes, int32_t peer);
+  int (*broadcast)(void* ctx, void* buf, uint64_t bytes, int32_t root);
+} edx_transport;
+
+/* Row shard [lo[r], hi[r]) of every rank r < world (the cost build's split). */
+int edx_shard_rows(uint64_t rows, int32_t world, uint64_t* lo, uint64_t* hi);
+/* The engine's gather: every rank holds its shard of the rows x n row-major
+ * matrix at its rows' place; afterwards the root holds all of it. */
+int edx_exchange_gather_rows(const edx_transport* t, double* matrix, uint64_t rows, int32_t n,
+                             int32_t world, int32_t rank, int32_t root);
+/* The engine's decision broadcast (one int32 per sample) from the root. */
+int edx_exchange_broadcast_decision(const edx_transport* t, int32_t* decision, uint64_t rows,
+                                    int32_t root);
+
 /* SimState::SimState(const ClusterConfig&) — sim.hpp:56-59.  With world_size
  * > 1 every rank holds a replica of the state; edx_engine_build computes this
  * rank's row shard and gathers the matrix to rank 0 over NCCL, rank 0 solves

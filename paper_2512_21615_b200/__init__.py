@@ -747,8 +747,53 @@ def nccl_unique_id() -> bytes:
 
 
 def shard_rows(rows: int, world: int):
-    """Row shard [lo, hi) of every rank (nccl_comm.h shard_rows)."""
-    return [(rows * r // world, rows * (r + 1) // world) for r in range(world)]
+    """Row shard [lo, hi) of every rank (edx_shard_rows: the cost build's split)."""
+    lo = np.empty(max(world, 1), np.uint64)
+    hi = np.empty(max(world, 1), np.uint64)
+    check(lib().edx_shard_rows(int(rows), int(world), _ptr(lo, C.c_uint64), _ptr(hi, C.c_uint64)))
+    return [(int(a), int(b)) for a, b in zip(lo[:world], hi[:world])]
+
+
+class HostTransport:
+    """An edx_transport over three Python callables on host byte buffers:
+    send(buf: np.ndarray[uint8], peer), recv(buf, peer) (fills buf in place),
+    broadcast(buf, root) (in place).  For driving the engine's multi-rank
+    exchange steps (edx_exchange_*) from a host harness, e.g. torch.distributed
+    gloo in tests; an exception in a callable fails the exchange call."""
+
+    def __init__(self, send, recv, broadcast):
+        from . import _lib as L
+
+        def wrap(fn):
+            def cb(_ctx, buf, nbytes, peer):
+                try:
+                    arr = np.ctypeslib.as_array(C.cast(buf, C.POINTER(C.c_uint8)), (int(nbytes),)) \
+                        if nbytes else np.empty(0, np.uint8)
+                    fn(arr, int(peer))
+                    return 0
+                except Exception:  # reported as the exchange call's error
+                    return 1
+            return cb
+        self._fns = (L.SEND_FN(wrap(send)), L.RECV_FN(wrap(recv)), L.BCAST_FN(wrap(broadcast)))
+        self.c = L.TransportC(None, *self._fns)
+
+
+def exchange_gather_rows(transport: HostTransport, matrix: np.ndarray, world: int, rank: int,
+                         root: int = 0) -> None:
+    """The multi-GPU engine's row gather (edx_exchange_gather_rows) on a host
+    matrix: this rank's shard rows are sent to the root, which receives every
+    other rank's rows in place."""
+    assert matrix.dtype == np.float64 and matrix.flags.c_contiguous and matrix.ndim == 2
+    check(lib().edx_exchange_gather_rows(C.byref(transport.c), _ptr(matrix, C.c_double),
+                                         matrix.shape[0], matrix.shape[1], world, rank, root))
+
+
+def exchange_broadcast_decision(transport: HostTransport, decision: np.ndarray,
+                                root: int = 0) -> None:
+    """The multi-GPU engine's decision broadcast (edx_exchange_broadcast_decision)."""
+    assert decision.dtype == np.int32 and decision.flags.c_contiguous
+    check(lib().edx_exchange_broadcast_decision(C.byref(transport.c), _ptr(decision, C.c_int32),
+                                                decision.size, root))
 
 
 def solver_stats(engine=None) -> dict:

@@ -61,6 +61,17 @@ class EngineOptionsC(C.Structure):
                 ("nccl_unique_id", C.c_void_p)]
 
 
+# edx_transport callbacks: (ctx, buf, bytes, peer/root) -> 0 on success
+SEND_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int32)
+RECV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int32)
+BCAST_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int32)
+
+
+class TransportC(C.Structure):
+    _fields_ = [("ctx", C.c_void_p), ("send", SEND_FN), ("recv", RECV_FN),
+                ("broadcast", BCAST_FN)]
+
+
 # (name, restype, argtypes) for every symbol include/edx.h declares
 def _sigs():
     vp, u64, i32, dbl, cint = C.c_void_p, C.c_uint64, C.c_int32, C.c_double, C.c_int
@@ -73,6 +84,9 @@ def _sigs():
         ("edx_validate_config", cint, [cfgp, u64]),
         ("edx_unit_costs", cint, [cfgp, dblp]),
         ("edx_nccl_unique_id", cint, [vp, u64]),
+        ("edx_shard_rows", cint, [u64, i32, u64p, u64p]),
+        ("edx_exchange_gather_rows", cint, [P(TransportC), dblp, u64, i32, i32, i32, i32]),
+        ("edx_exchange_broadcast_decision", cint, [P(TransportC), i32p, u64, i32]),
         ("edx_engine_create", cint, [cfgp, P(EngineOptionsC), P(vp)]),
         ("edx_engine_destroy", None, [vp]),
         ("edx_engine_load_batch", cint, [vp, vp, vp, u64, cint]),

@@ -522,8 +522,8 @@ void engine_build(edx_engine* e) {
                              e->ucost.p, e->matrix.p + a * e->n, nullptr, nullptr, e->flags.p,
                              e->stream);
     e->kname[edx::kKBuild] = edx::g_kernel_name[edx::kKBuild];
-    edx::nccl_gather_rows(e->comm, e->matrix.p, lo.data(), hi.data(), e->world, e->rank, 0, e->n,
-                          e->stream);
+    edx::NcclTransport tr(e->comm, e->stream);
+    edx::gather_rows(tr, e->matrix.p, lo.data(), hi.data(), e->world, e->rank, 0, e->n);
     e->gap_ready = false;
   }
   rec(e, 1, e->stream);
@@ -570,7 +570,8 @@ void engine_dispatch(edx_engine* e, double alpha) {
     // the decision goes out first; rank 0 (the only rank holding the gathered
     // matrix) computes decision_cost on its side stream, overlapping the step,
     // and the expected cost is broadcast only when a caller asks for it
-    edx::nccl_broadcast_i32(e->comm, e->decision.p, e->rows, 0, e->stream);
+    edx::NcclTransport tr(e->comm, e->stream);
+    edx::broadcast_decision(tr, e->decision.p, e->rows, 0);
     if (e->rank == 0) {
       EDX_CUDA(cudaEventRecord(e->disp.fork, e->stream));
       EDX_CUDA(cudaStreamWaitEvent(e->disp.side, e->disp.fork, 0));
@@ -607,8 +608,10 @@ void validate_decision_host(const int32_t* w, uint64_t count, int n, int m) {
 // multi-GPU engines broadcast rank 0's value (every rank must call this).
 double fetch_expected(edx_engine* e) {
   EDX_CUDA(cudaStreamWaitEvent(e->stream, e->cost_done, 0));
-  if (e->world > 1)
-    edx::nccl_broadcast_i32(e->comm, reinterpret_cast<int32_t*>(e->expected.p), 2, 0, e->stream);
+  if (e->world > 1) {
+    edx::NcclTransport tr(e->comm, e->stream);
+    edx::broadcast_cost(tr, e->expected.p, 0);
+  }
   EDX_CUDA(cudaMemcpyAsync(e->h_expected, e->expected.p, sizeof(double), cudaMemcpyDeviceToHost,
                            e->stream));
   EDX_CUDA(cudaStreamSynchronize(e->stream));
@@ -1234,6 +1237,66 @@ int edx_nccl_unique_id(void* out, uint64_t len) {
   return guard([&] {
     if (len < 128) edx::invalid("nccl unique id buffer must hold 128 bytes");
     edx::nccl_unique_id(out);
+  });
+}
+
+namespace {
+// edx_transport behind the exchange steps (host buffers; a failing callback
+// throws, and guard() turns it into the error code)
+struct CallbackTransport final : edx::Transport {
+  explicit CallbackTransport(const edx_transport* t) : t(t) {
+    if (!t || !t->send || !t->recv || !t->broadcast) edx::invalid("incomplete edx_transport");
+  }
+  void send(const void* buf, uint64_t bytes, int peer) override {
+    if (t->send(t->ctx, buf, bytes, peer) != 0) fail("send");
+  }
+  void recv(void* buf, uint64_t bytes, int peer) override {
+    if (t->recv(t->ctx, buf, bytes, peer) != 0) fail("recv");
+  }
+  void broadcast(void* buf, uint64_t bytes, int root) override {
+    if (t->broadcast(t->ctx, buf, bytes, root) != 0) fail("broadcast");
+  }
+  [[noreturn]] static void fail(const char* what) {
+    throw edx::Error(EDX_RUNTIME_ERROR, std::string("transport ") + what + " failed");
+  }
+  const edx_transport* t;
+};
+
+void check_group(int32_t world, int32_t rank, int32_t root) {
+  if (world < 1) edx::invalid("world_size must be >= 1");
+  if (rank < 0 || rank >= world) edx::invalid("rank out of range");
+  if (root < 0 || root >= world) edx::invalid("root out of range");
+}
+}  // namespace
+
+int edx_shard_rows(uint64_t rows, int32_t world, uint64_t* lo, uint64_t* hi) {
+  return guard([&] {
+    if (world < 1) edx::invalid("world_size must be >= 1");
+    if (!lo || !hi) edx::invalid("null shard bounds");
+    edx::shard_rows(rows, world, lo, hi);
+  });
+}
+
+int edx_exchange_gather_rows(const edx_transport* t, double* matrix, uint64_t rows, int32_t n,
+                             int32_t world, int32_t rank, int32_t root) {
+  return guard([&] {
+    check_group(world, rank, root);
+    if (n < 1) edx::invalid("n must be >= 1");
+    if (rows && !matrix) edx::invalid("null matrix");
+    CallbackTransport tr(t);
+    std::vector<uint64_t> lo(world), hi(world);
+    edx::shard_rows(rows, world, lo.data(), hi.data());
+    edx::gather_rows(tr, matrix, lo.data(), hi.data(), world, rank, root, n);
+  });
+}
+
+int edx_exchange_broadcast_decision(const edx_transport* t, int32_t* decision, uint64_t rows,
+                                    int32_t root) {
+  return guard([&] {
+    if (root < 0) edx::invalid("root out of range");
+    if (rows && !decision) edx::invalid("null decision");
+    CallbackTransport tr(t);
+    edx::broadcast_decision(tr, decision, rows, root);
   });
 }
 

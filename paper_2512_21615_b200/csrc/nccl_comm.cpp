@@ -85,27 +85,39 @@ void nccl_comm_destroy(void* comm) {
   if (comm) api()->comm_destroy(static_cast<ncclComm_t>(comm));
 }
 
-// Rows [lo_r, hi_r) of every rank -> the root's full matrix (grouped send/recv;
-// NCCL 2.27 has no Gather).
-void nccl_gather_rows(void* comm, double* matrix, const uint64_t* lo, const uint64_t* hi,
-                      int world, int rank, int root, int n, cudaStream_t s) {
-  auto* c = static_cast<ncclComm_t>(comm);
-  check(api()->group_start(), "ncclGroupStart");
+void NcclTransport::group_start() { check(api()->group_start(), "ncclGroupStart"); }
+void NcclTransport::group_end() { check(api()->group_end(), "ncclGroupEnd"); }
+void NcclTransport::send(const void* buf, uint64_t bytes, int peer) {
+  check(api()->send(buf, bytes, ncclInt8, peer, static_cast<ncclComm_t>(comm), stream), "ncclSend");
+}
+void NcclTransport::recv(void* buf, uint64_t bytes, int peer) {
+  check(api()->recv(buf, bytes, ncclInt8, peer, static_cast<ncclComm_t>(comm), stream), "ncclRecv");
+}
+void NcclTransport::broadcast(void* buf, uint64_t bytes, int root) {
+  check(api()->broadcast(buf, buf, bytes, ncclInt8, root, static_cast<ncclComm_t>(comm), stream),
+        "ncclBroadcast");
+}
+
+// (NCCL 2.27 has no Gather: grouped point-to-point.)
+void gather_rows(Transport& t, double* matrix, const uint64_t* lo, const uint64_t* hi, int world,
+                 int rank, int root, int n) {
+  const uint64_t row_bytes = static_cast<uint64_t>(n) * sizeof(double);
+  t.group_start();
   if (rank == root) {
     for (int r = 0; r < world; ++r) {
       if (r == root || hi[r] == lo[r]) continue;
-      check(api()->recv(matrix + lo[r] * n, (hi[r] - lo[r]) * n, ncclFloat64, r, c, s), "ncclRecv");
+      t.recv(matrix + lo[r] * n, (hi[r] - lo[r]) * row_bytes, r);
     }
   } else if (hi[rank] > lo[rank]) {
-    check(api()->send(matrix + lo[rank] * n, (hi[rank] - lo[rank]) * n, ncclFloat64, root, c, s),
-          "ncclSend");
+    t.send(matrix + lo[rank] * n, (hi[rank] - lo[rank]) * row_bytes, root);
   }
-  check(api()->group_end(), "ncclGroupEnd");
+  t.group_end();
 }
 
-void nccl_broadcast_i32(void* comm, int32_t* buf, uint64_t count, int root, cudaStream_t s) {
-  check(api()->broadcast(buf, buf, count, ncclInt32, root, static_cast<ncclComm_t>(comm), s),
-        "ncclBroadcast");
+void broadcast_decision(Transport& t, int32_t* decision, uint64_t rows, int root) {
+  if (rows) t.broadcast(decision, rows * sizeof(int32_t), root);
 }
+
+void broadcast_cost(Transport& t, double* cost, int root) { t.broadcast(cost, sizeof(double), root); }
 
 }  // namespace edx
