@@ -1283,12 +1283,15 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
       // overwrites them; from column 0 it takes row i, (S[i] - Dl) << 6
       // (AMODE >= 2: rebuilt from S and u, see the potentials above)
       const int64_t wi = (srow - Dl) << 6;
+      // The entry chain is fetched one hop ahead, so the pointer chase does
+      // not wait behind each hop's operand copy.
       int4 ent = L[nu - 1];
+      int4 prv = L[ent.y];
       for (;;) {
         const int jj = ent.x & 0xffff;
         if (jj == 0) break;
-        const int4 prv = L[ent.y];
         const int rn = prv.x >> 16, pc = prv.x & 0xffff;  // p[jj] = p[way[jj]]
+        const int4 nxt = pc != 0 ? L[prv.y] : prv;
         if (lane == 0) {
           p[jj] = rn;
           rtab[jj] = rn;
@@ -1302,6 +1305,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
           A[static_cast<size_t>(lane) * Kp + (jj - 1)] = w;
         }
         ent = prv;
+        prv = nxt;
       }
     }
     // re-sort the touched blocks, if needed (see warp_block_sorted)
