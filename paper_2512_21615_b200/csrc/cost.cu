@@ -379,6 +379,43 @@ __global__ void __launch_bounds__(kWarpRowsThreads)
   }
 }
 
+// The pushes of one id, owners ascending: every lane of a group reads the
+// same list (one broadcast 16-byte load feeds two adds of each of its cells)
+// and a cell holding the latest copy skips the add; blocks of 8 entries, then
+// pairs; entries past the last owner hold -0.0.  A cell slot none of whose
+// lanes lacks the latest copy (ids with many owners have few such cells) is
+// skipped as a whole (ON0/ON1: warp-uniform).
+template <int NC, bool ON0, bool ON1>
+__device__ __forceinline__ void push_list(double (&c)[NC], const double* buf, int pmax,
+                                          const bool (&act)[NC]) {
+  constexpr bool kOn[2] = {ON0, ON1};
+  int q = 0;
+#pragma unroll 1
+  for (; q + 8 <= pmax; q += 8) {
+    double2 v2[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) v2[e] = *reinterpret_cast<const double2*>(buf + q + 2 * e);
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+#pragma unroll
+      for (int h = 0; h < NC; ++h)
+        if (kOn[h] && act[h]) {
+          c[h] = __dadd_rn(c[h], v2[e].x);
+          c[h] = __dadd_rn(c[h], v2[e].y);
+        }
+  }
+#pragma unroll 1
+  for (; q < pmax; q += 2) {
+    const double2 v2 = *reinterpret_cast<const double2*>(buf + q);
+#pragma unroll
+    for (int h = 0; h < NC; ++h)
+      if (kOn[h] && act[h]) {
+        c[h] = __dadd_rn(c[h], v2.x);
+        c[h] = __dadd_rn(c[h], v2.y);
+      }
+  }
+}
+
 // K1 for 16 < n <= 64 (NP = 32: one row per warp; NP = 64: one row per warp,
 // two cells per lane -- workers j and j + 32, two independent chains over the
 // same lists).  A group of G = min(NP, 32) lanes
@@ -414,12 +451,15 @@ __global__ void __launch_bounds__(kWarpRowsThreads)
   int jw[NC];
   bool cell[NC];
   double uj[NC], c[NC];
+  M jbit[NC], below_mask[NC];
 #pragma unroll
   for (int h = 0; h < NC; ++h) {
     jw[h] = jl + 32 * h;
     cell[h] = rowok && jw[h] < n;
     uj[h] = jw[h] < n ? ucost[jw[h]] : 0.0;
     c[h] = 0.0;
+    jbit[h] = M(1) << jw[h];
+    below_mask[h] = jbit[h] - 1;
   }
   const M full = n >= static_cast<int>(8 * sizeof(M)) ? ~M(0) : ((M(1) << n) - 1);
   uint64_t beg = 0, end = 0;
@@ -471,10 +511,11 @@ __global__ void __launch_bounds__(kWarpRowsThreads)
       const M Lm = __shfl_sync(0xffffffffu, lat, s, G);
       bool act[NC];
 #pragma unroll
-      for (int h = 0; h < NC; ++h) act[h] = cell[h] && !((Lm >> jw[h]) & 1u);
+      for (int h = 0; h < NC; ++h) act[h] = cell[h] && !(Lm & jbit[h]);
       if (!__any_sync(0xffffffffu, O != 0)) {  // no owners: one pull per non-latest cell
 #pragma unroll
-        for (int h = 0; h < NC; ++h) c[h] = __dadd_rn(c[h], act[h] ? uj[h] : -0.0);
+        for (int h = 0; h < NC; ++h)
+          if (act[h]) c[h] = __dadd_rn(c[h], uj[h]);
         continue;
       }
       const int p = popc_mask(O);
@@ -483,43 +524,21 @@ __global__ void __launch_bounds__(kWarpRowsThreads)
       par ^= 1;
 #pragma unroll
       for (int h = 0; h < NC; ++h) {
-        const M below_mask = (M(1) << jw[h]) - 1;
-        const bool has = (O >> jw[h]) & 1u;
-        const int below = popc_mask(O & below_mask);
+        const bool has = (O & jbit[h]) != 0;
+        const int below = popc_mask(O & below_mask[h]);
         buf[has ? below : p + (jw[h] - below)] = has ? uj[h] : -0.0;
       }
       __syncwarp();
 #pragma unroll
       for (int h = 0; h < NC; ++h)
         if (act[h]) c[h] = __dadd_rn(c[h], uj[h]);  // miss pull
-      // pushes, owners ascending: every lane of a group reads the same list
-      // (one broadcast 16-byte load feeds two adds of each of its cells) and
-      // a cell holding the latest copy skips the add; blocks of 8 entries,
-      // then pairs; entries past the last owner hold -0.0
-      int q = 0;
-#pragma unroll 1
-      for (; q + 8 <= pmax; q += 8) {
-        double2 v2[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) v2[e] = *reinterpret_cast<const double2*>(buf + q + 2 * e);
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-#pragma unroll
-          for (int h = 0; h < NC; ++h)
-            if (act[h]) {
-              c[h] = __dadd_rn(c[h], v2[e].x);
-              c[h] = __dadd_rn(c[h], v2[e].y);
-            }
-      }
-#pragma unroll 1
-      for (; q < pmax; q += 2) {
-        const double2 v2 = *reinterpret_cast<const double2*>(buf + q);
-#pragma unroll
-        for (int h = 0; h < NC; ++h)
-          if (act[h]) {
-            c[h] = __dadd_rn(c[h], v2.x);
-            c[h] = __dadd_rn(c[h], v2.y);
-          }
+      if constexpr (NC == 2) {
+        const bool a0 = __any_sync(0xffffffffu, act[0]), a1 = __any_sync(0xffffffffu, act[1]);
+        if (a0 && a1) push_list<NC, true, true>(c, buf, pmax, act);
+        else if (a0) push_list<NC, true, false>(c, buf, pmax, act);
+        else push_list<NC, false, true>(c, buf, pmax, act);
+      } else {
+        push_list<NC, true, false>(c, buf, pmax, act);
       }
     }
   }
