@@ -1,5 +1,6 @@
 // K3 row ordering, K4 capacity-bounded greedy, decision checks, and the
 // EcoMix orchestration (assign.hpp:162-298).
+#include <cub/device/device_merge_sort.cuh>
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
@@ -17,9 +18,31 @@ namespace edx {
 // gap keys are ~bits(gap) (cost.cu), so an ascending *stable* radix sort of
 // (key, row) pairs with rows fed in index order reproduces std::sort with the
 // reference's total order exactly.
+namespace {
+struct KeyLess {
+  __device__ bool operator()(uint64_t a, uint64_t b) const { return a < b; }
+};
+}  // namespace
+
 void sort_rows_by_gap(SortScratch& sc, const uint64_t* keys_in, const uint32_t* idx_in,
                       uint32_t* idx_out, uint64_t rows, cudaStream_t s) {
   sc.keys_out.ensure(rows);
+  static const bool merge = [] {  // EDX_GAP_SORT=merge: stable merge sort (A/B)
+    const char* e = std::getenv("EDX_GAP_SORT");
+    return e && std::strcmp(e, "merge") == 0;
+  }();
+  if (merge) {
+    EDX_CUDA(cudaMemcpyAsync(sc.keys_out.p, keys_in, rows * sizeof(uint64_t),
+                             cudaMemcpyDeviceToDevice, s));
+    EDX_CUDA(cudaMemcpyAsync(idx_out, idx_in, rows * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+    size_t mb = 0;
+    EDX_CUDA(cub::DeviceMergeSort::StableSortPairs(nullptr, mb, sc.keys_out.p, idx_out,
+                                                   static_cast<int64_t>(rows), KeyLess{}, s));
+    sc.temp.ensure(mb);
+    EDX_CUDA(cub::DeviceMergeSort::StableSortPairs(sc.temp.p, mb, sc.keys_out.p, idx_out,
+                                                   static_cast<int64_t>(rows), KeyLess{}, s));
+    return;
+  }
   size_t bytes = 0;
   EDX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys_in, sc.keys_out.p, idx_in,
                                            idx_out, static_cast<int>(rows), 0, 64, s));
@@ -38,11 +61,10 @@ void sort_rows_by_gap(SortScratch& sc, const uint64_t* keys_in, const uint32_t* 
 // close and the next round starts at that row.  Rows after an exhaustion that
 // did not pick the exhausted worker keep their argmin (removing a worker that
 // is not the minimum does not move the minimum), so the first over-capacity
-// row is the first divergence.  Each round closes >= 1 worker: <= n rounds
-// plus one pass per 1024 rows.  One CTA: the matrix slice is L2-resident.
-// (A grid-wide version -- one cooperative CTA per tile of 1024 rows, one
-// grid-wide sync per round -- measured slower at every config: C5 greedy
-// 0.60 -> 1.03 ms, ~15 us per round against ~5 us per 1024-row chunk here.)
+// row is the first divergence.  Each cut closes >= 1 worker: <= n cut rounds
+// plus one round per 1024 rows.  (A grid-wide version -- one cooperative CTA
+// per tile of 1024 rows, one grid-wide sync per round -- measured slower at
+// every config: C5 greedy 0.60 -> 1.03 ms, ~15 us per grid-wide round.)
 namespace {
 
 
