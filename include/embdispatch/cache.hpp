@@ -96,8 +96,11 @@ class WorkerCache {
     uint64_t last = 0;
     edxc::check(edx_cache_find(dev_.get(), id, &found, &ver, &mark, &freq, &last));
     if (!found) return nullptr;
-    found_ = CacheEntry{id, ver != 0, mark, freq, last};
-    return &found_;
+    // per-id storage: a pointer from an earlier find() of another id stays
+    // valid and unchanged (it shows that id's entry as of its own find())
+    CacheEntry& slot = found_[id];
+    slot = CacheEntry{id, ver != 0, mark, freq, last};
+    return &slot;
   }
   // cache.hpp:102-122
   void touch(EmbeddingId id, bool latest, std::uint64_t now) {
@@ -154,7 +157,7 @@ class WorkerCache {
   std::uint32_t current_mark_ = 1;
   FootprintFn footprint_;
   std::shared_ptr<edx_cache> dev_;
-  mutable CacheEntry found_;
+  mutable std::unordered_map<EmbeddingId, CacheEntry> found_;
   mutable std::unordered_map<EmbeddingId, CacheEntry> entries_;
 };
 
