@@ -1102,29 +1102,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
         // one arrival per warp (lane 0, after the warp's shared writes)
         __syncwarp();
         if (lane == 0) mbar_arrive(mbar);
-        // speculative next chunk (this one complete, the run continuing)
         const bool more = sN + 32 < Tm;
-        const int64_t P31 = __shfl_sync(0xffffffffu, Qt, 31);
-        int64_t G31[BPW];
-#pragma unroll
-        for (int h = 0; h < BPW; ++h) G31[h] = __shfl_sync(0xffffffffu, Ga[h], 31);
-        int c2 = 0, r2 = 0;
-        int64_t Bc2 = kBig, Aw2 = 0, Ax2[BPW], V62 = 0, Ss2 = 0, M2[BPW];
-#pragma unroll
-        for (int h = 0; h < BPW; ++h) Ax2[h] = M2[h] = 0;
-        if (more) {
-          load(sN + 32, c2, r2, Bc2, Aw2, Ax2);
-          V62 = static_cast<int64_t>(ws) - Bc2;
-          int64_t V6p = __shfl_up_sync(0xffffffffu, V62, 1), Awp = __shfl_up_sync(0xffffffffu, Aw2, 1);
-          const int64_t V6l = __shfl_sync(0xffffffffu, V6, 31), Awl = __shfl_sync(0xffffffffu, Aw, 31);
-          if (lane == 0) {
-            V6p = V6l;
-            Awp = Awl;
-          }
-          int64_t dl = (V6p < Awp ? V6p : Awp) - V62;
-          if (sN + 32 + lane >= Tm) dl = 0;
-          scan(dl, Ax2, Ss2, M2);
-        }
         mbar_wait(mbar, mbph);
         mbph ^= 1u;
         const unsigned failm = __reduce_or_sync(0xffffffffu, lane < nw ? pfail[par * 32 + lane] : 0u);
@@ -1149,6 +1127,29 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
         }
         sN += vq;
         if (vq == 32 && !phase_end && more) {  // the whole chunk held: continue the run
+          // The next chunk's operands and scan are computed only now: the
+          // kernel is issue-bound (16 warps on 4 schedulers) and most runs end
+          // inside their first chunk, so speculating before the exchange
+          // costs more issue slots than the latency it hides.
+          const int64_t P31 = __shfl_sync(0xffffffffu, Qt, 31);
+          int64_t G31[BPW];
+#pragma unroll
+          for (int h = 0; h < BPW; ++h) G31[h] = __shfl_sync(0xffffffffu, Ga[h], 31);
+          int c2, r2;
+          int64_t Bc2, Aw2, Ax2[BPW], Ss2, M2[BPW];
+          load(sN, c2, r2, Bc2, Aw2, Ax2);
+          const int64_t V62 = static_cast<int64_t>(ws) - Bc2;
+          {
+            int64_t V6p = __shfl_up_sync(0xffffffffu, V62, 1), Awp = __shfl_up_sync(0xffffffffu, Aw2, 1);
+            const int64_t V6l = __shfl_sync(0xffffffffu, V6, 31), Awl = __shfl_sync(0xffffffffu, Aw, 31);
+            if (lane == 0) {
+              V6p = V6l;
+              Awp = Awl;
+            }
+            int64_t dl = (V6p < Awp ? V6p : Awp) - V62;
+            if (sN + lane >= Tm) dl = 0;
+            scan(dl, Ax2, Ss2, M2);
+          }
           P = P31;
 #pragma unroll
           for (int h = 0; h < BPW; ++h) {
@@ -1179,8 +1180,9 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
         }
         if (lane < n)
           Gy = vq > 0 ? GA[(par * 32 + lane) * 33 + vq - 1] : GA[((par ^ 1) * 32 + lane) * 33 + 31];
-        // the winner's next key offset: lane vq of this chunk, or lane 0 of the next
-        const int64_t bnext = __shfl_sync(0xffffffffu, vq < 32 ? Bc : Bc2, vq < 32 ? vq : 0);
+        // the winner's next key offset: lane vq of this chunk (a run ending after
+        // a whole chunk has exhausted the block or ended the row: no next key)
+        const int64_t bnext = __shfl_sync(0xffffffffu, Bc, vq < 32 ? vq : 0);
         par ^= 1;
         if (tid == 0) {
           sst[0] += sN;
