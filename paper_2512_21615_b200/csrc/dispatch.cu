@@ -1,7 +1,6 @@
 // K3 row ordering, K4 capacity-bounded greedy, decision checks, and the
 // EcoMix orchestration (assign.hpp:162-298).
 #include <cub/device/device_merge_sort.cuh>
-#include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
 #include <cmath>
@@ -15,9 +14,10 @@ namespace edx {
 
 // ------------------------------------------------------------------ K3 sort
 // rows_by_gap (assign.hpp:197-207) orders rows by (gap desc, index asc).  The
-// gap keys are ~bits(gap) (cost.cu), so an ascending *stable* radix sort of
+// gap keys are ~bits(gap) (cost.cu), so an ascending *stable* sort of
 // (key, row) pairs with rows fed in index order reproduces std::sort with the
-// reference's total order exactly.
+// reference's total order exactly.  A stable merge sort: the 64-bit keys cost
+// a radix sort eight onesweep passes (C3: 0.100 -> 0.049 ms, C5 0.119 -> 0.095).
 namespace {
 struct KeyLess {
   __device__ bool operator()(uint64_t a, uint64_t b) const { return a < b; }
@@ -27,28 +27,15 @@ struct KeyLess {
 void sort_rows_by_gap(SortScratch& sc, const uint64_t* keys_in, const uint32_t* idx_in,
                       uint32_t* idx_out, uint64_t rows, cudaStream_t s) {
   sc.keys_out.ensure(rows);
-  static const bool merge = [] {  // EDX_GAP_SORT=merge: stable merge sort (A/B)
-    const char* e = std::getenv("EDX_GAP_SORT");
-    return e && std::strcmp(e, "merge") == 0;
-  }();
-  if (merge) {
-    EDX_CUDA(cudaMemcpyAsync(sc.keys_out.p, keys_in, rows * sizeof(uint64_t),
-                             cudaMemcpyDeviceToDevice, s));
-    EDX_CUDA(cudaMemcpyAsync(idx_out, idx_in, rows * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
-    size_t mb = 0;
-    EDX_CUDA(cub::DeviceMergeSort::StableSortPairs(nullptr, mb, sc.keys_out.p, idx_out,
-                                                   static_cast<int64_t>(rows), KeyLess{}, s));
-    sc.temp.ensure(mb);
-    EDX_CUDA(cub::DeviceMergeSort::StableSortPairs(sc.temp.p, mb, sc.keys_out.p, idx_out,
-                                                   static_cast<int64_t>(rows), KeyLess{}, s));
-    return;
-  }
+  EDX_CUDA(cudaMemcpyAsync(sc.keys_out.p, keys_in, rows * sizeof(uint64_t), cudaMemcpyDeviceToDevice,
+                           s));
+  EDX_CUDA(cudaMemcpyAsync(idx_out, idx_in, rows * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
   size_t bytes = 0;
-  EDX_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys_in, sc.keys_out.p, idx_in,
-                                           idx_out, static_cast<int>(rows), 0, 64, s));
+  EDX_CUDA(cub::DeviceMergeSort::StableSortPairs(nullptr, bytes, sc.keys_out.p, idx_out,
+                                                 static_cast<int64_t>(rows), KeyLess{}, s));
   sc.temp.ensure(bytes);
-  EDX_CUDA(cub::DeviceRadixSort::SortPairs(sc.temp.p, bytes, keys_in, sc.keys_out.p, idx_in,
-                                           idx_out, static_cast<int>(rows), 0, 64, s));
+  EDX_CUDA(cub::DeviceMergeSort::StableSortPairs(sc.temp.p, bytes, sc.keys_out.p, idx_out,
+                                                 static_cast<int64_t>(rows), KeyLess{}, s));
 }
 
 // ---------------------------------------------------------------- K4 greedy
@@ -568,7 +555,7 @@ void run_ecomix(DispatchScratch& sc, const double* matrix, uint64_t rows, int n,
     if (launches) ++*launches;
   }
   sort_rows_by_gap(sc.sort, sc.gap_keys.p, sc.row_index.p, sc.order.p, rows, s);
-  if (launches) *launches += 4;  // CUB onesweep: histogram + 3..4 passes (approx.)
+  if (launches) *launches += 4;  // two copies + the merge sort's passes (counted from the launch list)
   if (ev && ev->sort1) EDX_CUDA(cudaEventRecord(ev->sort1, s));
   const bool greedy = k < rows;
   if (greedy) {

@@ -36,8 +36,8 @@ struct StepScratch {
   DevBuf<int32_t> item_slot;     // need item -> cache slot of a resident id (k_classify)
   DevBuf<uint32_t> uniq;         // unique ids in first-appearance order
   DevBuf<unsigned long long> umask;  // trainers mask per unique id
-  DevBuf<int32_t> need_first;    // U * n (id-major): first occurrence position of (j, id)
-  DevBuf<uint32_t> need_cnt;     // U * n (id-major): occurrences of (j, id)
+  DevBuf<int32_t> need_first;    // n * U : first occurrence position of (j, id)
+  DevBuf<uint32_t> need_cnt;     // n * U : occurrences of (j, id)
   DevBuf<uint8_t> flag;          // per occurrence: 1 = first occurrence of (worker, id)
   DevBuf<uint32_t> flag_scan;    // scratch
   DevBuf<uint64_t> need_key;     // (worker << 32 | pos) of first occurrences

@@ -124,7 +124,7 @@ __global__ void k_unique_scatter(const uint32_t* __restrict__ ids, uint64_t T,
 __global__ void k_needs(const uint32_t* __restrict__ ids, uint64_t T,
                         const uint32_t* __restrict__ occ_sample,
                         const int32_t* __restrict__ decision, const int32_t* __restrict__ first_pos,
-                        const uint32_t* __restrict__ uidx, int n,
+                        const uint32_t* __restrict__ uidx, uint64_t ucap,
                         int32_t* __restrict__ need_first, uint32_t* __restrict__ need_cnt,
                         unsigned long long* __restrict__ umask, uint32_t* __restrict__ upos) {
   pdl_wait();
@@ -134,7 +134,7 @@ __global__ void k_needs(const uint32_t* __restrict__ ids, uint64_t T,
   const int j = decision[occ_sample[p]];
   const uint32_t u = uidx[first_pos[ids[p]]];
   upos[p] = u;  // the later passes read it here instead of chasing ids -> first_pos -> uidx
-  const uint64_t x = static_cast<uint64_t>(u) * n + j;  // id-major: a hot id's cells share lines
+  const uint64_t x = static_cast<uint64_t>(j) * ucap + u;
   // test before the atomics (monotone tables, see k_first_pos)
   if (need_first[x] > static_cast<int32_t>(p)) atomicMin(need_first + x, static_cast<int32_t>(p));
   atomicAdd(need_cnt + x, 1u);
@@ -144,7 +144,7 @@ __global__ void k_needs(const uint32_t* __restrict__ ids, uint64_t T,
 // first occurrence of (worker, id) -> sortable key (worker << 32 | position)
 __global__ void k_need_keys(uint64_t T, const uint32_t* __restrict__ occ_sample,
                             const int32_t* __restrict__ decision, const uint32_t* __restrict__ upos,
-                            int n, const int32_t* __restrict__ need_first,
+                            uint64_t ucap, const int32_t* __restrict__ need_first,
                             uint64_t* __restrict__ keys, uint32_t* __restrict__ ws) {
   pdl_wait();
   pdl_trigger();
@@ -152,7 +152,7 @@ __global__ void k_need_keys(uint64_t T, const uint32_t* __restrict__ occ_sample,
   if (p >= T) return;
   const int j = decision[occ_sample[p]];
   const uint32_t u = upos[p];
-  const bool first = need_first[static_cast<uint64_t>(u) * n + j] == static_cast<int32_t>(p);
+  const bool first = need_first[static_cast<uint64_t>(j) * ucap + u] == static_cast<int32_t>(p);
   keys[p] = first ? ((static_cast<uint64_t>(j) << 32) | p) : ~0ULL;
   // per-worker need count: lanes of one sample share the worker, so one
   // atomic per (warp, worker) group
@@ -223,8 +223,8 @@ __device__ __forceinline__ uint32_t item_pos(uint64_t key) { return static_cast<
 __global__ void k_classify(const uint64_t* __restrict__ items,
                            const unsigned long long* counters_ro, int n,
                            const uint32_t* __restrict__ ids, const uint32_t* __restrict__ upos,
-                           int32_t* __restrict__ need_first,
-                           uint32_t* __restrict__ need_cnt, const ulonglong2* __restrict__ ol,
+                           uint64_t ucap, const uint32_t* __restrict__ need_cnt,
+                           const ulonglong2* __restrict__ ol,
                            const unsigned long long* __restrict__ res, uint64_t id_space,
                            const int32_t* __restrict__ slot_of, uint64_t capacity,
                            const uint32_t* __restrict__ smark, const uint32_t* __restrict__ cur_mark,
@@ -248,17 +248,11 @@ __global__ void k_classify(const uint64_t* __restrict__ items,
     const uint32_t id = ids[p];
     const unsigned long long bit = 1ULL << j;
     const ulonglong2 st = ol[id];
-    // this item is the only reader of its (worker, id) need cell from here
-    // on: read the count, then reset the cell for the next step
-    const uint64_t x = static_cast<uint64_t>(upos[p]) * n + j;
-    const uint32_t cnt = need_cnt[x];
-    need_first[x] = INT_MAX;
-    need_cnt[x] = 0;
     uint8_t t;
     int32_t c = 1;
     if (st.y & bit) {
       t = 0;
-      atomicAdd(&hits, static_cast<unsigned long long>(cnt));
+      atomicAdd(&hits, static_cast<unsigned long long>(need_cnt[static_cast<uint64_t>(j) * ucap + upos[p]]));
     } else {
       t = (res[id] & bit) ? 1 : 2;
       atomicAdd(&miss[j], 1u);
@@ -1057,15 +1051,26 @@ __global__ void k_apply(const uint64_t* __restrict__ items,
                         ulonglong2* __restrict__ ol, unsigned long long* __restrict__ res,
                         int32_t* __restrict__ slot_of, uint32_t* __restrict__ sid,
                         uint32_t* __restrict__ smark, uint32_t* __restrict__ sfreq,
-                        uint32_t* __restrict__ slast, const int32_t* __restrict__ item_slot) {
+                        uint32_t* __restrict__ slast, const int32_t* __restrict__ item_slot,
+                        const uint32_t* __restrict__ upos, uint64_t ucap,
+                        int32_t* __restrict__ need_first, uint32_t* __restrict__ need_cnt) {
   pdl_wait();
   pdl_trigger();
   const uint32_t clock = *clock_dev;
   const uint64_t N = counters_ro[3 * n + 2];
   const uint64_t q = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (q >= N) return;
-  const int j = item_worker(items[q]);
-  const uint32_t id = ids[item_pos(items[q])];
+  const uint64_t key = items[q];
+  const int j = item_worker(key);
+  const uint32_t p = item_pos(key);
+  const uint32_t id = ids[p];
+  {
+    // reset this need item's (worker, id) cell for the next step; nothing
+    // after the victim selection reads the need tables
+    const uint64_t x = static_cast<uint64_t>(j) * ucap + upos[p];
+    need_first[x] = INT_MAX;
+    need_cnt[x] = 0;
+  }
   const uint32_t* w = ws + j * kWS;
   const uint32_t local = static_cast<uint32_t>(q) - w[kWsNeedOff];
   const uint32_t mark = cur_mark[j] + (local >= w[kWsAdvance] ? 1u : 0u);
@@ -1299,7 +1304,7 @@ void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
   auto& s = e->step;
   auto& c = e->cache;
   const int n = e->n;
-  const uint64_t T = e->total_ids;
+  const uint64_t T = e->total_ids, ucap = e->max_ids;
   int launches = 0;
   if (e->head_pending) {  // launched by the fused iteration, overlapping the dispatch
     EDX_CUDA(cudaStreamWaitEvent(st, e->head_done, 0));
@@ -1308,9 +1313,9 @@ void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
     launches += launch_step_head(e, st);
   }
   k_needs<<<grid_for(T), kT, 0, st>>>(e->cur_ids, T, s.occ_sample.p, d_decision, s.first_pos.p,
-                                      s.uidx_of_pos.p, n, s.need_first.p, s.need_cnt.p,
+                                      s.uidx_of_pos.p, ucap, s.need_first.p, s.need_cnt.p,
                                       s.umask.p, s.upos.p);
-  launch_pdl(k_need_keys, grid_for(T), kT, 0, st, T, s.occ_sample.p, d_decision, s.upos.p, n,
+  launch_pdl(k_need_keys, grid_for(T), kT, 0, st, T, s.occ_sample.p, d_decision, s.upos.p, ucap,
              s.need_first.p, s.need_key.p, s.wscalars.p);
   EDX_LAUNCHED();
   launches += 2;
@@ -1326,7 +1331,7 @@ void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
   launch_pdl(k_phase1, grid_for(T), kT, 0, st, s.uniq.p, s.umask.p, s.counters.p, n, e->ol.p, s.counters.p,
                                        s.wscalars.p, c.size.p, e->capacity);
   launch_pdl(k_classify, grid_for(T + 1), kT, 0, st, 
-      s.need_key_sorted.p, s.counters.p, n, e->cur_ids, s.upos.p, s.need_first.p,
+      s.need_key_sorted.p, s.counters.p, n, e->cur_ids, s.upos.p, ucap,
       s.need_cnt.p, e->ol.p, e->res.p, e->id_space, c.slot_of.p, e->capacity, c.smark.p,
       c.cur_mark.p, s.need_type.p, s.flag_scan.p, s.need_contrib.p, s.counters.p,
       c.pin.p, e->d_clock.p, s.item_slot.p);
@@ -1416,7 +1421,8 @@ void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
                                       s.need_type.p, s.ins_rank.p, s.wscalars.p,
                                       s.cand_slot_sorted.p, e->capacity, e->id_space, c.cur_mark.p,
                                       e->d_clock.p, e->ol.p, e->res.p, c.slot_of.p, c.sid.p,
-                                      c.smark.p, c.sfreq.p, c.slast.p, s.item_slot.p);
+                                      c.smark.p, c.sfreq.p, c.slast.p, s.item_slot.p, s.upos.p,
+                                      ucap, s.need_first.p, s.need_cnt.p);
   launch_pdl(k_step_tail, grid_for(T), kT, 0, st, n, s.wscalars.p, con_scan, c.size.p, c.cur_mark.p,
                                           c.at_cur.p, s.uniq.p, s.counters.p, e->ol.p,
                                           s.first_pos.p, s.umask.p);
