@@ -555,7 +555,12 @@ void run_ecomix(DispatchScratch& sc, const double* matrix, uint64_t rows, int n,
     if (launches) ++*launches;
   }
   sort_rows_by_gap(sc.sort, sc.gap_keys.p, sc.row_index.p, sc.order.p, rows, s);
-  if (launches) *launches += 4;  // two copies + the merge sort's passes (counted from the launch list)
+  if (launches) {  // CUB merge sort: one block sort of 2048-key tiles, then a partition and a
+                   // merge kernel per pass (as in the launch lists: 5 at 8,192 rows, 11 at 65,536)
+    int passes = 0;
+    for (uint64_t tiles = (rows + 2047) / 2048; tiles > 1; tiles = (tiles + 1) / 2) ++passes;
+    *launches += 1 + 2 * passes;
+  }
   if (ev && ev->sort1) EDX_CUDA(cudaEventRecord(ev->sort1, s));
   const bool greedy = k < rows;
   if (greedy) {
