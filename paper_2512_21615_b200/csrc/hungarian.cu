@@ -1218,52 +1218,63 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
     // row's potential lives only in its column's words).  With A in global
     // memory (AMODE >= 2) a read-modify-write would wait on L2, while S is
     // read-only (cached): the words are rewritten from S and u is kept.  A
-    // group of gs >= n lanes per column, lanes over workers; two columns per
-    // group, every load issued before the first store.
+    // group of gs >= n lanes per column, lanes over workers; every load of a
+    // pass issued before its first store.
     {
       const int gs = n <= 8 ? 8 : (n <= 16 ? 16 : 32);
       const int gpw = 32 / gs, sub = lane / gs, lw = lane - sub * gs;
       const int stride = nw * gpw;
-      for (int eb = warp * gpw; eb < nu; eb += 2 * stride) {  // warp-uniform trip count
-        const int e0 = eb + sub, e1 = e0 + stride;
-        const bool act0 = e0 < nu, act1 = e1 < nu;
-        const int4 q0 = act0 ? L[e0] : make_int4(0, 0, 0, 0);
-        const int4 q1 = act1 ? L[e1] : make_int4(0, 0, 0, 0);
-        const int c0 = q0.x & 0xffff, r0 = q0.x >> 16, c1 = q1.x & 0xffff, r1 = q1.x >> 16;
-        const int64_t dd0 = Dl - ((static_cast<int64_t>(q0.w) << 32) | static_cast<uint32_t>(q0.z));
-        const int64_t dd1 = Dl - ((static_cast<int64_t>(q1.w) << 32) | static_cast<uint32_t>(q1.z));
-        // entry 0 (column 0, row i) sits at e == 0 only; the free column (r == 0) has no words
-        const bool a0 = act0 && c0 != 0, a1 = act1;
-        const bool w0 = a0 && r0 > 0 && lw < n, w1 = a1 && r1 > 0 && lw < n;
-        const bool l0 = lw == 0 && a0, l1 = lw == 0 && a1;
-        const int64_t v0 = l0 ? v[c0] - dd0 : 0, v1 = l1 ? v[c1] - dd1 : 0;
-        const int64_t b0 = l0 ? cblk[c0] : 0, b1 = l1 ? cblk[c1] : 0;
-        int64_t* A0 = A + static_cast<size_t>(lw) * Kp + (c0 - 1);
-        int64_t* A1 = A + static_cast<size_t>(lw) * Kp + (c1 - 1);
-        int64_t x0 = 0, x1 = 0;
+      // columns in flight per group: two with A in shared memory; six with A
+      // in global memory, so one row's S reads (L2) overlap instead of queueing
+      constexpr int NE = AMODE <= 1 ? 2 : 6;
+      for (int eb = warp * gpw; eb < nu; eb += NE * stride) {  // warp-uniform trip count
+        int e[NE], cc[NE], rr[NE];
+        bool act[NE], aa[NE], ww[NE], ll[NE];
+        int64_t dd[NE], vv[NE], bb[NE], xx[NE];
+#pragma unroll
+        for (int q = 0; q < NE; ++q) {
+          e[q] = eb + sub + q * stride;
+          act[q] = e[q] < nu;
+          const int4 qe = act[q] ? L[e[q]] : make_int4(0, 0, 0, 0);
+          cc[q] = qe.x & 0xffff;
+          rr[q] = qe.x >> 16;
+          dd[q] = Dl - ((static_cast<int64_t>(qe.w) << 32) | static_cast<uint32_t>(qe.z));
+          // entry 0 (column 0, row i) sits at e == 0 only; the free column (r == 0) has no words
+          aa[q] = act[q] && cc[q] != 0;
+          ww[q] = aa[q] && rr[q] > 0 && lw < n;
+          ll[q] = lw == 0 && aa[q];
+        }
+#pragma unroll
+        for (int q = 0; q < NE; ++q) {
+          vv[q] = ll[q] ? v[cc[q]] - dd[q] : 0;
+          bb[q] = ll[q] ? cblk[cc[q]] : 0;
+        }
         if constexpr (AMODE <= 1) {
-          x0 = w0 ? *A0 - (dd0 << 6) : 0;
-          x1 = w1 ? *A1 - (dd1 << 6) : 0;
+#pragma unroll
+          for (int q = 0; q < NE; ++q)
+            xx[q] = ww[q] ? A[static_cast<size_t>(lw) * Kp + (cc[q] - 1)] - (dd[q] << 6) : 0;
         } else {
-          const int64_t u0 = act0 ? u[r0] + dd0 : 0, u1 = act1 ? u[r1] + dd1 : 0;
-          x0 = w0 ? (S[static_cast<size_t>(r0 - 1) * n + lw] - u0) << 6 : 0;
-          x1 = w1 ? (S[static_cast<size_t>(r1 - 1) * n + lw] - u1) << 6 : 0;
+          int64_t uu[NE];
+#pragma unroll
+          for (int q = 0; q < NE; ++q) {
+            uu[q] = act[q] ? u[rr[q]] + dd[q] : 0;
+            xx[q] = ww[q] ? (S[static_cast<size_t>(rr[q] - 1) * n + lw] - uu[q]) << 6 : 0;
+          }
           __syncwarp();  // every lane has read u[r] before the group leader writes it
           if (lw == 0) {
-            if (act0) u[r0] = u0;
-            if (act1) u[r1] = u1;
+#pragma unroll
+            for (int q = 0; q < NE; ++q)
+              if (act[q]) u[rr[q]] = uu[q];
           }
         }
-        if (l0) {
-          v[c0] = v0;
-          Btab[c0] = b0 - (v0 << 6);
+#pragma unroll
+        for (int q = 0; q < NE; ++q) {
+          if (ll[q]) {
+            v[cc[q]] = vv[q];
+            Btab[cc[q]] = bb[q] - (vv[q] << 6);
+          }
+          if (ww[q]) A[static_cast<size_t>(lw) * Kp + (cc[q] - 1)] = xx[q];
         }
-        if (l1) {
-          v[c1] = v1;
-          Btab[c1] = b1 - (v1 << 6);
-        }
-        if (w0) *A0 = x0;
-        if (w1) *A1 = x1;
       }
     }
     if constexpr (AMODE >= 2) __threadfence_block();
