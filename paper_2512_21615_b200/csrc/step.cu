@@ -119,21 +119,29 @@ __global__ void k_unique_scatter(const uint32_t* __restrict__ ids, uint64_t T,
   if (first_pos[ids[p]] == static_cast<int32_t>(p)) uniq[uidx[p]] = ids[p];
 }
 
+// The unique index of every occurrence's id, in the decision-independent head
+// (which overlaps the dispatch): the step's passes read it by position.
+__global__ void k_unique_of_pos(const uint32_t* __restrict__ ids, uint64_t T,
+                                const int32_t* __restrict__ first_pos,
+                                const uint32_t* __restrict__ uidx, uint32_t* __restrict__ upos) {
+  pdl_wait();
+  pdl_trigger();
+  const uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (p < T) upos[p] = uidx[first_pos[ids[p]]];
+}
+
 // needs (sim.hpp:103-117): per (worker, id) first position and count, and
 // the trainer mask of every id.
-__global__ void k_needs(const uint32_t* __restrict__ ids, uint64_t T,
-                        const uint32_t* __restrict__ occ_sample,
-                        const int32_t* __restrict__ decision, const int32_t* __restrict__ first_pos,
-                        const uint32_t* __restrict__ uidx, uint64_t ucap,
-                        int32_t* __restrict__ need_first, uint32_t* __restrict__ need_cnt,
-                        unsigned long long* __restrict__ umask, uint32_t* __restrict__ upos) {
+__global__ void k_needs(uint64_t T, const uint32_t* __restrict__ occ_sample,
+                        const int32_t* __restrict__ decision, const uint32_t* __restrict__ upos,
+                        uint64_t ucap, int32_t* __restrict__ need_first,
+                        uint32_t* __restrict__ need_cnt, unsigned long long* __restrict__ umask) {
   pdl_wait();
   pdl_trigger();
   const uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (p >= T) return;
   const int j = decision[occ_sample[p]];
-  const uint32_t u = uidx[first_pos[ids[p]]];
-  upos[p] = u;  // the later passes read it here instead of chasing ids -> first_pos -> uidx
+  const uint32_t u = upos[p];
   const uint64_t x = static_cast<uint64_t>(j) * ucap + u;
   // test before the atomics (monotone tables, see k_first_pos)
   if (need_first[x] > static_cast<int32_t>(p)) atomicMin(need_first + x, static_cast<int32_t>(p));
@@ -252,7 +260,8 @@ __global__ void k_classify(const uint64_t* __restrict__ items,
     int32_t c = 1;
     if (st.y & bit) {
       t = 0;
-      atomicAdd(&hits, static_cast<unsigned long long>(need_cnt[static_cast<uint64_t>(j) * ucap + upos[p]]));
+      const uint32_t cnt = need_cnt[static_cast<uint64_t>(j) * ucap + upos[p]];
+      atomicAdd(&hits, static_cast<unsigned long long>(cnt));
     } else {
       t = (res[id] & bit) ? 1 : 2;
       atomicAdd(&miss[j], 1u);
@@ -1274,8 +1283,10 @@ int launch_step_head(edx_engine* e, cudaStream_t st) {
   });
   launch_pdl(k_unique_scatter, grid_for(T + 1), kT, 0, st, e->cur_ids, T, s.first_pos.p, s.uidx_of_pos.p,
                                                    s.uniq.p, s.counters.p, n);
+  launch_pdl(k_unique_of_pos, grid_for(T), kT, 0, st, e->cur_ids, T, s.first_pos.p,
+             s.uidx_of_pos.p, s.upos.p);
   EDX_LAUNCHED();
-  return 5;
+  return 6;
 }
 
 }  // namespace
@@ -1312,9 +1323,8 @@ void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
   } else {
     launches += launch_step_head(e, st);
   }
-  k_needs<<<grid_for(T), kT, 0, st>>>(e->cur_ids, T, s.occ_sample.p, d_decision, s.first_pos.p,
-                                      s.uidx_of_pos.p, ucap, s.need_first.p, s.need_cnt.p,
-                                      s.umask.p, s.upos.p);
+  k_needs<<<grid_for(T), kT, 0, st>>>(T, s.occ_sample.p, d_decision, s.upos.p, ucap,
+                                      s.need_first.p, s.need_cnt.p, s.umask.p);
   launch_pdl(k_need_keys, grid_for(T), kT, 0, st, T, s.occ_sample.p, d_decision, s.upos.p, ucap,
              s.need_first.p, s.need_key.p, s.wscalars.p);
   EDX_LAUNCHED();
