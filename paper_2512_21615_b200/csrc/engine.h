@@ -36,8 +36,9 @@ struct StepScratch {
   DevBuf<int32_t> item_slot;     // need item -> cache slot of a resident id (k_classify)
   DevBuf<uint32_t> uniq;         // unique ids in first-appearance order
   DevBuf<unsigned long long> umask;  // trainers mask per unique id
-  DevBuf<int32_t> need_first;    // n * U : first occurrence position of (j, id)
-  DevBuf<uint32_t> need_cnt;     // n * U : occurrences of (j, id)
+  DevBuf<unsigned long long> need_first;  // n * U : epoch << 32 | ~first position of (j, id)
+  DevBuf<unsigned long long> need_cnt;    // n * U : epoch << 32 | occurrences of (j, id)
+  DevBuf<uint32_t> epoch;                 // step counter tagging the need cells
   DevBuf<uint8_t> flag;          // per occurrence: 1 = first occurrence of (worker, id)
   DevBuf<uint32_t> flag_scan;    // scratch
   DevBuf<uint64_t> need_key;     // (worker << 32 | pos) of first occurrences

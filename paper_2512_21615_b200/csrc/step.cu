@@ -80,10 +80,11 @@ __global__ void k_step_begin(const uint64_t* __restrict__ offsets, uint64_t rows
                              uint32_t* __restrict__ occ_sample, const uint32_t* __restrict__ ids,
                              uint64_t T, int32_t* __restrict__ first_pos,
                              unsigned long long* __restrict__ counters, uint32_t ncnt,
-                             uint32_t* __restrict__ ws, uint32_t nws) {
+                             uint32_t* __restrict__ ws, uint32_t nws, uint32_t* __restrict__ epoch) {
   pdl_wait();
   pdl_trigger();
   const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i == 0) *epoch += 1;  // this step's need-cell tag (never 0, never reused)
   if (i < ncnt) counters[i] = 0;
   if (i < nws) ws[i] = 0;
   if (i < rows)
@@ -130,37 +131,62 @@ __global__ void k_unique_of_pos(const uint32_t* __restrict__ ids, uint64_t T,
   if (p < T) upos[p] = uidx[first_pos[ids[p]]];
 }
 
+// Need cells are tagged with the step's epoch (high 32 bits), so no pass
+// resets them: a cell from an earlier step reads as empty.
+//   first: epoch << 32 | ~position, kept by atomicMax (newest epoch, then
+//          the least position);
+//   count: epoch << 32 | occurrences; the first adder of a step installs
+//          (epoch, 1) by CAS, every other occurrence adds 1.
+__device__ __forceinline__ unsigned long long first_tag(uint32_t epoch, uint64_t p) {
+  return (static_cast<unsigned long long>(epoch) << 32) | (0xFFFFFFFFu - static_cast<uint32_t>(p));
+}
+
 // needs (sim.hpp:103-117): per (worker, id) first position and count, and
 // the trainer mask of every id.
 __global__ void k_needs(uint64_t T, const uint32_t* __restrict__ occ_sample,
                         const int32_t* __restrict__ decision, const uint32_t* __restrict__ upos,
-                        uint64_t ucap, int32_t* __restrict__ need_first,
-                        uint32_t* __restrict__ need_cnt, unsigned long long* __restrict__ umask) {
+                        uint64_t ucap, unsigned long long* __restrict__ need_first,
+                        unsigned long long* __restrict__ need_cnt,
+                        unsigned long long* __restrict__ umask, const uint32_t* __restrict__ epoch_dev) {
   pdl_wait();
   pdl_trigger();
   const uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (p >= T) return;
+  const uint32_t epoch = *epoch_dev;
   const int j = decision[occ_sample[p]];
   const uint32_t u = upos[p];
   const uint64_t x = static_cast<uint64_t>(j) * ucap + u;
-  // test before the atomics (monotone tables, see k_first_pos)
-  if (need_first[x] > static_cast<int32_t>(p)) atomicMin(need_first + x, static_cast<int32_t>(p));
-  atomicAdd(need_cnt + x, 1u);
+  // test before the atomics: the cell only grows within a step
+  const unsigned long long f = first_tag(epoch, p);
+  if (need_first[x] < f) atomicMax(need_first + x, f);
+  const unsigned long long tag = static_cast<unsigned long long>(epoch) << 32;
+  unsigned long long cur = need_cnt[x];
+  bool counted = false;
+  while ((cur & 0xFFFFFFFF00000000ULL) != tag) {  // a stale cell: install (epoch, 1)
+    const unsigned long long prev = atomicCAS(need_cnt + x, cur, tag | 1ULL);
+    if (prev == cur) {
+      counted = true;
+      break;
+    }
+    cur = prev;
+  }
+  if (!counted) atomicAdd(need_cnt + x, 1ULL);
   if (!((umask[u] >> j) & 1ULL)) atomicOr(umask + u, 1ULL << j);
 }
 
 // first occurrence of (worker, id) -> sortable key (worker << 32 | position)
 __global__ void k_need_keys(uint64_t T, const uint32_t* __restrict__ occ_sample,
                             const int32_t* __restrict__ decision, const uint32_t* __restrict__ upos,
-                            uint64_t ucap, const int32_t* __restrict__ need_first,
-                            uint64_t* __restrict__ keys, uint32_t* __restrict__ ws) {
+                            uint64_t ucap, const unsigned long long* __restrict__ need_first,
+                            uint64_t* __restrict__ keys, uint32_t* __restrict__ ws,
+                            const uint32_t* __restrict__ epoch_dev) {
   pdl_wait();
   pdl_trigger();
   const uint64_t p = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (p >= T) return;
   const int j = decision[occ_sample[p]];
   const uint32_t u = upos[p];
-  const bool first = need_first[static_cast<uint64_t>(j) * ucap + u] == static_cast<int32_t>(p);
+  const bool first = need_first[static_cast<uint64_t>(j) * ucap + u] == first_tag(*epoch_dev, p);
   keys[p] = first ? ((static_cast<uint64_t>(j) << 32) | p) : ~0ULL;
   // per-worker need count: lanes of one sample share the worker, so one
   // atomic per (warp, worker) group
@@ -231,7 +257,7 @@ __device__ __forceinline__ uint32_t item_pos(uint64_t key) { return static_cast<
 __global__ void k_classify(const uint64_t* __restrict__ items,
                            const unsigned long long* counters_ro, int n,
                            const uint32_t* __restrict__ ids, const uint32_t* __restrict__ upos,
-                           uint64_t ucap, const uint32_t* __restrict__ need_cnt,
+                           uint64_t ucap, const unsigned long long* __restrict__ need_cnt,
                            const ulonglong2* __restrict__ ol,
                            const unsigned long long* __restrict__ res, uint64_t id_space,
                            const int32_t* __restrict__ slot_of, uint64_t capacity,
@@ -260,7 +286,9 @@ __global__ void k_classify(const uint64_t* __restrict__ items,
     int32_t c = 1;
     if (st.y & bit) {
       t = 0;
-      const uint32_t cnt = need_cnt[static_cast<uint64_t>(j) * ucap + upos[p]];
+      // (the cell carries this step's tag: its item exists)
+      const uint64_t x = static_cast<uint64_t>(j) * ucap + upos[p];
+      const uint32_t cnt = static_cast<uint32_t>(need_cnt[x]);
       atomicAdd(&hits, static_cast<unsigned long long>(cnt));
     } else {
       t = (res[id] & bit) ? 1 : 2;
@@ -1060,9 +1088,7 @@ __global__ void k_apply(const uint64_t* __restrict__ items,
                         ulonglong2* __restrict__ ol, unsigned long long* __restrict__ res,
                         int32_t* __restrict__ slot_of, uint32_t* __restrict__ sid,
                         uint32_t* __restrict__ smark, uint32_t* __restrict__ sfreq,
-                        uint32_t* __restrict__ slast, const int32_t* __restrict__ item_slot,
-                        const uint32_t* __restrict__ upos, uint64_t ucap,
-                        int32_t* __restrict__ need_first, uint32_t* __restrict__ need_cnt) {
+                        uint32_t* __restrict__ slast, const int32_t* __restrict__ item_slot) {
   pdl_wait();
   pdl_trigger();
   const uint32_t clock = *clock_dev;
@@ -1071,15 +1097,7 @@ __global__ void k_apply(const uint64_t* __restrict__ items,
   if (q >= N) return;
   const uint64_t key = items[q];
   const int j = item_worker(key);
-  const uint32_t p = item_pos(key);
-  const uint32_t id = ids[p];
-  {
-    // reset this need item's (worker, id) cell for the next step; nothing
-    // after the victim selection reads the need tables
-    const uint64_t x = static_cast<uint64_t>(j) * ucap + upos[p];
-    need_first[x] = INT_MAX;
-    need_cnt[x] = 0;
-  }
+  const uint32_t id = ids[item_pos(key)];
   const uint32_t* w = ws + j * kWS;
   const uint32_t local = static_cast<uint32_t>(q) - w[kWsNeedOff];
   const uint32_t mark = cur_mark[j] + (local >= w[kWsAdvance] ? 1u : 0u);
@@ -1195,11 +1213,13 @@ void step_init_state(edx_engine* e) {
   s.uniq.ensure(T);
   s.umask.ensure(T);
   EDX_CUDA(cudaMemsetAsync(s.umask.p, 0, T * sizeof(unsigned long long), e->stream));
+  // epoch-tagged need cells (k_needs): all-zero = no step
   s.need_first.ensure(n * T);
-  k_fill_i32<<<grid_for(n * T), kT, 0, e->stream>>>(s.need_first.p, n * T, INT_MAX);
-  EDX_LAUNCHED();
+  EDX_CUDA(cudaMemsetAsync(s.need_first.p, 0, n * T * sizeof(unsigned long long), e->stream));
   s.need_cnt.ensure(n * T);
-  EDX_CUDA(cudaMemsetAsync(s.need_cnt.p, 0, n * T * sizeof(uint32_t), e->stream));
+  EDX_CUDA(cudaMemsetAsync(s.need_cnt.p, 0, n * T * sizeof(unsigned long long), e->stream));
+  s.epoch.ensure(1);
+  EDX_CUDA(cudaMemsetAsync(s.epoch.p, 0, sizeof(uint32_t), e->stream));
   s.flag_scan.ensure(T + 1);
   s.need_key.ensure(T);
   s.need_key_sorted.ensure(T);
@@ -1274,7 +1294,8 @@ int launch_step_head(edx_engine* e, cudaStream_t st) {
   const uint32_t ncnt = static_cast<uint32_t>(3 * n + 4), nws = static_cast<uint32_t>(n * kWS);
   const uint64_t span = std::max<uint64_t>(std::max<uint64_t>(R, T), nws);
   k_step_begin<<<grid_for(span), kT, 0, st>>>(e->cur_offsets, R, s.occ_sample.p, e->cur_ids, T,
-                                              s.first_pos.p, s.counters.p, ncnt, s.wscalars.p, nws);
+                                              s.first_pos.p, s.counters.p, ncnt, s.wscalars.p, nws,
+                                              s.epoch.p);
   launch_pdl(k_unique_flag, grid_for(T + 1), kT, 0, st, e->cur_ids, T, s.first_pos.p, s.flag_scan.p);
   EDX_LAUNCHED();
   cub_call(e, [&](void* tmp, size_t& b) {
@@ -1324,9 +1345,9 @@ void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
     launches += launch_step_head(e, st);
   }
   k_needs<<<grid_for(T), kT, 0, st>>>(T, s.occ_sample.p, d_decision, s.upos.p, ucap,
-                                      s.need_first.p, s.need_cnt.p, s.umask.p);
+                                      s.need_first.p, s.need_cnt.p, s.umask.p, s.epoch.p);
   launch_pdl(k_need_keys, grid_for(T), kT, 0, st, T, s.occ_sample.p, d_decision, s.upos.p, ucap,
-             s.need_first.p, s.need_key.p, s.wscalars.p);
+             s.need_first.p, s.need_key.p, s.wscalars.p, s.epoch.p);
   EDX_LAUNCHED();
   launches += 2;
   int wbits = 1;
@@ -1431,8 +1452,7 @@ void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
                                       s.need_type.p, s.ins_rank.p, s.wscalars.p,
                                       s.cand_slot_sorted.p, e->capacity, e->id_space, c.cur_mark.p,
                                       e->d_clock.p, e->ol.p, e->res.p, c.slot_of.p, c.sid.p,
-                                      c.smark.p, c.sfreq.p, c.slast.p, s.item_slot.p, s.upos.p,
-                                      ucap, s.need_first.p, s.need_cnt.p);
+                                      c.smark.p, c.sfreq.p, c.slast.p, s.item_slot.p);
   launch_pdl(k_step_tail, grid_for(T), kT, 0, st, n, s.wscalars.p, con_scan, c.size.p, c.cur_mark.p,
                                           c.at_cur.p, s.uniq.p, s.counters.p, e->ol.p,
                                           s.first_pos.p, s.umask.p);
