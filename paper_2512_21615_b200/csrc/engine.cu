@@ -687,7 +687,11 @@ void engine_step(edx_engine* e, const int32_t* decision, edx_report* rep) {
 void iterate_enqueue(edx_engine* e, double alpha) {
   if (!e->cur_ids) edx::invalid("no batch loaded");
   ensure_translated(e);
-  if (!e->profiling) edx::step_head(e);  // profiled runs time the whole step in its phase
+  static const bool overlap = [] {  // EDX_HEAD_OVERLAP=0: the head runs inside the step (A/B)
+    const char* v = std::getenv("EDX_HEAD_OVERLAP");
+    return !(v && std::strcmp(v, "0") == 0);
+  }();
+  if (!e->profiling && overlap) edx::step_head(e);  // profiled runs time the whole step
   try {
     engine_build(e);
     engine_dispatch(e, alpha);
