@@ -84,7 +84,7 @@ __global__ void k_step_begin(const uint64_t* __restrict__ offsets, uint64_t rows
   pdl_wait();
   pdl_trigger();
   const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  if (i == 0) *epoch += 1;  // this step's need-cell tag (never 0, never reused)
+  if (i == 0) *epoch += 1;  // this step's need-cell tag (never 0; unique for 2^32 - 1 steps)
   if (i < ncnt) counters[i] = 0;
   if (i < nws) ws[i] = 0;
   if (i < rows)
