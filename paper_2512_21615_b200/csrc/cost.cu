@@ -381,39 +381,41 @@ __global__ void __launch_bounds__(kWarpRowsThreads)
 
 // The pushes of one id, owners ascending: every lane of a group reads the
 // same list (one broadcast 16-byte load feeds two adds of each of its cells)
-// and a cell holding the latest copy skips the add; blocks of 8 entries, then
-// pairs; entries past the last owner hold -0.0.  A cell slot none of whose
+// and a cell holding the latest copy skips the add; entries past the last
+// owner hold -0.0.  A cell slot none of whose
 // lanes lacks the latest copy (ids with many owners have few such cells) is
 // skipped as a whole (ON0/ON1: warp-uniform).
 template <int NC, bool ON0, bool ON1>
 __device__ __forceinline__ void push_list(double (&c)[NC], const double* buf, int pmax,
                                           const bool (&act)[NC]) {
   constexpr bool kOn[2] = {ON0, ON1};
-  int q = 0;
-#pragma unroll 1
-  for (; q + 8 <= pmax; q += 8) {
-    double2 v2[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) v2[e] = *reinterpret_cast<const double2*>(buf + q + 2 * e);
-#pragma unroll
-    for (int e = 0; e < 4; ++e)
-#pragma unroll
-      for (int h = 0; h < NC; ++h)
-        if (kOn[h] && act[h]) {
-          c[h] = __dadd_rn(c[h], v2[e].x);
-          c[h] = __dadd_rn(c[h], v2[e].y);
-        }
+  // an unrolled ladder of 32 pairs entered at pair 32 - ceil(pmax / 2) (one
+  // indirect branch per id, no loop counter); pairs past pmax hold -0.0
+  const int skip = 32 - ((pmax + 1) >> 1);
+  const double2* base = reinterpret_cast<const double2*>(buf) - skip;
+#define EDX_PUSH_PAIR(k)                                  \
+  case k: {                                               \
+    const double2 v2 = base[k];                           \
+    _Pragma("unroll") for (int h = 0; h < NC; ++h)        \
+      if (kOn[h] && act[h]) {                             \
+        c[h] = __dadd_rn(c[h], v2.x);                     \
+        c[h] = __dadd_rn(c[h], v2.y);                     \
+      }                                                   \
+  }                                                       \
+    [[fallthrough]];
+  switch (skip) {
+    EDX_PUSH_PAIR(0) EDX_PUSH_PAIR(1) EDX_PUSH_PAIR(2) EDX_PUSH_PAIR(3)
+    EDX_PUSH_PAIR(4) EDX_PUSH_PAIR(5) EDX_PUSH_PAIR(6) EDX_PUSH_PAIR(7)
+    EDX_PUSH_PAIR(8) EDX_PUSH_PAIR(9) EDX_PUSH_PAIR(10) EDX_PUSH_PAIR(11)
+    EDX_PUSH_PAIR(12) EDX_PUSH_PAIR(13) EDX_PUSH_PAIR(14) EDX_PUSH_PAIR(15)
+    EDX_PUSH_PAIR(16) EDX_PUSH_PAIR(17) EDX_PUSH_PAIR(18) EDX_PUSH_PAIR(19)
+    EDX_PUSH_PAIR(20) EDX_PUSH_PAIR(21) EDX_PUSH_PAIR(22) EDX_PUSH_PAIR(23)
+    EDX_PUSH_PAIR(24) EDX_PUSH_PAIR(25) EDX_PUSH_PAIR(26) EDX_PUSH_PAIR(27)
+    EDX_PUSH_PAIR(28) EDX_PUSH_PAIR(29) EDX_PUSH_PAIR(30) EDX_PUSH_PAIR(31)
+    default:
+      break;
   }
-#pragma unroll 1
-  for (; q < pmax; q += 2) {
-    const double2 v2 = *reinterpret_cast<const double2*>(buf + q);
-#pragma unroll
-    for (int h = 0; h < NC; ++h)
-      if (kOn[h] && act[h]) {
-        c[h] = __dadd_rn(c[h], v2.x);
-        c[h] = __dadd_rn(c[h], v2.y);
-      }
-  }
+#undef EDX_PUSH_PAIR
 }
 
 // K1 for 16 < n <= 64 (NP = 32: one row per warp; NP = 64: one row per warp,

@@ -806,10 +806,11 @@ __device__ __forceinline__ void warp_resort_dispatch(int32_t* ord, const int64_t
 // adjacent pair violates (v desc, j asc) -- which never happened in any
 // measured solve.
 __device__ __forceinline__ bool warp_block_sorted(const int32_t* ord, const int64_t* v, int base,
-                                                  int mult, int lane) {
+                                                  int mult, int lane, bool ordid) {
   bool bad = false;
   for (int q = lane; q < mult - 1; q += 32) {
-    const int a = ord[base + q], b = ord[base + q + 1];
+    // (identity order: position q holds column q + 1, no lookup)
+    const int a = ordid ? base + q + 1 : ord[base + q], b = ordid ? a + 1 : ord[base + q + 1];
     const int64_t va = v[a], vb = v[b];
     bad |= !(va > vb || (va == vb && a < b));
   }
@@ -1324,7 +1325,7 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
     // re-sort the touched blocks, if needed (see warp_block_sorted)
     for (int w = warp; w < n; w += nw) {
       if (curs[w] == 0) continue;
-      if (!warp_block_sorted(ord, v, w * mult, mult, lane)) {
+      if (!warp_block_sorted(ord, v, w * mult, mult, lane, ordflag[0] != 0)) {
         if (lane == 0) {
           atomicAdd(&sst[3], 1ULL);
           ordflag[0] = 0;
