@@ -335,7 +335,10 @@ __global__ void __launch_bounds__(kGreedyThreads)
         }
       }
       lap(5);
-      if (limit >= kGreedyThreads) break;  // uniform: the window is committed
+      if (limit >= kGreedyThreads) {  // uniform: the window is committed
+        if (valid && choice < 0) pair_worker[t] = -1;  // left without a worker (flagged)
+        break;
+      }
       q0 = limit;
     }
     ++round;
@@ -456,8 +459,6 @@ void launch_greedy(const double* matrix, uint64_t rows, int n, const uint32_t* o
     g.pw.ensure(n_order);
     pw = g.pw.p;
   }
-  if (decision)  // positions left without a worker keep -1 (and raise kFlagUnbalanced)
-    EDX_CUDA(cudaMemsetAsync(pw, 0xFF, n_order * sizeof(int32_t), s));
   k_greedy_prefs<<<static_cast<unsigned>((n_order * 32 + 255) / 256), 256, 0, s>>>(
       matrix, n, order, n_order, capacity_dev, cap_uniform, row_ids, g.prefs.p, g.dest.p);
   g_kernel_name[kKGreedy] = "k_greedy";
