@@ -505,21 +505,25 @@ __global__ void __launch_bounds__(kWarpRowsThreads)
     }
     // ids some worker of its row lacks, slot-aligned over the warp's groups
     unsigned todo = __ballot_sync(0xffffffffu, (lat & full) != full);
-    if constexpr (RPW == 2) todo = (todo | (todo >> 16)) & gmask;
+    unsigned owned = __ballot_sync(0xffffffffu, own != 0);  // ids with a push list
+    if constexpr (RPW == 2) {
+      todo = (todo | (todo >> 16)) & gmask;
+      owned = (owned | (owned >> 16)) & gmask;
+    }
     while (todo) {
       const int s = __ffs(todo) - 1;
       todo &= todo - 1;
-      const M O = __shfl_sync(0xffffffffu, own, s, G);
       const M Lm = __shfl_sync(0xffffffffu, lat, s, G);
       bool act[NC];
 #pragma unroll
       for (int h = 0; h < NC; ++h) act[h] = cell[h] && !(Lm & jbit[h]);
-      if (!__any_sync(0xffffffffu, O != 0)) {  // no owners: one pull per non-latest cell
+      if (!((owned >> s) & 1u)) {  // no owners: one pull per non-latest cell
 #pragma unroll
         for (int h = 0; h < NC; ++h)
           if (act[h]) c[h] = __dadd_rn(c[h], uj[h]);
         continue;
       }
+      const M O = __shfl_sync(0xffffffffu, own, s, G);
       const int p = popc_mask(O);
       const int pmax = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(p)));
       double* buf = mylist + par * (RPW * NP);
