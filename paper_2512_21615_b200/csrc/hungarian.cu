@@ -1225,11 +1225,9 @@ __global__ void __launch_bounds__(MAXW * 32, 1)                   // BPW: blocks
       const int gs = n <= 8 ? 8 : (n <= 16 ? 16 : 32);
       const int gpw = 32 / gs, sub = lane / gs, lw = lane - sub * gs;
       const int stride = nw * gpw;
-      // columns in flight per group: four with A in shared memory (a row's
-      // ~120 reached columns in one pass of 16 warps); two with A in global
-      // memory (six, meant to overlap the S reads, measured slower: C4 row
-      // end 5.1 -> 7.9 K cycles)
-      constexpr int NE = AMODE <= 1 ? 4 : 2;
+      // two columns in flight per group (four with A in shared memory: C3 row
+      // end 2.37 -> 2.84 K cycles; six with A in global memory: C4 5.1 -> 7.9 K)
+      constexpr int NE = 2;
       for (int eb = warp * gpw; eb < nu; eb += NE * stride) {  // warp-uniform trip count
         int e[NE], cc[NE], rr[NE];
         bool act[NE], aa[NE], ww[NE], ll[NE];
