@@ -1,6 +1,5 @@
 // K3 row ordering, K4 capacity-bounded greedy, decision checks, and the
 // EcoMix orchestration (assign.hpp:162-298).
-#include <cub/block/block_radix_sort.cuh>
 #include <cub/device/device_merge_sort.cuh>
 
 #include <algorithm>
@@ -17,64 +16,16 @@ namespace edx {
 // rows_by_gap (assign.hpp:197-207) orders rows by (gap desc, index asc).  The
 // gap keys are ~bits(gap) (cost.cu), so an ascending *stable* sort of
 // (key, row) pairs with rows fed in index order reproduces std::sort with the
-// reference's total order exactly.  Up to 8,192 rows: one CTA sorts them in
-// shared memory (CUB block radix sort, 8 keys per thread, blocked and so
-// stable; padding keys sort last as they enter last).  Above: CUB's stable
-// merge sort (the 64-bit keys cost a device radix sort eight onesweep
-// passes: C3 0.100 -> 0.049 ms, C5 0.119 -> 0.095 ms).
+// reference's total order exactly.  A stable merge sort: the 64-bit keys cost
+// a radix sort eight onesweep passes (C3: 0.100 -> 0.049 ms, C5 0.119 -> 0.095).
 namespace {
 struct KeyLess {
   __device__ bool operator()(uint64_t a, uint64_t b) const { return a < b; }
 };
-
-constexpr int kSortThreads = 1024, kSortItems = 8, kSortTile = kSortThreads * kSortItems;
-using BlockSort = cub::BlockRadixSort<uint64_t, kSortThreads, kSortItems, uint32_t>;
-
-__global__ void __launch_bounds__(kSortThreads, 1)
-    k_gap_sort_block(const uint64_t* __restrict__ keys_in, const uint32_t* __restrict__ idx_in,
-                     uint32_t* __restrict__ idx_out, int rows) {
-  extern __shared__ __align__(16) uint8_t sort_smem[];
-  auto& tmp = *reinterpret_cast<typename BlockSort::TempStorage*>(sort_smem);
-  uint64_t k[kSortItems];
-  uint32_t v[kSortItems];
-#pragma unroll
-  for (int q = 0; q < kSortItems; ++q) {  // blocked: thread t holds positions t*8 .. t*8+7
-    const int i = threadIdx.x * kSortItems + q;
-    k[q] = i < rows ? keys_in[i] : ~0ULL;
-    v[q] = i < rows ? idx_in[i] : 0xFFFFFFFFu;
-  }
-  BlockSort(tmp).Sort(k, v);
-#pragma unroll
-  for (int q = 0; q < kSortItems; ++q) {
-    const int i = threadIdx.x * kSortItems + q;
-    if (i < rows) idx_out[i] = v[q];
-  }
-}
 }  // namespace
-
-int gap_sort_launches(uint64_t rows) {
-  if (rows <= static_cast<uint64_t>(kSortTile)) return 1;
-  // two copies, then CUB's merge sort: a block sort of 2048-key tiles and a
-  // partition and a merge kernel per pass (11 launches at 65,536 rows)
-  int passes = 0;
-  for (uint64_t tiles = (rows + 2047) / 2048; tiles > 1; tiles = (tiles + 1) / 2) ++passes;
-  return 1 + 2 * passes;
-}
 
 void sort_rows_by_gap(SortScratch& sc, const uint64_t* keys_in, const uint32_t* idx_in,
                       uint32_t* idx_out, uint64_t rows, cudaStream_t s) {
-  if (rows <= static_cast<uint64_t>(kSortTile)) {
-    constexpr size_t smem = sizeof(typename BlockSort::TempStorage);
-    static bool attr = [] {
-      EDX_CUDA(cudaFuncSetAttribute(k_gap_sort_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem)));
-      return true;
-    }();
-    (void)attr;
-    k_gap_sort_block<<<1, kSortThreads, smem, s>>>(keys_in, idx_in, idx_out, static_cast<int>(rows));
-    EDX_LAUNCHED();
-    return;
-  }
   sc.keys_out.ensure(rows);
   EDX_CUDA(cudaMemcpyAsync(sc.keys_out.p, keys_in, rows * sizeof(uint64_t), cudaMemcpyDeviceToDevice,
                            s));
@@ -605,7 +556,12 @@ void run_ecomix(DispatchScratch& sc, const double* matrix, uint64_t rows, int n,
     if (launches) ++*launches;
   }
   sort_rows_by_gap(sc.sort, sc.gap_keys.p, sc.row_index.p, sc.order.p, rows, s);
-  if (launches) *launches += gap_sort_launches(rows);
+  if (launches) {  // CUB merge sort: one block sort of 2048-key tiles, then a partition and a
+                   // merge kernel per pass (as in the launch lists: 5 at 8,192 rows, 11 at 65,536)
+    int passes = 0;
+    for (uint64_t tiles = (rows + 2047) / 2048; tiles > 1; tiles = (tiles + 1) / 2) ++passes;
+    *launches += 1 + 2 * passes;
+  }
   if (ev && ev->sort1) EDX_CUDA(cudaEventRecord(ev->sort1, s));
   const bool greedy = k < rows;
   if (greedy) {
