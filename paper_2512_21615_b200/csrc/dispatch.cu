@@ -461,10 +461,6 @@ void launch_greedy(const double* matrix, uint64_t rows, int n, const uint32_t* o
   }
   k_greedy_prefs<<<static_cast<unsigned>((n_order * 32 + 255) / 256), 256, 0, s>>>(
       matrix, n, order, n_order, capacity_dev, cap_uniform, row_ids, g.prefs.p, g.dest.p);
-  if (g.prefs_done) {  // the engine may hang independent work on it (the step head)
-    EDX_CUDA(cudaEventRecord(g.prefs_done, s));
-    g.prefs_recorded = true;
-  }
   g_kernel_name[kKGreedy] = "k_greedy";
   static bool attr = [] {
     EDX_CUDA(cudaFuncSetAttribute(k_greedy, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -527,7 +523,6 @@ int exact_multiplicity(int m, double alpha) {
 }
 
 DispatchScratch::~DispatchScratch() {
-  if (greedy.prefs_done) cudaEventDestroy(greedy.prefs_done);
   if (fork) cudaEventDestroy(fork);
   if (join) cudaEventDestroy(join);
   if (side) cudaStreamDestroy(side);
@@ -539,7 +534,6 @@ void DispatchScratch::init(int device) {
   EDX_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
   EDX_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
   EDX_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
-  EDX_CUDA(cudaEventCreateWithFlags(&greedy.prefs_done, cudaEventDisableTiming));
 }
 
 // ecomix (assign.hpp:247-285): rows ordered by gap; the top n*mult rows go to
@@ -551,7 +545,6 @@ void run_ecomix(DispatchScratch& sc, const double* matrix, uint64_t rows, int n,
                 double alpha, bool gap_ready, int32_t* decision, int* flags, cudaStream_t s,
                 int device, const PhaseEvents* ev, int* launches) {
   sc.init(device);
-  sc.greedy.prefs_recorded = false;
   const int mult = exact_multiplicity(m, alpha);
   const uint64_t k = static_cast<uint64_t>(n) * static_cast<uint64_t>(mult);
   sc.gap_keys.ensure(rows);

@@ -221,8 +221,6 @@ struct GreedyScratch {
   DevBuf<uint32_t> dest;  // per position: its decision index (row_ids[order[t]])
   DevBuf<int32_t> pw;     // per position: its worker (when the caller wants rows only)
   DevBuf<unsigned long long> stats;  // EDX_GREEDY_STATS=1 only
-  cudaEvent_t prefs_done = nullptr;  // recorded after the preference lists (owner: DispatchScratch)
-  bool prefs_recorded = false;       // ... in the current dispatch
 };
 void launch_greedy(const double* matrix, uint64_t rows, int n, const uint32_t* order,
                    uint64_t n_order, const int32_t* capacity_dev, int cap_uniform,

@@ -691,18 +691,13 @@ void iterate_enqueue(edx_engine* e, double alpha) {
     const char* v = std::getenv("EDX_HEAD_OVERLAP");
     return !(v && std::strcmp(v, "0") == 0);
   }();
-  const bool small = e->total_ids <= (1ULL << 20);
   try {
     engine_build(e);
-    // Up to 2^20 ids the head is forked after the build and overlaps the
-    // whole dispatch (C1 0.271 -> 0.265 ms per iteration).  On larger batches
-    // it competes with the dispatch's grids (C5: 1.148 ms overlapped that way
-    // against 1.109 inside the step), so it is forked only after the greedy's
-    // preference lists, beside the one-CTA greedy sweep.
-    if (!e->profiling && overlap && small) edx::step_head(e);
+    // forked after the build, so it overlaps the dispatch, for batches up to
+    // 2^20 ids (C1 0.271 -> 0.265 ms per iteration); on larger batches it
+    // runs inside the step (C5: 1.148 ms overlapped against 1.109 inside)
+    if (!e->profiling && overlap && e->total_ids <= (1ULL << 20)) edx::step_head(e);
     engine_dispatch(e, alpha);
-    if (!e->profiling && overlap && !small && e->disp.greedy.prefs_recorded)
-      edx::step_head(e, e->disp.greedy.prefs_done);
     step_enqueue(e, nullptr);
   } catch (...) {
     edx::step_head_abandon(e);

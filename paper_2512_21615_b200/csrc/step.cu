@@ -1312,13 +1312,10 @@ int launch_step_head(edx_engine* e, cudaStream_t st) {
 
 }  // namespace
 
-void step_head(edx_engine* e, cudaEvent_t after) {
+void step_head(edx_engine* e) {
   if (e->head_pending) return;
-  if (!after) {
-    EDX_CUDA(cudaEventRecord(e->head_fork, e->stream));
-    after = e->head_fork;
-  }
-  EDX_CUDA(cudaStreamWaitEvent(e->step_side, after, 0));
+  EDX_CUDA(cudaEventRecord(e->head_fork, e->stream));
+  EDX_CUDA(cudaStreamWaitEvent(e->step_side, e->head_fork, 0));
   e->launches += launch_step_head(e, e->step_side);
   EDX_CUDA(cudaEventRecord(e->head_done, e->step_side));
   e->head_pending = true;

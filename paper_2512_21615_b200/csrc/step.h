@@ -17,10 +17,10 @@ void step_init_state(edx_engine* e);
 // caller synchronises the stream).
 void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out);
 // Enqueues the decision-independent head of the step (clock, counters, the
-// batch's unique ids) on e->step_side, forked from e->stream (or after the
-// event `after`) and later joined into e->stream by step_run.  Used by the
-// fused iteration so the head overlaps the dispatch.
-void step_head(edx_engine* e, cudaEvent_t after = nullptr);
+// batch's unique ids) on e->step_side, forked from and later joined into
+// e->stream by step_run.  Used by the fused iteration so the head overlaps
+// the cost build and the dispatch.
+void step_head(edx_engine* e);
 // Undoes a launched head whose step will not run (the iteration failed).
 void step_head_abandon(edx_engine* e);
 // True when step_run decides every victim on the device (no host round trip),
