@@ -695,7 +695,9 @@ void iterate_enqueue(edx_engine* e, double alpha) {
     engine_build(e);
     // forked after the build, so it overlaps the dispatch, for batches up to
     // 2^20 ids (C1 0.271 -> 0.265 ms per iteration); on larger batches it
-    // runs inside the step (C5: 1.148 ms overlapped against 1.109 inside)
+    // runs inside the step (C5: 1.148 ms overlapped against 1.109 inside;
+    // 1.128 against 1.096 even when forked only after the greedy's
+    // preference lists, beside the one-CTA sweep)
     if (!e->profiling && overlap && e->total_ids <= (1ULL << 20)) edx::step_head(e);
     engine_dispatch(e, alpha);
     step_enqueue(e, nullptr);
