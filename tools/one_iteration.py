@@ -18,14 +18,15 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C3")
     ap.add_argument("--prefill", type=int, default=None)
+    ap.add_argument("--batch", type=int, default=None, help="C5 sweep point (bench.py --batch)")
+    ap.add_argument("--workers", type=int, default=None, help="C5 sweep point (bench.py --workers)")
     args = ap.parse_args()
     import torch
     import paper_2512_21615_b200 as edx
-    w = dict(bench.WORKLOADS[args.config])
-    if args.prefill is not None:
-        w["prefill"] = args.prefill
+    args.alpha, args.spread_ids = None, False
+    w = bench.workload(args)  # the bench's own workload (C5 sweep overrides included)
     n, m, L = w["n"], w["m"], w["L"]
-    w["R"] = R = n * m
+    R = w["R"]
     host = bench.batches(w, w["prefill"] + 2)
     offs = np.arange(R + 1, dtype=np.uint64) * np.uint64(L)
     cfg = edx.ClusterConfig(n=n, m=m, bandwidths_bps=w["bw"], cache_capacity=w["cap"],
