@@ -440,6 +440,16 @@ __device__ __forceinline__ BigEntry big_entry(const BigArgs& a, int j, uint32_t 
   return e;
 }
 
+// One histogram increment per warp and digit: the lanes holding the same
+// digit are grouped (a concentrated key distribution would otherwise
+// serialise whole warps on one shared-memory word).  kNoBin: no increment.
+constexpr uint32_t kNoBin = 0xFFFFFFFFu;
+__device__ __forceinline__ void hist_add(uint32_t* hsh, uint32_t d) {
+  const unsigned act = __activemask();
+  const unsigned peers = __match_any_sync(act, d);
+  if (d != kNoBin && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hsh[d], __popc(peers));
+}
+
 // block-wide sum of two counters into shared memory
 __device__ void big_block_hist_flush(uint32_t* sh, uint32_t* gh) {
   for (int b = threadIdx.x; b < big::kBins; b += blockDim.x) {
@@ -498,7 +508,7 @@ __device__ void big_select(const BigArgs& a, int j, uint32_t* scan_sh) {
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(big::kThreads)
+__global__ void __launch_bounds__(big::kThreads, 1)
     k_big_select(BigArgs a) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
@@ -634,8 +644,8 @@ __global__ void __launch_bounds__(big::kThreads)
         if (base >= size0) continue;
         for (uint32_t s = base + threadIdx.x; s < base + big::kChunk && s < size0; s += blockDim.x) {
           const BigEntry e = big_entry(a, j, s, size0, stamp);
-          if (e.cand)
-            atomicAdd(&hsh[key_digit(victim_key(st, e.ver, e.mark, e.freq, e.last, e.rid), 0)], 1u);
+          hist_add(hsh, e.cand ? key_digit(victim_key(st, e.ver, e.mark, e.freq, e.last, e.rid), 0)
+                               : kNoBin);
         }
         __syncthreads();
         big_block_hist_flush(hsh, a.hist + static_cast<uint64_t>(j) * big::kBins);
@@ -651,7 +661,7 @@ __global__ void __launch_bounds__(big::kThreads)
         for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
           const uint32_t base = u * big::kChunk;
           for (uint32_t t = base + threadIdx.x; t < base + big::kChunk && t < cnt; t += blockDim.x)
-            atomicAdd(&hsh[key_digit(K[t], level)], 1u);
+            hist_add(hsh, key_digit(K[t], level));
           __syncthreads();
           big_block_hist_flush(hsh, a.hist + static_cast<uint64_t>(j) * big::kBins);
           __syncthreads();
@@ -682,9 +692,14 @@ __global__ void __launch_bounds__(big::kThreads)
       const bool victim = live && (d < stc.bin || (d == stc.bin && stc.take_all));
       const bool undecided = live && d == stc.bin && !stc.take_all;
       const uint32_t vi = warp_append(&st.nv, victim, mask);
-      if (victim) {
-        a.victims[static_cast<uint64_t>(j) * a.capacity + vi] = slot;
-        if (!(ver == 1 && cur)) atomicAdd(&st.vc[ver ? 2 : (cur ? 1 : 0)], 1u);
+      if (victim) a.victims[static_cast<uint64_t>(j) * a.capacity + vi] = slot;
+      // class counts, one atomic per warp and class (a mass eviction puts
+      // ~10^5 victims per worker on these three words)
+      const int cls = victim ? (ver ? (cur ? 3 : 2) : (cur ? 1 : 0)) : 3;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const unsigned b = __ballot_sync(mask, cls == c);
+        if (b && lane == __ffs(mask) - 1) atomicAdd(&st.vc[c], static_cast<uint32_t>(__popc(b)));
       }
       const uint32_t ui = warp_append(&st.nu[out], undecided, mask);
       if (undecided) {
