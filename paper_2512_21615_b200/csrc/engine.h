@@ -57,6 +57,7 @@ struct StepScratch {
   DevBuf<uint32_t> big_hist;     // n * 4096
   DevBuf<uint8_t> big_key[2];    // n * capacity 128-bit keys (undecided, ping-pong)
   DevBuf<uint32_t> big_slot[2];  // n * capacity
+  DevBuf<uint8_t> big_eflag;     // n * capacity: candidate / version bits of each entry
   uint64_t big_grid = 0;
   DevBuf<uint8_t> temp;          // CUB temp storage
   DevBuf<uint32_t> ucount;       // number of unique ids

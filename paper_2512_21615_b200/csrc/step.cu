@@ -414,6 +414,8 @@ struct BigArgs {
   u128* ukey[2];           // n * capacity each
   uint32_t* uslot[2];
   uint32_t* victims;       // n * capacity: worker j's victims from j * capacity
+  uint8_t* eflag;          // n * capacity: candidate (bit 0) and version (bit 1) per entry,
+                           // written by the ranges pass, read by the later passes
   int* flags;
 };
 
@@ -424,14 +426,28 @@ struct BigEntry {
   uint32_t ver, mark, freq, last, rid;
 };
 
+// The first pass (`first`) derives candidacy and version from the pin stamp
+// and the global masks (a random 16-byte gather per entry) and records them
+// in one byte per entry; the later passes read that byte instead.
 __device__ __forceinline__ BigEntry big_entry(const BigArgs& a, int j, uint32_t s, uint32_t size0,
-                                              uint32_t stamp) {
+                                              uint32_t stamp, bool first = false) {
   BigEntry e{};
   const uint64_t g = static_cast<uint64_t>(j) * a.capacity + s;
-  e.cand = s < size0 && a.pin[g] != stamp;
+  uint32_t slot = 0;
+  if (first) {
+    e.cand = s < size0 && a.pin[g] != stamp;
+    if (e.cand) {
+      slot = a.sid[g];
+      e.ver = static_cast<uint32_t>((a.ol[slot].y >> j) & 1ULL);
+    }
+    if (s < size0) a.eflag[g] = static_cast<uint8_t>((e.cand ? 1u : 0u) | (e.ver << 1));
+  } else {
+    const uint32_t f = s < size0 ? a.eflag[g] : 0u;
+    e.cand = f & 1u;
+    e.ver = (f >> 1) & 1u;
+    if (e.cand) slot = a.sid[g];
+  }
   if (e.cand) {
-    const uint32_t slot = a.sid[g];
-    e.ver = static_cast<uint32_t>((a.ol[slot].y >> j) & 1ULL);
     e.mark = a.smark[g];
     e.freq = a.sfreq[g];
     e.last = a.slast[g];
@@ -565,7 +581,7 @@ __global__ void __launch_bounds__(big::kThreads, 1)
     if (base >= size0) continue;
     uint32_t v[9] = {UINT_MAX, UINT_MAX, UINT_MAX, UINT_MAX, 0, 0, 0, 0, 0};
     for (uint32_t s = base + threadIdx.x; s < base + big::kChunk && s < size0; s += blockDim.x) {
-      const BigEntry e = big_entry(a, j, s, size0, stamp);
+      const BigEntry e = big_entry(a, j, s, size0, stamp, true);
       if (!e.cand) continue;
       const uint32_t f[4] = {e.mark, e.freq, e.last, e.rid};
 #pragma unroll
@@ -1260,6 +1276,7 @@ void step_init_state(edx_engine* e) {
       s.big_key[b].ensure(cand * sizeof(u128));
       s.big_slot[b].ensure(cand);
     }
+    s.big_eflag.ensure(cand);
     int per_sm = 0, sms = 0;
     EDX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_big_select, big::kThreads, 0));
     EDX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, e->device));
@@ -1430,6 +1447,7 @@ void step_run(edx_engine* e, const int32_t* d_decision, StepResult* out) {
     ba.uslot[0] = s.big_slot[0].p;
     ba.uslot[1] = s.big_slot[1].p;
     ba.victims = s.cand_slot_sorted.p;
+    ba.eflag = s.big_eflag.p;
     ba.flags = e->flags.p;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(s.big_grid));
