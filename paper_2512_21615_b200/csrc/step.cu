@@ -365,11 +365,6 @@ struct BigState {
   uint32_t cand, need, bin, take_all, active, level, nv, pinned_err;
   uint32_t vc[3];  // victims: version 0 non-current, version 0 current, version 1 non-current
   uint32_t nu[2];  // undecided keys per ping-pong buffer
-  // where level L reads its undecided keys: srcv[L & 1] = 0 (the cache
-  // entries themselves, no key materialised yet) or 1 + buffer; a level whose
-  // bin holds every undecided key (`skip`) compacts nothing and passes its
-  // source on; dst = the buffer a compacting level writes
-  uint32_t srcv[2], dst, skip;
   int w[5];        // field widths: version, mark, freq, last, id
   int W;
   uint32_t pad[2];
@@ -521,9 +516,6 @@ __device__ void big_select(const BigArgs& a, int j, uint32_t* scan_sh) {
         st.bin = threadIdx.x * per + q;
         st.need = need - run;
         st.take_all = (need - run == v[q]) ? 1u : 0u;
-        // every undecided key in this bin: nothing to compact at this level
-        const uint32_t total = scan_sh[32 + big::kThreads / 32 - 1] + scan_sh[big::kThreads / 32 - 1];
-        st.skip = (!st.take_all && v[q] == total) ? 1u : 0u;
         break;
       }
       run += v[q];
@@ -573,8 +565,6 @@ __global__ void __launch_bounds__(big::kThreads, 1)
     st.pad[0] = UINT_MAX;  // level at which the worker's selection finished
     st.vc[0] = st.vc[1] = st.vc[2] = 0;
     st.nu[0] = st.nu[1] = 0;
-    st.srcv[0] = st.srcv[1] = 0;
-    st.dst = st.skip = 0;
     st.need = w[kWsEvict];
     st.active = w[kWsEvict] > 0 ? 1u : 0u;
   }
@@ -659,37 +649,39 @@ __global__ void __launch_bounds__(big::kThreads, 1)
     bool any = false;
     for (int j = 0; j < n; ++j) any |= a.st[j].active != 0 && a.st[j].pad[0] == UINT_MAX;
     if (!any) break;
-    const int lp = level & 1;  // this level's source slot (BigState::srcv)
-    // histogram of this level's digit: workers still reading their entries
-    for (uint32_t u = blockIdx.x; u < static_cast<uint32_t>(n) * chunks; u += gridDim.x) {
-      const int j = static_cast<int>(u / chunks);
-      const BigState& st = a.st[j];
-      if (!st.active || st.pad[0] != UINT_MAX || st.srcv[lp] != 0) continue;
-      const uint32_t size0 = a.ws[j * kWS + kWsSize0], base = (u % chunks) * big::kChunk;
-      if (base >= size0) continue;
-      for (uint32_t s = base + threadIdx.x; s < base + big::kChunk && s < size0; s += blockDim.x) {
-        const BigEntry e = big_entry(a, j, s, size0, stamp);
-        hist_add(hsh, e.cand ? key_digit(victim_key(st, e.ver, e.mark, e.freq, e.last, e.rid), level)
-                             : kNoBin);
-      }
-      __syncthreads();
-      big_block_hist_flush(hsh, a.hist + static_cast<uint64_t>(j) * big::kBins);
-      __syncthreads();
-    }
-    // ... and workers reading compacted keys
-    for (int j = 0; j < n; ++j) {
-      const BigState& st = a.st[j];
-      if (!st.active || st.pad[0] != UINT_MAX || st.srcv[lp] == 0) continue;
-      const uint32_t b = st.srcv[lp] - 1, cnt = st.nu[b];
-      const uint32_t units = (cnt + big::kChunk - 1) / big::kChunk;
-      const u128* K = a.ukey[b] + static_cast<uint64_t>(j) * a.capacity;
-      for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
-        const uint32_t base = u * big::kChunk;
-        for (uint32_t t = base + threadIdx.x; t < base + big::kChunk && t < cnt; t += blockDim.x)
-          hist_add(hsh, key_digit(K[t], level));
+    const int in = (level + 1) & 1, out = level & 1;  // U buffers: level L reads in, writes out
+    // histogram of this level's digit
+    if (level == 0) {
+      for (uint32_t u = blockIdx.x; u < static_cast<uint32_t>(n) * chunks; u += gridDim.x) {
+        const int j = static_cast<int>(u / chunks);
+        const BigState& st = a.st[j];
+        if (!st.active || st.pad[0] != UINT_MAX) continue;
+        const uint32_t size0 = a.ws[j * kWS + kWsSize0], base = (u % chunks) * big::kChunk;
+        if (base >= size0) continue;
+        for (uint32_t s = base + threadIdx.x; s < base + big::kChunk && s < size0; s += blockDim.x) {
+          const BigEntry e = big_entry(a, j, s, size0, stamp);
+          hist_add(hsh, e.cand ? key_digit(victim_key(st, e.ver, e.mark, e.freq, e.last, e.rid), 0)
+                               : kNoBin);
+        }
         __syncthreads();
         big_block_hist_flush(hsh, a.hist + static_cast<uint64_t>(j) * big::kBins);
         __syncthreads();
+      }
+    } else {
+      for (int j = 0; j < n; ++j) {
+        const BigState& st = a.st[j];
+        if (!st.active || st.pad[0] != UINT_MAX) continue;
+        const uint32_t cnt = st.nu[in];
+        const uint32_t units = (cnt + big::kChunk - 1) / big::kChunk;
+        const u128* K = a.ukey[in] + static_cast<uint64_t>(j) * a.capacity;
+        for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
+          const uint32_t base = u * big::kChunk;
+          for (uint32_t t = base + threadIdx.x; t < base + big::kChunk && t < cnt; t += blockDim.x)
+            hist_add(hsh, key_digit(K[t], level));
+          __syncthreads();
+          big_block_hist_flush(hsh, a.hist + static_cast<uint64_t>(j) * big::kBins);
+          __syncthreads();
+        }
       }
     }
     grid.sync();
@@ -699,10 +691,7 @@ __global__ void __launch_bounds__(big::kThreads, 1)
       big_select(a, j, scan_sh);
       if (threadIdx.x == 0) {
         BigState& st = a.st[j];
-        const uint32_t src = st.srcv[lp];
-        st.dst = src == 1 ? 1u : 0u;  // the buffer that is not the source
-        if (!st.skip) st.nu[st.dst] = 0;
-        st.srcv[lp ^ 1] = st.skip ? src : 1 + st.dst;
+        st.nu[out] = 0;
         if (!st.take_all && level >= (128 + big::kDigit - 1) / big::kDigit - 1) {
           atomicOr(a.flags + kFlagInternal, 1);  // unique keys: unreachable
           st.take_all = 1;
@@ -728,54 +717,53 @@ __global__ void __launch_bounds__(big::kThreads, 1)
         const unsigned b = __ballot_sync(mask, cls == c);
         if (b && lane == __ffs(mask) - 1) atomicAdd(&st.vc[c], static_cast<uint32_t>(__popc(b)));
       }
-      const uint32_t ui = warp_append(&st.nu[stc.dst], undecided, mask);
+      const uint32_t ui = warp_append(&st.nu[out], undecided, mask);
       if (undecided) {
-        a.ukey[stc.dst][static_cast<uint64_t>(j) * a.capacity + ui] = key;
-        a.uslot[stc.dst][static_cast<uint64_t>(j) * a.capacity + ui] = slot;
+        a.ukey[out][static_cast<uint64_t>(j) * a.capacity + ui] = key;
+        a.uslot[out][static_cast<uint64_t>(j) * a.capacity + ui] = slot;
       }
     };
-    // (a worker compacts when it is still selecting or finished at this level,
-    // and its bin did not hold every undecided key)
-    for (uint32_t u = blockIdx.x; u < static_cast<uint32_t>(n) * chunks; u += gridDim.x) {
-      const int j = static_cast<int>(u / chunks);
-      BigState& st = a.st[j];
-      if (!st.active || (st.pad[0] != UINT_MAX && st.pad[0] != level)) continue;
-      const BigState stc = st;
-      if (stc.skip || stc.srcv[lp] != 0) continue;
-      const uint32_t size0 = a.ws[j * kWS + kWsSize0], base = (u % chunks) * big::kChunk;
-      if (base >= size0) continue;
-      const uint32_t cm = a.cur_mark[j];
-      for (uint32_t s0 = base; s0 < base + big::kChunk && s0 < size0; s0 += blockDim.x) {
-        const uint32_t s = s0 + threadIdx.x;
-        const bool in_range = s < base + big::kChunk && s < size0;
-        const unsigned mask = __ballot_sync(0xffffffffu, in_range);
-        if (!in_range) continue;
-        const BigEntry e = big_entry(a, j, s, size0, stamp);
-        const u128 key = e.cand ? victim_key(stc, e.ver, e.mark, e.freq, e.last, e.rid) : u128(0);
-        place(stc, st, j, e.cand, key, s, e.ver, e.mark == cm, mask);
+    if (level == 0) {
+      for (uint32_t u = blockIdx.x; u < static_cast<uint32_t>(n) * chunks; u += gridDim.x) {
+        const int j = static_cast<int>(u / chunks);
+        BigState& st = a.st[j];
+        if (!st.active || (st.pad[0] != UINT_MAX && st.pad[0] != level)) continue;
+        const BigState stc = st;
+        const uint32_t size0 = a.ws[j * kWS + kWsSize0], base = (u % chunks) * big::kChunk;
+        if (base >= size0) continue;
+        const uint32_t cm = a.cur_mark[j];
+        for (uint32_t s0 = base; s0 < base + big::kChunk && s0 < size0; s0 += blockDim.x) {
+          const uint32_t s = s0 + threadIdx.x;
+          const bool in_range = s < base + big::kChunk && s < size0;
+          const unsigned mask = __ballot_sync(0xffffffffu, in_range);
+          if (!in_range) continue;
+          const BigEntry e = big_entry(a, j, s, size0, stamp);
+          const u128 key = e.cand ? victim_key(stc, e.ver, e.mark, e.freq, e.last, e.rid) : u128(0);
+          place(stc, st, j, e.cand, key, s, e.ver, e.mark == cm, mask);
+        }
       }
-    }
-    for (int j = 0; j < n; ++j) {
-      BigState& st = a.st[j];
-      if (!st.active || (st.pad[0] != UINT_MAX && st.pad[0] != level)) continue;
-      const BigState stc = st;
-      if (stc.skip || stc.srcv[lp] == 0) continue;
-      const uint32_t b = stc.srcv[lp] - 1, cnt = stc.nu[b];
-      const uint32_t units = (cnt + big::kChunk - 1) / big::kChunk;
-      const uint64_t gb = static_cast<uint64_t>(j) * a.capacity;
-      const uint32_t cm = a.cur_mark[j];
-      for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
-        const uint32_t base = u * big::kChunk;
-        for (uint32_t t0 = base; t0 < base + big::kChunk && t0 < cnt; t0 += blockDim.x) {
-          const uint32_t t = t0 + threadIdx.x;
-          const bool live = t < base + big::kChunk && t < cnt;
-          const unsigned mask = __ballot_sync(0xffffffffu, live);
-          if (!live) continue;
-          const u128 key = a.ukey[b][gb + t];
-          const uint32_t slot = a.uslot[b][gb + t];
-          const uint32_t ver = static_cast<uint32_t>(key >> 127);
-          const bool cur = a.smark[gb + slot] == cm;
-          place(stc, st, j, true, key, slot, ver, cur, mask);
+    } else {
+      for (int j = 0; j < n; ++j) {
+        BigState& st = a.st[j];
+        if (!st.active || (st.pad[0] != UINT_MAX && st.pad[0] != level)) continue;
+        const BigState stc = st;
+        const uint32_t cnt = stc.nu[in];
+        const uint32_t units = (cnt + big::kChunk - 1) / big::kChunk;
+        const uint64_t gb = static_cast<uint64_t>(j) * a.capacity;
+        const uint32_t cm = a.cur_mark[j];
+        for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
+          const uint32_t base = u * big::kChunk;
+          for (uint32_t t0 = base; t0 < base + big::kChunk && t0 < cnt; t0 += blockDim.x) {
+            const uint32_t t = t0 + threadIdx.x;
+            const bool live = t < base + big::kChunk && t < cnt;
+            const unsigned mask = __ballot_sync(0xffffffffu, live);
+            if (!live) continue;
+            const u128 key = a.ukey[in][gb + t];
+            const uint32_t slot = a.uslot[in][gb + t];
+            const uint32_t ver = static_cast<uint32_t>(key >> 127);
+            const bool cur = a.smark[gb + slot] == cm;
+            place(stc, st, j, true, key, slot, ver, cur, mask);
+          }
         }
       }
     }
